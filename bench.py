@@ -1,0 +1,394 @@
+"""Offloaded DSA decode step benchmark (BASELINE.json metric: decode tokens/s/GPU with
+the latent cache offloaded, plus H2D gather GB/s).
+
+    python bench.py [--gpus N --steps K --warmup W] [--config c2|c4] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU, weak scaling)
+
+One step = one DSA layer decode for every request on the GPU: K1 lightning indexer
+-> K2 top-2048 -> K3 LRU cache manager -> K4 zero-copy miss gather -> K5 sparse MLA,
+then each request appends its generated token (grow, admit, D2H write-back).
+Synthetic inputs of DeepSeek-V3.2-Exp shapes, random weights; every per-step input
+is generated before the timed region.  The working set (indexer keys + slot pool,
+>600 MB/GPU at C2) is larger than the 126 MB L2, so no flush is needed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[1]: one V3.2-Exp DSA layer, batch 64, ctx 32K, 25% slot pool
+    "c2": dict(batch=64, context_len=32768, sparse_ratio=0.25,
+               workload="C2: one DSA layer decode, batch 64/GPU, ctx 32K, 25% GPU slot pool"),
+    # configs[3]: ctx 128K, batch 64/GPU, 10% slot pool
+    "c4": dict(batch=64, context_len=131072, sparse_ratio=0.10,
+               workload="C4: one DSA layer decode, batch 64/GPU, ctx 128K, 10% GPU slot pool"),
+}
+TOPK = 2048
+METRIC = "decode tokens/s/GPU at 32K/128K ctx, latent cache offloaded; H2D gather GB/s"
+LAUNCHES_PER_STEP = 8  # indexer, topk, access, gather, sparse_mla, grow, append, write_generated
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+# -------------------------------------------------------------------------------------
+# CPU leg: the oracle port on host cores (cpu_baseline and --impl reference)
+# -------------------------------------------------------------------------------------
+def cpu_reference_rate(cfg, budget_s: float = 12.0, seed: int = 0):
+    """Time the CPU oracle for one decode step of a sample of requests at the config's
+    shapes: numpy indexer + top-k + C LRU step + numpy sparse MLA.  Returns
+    (tokens/s, sample description, threads)."""
+    import numpy as np
+
+    from oracle import dsa
+    from oracle import lru as olru
+
+    rng = np.random.default_rng(seed)
+    L, K, rho = cfg["context_len"], TOPK, cfg["sparse_ratio"]
+    e4 = lambda a: np.clip(np.round(a), -6, 6).astype(np.int8).view(np.uint8)  # noqa: E731
+    n_req, t_total = 0, 0.0
+    while n_req < 1 or (t_total < budget_s and n_req < cfg["batch"]):
+        k = e4(rng.standard_normal((L, 128)) * 2)
+        q = e4(rng.standard_normal((64, 128)) * 2)
+        w = rng.standard_normal(64).astype(np.float32) / 8
+        ks = (rng.random(L).astype(np.float32) + 0.5)
+        rows = rng.integers(0, 120, size=(L, 656), dtype=np.uint8)
+        rows[:, 512:528] = np.full((L, 4), 0.03, np.float32).view(np.uint8)
+        rows[:, 528:] = 0
+        qa = rng.standard_normal((128, 576)).astype(np.float32)
+        pool = olru.OraclePool(olru.pool_capacity(rho, L))
+        pool.warmup([rng.choice(L, size=K, replace=False)])
+        t0 = time.perf_counter()
+        logits = dsa.indexer_logits(q, w, k, ks, L)
+        idx = dsa.topk_indices(logits, L, K)
+        pool.access_step(idx.tolist())
+        dsa.sparse_mla(qa, rows[idx], 1.0 / 192 ** 0.5)
+        t_total += time.perf_counter() - t0
+        n_req += 1
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    sample = (f"{n_req} request(s) x 1 step of the {cfg['workload']} workload: numpy indexer "
+              f"(fp64 BLAS) + top-k + C LRU step + fp64 sparse MLA, {t_total:.2f}s")
+    return n_req / t_total, sample, threads
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    vals = []
+    for _ in range(args.warmup):
+        cpu_reference_rate(cfg, budget_s=2.0)
+    t0 = time.perf_counter()
+    sample = threads = None
+    for _ in range(args.steps):
+        v, sample, threads = cpu_reference_rate(cfg, budget_s=5.0)
+        vals.append(v)
+    el = time.perf_counter() - t0
+    value = statistics.mean(vals)
+    line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": cfg["workload"], "layers": 1, "batch_per_gpu": cfg["batch"],
+                       "context_len": cfg["context_len"], "sparse_ratio": cfg["sparse_ratio"],
+                       "topk": TOPK},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------------------------------
+# GPU leg
+# -------------------------------------------------------------------------------------
+def host_link_peak_gbs(device, nbytes=1 << 28):
+    """Bulk pinned H2D cudaMemcpy bandwidth (the K4 roofline denominator)."""
+    import torch
+    src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    for _ in range(2):
+        dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 0.0
+    for _ in range(5):
+        e0.record()
+        dst.copy_(src, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+    return best
+
+
+def time_steps(layer, inputs, new_rows, steps, timers=None):
+    """Run `steps` decode steps; per-kernel CUDA events when `timers` is given."""
+    import torch
+    from paper_2512_10576_b200.attention import sparse_mla
+    from paper_2512_10576_b200.indexer import indexer_logits, topk
+    from paper_2512_10576_b200.transfer import gather
+    for t in range(steps):
+        q_idx, q = inputs[t]
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if timers is not None else None
+        if ev: ev[0].record()
+        indexer_logits(q_idx, layer.w, layer.k_cache, layer.k_scale, layer.lens, out=layer.logits)
+        if ev: ev[1].record()
+        topk(layer.logits, layer.lens, layer.K, out=layer.idx, count=layer.cnt)
+        if ev: ev[2].record()
+        layer.acc = layer.pool.access(layer.idx, layer.cnt, out=layer.acc)
+        if ev: ev[3].record()
+        gather(layer.pool, layer.store, layer.acc, max_ctas=layer.gather_ctas)
+        if ev: ev[4].record()
+        sparse_mla(layer.pool, q, layer.acc.sel_row, layer.cnt, layer.sm_scale, out=layer.out, lse=layer.lse)
+        if ev: ev[5].record()
+        layer.append_token(new_rows=new_rows[t])
+        if timers is not None:
+            timers.append((ev, layer.acc.counts.clone()))
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+    from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows
+
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peaks, peak_kind = measured_peaks()
+    B, L, rho = cfg["batch"], cfg["context_len"], cfg["sparse_ratio"]
+    total = args.warmup + args.steps
+    layer = DSADecodeLayer(B, L, rho, TOPK, max_new_tokens=args.warmup + 2 * args.steps + 8, device=dev,
+                           seed=1234 + rank, drift=args.drift)
+    layer.gather_ctas = args.gather_ctas
+    layer.prefill_warmup(windows=32)
+    inputs = [layer.next_queries() for _ in range(total)]
+    new_rows = [random_latent_rows(B, dev, layer.gen).view(B, 1, 656) for _ in range(total)]
+    torch.cuda.synchronize()
+
+    # warm-up steps (untimed)
+    time_steps(layer, inputs[:args.warmup], new_rows[:args.warmup], args.warmup)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    # timed region: K steps, device clock (CUDA events), per-kernel events inside
+    timers = []
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        start.record()
+        time_steps(layer, inputs[args.warmup:], new_rows[args.warmup:], args.steps, timers)
+        end.record()
+        torch.cuda.synchronize()
+    step_ms = start.elapsed_time(end) / args.steps
+    layer.pool.check("bench")
+    from paper_2512_10576_b200.dp import aggregate
+    tokens_total, t_max = aggregate(B * args.steps, step_ms * args.steps / 1e3, device=dev)
+    value = tokens_total / t_max
+
+    # per-kernel breakdown + gather bytes
+    names = ["indexer", "topk", "cache", "gather", "sparse_mla"]
+    ktimes = {n: 0.0 for n in names}
+    misses = hits = 0
+    for ev, counts in timers:
+        for i, n in enumerate(names):
+            ktimes[n] += ev[i].elapsed_time(ev[i + 1])
+        c = counts.sum(0).tolist()
+        hits, misses = hits + c[0], misses + c[1]
+    ktimes = {n: v / args.steps for n, v in ktimes.items()}
+    lens_mean = L + args.warmup + (args.steps - 1) / 2
+    idx_bytes = B * lens_mean * (132 + 4) + B * (64 * 128 + 64 * 4)
+    achieved = idx_bytes / (ktimes["indexer"] * 1e-3) / 1e9
+    gather_bytes = misses * 656 / args.steps
+    link_peak = host_link_peak_gbs(dev) if rank == 0 else None
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tfile):
+        with open(tfile) as f:
+            traffic = json.load(f).get("indexer_dram_bytes_per_launch")
+
+    # e2e: through the public API with host buffers: H2D of the step's queries from pinned
+    # memory, the step, D2H of the attention output, every step
+    h_in = [(qi.cpu().pin_memory(), q.cpu().pin_memory()) for qi, q in inputs[args.warmup:]]
+    h_out = torch.empty(layer.out.shape, dtype=layer.out.dtype).pin_memory()
+    e2e_layer_inputs = []
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for t in range(args.steps):
+        qi = h_in[t][0].to(dev, non_blocking=True)
+        q = h_in[t][1].to(dev, non_blocking=True)
+        time_steps(layer, [(qi, q)], [new_rows[args.warmup + t]], 1)
+        h_out.copy_(layer.out, non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / args.steps
+    e2e_tok, e2e_t = aggregate(B * args.steps, e2e_ms * args.steps / 1e3, device=dev)
+    h2d = h_in[0][0].numel() + h_in[0][1].numel() * 2
+    d2h = h_out.numel() * 2
+    del e2e_layer_inputs
+
+    line = None
+    if rank == 0:
+        cpu_v, cpu_sample, cpu_threads = cpu_reference_rate(cfg, budget_s=12.0)
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "e4m3/f16/f32",
+            "data": "synthetic (random-weight DeepSeek-V3.2-Exp DSA shapes, drifting queries)",
+            "config": {"workload": cfg["workload"], "layers": 1, "batch_per_gpu": B,
+                       "context_len": L, "sparse_ratio": rho, "topk": TOPK, "query_drift": args.drift,
+                       "parallelism": f"dp{world} (requests sharded, no collective)",
+                       "l2": "inputs larger than L2 (indexer keys + slot pool > 600 MB/GPU)"},
+            "e2e": {"value": e2e_tok / e2e_t, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "roofline": {"bound": "hbm", "kernel": "indexer (K1)", "achieved": achieved,
+                         "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                         "traffic": traffic, "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": idx_bytes},
+            "cpu_baseline": {"value": cpu_v, "unit": "tokens/s", "cores": cpu_threads, "kind": "port",
+                             "sample": cpu_sample},
+            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "clocks": clocks.summary(),
+            "kernels_ms": ktimes,
+            "gather": {"bytes_per_step": gather_bytes,
+                       "gbs": gather_bytes / (ktimes["gather"] * 1e-3) / 1e9 if ktimes["gather"] else None,
+                       "host_link_peak_gbs": link_peak,
+                       "paper_flashtrans_gbs": 37.0},
+            "hit_rate": hits / max(1, hits + misses),
+            "misses_per_request_step": misses / (B * args.steps),
+        }
+    if args.ceiling and world == 1:
+        line["all_hbm_ceiling"] = run_ceiling(args, cfg, dev)
+        line["all_hbm_ceiling"]["frac_of_ceiling"] = value / line["all_hbm_ceiling"]["value"]
+    layer.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_ceiling(args, cfg, dev):
+    """Same kernels with the whole latent cache in HBM (rho = 1, full history preloaded):
+    every selection hits and the gather moves nothing (SURVEY §8d ceiling)."""
+    import torch
+    from paper_2512_10576_b200.cache import AccessBatch
+    from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows
+    from paper_2512_10576_b200.transfer import gather
+    B, L = cfg["batch"], cfg["context_len"]
+    total = args.warmup + args.steps
+    layer = DSADecodeLayer(B, L, 1.0, TOPK, max_new_tokens=total + 8, device=dev, seed=99,
+                           drift=args.drift)
+    layer.gather_ctas = args.gather_ctas
+    full = torch.arange(L, dtype=torch.int32, device=dev)
+    for c0 in range(0, L, 2048):
+        ids = full[c0:c0 + 2048].expand(B, -1).contiguous()
+        layer.pool.warmup(ids, torch.full((B,), ids.shape[1], dtype=torch.int32, device=dev))
+        slots = torch.stack([layer.pool.lookup(b, ids[b]) for b in range(B)])
+        cnt = torch.zeros((B, 4), dtype=torch.int32, device=dev)
+        cnt[:, 1] = ids.shape[1]
+        gather(layer.pool, layer.store, AccessBatch(cnt, None, ids, slots.contiguous()), max_ctas=148)
+    inputs = [layer.next_queries() for _ in range(total)]
+    new_rows = [random_latent_rows(B, dev, layer.gen).view(B, 1, 656) for _ in range(total)]
+    time_steps(layer, inputs[:args.warmup], new_rows[:args.warmup], args.warmup)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    time_steps(layer, inputs[args.warmup:], new_rows[args.warmup:], args.steps)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    hr = layer.acc.counts[:, 0].sum().item() / max(1, layer.cnt.sum().item())
+    layer.pool.check("ceiling")
+    layer.close()
+    return {"value": B / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms, "hit_rate": hr}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--drift", type=float, default=0.97)
+    ap.add_argument("--gather-ctas", type=int, default=32)
+    ap.add_argument("--no-ceiling", dest="ceiling", action="store_false")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

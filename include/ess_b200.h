@@ -1,0 +1,161 @@
+/*
+ * ess_b200.h — C ABI of the B200-native ESS decode hot path (libess_b200.so).
+ *
+ * Plain pointers and sizes only: every d_* argument is a device pointer (or a
+ * device-mapped pointer to cudaHostRegister'd memory), every call is
+ * asynchronous on the caller's cudaStream_t (passed as void*), nothing
+ * allocates on the hot path, and every function returns an ESS_* status.
+ * Errors that can only be detected on the device (the reference's ValueError
+ * classes) are latched in a per-pool status word read by ess_pool_status().
+ *
+ * The reference (offsim, /root/reference/pkg/src/offsim) is pure Python and
+ * has no FFI; each entry point below names the Python interface it replaces,
+ * i.e. what an `offsim` maintainer would bind with ctypes.
+ *
+ * Data layouts:
+ *   latent row   656 B = [0,512) e4m3 NoPE | [512,528) 4 x f32 group scales |
+ *                [528,656) 64 x bf16 RoPE          (scenario.py:25, costmodel.py:31)
+ *   indexer key  128 B e4m3 + f32 scale per token (separate arrays)
+ *                                                   (scenario.py:26, :30-33)
+ *   pools        P = layers x requests independent LRU pools, pool id = l*B + b
+ *                (one pool per (request, layer): SPEC.md:281, cache.py:176-177)
+ */
+#ifndef ESS_B200_H
+#define ESS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ESS_LATENT_ROW_BYTES 656
+#define ESS_NOPE_DIM 512
+#define ESS_ROPE_DIM 64
+#define ESS_INDEXER_HEADS 64
+#define ESS_INDEXER_DIM 128
+#define ESS_MLA_HEADS 128
+#define ESS_MLA_QK_DIM 576
+#define ESS_MLA_V_DIM 512
+#define ESS_MAX_REQUEST 2048 /* max ids per pool per access/warm-up call (top-k 2048, scenario.py:24) */
+
+/* status codes; the negative ones mirror the reference's ValueError classes */
+#define ESS_OK 0
+#define ESS_ERR_CAPACITY (-1)  /* capacity < 1 (cache.py:37-38) or > cap_max          */
+#define ESS_ERR_SHRINK (-2)    /* "capacity may only grow" (cache.py:60-61)            */
+#define ESS_ERR_DUPLICATE (-3) /* "duplicate generated entry id" (cache.py:127-128)    */
+#define ESS_ERR_NOMEM (-4)
+#define ESS_ERR_RATIO (-5)     /* sparse_ratio not in (0, 1] (cache.py:174-175)        */
+#define ESS_ERR_ARG (-6)       /* id out of [0, max_ids), request too long, bad sizes  */
+#define ESS_ERR_CUDA (-7)      /* CUDA runtime / driver failure                        */
+#define ESS_ERR_CLOCK (-8)     /* 32-bit recency clock exhausted (> 4e9 touches)       */
+
+#define ESS_CLOCK_BASE (1u << 24)   /* recency stamps start here; free slots key = slot index */
+
+#define ESS_ACCESS_SORT_EVICTED 1 /* emit evicted ids sorted ascending (cache.py:120) */
+
+typedef struct ess_pool ess_pool;
+
+/* ---- library ---------------------------------------------------------------- */
+const char *ess_version(void);
+const char *ess_status_string(int status);
+/* cudaHostRegister(mapped) + device alias: the host latent store (UVA gather source) */
+int ess_host_register(void *host_ptr, size_t bytes, void **d_alias);
+int ess_host_unregister(void *host_ptr);
+
+/* ---- K3 cache manager: replaces offsim.cache.SparsePool (cache.py:29-134) ------ */
+/* num_pools pools over ids [0, max_ids), each with up to cap_max slots.  When
+ * row_bytes > 0 the pool also owns its GPU slot store: per pool cap_max slot
+ * rows + staging_rows transient rows (oversize requests, cache.py:103-111). */
+int ess_pool_create(ess_pool **out, int32_t num_pools, int64_t max_ids, int32_t cap_max,
+                    int32_t row_bytes, int32_t staging_rows);
+int ess_pool_destroy(ess_pool *pool);
+/* empty pools [begin, begin+num) with capacity d_capacity[i]   (SparsePool(capacity)) */
+int ess_pool_reset(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_capacity,
+                   void *stream);
+/* capacity may only grow                                      (SparsePool.grow_capacity) */
+int ess_pool_grow(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_capacity,
+                  void *stream);
+/* one warm-up window per pool (<= ESS_MAX_REQUEST ids, duplicate-free); adds the
+ * number of newly inserted ids to d_inserted[i]                   (SparsePool.warmup) */
+int ess_pool_warmup(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_ids,
+                    const int32_t *d_n, int32_t stride, int64_t *d_inserted, void *stream);
+/* one selection set per pool (unique ids, any order, n <= ESS_MAX_REQUEST)
+ *                                                            (SparsePool.access_step)
+ * outputs, each [num][out_stride] (any may be NULL):
+ *   d_hit_ids, d_miss_ids   in requested order (cache.py:98-99)
+ *   d_evicted_ids           ascending if flags & ESS_ACCESS_SORT_EVICTED
+ *   d_sel_row               slot-store row of every requested id (attention input)
+ *   d_miss_row              destination row of every miss (gather input)
+ *   d_counts [num][4]       nhit, nmiss (= h2d_blocks), nevicted, ntransient      */
+int ess_pool_access(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_req,
+                    const int32_t *d_n, int32_t req_stride, int32_t *d_hit_ids,
+                    int32_t *d_miss_ids, int32_t *d_evicted_ids, int32_t *d_sel_row,
+                    int32_t *d_miss_row, int32_t *d_counts, int32_t out_stride, int32_t flags,
+                    void *stream);
+/* admit generated ids at top recency; d_slot_out [num][stride] gets each id's
+ * slot (may be NULL)                                     (SparsePool.append_generated) */
+int ess_pool_append(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_ids,
+                    const int32_t *d_m, int32_t stride, int32_t *d_slot_out, void *stream);
+/* least- to most-recent resident ids: d_out [num][cap_max], d_count [num]
+ *                                                 (SparsePool.lru_order, cache.py:55-57) */
+int ess_pool_lru_order(ess_pool *pool, int32_t begin, int32_t num, int32_t *d_out,
+                       int32_t *d_count, void *stream);
+/* d_out [num][8] int64: capacity, size, hits, misses, evictions, clock, watermark, 0 */
+int ess_pool_counters(ess_pool *pool, int32_t begin, int32_t num, int64_t *d_out, void *stream);
+/* slot of each id in pool `pool` (-1 = not resident)         (SparsePool.__contains__) */
+int ess_pool_lookup(ess_pool *pool, int32_t pool_index, const int32_t *d_ids, int32_t n,
+                    int32_t *d_slot_out, void *stream);
+/* copy pool state (and slot rows) into another pool set with >= max_ids / cap_max;
+ * used to grow a pool past its allocated cap_max            (SparsePool.grow_capacity) */
+int ess_pool_copy_state(ess_pool *dst, int32_t dst_begin, ess_pool *src, int32_t src_begin,
+                        int32_t num, void *stream);
+/* synchronous: read and clear the pool's device status word */
+int ess_pool_status(ess_pool *pool, int32_t *status_out);
+int ess_pool_info(ess_pool *pool, int32_t *num_pools, int64_t *max_ids, int32_t *cap_max,
+                  int32_t *row_bytes, int64_t *rows_per_pool, void **d_rows);
+
+/* ---- K4 FlashTrans-style zero-copy gather (replaces the
+ *      transfer_time(..., "h2d") cost term, costmodel.py:173-186) ------------------ */
+/* copies every miss row host_rows[pool][miss_id] -> slot store[pool][miss_row]
+ * with 16-B loads through the device alias of registered host memory.  Pool i
+ * of the range reads host rows at d_host_rows + i*host_pool_stride_rows*656. */
+int ess_gather(ess_pool *pool, int32_t begin, int32_t num, const void *d_host_rows,
+               int64_t host_pool_stride_rows, const int32_t *d_miss_ids,
+               const int32_t *d_miss_row, const int32_t *d_counts, int32_t stride,
+               int32_t max_ctas, void *stream);
+/* D2H write-back + slot fill of generated rows (cache.py:122-134):
+ * src rows [num][stride][656] -> host_rows[pool][id] and slot store[pool][slot] */
+int ess_write_generated(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_ids,
+                        const int32_t *d_m, const int32_t *d_slot, int32_t stride,
+                        const void *d_src_rows, void *d_host_rows,
+                        int64_t host_pool_stride_rows, void *stream);
+
+/* ---- K1 lightning indexer (op "indexer_logits", costmodel.py:18-27) ------------- */
+/* logits[b][s] = kscale[b][s] * sum_h w[b][h] * relu(q[b][h] . k[b][s]), s < len[b]
+ * q [B][64][128] e4m3, w [B][64] f32, k [B][k_ld][128] e4m3 (k_ld % 128 == 0),
+ * kscale [B][k_ld] f32, logits [B][k_ld] f32.  tcgen05 kind::f8f6f4 + TMA.       */
+int ess_indexer_logits(const void *d_q, const float *d_w, const void *d_k,
+                       const float *d_kscale, const int32_t *d_len, int32_t batch,
+                       int64_t k_ld, float *d_logits, void *stream);
+
+/* ---- K2 top-k (op "indexer_topk") ---------------------------------------------- */
+/* per row: the k largest logits[b][0:len[b]) by (score desc, index asc), written
+ * ascending to d_idx [B][idx_ld]; d_count[b] = min(k, len[b]) (scenario.py:110-112) */
+int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
+             int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count, void *stream);
+
+/* ---- K5 sparse MLA decode (op "sparse_mla") ------------------------------------ */
+/* out[b][h] = softmax_j(q[b][h] . K[j] * sm_scale) V[j] over the d_count[b] rows
+ * sel_row[b][0:count) of pool (pool_begin + b)'s slot store; K = dequant NoPE ++
+ * RoPE (576), V = dequant NoPE (512).  q [B][128][576] bf16, out [B][128][512]
+ * bf16, lse [B][128] f32 (natural log).                                          */
+int ess_sparse_mla(ess_pool *pool, int32_t pool_begin, const void *d_q,
+                   const int32_t *d_sel_row, int32_t sel_stride, const int32_t *d_count,
+                   int32_t batch, float sm_scale, void *d_out, float *d_lse, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ESS_B200_H */

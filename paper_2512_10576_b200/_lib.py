@@ -1,0 +1,103 @@
+"""ctypes binding of libess_b200.so (include/ess_b200.h).
+
+The product path has exactly one implementation: the sm_100a kernels behind this
+library.  If the library is missing or no CUDA device is present, calls fail
+loudly — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libess_b200.so")
+
+V, I32, I64, F32, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_size_t
+PI32, PI64, PV = ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_void_p)
+
+# name -> argtypes (restype int unless noted); mirrors include/ess_b200.h
+SIGNATURES = {
+    "ess_version": ([], ctypes.c_char_p),
+    "ess_status_string": ([ctypes.c_int], ctypes.c_char_p),
+    "ess_host_register": ([V, SZ, PV], ctypes.c_int),
+    "ess_host_unregister": ([V], ctypes.c_int),
+    "ess_pool_create": ([PV, I32, I64, I32, I32, I32], ctypes.c_int),
+    "ess_pool_destroy": ([V], ctypes.c_int),
+    "ess_pool_reset": ([V, I32, I32, V, V], ctypes.c_int),
+    "ess_pool_grow": ([V, I32, I32, V, V], ctypes.c_int),
+    "ess_pool_warmup": ([V, I32, I32, V, V, I32, V, V], ctypes.c_int),
+    "ess_pool_access": ([V, I32, I32, V, V, I32, V, V, V, V, V, V, I32, I32, V], ctypes.c_int),
+    "ess_pool_append": ([V, I32, I32, V, V, I32, V, V], ctypes.c_int),
+    "ess_pool_lru_order": ([V, I32, I32, V, V, V], ctypes.c_int),
+    "ess_pool_counters": ([V, I32, I32, V, V], ctypes.c_int),
+    "ess_pool_lookup": ([V, I32, V, I32, V, V], ctypes.c_int),
+    "ess_pool_copy_state": ([V, I32, V, I32, I32, V], ctypes.c_int),
+    "ess_pool_status": ([V, PI32], ctypes.c_int),
+    "ess_pool_info": ([V, PI32, PI64, PI32, PI32, PI64, PV], ctypes.c_int),
+    "ess_gather": ([V, I32, I32, V, I64, V, V, V, I32, I32, V], ctypes.c_int),
+    "ess_write_generated": ([V, I32, I32, V, V, V, I32, V, V, I64, V], ctypes.c_int),
+    "ess_indexer_logits": ([V, V, V, V, V, I32, I64, V, V], ctypes.c_int),
+    "ess_topk": ([V, I64, V, I32, I32, V, I32, V, V], ctypes.c_int),
+    "ess_sparse_mla": ([V, I32, V, V, I32, V, I32, F32, V, V, V], ctypes.c_int),
+}
+
+ESS_OK = 0
+ESS_ERR_CAPACITY, ESS_ERR_SHRINK, ESS_ERR_DUPLICATE = -1, -2, -3
+ESS_ERR_NOMEM, ESS_ERR_RATIO, ESS_ERR_ARG, ESS_ERR_CUDA, ESS_ERR_CLOCK = -4, -5, -6, -7, -8
+ESS_ACCESS_SORT_EVICTED = 1
+MAX_REQUEST = 2048
+LATENT_ROW_BYTES = 656
+
+_lib = None
+
+
+def load():
+    """Load the library (no CUDA calls).  Raises if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing; build it with "
+                              "`python -m paper_2512_10576_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def status_text(rc: int) -> str:
+    return load().ess_status_string(rc).decode()
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map an ESS_* status to the reference's exception classes."""
+    if rc == ESS_OK:
+        return
+    msg = f"{what}: {status_text(rc)}" if what else status_text(rc)
+    if rc in (ESS_ERR_CAPACITY, ESS_ERR_SHRINK, ESS_ERR_DUPLICATE, ESS_ERR_RATIO, ESS_ERR_ARG):
+        raise ValueError(msg)
+    if rc == ESS_ERR_NOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None passes NULL)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def require_cuda(t=None) -> None:
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("ess_b200 needs a CUDA device (sm_100a); no CPU fallback exists")
+    if t is not None and not t.is_cuda:
+        raise ValueError("tensor must be on the CUDA device")

@@ -1,0 +1,254 @@
+// K1: lightning indexer (op "indexer_logits", costmodel.py:18-27).
+//
+//   logits[b][s] = kscale[b][s] * sum_h w[b][h] * relu(q[b][h] . k[b][s])
+//
+// The head contraction is a real GEMM per 128-token tile: D[128 tok][64 heads] =
+// K_tile[128 x 128 e4m3] . Q[64 x 128 e4m3]^T, issued as tcgen05.mma kind::f8f6f4
+// (M=128, N=64, 4 x K=32) by one thread into a TMEM accumulator, double-buffered so
+// the epilogue (ReLU, head-weighted sum, x kscale) of tile i overlaps the MMA of
+// tile i+1.  TMA (SWIZZLE_128B) streams K tiles through a 6-stage mbarrier ring;
+// the kernel is persistent (one CTA per SM, contiguous tile ranges) and HBM-bound:
+// 132 B/token in, 4 B/token out.
+//
+// Warp roles (192 threads): w0 TMA producer, w1 TMEM alloc + MMA issuer,
+// w2..w5 epilogue (TMEM lane quarter = warp % 4).
+#include <cuda.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int STAGES = 6;
+constexpr int TILE_M = 128;                 // tokens per tile
+constexpr int HEADS = ESS_INDEXER_HEADS;    // 64 = N
+constexpr int DIM = ESS_INDEXER_DIM;        // 128 = K (bytes, e4m3)
+constexpr int KT_BYTES = TILE_M * DIM;      // 16 KB
+constexpr int QT_BYTES = HEADS * DIM;       // 8 KB
+constexpr int STAGE_BYTES = KT_BYTES + QT_BYTES;
+constexpr int NTHREADS = 192;
+constexpr int MAX_BATCH = 4096;
+constexpr int TMEM_COLS = 128;              // 2 accumulators x 64 columns
+constexpr uint32_t IDESC = make_idesc(0 /*e4m3*/, 0 /*e4m3*/, TILE_M, HEADS, 0, 0);
+
+struct Ctrl {
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t tfull[2];
+  uint64_t tempty[2];
+  uint32_t tmem;
+  int pref[MAX_BATCH + 1];
+};
+
+constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + sizeof(Ctrl);
+
+// Walk the flattened (request, tile) sequence.
+struct TileCursor {
+  int b, t;
+  __device__ void seek(const int *pref, int B, int idx) {
+    int lo = 0, hi = B - 1;
+    while (lo < hi) {  // last b with pref[b] <= idx
+      int mid = (lo + hi + 1) >> 1;
+      if (pref[mid] <= idx) lo = mid; else hi = mid - 1;
+    }
+    b = lo;
+    t = idx - pref[lo];
+  }
+  __device__ void next(const int *pref, int B) {
+    t++;
+    while (b < B && pref[b] + t >= pref[b + 1]) {
+      t = t - (pref[b + 1] - pref[b]);
+      b++;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    indexer_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_q,
+                   const float *__restrict__ w, const float *__restrict__ kscale,
+                   const int32_t *__restrict__ lens, int B, int64_t k_ld, float *__restrict__ logits) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Ctrl &c = *reinterpret_cast<Ctrl *>(smem + (size_t)STAGES * STAGE_BYTES);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // tile prefix over requests (every CTA computes it; B is small)
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int b = 0; b < B; b++) {
+      c.pref[b] = acc;
+      int L = lens[b];
+      acc += L > 0 ? (L + TILE_M - 1) / TILE_M : 0;
+    }
+    c.pref[B] = acc;
+    for (int s = 0; s < STAGES; s++) {
+      mbar_init(&c.full[s], 1);
+      mbar_init(&c.empty[s], 1);
+    }
+    for (int a = 0; a < 2; a++) {
+      mbar_init(&c.tfull[a], 1);
+      mbar_init(&c.tempty[a], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(&c.tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = c.tmem;
+  const int total = c.pref[B];
+  const int t0 = (int)((int64_t)total * blockIdx.x / gridDim.x);
+  const int t1 = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
+
+  if (t0 < t1) {
+    if (warp == 0) {
+      if (elect_one()) {
+        prefetch_tmap(&tm_k);
+        prefetch_tmap(&tm_q);
+        TileCursor cur;
+        cur.seek(c.pref, B, t0);
+        for (int it = 0; it < t1 - t0; it++) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          mbar_wait(&c.empty[s], ph ^ 1);
+          uint8_t *kb = smem + (size_t)s * STAGE_BYTES;
+          mbar_arrive_expect_tx(&c.full[s], STAGE_BYTES);
+          tma_load_2d(kb, &tm_k, &c.full[s], 0, (int32_t)(cur.b * k_ld + (int64_t)cur.t * TILE_M));
+          tma_load_2d(kb + KT_BYTES, &tm_q, &c.full[s], 0, cur.b * HEADS);
+          cur.next(c.pref, B);
+        }
+      }
+    } else if (warp == 1) {
+      if (elect_one()) {
+        for (int it = 0; it < t1 - t0; it++) {
+          const int s = it % STAGES;
+          const uint32_t ph = (it / STAGES) & 1;
+          const int a = it & 1;
+          const uint32_t aph = (it >> 1) & 1;
+          mbar_wait(&c.tempty[a], aph ^ 1);
+          mbar_wait(&c.full[s], ph);
+          tc_fence_after();
+          const uint32_t kaddr = smem_u32(smem + (size_t)s * STAGE_BYTES);
+          const uint32_t qaddr = kaddr + KT_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < DIM / 32; kk++) {
+            uint64_t ad = sw128_desc(kaddr + kk * 32, 16, 1024);
+            uint64_t bd = sw128_desc(qaddr + kk * 32, 16, 1024);
+            mma_f8f6f4_ss(tmem + a * HEADS, ad, bd, IDESC, kk > 0 ? 1u : 0u);
+          }
+          tc_commit(&c.empty[s]);
+          tc_commit(&c.tfull[a]);
+        }
+      }
+    } else {
+      // epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
+      const int quarter = warp & 3;
+      const int row = quarter * 32 + lane;
+      TileCursor cur;
+      cur.seek(c.pref, B, t0);
+      for (int it = 0; it < t1 - t0; it++) {
+        const int a = it & 1;
+        const uint32_t aph = (it >> 1) & 1;
+        mbar_wait(&c.tfull[a], aph);
+        tc_fence_after();
+        uint32_t r[64];
+        tmem_ld_32x32b_x64(tmem + ((uint32_t)(quarter * 32) << 16) + a * HEADS, r);
+        tmem_ld_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&c.tempty[a]);
+        const int b = cur.b;
+        const int64_t tok = (int64_t)cur.t * TILE_M + row;
+        if (tok < lens[b]) {
+          const float4 *wb = reinterpret_cast<const float4 *>(w + (int64_t)b * HEADS);
+          float acc = 0.f;
+#pragma unroll
+          for (int h4 = 0; h4 < HEADS / 4; h4++) {
+            float4 wv = __ldg(wb + h4);
+            acc = fmaf(wv.x, fmaxf(__uint_as_float(r[4 * h4 + 0]), 0.f), acc);
+            acc = fmaf(wv.y, fmaxf(__uint_as_float(r[4 * h4 + 1]), 0.f), acc);
+            acc = fmaf(wv.z, fmaxf(__uint_as_float(r[4 * h4 + 2]), 0.f), acc);
+            acc = fmaf(wv.w, fmaxf(__uint_as_float(r[4 * h4 + 3]), 0.f), acc);
+          }
+          const int64_t off = (int64_t)b * k_ld + tok;
+          logits[off] = acc * __ldg(kscale + off);
+        }
+        cur.next(c.pref, B);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2D uint8 tensor [rows][128 B], box [box_rows][128 B], 128-B swizzle
+bool make_map(CUtensorMap *m, const void *base, uint64_t rows, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {128, rows};
+  cuuint64_t strides[1] = {128};
+  cuuint32_t box[2] = {128, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+}  // namespace
+
+extern "C" int ess_indexer_logits(const void *d_q, const float *d_w, const void *d_k,
+                                  const float *d_kscale, const int32_t *d_len, int32_t batch,
+                                  int64_t k_ld, float *d_logits, void *stream) {
+  if (!d_q || !d_w || !d_k || !d_kscale || !d_len || !d_logits || batch < 0 ||
+      batch > MAX_BATCH || k_ld < TILE_M || (k_ld % TILE_M) != 0 ||
+      (reinterpret_cast<uintptr_t>(d_k) & 15) || (reinterpret_cast<uintptr_t>(d_q) & 15) ||
+      (reinterpret_cast<uintptr_t>(d_w) & 15))
+    return ESS_ERR_ARG;
+  if (batch == 0) return ESS_OK;
+  CUtensorMap tk, tq;
+  if (!make_map(&tk, d_k, (uint64_t)batch * (uint64_t)k_ld, TILE_M)) return ESS_ERR_CUDA;
+  if (!make_map(&tq, d_q, (uint64_t)batch * HEADS, HEADS)) return ESS_ERR_CUDA;
+  static bool attr = false;
+  if (!attr) {
+    ESS_CUDA_TRY(cudaFuncSetAttribute(indexer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)SMEM_BYTES));
+    attr = true;
+  }
+  indexer_kernel<<<sm_count(), NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
+      tk, tq, d_w, d_kscale, d_len, batch, k_ld, d_logits);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}

@@ -1,0 +1,951 @@
+// K3: on-device LRU latent-cache manager, plus K4 zero-copy miss gather and the
+// generated-row write-back.  Replaces offsim.cache.SparsePool
+// (/root/reference/pkg/src/offsim/cache.py:29-134) for P independent pools at once.
+//
+// Parallel contract (verified bit-exact against the reference):
+//   * every pool keeps key[slot]: a free slot has key == slot index (< cap_max), a
+//     resident slot a stamp from a strictly increasing clock (>= ESS_CLOCK_BASE);
+//   * access, n <= cap (cache.py:112-118): hits (requested order) get stamps
+//     clk.., then the nmiss smallest keys are selected (radix select) — free slots
+//     first, then the least-recent residents that were NOT requested (hits were
+//     just re-stamped above every old stamp) — and the j-th miss takes the j-th
+//     selected slot (ascending slot index) with stamp clk+nhit+j;
+//   * access, n > cap (cache.py:103-111): keep = requested[n-cap:], every other
+//     resident is evicted (counted), kept misses take the freed slots, requested
+//     ids before keep are transient (served from per-pool staging rows);
+//   * warm-up (cache.py:73-88): same machinery with stamps in window order and
+//     uncounted evictions; windows longer than cap get the exact "inserted" count
+//     from a reuse-distance test;
+//   * append (cache.py:122-134): per new id, the smallest key is either a free
+//     slot or the LRU resident (evicted, counted).
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int NT = 1024;                 // threads per pool CTA
+constexpr int MAXR = ESS_MAX_REQUEST;    // 2048 ids per call
+constexpr int EPT = MAXR / NT;           // elements per thread (contiguous)
+constexpr int ROW_CHUNKS = ESS_LATENT_ROW_BYTES / 16;  // 41 x 16 B
+
+enum { MODE_ACCESS = 0, MODE_WARMUP = 1 };
+
+struct StepSmem {
+  int id[MAXR];
+  int slot[MAXR];      // old slot (-1 = not resident), later the final row
+  int sel[MAXR];       // selected / free slots, ascending
+  int ev[MAXR];        // evicted ids (unsorted, then optionally sorted)
+  unsigned char mark[MAXR];
+  int hist[256];
+  int warp[32];
+  int scal[8];
+};
+
+struct PoolView {
+  PoolMeta *meta;
+  int32_t *slot_of;
+  int32_t *slot_id;
+  uint32_t *key;
+  uint8_t *rows;
+  int32_t *status;
+  int64_t max_ids;
+  int32_t cap_max;
+  int32_t row_bytes;
+  int32_t staging;
+  int64_t rows_per_pool;
+};
+
+PoolView view(const ess_pool *p) {
+  return PoolView{p->meta,   p->slot_of,   p->slot_id, p->key,     p->rows,         p->status,
+                  p->max_ids, p->cap_max, p->row_bytes, p->staging, p->rows_per_pool};
+}
+
+// k-th smallest (1-based) of keys[0:cnt) — keys are unique, so exactly kth keys
+// are <= the result.  4 passes of 8-bit digits, histogram in shared memory.
+__device__ uint32_t select_kth_smallest(const uint32_t *__restrict__ keys, int cnt, int kth,
+                                        StepSmem &sm) {
+  uint32_t prefix = 0, mask = 0;
+  int rem = kth;
+  for (int shift = 24; shift >= 0; shift -= 8) {
+    for (int i = threadIdx.x; i < 256; i += NT) sm.hist[i] = 0;
+    __syncthreads();
+    for (int s = threadIdx.x; s < cnt; s += NT) {
+      uint32_t k = keys[s];
+      if ((k & mask) == prefix) atomicAdd(&sm.hist[(k >> shift) & 255u], 1);
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      int loc[8], sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; j++) {
+        loc[j] = sm.hist[lane * 8 + j];
+        sum += loc[j];
+      }
+      int incl = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int c = incl - sum;
+      if (c < rem && rem <= incl) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          if (c + loc[j] >= rem) {
+            sm.scal[0] = lane * 8 + j;
+            sm.scal[1] = rem - c;
+            break;
+          }
+          c += loc[j];
+        }
+      }
+    }
+    __syncthreads();
+    prefix |= (uint32_t)sm.scal[0] << shift;
+    mask |= 0xFFu << shift;
+    rem = sm.scal[1];
+    __syncthreads();
+  }
+  return prefix;
+}
+
+// Ascending bitonic sort of sm.ev[0:n), n <= MAXR.
+__device__ void sort_ids(StepSmem &sm, int n) {
+  int m = 1;
+  while (m < n) m <<= 1;
+  for (int i = n + threadIdx.x; i < m; i += NT) sm.ev[i] = 0x7fffffff;
+  __syncthreads();
+  for (int k = 2; k <= m; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < m; i += NT) {
+        int l = i ^ j;
+        if (l > i) {
+          int a = sm.ev[i], b = sm.ev[l];
+          bool up = (i & k) == 0;
+          if ((a > b) == up) {
+            sm.ev[i] = b;
+            sm.ev[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ void copy_row(const uint8_t *src, uint8_t *dst, int lane) {
+  for (int c = lane; c < ROW_CHUNKS; c += 32)
+    reinterpret_cast<uint4 *>(dst)[c] = reinterpret_cast<const uint4 *>(src)[c];
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(NT, 1)
+    pool_step_kernel(PoolView pv, int begin, const int32_t *__restrict__ req,
+                     const int32_t *__restrict__ req_n, int req_stride, int32_t *hit_out,
+                     int32_t *miss_out, int32_t *ev_out, int32_t *sel_row_out,
+                     int32_t *miss_row_out, int32_t *counts_out, int out_stride, int flags,
+                     int64_t *inserted_out) {
+  __shared__ StepSmem sm;
+  const int t = threadIdx.x;
+  const int b = blockIdx.x;
+  const int p = begin + b;
+  const int n = req_n[b];
+  PoolMeta *meta = pv.meta + p;
+  int32_t *slot_of = pv.slot_of + (int64_t)p * pv.max_ids;
+  int32_t *slot_id = pv.slot_id + (int64_t)p * pv.cap_max;
+  uint32_t *key = pv.key + (int64_t)p * pv.cap_max;
+  const int cap = meta->cap;
+  const int size0 = meta->size;
+  const uint32_t clk = meta->clk;
+  const int64_t out_base = (int64_t)b * out_stride;
+
+  // ---- load + validate -------------------------------------------------------
+  bool bad = n < 0 || n > MAXR || (uint64_t)clk + (uint64_t)n > 0xFFFFFF00ull;
+  int hflag[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; e++) {
+    int i = t * EPT + e;
+    hflag[e] = 0;
+    if (!bad && i < n) {
+      int x = req[(int64_t)b * req_stride + i];
+      if (x < 0 || x >= pv.max_ids) {
+        bad = true;
+      } else {
+        sm.id[i] = x;
+        int s = slot_of[x];
+        sm.slot[i] = s;
+        hflag[e] = s >= 0;
+      }
+    }
+  }
+  if (__syncthreads_or(bad)) {
+    if (t == 0) ess_set_status(pv.status, (n > MAXR || n < 0) ? ESS_ERR_ARG
+                                          : ((uint64_t)clk + (uint64_t)n > 0xFFFFFF00ull)
+                                              ? ESS_ERR_CLOCK
+                                              : ESS_ERR_ARG);
+    return;
+  }
+
+  // ---- hit / miss split in requested order (cache.py:98-99) ---------------------
+  int nh_local = 0;
+#pragma unroll
+  for (int e = 0; e < EPT; e++) nh_local += hflag[e];
+  int nhit;
+  int hr = block_exclusive_scan<NT>(nh_local, sm.warp, &nhit);
+  const int nmiss = n - nhit;
+  int hrank[EPT], mrank[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; e++) {
+    int i = t * EPT + e;
+    hrank[e] = hr;
+    mrank[e] = i - hr;
+    if (i < n) {
+      if (hflag[e]) {
+        if (MODE == MODE_ACCESS && hit_out) hit_out[out_base + hr] = sm.id[i];
+        hr++;
+      } else if (MODE == MODE_ACCESS && miss_out) {
+        miss_out[out_base + (i - hrank[e])] = sm.id[i];
+      }
+    }
+  }
+
+  int nev = 0;
+  int64_t inserted = 0;
+  if (n <= cap) {
+    // ---- normal path (cache.py:112-118; warm-up windows <= cap, cache.py:79-87) --
+#pragma unroll
+    for (int e = 0; e < EPT; e++) {
+      int i = t * EPT + e;
+      if (i < n && hflag[e])
+        key[sm.slot[i]] = (MODE == MODE_ACCESS) ? clk + hrank[e] : clk + i;
+    }
+    __syncthreads();
+    if (nmiss > 0) {
+      const uint32_t T = select_kth_smallest(key, cap, nmiss, sm);
+      int base = 0;
+      for (int s0 = 0; s0 < cap; s0 += NT) {
+        int s = s0 + t;
+        int f = (s < cap && key[s] <= T) ? 1 : 0;
+        int tot;
+        int pos = block_exclusive_scan<NT>(f, sm.warp, &tot);
+        if (f && base + pos < MAXR) sm.sel[base + pos] = s;
+        base += tot;
+      }
+      __syncthreads();
+      // victims: selected slots that were occupied (least recent first is not needed:
+      // the set is what matters, evicted_ids is reported sorted, cache.py:120)
+      int ef[EPT], eid[EPT], ne_local = 0;
+#pragma unroll
+      for (int e = 0; e < EPT; e++) {
+        int j = t * EPT + e;
+        ef[e] = 0;
+        if (j < nmiss) {
+          int old = slot_id[sm.sel[j]];
+          eid[e] = old;
+          ef[e] = old >= 0;
+          ne_local += ef[e];
+        }
+      }
+      int epos = block_exclusive_scan<NT>(ne_local, sm.warp, &nev);
+#pragma unroll
+      for (int e = 0; e < EPT; e++) {
+        if (ef[e]) {
+          sm.ev[epos++] = eid[e];
+          slot_of[eid[e]] = -1;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < EPT; e++) {
+        int i = t * EPT + e;
+        if (i < n && !hflag[e]) {
+          int j = mrank[e];
+          int s = sm.sel[j];
+          slot_of[sm.id[i]] = s;
+          slot_id[s] = sm.id[i];
+          key[s] = (MODE == MODE_ACCESS) ? clk + nhit + j : clk + i;
+          sm.slot[i] = s;
+          if (MODE == MODE_ACCESS && miss_row_out) miss_row_out[out_base + j] = s;
+        }
+      }
+    }
+    if (MODE == MODE_WARMUP) inserted = nmiss;
+  } else {
+    // ---- oversize path: keep requested[n-cap:] (cache.py:103-111) -----------------
+    const int keep0 = n - cap;  // cap < n <= MAXR, so every slot index < MAXR
+    if (MODE == MODE_ACCESS && pv.rows && keep0 > pv.staging && t == 0)
+      ess_set_status(pv.status, ESS_ERR_ARG);  // not enough staging rows for transients
+    if (MODE == MODE_WARMUP) {
+      // reuse-distance test for the exact inserted count (see file header)
+      uint32_t *okey = reinterpret_cast<uint32_t *>(sm.ev);   // occupied old keys by slot
+      uint32_t *pkey = reinterpret_cast<uint32_t *>(sm.sel);  // old key by window position
+      for (int s = t; s < cap; s += NT) okey[s] = slot_id[s] >= 0 ? key[s] : 0u;
+#pragma unroll
+      for (int e = 0; e < EPT; e++) {
+        int i = t * EPT + e;
+        if (i < n) pkey[i] = hflag[e] ? key[sm.slot[i]] : 0u;
+      }
+      __syncthreads();
+      int ins_local = 0;
+#pragma unroll
+      for (int e = 0; e < EPT; e++) {
+        int i = t * EPT + e;
+        if (i >= n) continue;
+        if (!hflag[e] || i >= cap) {
+          ins_local++;
+          continue;
+        }
+        uint32_t sx = pkey[i];
+        int A = 0, B = 0;
+        for (int s = 0; s < cap; s++) A += okey[s] > sx;
+        for (int j = 0; j < i; j++) B += pkey[j] > sx;
+        ins_local += (A + i - B >= cap);
+      }
+      int tot;
+      block_exclusive_scan<NT>(ins_local, sm.warp, &tot);
+      inserted = tot;
+    }
+    for (int s = t; s < MAXR; s += NT) sm.mark[s] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < EPT; e++) {
+      int i = t * EPT + e;
+      if (i >= keep0 && i < n && hflag[e]) sm.mark[sm.slot[i]] = 1;
+    }
+    __syncthreads();
+    // transient requested-but-not-kept residents: preserve their rows in staging
+    // before their slots are reused (the attention kernel reads them this step)
+    if (MODE == MODE_ACCESS && pv.rows) {
+      const int warp = t >> 5, lane = t & 31;
+      uint8_t *rbase = pv.rows + (int64_t)p * pv.rows_per_pool * pv.row_bytes;
+      for (int i = warp; i < keep0; i += NT / 32) {
+        int s = sm.slot[i];
+        if (s >= 0)
+          copy_row(rbase + (int64_t)s * pv.row_bytes,
+                   rbase + (int64_t)(pv.cap_max + i) * pv.row_bytes, lane);
+      }
+    }
+    // evict every resident outside keep; the freed slots (ascending) host kept misses
+    int ebase = 0, fbase = 0;
+    for (int s0 = 0; s0 < cap; s0 += NT) {
+      int s = s0 + t;
+      int freef = (s < cap && !sm.mark[s]) ? 1 : 0;
+      int old = freef ? slot_id[s] : -1;
+      int evf = old >= 0 ? 1 : 0;
+      int etot, ftot;
+      int ep = block_exclusive_scan<NT>(evf, sm.warp, &etot);
+      int fp = block_exclusive_scan<NT>(freef, sm.warp, &ftot);
+      if (evf) {
+        sm.ev[ebase + ep] = old;
+        slot_of[old] = -1;
+        slot_id[s] = -1;
+      }
+      if (freef) sm.sel[fbase + fp] = s;
+      ebase += etot;
+      fbase += ftot;
+    }
+    nev = ebase;
+    __syncthreads();
+    int km_local = 0;
+#pragma unroll
+    for (int e = 0; e < EPT; e++) {
+      int i = t * EPT + e;
+      km_local += (i >= keep0 && i < n && !hflag[e]);
+    }
+    int kmtot;
+    int km = block_exclusive_scan<NT>(km_local, sm.warp, &kmtot);
+#pragma unroll
+    for (int e = 0; e < EPT; e++) {
+      int i = t * EPT + e;
+      if (i >= n) continue;
+      if (i >= keep0) {
+        int s;
+        if (hflag[e]) {
+          s = sm.slot[i];
+        } else {
+          s = sm.sel[km++];
+          slot_of[sm.id[i]] = s;
+          slot_id[s] = sm.id[i];
+        }
+        key[s] = (MODE == MODE_ACCESS) ? clk + (i - keep0) : clk + i;
+        sm.slot[i] = s;
+      } else {
+        sm.slot[i] = pv.cap_max + i;  // transient: staging row
+      }
+      if (MODE == MODE_ACCESS && miss_row_out && !hflag[e]) miss_row_out[out_base + mrank[e]] = sm.slot[i];
+    }
+  }
+  __syncthreads();
+
+  // ---- outputs + counters -----------------------------------------------------
+  if (MODE == MODE_ACCESS) {
+    if (sel_row_out) {
+#pragma unroll
+      for (int e = 0; e < EPT; e++) {
+        int i = t * EPT + e;
+        if (i < n) sel_row_out[out_base + i] = sm.slot[i];
+      }
+    }
+    if (ev_out) {
+      if (flags & ESS_ACCESS_SORT_EVICTED) sort_ids(sm, nev);
+      for (int j = t; j < nev; j += NT) ev_out[out_base + j] = sm.ev[j];
+    }
+  }
+  if (t == 0) {
+    if (MODE == MODE_ACCESS) {
+      meta->hits += nhit;
+      meta->misses += nmiss;
+      meta->evictions += nev;
+      if (counts_out) {
+        counts_out[b * 4 + 0] = nhit;
+        counts_out[b * 4 + 1] = nmiss;
+        counts_out[b * 4 + 2] = nev;
+        counts_out[b * 4 + 3] = n > cap ? n - cap : 0;
+      }
+    } else if (inserted_out) {
+      inserted_out[b] += inserted;
+    }
+    if (n <= cap) {
+      meta->clk = clk + n;
+      meta->size = size0 + nmiss - nev;
+    } else {
+      meta->clk = clk + n;
+      meta->size = cap;
+    }
+  }
+}
+
+__global__ void pool_reset_kernel(PoolView pv, int begin, int num, const int32_t *cap) {
+  // grid: (num, y) — y-blocks stride over the per-pool arrays
+  const int b = blockIdx.x, p = begin + b;
+  const int c = cap[b];
+  if (blockIdx.y == 0 && threadIdx.x == 0) {
+    if (c < 1 || c > pv.cap_max) {
+      ess_set_status(pv.status, ESS_ERR_CAPACITY);
+    }
+    PoolMeta m;
+    memset(&m, 0, sizeof(m));
+    m.cap = (c < 1 || c > pv.cap_max) ? 1 : c;
+    m.clk = ESS_CLOCK_BASE;
+    m.watermark = -1;
+    pv.meta[p] = m;
+  }
+  int32_t *so = pv.slot_of + (int64_t)p * pv.max_ids;
+  for (int64_t i = (int64_t)blockIdx.y * blockDim.x + threadIdx.x; i < pv.max_ids;
+       i += (int64_t)gridDim.y * blockDim.x)
+    so[i] = -1;
+  int32_t *sid = pv.slot_id + (int64_t)p * pv.cap_max;
+  uint32_t *k = pv.key + (int64_t)p * pv.cap_max;
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < pv.cap_max; i += gridDim.y * blockDim.x) {
+    sid[i] = -1;
+    k[i] = (uint32_t)i;
+  }
+}
+
+__global__ void pool_grow_kernel(PoolView pv, int begin, int num, const int32_t *cap) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= num) return;
+  PoolMeta *m = pv.meta + begin + b;
+  int c = cap[b];
+  if (c < m->cap) {
+    ess_set_status(pv.status, ESS_ERR_SHRINK);
+  } else if (c > pv.cap_max) {
+    ess_set_status(pv.status, ESS_ERR_CAPACITY);
+  } else {
+    m->cap = c;
+  }
+}
+
+constexpr int NTA = 256;
+
+// block-wide argmin of key[0:cap) -> slot (keys unique)
+__device__ int argmin_key(const uint32_t *key, int cap, unsigned long long *red) {
+  unsigned long long best = ~0ull;
+  for (int s = threadIdx.x; s < cap; s += NTA) {
+    unsigned long long v = ((unsigned long long)key[s] << 32) | (unsigned)s;
+    best = v < best ? v : best;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long y = __shfl_xor_sync(0xffffffffu, best, o);
+    best = y < best ? y : best;
+  }
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long v = red[0];
+    for (int w = 1; w < NTA / 32; w++) v = red[w] < v ? red[w] : v;
+    red[NTA / 32] = v;
+  }
+  __syncthreads();
+  int s = (int)(red[NTA / 32] & 0xffffffffu);
+  __syncthreads();
+  return s;
+}
+
+// cache.py:122-134 — validation of all ids first, then per id: evict the LRU if
+// full (counted), touch.  Sequential over the (few) generated ids of a step.
+__global__ void __launch_bounds__(NTA) pool_append_kernel(PoolView pv, int begin,
+                                                         const int32_t *ids, const int32_t *m,
+                                                         int stride, int32_t *slot_out) {
+  __shared__ unsigned long long red[NTA / 32 + 1];
+  const int b = blockIdx.x, p = begin + b;
+  const int M = m[b];
+  PoolMeta *meta = pv.meta + p;
+  int32_t *slot_of = pv.slot_of + (int64_t)p * pv.max_ids;
+  int32_t *slot_id = pv.slot_id + (int64_t)p * pv.cap_max;
+  uint32_t *key = pv.key + (int64_t)p * pv.cap_max;
+  const int64_t wm = meta->watermark;
+  uint32_t clk = meta->clk;
+  int code = 0;
+  if (M < 0 || (uint64_t)clk + (uint64_t)(M < 0 ? 0 : M) > 0xFFFFFF00ull) code = ESS_ERR_ARG;
+  for (int i = threadIdx.x; code == 0 && i < M; i += NTA) {
+    int x = ids[(int64_t)b * stride + i];
+    if (x < 0 || x >= pv.max_ids) code = ESS_ERR_ARG;
+    else if (slot_of[x] >= 0 || (int64_t)x <= wm) code = ESS_ERR_DUPLICATE;
+  }
+  if (__syncthreads_or(code != 0)) {
+    if (code && threadIdx.x == 0) ess_set_status(pv.status, code);
+    if (code) ess_set_status(pv.status, code);
+    return;
+  }
+  const int cap = meta->cap;
+  int size = meta->size;
+  int64_t evictions = 0, w = wm;
+  for (int i = 0; i < M; i++) {
+    const int x = ids[(int64_t)b * stride + i];
+    int s = -1;
+    if (size >= cap) {
+      s = argmin_key(key, cap, reinterpret_cast<unsigned long long *>(red));
+      if (threadIdx.x == 0) {
+        int old = slot_id[s];
+        slot_of[old] = -1;
+        slot_id[s] = -1;
+        key[s] = (uint32_t)s;
+      }
+      size--;
+      evictions++;
+      __syncthreads();
+    }
+    int cur = slot_of[x];
+    __syncthreads();
+    if (cur >= 0) {  // duplicate inside this call: refresh only (cache.py:132 touch)
+      if (threadIdx.x == 0) key[cur] = clk;
+      s = cur;
+    } else {
+      if (s < 0) s = argmin_key(key, cap, reinterpret_cast<unsigned long long *>(red));
+      if (threadIdx.x == 0) {
+        slot_of[x] = s;
+        slot_id[s] = x;
+        key[s] = clk;
+      }
+      size++;
+    }
+    clk++;
+    if (x > w) w = x;
+    if (slot_out && threadIdx.x == 0) slot_out[(int64_t)b * stride + i] = s;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    meta->size = size;
+    meta->clk = clk;
+    meta->watermark = w;
+    meta->evictions += evictions;
+  }
+}
+
+// rank of each resident by stamp = its LRU position (cache.py:55-57)
+__global__ void pool_lru_order_kernel(PoolView pv, int begin, int32_t *out, int32_t *count) {
+  __shared__ uint32_t tile[256];
+  const int b = blockIdx.x, p = begin + b;
+  const int cap = pv.meta[p].cap;
+  const int32_t *slot_id = pv.slot_id + (int64_t)p * pv.cap_max;
+  const uint32_t *key = pv.key + (int64_t)p * pv.cap_max;
+  const int s = blockIdx.y * 256 + threadIdx.x;
+  const bool valid = s < cap && slot_id[s] >= 0;
+  const uint32_t mk = valid ? key[s] : 0xFFFFFFFFu;
+  int rank = 0;
+  for (int t0 = 0; t0 < cap; t0 += 256) {
+    int u = t0 + threadIdx.x;
+    tile[threadIdx.x] = (u < cap && slot_id[u] >= 0) ? key[u] : 0xFFFFFFFFu;
+    __syncthreads();
+    int lim = min(256, cap - t0);
+    for (int j = 0; j < lim; j++) rank += tile[j] < mk;
+    __syncthreads();
+  }
+  if (valid) out[(int64_t)b * pv.cap_max + rank] = slot_id[s];
+  if (blockIdx.y == 0 && threadIdx.x == 0) count[b] = pv.meta[p].size;
+}
+
+__global__ void pool_counters_kernel(PoolView pv, int begin, int num, int64_t *out) {
+  int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= num) return;
+  const PoolMeta m = pv.meta[begin + b];
+  int64_t *o = out + (int64_t)b * 8;
+  o[0] = m.cap;
+  o[1] = m.size;
+  o[2] = m.hits;
+  o[3] = m.misses;
+  o[4] = m.evictions;
+  o[5] = m.clk;
+  o[6] = m.watermark;
+  o[7] = 0;
+}
+
+// ---- K4: zero-copy gather of miss rows ------------------------
+constexpr int NTG = 256;
+constexpr int GROWS = 4;  // rows per warp iteration -> 8 x 16-B loads in flight per lane
+
+__global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int num,
+                                                     const uint8_t *host, int64_t host_stride,
+                                                     const int32_t *__restrict__ miss_ids,
+                                                     const int32_t *__restrict__ miss_row,
+                                                     const int32_t *__restrict__ counts,
+                                                     int stride) {
+  extern __shared__ int pref[];  // [num + 1]
+  __shared__ int wbuf[NTG / 32];
+  int run = 0;
+  for (int c0 = 0; c0 < num; c0 += NTG) {
+    int i = c0 + threadIdx.x;
+    int v = i < num ? counts[i * 4 + 1] : 0;
+    int tot;
+    int ex = block_exclusive_scan<NTG>(v, wbuf, &tot);
+    if (i < num) pref[i] = run + ex;
+    run += tot;
+  }
+  if (threadIdx.x == 0) pref[num] = run;
+  __syncthreads();
+  const int total = run;
+  const int lane = threadIdx.x & 31;
+  const int gwarp = blockIdx.x * (NTG / 32) + (threadIdx.x >> 5);
+  const int nwarps = gridDim.x * (NTG / 32);
+  const int64_t rb = pv.row_bytes;
+  for (int g0 = gwarp * GROWS; g0 < total; g0 += nwarps * GROWS) {
+    const uint8_t *src[GROWS];
+    uint8_t *dst[GROWS];
+#pragma unroll
+    for (int r = 0; r < GROWS; r++) {
+      int g = g0 + r;
+      src[r] = nullptr;
+      if (g < total) {
+        int lo = 0, hi = num - 1;  // last pool with pref <= g
+        while (lo < hi) {
+          int mid = (lo + hi + 1) >> 1;
+          if (pref[mid] <= g) lo = mid; else hi = mid - 1;
+        }
+        int j = g - pref[lo];
+        int id = miss_ids[(int64_t)lo * stride + j];
+        int row = miss_row[(int64_t)lo * stride + j];
+        src[r] = host + ((int64_t)lo * host_stride + id) * rb;
+        dst[r] = pv.rows + ((int64_t)(begin + lo) * pv.rows_per_pool + row) * rb;
+      }
+    }
+    uint4 v[GROWS][2];
+#pragma unroll
+    for (int r = 0; r < GROWS; r++) {
+      if (src[r]) {
+        v[r][0] = ld_nc_v4(src[r] + lane * 16);
+        if (lane + 32 < ROW_CHUNKS) v[r][1] = ld_nc_v4(src[r] + (lane + 32) * 16);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < GROWS; r++) {
+      if (src[r]) {
+        st_v4(dst[r] + lane * 16, v[r][0]);
+        if (lane + 32 < ROW_CHUNKS) st_v4(dst[r] + (lane + 32) * 16, v[r][1]);
+      }
+    }
+  }
+}
+
+// generated rows -> host store (D2H through the mapped alias) and their slots
+__global__ void write_generated_kernel(PoolView pv, int begin, const int32_t *ids,
+                                       const int32_t *m, const int32_t *slot, int stride,
+                                       const uint8_t *src, uint8_t *host, int64_t host_stride) {
+  const int b = blockIdx.x;
+  const int M = m[b];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t rb = pv.row_bytes;
+  for (int j = warp; j < M; j += blockDim.x / 32) {
+    const int id = ids[(int64_t)b * stride + j];
+    const int s = slot ? slot[(int64_t)b * stride + j] : -1;
+    const uint8_t *sr = src + ((int64_t)b * stride + j) * rb;
+    for (int c = lane; c < ROW_CHUNKS; c += 32) {
+      uint4 v = reinterpret_cast<const uint4 *>(sr)[c];
+      if (host) st_v4(host + ((int64_t)b * host_stride + id) * rb + c * 16, v);
+      if (s >= 0) st_v4(pv.rows + ((int64_t)(begin + b) * pv.rows_per_pool + s) * rb + c * 16, v);
+    }
+  }
+}
+
+__global__ void pool_lookup_kernel(PoolView pv, int p, const int32_t *ids, int n, int32_t *out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int x = ids[i];
+  out[i] = (x >= 0 && x < pv.max_ids) ? pv.slot_of[(int64_t)p * pv.max_ids + x] : -1;
+}
+
+// dst pools [dst_begin, +num) <- src pools [src_begin, +num); dst may be larger in
+// max_ids / cap_max (the extra ids are absent, the extra slots free)
+__global__ void pool_copy_kernel(PoolView d, int dst_begin, PoolView s, int src_begin) {
+  const int b = blockIdx.x;
+  const int pd = dst_begin + b, ps = src_begin + b;
+  if (blockIdx.y == 0 && threadIdx.x == 0) d.meta[pd] = s.meta[ps];
+  const int64_t stride = (int64_t)gridDim.y * blockDim.x;
+  const int64_t i0 = (int64_t)blockIdx.y * blockDim.x + threadIdx.x;
+  for (int64_t i = i0; i < d.max_ids; i += stride)
+    d.slot_of[(int64_t)pd * d.max_ids + i] = i < s.max_ids ? s.slot_of[(int64_t)ps * s.max_ids + i] : -1;
+  for (int64_t i = i0; i < d.cap_max; i += stride) {
+    bool in = i < s.cap_max;
+    d.slot_id[(int64_t)pd * d.cap_max + i] = in ? s.slot_id[(int64_t)ps * s.cap_max + i] : -1;
+    d.key[(int64_t)pd * d.cap_max + i] = in ? s.key[(int64_t)ps * s.cap_max + i] : (uint32_t)i;
+  }
+  if (d.rows && s.rows) {
+    const int64_t nb = (int64_t)(s.cap_max < d.cap_max ? s.cap_max : d.cap_max) * s.row_bytes / 16;
+    const uint4 *src = reinterpret_cast<const uint4 *>(s.rows + (int64_t)ps * s.rows_per_pool * s.row_bytes);
+    uint4 *dst = reinterpret_cast<uint4 *>(d.rows + (int64_t)pd * d.rows_per_pool * d.row_bytes);
+    for (int64_t i = i0; i < nb; i += stride) dst[i] = src[i];
+  }
+}
+
+thread_local int g_last_cuda_error = 0;
+
+bool range_ok(const ess_pool *p, int begin, int num) {
+  return p && begin >= 0 && num >= 0 && (int64_t)begin + num <= p->P;
+}
+
+}  // namespace
+
+int ess_record_cuda_error(cudaError_t e) {
+  g_last_cuda_error = (int)e;
+  return ESS_ERR_CUDA;
+}
+
+extern "C" {
+
+int ess_pool_create(ess_pool **out, int32_t num_pools, int64_t max_ids, int32_t cap_max,
+                    int32_t row_bytes, int32_t staging_rows) {
+  if (!out || num_pools < 1 || max_ids < 1 || max_ids > 0x7fffffff || cap_max < 1 ||
+      cap_max > 0x00ffffff || staging_rows < 0 || row_bytes < 0 ||
+      (row_bytes && row_bytes != ESS_LATENT_ROW_BYTES))
+    return ESS_ERR_ARG;
+  ess_pool *p = (ess_pool *)calloc(1, sizeof(ess_pool));
+  if (!p) return ESS_ERR_NOMEM;
+  p->P = num_pools;
+  p->max_ids = max_ids;
+  p->cap_max = cap_max;
+  p->row_bytes = row_bytes;
+  p->staging = staging_rows;
+  p->rows_per_pool = (int64_t)cap_max + staging_rows;
+  cudaGetDevice(&p->device);
+  cudaError_t e = cudaSuccess;
+  e = cudaMalloc(&p->meta, sizeof(PoolMeta) * num_pools);
+  if (e == cudaSuccess) e = cudaMalloc(&p->slot_of, sizeof(int32_t) * num_pools * max_ids);
+  if (e == cudaSuccess) e = cudaMalloc(&p->slot_id, sizeof(int32_t) * num_pools * (int64_t)cap_max);
+  if (e == cudaSuccess) e = cudaMalloc(&p->key, sizeof(uint32_t) * num_pools * (int64_t)cap_max);
+  if (e == cudaSuccess) e = cudaMalloc(&p->status, sizeof(int32_t));
+  if (e == cudaSuccess && row_bytes)
+    e = cudaMalloc(&p->rows, (size_t)num_pools * p->rows_per_pool * row_bytes);
+  if (e == cudaSuccess) e = cudaMemset(p->status, 0, sizeof(int32_t));
+  if (e == cudaSuccess && row_bytes)
+    e = cudaMemset(p->rows, 0, (size_t)num_pools * p->rows_per_pool * row_bytes);
+  if (e != cudaSuccess) {
+    ess_pool_destroy(p);
+    cudaGetLastError();
+    return e == cudaErrorMemoryAllocation ? ESS_ERR_NOMEM : ess_record_cuda_error(e);
+  }
+  // initial state: every pool empty at capacity cap_max
+  int32_t *caps = nullptr;
+  e = cudaMalloc(&caps, sizeof(int32_t) * num_pools);
+  if (e == cudaSuccess) {
+    int32_t *h = (int32_t *)malloc(sizeof(int32_t) * num_pools);
+    for (int i = 0; i < num_pools; i++) h[i] = cap_max;
+    cudaMemcpy(caps, h, sizeof(int32_t) * num_pools, cudaMemcpyHostToDevice);
+    free(h);
+    int rc = ess_pool_reset(p, 0, num_pools, caps, nullptr);
+    cudaDeviceSynchronize();
+    cudaFree(caps);
+    if (rc) {
+      ess_pool_destroy(p);
+      return rc;
+    }
+  }
+  *out = p;
+  return ESS_OK;
+}
+
+int ess_pool_destroy(ess_pool *p) {
+  if (!p) return ESS_ERR_ARG;
+  cudaFree(p->meta);
+  cudaFree(p->slot_of);
+  cudaFree(p->slot_id);
+  cudaFree(p->key);
+  cudaFree(p->rows);
+  cudaFree(p->status);
+  free(p);
+  return ESS_OK;
+}
+
+int ess_pool_reset(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_capacity,
+                   void *stream) {
+  if (!range_ok(p, begin, num) || !d_capacity) return ESS_ERR_ARG;
+  if (num == 0) return ESS_OK;
+  int64_t per = p->max_ids > p->cap_max ? p->max_ids : p->cap_max;
+  int gy = (int)((per + 256 * 8 - 1) / (256 * 8));
+  if (gy > 64) gy = 64;
+  dim3 grid(num, gy);
+  pool_reset_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(view(p), begin, num, d_capacity);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+int ess_pool_grow(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_capacity,
+                  void *stream) {
+  if (!range_ok(p, begin, num) || !d_capacity) return ESS_ERR_ARG;
+  if (num == 0) return ESS_OK;
+  pool_grow_kernel<<<(num + 255) / 256, 256, 0, (cudaStream_t)stream>>>(view(p), begin, num,
+                                                                         d_capacity);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+int ess_pool_warmup(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_ids,
+                    const int32_t *d_n, int32_t stride, int64_t *d_inserted, void *stream) {
+  if (!range_ok(p, begin, num) || !d_ids || !d_n || stride < 0) return ESS_ERR_ARG;
+  if (num == 0) return ESS_OK;
+  pool_step_kernel<MODE_WARMUP><<<num, NT, 0, (cudaStream_t)stream>>>(
+      view(p), begin, d_ids, d_n, stride, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+      0, 0, d_inserted);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+int ess_pool_access(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_req,
+                    const int32_t *d_n, int32_t req_stride, int32_t *d_hit_ids,
+                    int32_t *d_miss_ids, int32_t *d_evicted_ids, int32_t *d_sel_row,
+                    int32_t *d_miss_row, int32_t *d_counts, int32_t out_stride, int32_t flags,
+                    void *stream) {
+  if (!range_ok(p, begin, num) || !d_req || !d_n || req_stride < 0) return ESS_ERR_ARG;
+  if ((d_hit_ids || d_miss_ids || d_evicted_ids || d_sel_row || d_miss_row) &&
+      out_stride < 1)
+    return ESS_ERR_ARG;
+  if (num == 0) return ESS_OK;
+  pool_step_kernel<MODE_ACCESS><<<num, NT, 0, (cudaStream_t)stream>>>(
+      view(p), begin, d_req, d_n, req_stride, d_hit_ids, d_miss_ids, d_evicted_ids, d_sel_row,
+      d_miss_row, d_counts, out_stride, flags, nullptr);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+int ess_pool_append(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_ids,
+                    const int32_t *d_m, int32_t stride, int32_t *d_slot_out, void *stream) {
+  if (!range_ok(p, begin, num) || !d_ids || !d_m || stride < 0) return ESS_ERR_ARG;
+  if (num == 0) return ESS_OK;
+  pool_append_kernel<<<num, NTA, 0, (cudaStream_t)stream>>>(view(p), begin, d_ids, d_m, stride,
+                                                            d_slot_out);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+int ess_pool_lru_order(ess_pool *p, int32_t begin, int32_t num, int32_t *d_out,
+                       int32_t *d_count, void *stream) {
+  if (!range_ok(p, begin, num) || !d_out || !d_count) return ESS_ERR_ARG;
+  if (num == 0) return ESS_OK;
+  dim3 grid(num, (p->cap_max + 255) / 256);
+  pool_lru_order_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(view(p), begin, d_out, d_count);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+int ess_pool_counters(ess_pool *p, int32_t begin, int32_t num, int64_t *d_out, void *stream) {
+  if (!range_ok(p, begin, num) || !d_out) return ESS_ERR_ARG;
+  if (num == 0) return ESS_OK;
+  pool_counters_kernel<<<(num + 127) / 128, 128, 0, (cudaStream_t)stream>>>(view(p), begin, num,
+                                                                            d_out);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+int ess_pool_status(ess_pool *p, int32_t *status_out) {
+  if (!p || !status_out) return ESS_ERR_ARG;
+  int32_t h = 0;
+  ESS_CUDA_TRY(cudaMemcpy(&h, p->status, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  ESS_CUDA_TRY(cudaMemset(p->status, 0, sizeof(int32_t)));
+  *status_out = h;
+  return ESS_OK;
+}
+
+int ess_pool_info(ess_pool *p, int32_t *num_pools, int64_t *max_ids, int32_t *cap_max,
+                  int32_t *row_bytes, int64_t *rows_per_pool, void **d_rows) {
+  if (!p) return ESS_ERR_ARG;
+  if (num_pools) *num_pools = p->P;
+  if (max_ids) *max_ids = p->max_ids;
+  if (cap_max) *cap_max = p->cap_max;
+  if (row_bytes) *row_bytes = p->row_bytes;
+  if (rows_per_pool) *rows_per_pool = p->rows_per_pool;
+  if (d_rows) *d_rows = p->rows;
+  return ESS_OK;
+}
+
+int ess_pool_lookup(ess_pool *p, int32_t pool, const int32_t *d_ids, int32_t n,
+                    int32_t *d_slot_out, void *stream) {
+  if (!p || pool < 0 || pool >= p->P || n < 0 || (n && (!d_ids || !d_slot_out))) return ESS_ERR_ARG;
+  if (n == 0) return ESS_OK;
+  pool_lookup_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(view(p), pool, d_ids, n,
+                                                                        d_slot_out);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+int ess_pool_copy_state(ess_pool *dst, int32_t dst_begin, ess_pool *src, int32_t src_begin,
+                        int32_t num, void *stream) {
+  if (!range_ok(dst, dst_begin, num) || !range_ok(src, src_begin, num) ||
+      dst->max_ids < src->max_ids || dst->cap_max < src->cap_max ||
+      dst->row_bytes != src->row_bytes)
+    return ESS_ERR_ARG;
+  if (num == 0) return ESS_OK;
+  dim3 grid(num, 32);
+  pool_copy_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(view(dst), dst_begin, view(src), src_begin);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+int ess_gather(ess_pool *p, int32_t begin, int32_t num, const void *d_host_rows,
+               int64_t host_pool_stride_rows, const int32_t *d_miss_ids,
+               const int32_t *d_miss_row, const int32_t *d_counts, int32_t stride,
+               int32_t max_ctas, void *stream) {
+  if (!range_ok(p, begin, num) || !p->rows || !d_host_rows || !d_miss_ids || !d_miss_row ||
+      !d_counts || stride < 1 || max_ctas < 1)
+    return ESS_ERR_ARG;
+  if (num == 0) return ESS_OK;
+  size_t smem = sizeof(int) * (num + 1);
+  if (smem > 48 * 1024) {
+    ESS_CUDA_TRY(cudaFuncSetAttribute(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+  }
+  gather_kernel<<<max_ctas, NTG, smem, (cudaStream_t)stream>>>(
+      view(p), begin, num, (const uint8_t *)d_host_rows, host_pool_stride_rows, d_miss_ids,
+      d_miss_row, d_counts, stride);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+int ess_write_generated(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_ids,
+                        const int32_t *d_m, const int32_t *d_slot, int32_t stride,
+                        const void *d_src_rows, void *d_host_rows,
+                        int64_t host_pool_stride_rows, void *stream) {
+  if (!range_ok(p, begin, num) || !p->rows || !d_ids || !d_m || !d_src_rows || stride < 1)
+    return ESS_ERR_ARG;
+  if (num == 0) return ESS_OK;
+  write_generated_kernel<<<num, 128, 0, (cudaStream_t)stream>>>(
+      view(p), begin, d_ids, d_m, d_slot, stride, (const uint8_t *)d_src_rows,
+      (uint8_t *)d_host_rows, host_pool_stride_rows);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,56 @@
+"""Lightning indexer (K1) and top-k selection (K2) — the two operators the
+reference reduces to the cost entries ``indexer_logits`` / ``indexer_topk``
+(/root/reference/pkg/src/offsim/costmodel.py:18-27, used at pipeline.py:215-216).
+
+K2's output is the canonical selection set of ``AccessTrace`` (trace.py:31-46):
+ascending unique ids, |set| = min(k, len) (scenario.py:110-112).
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _lib
+
+HEADS = 64
+DIM = 128
+TOPK = 2048
+
+
+def indexer_logits(q_fp8: torch.Tensor, w: torch.Tensor, k_cache: torch.Tensor,
+                   k_scale: torch.Tensor, lens: torch.Tensor,
+                   out: torch.Tensor | None = None) -> torch.Tensor:
+    """logits[b, s] = k_scale[b, s] * sum_h w[b, h] * relu(q[b, h] . k[b, s]) for s < lens[b].
+
+    q_fp8 [B, 64, 128] and k_cache [B, Lmax, 128] hold e4m3 bytes (uint8 or
+    float8_e4m3fn), w [B, 64] f32, k_scale [B, Lmax] f32, lens [B] int32.
+    Lmax must be a multiple of 128 and k_cache 16-byte aligned (TMA).
+    Entries at s >= lens[b] are left untouched.
+    """
+    _lib.require_cuda(k_cache)
+    B, Lmax, D = k_cache.shape
+    if D != DIM or q_fp8.shape != (B, HEADS, DIM) or w.shape != (B, HEADS):
+        raise ValueError("expected q [B,64,128], w [B,64], k [B,Lmax,128]")
+    if out is None:
+        out = torch.empty((B, Lmax), dtype=torch.float32, device=k_cache.device)
+    _lib.check(_lib.load().ess_indexer_logits(
+        q_fp8.data_ptr(), w.data_ptr(), k_cache.data_ptr(), k_scale.data_ptr(), lens.data_ptr(),
+        B, Lmax, out.data_ptr(), _lib.stream_handle()), "ess_indexer_logits")
+    return out
+
+
+def topk(logits: torch.Tensor, lens: torch.Tensor, k: int = TOPK,
+         out: torch.Tensor | None = None, count: torch.Tensor | None = None):
+    """Top-k of each row logits[b, :lens[b]] by (score desc, index asc), ascending ids.
+
+    Returns (idx [B, k] int32, count [B] int32) with count = min(k, lens)."""
+    _lib.require_cuda(logits)
+    B, ld = logits.shape
+    if out is None:
+        out = torch.empty((B, k), dtype=torch.int32, device=logits.device)
+    if count is None:
+        count = torch.empty(B, dtype=torch.int32, device=logits.device)
+    _lib.check(_lib.load().ess_topk(logits.data_ptr(), logits.stride(0), lens.data_ptr(), B, k,
+                                    out.data_ptr(), out.stride(0), count.data_ptr(),
+                                    _lib.stream_handle()), "ess_topk")
+    return out, count

@@ -1,0 +1,121 @@
+"""Host latent store and the zero-copy miss gather (K4).
+
+* ``TransferModel`` / ``transfer_time`` restate the reference's PCIe yardstick
+  (/root/reference/pkg/src/offsim/costmodel.py:128-186): batched FlashTrans
+  37/43 GB/s and per-call cudaMemcpyAsync 0.79/0.23 GB/s at 656-B blocks
+  (PAPER.md:273, :279).  The bench reports measured gather GB/s against these.
+* ``HostLatentStore`` — the CPU-side "total memory pool": pinned,
+  mapped (cudaHostRegister) so the gather kernel reads rows with 16-B loads.
+* ``gather`` / ``write_generated`` — the H2D miss fill and the D2H write-back of
+  newly generated rows (cache.py:122-134).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from .cache import AccessBatch, PoolSet
+
+LATENT_BLOCK_BYTES = 656
+PER_CALL_EFFECTIVE_H2D_GBS = 0.79
+PER_CALL_EFFECTIVE_D2H_GBS = 0.23
+
+
+def fit_per_call_overhead_us(block_bytes: float, bw_link_gbs: float, bw_effective_gbs: float) -> float:
+    """Per-copy overhead making a ``bw_link_gbs`` link deliver ``bw_effective_gbs``."""
+    return block_bytes * (1.0 / bw_effective_gbs - 1.0 / bw_link_gbs) / 1e3
+
+
+@dataclass(frozen=True)
+class TransferModel:
+    mode: str = "batched"
+    bw_h2d_gbs: float = 37.0
+    bw_d2h_gbs: float = 43.0
+    block_bytes: int = LATENT_BLOCK_BYTES
+    per_call_overhead_h2d_us: float | None = None
+    per_call_overhead_d2h_us: float | None = None
+
+    def __post_init__(self):
+        if self.mode not in ("per_call", "batched"):
+            raise ValueError(f"unknown transfer mode {self.mode!r}")
+        if min(self.bw_h2d_gbs, self.bw_d2h_gbs) <= 0:
+            raise ValueError("bandwidths must be > 0")
+        for attr, bw, eff in (("per_call_overhead_h2d_us", self.bw_h2d_gbs, PER_CALL_EFFECTIVE_H2D_GBS),
+                              ("per_call_overhead_d2h_us", self.bw_d2h_gbs, PER_CALL_EFFECTIVE_D2H_GBS)):
+            if getattr(self, attr) is None:
+                object.__setattr__(self, attr, fit_per_call_overhead_us(self.block_bytes, bw, eff))
+        if min(self.per_call_overhead_h2d_us, self.per_call_overhead_d2h_us) < 0:
+            raise ValueError("per-call overheads must be >= 0")
+
+
+def transfer_time(model: TransferModel, blocks: int, direction: str) -> float:
+    """Microseconds to move ``blocks`` latent rows one way (costmodel.py:173-186)."""
+    if blocks < 0:
+        raise ValueError("blocks must be >= 0")
+    if direction not in ("h2d", "d2h"):
+        raise ValueError(f"direction must be h2d or d2h, got {direction!r}")
+    h2d = direction == "h2d"
+    us = blocks * model.block_bytes / ((model.bw_h2d_gbs if h2d else model.bw_d2h_gbs) * 1e3)
+    if model.mode == "per_call":
+        us += blocks * (model.per_call_overhead_h2d_us if h2d else model.per_call_overhead_d2h_us)
+    return us
+
+
+class HostLatentStore:
+    """[pools, rows_per_pool, 656] bytes of page-locked, device-mapped host memory."""
+
+    def __init__(self, num_pools: int, rows_per_pool: int, row_bytes: int = LATENT_BLOCK_BYTES):
+        _lib.require_cuda()
+        self.num_pools, self.rows_per_pool, self.row_bytes = num_pools, rows_per_pool, row_bytes
+        self.host = torch.empty((num_pools, rows_per_pool, row_bytes), dtype=torch.uint8)
+        alias = ctypes.c_void_p()
+        _lib.check(_lib.load().ess_host_register(self.host.data_ptr(), self.host.numel(),
+                                                 ctypes.byref(alias)), "ess_host_register")
+        self.device_ptr = alias.value
+        self._registered = True
+
+    @property
+    def nbytes(self) -> int:
+        return self.host.numel()
+
+    def pool_ptr(self, begin: int) -> int:
+        return self.device_ptr + begin * self.rows_per_pool * self.row_bytes
+
+    def close(self):
+        if getattr(self, "_registered", False):
+            torch.cuda.synchronize()
+            _lib.load().ess_host_unregister(self.host.data_ptr())
+            self._registered = False
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gather(pool: PoolSet, store: HostLatentStore, acc: AccessBatch, begin: int = 0,
+           store_begin: int | None = None, max_ctas: int = 32, stream=None) -> None:
+    """Copy every miss row host[pool][miss_id] -> slot store[pool][miss_row] (K4)."""
+    num = acc.counts.shape[0]
+    sb = begin if store_begin is None else store_begin
+    _lib.check(_lib.load().ess_gather(
+        pool.handle, begin, num, store.pool_ptr(sb), store.rows_per_pool,
+        acc.miss_ids.data_ptr(), acc.miss_row.data_ptr(), acc.counts.data_ptr(),
+        acc.miss_ids.stride(0), max_ctas, _lib.stream_handle(stream)), "ess_gather")
+
+
+def write_generated(pool: PoolSet, store: HostLatentStore, ids: torch.Tensor, m: torch.Tensor,
+                    slots: torch.Tensor, rows: torch.Tensor, begin: int = 0,
+                    store_begin: int | None = None, stream=None) -> None:
+    """New rows [num, M, 656] -> host store (D2H) and their pool slots."""
+    num = ids.shape[0]
+    sb = begin if store_begin is None else store_begin
+    _lib.check(_lib.load().ess_write_generated(
+        pool.handle, begin, num, ids.data_ptr(), m.data_ptr(), slots.data_ptr(), ids.stride(0),
+        rows.data_ptr(), store.pool_ptr(sb), store.rows_per_pool, _lib.stream_handle(stream)),
+        "ess_write_generated")

@@ -1,0 +1,56 @@
+"""End-to-end parity of one offloaded DSA decode layer (K1 -> K5 + append) against
+the CPU oracle chain: oracle top-k on the GPU's logits, the C LRU oracle driven
+with the same selections, and fp64 attention over the HOST store's rows of the
+selected ids (so the gather is checked too)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import dsa
+from oracle import lru as olru
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("ctx,rho", [(8192, 0.25), (4096, 0.25)])
+def test_decode_layer_matches_oracle_chain(ctx, rho):
+    from paper_2512_10576_b200.cache import pool_capacity
+    from paper_2512_10576_b200.decode import DSADecodeLayer
+    B, K = 3, 2048
+    layer = DSADecodeLayer(B, ctx, rho, K, max_new_tokens=8, seed=1, drift=0.97)
+    windows = layer.prefill_warmup(windows=8, record=True)
+    orc = [olru.OraclePool(pool_capacity(rho, ctx)) for _ in range(B)]
+    for w in windows:
+        for b in range(B):
+            orc[b].warmup([w[b].tolist()])
+    hist = ctx
+    for step in range(4):
+        q_idx, q = layer.next_queries()
+        out, lse = layer.attend(q_idx, q)
+        torch.cuda.synchronize()
+        logits = layer.logits.cpu().numpy()
+        idx, cnt = layer.idx.cpu().numpy(), layer.cnt.cpu().numpy()
+        counts = layer.acc.counts.cpu().numpy()
+        host = layer.store.host.numpy()
+        o_all, l_all = out.float().cpu().numpy(), lse.cpu().numpy()
+        qf = q.float().cpu().numpy()
+        for b in range(B):
+            n = hist
+            want = dsa.topk_indices(logits[b], n, K)
+            np.testing.assert_array_equal(idx[b, :cnt[b]], want)
+            r = orc[b].access_step(want.tolist())
+            assert counts[b, 0] == len(r.hit_ids) and counts[b, 1] == len(r.miss_ids)
+            ref_o, ref_l = dsa.sparse_mla(qf[b], host[b, want], layer.sm_scale)
+            rel = np.linalg.norm(o_all[b] - ref_o) / np.linalg.norm(ref_o)
+            assert rel <= 1e-2, (step, b, rel)
+            assert np.abs(l_all[b] - ref_l).max() <= 1e-2
+        layer.append_token()
+        hist += 1
+        for o in orc:
+            o.grow_capacity(pool_capacity(rho, hist))
+            o.append_generated([hist - 1])
+    layer.pool.check()
+    out, cnt = layer.pool.lru_order()
+    for b in range(B):
+        assert out[b, :int(cnt[b])].tolist() == orc[b].lru_order()
+    layer.close()

@@ -1,0 +1,192 @@
+"""K1 / K2 / K4 / K5 parity on the GPU against the CPU oracle (oracle/dsa.py).
+
+Tolerances (stated per north star):
+  * top-k: bit-exact given the same logits (tie rule score desc, index asc)
+  * indexer: bit-exact in the exact-arithmetic regime (small-integer e4m3 q/k,
+    power-of-two w and scales: every product and partial sum is exact in fp32);
+    otherwise |err| <= 1e-3 * max|logit| + 1e-5
+  * gather / write-back: byte-exact
+  * sparse MLA: rel-L2 <= 1e-2 and max-abs <= 2e-2 * max|ref| against the fp64
+    reference on the same dequantised rows; lse abs <= 1e-2
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import dsa
+
+pytestmark = pytest.mark.gpu
+
+
+def e4m3(x):
+    return x.clamp(-448, 448).to(torch.float8_e4m3fn).view(torch.uint8)
+
+
+# ---------------------------------------------------------------------------- K2
+@pytest.mark.parametrize("lens", [[32768, 4096, 2049, 2048, 100, 0, 131072, 5001],
+                                  [32768] * 16])
+def test_topk_matches_oracle(lens):
+    from paper_2512_10576_b200.indexer import topk
+    g = torch.Generator(device="cuda").manual_seed(7)
+    B, ld = len(lens), max(lens) + 3  # odd stride exercises the scalar path
+    logits = torch.randn((B, ld), device="cuda", generator=g)
+    logits[1::2] = torch.relu(torch.round(logits[1::2] * 3))  # heavy exact ties (ReLU zeros)
+    logits[0, 5] = -0.0
+    L = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    idx, cnt = topk(logits, L, 2048)
+    idx, cnt, host = idx.cpu().numpy(), cnt.cpu().numpy(), logits.cpu().numpy()
+    for b, n in enumerate(lens):
+        want = dsa.topk_indices(host[b], n, 2048)
+        assert cnt[b] == len(want)
+        np.testing.assert_array_equal(idx[b, :cnt[b]], want)
+
+
+def test_topk_all_equal_row():
+    from paper_2512_10576_b200.indexer import topk
+    logits = torch.zeros((2, 40000), device="cuda")
+    L = torch.tensor([40000, 39999], dtype=torch.int32, device="cuda")
+    idx, cnt = topk(logits, L, 2048)
+    assert (idx.cpu().numpy() == np.arange(2048)).all()
+
+
+# ---------------------------------------------------------------------------- K1
+def _indexer_inputs(B, Lmax, exact, seed=0):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    if exact:
+        q = torch.randint(-4, 5, (B, 64, 128), device="cuda", generator=g).float()
+        k = torch.randint(-4, 5, (B, Lmax, 128), device="cuda", generator=g).float()
+        w = 2.0 ** torch.randint(-6, 0, (B, 64), device="cuda", generator=g).float()
+        w = w * (torch.randint(0, 2, (B, 64), device="cuda", generator=g) * 2 - 1)
+        ks = 2.0 ** torch.randint(-4, 2, (B, Lmax), device="cuda", generator=g).float()
+    else:
+        q = torch.randn((B, 64, 128), device="cuda", generator=g) * 2
+        k = torch.randn((B, Lmax, 128), device="cuda", generator=g) * 2
+        w = torch.randn((B, 64), device="cuda", generator=g) / 8
+        ks = torch.rand((B, Lmax), device="cuda", generator=g) + 0.5
+    return e4m3(q), w.contiguous(), e4m3(k), ks.contiguous()
+
+
+@pytest.mark.parametrize("exact", [True, False])
+def test_indexer_matches_oracle(exact):
+    from paper_2512_10576_b200.indexer import indexer_logits
+    lens = [4096, 130, 1, 0, 4000, 2048]
+    B, Lmax = len(lens), 4096
+    q, w, k, ks = _indexer_inputs(B, Lmax, exact)
+    L = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    out = torch.full((B, Lmax), 12345.0, device="cuda")
+    indexer_logits(q, w, k, ks, L, out=out)
+    got = out.cpu().numpy()
+    qn, wn, kn, ksn = (t.cpu().numpy() for t in (q, w, k, ks))
+    for b, n in enumerate(lens):
+        want = dsa.indexer_logits(qn[b], wn[b], kn[b], ksn[b], n)
+        if exact:
+            np.testing.assert_array_equal(got[b, :n], want)
+        else:
+            tol = 1e-3 * max(1e-6, float(np.abs(want).max(initial=0))) + 1e-5
+            assert np.abs(got[b, :n] - want).max(initial=0) <= tol
+        assert (got[b, n:] == 12345.0).all()  # nothing written past len
+
+
+def test_indexer_then_topk_exact_regime_end_to_end():
+    from paper_2512_10576_b200.indexer import indexer_logits, topk
+    B, Lmax = 4, 32768
+    q, w, k, ks = _indexer_inputs(B, Lmax, True, seed=3)
+    L = torch.tensor([32768, 32000, 20000, 2500], dtype=torch.int32, device="cuda")
+    logits = indexer_logits(q, w, k, ks, L)
+    idx, cnt = topk(logits, L, 2048)
+    qn, wn, kn, ksn = (t.cpu().numpy() for t in (q, w, k, ks))
+    for b in range(B):
+        n = int(L[b])
+        want = dsa.topk_indices(dsa.indexer_logits(qn[b], wn[b], kn[b], ksn[b], n), n, 2048)
+        np.testing.assert_array_equal(idx[b].cpu().numpy()[:cnt[b]], want)
+
+
+# ---------------------------------------------------------------------------- K4
+def test_gather_and_write_back_are_byte_exact():
+    from paper_2512_10576_b200.cache import PoolSet
+    from paper_2512_10576_b200.decode import random_latent_rows
+    from paper_2512_10576_b200.transfer import HostLatentStore, gather, write_generated
+    P, ids, cap = 3, 5000, 1200
+    store = HostLatentStore(P, ids)
+    for p in range(P):
+        store.host[p].copy_(random_latent_rows(ids, "cuda"))
+    pools = PoolSet(P, ids, cap, cap, row_bytes=656, staging_rows=0)
+    rng = np.random.default_rng(0)
+    sets = np.stack([rng.choice(4000, size=1000, replace=False) for _ in range(P)]).astype(np.int32)
+    acc = pools.access(torch.as_tensor(sets, device="cuda"),
+                       torch.full((P,), 1000, dtype=torch.int32, device="cuda"))
+    gather(pools, store, acc)
+    rows = pools.rows_view().cpu().numpy()
+    sel = acc.sel_row.cpu().numpy()
+    host = store.host.numpy()
+    for p in range(P):
+        np.testing.assert_array_equal(rows[p, sel[p]], host[p, sets[p]])
+    # write-back of generated rows (append) lands in host store and slot
+    new = torch.full((P, 1), 4500, dtype=torch.int32, device="cuda")
+    one = torch.ones(P, dtype=torch.int32, device="cuda")
+    slots = pools.append(new, one)
+    src = random_latent_rows(P, "cuda").view(P, 1, 656)
+    write_generated(pools, store, new, one, slots, src)
+    torch.cuda.synchronize()
+    rows = pools.rows_view().cpu().numpy()
+    s = slots.cpu().numpy()[:, 0]
+    for p in range(P):
+        np.testing.assert_array_equal(store.host.numpy()[p, 4500], src[p, 0].cpu().numpy())
+        np.testing.assert_array_equal(rows[p, s[p]], src[p, 0].cpu().numpy())
+    pools.check()
+    store.close()
+
+
+# ---------------------------------------------------------------------------- K5
+@pytest.mark.parametrize("counts", [[2048, 1000, 17, 1], [2048] * 3])
+def test_sparse_mla_matches_oracle(counts):
+    from paper_2512_10576_b200.attention import sparse_mla, DEFAULT_SM_SCALE
+    from paper_2512_10576_b200.cache import PoolSet
+    from paper_2512_10576_b200.decode import random_latent_rows
+    B, cap = len(counts), 4096
+    pools = PoolSet(B, 8192, cap, cap, row_bytes=656)
+    rv = pools.rows_view()
+    g = torch.Generator(device="cuda").manual_seed(11)
+    for b in range(B):
+        rv[b, :cap].copy_(random_latent_rows(cap, "cuda", g))
+    sel = torch.stack([torch.randperm(cap, device="cuda", generator=g)[:2048] for _ in range(B)]).int()
+    cnt = torch.tensor(counts, dtype=torch.int32, device="cuda")
+    q = (torch.randn((B, 128, 576), device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    out, lse = sparse_mla(pools, q, sel, cnt)
+    out, lse = out.float().cpu().numpy(), lse.cpu().numpy()
+    rows = rv.cpu().numpy()
+    qf = q.float().cpu().numpy()
+    for b, n in enumerate(counts):
+        ref_o, ref_l = dsa.sparse_mla(qf[b], rows[b, sel[b, :n].cpu().numpy()], DEFAULT_SM_SCALE)
+        err = out[b] - ref_o
+        rel = np.linalg.norm(err) / max(np.linalg.norm(ref_o), 1e-12)
+        assert rel <= 1e-2, (b, n, rel)
+        assert np.abs(err).max() <= 2e-2 * max(np.abs(ref_o).max(), 1e-6), (b, n)
+        assert np.abs(lse[b] - ref_l).max() <= 1e-2, (b, n)
+
+
+def test_sparse_mla_rescale_path():
+    """Scores that grow tile by tile force the lazy O rescale (> 2^8 jumps)."""
+    from paper_2512_10576_b200.attention import sparse_mla
+    from paper_2512_10576_b200.cache import PoolSet
+    from paper_2512_10576_b200.decode import random_latent_rows
+    B, n = 2, 2048
+    pools = PoolSet(B, 4096, n, n, row_bytes=656)
+    rv = pools.rows_view()
+    g = torch.Generator(device="cuda").manual_seed(2)
+    for b in range(B):
+        rows = random_latent_rows(n, "cuda", g)
+        # scale rows so later tiles have larger norms -> larger scores
+        sc = rows[:, 512:528].clone().view(torch.float32) * torch.linspace(0.2, 3.0, n, device="cuda")[:, None]
+        rows[:, 512:528] = sc.view(torch.uint8)
+        rv[b, :n].copy_(rows)
+    sel = torch.arange(n, dtype=torch.int32, device="cuda").repeat(B, 1).contiguous()
+    cnt = torch.full((B,), n, dtype=torch.int32, device="cuda")
+    q = (torch.randn((B, 128, 576), device="cuda", generator=g) * 2).to(torch.bfloat16)
+    out, lse = sparse_mla(pools, q, sel, cnt, sm_scale=0.2)
+    rows = rv.cpu().numpy()
+    for b in range(B):
+        ref_o, ref_l = dsa.sparse_mla(q[b].float().cpu().numpy(), rows[b, :n], 0.2)
+        o = out[b].float().cpu().numpy()
+        assert np.linalg.norm(o - ref_o) / np.linalg.norm(ref_o) <= 1e-2
+        assert np.abs(lse[b].cpu().numpy() - ref_l).max() <= 1e-2
