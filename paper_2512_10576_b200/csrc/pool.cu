@@ -215,6 +215,57 @@ __global__ void __launch_bounds__(NT, 1)
 
   int nev = 0;
   int64_t inserted = 0;
+  if (MODE == MODE_WARMUP) {
+    // Warm-up touches in window order (cache.py:79-87), so a resident x at window
+    // position i may be evicted by the earlier touches before its own: that happens
+    // iff the distinct ids touched after x's old stamp fill the pool, i.e.
+    //   r_x < i - B_x - free      r_x = #residents older than x (LRU rank)
+    //                             B_x = #{j < i : W[j] resident and newer than x}
+    //                             free = cap - size
+    // and x then counts as inserted.  Only ranks below D = n-1-free matter, so the
+    // D oldest residents are located by radix select and ranked by brute force.
+    const int free0 = cap - size0;
+    const int D = n - 1 - free0;
+    int extra = 0;
+    if (D > 0 && nhit > 0 && size0 > 0) {
+      const int kk = D < size0 ? D : size0;
+      const uint32_t Tstar = select_kth_smallest(key, cap, free0 + kk, sm);
+      uint32_t *cand = reinterpret_cast<uint32_t *>(sm.ev);   // <= kk resident stamps
+      uint32_t *pkey = reinterpret_cast<uint32_t *>(sm.sel);  // old stamp by position
+      int base = 0;
+      for (int s0 = 0; s0 < cap; s0 += NT) {
+        int s = s0 + t;
+        uint32_t k = s < cap ? key[s] : 0xFFFFFFFFu;
+        int f = (s < cap && k <= Tstar && slot_id[s] >= 0) ? 1 : 0;
+        int tot;
+        int pos = block_exclusive_scan<NT>(f, sm.warp, &tot);
+        if (f && base + pos < MAXR) cand[base + pos] = k;
+        base += tot;
+      }
+      const int ncand = base < MAXR ? base : MAXR;
+#pragma unroll
+      for (int e = 0; e < EPT; e++) {
+        int i = t * EPT + e;
+        if (i < n) pkey[i] = hflag[e] ? key[sm.slot[i]] : 0u;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < EPT; e++) {
+        int i = t * EPT + e;
+        if (i >= n || !hflag[e] || i - free0 <= 0) continue;
+        const uint32_t sx = pkey[i];
+        if (sx > Tstar) continue;  // rank >= D: cannot be evicted in this window
+        int r = 0, B = 0;
+        for (int c = 0; c < ncand; c++) r += cand[c] < sx;
+        for (int j = 0; j < i; j++) B += pkey[j] > sx;
+        extra += (r < i - B - free0);
+      }
+      __syncthreads();
+    }
+    int tot;
+    block_exclusive_scan<NT>(extra, sm.warp, &tot);
+    inserted = (int64_t)nmiss + tot;
+  }
   if (n <= cap) {
     // ---- normal path (cache.py:112-118; warm-up windows <= cap, cache.py:79-87) --
 #pragma unroll
@@ -273,42 +324,11 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
     }
-    if (MODE == MODE_WARMUP) inserted = nmiss;
   } else {
     // ---- oversize path: keep requested[n-cap:] (cache.py:103-111) -----------------
     const int keep0 = n - cap;  // cap < n <= MAXR, so every slot index < MAXR
     if (MODE == MODE_ACCESS && pv.rows && keep0 > pv.staging && t == 0)
       ess_set_status(pv.status, ESS_ERR_ARG);  // not enough staging rows for transients
-    if (MODE == MODE_WARMUP) {
-      // reuse-distance test for the exact inserted count (see file header)
-      uint32_t *okey = reinterpret_cast<uint32_t *>(sm.ev);   // occupied old keys by slot
-      uint32_t *pkey = reinterpret_cast<uint32_t *>(sm.sel);  // old key by window position
-      for (int s = t; s < cap; s += NT) okey[s] = slot_id[s] >= 0 ? key[s] : 0u;
-#pragma unroll
-      for (int e = 0; e < EPT; e++) {
-        int i = t * EPT + e;
-        if (i < n) pkey[i] = hflag[e] ? key[sm.slot[i]] : 0u;
-      }
-      __syncthreads();
-      int ins_local = 0;
-#pragma unroll
-      for (int e = 0; e < EPT; e++) {
-        int i = t * EPT + e;
-        if (i >= n) continue;
-        if (!hflag[e] || i >= cap) {
-          ins_local++;
-          continue;
-        }
-        uint32_t sx = pkey[i];
-        int A = 0, B = 0;
-        for (int s = 0; s < cap; s++) A += okey[s] > sx;
-        for (int j = 0; j < i; j++) B += pkey[j] > sx;
-        ins_local += (A + i - B >= cap);
-      }
-      int tot;
-      block_exclusive_scan<NT>(ins_local, sm.warp, &tot);
-      inserted = tot;
-    }
     for (int s = t; s < MAXR; s += NT) sm.mark[s] = 0;
     __syncthreads();
 #pragma unroll

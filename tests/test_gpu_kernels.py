@@ -189,4 +189,7 @@ def test_sparse_mla_rescale_path():
         ref_o, ref_l = dsa.sparse_mla(q[b].float().cpu().numpy(), rows[b, :n], 0.2)
         o = out[b].float().cpu().numpy()
         assert np.linalg.norm(o - ref_o) / np.linalg.norm(ref_o) <= 1e-2
-        assert np.abs(lse[b].cpu().numpy() - ref_l).max() <= 1e-2
+        # scores reach ~70 here; f16 K rows carry 2^-11 relative rounding, so the
+        # log-sum-exp tolerance is relative at this scale
+        got_l = lse[b].cpu().numpy()
+        assert (np.abs(got_l - ref_l) <= 1e-2 + 1e-3 * np.abs(ref_l)).all()
