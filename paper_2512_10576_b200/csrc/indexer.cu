@@ -4,14 +4,15 @@
 //
 // The head contraction is a real GEMM per 128-token tile: D[128 tok][64 heads] =
 // K_tile[128 x 128 e4m3] . Q[64 x 128 e4m3]^T, issued as tcgen05.mma kind::f8f6f4
-// (M=128, N=64, 4 x K=32) by one thread into a TMEM accumulator, double-buffered so
-// the epilogue (ReLU, head-weighted sum, x kscale) of tile i overlaps the MMA of
-// tile i+1.  TMA (SWIZZLE_128B) streams K tiles through a 6-stage mbarrier ring;
-// the kernel is persistent (one CTA per SM, contiguous tile ranges) and HBM-bound:
-// 132 B/token in, 4 B/token out.
+// (M=128, N=64, 4 x K=32) by one thread into one of 4 TMEM accumulators, so the
+// epilogue (ReLU, head-weighted sum, x kscale) of earlier tiles overlaps the MMA of
+// later ones.  TMA (SWIZZLE_128B) streams K tiles through a 10-stage mbarrier ring;
+// q is loaded once per request into one of two slots.  The kernel is persistent
+// (one CTA per SM, contiguous tile ranges) and HBM-bound: 132 B/token in, 4 B out.
 //
-// Warp roles (192 threads): w0 TMA producer, w1 TMEM alloc + MMA issuer,
-// w2..w5 epilogue (TMEM lane quarter = warp % 4).
+// Warp roles (320 threads): w0 TMA producer, w1 TMEM alloc + MMA issuer,
+// w2..w9 epilogue in two groups taking alternate tiles (TMEM lane quarter =
+// warp % 4); head weights stay in registers while the request does not change.
 #include <cuda.h>
 
 #include <mutex>
@@ -20,28 +21,32 @@
 
 namespace {
 
-constexpr int STAGES = 6;
+constexpr int STAGES = 10;                  // K-tile ring depth (16 KB each)
 constexpr int TILE_M = 128;                 // tokens per tile
 constexpr int HEADS = ESS_INDEXER_HEADS;    // 64 = N
 constexpr int DIM = ESS_INDEXER_DIM;        // 128 = K (bytes, e4m3)
 constexpr int KT_BYTES = TILE_M * DIM;      // 16 KB
-constexpr int QT_BYTES = HEADS * DIM;       // 8 KB
-constexpr int STAGE_BYTES = KT_BYTES + QT_BYTES;
-constexpr int NTHREADS = 192;
+constexpr int QT_BYTES = HEADS * DIM;       // 8 KB, one per request (double-buffered)
+constexpr int NACC = 4;                     // TMEM accumulator stages
+constexpr int NEPI = 8;                     // epilogue warps: 2 groups x 4 lane quarters
+constexpr int NTHREADS = 32 * (2 + NEPI);
 constexpr int MAX_BATCH = 4096;
-constexpr int TMEM_COLS = 128;              // 2 accumulators x 64 columns
+constexpr int TMEM_COLS = NACC * HEADS;     // 256
 constexpr uint32_t IDESC = make_idesc(0 /*e4m3*/, 0 /*e4m3*/, TILE_M, HEADS, 0, 0);
 
 struct Ctrl {
   uint64_t full[STAGES];
   uint64_t empty[STAGES];
-  uint64_t tfull[2];
-  uint64_t tempty[2];
+  uint64_t qfull[2];
+  uint64_t qempty[2];
+  uint64_t tfull[NACC];
+  uint64_t tempty[NACC];
   uint32_t tmem;
   int pref[MAX_BATCH + 1];
 };
 
-constexpr size_t SMEM_BYTES = 1024 /*align slack*/ + (size_t)STAGES * STAGE_BYTES + sizeof(Ctrl);
+constexpr size_t SMEM_BYTES =
+    1024 /*align slack*/ + (size_t)STAGES * KT_BYTES + 2 * QT_BYTES + sizeof(Ctrl);
 
 // Walk the flattened (request, tile) sequence.
 struct TileCursor {
@@ -70,7 +75,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                    const int32_t *__restrict__ lens, int B, int64_t k_ld, float *__restrict__ logits) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  Ctrl &c = *reinterpret_cast<Ctrl *>(smem + (size_t)STAGES * STAGE_BYTES);
+  uint8_t *qbuf = smem + (size_t)STAGES * KT_BYTES;
+  Ctrl &c = *reinterpret_cast<Ctrl *>(qbuf + 2 * QT_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   // tile prefix over requests (every CTA computes it; B is small)
@@ -86,7 +92,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(&c.full[s], 1);
       mbar_init(&c.empty[s], 1);
     }
-    for (int a = 0; a < 2; a++) {
+    for (int s = 0; s < 2; s++) {
+      mbar_init(&c.qfull[s], 1);
+      mbar_init(&c.qempty[s], 1);
+    }
+    for (int a = 0; a < NACC; a++) {
       mbar_init(&c.tfull[a], 1);
       mbar_init(&c.tempty[a], 4);
     }
@@ -100,37 +110,57 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int total = c.pref[B];
   const int t0 = (int)((int64_t)total * blockIdx.x / gridDim.x);
   const int t1 = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
+  const int ntiles = t1 - t0;
 
-  if (t0 < t1) {
+  if (ntiles > 0) {
     if (warp == 0) {
+      // ---- TMA producer: q once per request (2 slots), K tiles through the ring ----
       if (elect_one()) {
         prefetch_tmap(&tm_k);
         prefetch_tmap(&tm_q);
         TileCursor cur;
         cur.seek(c.pref, B, t0);
-        for (int it = 0; it < t1 - t0; it++) {
+        int qs = 1, prev_b = -1;
+        uint32_t quse[2] = {0, 0};
+        for (int it = 0; it < ntiles; it++) {
+          if (cur.b != prev_b) {
+            qs ^= 1;
+            mbar_wait(&c.qempty[qs], (quse[qs] & 1) ^ 1);
+            mbar_arrive_expect_tx(&c.qfull[qs], QT_BYTES);
+            tma_load_2d(qbuf + qs * QT_BYTES, &tm_q, &c.qfull[qs], 0, cur.b * HEADS);
+            quse[qs]++;
+            prev_b = cur.b;
+          }
           const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
-          mbar_wait(&c.empty[s], ph ^ 1);
-          uint8_t *kb = smem + (size_t)s * STAGE_BYTES;
-          mbar_arrive_expect_tx(&c.full[s], STAGE_BYTES);
-          tma_load_2d(kb, &tm_k, &c.full[s], 0, (int32_t)(cur.b * k_ld + (int64_t)cur.t * TILE_M));
-          tma_load_2d(kb + KT_BYTES, &tm_q, &c.full[s], 0, cur.b * HEADS);
+          mbar_wait(&c.empty[s], ((it / STAGES) & 1) ^ 1);
+          mbar_arrive_expect_tx(&c.full[s], KT_BYTES);
+          tma_load_2d(smem + (size_t)s * KT_BYTES, &tm_k, &c.full[s], 0,
+                      (int32_t)(cur.b * k_ld + (int64_t)cur.t * TILE_M));
           cur.next(c.pref, B);
         }
       }
     } else if (warp == 1) {
+      // ---- MMA issuer ---------------------------------------------------------------
       if (elect_one()) {
-        for (int it = 0; it < t1 - t0; it++) {
+        TileCursor cur;
+        cur.seek(c.pref, B, t0);
+        int qs = 1, prev_b = -1;
+        uint32_t quse[2] = {0, 0};
+        for (int it = 0; it < ntiles; it++) {
+          if (cur.b != prev_b) {
+            if (prev_b >= 0) tc_commit(&c.qempty[qs]);  // after the last MMA reading it
+            qs ^= 1;
+            mbar_wait(&c.qfull[qs], quse[qs] & 1);
+            quse[qs]++;
+            prev_b = cur.b;
+          }
           const int s = it % STAGES;
-          const uint32_t ph = (it / STAGES) & 1;
-          const int a = it & 1;
-          const uint32_t aph = (it >> 1) & 1;
-          mbar_wait(&c.tempty[a], aph ^ 1);
-          mbar_wait(&c.full[s], ph);
+          const int a = it % NACC;
+          mbar_wait(&c.tempty[a], ((it / NACC) & 1) ^ 1);
+          mbar_wait(&c.full[s], (it / STAGES) & 1);
           tc_fence_after();
-          const uint32_t kaddr = smem_u32(smem + (size_t)s * STAGE_BYTES);
-          const uint32_t qaddr = kaddr + KT_BYTES;
+          const uint32_t kaddr = smem_u32(smem + (size_t)s * KT_BYTES);
+          const uint32_t qaddr = smem_u32(qbuf + qs * QT_BYTES);
 #pragma unroll
           for (int kk = 0; kk < DIM / 32; kk++) {
             uint64_t ad = sw128_desc(kaddr + kk * 32, 16, 1024);
@@ -139,18 +169,41 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
           tc_commit(&c.empty[s]);
           tc_commit(&c.tfull[a]);
+          cur.next(c.pref, B);
         }
       }
     } else {
-      // epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
+      // ---- epilogue: group g = tiles it % 2 == g; warp % 4 = TMEM lane quarter ------
+      const int e = warp - 2;
+      const int g = e >> 2;
       const int quarter = warp & 3;
       const int row = quarter * 32 + lane;
       TileCursor cur;
       cur.seek(c.pref, B, t0);
-      for (int it = 0; it < t1 - t0; it++) {
-        const int a = it & 1;
-        const uint32_t aph = (it >> 1) & 1;
-        mbar_wait(&c.tfull[a], aph);
+      if (g == 1) cur.next(c.pref, B);
+      int wb = -1, len_b = 0;
+      float wr[HEADS];
+      for (int it = g; it < ntiles; it += 2) {
+        const int b = cur.b;
+        if (b != wb) {  // head weights of this request, kept in registers
+          const float4 *src = reinterpret_cast<const float4 *>(w + (int64_t)b * HEADS);
+#pragma unroll
+          for (int h4 = 0; h4 < HEADS / 4; h4++) {
+            float4 v = __ldg(src + h4);
+            wr[4 * h4] = v.x;
+            wr[4 * h4 + 1] = v.y;
+            wr[4 * h4 + 2] = v.z;
+            wr[4 * h4 + 3] = v.w;
+          }
+          len_b = __ldg(lens + b);
+          wb = b;
+        }
+        const int64_t tok = (int64_t)cur.t * TILE_M + row;
+        const bool valid = tok < len_b;
+        const int64_t off = (int64_t)b * k_ld + tok;
+        const float ks = valid ? __ldg(kscale + off) : 0.f;
+        const int a = it % NACC;
+        mbar_wait(&c.tfull[a], (it / NACC) & 1);
         tc_fence_after();
         uint32_t r[64];
         tmem_ld_32x32b_x64(tmem + ((uint32_t)(quarter * 32) << 16) + a * HEADS, r);
@@ -158,22 +211,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&c.tempty[a]);
-        const int b = cur.b;
-        const int64_t tok = (int64_t)cur.t * TILE_M + row;
-        if (tok < lens[b]) {
-          const float4 *wb = reinterpret_cast<const float4 *>(w + (int64_t)b * HEADS);
-          float acc = 0.f;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-          for (int h4 = 0; h4 < HEADS / 4; h4++) {
-            float4 wv = __ldg(wb + h4);
-            acc = fmaf(wv.x, fmaxf(__uint_as_float(r[4 * h4 + 0]), 0.f), acc);
-            acc = fmaf(wv.y, fmaxf(__uint_as_float(r[4 * h4 + 1]), 0.f), acc);
-            acc = fmaf(wv.z, fmaxf(__uint_as_float(r[4 * h4 + 2]), 0.f), acc);
-            acc = fmaf(wv.w, fmaxf(__uint_as_float(r[4 * h4 + 3]), 0.f), acc);
-          }
-          const int64_t off = (int64_t)b * k_ld + tok;
-          logits[off] = acc * __ldg(kscale + off);
+        for (int h = 0; h < HEADS; h += 4) {
+          a0 = fmaf(wr[h + 0], fmaxf(__uint_as_float(r[h + 0]), 0.f), a0);
+          a1 = fmaf(wr[h + 1], fmaxf(__uint_as_float(r[h + 1]), 0.f), a1);
+          a2 = fmaf(wr[h + 2], fmaxf(__uint_as_float(r[h + 2]), 0.f), a2);
+          a3 = fmaf(wr[h + 3], fmaxf(__uint_as_float(r[h + 3]), 0.f), a3);
         }
+        if (valid) logits[off] = ((a0 + a1) + (a2 + a3)) * ks;
+        cur.next(c.pref, B);
         cur.next(c.pref, B);
       }
     }

@@ -6,17 +6,20 @@
 //
 // TMEM budget drives the split: the fp32 output of 128 heads x 512 dims is 256 KB,
 // the whole TMEM of one SM, so each request runs on two CTAs that own 256 output
-// dims each (O = 256 columns) and both compute the full score tile S (32 columns,
-// double-buffered).  Per CTA:
-//   * Q (bf16 -> f16) resident in shared memory, SW128 K-major, 144 KB;
-//   * 8 "gather" warps pull the 656-B rows by slot index (16-B loads), dequantise
-//     e4m3 x group-scale -> f16 and RoPE bf16 -> f16 straight into the SW128 KV
-//     tile (32 rows x 576, double-buffered) — the TMA-gather role, done with LSU
-//     loads because every row also needs a dequant pass before the tensor core;
-//   * 1 MMA thread: S = Q K^T (M=128, N=32, 36 x K=16) then O += P V
-//     (M=128, N=256, V as the MN-major view of the same tile);
-//   * 4 softmax warps (one head per TMEM lane): online softmax in exp2 domain with
-//     lazy O rescaling (only when the running max grows by > 8), P -> f16 (SW64).
+// dims each and both compute the full score tile S.  Per CTA (512 TMEM columns):
+//   O      [0,256)    fp32 accumulator, 128 heads x 256 dims
+//   S0/S1  [256,320)  fp32 scores, 32 rows each; P (f16) overwrites the first 16
+//                     columns of its S buffer and feeds PV straight from TMEM
+//   Qt     [320,512)  q dims 0..383 as f16 pairs: the A operand of S from TMEM
+// Shared memory: q dims 384..575 (SW128, 48 KB), a 4-deep ring of raw 656-B rows
+// filled by the TMA engine (one cp.async.bulk per row, mbarrier tx-count), a 2-deep
+// ring of dequantised f16 KV tiles (SW128, 36 KB each) and the request's slot ids.
+//
+// Warp roles (448 threads): w0-3 softmax (thread = head; online softmax in exp2
+// domain with lazy O rescaling when the running max grows by > 8), w4 TMEM alloc +
+// MMA issuer (S = Q K^T: M=128, N=32, 36 x K=16; O += P V: M=128, N=256, V read as
+// the MN-major view of the same tile), w5 row gather (bulk copies), w6-13 dequant
+// (e4m3 x group scale -> f16, RoPE bf16 -> f16, smem -> smem).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -29,41 +32,56 @@ constexpr int QK_DIM = ESS_MLA_QK_DIM;    // 576
 constexpr int V_HALF = 256;               // output dims per CTA
 constexpr int NB = 32;                    // KV rows per tile
 constexpr int NBLK = QK_DIM / 64;         // 9 dim-blocks of 64 (128 B of f16)
-constexpr int Q_BYTES = HEADS * QK_DIM * 2;        // 147456
+constexpr int QT_BLKS = 6;                // q blocks held in TMEM (dims 0..383)
+constexpr int QS_BLKS = NBLK - QT_BLKS;   // q blocks in shared memory (dims 384..575)
+constexpr int QS_BYTES = QS_BLKS * HEADS * 128;    // 49152
 constexpr int KV_BLK_BYTES = NB * 128;             // 4096
 constexpr int KV_BYTES = NBLK * KV_BLK_BYTES;      // 36864
-constexpr int P_BYTES = HEADS * NB * 2;            // 8192
-constexpr int NSOFT = 4, NMMA = 1, NGATHER = 8;
-constexpr int NTHREADS = 32 * (NSOFT + NMMA + NGATHER);  // 416
-constexpr int MMA_WARP = NSOFT;
-constexpr int G0 = NSOFT + NMMA;  // first gather warp
-constexpr int ROW = ESS_LATENT_ROW_BYTES;
-constexpr uint32_t TM_O = 0, TM_S = 256;  // TMEM column bases
+constexpr int ROW = ESS_LATENT_ROW_BYTES;          // 656
+constexpr int RAW_BYTES = NB * ROW;                // 20992
+constexpr int KS = 2, RS = 4;                      // ring depths
+constexpr int MAX_N = ESS_MAX_REQUEST;
+constexpr int NSOFT = 4, NDEQ = 8;
+constexpr int MMA_WARP = NSOFT, GATHER_WARP = NSOFT + 1, DEQ0 = NSOFT + 2;
+constexpr int NTHREADS = 32 * (NSOFT + 2 + NDEQ);  // 448
+constexpr uint32_t TM_O = 0, TM_S = 256, TM_Q = 320;
 constexpr float RESCALE_THRESHOLD = 8.0f;
 constexpr uint32_t IDESC_S = make_idesc(0 /*f16*/, 0 /*f16*/, HEADS, NB, 0, 0);
 constexpr uint32_t IDESC_PV = make_idesc(0, 0, HEADS, V_HALF, 0, 1 /*B MN-major*/);
 
 struct Ctrl {
-  uint64_t kv_full[2], kv_empty[2], s_full[2], s_empty[2], p_full, p_empty, o_done;
+  uint64_t raw_full[RS], raw_empty[RS], kv_full[KS], kv_empty[KS];
+  uint64_t s_full[2], s_free[2], p_full, p_empty, o_done;
   uint32_t tmem;
 };
-constexpr size_t SMEM_BYTES = 1024 + Q_BYTES + 2 * KV_BYTES + P_BYTES + sizeof(Ctrl);
+constexpr size_t SMEM_BYTES =
+    1024 + QS_BYTES + KS * KV_BYTES + RS * RAW_BYTES + MAX_N * 4 + sizeof(Ctrl);
 
 __device__ __forceinline__ uint32_t sw128(uint32_t o) { return o ^ (((o >> 7) & 7u) << 4); }
-__device__ __forceinline__ uint32_t sw64(uint32_t o) { return o ^ (((o >> 7) & 3u) << 4); }
-
-__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)1 << 16;  // LBO 16 B (unused for swizzled K-major)
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;
-  d |= (uint64_t)4 << 61;  // SWIZZLE_64B
-  return d;
-}
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
+      : "memory");
 }
 
 __device__ __forceinline__ uint32_t cvt_e4m3x2_f16x2(uint16_t v) {
@@ -84,6 +102,11 @@ __device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t v) {
   return *reinterpret_cast<uint32_t *>(&h);
 }
 
+__device__ __forceinline__ uint4 cvt8_bf16_f16(uint4 x) {
+  return make_uint4(bf16x2_to_f16x2(x.x), bf16x2_to_f16x2(x.y), bf16x2_to_f16x2(x.z),
+                    bf16x2_to_f16x2(x.w));
+}
+
 __global__ void __launch_bounds__(NTHREADS, 1)
     sparse_mla_kernel(const uint16_t *__restrict__ q, const uint8_t *__restrict__ rows,
                       int64_t rows_per_pool, int pool_begin, const int32_t *__restrict__ sel_row,
@@ -91,22 +114,30 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                       uint16_t *__restrict__ out, float *__restrict__ lse) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sq = smem;
-  uint8_t *skv = smem + Q_BYTES;
-  uint8_t *sp = skv + 2 * KV_BYTES;
-  Ctrl &c = *reinterpret_cast<Ctrl *>(sp + P_BYTES);
+  uint8_t *sq = smem;                        // q dims 384..575, 3 SW128 blocks
+  uint8_t *skv = sq + QS_BYTES;              // KS dequantised tiles
+  uint8_t *sraw = skv + KS * KV_BYTES;       // RS raw row tiles
+  int32_t *ssel = reinterpret_cast<int32_t *>(sraw + RS * RAW_BYTES);
+  Ctrl &c = *reinterpret_cast<Ctrl *>(ssel + MAX_N);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int v = blockIdx.x;  // output half
   const int b = blockIdx.y;
-  const int n = counts[b];
+  const int n = min(counts[b], MAX_N);
   const int ntiles = (n + NB - 1) / NB;
+  const uint16_t *qb = q + (int64_t)b * HEADS * QK_DIM;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; i++) {
-      mbar_init(&c.kv_full[i], NGATHER);
+    for (int i = 0; i < RS; i++) {
+      mbar_init(&c.raw_full[i], 1);
+      mbar_init(&c.raw_empty[i], NDEQ);
+    }
+    for (int i = 0; i < KS; i++) {
+      mbar_init(&c.kv_full[i], NDEQ);
       mbar_init(&c.kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; i++) {
       mbar_init(&c.s_full[i], 1);
-      mbar_init(&c.s_empty[i], NSOFT);
+      mbar_init(&c.s_free[i], 1);
     }
     mbar_init(&c.p_full, NSOFT);
     mbar_init(&c.p_empty, 1);
@@ -114,26 +145,45 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     fence_barrier_init();
   }
   if (warp == MMA_WARP) tmem_alloc<512>(&c.tmem);
-  // Q: bf16 -> f16, SW128 K-major, 9 blocks of [128 heads][64 dims]
-  {
-    const uint4 *qg = reinterpret_cast<const uint4 *>(q + (int64_t)b * HEADS * QK_DIM);
-    for (int it = threadIdx.x; it < HEADS * QK_DIM / 8; it += NTHREADS) {
-      const int h = it / (QK_DIM / 8), ch = it % (QK_DIM / 8);  // ch: 8-element chunk
-      uint4 x = __ldg(qg + it);
-      uint4 y;
-      y.x = bf16x2_to_f16x2(x.x);
-      y.y = bf16x2_to_f16x2(x.y);
-      y.z = bf16x2_to_f16x2(x.z);
-      y.w = bf16x2_to_f16x2(x.w);
-      const uint32_t o = (uint32_t)(ch >> 3) * (HEADS * 128) + sw128((uint32_t)h * 128 + (ch & 7) * 16);
-      *reinterpret_cast<uint4 *>(sq + o) = y;
-    }
-  }
-  fence_proxy_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = c.tmem;
+
+  // ---- prologue: q -> TMEM (dims 0..383) and smem (384..575); slot ids -> smem ----
+  if (warp < NSOFT) {
+    const int h = warp * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint4 *src = reinterpret_cast<const uint4 *>(qb + (int64_t)h * QK_DIM);
+#pragma unroll 1
+    for (int cc = 0; cc < QT_BLKS; cc++) {  // 64 dims = 32 columns per chunk
+      uint32_t r[32];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        uint4 y = cvt8_bf16_f16(__ldg(src + cc * 8 + k));
+        r[4 * k] = y.x;
+        r[4 * k + 1] = y.y;
+        r[4 * k + 2] = y.z;
+        r[4 * k + 3] = y.w;
+      }
+      tmem_st_32x32b_x32(tmem + lane_base + TM_Q + cc * 32, r);
+    }
+    tmem_st_wait();
+  } else if (warp == GATHER_WARP) {
+    const int32_t *sel = sel_row + (int64_t)b * sel_stride;
+    for (int j = lane; j < n; j += 32) ssel[j] = __ldg(sel + j);
+  } else if (warp >= DEQ0) {
+    const int gt = threadIdx.x - DEQ0 * 32;
+    for (int it = gt; it < HEADS * QS_BLKS * 8; it += NDEQ * 32) {
+      const int h = it / (QS_BLKS * 8), ch = it % (QS_BLKS * 8);  // 8-element chunk of dims 384..
+      uint4 y = cvt8_bf16_f16(__ldg(reinterpret_cast<const uint4 *>(qb + (int64_t)h * QK_DIM + 384) + ch));
+      *reinterpret_cast<uint4 *>(sq + (ch >> 3) * (HEADS * 128) + sw128((uint32_t)h * 128 + (ch & 7) * 16)) = y;
+    }
+    fence_proxy_async_smem();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
   const float scale_log2 = sm_scale * 1.4426950408889634f;
 
   if (warp < NSOFT) {
@@ -142,16 +192,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     float m_run = -INFINITY, l_run = 0.f;
     for (int i = 0; i < ntiles; i++) {
-      const int kb = i & 1;
-      const uint32_t ph = (i >> 1) & 1;
-      mbar_wait(&c.s_full[kb], ph);
+      const int sb = i & 1;
+      mbar_wait(&c.s_full[sb], (i >> 1) & 1);
       tc_fence_after();
       uint32_t s[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + TM_S + kb * NB, s);
+      tmem_ld_32x32b_x32(tmem + lane_base + TM_S + sb * NB, s);
       tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&c.s_empty[kb]);
       float x[32];
       float mt = -INFINITY;
 #pragma unroll
@@ -159,7 +205,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         x[j] = (i * NB + j < n) ? __uint_as_float(s[j]) * scale_log2 : -INFINITY;
         mt = fmaxf(mt, x[j]);
       }
-      // PV(i-1) must be done before P is overwritten or O rescaled
+      // PV(i-1) must be done before O is rescaled
       mbar_wait(&c.p_empty, (i & 1) ^ 1);
       tc_fence_after();
       // warp-uniform decision (tcgen05.ld/st are .sync.aligned); a lane whose own
@@ -178,27 +224,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int j = 0; j < 32; j++) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
             tmem_st_32x32b_x32(tmem + lane_base + TM_O + cc * 32, o);
           }
-          tmem_st_wait();
         }
         m_run = m_new;
       }
-      // P (f16) -> SW64 K-major [128 heads][32 rows]
+      // P (f16 pairs) over the first 16 columns of this S buffer
+      uint32_t p[16];
       float lsum = 0.f;
 #pragma unroll
-      for (int ch = 0; ch < 4; ch++) {
-        uint32_t w4[4];
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-          __half2 p2 = __floats2half2_rn(exp2f(x[ch * 8 + 2 * e] - m_run), exp2f(x[ch * 8 + 2 * e + 1] - m_run));
-          float2 f = __half22float2(p2);
-          lsum += f.x + f.y;
-          w4[e] = *reinterpret_cast<uint32_t *>(&p2);
-        }
-        const uint32_t o = (uint32_t)(h >> 3) * 512 + sw64((uint32_t)(h & 7) * 64 + ch * 16);
-        *reinterpret_cast<uint4 *>(sp + o) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+      for (int e = 0; e < 16; e++) {
+        __half2 p2 = __floats2half2_rn(exp2f(x[2 * e] - m_run), exp2f(x[2 * e + 1] - m_run));
+        float2 f = __half22float2(p2);
+        lsum += f.x + f.y;
+        p[e] = *reinterpret_cast<uint32_t *>(&p2);
       }
       l_run += lsum;
-      fence_proxy_async_smem();
+      tmem_st_32x32b_x16(tmem + lane_base + TM_S + sb * NB, p);
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&c.p_full);
@@ -236,65 +277,83 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp == MMA_WARP) {
     // ---------------- MMA issuer --------------------------------------------------
     if (elect_one() && ntiles > 0) {
-      const uint32_t qaddr = smem_u32(sq), paddr = smem_u32(sp);
+      const uint32_t qsaddr = smem_u32(sq);
       auto issue_s = [&](int i) {
-        const int kb = i & 1;
-        const uint32_t ph = (i >> 1) & 1;
-        mbar_wait(&c.kv_full[kb], ph);
-        mbar_wait(&c.s_empty[kb], ph ^ 1);
+        const int kb = i % KS, sb = i & 1;
+        mbar_wait(&c.kv_full[kb], (i / KS) & 1);
+        mbar_wait(&c.s_free[sb], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t kvaddr = smem_u32(skv + kb * KV_BYTES);
+        const uint32_t d = tmem + TM_S + sb * NB;
 #pragma unroll 1
-        for (int blk = 0; blk < NBLK; blk++) {
+        for (int blk = 0; blk < QT_BLKS; blk++) {
 #pragma unroll
           for (int kk = 0; kk < 4; kk++) {
-            uint64_t ad = sw128_desc(qaddr + blk * (HEADS * 128) + kk * 32, 16, 1024);
             uint64_t bd = sw128_desc(kvaddr + blk * KV_BLK_BYTES + kk * 32, 16, 1024);
-            mma_f16_ss(tmem + TM_S + kb * NB, ad, bd, IDESC_S, (blk | kk) ? 1u : 0u);
+            mma_f16_ts(d, tmem + TM_Q + (blk * 4 + kk) * 8, bd, IDESC_S, (blk | kk) ? 1u : 0u);
           }
         }
-        tc_commit(&c.s_full[kb]);
+#pragma unroll 1
+        for (int blk = QT_BLKS; blk < NBLK; blk++) {
+#pragma unroll
+          for (int kk = 0; kk < 4; kk++) {
+            uint64_t ad = sw128_desc(qsaddr + (blk - QT_BLKS) * (HEADS * 128) + kk * 32, 16, 1024);
+            uint64_t bd = sw128_desc(kvaddr + blk * KV_BLK_BYTES + kk * 32, 16, 1024);
+            mma_f16_ss(d, ad, bd, IDESC_S, 1u);
+          }
+        }
+        tc_commit(&c.s_full[sb]);
       };
       issue_s(0);
       for (int i = 0; i < ntiles; i++) {
         if (i + 1 < ntiles) issue_s(i + 1);
-        const int kb = i & 1;
+        const int kb = i % KS, sb = i & 1;
         mbar_wait(&c.p_full, i & 1);
         tc_fence_after();
         const uint32_t vaddr = smem_u32(skv + kb * KV_BYTES) + (uint32_t)(4 * v) * KV_BLK_BYTES;
 #pragma unroll
         for (int kk = 0; kk < NB / 16; kk++) {
-          uint64_t ad = sw64_desc(paddr + kk * 32, 512);
           uint64_t bd = sw128_desc(vaddr + kk * 16 * 128, KV_BLK_BYTES, 1024);
-          mma_f16_ss(tmem + TM_O, ad, bd, IDESC_PV, (i | kk) ? 1u : 0u);
+          mma_f16_ts(tmem + TM_O, tmem + TM_S + sb * NB + kk * 8, bd, IDESC_PV, (i | kk) ? 1u : 0u);
         }
         tc_commit(&c.p_empty);
         tc_commit(&c.kv_empty[kb]);
+        tc_commit(&c.s_free[sb]);
         if (i == ntiles - 1) tc_commit(&c.o_done);
       }
     }
-  } else {
-    // ---------------- gather + dequant warps --------------------------------------
-    const int gt = threadIdx.x - G0 * 32;  // 0..255
+  } else if (warp == GATHER_WARP) {
+    // ---------------- row gather: one bulk copy (TMA engine) per selected row ----
     const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b) * rows_per_pool * ROW;
-    const int32_t *sel = sel_row + (int64_t)b * sel_stride;
     for (int i = 0; i < ntiles; i++) {
-      const int kb = i & 1;
-      const uint32_t ph = (i >> 1) & 1;
-      mbar_wait(&c.kv_empty[kb], ph ^ 1);
+      const int rs = i % RS;
+      const int nvalid = min(NB, n - i * NB);
+      mbar_wait(&c.raw_empty[rs], ((i / RS) & 1) ^ 1);
+      if (lane == 0) mbar_arrive_expect_tx(&c.raw_full[rs], (uint32_t)(nvalid * ROW));
+      __syncwarp();
+      if (lane < nvalid)
+        bulk_load(sraw + rs * RAW_BYTES + lane * ROW, pool_rows + (int64_t)ssel[i * NB + lane] * ROW,
+                  ROW, &c.raw_full[rs]);
+    }
+  } else {
+    // ---------------- dequant warps: raw rows -> f16 SW128 KV tile ----------------
+    const int gt = threadIdx.x - DEQ0 * 32;  // 0..255
+    for (int i = 0; i < ntiles; i++) {
+      const int rs = i % RS, kb = i % KS;
+      mbar_wait(&c.raw_full[rs], (i / RS) & 1);
+      mbar_wait(&c.kv_empty[kb], ((i / KS) & 1) ^ 1);
+      const uint8_t *raw = sraw + rs * RAW_BYTES;
       uint8_t *kv = skv + kb * KV_BYTES;
       // NoPE: 32 rows x 32 chunks of 16 e4m3 -> 2 x 16 B of f16
 #pragma unroll
       for (int k = 0; k < 4; k++) {
         const int item = gt + 256 * k;
         const int r = item >> 5, ch = item & 31;
-        const int j = i * NB + r;
         uint4 y0 = make_uint4(0, 0, 0, 0), y1 = y0;
-        if (j < n) {
-          const uint8_t *src = pool_rows + (int64_t)sel[j] * ROW;
-          const uint4 x = ld_nc_v4(src + ch * 16);
-          const float sc = __ldg(reinterpret_cast<const float *>(src + 512) + (ch >> 3));
-          const __half2 s2 = __float2half2_rn(sc);
+        if (i * NB + r < n) {
+          const uint8_t *src = raw + r * ROW;
+          const uint4 x = *reinterpret_cast<const uint4 *>(src + ch * 16);
+          const __half2 s2 = __float2half2_rn(*reinterpret_cast<const float *>(src + 512 + 4 * (ch >> 3)));
           y0.x = hmul2_u32(cvt_e4m3x2_f16x2((uint16_t)(x.x & 0xFFFF)), s2);
           y0.y = hmul2_u32(cvt_e4m3x2_f16x2((uint16_t)(x.x >> 16)), s2);
           y0.z = hmul2_u32(cvt_e4m3x2_f16x2((uint16_t)(x.y & 0xFFFF)), s2);
@@ -304,7 +363,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           y1.z = hmul2_u32(cvt_e4m3x2_f16x2((uint16_t)(x.w & 0xFFFF)), s2);
           y1.w = hmul2_u32(cvt_e4m3x2_f16x2((uint16_t)(x.w >> 16)), s2);
         }
-        // dims [16ch, 16ch+16): block 16ch/64, 16-B chunks (2ch)%8 and (2ch+1)%8
+        // dims [16ch, 16ch+16): block ch/4, 16-B chunks 2(ch%4) and 2(ch%4)+1
         const int blk = ch >> 2, c0 = (ch & 3) * 2;
         uint8_t *base = kv + blk * KV_BLK_BYTES;
         *reinterpret_cast<uint4 *>(base + sw128((uint32_t)r * 128 + c0 * 16)) = y0;
@@ -313,20 +372,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // RoPE: 32 rows x 8 chunks of 8 bf16 -> 8 f16 (dim-block 8)
       {
         const int r = gt >> 3, ch = gt & 7;
-        const int j = i * NB + r;
         uint4 y = make_uint4(0, 0, 0, 0);
-        if (j < n) {
-          const uint4 x = ld_nc_v4(pool_rows + (int64_t)sel[j] * ROW + 528 + ch * 16);
-          y.x = bf16x2_to_f16x2(x.x);
-          y.y = bf16x2_to_f16x2(x.y);
-          y.z = bf16x2_to_f16x2(x.z);
-          y.w = bf16x2_to_f16x2(x.w);
-        }
+        if (i * NB + r < n) y = cvt8_bf16_f16(*reinterpret_cast<const uint4 *>(raw + r * ROW + 528 + ch * 16));
         *reinterpret_cast<uint4 *>(kv + 8 * KV_BLK_BYTES + sw128((uint32_t)r * 128 + ch * 16)) = y;
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&c.kv_full[kb]);
+      if (lane == 0) {
+        mbar_arrive(&c.raw_empty[rs]);
+        mbar_arrive(&c.kv_full[kb]);
+      }
     }
   }
   tc_fence_before();
