@@ -15,6 +15,10 @@
  * Data layouts:
  *   latent row   656 B = [0,512) e4m3 NoPE | [512,528) 4 x f32 group scales |
  *                [528,656) 64 x bf16 RoPE          (scenario.py:25, costmodel.py:31)
+ *                — the host store and every H2D/D2H transfer use this format
+ *   slot row     1152 B = 576 x f16: dequantised NoPE (e4m3 x scale) ++ RoPE; the
+ *                GPU slot store holds attention-ready rows, dequantised once when
+ *                a row is admitted (gather / write-back), never per step
  *   indexer key  128 B e4m3 + f32 scale per token (separate arrays)
  *                                                   (scenario.py:26, :30-33)
  *   pools        P = layers x requests independent LRU pools, pool id = l*B + b
@@ -31,6 +35,7 @@ extern "C" {
 #endif
 
 #define ESS_LATENT_ROW_BYTES 656
+#define ESS_SLOT_ROW_BYTES 1152 /* 576 x f16 */
 #define ESS_NOPE_DIM 512
 #define ESS_ROPE_DIM 64
 #define ESS_INDEXER_HEADS 64
@@ -66,8 +71,9 @@ int ess_host_unregister(void *host_ptr);
 
 /* ---- K3 cache manager: replaces offsim.cache.SparsePool (cache.py:29-134) ------ */
 /* num_pools pools over ids [0, max_ids), each with up to cap_max slots.  When
- * row_bytes > 0 the pool also owns its GPU slot store: per pool cap_max slot
- * rows + staging_rows transient rows (oversize requests, cache.py:103-111). */
+ * row_bytes == ESS_SLOT_ROW_BYTES the pool also owns its GPU slot store: per pool
+ * cap_max slot rows + staging_rows transient rows (oversize requests,
+ * cache.py:103-111).  row_bytes == 0: bookkeeping only (replay). */
 int ess_pool_create(ess_pool **out, int32_t num_pools, int64_t max_ids, int32_t cap_max,
                     int32_t row_bytes, int32_t staging_rows);
 int ess_pool_destroy(ess_pool *pool);

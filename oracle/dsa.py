@@ -111,6 +111,18 @@ def unpack_latent_rows(rows_u8: np.ndarray):
     return k_nope.astype(np.float32), bf16_decode(rope)
 
 
+def slot_rows(rows_u8: np.ndarray) -> np.ndarray:
+    """[n, 656] latent rows -> [n, 576] f16 slot rows, the GPU slot-store format
+    (include/ess_b200.h): NoPE = f16(f32(e4m3) * f32 scale), RoPE = f16(bf16)."""
+    rows_u8 = np.ascontiguousarray(rows_u8, dtype=np.uint8)
+    n = rows_u8.shape[0]
+    nope = e4m3_decode(rows_u8[:, :NOPE_DIM]).astype(np.float32)
+    scales = rows_u8[:, NOPE_DIM:NOPE_DIM + 16].copy().view(np.float32).reshape(n, 4)
+    k_nope = (nope * np.repeat(scales, NOPE_GROUP, axis=1)).astype(np.float16)
+    rope = bf16_decode(rows_u8[:, NOPE_DIM + 16:].copy().view(np.uint16).reshape(n, ROPE_DIM))
+    return np.concatenate([k_nope, rope.astype(np.float16)], axis=1)
+
+
 def sparse_mla(q: np.ndarray, rows_u8: np.ndarray, sm_scale: float):
     """One request: q [H, 576] f32 (bf16 values), rows_u8 [n, 656] selected rows.
 

@@ -47,7 +47,8 @@ ESS_ERR_CAPACITY, ESS_ERR_SHRINK, ESS_ERR_DUPLICATE = -1, -2, -3
 ESS_ERR_NOMEM, ESS_ERR_RATIO, ESS_ERR_ARG, ESS_ERR_CUDA, ESS_ERR_CLOCK = -4, -5, -6, -7, -8
 ESS_ACCESS_SORT_EVICTED = 1
 MAX_REQUEST = 2048
-LATENT_ROW_BYTES = 656
+LATENT_ROW_BYTES = 656   # host store / transfer format (e4m3 NoPE + scales + bf16 RoPE)
+SLOT_ROW_BYTES = 1152    # GPU slot store format (576 x f16, dequantised on admission)
 
 _lib = None
 

@@ -59,7 +59,8 @@ def _i32(x, device) -> torch.Tensor:
 class PoolSet:
     """P LRU pools over entry ids [0, max_ids) with at most ``cap_max`` slots each.
 
-    With ``row_bytes`` = 656 the set also owns the GPU slot store (cap_max rows per
+    With ``row_bytes`` = 1152 (576 x f16) the set also owns the GPU slot store of
+    attention-ready rows, dequantised once on admission (cap_max rows per
     pool + ``staging_rows`` transient rows for oversize requests, cache.py:103-111).
     All methods enqueue on the current CUDA stream; ``check()`` synchronises and
     raises the reference's exceptions for errors detected on the device.
@@ -196,12 +197,13 @@ class PoolSet:
         return p.value or 0
 
     def rows_view(self) -> torch.Tensor:
-        """The slot store as a [P, rows_per_pool, row_bytes] uint8 tensor (aliasing view)."""
+        """The slot store as a [P, rows_per_pool, 576] float16 tensor (aliasing view):
+        dequantised NoPE (512) ++ RoPE (64) per slot row."""
         if not self.row_bytes:
             raise ValueError("pool set has no slot store")
         n = self.num_pools * self.rows_per_pool * self.row_bytes
-        return _wrap_device(self.rows_ptr(), n, self.device, self).view(
-            self.num_pools, self.rows_per_pool, self.row_bytes)
+        return _wrap_device(self.rows_ptr(), n, self.device, self).view(torch.float16).view(
+            self.num_pools, self.rows_per_pool, self.row_bytes // 2)
 
     def status(self) -> int:
         st = ctypes.c_int32(0)

@@ -1,6 +1,8 @@
 // Shared device/host helpers for libess_b200 (sm_100a only).
 #pragma once
 
+#include <cuda.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -14,10 +16,17 @@
 
 int ess_record_cuda_error(cudaError_t e);
 
+// Host: 2D tiled tensor map (driver entry point fetched through the runtime, so
+// the library does not link libcuda).  inner/box_inner in elements.
+bool ess_make_tmap_2d(CUtensorMap *m, CUtensorMapDataType dtype, const void *base,
+                      uint64_t inner, uint64_t rows, uint64_t row_stride_bytes,
+                      uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swizzle);
+int ess_sm_count();
+
 // Per-pool mutable scalars (one 64-byte record per pool).  Recency is a strictly
 // increasing 32-bit clock; free slots carry key == slot index (< cap_max) and
-// resident slots carry a stamp >= cap_max, so "the v smallest keys" is exactly
-// "free slots first, then least-recent residents" (no ties).
+// resident slots carry a stamp >= ESS_CLOCK_BASE, so "the v smallest keys" is
+// exactly "free slots first, then least-recent residents" (no ties).
 struct PoolMeta {
   int32_t cap;
   int32_t size;
@@ -80,6 +89,32 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int *warp_buf, int *t
   *total = warp_buf[NT / 32 - 1];
   __syncthreads();
   return base + x - v;
+}
+
+// ---- number formats ---------------------------------------------------------------
+__device__ __forceinline__ uint32_t cvt_e4m3x2_f16x2(uint16_t v) {  // exact
+  uint32_t r;
+  asm("{\n\t.reg .b16 t;\n\tmov.b16 t, %1;\n\tcvt.rn.f16x2.e4m3x2 %0, t;\n\t}" : "=r"(r) : "h"(v));
+  return r;
+}
+
+// f16(f32(e4m3) * s) for two packed e4m3 values (one rounding)
+__device__ __forceinline__ uint32_t e4m3x2_scaled_f16x2(uint16_t v, float s) {
+  uint32_t h = cvt_e4m3x2_f16x2(v);
+  float2 f = __half22float2(*reinterpret_cast<__half2 *>(&h));
+  __half2 r = __floats2half2_rn(f.x * s, f.y * s);
+  return *reinterpret_cast<uint32_t *>(&r);
+}
+
+__device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t v) {
+  float lo = __uint_as_float(v << 16), hi = __uint_as_float(v & 0xFFFF0000u);
+  __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+
+__device__ __forceinline__ uint4 cvt8_bf16_f16(uint4 x) {
+  return make_uint4(bf16x2_to_f16x2(x.x), bf16x2_to_f16x2(x.y), bf16x2_to_f16x2(x.z),
+                    bf16x2_to_f16x2(x.w));
 }
 
 // Bounded mbarrier / flag spin: trap instead of hanging the GPU on a protocol bug.

@@ -15,8 +15,6 @@
 // warp % 4); head weights stay in registers while the request does not change.
 #include <cuda.h>
 
-#include <mutex>
-
 #include "common.cuh"
 
 namespace {
@@ -231,47 +229,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
-typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
-                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
-                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+// 2D uint8 tensor [rows][128 B], box [box_rows][128 B], 128-B swizzle.  The last
+// encoded maps are cached: the decode loop calls with the same buffers every step.
+struct MapCache {
+  const void *base = nullptr;
+  uint64_t rows = 0;
+  uint32_t box = 0;
+  CUtensorMap map;
+};
 
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void *p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  });
-  return fn;
-}
-
-// 2D uint8 tensor [rows][128 B], box [box_rows][128 B], 128-B swizzle
-bool make_map(CUtensorMap *m, const void *base, uint64_t rows, uint32_t box_rows) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return false;
-  cuuint64_t dims[2] = {128, rows};
-  cuuint64_t strides[1] = {128};
-  cuuint32_t box[2] = {128, box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+bool make_map(CUtensorMap *m, const void *base, uint64_t rows, uint32_t box_rows, MapCache &cache) {
+  if (cache.base == base && cache.rows == rows && cache.box == box_rows) {
+    *m = cache.map;
+    return true;
   }
-  return n;
+  if (!ess_make_tmap_2d(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, base, 128, rows, 128, 128, box_rows,
+                        CU_TENSOR_MAP_SWIZZLE_128B))
+    return false;
+  cache.base = base;
+  cache.rows = rows;
+  cache.box = box_rows;
+  cache.map = *m;
+  return true;
 }
 
 }  // namespace
@@ -285,16 +264,18 @@ extern "C" int ess_indexer_logits(const void *d_q, const float *d_w, const void 
       (reinterpret_cast<uintptr_t>(d_w) & 15))
     return ESS_ERR_ARG;
   if (batch == 0) return ESS_OK;
-  CUtensorMap tk, tq;
-  if (!make_map(&tk, d_k, (uint64_t)batch * (uint64_t)k_ld, TILE_M)) return ESS_ERR_CUDA;
-  if (!make_map(&tq, d_q, (uint64_t)batch * HEADS, HEADS)) return ESS_ERR_CUDA;
+  static thread_local MapCache kc, qc;
+  alignas(64) CUtensorMap tk;
+  alignas(64) CUtensorMap tq;
+  if (!make_map(&tk, d_k, (uint64_t)batch * (uint64_t)k_ld, TILE_M, kc)) return ESS_ERR_CUDA;
+  if (!make_map(&tq, d_q, (uint64_t)batch * HEADS, HEADS, qc)) return ESS_ERR_CUDA;
   static bool attr = false;
   if (!attr) {
     ESS_CUDA_TRY(cudaFuncSetAttribute(indexer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)SMEM_BYTES));
     attr = true;
   }
-  indexer_kernel<<<sm_count(), NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
+  indexer_kernel<<<ess_sm_count(), NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
       tk, tq, d_w, d_kscale, d_len, batch, k_ld, d_logits);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;

@@ -1,8 +1,10 @@
-// K5: sparse MLA decode over the selected latent rows (op "sparse_mla",
+// K5: sparse MLA decode over the selected slot rows (op "sparse_mla",
 // costmodel.py:18-27).
 //
-// out[h] = softmax_j(q[h] . K[j] * sm_scale) V[j], K[j] = dequant(NoPE) ++ RoPE (576),
-// V[j] = dequant(NoPE) (512), over the count[b] slot-store rows sel_row[b][:].
+// out[h] = softmax_j(q[h] . K[j] * sm_scale) V[j], K[j] = NoPE ++ RoPE (576 f16),
+// V[j] = NoPE (512 f16), over the count[b] slot rows sel_row[b][:].  Slot rows are
+// attention-ready f16 (dequantised once on admission by K4), so this kernel is a
+// pure row-gather + tensor-core kernel.
 //
 // TMEM budget drives the split: the fp32 output of 128 heads x 512 dims is 256 KB,
 // the whole TMEM of one SM, so each request runs on two CTAs that own 256 output
@@ -11,15 +13,16 @@
 //   S0/S1  [256,320)  fp32 scores, 32 rows each; P (f16) overwrites the first 16
 //                     columns of its S buffer and feeds PV straight from TMEM
 //   Qt     [320,512)  q dims 0..383 as f16 pairs: the A operand of S from TMEM
-// Shared memory: q dims 384..575 (SW128, 48 KB), a 4-deep ring of raw 656-B rows
-// filled by the TMA engine (one cp.async.bulk per row, mbarrier tx-count), a 2-deep
-// ring of dequantised f16 KV tiles (SW128, 36 KB each) and the request's slot ids.
+// Shared memory: q dims 384..575 (SW128 K-major, 48 KB), a 4-deep ring of KV tiles
+// (32 rows x 576 f16, SW128: 9 blocks of [32 rows][64 dims]) filled by 16-B
+// cp.async straight into the swizzled positions (TMA tile::gather4 moves only
+// 4 x 128 B per instruction and was instruction-rate bound here), and the
+// request's slot ids.
 //
-// Warp roles (448 threads): w0-3 softmax (thread = head; online softmax in exp2
+// Warp roles (288 threads): w0-3 softmax (thread = head; online softmax in exp2
 // domain with lazy O rescaling when the running max grows by > 8), w4 TMEM alloc +
 // MMA issuer (S = Q K^T: M=128, N=32, 36 x K=16; O += P V: M=128, N=256, V read as
-// the MN-major view of the same tile), w5 row gather (bulk copies), w6-13 dequant
-// (e4m3 x group scale -> f16, RoPE bf16 -> f16, smem -> smem).
+// the MN-major view of the same tile), w5-8 row loaders.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -37,25 +40,24 @@ constexpr int QS_BLKS = NBLK - QT_BLKS;   // q blocks in shared memory (dims 384
 constexpr int QS_BYTES = QS_BLKS * HEADS * 128;    // 49152
 constexpr int KV_BLK_BYTES = NB * 128;             // 4096
 constexpr int KV_BYTES = NBLK * KV_BLK_BYTES;      // 36864
-constexpr int ROW = ESS_LATENT_ROW_BYTES;          // 656
-constexpr int RAW_BYTES = NB * ROW;                // 20992
-constexpr int KS = 2, RS = 4;                      // ring depths
+constexpr int KS = 4;                              // KV ring depth
 constexpr int MAX_N = ESS_MAX_REQUEST;
-constexpr int NSOFT = 4, NDEQ = 8;
-constexpr int MMA_WARP = NSOFT, GATHER_WARP = NSOFT + 1, DEQ0 = NSOFT + 2;
-constexpr int NTHREADS = 32 * (NSOFT + 2 + NDEQ);  // 448
+constexpr int NSOFT = 4, NLOAD = 4;
+constexpr int MMA_WARP = NSOFT, LOAD0 = NSOFT + 1;
+constexpr int NTHREADS = 32 * (NSOFT + 1 + NLOAD);  // 288
+constexpr int ROWS_PER_LOADER = NB / NLOAD;         // 8
+constexpr int SLOT_CHUNKS = ESS_SLOT_ROW_BYTES / 16; // 72
 constexpr uint32_t TM_O = 0, TM_S = 256, TM_Q = 320;
 constexpr float RESCALE_THRESHOLD = 8.0f;
 constexpr uint32_t IDESC_S = make_idesc(0 /*f16*/, 0 /*f16*/, HEADS, NB, 0, 0);
 constexpr uint32_t IDESC_PV = make_idesc(0, 0, HEADS, V_HALF, 0, 1 /*B MN-major*/);
 
 struct Ctrl {
-  uint64_t raw_full[RS], raw_empty[RS], kv_full[KS], kv_empty[KS];
+  uint64_t kv_full[KS], kv_empty[KS];
   uint64_t s_full[2], s_free[2], p_full, p_empty, o_done;
   uint32_t tmem;
 };
-constexpr size_t SMEM_BYTES =
-    1024 + QS_BYTES + KS * KV_BYTES + RS * RAW_BYTES + MAX_N * 4 + sizeof(Ctrl);
+constexpr size_t SMEM_BYTES = 1024 + QS_BYTES + KS * KV_BYTES + MAX_N * 4 + sizeof(Ctrl);
 
 __device__ __forceinline__ uint32_t sw128(uint32_t o) { return o ^ (((o >> 7) & 7u) << 4); }
 
@@ -74,6 +76,15 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
       : "memory");
 }
 
+// 16-B async global -> shared copy (L1 bypass); src_bytes = 0 zero-fills
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -84,40 +95,16 @@ __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_
       : "memory");
 }
 
-__device__ __forceinline__ uint32_t cvt_e4m3x2_f16x2(uint16_t v) {
-  uint32_t r;
-  asm("{\n\t.reg .b16 t;\n\tmov.b16 t, %1;\n\tcvt.rn.f16x2.e4m3x2 %0, t;\n\t}" : "=r"(r) : "h"(v));
-  return r;
-}
-
-__device__ __forceinline__ uint32_t hmul2_u32(uint32_t a, __half2 s) {
-  __half2 x = *reinterpret_cast<__half2 *>(&a);
-  x = __hmul2(x, s);
-  return *reinterpret_cast<uint32_t *>(&x);
-}
-
-__device__ __forceinline__ uint32_t bf16x2_to_f16x2(uint32_t v) {
-  float lo = __uint_as_float(v << 16), hi = __uint_as_float(v & 0xFFFF0000u);
-  __half2 h = __floats2half2_rn(lo, hi);
-  return *reinterpret_cast<uint32_t *>(&h);
-}
-
-__device__ __forceinline__ uint4 cvt8_bf16_f16(uint4 x) {
-  return make_uint4(bf16x2_to_f16x2(x.x), bf16x2_to_f16x2(x.y), bf16x2_to_f16x2(x.z),
-                    bf16x2_to_f16x2(x.w));
-}
-
 __global__ void __launch_bounds__(NTHREADS, 1)
-    sparse_mla_kernel(const uint16_t *__restrict__ q, const uint8_t *__restrict__ rows,
+    sparse_mla_kernel(const uint8_t *__restrict__ rows, const uint16_t *__restrict__ q,
                       int64_t rows_per_pool, int pool_begin, const int32_t *__restrict__ sel_row,
                       int sel_stride, const int32_t *__restrict__ counts, float sm_scale,
                       uint16_t *__restrict__ out, float *__restrict__ lse) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sq = smem;                        // q dims 384..575, 3 SW128 blocks
-  uint8_t *skv = sq + QS_BYTES;              // KS dequantised tiles
-  uint8_t *sraw = skv + KS * KV_BYTES;       // RS raw row tiles
-  int32_t *ssel = reinterpret_cast<int32_t *>(sraw + RS * RAW_BYTES);
+  uint8_t *skv = sq + QS_BYTES;              // KS f16 KV tiles
+  int32_t *ssel = reinterpret_cast<int32_t *>(skv + KS * KV_BYTES);
   Ctrl &c = *reinterpret_cast<Ctrl *>(ssel + MAX_N);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int v = blockIdx.x;  // output half
@@ -127,12 +114,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint16_t *qb = q + (int64_t)b * HEADS * QK_DIM;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < RS; i++) {
-      mbar_init(&c.raw_full[i], 1);
-      mbar_init(&c.raw_empty[i], NDEQ);
-    }
     for (int i = 0; i < KS; i++) {
-      mbar_init(&c.kv_full[i], NDEQ);
+      mbar_init(&c.kv_full[i], NLOAD);
       mbar_init(&c.kv_empty[i], 1);
     }
     for (int i = 0; i < 2; i++) {
@@ -169,13 +152,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tmem_st_32x32b_x32(tmem + lane_base + TM_Q + cc * 32, r);
     }
     tmem_st_wait();
-  } else if (warp == GATHER_WARP) {
+  } else {
+    // warps 4-8: slot ids, then q dims 384..575 into SW128 smem
+    constexpr int NT = NTHREADS - NSOFT * 32;
+    const int t = threadIdx.x - NSOFT * 32;
     const int32_t *sel = sel_row + (int64_t)b * sel_stride;
-    for (int j = lane; j < n; j += 32) ssel[j] = __ldg(sel + j);
-  } else if (warp >= DEQ0) {
-    const int gt = threadIdx.x - DEQ0 * 32;
-    for (int it = gt; it < HEADS * QS_BLKS * 8; it += NDEQ * 32) {
-      const int h = it / (QS_BLKS * 8), ch = it % (QS_BLKS * 8);  // 8-element chunk of dims 384..
+    for (int j = t; j < n; j += NT) ssel[j] = __ldg(sel + j);
+    for (int it = t; it < HEADS * QS_BLKS * 8; it += NT) {
+      const int h = it / (QS_BLKS * 8), ch = it % (QS_BLKS * 8);  // 8-element chunk
       uint4 y = cvt8_bf16_f16(__ldg(reinterpret_cast<const uint4 *>(qb + (int64_t)h * QK_DIM + 384) + ch));
       *reinterpret_cast<uint4 *>(sq + (ch >> 3) * (HEADS * 128) + sw128((uint32_t)h * 128 + (ch & 7) * 16)) = y;
     }
@@ -322,66 +306,46 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (i == ntiles - 1) tc_commit(&c.o_done);
       }
     }
-  } else if (warp == GATHER_WARP) {
-    // ---------------- row gather: one bulk copy (TMA engine) per selected row ----
-    const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b) * rows_per_pool * ROW;
-    for (int i = 0; i < ntiles; i++) {
-      const int rs = i % RS;
-      const int nvalid = min(NB, n - i * NB);
-      mbar_wait(&c.raw_empty[rs], ((i / RS) & 1) ^ 1);
-      if (lane == 0) mbar_arrive_expect_tx(&c.raw_full[rs], (uint32_t)(nvalid * ROW));
-      __syncwarp();
-      if (lane < nvalid)
-        bulk_load(sraw + rs * RAW_BYTES + lane * ROW, pool_rows + (int64_t)ssel[i * NB + lane] * ROW,
-                  ROW, &c.raw_full[rs]);
-    }
   } else {
-    // ---------------- dequant warps: raw rows -> f16 SW128 KV tile ----------------
-    const int gt = threadIdx.x - DEQ0 * 32;  // 0..255
-    for (int i = 0; i < ntiles; i++) {
-      const int rs = i % RS, kb = i % KS;
-      mbar_wait(&c.raw_full[rs], (i / RS) & 1);
-      mbar_wait(&c.kv_empty[kb], ((i / KS) & 1) ^ 1);
-      const uint8_t *raw = sraw + rs * RAW_BYTES;
-      uint8_t *kv = skv + kb * KV_BYTES;
-      // NoPE: 32 rows x 32 chunks of 16 e4m3 -> 2 x 16 B of f16
-#pragma unroll
-      for (int k = 0; k < 4; k++) {
-        const int item = gt + 256 * k;
-        const int r = item >> 5, ch = item & 31;
-        uint4 y0 = make_uint4(0, 0, 0, 0), y1 = y0;
-        if (i * NB + r < n) {
-          const uint8_t *src = raw + r * ROW;
-          const uint4 x = *reinterpret_cast<const uint4 *>(src + ch * 16);
-          const __half2 s2 = __float2half2_rn(*reinterpret_cast<const float *>(src + 512 + 4 * (ch >> 3)));
-          y0.x = hmul2_u32(cvt_e4m3x2_f16x2((uint16_t)(x.x & 0xFFFF)), s2);
-          y0.y = hmul2_u32(cvt_e4m3x2_f16x2((uint16_t)(x.x >> 16)), s2);
-          y0.z = hmul2_u32(cvt_e4m3x2_f16x2((uint16_t)(x.y & 0xFFFF)), s2);
-          y0.w = hmul2_u32(cvt_e4m3x2_f16x2((uint16_t)(x.y >> 16)), s2);
-          y1.x = hmul2_u32(cvt_e4m3x2_f16x2((uint16_t)(x.z & 0xFFFF)), s2);
-          y1.y = hmul2_u32(cvt_e4m3x2_f16x2((uint16_t)(x.z >> 16)), s2);
-          y1.z = hmul2_u32(cvt_e4m3x2_f16x2((uint16_t)(x.w & 0xFFFF)), s2);
-          y1.w = hmul2_u32(cvt_e4m3x2_f16x2((uint16_t)(x.w >> 16)), s2);
-        }
-        // dims [16ch, 16ch+16): block ch/4, 16-B chunks 2(ch%4) and 2(ch%4)+1
-        const int blk = ch >> 2, c0 = (ch & 3) * 2;
-        uint8_t *base = kv + blk * KV_BLK_BYTES;
-        *reinterpret_cast<uint4 *>(base + sw128((uint32_t)r * 128 + c0 * 16)) = y0;
-        *reinterpret_cast<uint4 *>(base + sw128((uint32_t)r * 128 + (c0 + 1) * 16)) = y1;
-      }
-      // RoPE: 32 rows x 8 chunks of 8 bf16 -> 8 f16 (dim-block 8)
-      {
-        const int r = gt >> 3, ch = gt & 7;
-        uint4 y = make_uint4(0, 0, 0, 0);
-        if (i * NB + r < n) y = cvt8_bf16_f16(*reinterpret_cast<const uint4 *>(raw + r * ROW + 528 + ch * 16));
-        *reinterpret_cast<uint4 *>(kv + 8 * KV_BLK_BYTES + sw128((uint32_t)r * 128 + ch * 16)) = y;
-      }
-      fence_proxy_async_smem();
+    // ---------------- row loaders: warp w owns rows 8w..8w+7 of every tile; each lane
+    // copies 16-B chunks (lane, lane+32, lane+64 < 72) of those rows with cp.async
+    // straight into the SW128 position; one commit group per tile, signalled one
+    // tile later (wait_group 1) so two tiles are in flight per warp ----------------
+    const int w = warp - LOAD0;
+    const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b) * rows_per_pool * ESS_SLOT_ROW_BYTES;
+    const uint32_t kv0 = smem_u32(skv);
+    auto signal = [&](int i) {
+      fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&c.raw_empty[rs]);
-        mbar_arrive(&c.kv_full[kb]);
+      if (lane == 0) mbar_arrive(&c.kv_full[i % KS]);
+    };
+    for (int i = 0; i < ntiles; i++) {
+      const int kb = i % KS;
+      mbar_wait(&c.kv_empty[kb], ((i / KS) & 1) ^ 1);
+      const uint32_t kv = kv0 + kb * KV_BYTES;
+#pragma unroll
+      for (int rr = 0; rr < ROWS_PER_LOADER; rr++) {
+        const int r = w * ROWS_PER_LOADER + rr;
+        const int j = i * NB + r;
+        const bool ok = j < n;
+        const uint8_t *src = pool_rows + (int64_t)ssel[ok ? j : 0] * ESS_SLOT_ROW_BYTES;
+#pragma unroll
+        for (int k = 0; k < 3; k++) {
+          const int ch = lane + 32 * k;
+          if (ch < SLOT_CHUNKS)
+            cp_async16(kv + (ch >> 3) * KV_BLK_BYTES + r * 128 + (((ch & 7) ^ (r & 7)) << 4),
+                       src + ch * 16, ok ? 16u : 0u);
+        }
       }
+      cp_async_commit();
+      if (i > 0) {
+        cp_async_wait<1>();
+        signal(i - 1);
+      }
+    }
+    if (ntiles > 0) {
+      cp_async_wait<0>();
+      signal(ntiles - 1);
     }
   }
   tc_fence_before();
@@ -396,10 +360,10 @@ extern "C" int ess_sparse_mla(ess_pool *pool, int32_t pool_begin, const void *d_
                               const int32_t *d_sel_row, int32_t sel_stride, const int32_t *d_count,
                               int32_t batch, float sm_scale, void *d_out, float *d_lse,
                               void *stream) {
-  if (!pool || !pool->rows || pool->row_bytes != ROW || !d_q || !d_sel_row || !d_count ||
-      !d_out || !d_lse || batch < 0 || pool_begin < 0 || (int64_t)pool_begin + batch > pool->P ||
-      sel_stride < 1 || (reinterpret_cast<uintptr_t>(d_q) & 15) ||
-      (reinterpret_cast<uintptr_t>(d_out) & 15))
+  if (!pool || !pool->rows || pool->row_bytes != ESS_SLOT_ROW_BYTES || !d_q || !d_sel_row ||
+      !d_count || !d_out || !d_lse || batch < 0 || pool_begin < 0 ||
+      (int64_t)pool_begin + batch > pool->P || sel_stride < 1 ||
+      (reinterpret_cast<uintptr_t>(d_q) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15))
     return ESS_ERR_ARG;
   if (batch == 0) return ESS_OK;
   static bool attr = false;
@@ -410,8 +374,8 @@ extern "C" int ess_sparse_mla(ess_pool *pool, int32_t pool_begin, const void *d_
   }
   dim3 grid(2, batch);
   sparse_mla_kernel<<<grid, NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
-      (const uint16_t *)d_q, pool->rows, pool->rows_per_pool, pool_begin, d_sel_row, sel_stride,
-      d_count, sm_scale, (uint16_t *)d_out, d_lse);
+      pool->rows, (const uint16_t *)d_q, pool->rows_per_pool, pool_begin, d_sel_row,
+      sel_stride, d_count, sm_scale, (uint16_t *)d_out, d_lse);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }

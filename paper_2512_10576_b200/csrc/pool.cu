@@ -137,9 +137,34 @@ __device__ void sort_ids(StepSmem &sm, int n) {
   }
 }
 
-__device__ __forceinline__ void copy_row(const uint8_t *src, uint8_t *dst, int lane) {
-  for (int c = lane; c < ROW_CHUNKS; c += 32)
+__device__ __forceinline__ void copy_row(const uint8_t *src, uint8_t *dst, int lane, int bytes) {
+  for (int c = lane; c < bytes / 16; c += 32)
     reinterpret_cast<uint4 *>(dst)[c] = reinterpret_cast<const uint4 *>(src)[c];
+}
+
+// One 656-B latent row held by a warp (lane l: chunk l in v0; lanes 0..8: chunk
+// 32+l in v1 — lane 0 has the four f32 group scales, lanes 1..8 the RoPE) ->
+// the 1152-B f16 slot row.  NoPE: f16(f32(e4m3) * scale), RoPE: f16(bf16) — both
+// single roundings, so the slot row is a pure function of the latent row.
+__device__ __forceinline__ void dequant_row_to_slot(uint4 v0, uint4 v1, int lane, uint8_t *dst) {
+  const float s0 = __uint_as_float(__shfl_sync(0xffffffffu, v1.x, 0));
+  const float s1 = __uint_as_float(__shfl_sync(0xffffffffu, v1.y, 0));
+  const float s2 = __uint_as_float(__shfl_sync(0xffffffffu, v1.z, 0));
+  const float s3 = __uint_as_float(__shfl_sync(0xffffffffu, v1.w, 0));
+  const int g = lane >> 3;
+  const float s = g == 0 ? s0 : g == 1 ? s1 : g == 2 ? s2 : s3;
+  uint4 a, c;
+  a.x = e4m3x2_scaled_f16x2((uint16_t)(v0.x & 0xFFFF), s);
+  a.y = e4m3x2_scaled_f16x2((uint16_t)(v0.x >> 16), s);
+  a.z = e4m3x2_scaled_f16x2((uint16_t)(v0.y & 0xFFFF), s);
+  a.w = e4m3x2_scaled_f16x2((uint16_t)(v0.y >> 16), s);
+  c.x = e4m3x2_scaled_f16x2((uint16_t)(v0.z & 0xFFFF), s);
+  c.y = e4m3x2_scaled_f16x2((uint16_t)(v0.z >> 16), s);
+  c.z = e4m3x2_scaled_f16x2((uint16_t)(v0.w & 0xFFFF), s);
+  c.w = e4m3x2_scaled_f16x2((uint16_t)(v0.w >> 16), s);
+  st_v4(dst + lane * 32, a);
+  st_v4(dst + lane * 32 + 16, c);
+  if (lane >= 1 && lane <= 8) st_v4(dst + 1024 + (lane - 1) * 16, cvt8_bf16_f16(v1));
 }
 
 template <int MODE>
@@ -346,7 +371,7 @@ __global__ void __launch_bounds__(NT, 1)
         int s = sm.slot[i];
         if (s >= 0)
           copy_row(rbase + (int64_t)s * pv.row_bytes,
-                   rbase + (int64_t)(pv.cap_max + i) * pv.row_bytes, lane);
+                   rbase + (int64_t)(pv.cap_max + i) * pv.row_bytes, lane, pv.row_bytes);
       }
     }
     // evict every resident outside keep; the freed slots (ascending) host kept misses
@@ -660,45 +685,47 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
         int j = g - pref[lo];
         int id = miss_ids[(int64_t)lo * stride + j];
         int row = miss_row[(int64_t)lo * stride + j];
-        src[r] = host + ((int64_t)lo * host_stride + id) * rb;
+        src[r] = host + ((int64_t)lo * host_stride + id) * ESS_LATENT_ROW_BYTES;
         dst[r] = pv.rows + ((int64_t)(begin + lo) * pv.rows_per_pool + row) * rb;
       }
     }
+    // all 16-B PCIe loads of the warp's rows in flight first, then dequantise
     uint4 v[GROWS][2];
 #pragma unroll
     for (int r = 0; r < GROWS; r++) {
+      v[r][1] = make_uint4(0, 0, 0, 0);
       if (src[r]) {
         v[r][0] = ld_nc_v4(src[r] + lane * 16);
         if (lane + 32 < ROW_CHUNKS) v[r][1] = ld_nc_v4(src[r] + (lane + 32) * 16);
       }
     }
 #pragma unroll
-    for (int r = 0; r < GROWS; r++) {
-      if (src[r]) {
-        st_v4(dst[r] + lane * 16, v[r][0]);
-        if (lane + 32 < ROW_CHUNKS) st_v4(dst[r] + (lane + 32) * 16, v[r][1]);
-      }
-    }
+    for (int r = 0; r < GROWS; r++)
+      if (src[r]) dequant_row_to_slot(v[r][0], v[r][1], lane, dst[r]);
   }
 }
 
-// generated rows -> host store (D2H through the mapped alias) and their slots
+// generated rows (656-B latent format) -> host store (D2H through the mapped alias)
+// and, dequantised, their slots
 __global__ void write_generated_kernel(PoolView pv, int begin, const int32_t *ids,
                                        const int32_t *m, const int32_t *slot, int stride,
                                        const uint8_t *src, uint8_t *host, int64_t host_stride) {
   const int b = blockIdx.x;
   const int M = m[b];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t rb = pv.row_bytes;
+  constexpr int64_t LB = ESS_LATENT_ROW_BYTES;
   for (int j = warp; j < M; j += blockDim.x / 32) {
     const int id = ids[(int64_t)b * stride + j];
     const int s = slot ? slot[(int64_t)b * stride + j] : -1;
-    const uint8_t *sr = src + ((int64_t)b * stride + j) * rb;
-    for (int c = lane; c < ROW_CHUNKS; c += 32) {
-      uint4 v = reinterpret_cast<const uint4 *>(sr)[c];
-      if (host) st_v4(host + ((int64_t)b * host_stride + id) * rb + c * 16, v);
-      if (s >= 0) st_v4(pv.rows + ((int64_t)(begin + b) * pv.rows_per_pool + s) * rb + c * 16, v);
+    const uint8_t *sr = src + ((int64_t)b * stride + j) * LB;
+    uint4 v0 = reinterpret_cast<const uint4 *>(sr)[lane];
+    uint4 v1 = lane + 32 < ROW_CHUNKS ? reinterpret_cast<const uint4 *>(sr)[lane + 32] : make_uint4(0, 0, 0, 0);
+    if (host) {
+      uint8_t *h = host + ((int64_t)b * host_stride + id) * LB;
+      st_v4(h + lane * 16, v0);
+      if (lane + 32 < ROW_CHUNKS) st_v4(h + (lane + 32) * 16, v1);
     }
+    if (s >= 0) dequant_row_to_slot(v0, v1, lane, pv.rows + ((int64_t)(begin + b) * pv.rows_per_pool + s) * pv.row_bytes);
   }
 }
 
@@ -751,10 +778,12 @@ int ess_pool_create(ess_pool **out, int32_t num_pools, int64_t max_ids, int32_t 
                     int32_t row_bytes, int32_t staging_rows) {
   if (!out || num_pools < 1 || max_ids < 1 || max_ids > 0x7fffffff || cap_max < 1 ||
       cap_max > 0x00ffffff || staging_rows < 0 || row_bytes < 0 ||
-      (row_bytes && row_bytes != ESS_LATENT_ROW_BYTES))
+      (row_bytes && row_bytes != ESS_SLOT_ROW_BYTES))
     return ESS_ERR_ARG;
-  ess_pool *p = (ess_pool *)calloc(1, sizeof(ess_pool));
+  // 64-B alignment for the embedded CUtensorMap
+  ess_pool *p = (ess_pool *)aligned_alloc(64, (sizeof(ess_pool) + 63) & ~size_t(63));
   if (!p) return ESS_ERR_NOMEM;
+  memset(p, 0, sizeof(ess_pool));
   p->P = num_pools;
   p->max_ids = max_ids;
   p->cap_max = cap_max;

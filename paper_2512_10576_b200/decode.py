@@ -82,7 +82,7 @@ class DSADecodeLayer:
         self.cap0 = pool_capacity(sparse_ratio, context_len)
         self.cap_max = pool_capacity(sparse_ratio, self.Lmax)
         staging = topk_k if self.cap0 < topk_k else 0
-        self.pool = PoolSet(B, self.Lmax, self.cap_max, self.cap0, row_bytes=ROW,
+        self.pool = PoolSet(B, self.Lmax, self.cap_max, self.cap0, row_bytes=_lib.SLOT_ROW_BYTES,
                             staging_rows=staging, device=d)
         # drifting queries
         self._zi = torch.randn((B, 64, 128), device=d, generator=g)

@@ -185,7 +185,7 @@ def test_sel_row_and_miss_rows_consistent(ess):
     """sel_row is where every requested id lives after the step; miss_row lists the
     misses' rows in requested order; transient (oversize) ids land in staging."""
     P, cap, K = 4, 1000, 2048
-    pools = ess.PoolSet(P, 8192, cap, cap, row_bytes=656, staging_rows=K)
+    pools = ess.PoolSet(P, 8192, cap, cap, row_bytes=1152, staging_rows=K)
     rng = np.random.default_rng(1)
     sets = _random_sets(rng, P, K, 8192)
     n = np.full(P, K, np.int32)

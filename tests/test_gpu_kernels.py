@@ -5,7 +5,7 @@ Tolerances (stated per north star):
   * indexer: bit-exact in the exact-arithmetic regime (small-integer e4m3 q/k,
     power-of-two w and scales: every product and partial sum is exact in fp32);
     otherwise |err| <= 1e-3 * max|logit| + 1e-5
-  * gather / write-back: byte-exact
+  * gather / write-back: bit-exact (slot row = f16(f32(e4m3) * scale) ++ f16(bf16))
   * sparse MLA: rel-L2 <= 1e-2 and max-abs <= 2e-2 * max|ref| against the fp64
     reference on the same dequantised rows; lse abs <= 1e-2
 """
@@ -102,7 +102,16 @@ def test_indexer_then_topk_exact_regime_end_to_end():
 
 
 # ---------------------------------------------------------------------------- K4
-def test_gather_and_write_back_are_byte_exact():
+def _fill_slots(pools, rows_u8_per_pool, count):
+    """Test setup: write the slot-store (f16) form of 656-B latent rows."""
+    rv = pools.rows_view()
+    for b, rows in enumerate(rows_u8_per_pool):
+        rv[b, :count].copy_(torch.as_tensor(dsa.slot_rows(rows.cpu().numpy()), device="cuda"))
+
+
+def test_gather_and_write_back_are_exact():
+    """K4 reads 656-B rows over the host link and admits them dequantised; the slot
+    row must equal the oracle's f16(f32(e4m3) * scale) ++ f16(bf16) bit for bit."""
     from paper_2512_10576_b200.cache import PoolSet
     from paper_2512_10576_b200.decode import random_latent_rows
     from paper_2512_10576_b200.transfer import HostLatentStore, gather, write_generated
@@ -110,7 +119,7 @@ def test_gather_and_write_back_are_byte_exact():
     store = HostLatentStore(P, ids)
     for p in range(P):
         store.host[p].copy_(random_latent_rows(ids, "cuda"))
-    pools = PoolSet(P, ids, cap, cap, row_bytes=656, staging_rows=0)
+    pools = PoolSet(P, ids, cap, cap, row_bytes=1152, staging_rows=0)
     rng = np.random.default_rng(0)
     sets = np.stack([rng.choice(4000, size=1000, replace=False) for _ in range(P)]).astype(np.int32)
     acc = pools.access(torch.as_tensor(sets, device="cuda"),
@@ -120,8 +129,9 @@ def test_gather_and_write_back_are_byte_exact():
     sel = acc.sel_row.cpu().numpy()
     host = store.host.numpy()
     for p in range(P):
-        np.testing.assert_array_equal(rows[p, sel[p]], host[p, sets[p]])
-    # write-back of generated rows (append) lands in host store and slot
+        want = dsa.slot_rows(host[p, sets[p]])
+        np.testing.assert_array_equal(rows[p, sel[p]].view(np.uint16), want.view(np.uint16))
+    # write-back of generated rows (append) lands in host store and (dequantised) slot
     new = torch.full((P, 1), 4500, dtype=torch.int32, device="cuda")
     one = torch.ones(P, dtype=torch.int32, device="cuda")
     slots = pools.append(new, one)
@@ -130,9 +140,11 @@ def test_gather_and_write_back_are_byte_exact():
     torch.cuda.synchronize()
     rows = pools.rows_view().cpu().numpy()
     s = slots.cpu().numpy()[:, 0]
+    srcn = src.cpu().numpy()
     for p in range(P):
-        np.testing.assert_array_equal(store.host.numpy()[p, 4500], src[p, 0].cpu().numpy())
-        np.testing.assert_array_equal(rows[p, s[p]], src[p, 0].cpu().numpy())
+        np.testing.assert_array_equal(store.host.numpy()[p, 4500], srcn[p, 0])
+        np.testing.assert_array_equal(rows[p, s[p]].view(np.uint16),
+                                      dsa.slot_rows(srcn[p, :1])[0].view(np.uint16))
     pools.check()
     store.close()
 
@@ -144,20 +156,19 @@ def test_sparse_mla_matches_oracle(counts):
     from paper_2512_10576_b200.cache import PoolSet
     from paper_2512_10576_b200.decode import random_latent_rows
     B, cap = len(counts), 4096
-    pools = PoolSet(B, 8192, cap, cap, row_bytes=656)
-    rv = pools.rows_view()
+    pools = PoolSet(B, 8192, cap, cap, row_bytes=1152)
     g = torch.Generator(device="cuda").manual_seed(11)
-    for b in range(B):
-        rv[b, :cap].copy_(random_latent_rows(cap, "cuda", g))
+    lat = [random_latent_rows(cap, "cuda", g) for _ in range(B)]
+    _fill_slots(pools, lat, cap)
     sel = torch.stack([torch.randperm(cap, device="cuda", generator=g)[:2048] for _ in range(B)]).int()
     cnt = torch.tensor(counts, dtype=torch.int32, device="cuda")
     q = (torch.randn((B, 128, 576), device="cuda", generator=g) * 0.5).to(torch.bfloat16)
     out, lse = sparse_mla(pools, q, sel, cnt)
     out, lse = out.float().cpu().numpy(), lse.cpu().numpy()
-    rows = rv.cpu().numpy()
     qf = q.float().cpu().numpy()
     for b, n in enumerate(counts):
-        ref_o, ref_l = dsa.sparse_mla(qf[b], rows[b, sel[b, :n].cpu().numpy()], DEFAULT_SM_SCALE)
+        rows = lat[b].cpu().numpy()[sel[b, :n].cpu().numpy()]
+        ref_o, ref_l = dsa.sparse_mla(qf[b], rows, DEFAULT_SM_SCALE)
         err = out[b] - ref_o
         rel = np.linalg.norm(err) / max(np.linalg.norm(ref_o), 1e-12)
         assert rel <= 1e-2, (b, n, rel)
@@ -171,22 +182,22 @@ def test_sparse_mla_rescale_path():
     from paper_2512_10576_b200.cache import PoolSet
     from paper_2512_10576_b200.decode import random_latent_rows
     B, n = 2, 2048
-    pools = PoolSet(B, 4096, n, n, row_bytes=656)
-    rv = pools.rows_view()
+    pools = PoolSet(B, 4096, n, n, row_bytes=1152)
     g = torch.Generator(device="cuda").manual_seed(2)
+    lat = []
     for b in range(B):
         rows = random_latent_rows(n, "cuda", g)
         # scale rows so later tiles have larger norms -> larger scores
         sc = rows[:, 512:528].clone().view(torch.float32) * torch.linspace(0.2, 3.0, n, device="cuda")[:, None]
         rows[:, 512:528] = sc.view(torch.uint8)
-        rv[b, :n].copy_(rows)
+        lat.append(rows)
+    _fill_slots(pools, lat, n)
     sel = torch.arange(n, dtype=torch.int32, device="cuda").repeat(B, 1).contiguous()
     cnt = torch.full((B,), n, dtype=torch.int32, device="cuda")
     q = (torch.randn((B, 128, 576), device="cuda", generator=g) * 2).to(torch.bfloat16)
     out, lse = sparse_mla(pools, q, sel, cnt, sm_scale=0.2)
-    rows = rv.cpu().numpy()
     for b in range(B):
-        ref_o, ref_l = dsa.sparse_mla(q[b].float().cpu().numpy(), rows[b, :n], 0.2)
+        ref_o, ref_l = dsa.sparse_mla(q[b].float().cpu().numpy(), lat[b].cpu().numpy(), 0.2)
         o = out[b].float().cpu().numpy()
         assert np.linalg.norm(o - ref_o) / np.linalg.norm(ref_o) <= 1e-2
         # scores reach ~70 here; f16 K rows carry 2^-11 relative rounding, so the
