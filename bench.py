@@ -36,7 +36,6 @@ CONFIGS = {
 }
 TOPK = 2048
 METRIC = "decode tokens/s/GPU at 32K/128K ctx, latent cache offloaded; H2D gather GB/s"
-LAUNCHES_PER_STEP = 8  # indexer, topk, access, gather, sparse_mla, grow, append, write_generated
 
 
 def measured_peaks():
@@ -192,35 +191,51 @@ def host_link_peak_gbs(device, nbytes=1 << 28):
     return best
 
 
-def time_steps(layer, inputs, new_rows, steps, timers=None):
-    """Run `steps` decode steps; per-kernel CUDA events when `timers` is given."""
+def run_steps(layer, inputs, new_rows, overlap, counts=None):
+    """The product decode step: layer.attend (K1..K5, micro-batched overlap) + append."""
+    for t, (q_idx, q) in enumerate(inputs):
+        layer.attend(q_idx, q, gather_ctas=layer.gather_ctas, overlap=overlap)
+        layer.append_token(new_rows=new_rows[t])
+        if counts is not None:
+            counts.append(layer.step_counts().clone())
+
+
+def kernel_breakdown(layer, inputs, new_rows):
+    """Sequential steps with CUDA events around every kernel of the path (one stream,
+    no overlap): per-kernel device time for the roofline and the gather GB/s."""
     import torch
     from paper_2512_10576_b200.attention import sparse_mla
     from paper_2512_10576_b200.indexer import indexer_logits, topk
     from paper_2512_10576_b200.transfer import gather
-    for t in range(steps):
-        q_idx, q = inputs[t]
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)] if timers is not None else None
-        if ev: ev[0].record()
+    names = ["indexer", "topk", "cache", "gather", "sparse_mla", "append"]
+    evs, counts = [], []
+    for t, (q_idx, q) in enumerate(inputs):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+        ev[0].record()
         indexer_logits(q_idx, layer.w, layer.k_cache, layer.k_scale, layer.lens, out=layer.logits)
-        if ev: ev[1].record()
+        ev[1].record()
         topk(layer.logits, layer.lens, layer.K, out=layer.idx, count=layer.cnt)
-        if ev: ev[2].record()
-        layer.acc = layer.pool.access(layer.idx, layer.cnt, out=layer.acc)
-        if ev: ev[3].record()
-        gather(layer.pool, layer.store, layer.acc, max_ctas=layer.gather_ctas)
-        if ev: ev[4].record()
-        sparse_mla(layer.pool, q, layer.acc.sel_row, layer.cnt, layer.sm_scale, out=layer.out, lse=layer.lse)
-        if ev: ev[5].record()
+        ev[2].record()
+        acc = layer.pool.access(layer.idx, layer.cnt)
+        ev[3].record()
+        gather(layer.pool, layer.store, acc, max_ctas=layer.gather_ctas)
+        ev[4].record()
+        sparse_mla(layer.pool, q, acc.sel_row, layer.cnt, layer.sm_scale, out=layer.out, lse=layer.lse)
+        ev[5].record()
         layer.append_token(new_rows=new_rows[t])
-        if timers is not None:
-            timers.append((ev, layer.acc.counts.clone()))
+        ev[6].record()
+        evs.append(ev)
+        counts.append(acc.counts.clone())
+    torch.cuda.synchronize()
+    ms = {n: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / len(evs) for i, n in enumerate(names)}
+    return ms, torch.stack(counts)
 
 
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
     from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows
+    from paper_2512_10576_b200.dp import aggregate
 
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -230,8 +245,9 @@ def run_ours(args, cfg):
         dist.init_process_group("nccl", device_id=dev)
     peaks, peak_kind = measured_peaks()
     B, L, rho = cfg["batch"], cfg["context_len"], cfg["sparse_ratio"]
-    total = args.warmup + args.steps
-    layer = DSADecodeLayer(B, L, rho, TOPK, max_new_tokens=args.warmup + 2 * args.steps + 8, device=dev,
+    W, K, NB = args.warmup, args.steps, args.breakdown_steps
+    total = W + K + NB
+    layer = DSADecodeLayer(B, L, rho, TOPK, max_new_tokens=total + K + 16, device=dev,
                            seed=1234 + rank, drift=args.drift)
     layer.gather_ctas = args.gather_ctas
     layer.prefill_warmup(windows=32)
@@ -239,40 +255,38 @@ def run_ours(args, cfg):
     new_rows = [random_latent_rows(B, dev, layer.gen).view(B, 1, 656) for _ in range(total)]
     torch.cuda.synchronize()
 
-    # warm-up steps (untimed)
-    time_steps(layer, inputs[:args.warmup], new_rows[:args.warmup], args.warmup)
+    # warm-up (untimed): capture the whole step as one CUDA graph (its first, eager
+    # execution is a real step), then W-1 graph replays
+    layer.capture(args.overlap, args.gather_ctas)
+    for t in range(1, W):
+        layer.step(inputs[t][0], inputs[t][1], new_rows[t])
     torch.cuda.synchronize()
+    layer.counter_acc.zero_()
     if world > 1:
         dist.barrier()
-    # timed region: K steps, device clock (CUDA events), per-kernel events inside
-    timers = []
+    # timed region: K product steps (graph replays incl. input copies), device clock
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev) as clocks:
         torch.cuda.synchronize()
         start.record()
-        time_steps(layer, inputs[args.warmup:], new_rows[args.warmup:], args.steps, timers)
+        for t in range(W, W + K):
+            layer.step(inputs[t][0], inputs[t][1], new_rows[t])
         end.record()
         torch.cuda.synchronize()
-    step_ms = start.elapsed_time(end) / args.steps
+    if world > 1:
+        dist.barrier()
+    step_ms = start.elapsed_time(end) / K
     layer.pool.check("bench")
-    from paper_2512_10576_b200.dp import aggregate
-    tokens_total, t_max = aggregate(B * args.steps, step_ms * args.steps / 1e3, device=dev)
+    tokens_total, t_max = aggregate(B * K, step_ms * K / 1e3, device=dev)
     value = tokens_total / t_max
+    hits, misses = layer.counter_acc[:2].tolist()
 
-    # per-kernel breakdown + gather bytes
-    names = ["indexer", "topk", "cache", "gather", "sparse_mla"]
-    ktimes = {n: 0.0 for n in names}
-    misses = hits = 0
-    for ev, counts in timers:
-        for i, n in enumerate(names):
-            ktimes[n] += ev[i].elapsed_time(ev[i + 1])
-        c = counts.sum(0).tolist()
-        hits, misses = hits + c[0], misses + c[1]
-    ktimes = {n: v / args.steps for n, v in ktimes.items()}
-    lens_mean = L + args.warmup + (args.steps - 1) / 2
+    # per-kernel breakdown (sequential, separate steps) for the roofline
+    ktimes, bcounts = kernel_breakdown(layer, inputs[W + K:], new_rows[W + K:])
+    lens_mean = L + W + K + (NB - 1) / 2
     idx_bytes = B * lens_mean * (132 + 4) + B * (64 * 128 + 64 * 4)
     achieved = idx_bytes / (ktimes["indexer"] * 1e-3) / 1e9
-    gather_bytes = misses * 656 / args.steps
+    gather_bytes = bcounts[:, :, 1].sum().item() * 656 / NB
     link_peak = host_link_peak_gbs(dev) if rank == 0 else None
     traffic = None
     tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
@@ -282,35 +296,32 @@ def run_ours(args, cfg):
 
     # e2e: through the public API with host buffers: H2D of the step's queries from pinned
     # memory, the step, D2H of the attention output, every step
-    h_in = [(qi.cpu().pin_memory(), q.cpu().pin_memory()) for qi, q in inputs[args.warmup:]]
+    h_in = [(qi.cpu().pin_memory(), q.cpu().pin_memory()) for qi, q in inputs[W:W + K]]
     h_out = torch.empty(layer.out.shape, dtype=layer.out.dtype).pin_memory()
-    e2e_layer_inputs = []
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for t in range(args.steps):
-        qi = h_in[t][0].to(dev, non_blocking=True)
-        q = h_in[t][1].to(dev, non_blocking=True)
-        time_steps(layer, [(qi, q)], [new_rows[args.warmup + t]], 1)
+    for t in range(K):
+        layer.step(h_in[t][0], h_in[t][1], new_rows[W + t])  # H2D into the graph inputs
         h_out.copy_(layer.out, non_blocking=True)
     e1.record()
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / args.steps
-    e2e_tok, e2e_t = aggregate(B * args.steps, e2e_ms * args.steps / 1e3, device=dev)
+    e2e_ms = e0.elapsed_time(e1) / K
+    e2e_tok, e2e_t = aggregate(B * K, e2e_ms * K / 1e3, device=dev)
     h2d = h_in[0][0].numel() + h_in[0][1].numel() * 2
     d2h = h_out.numel() * 2
-    del e2e_layer_inputs
 
     line = None
     if rank == 0:
         cpu_v, cpu_sample, cpu_threads = cpu_reference_rate(cfg, budget_s=12.0)
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_max * 1e3 / args.steps,
+            "steps": K, "warmup": W, "ms_per_step": t_max * 1e3 / K,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "e4m3/f16/f32",
             "data": "synthetic (random-weight DeepSeek-V3.2-Exp DSA shapes, drifting queries)",
             "config": {"workload": cfg["workload"], "layers": 1, "batch_per_gpu": B,
                        "context_len": L, "sparse_ratio": rho, "topk": TOPK, "query_drift": args.drift,
+                       "overlap": args.overlap,
                        "parallelism": f"dp{world} (requests sharded, no collective)",
                        "l2": "inputs larger than L2 (indexer keys + slot pool > 600 MB/GPU)"},
             "e2e": {"value": e2e_tok / e2e_t, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
@@ -321,7 +332,8 @@ def run_ours(args, cfg):
                          "algorithmic_bytes_per_launch": idx_bytes},
             "cpu_baseline": {"value": cpu_v, "unit": "tokens/s", "cores": cpu_threads, "kind": "port",
                              "sample": cpu_sample},
-            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "gpu_launches": (9 if args.overlap == "da" else 8) * K,
+            "cuda_graph": True,
             "clocks": clocks.summary(),
             "kernels_ms": ktimes,
             "gather": {"bytes_per_step": gather_bytes,
@@ -329,7 +341,7 @@ def run_ours(args, cfg):
                        "host_link_peak_gbs": link_peak,
                        "paper_flashtrans_gbs": 37.0},
             "hit_rate": hits / max(1, hits + misses),
-            "misses_per_request_step": misses / (B * args.steps),
+            "misses_per_request_step": misses / (B * K),
         }
     if args.ceiling and world == 1:
         line["all_hbm_ceiling"] = run_ceiling(args, cfg, dev)
@@ -364,18 +376,23 @@ def run_ceiling(args, cfg, dev):
         gather(layer.pool, layer.store, AccessBatch(cnt, None, ids, slots.contiguous()), max_ctas=148)
     inputs = [layer.next_queries() for _ in range(total)]
     new_rows = [random_latent_rows(B, dev, layer.gen).view(B, 1, 656) for _ in range(total)]
-    time_steps(layer, inputs[:args.warmup], new_rows[:args.warmup], args.warmup)
+    layer.capture("none", args.gather_ctas)  # nothing to gather
+    for t in range(1, args.warmup):
+        layer.step(inputs[t][0], inputs[t][1], new_rows[t])
     torch.cuda.synchronize()
+    layer.counter_acc.zero_()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    time_steps(layer, inputs[args.warmup:], new_rows[args.warmup:], args.steps)
+    for t in range(args.warmup, total):
+        layer.step(inputs[t][0], inputs[t][1], new_rows[t])
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
-    hr = layer.acc.counts[:, 0].sum().item() / max(1, layer.cnt.sum().item())
+    c = layer.counter_acc.tolist()
     layer.pool.check("ceiling")
     layer.close()
-    return {"value": B / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms, "hit_rate": hr}
+    return {"value": B / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms,
+            "hit_rate": c[0] / max(1, c[0] + c[1])}
 
 
 def main():
@@ -387,6 +404,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--drift", type=float, default=0.97)
     ap.add_argument("--gather-ctas", type=int, default=32)
+    ap.add_argument("--overlap", default="da", choices=["da", "none"])
+    ap.add_argument("--breakdown-steps", type=int, default=5)
     ap.add_argument("--no-ceiling", dest="ceiling", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:

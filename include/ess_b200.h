@@ -93,13 +93,15 @@ int ess_pool_warmup(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d
  *   d_hit_ids, d_miss_ids   in requested order (cache.py:98-99)
  *   d_evicted_ids           ascending if flags & ESS_ACCESS_SORT_EVICTED
  *   d_sel_row               slot-store row of every requested id (attention input)
+ *   d_hit_row               row of every hit, in hit order (attention over the
+ *                           resident rows while the misses are in flight)
  *   d_miss_row              destination row of every miss (gather input)
  *   d_counts [num][4]       nhit, nmiss (= h2d_blocks), nevicted, ntransient      */
 int ess_pool_access(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_req,
                     const int32_t *d_n, int32_t req_stride, int32_t *d_hit_ids,
                     int32_t *d_miss_ids, int32_t *d_evicted_ids, int32_t *d_sel_row,
-                    int32_t *d_miss_row, int32_t *d_counts, int32_t out_stride, int32_t flags,
-                    void *stream);
+                    int32_t *d_hit_row, int32_t *d_miss_row, int32_t *d_counts,
+                    int32_t out_stride, int32_t flags, void *stream);
 /* admit generated ids at top recency; d_slot_out [num][stride] gets each id's
  * slot (may be NULL)                                     (SparsePool.append_generated) */
 int ess_pool_append(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_ids,
@@ -127,10 +129,12 @@ int ess_pool_info(ess_pool *pool, int32_t *num_pools, int64_t *max_ids, int32_t 
 /* copies every miss row host_rows[pool][miss_id] -> slot store[pool][miss_row]
  * with 16-B loads through the device alias of registered host memory.  Pool i
  * of the range reads host rows at d_host_rows + i*host_pool_stride_rows*656. */
+#define ESS_GATHER_EXCLUSIVE_SM 1        /* run only on SMs no attention CTA occupies */
+#define ESS_GATHER_EXCLUSIVE_SMEM (64 * 1024)
 int ess_gather(ess_pool *pool, int32_t begin, int32_t num, const void *d_host_rows,
                int64_t host_pool_stride_rows, const int32_t *d_miss_ids,
                const int32_t *d_miss_row, const int32_t *d_counts, int32_t stride,
-               int32_t max_ctas, void *stream);
+               int32_t max_ctas, int32_t flags, void *stream);
 /* D2H write-back + slot fill of generated rows (cache.py:122-134):
  * src rows [num][stride][656] -> host_rows[pool][id] and slot store[pool][slot] */
 int ess_write_generated(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_ids,
@@ -152,14 +156,23 @@ int ess_indexer_logits(const void *d_q, const float *d_w, const void *d_k,
 int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
              int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count, void *stream);
 
-/* ---- K5 sparse MLA decode (op "sparse_mla") ------------------------------------ */
-/* out[b][h] = softmax_j(q[b][h] . K[j] * sm_scale) V[j] over the d_count[b] rows
- * sel_row[b][0:count) of pool (pool_begin + b)'s slot store; K = dequant NoPE ++
- * RoPE (576), V = dequant NoPE (512).  q [B][128][576] bf16, out [B][128][512]
- * bf16, lse [B][128] f32 (natural log).                                          */
+/* ---- K5 sparse MLA decode (ops "sparse_mla" + "merge_attn") --------------------- */
+/* out[b][h] = softmax_j(q[b][h] . K[j] * sm_scale) V[j] over the rows
+ * sel_row[b][0:count) (count = d_count[b * count_stride]) of pool (pool_begin + b)'s
+ * slot store; K = NoPE ++ RoPE (576), V = NoPE (512).  q [B][128][576] bf16,
+ * out [B][128][512] bf16, lse [B][128] f32 (natural log).
+ * The paper's split attention is two calls sharing a workspace
+ * (d_ws_o [B][128][512] f32, d_ws_ml [B][128][2] f32):
+ *   ESS_MLA_PARTIAL  write the unnormalised state (O, running max, sum) to the
+ *                    workspace instead of out/lse            (Attn0: resident rows)
+ *   ESS_MLA_RESUME   start from the workspace state and finish (Attn1: fetched rows
+ *                    + the merge)                                                   */
+#define ESS_MLA_PARTIAL 1
+#define ESS_MLA_RESUME 2
 int ess_sparse_mla(ess_pool *pool, int32_t pool_begin, const void *d_q,
                    const int32_t *d_sel_row, int32_t sel_stride, const int32_t *d_count,
-                   int32_t batch, float sm_scale, void *d_out, float *d_lse, void *stream);
+                   int32_t count_stride, int32_t batch, float sm_scale, void *d_out,
+                   float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags, void *stream);
 
 #ifdef __cplusplus
 }

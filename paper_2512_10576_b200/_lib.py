@@ -27,7 +27,7 @@ SIGNATURES = {
     "ess_pool_reset": ([V, I32, I32, V, V], ctypes.c_int),
     "ess_pool_grow": ([V, I32, I32, V, V], ctypes.c_int),
     "ess_pool_warmup": ([V, I32, I32, V, V, I32, V, V], ctypes.c_int),
-    "ess_pool_access": ([V, I32, I32, V, V, I32, V, V, V, V, V, V, I32, I32, V], ctypes.c_int),
+    "ess_pool_access": ([V, I32, I32, V, V, I32, V, V, V, V, V, V, V, I32, I32, V], ctypes.c_int),
     "ess_pool_append": ([V, I32, I32, V, V, I32, V, V], ctypes.c_int),
     "ess_pool_lru_order": ([V, I32, I32, V, V, V], ctypes.c_int),
     "ess_pool_counters": ([V, I32, I32, V, V], ctypes.c_int),
@@ -35,17 +35,19 @@ SIGNATURES = {
     "ess_pool_copy_state": ([V, I32, V, I32, I32, V], ctypes.c_int),
     "ess_pool_status": ([V, PI32], ctypes.c_int),
     "ess_pool_info": ([V, PI32, PI64, PI32, PI32, PI64, PV], ctypes.c_int),
-    "ess_gather": ([V, I32, I32, V, I64, V, V, V, I32, I32, V], ctypes.c_int),
+    "ess_gather": ([V, I32, I32, V, I64, V, V, V, I32, I32, I32, V], ctypes.c_int),
     "ess_write_generated": ([V, I32, I32, V, V, V, I32, V, V, I64, V], ctypes.c_int),
     "ess_indexer_logits": ([V, V, V, V, V, I32, I64, V, V], ctypes.c_int),
     "ess_topk": ([V, I64, V, I32, I32, V, I32, V, V], ctypes.c_int),
-    "ess_sparse_mla": ([V, I32, V, V, I32, V, I32, F32, V, V, V], ctypes.c_int),
+    "ess_sparse_mla": ([V, I32, V, V, I32, V, I32, I32, F32, V, V, V, V, I32, V], ctypes.c_int),
 }
 
 ESS_OK = 0
 ESS_ERR_CAPACITY, ESS_ERR_SHRINK, ESS_ERR_DUPLICATE = -1, -2, -3
 ESS_ERR_NOMEM, ESS_ERR_RATIO, ESS_ERR_ARG, ESS_ERR_CUDA, ESS_ERR_CLOCK = -4, -5, -6, -7, -8
 ESS_ACCESS_SORT_EVICTED = 1
+ESS_MLA_PARTIAL, ESS_MLA_RESUME = 1, 2
+ESS_GATHER_EXCLUSIVE_SM = 1
 MAX_REQUEST = 2048
 LATENT_ROW_BYTES = 656   # host store / transfer format (e4m3 NoPE + scales + bf16 RoPE)
 SLOT_ROW_BYTES = 1152    # GPU slot store format (576 x f16, dequantised on admission)

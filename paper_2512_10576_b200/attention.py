@@ -1,5 +1,8 @@
-"""Sparse MLA decode (K5) over the GPU slot store — the operator the reference
-reduces to ``op_time("sparse_mla", ...)`` (costmodel.py:18-27, pipeline.py:217-218).
+"""Sparse MLA decode (K5) over the GPU slot store — the operators the reference
+reduces to ``op_time("sparse_mla" | "merge_attn", ...)`` (costmodel.py:18-27,
+pipeline.py:217-219) and the DA split (Attn0 on resident rows while the misses
+are fetched, Attn1 on the fetched rows, merge; PAPER.md:350-352,
+pipeline.py:125-141).
 """
 
 from __future__ import annotations
@@ -18,24 +21,43 @@ V_DIM = 512
 DEFAULT_SM_SCALE = 1.0 / math.sqrt(192.0)
 
 
+class SplitWorkspace:
+    """Carry-over state between the two attention passes: unnormalised O (f32) and
+    the running (max, sum) per head."""
+
+    def __init__(self, batch: int, device):
+        self.o = torch.empty((batch, HEADS, V_DIM), dtype=torch.float32, device=device)
+        self.ml = torch.empty((batch, HEADS, 2), dtype=torch.float32, device=device)
+
+
 def sparse_mla(pool: PoolSet, q: torch.Tensor, sel_row: torch.Tensor, count: torch.Tensor,
                sm_scale: float = DEFAULT_SM_SCALE, pool_begin: int = 0,
-               out: torch.Tensor | None = None, lse: torch.Tensor | None = None):
+               out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
+               workspace: SplitWorkspace | None = None, mode: str = "full"):
     """out[b, h] = softmax_j(q[b, h] . K_j * sm_scale) V_j over rows sel_row[b, :count[b]]
     of pool (pool_begin + b)'s slot store.
 
-    q [B, 128, 576] bf16; returns (out [B, 128, 512] bf16, lse [B, 128] f32, natural log).
+    q [B, 128, 576] bf16; ``count`` may be a strided view (e.g. AccessBatch.counts[:, 0]).
+    mode "full" returns (out [B, 128, 512] bf16, lse [B, 128] f32, natural log);
+    "partial" stores the unnormalised state into ``workspace`` (Attn0); "resume"
+    continues from it over further rows and returns the merged result (Attn1 + merge).
     """
     _lib.require_cuda(q)
     B = q.shape[0]
     if q.shape != (B, HEADS, QK_DIM) or q.dtype != torch.bfloat16:
         raise ValueError("q must be [B, 128, 576] bfloat16")
-    if out is None:
-        out = torch.empty((B, HEADS, V_DIM), dtype=torch.bfloat16, device=q.device)
-    if lse is None:
-        lse = torch.empty((B, HEADS), dtype=torch.float32, device=q.device)
+    flags = {"full": 0, "partial": _lib.ESS_MLA_PARTIAL, "resume": _lib.ESS_MLA_RESUME}[mode]
+    if flags and workspace is None:
+        raise ValueError(f"mode {mode!r} needs a SplitWorkspace")
+    if mode != "partial":
+        if out is None:
+            out = torch.empty((B, HEADS, V_DIM), dtype=torch.bfloat16, device=q.device)
+        if lse is None:
+            lse = torch.empty((B, HEADS), dtype=torch.float32, device=q.device)
+    ws_o = _lib.ptr(workspace.o) if workspace is not None else None
+    ws_ml = _lib.ptr(workspace.ml) if workspace is not None else None
     _lib.check(_lib.load().ess_sparse_mla(
         pool.handle, pool_begin, q.data_ptr(), sel_row.data_ptr(), sel_row.stride(0),
-        count.data_ptr(), B, float(sm_scale), out.data_ptr(), lse.data_ptr(),
-        _lib.stream_handle()), "ess_sparse_mla")
+        count.data_ptr(), count.stride(0), B, float(sm_scale), _lib.ptr(out), _lib.ptr(lse),
+        ws_o, ws_ml, flags, _lib.stream_handle()), "ess_sparse_mla")
     return out, lse

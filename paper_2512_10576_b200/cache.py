@@ -48,6 +48,7 @@ class AccessBatch:
     miss_row: torch.Tensor | None   # [num, K] destination row of each miss
     hit_ids: torch.Tensor | None = None
     evicted_ids: torch.Tensor | None = None
+    hit_row: torch.Tensor | None = None  # [num, K] row of each hit (resident before the step)
 
 
 def _i32(x, device) -> torch.Tensor:
@@ -137,21 +138,23 @@ class PoolSet:
 
     def access(self, req: torch.Tensor, n: torch.Tensor, begin: int = 0, lists: bool = False,
                sort_evicted: bool = True, out: AccessBatch | None = None) -> AccessBatch:
-        """One selection set per pool.  Hot path: counts, sel_row, miss ids/rows.
-        ``lists=True`` also returns hit ids and evicted ids (API/tests)."""
+        """One selection set per pool.  Hot path: counts, sel_row, hit rows, miss
+        ids/rows.  ``lists=True`` also returns hit ids and evicted ids (API/tests)."""
         num, K = req.shape
         self._range(begin, num)
         if out is None:
             z = lambda: torch.empty((num, K), dtype=torch.int32, device=self.device)  # noqa: E731
             out = AccessBatch(counts=torch.empty((num, 4), dtype=torch.int32, device=self.device),
-                              sel_row=z(), miss_ids=z(), miss_row=z(),
+                              sel_row=z(), miss_ids=z(), miss_row=z(), hit_row=z(),
                               hit_ids=z() if lists else None, evicted_ids=z() if lists else None)
         flags = _lib.ESS_ACCESS_SORT_EVICTED if sort_evicted else 0
+        stride = next(t.stride(0) for t in (out.sel_row, out.miss_ids, out.miss_row, out.hit_row,
+                                            out.hit_ids, out.evicted_ids, req) if t is not None)
         _lib.check(self._L.ess_pool_access(
             self._h, begin, num, req.data_ptr(), n.data_ptr(), req.stride(0),
             _lib.ptr(out.hit_ids), _lib.ptr(out.miss_ids), _lib.ptr(out.evicted_ids),
-            _lib.ptr(out.sel_row), _lib.ptr(out.miss_row), out.counts.data_ptr(),
-            K, flags, _lib.stream_handle()))
+            _lib.ptr(out.sel_row), _lib.ptr(out.hit_row), _lib.ptr(out.miss_row),
+            out.counts.data_ptr(), stride, flags, _lib.stream_handle()))
         return out
 
     def append(self, ids: torch.Tensor, m: torch.Tensor, begin: int = 0,

@@ -98,8 +98,9 @@ __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_
 __global__ void __launch_bounds__(NTHREADS, 1)
     sparse_mla_kernel(const uint8_t *__restrict__ rows, const uint16_t *__restrict__ q,
                       int64_t rows_per_pool, int pool_begin, const int32_t *__restrict__ sel_row,
-                      int sel_stride, const int32_t *__restrict__ counts, float sm_scale,
-                      uint16_t *__restrict__ out, float *__restrict__ lse) {
+                      int sel_stride, const int32_t *__restrict__ counts, int count_stride,
+                      float sm_scale, uint16_t *__restrict__ out, float *__restrict__ lse,
+                      float *__restrict__ ws_o, float *__restrict__ ws_ml, int flags) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sq = smem;                        // q dims 384..575, 3 SW128 blocks
@@ -109,7 +110,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int v = blockIdx.x;  // output half
   const int b = blockIdx.y;
-  const int n = min(counts[b], MAX_N);
+  const int n = min(counts[(int64_t)b * count_stride], MAX_N);
+  const bool partial = flags & ESS_MLA_PARTIAL, resume = flags & ESS_MLA_RESUME;
   const int ntiles = (n + NB - 1) / NB;
   const uint16_t *qb = q + (int64_t)b * HEADS * QK_DIM;
 
@@ -174,7 +176,27 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // ---------------- softmax / epilogue warps: thread = head --------------------
     const int h = warp * 32 + lane;
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const int64_t hrow = (int64_t)b * HEADS + h;
+    float *wso = ws_o ? ws_o + hrow * ESS_MLA_V_DIM + v * V_HALF : nullptr;
     float m_run = -INFINITY, l_run = 0.f;
+    if (resume) {  // continue from pass 1: running max / sum and this CTA's O half
+      m_run = ws_ml[hrow * 2 + 0];
+      l_run = ws_ml[hrow * 2 + 1];
+#pragma unroll 1
+      for (int cc = 0; cc < V_HALF / 32; cc++) {
+        uint32_t o[32];
+#pragma unroll
+        for (int j = 0; j < 32; j += 4) {
+          float4 f = *reinterpret_cast<const float4 *>(wso + cc * 32 + j);
+          o[j] = __float_as_uint(f.x);
+          o[j + 1] = __float_as_uint(f.y);
+          o[j + 2] = __float_as_uint(f.z);
+          o[j + 3] = __float_as_uint(f.w);
+        }
+        tmem_st_32x32b_x32(tmem + lane_base + TM_O + cc * 32, o);
+      }
+      tmem_st_wait();
+    }
     for (int i = 0; i < ntiles; i++) {
       const int sb = i & 1;
       mbar_wait(&c.s_full[sb], (i >> 1) & 1);
@@ -189,16 +211,20 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         x[j] = (i * NB + j < n) ? __uint_as_float(s[j]) * scale_log2 : -INFINITY;
         mt = fmaxf(mt, x[j]);
       }
-      // PV(i-1) must be done before O is rescaled
-      mbar_wait(&c.p_empty, (i & 1) ^ 1);
-      tc_fence_after();
       // warp-uniform decision (tcgen05.ld/st are .sync.aligned); a lane whose own
       // max did not grow rescales by alpha = 1
-      if (__any_sync(0xffffffffu, mt > m_run + RESCALE_THRESHOLD) || i == 0) {
+      if (__any_sync(0xffffffffu, mt > m_run + RESCALE_THRESHOLD) || (i == 0 && !resume)) {
         const float m_new = fmaxf(mt, m_run);
         const float alpha = exp2f(m_run - m_new);  // 0 when m_run = -inf
         l_run *= alpha;
-        if (i > 0) {
+        if (i > 0 || resume) {
+          // O holds PV(i-1) (or the resumed state): wait for it, then rescale.  P(i)
+          // itself goes to the other S buffer, so without a rescale there is nothing
+          // to wait for; the barrier is never more than one phase ahead here.
+          if (i > 0) {
+            mbar_wait(&c.p_empty, (i & 1) ^ 1);
+            tc_fence_after();
+          }
 #pragma unroll 1
           for (int cc = 0; cc < V_HALF / 32; cc++) {
             uint32_t o[32];
@@ -228,35 +254,62 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&c.p_full);
     }
-    // ---------------- final normalisation ---------------------------------------
-    uint16_t *ob = out + ((int64_t)b * HEADS + h) * ESS_MLA_V_DIM + v * V_HALF;
+    // ---------------- epilogue ---------------------------------------------------
+    const bool have_o = ntiles > 0 || resume;  // TMEM O holds a valid accumulator
     if (ntiles > 0) {
       mbar_wait(&c.o_done, 0);
       tc_fence_after();
-      const float inv = 1.f / l_run;
+    }
+    if (partial) {
+      // pass 1 of the split attention: unnormalised O and (max, sum) to the workspace
 #pragma unroll 1
       for (int cc = 0; cc < V_HALF / 32; cc++) {
         uint32_t o[32];
-        tmem_ld_32x32b_x32(tmem + lane_base + TM_O + cc * 32, o);
-        tmem_ld_wait();
+        if (have_o) {
+          tmem_ld_32x32b_x32(tmem + lane_base + TM_O + cc * 32, o);
+          tmem_ld_wait();
+        } else {
 #pragma unroll
-        for (int j = 0; j < 32; j += 8) {
-          uint4 pk;
-          __nv_bfloat162 t0 = __floats2bfloat162_rn(__uint_as_float(o[j]) * inv, __uint_as_float(o[j + 1]) * inv);
-          __nv_bfloat162 t1 = __floats2bfloat162_rn(__uint_as_float(o[j + 2]) * inv, __uint_as_float(o[j + 3]) * inv);
-          __nv_bfloat162 t2 = __floats2bfloat162_rn(__uint_as_float(o[j + 4]) * inv, __uint_as_float(o[j + 5]) * inv);
-          __nv_bfloat162 t3 = __floats2bfloat162_rn(__uint_as_float(o[j + 6]) * inv, __uint_as_float(o[j + 7]) * inv);
-          pk.x = *reinterpret_cast<uint32_t *>(&t0);
-          pk.y = *reinterpret_cast<uint32_t *>(&t1);
-          pk.z = *reinterpret_cast<uint32_t *>(&t2);
-          pk.w = *reinterpret_cast<uint32_t *>(&t3);
-          *reinterpret_cast<uint4 *>(ob + cc * 32 + j) = pk;
+          for (int j = 0; j < 32; j++) o[j] = 0u;
         }
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4 *>(wso + cc * 32 + j) =
+              make_float4(__uint_as_float(o[j]), __uint_as_float(o[j + 1]),
+                          __uint_as_float(o[j + 2]), __uint_as_float(o[j + 3]));
       }
-      if (v == 0) lse[(int64_t)b * HEADS + h] = (m_run + log2f(l_run)) * 0.6931471805599453f;
+      if (v == 0) {
+        ws_ml[hrow * 2 + 0] = m_run;
+        ws_ml[hrow * 2 + 1] = l_run;
+      }
     } else {
-      for (int j = 0; j < V_HALF; j += 8) *reinterpret_cast<uint4 *>(ob + j) = make_uint4(0, 0, 0, 0);
-      if (v == 0) lse[(int64_t)b * HEADS + h] = -INFINITY;
+      uint16_t *ob = out + hrow * ESS_MLA_V_DIM + v * V_HALF;
+      if (have_o && l_run > 0.f) {
+        const float inv = 1.f / l_run;
+#pragma unroll 1
+        for (int cc = 0; cc < V_HALF / 32; cc++) {
+          uint32_t o[32];
+          tmem_ld_32x32b_x32(tmem + lane_base + TM_O + cc * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            uint4 pk;
+            __nv_bfloat162 t0 = __floats2bfloat162_rn(__uint_as_float(o[j]) * inv, __uint_as_float(o[j + 1]) * inv);
+            __nv_bfloat162 t1 = __floats2bfloat162_rn(__uint_as_float(o[j + 2]) * inv, __uint_as_float(o[j + 3]) * inv);
+            __nv_bfloat162 t2 = __floats2bfloat162_rn(__uint_as_float(o[j + 4]) * inv, __uint_as_float(o[j + 5]) * inv);
+            __nv_bfloat162 t3 = __floats2bfloat162_rn(__uint_as_float(o[j + 6]) * inv, __uint_as_float(o[j + 7]) * inv);
+            pk.x = *reinterpret_cast<uint32_t *>(&t0);
+            pk.y = *reinterpret_cast<uint32_t *>(&t1);
+            pk.z = *reinterpret_cast<uint32_t *>(&t2);
+            pk.w = *reinterpret_cast<uint32_t *>(&t3);
+            *reinterpret_cast<uint4 *>(ob + cc * 32 + j) = pk;
+          }
+        }
+        if (v == 0) lse[hrow] = (m_run + log2f(l_run)) * 0.6931471805599453f;
+      } else {
+        for (int j = 0; j < V_HALF; j += 8) *reinterpret_cast<uint4 *>(ob + j) = make_uint4(0, 0, 0, 0);
+        if (v == 0) lse[hrow] = -INFINITY;
+      }
     }
   } else if (warp == MMA_WARP) {
     // ---------------- MMA issuer --------------------------------------------------
@@ -298,7 +351,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < NB / 16; kk++) {
           uint64_t bd = sw128_desc(vaddr + kk * 16 * 128, KV_BLK_BYTES, 1024);
-          mma_f16_ts(tmem + TM_O, tmem + TM_S + sb * NB + kk * 8, bd, IDESC_PV, (i | kk) ? 1u : 0u);
+          mma_f16_ts(tmem + TM_O, tmem + TM_S + sb * NB + kk * 8, bd, IDESC_PV,
+                     (i | kk) || resume ? 1u : 0u);
         }
         tc_commit(&c.p_empty);
         tc_commit(&c.kv_empty[kb]);
@@ -358,10 +412,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
 extern "C" int ess_sparse_mla(ess_pool *pool, int32_t pool_begin, const void *d_q,
                               const int32_t *d_sel_row, int32_t sel_stride, const int32_t *d_count,
-                              int32_t batch, float sm_scale, void *d_out, float *d_lse,
+                              int32_t count_stride, int32_t batch, float sm_scale, void *d_out,
+                              float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags,
                               void *stream) {
+  if ((flags & (ESS_MLA_PARTIAL | ESS_MLA_RESUME)) && (!d_ws_o || !d_ws_ml)) return ESS_ERR_ARG;
+  if ((flags & ESS_MLA_PARTIAL) && (flags & ESS_MLA_RESUME)) return ESS_ERR_ARG;
   if (!pool || !pool->rows || pool->row_bytes != ESS_SLOT_ROW_BYTES || !d_q || !d_sel_row ||
-      !d_count || !d_out || !d_lse || batch < 0 || pool_begin < 0 ||
+      !d_count || count_stride < 1 || (!(flags & ESS_MLA_PARTIAL) && (!d_out || !d_lse)) ||
+      batch < 0 || pool_begin < 0 ||
       (int64_t)pool_begin + batch > pool->P || sel_stride < 1 ||
       (reinterpret_cast<uintptr_t>(d_q) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15))
     return ESS_ERR_ARG;
@@ -375,7 +433,8 @@ extern "C" int ess_sparse_mla(ess_pool *pool, int32_t pool_begin, const void *d_
   dim3 grid(2, batch);
   sparse_mla_kernel<<<grid, NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
       pool->rows, (const uint16_t *)d_q, pool->rows_per_pool, pool_begin, d_sel_row,
-      sel_stride, d_count, sm_scale, (uint16_t *)d_out, d_lse);
+      sel_stride, d_count, count_stride, sm_scale, (uint16_t *)d_out, d_lse, d_ws_o, d_ws_ml,
+      flags);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }

@@ -172,7 +172,8 @@ __global__ void __launch_bounds__(NT, 1)
     pool_step_kernel(PoolView pv, int begin, const int32_t *__restrict__ req,
                      const int32_t *__restrict__ req_n, int req_stride, int32_t *hit_out,
                      int32_t *miss_out, int32_t *ev_out, int32_t *sel_row_out,
-                     int32_t *miss_row_out, int32_t *counts_out, int out_stride, int flags,
+                     int32_t *hit_row_out, int32_t *miss_row_out, int32_t *counts_out,
+                     int out_stride, int flags,
                      int64_t *inserted_out) {
   __shared__ StepSmem sm;
   const int t = threadIdx.x;
@@ -433,6 +434,13 @@ __global__ void __launch_bounds__(NT, 1)
       for (int e = 0; e < EPT; e++) {
         int i = t * EPT + e;
         if (i < n) sel_row_out[out_base + i] = sm.slot[i];
+      }
+    }
+    if (hit_row_out) {  // rows already resident before this step (attention pass 1)
+#pragma unroll
+      for (int e = 0; e < EPT; e++) {
+        int i = t * EPT + e;
+        if (i < n && hflag[e]) hit_row_out[out_base + hrank[e]] = sm.slot[i];
       }
     }
     if (ev_out) {
@@ -868,7 +876,7 @@ int ess_pool_warmup(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_id
   if (num == 0) return ESS_OK;
   pool_step_kernel<MODE_WARMUP><<<num, NT, 0, (cudaStream_t)stream>>>(
       view(p), begin, d_ids, d_n, stride, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-      0, 0, d_inserted);
+      nullptr, 0, 0, d_inserted);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }
@@ -876,16 +884,16 @@ int ess_pool_warmup(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_id
 int ess_pool_access(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_req,
                     const int32_t *d_n, int32_t req_stride, int32_t *d_hit_ids,
                     int32_t *d_miss_ids, int32_t *d_evicted_ids, int32_t *d_sel_row,
-                    int32_t *d_miss_row, int32_t *d_counts, int32_t out_stride, int32_t flags,
-                    void *stream) {
+                    int32_t *d_hit_row, int32_t *d_miss_row, int32_t *d_counts,
+                    int32_t out_stride, int32_t flags, void *stream) {
   if (!range_ok(p, begin, num) || !d_req || !d_n || req_stride < 0) return ESS_ERR_ARG;
-  if ((d_hit_ids || d_miss_ids || d_evicted_ids || d_sel_row || d_miss_row) &&
+  if ((d_hit_ids || d_miss_ids || d_evicted_ids || d_sel_row || d_hit_row || d_miss_row) &&
       out_stride < 1)
     return ESS_ERR_ARG;
   if (num == 0) return ESS_OK;
   pool_step_kernel<MODE_ACCESS><<<num, NT, 0, (cudaStream_t)stream>>>(
       view(p), begin, d_req, d_n, req_stride, d_hit_ids, d_miss_ids, d_evicted_ids, d_sel_row,
-      d_miss_row, d_counts, out_stride, flags, nullptr);
+      d_hit_row, d_miss_row, d_counts, out_stride, flags, nullptr);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }
@@ -966,12 +974,18 @@ int ess_pool_copy_state(ess_pool *dst, int32_t dst_begin, ess_pool *src, int32_t
 int ess_gather(ess_pool *p, int32_t begin, int32_t num, const void *d_host_rows,
                int64_t host_pool_stride_rows, const int32_t *d_miss_ids,
                const int32_t *d_miss_row, const int32_t *d_counts, int32_t stride,
-               int32_t max_ctas, void *stream) {
+               int32_t max_ctas, int32_t flags, void *stream) {
   if (!range_ok(p, begin, num) || !p->rows || !d_host_rows || !d_miss_ids || !d_miss_row ||
       !d_counts || stride < 1 || max_ctas < 1)
     return ESS_ERR_ARG;
   if (num == 0) return ESS_OK;
   size_t smem = sizeof(int) * (num + 1);
+  // ESS_GATHER_EXCLUSIVE_SM: reserve enough shared memory that a gather CTA can never
+  // share an SM with a K5 CTA (~205 KB), so the long-latency host-link loads do not
+  // compete with attention for the SM's L1 miss tracking — the gather runs on the SMs
+  // attention leaves idle.
+  if ((flags & ESS_GATHER_EXCLUSIVE_SM) && smem < ESS_GATHER_EXCLUSIVE_SMEM)
+    smem = ESS_GATHER_EXCLUSIVE_SMEM;
   if (smem > 48 * 1024) {
     ESS_CUDA_TRY(cudaFuncSetAttribute(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));

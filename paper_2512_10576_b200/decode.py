@@ -28,8 +28,8 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _lib
-from .attention import DEFAULT_SM_SCALE, sparse_mla
-from .cache import PoolSet, pool_capacity
+from .attention import DEFAULT_SM_SCALE, SplitWorkspace, sparse_mla
+from .cache import AccessBatch, PoolSet, pool_capacity
 from .indexer import indexer_logits, topk
 from .transfer import HostLatentStore, gather, write_generated
 
@@ -131,14 +131,122 @@ class DSADecodeLayer:
         return rec
 
     # -- the decode step -------------------------------------------------------------------
-    def attend(self, q_idx, q, gather_ctas: int = 32):
-        """K1..K5 for every request of the layer."""
-        indexer_logits(q_idx, self.w, self.k_cache, self.k_scale, self.lens, out=self.logits)
-        topk(self.logits, self.lens, self.K, out=self.idx, count=self.cnt)
-        self.acc = self.pool.access(self.idx, self.cnt, out=self.acc)
-        gather(self.pool, self.store, self.acc, max_ctas=gather_ctas)
-        sparse_mla(self.pool, q, self.acc.sel_row, self.cnt, self.sm_scale, out=self.out, lse=self.lse)
+    def _select(self, q_idx, a, b):
+        """K1 -> K2 -> K3 for requests [a, b) on the current stream, writing into the
+        step's shared access buffers (row slices)."""
+        indexer_logits(q_idx[a:b], self.w[a:b], self.k_cache[a:b], self.k_scale[a:b],
+                       self.lens[a:b], out=self.logits[a:b])
+        topk(self.logits[a:b], self.lens[a:b], self.K, out=self.idx[a:b], count=self.cnt[a:b])
+        acc = self.acc
+        view = AccessBatch(counts=acc.counts[a:b], sel_row=acc.sel_row[a:b],
+                           miss_ids=acc.miss_ids[a:b], miss_row=acc.miss_row[a:b],
+                           hit_row=acc.hit_row[a:b])
+        return self.pool.access(self.idx[a:b], self.cnt[a:b], begin=a, out=view)
+
+    def attend(self, q_idx, q, gather_ctas: int = 32, overlap: str = "da"):
+        """K1..K5 for every request of the layer.
+
+        overlap="da" is the paper's DA schedule (the reference
+        models it as span DAGs, pipeline.py:125-141): right after the cache manager,
+        the host-link miss gather (K4) runs on a high-priority side stream while
+        attention pass 1 (Attn0) runs over the rows that were already resident; pass 2
+        (Attn1) resumes the online softmax over the fetched rows once the gather lands
+        — the merge is the resume itself.  overlap="none" runs K4 then one K5 pass.
+        """
+        B = self.B
+        if self.acc is None:
+            z = lambda: torch.empty((B, self.K), dtype=torch.int32, device=self.device)  # noqa: E731
+            self.acc = AccessBatch(counts=torch.empty((B, 4), dtype=torch.int32, device=self.device),
+                                   sel_row=z(), miss_ids=z(), miss_row=z(), hit_row=z())
+        self._select(q_idx, 0, B)
+        acc = self.acc
+        if overlap == "none":
+            gather(self.pool, self.store, acc, max_ctas=gather_ctas)
+            sparse_mla(self.pool, q, acc.sel_row, self.cnt, self.sm_scale, out=self.out, lse=self.lse)
+            return self.out, self.lse
+        if overlap != "da":
+            raise ValueError(f"unknown overlap schedule {overlap!r}")
+        main = torch.cuda.current_stream(self.device)
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(self.device, priority=-1)
+            self._ws = SplitWorkspace(B, self.device)
+        side = self._side
+        ready = torch.cuda.Event()
+        ready.record(main)
+        side.wait_event(ready)
+        with torch.cuda.stream(side):
+            # attention takes 2 CTAs per request (one SM each); the gather gets the rest
+            free_sms = torch.cuda.get_device_properties(self.device).multi_processor_count - 2 * B
+            gather(self.pool, self.store, acc, max_ctas=max(8, free_sms), exclusive=True)
+        done = torch.cuda.Event()
+        done.record(side)
+        sparse_mla(self.pool, q, acc.hit_row, acc.counts[:, 0], self.sm_scale,
+                   workspace=self._ws, mode="partial")
+        main.wait_event(done)
+        sparse_mla(self.pool, q, acc.miss_row, acc.counts[:, 1], self.sm_scale, out=self.out,
+                   lse=self.lse, workspace=self._ws, mode="resume")
         return self.out, self.lse
+
+    # -- whole-step CUDA graph ------------------------------------------------------------
+    def _append_device(self, new_rows: torch.Tensor) -> None:
+        """append_token with every per-step scalar derived on the device: the new id is
+        each request's history length and the capacity floor(rho * (history + 1))
+        (cache.py:137-138, :191-195) — float64, bit-identical to math.floor."""
+        B = self.B
+        self._ids.copy_(self.lens.view(B, 1))
+        self._caps.copy_(torch.floor(self.lens.double().add(1).mul(self.rho)).clamp_min(1).to(torch.int32))
+        self.pool.grow(self._caps)
+        slots = self.pool.append(self._ids, self._one)
+        write_generated(self.pool, self.store, self._ids, self._one, slots, new_rows)
+        self.lens += 1
+
+    def _device_step(self, overlap: str, gather_ctas: int) -> None:
+        self.attend(self.q_idx_in, self.q_in, gather_ctas=gather_ctas, overlap=overlap)
+        self.counter_acc += self.step_counts().sum(0, dtype=torch.int64)
+        self._append_device(self.rows_in)
+
+    def capture(self, overlap: str = "da", gather_ctas: int = 32) -> None:
+        """Record one full decode step (K1..K5 for every micro-batch, the side-stream
+        gathers, grow/append/write-back) as a CUDA graph; ``step`` replays it.  The
+        first (eager) step also runs here — it advances the state like any step."""
+        B, d = self.B, self.device
+        self.q_idx_in = torch.empty((B, 64, 128), dtype=torch.uint8, device=d)
+        self.q_in = torch.empty((B, 128, 576), dtype=torch.bfloat16, device=d)
+        self.rows_in = torch.zeros((B, 1, ROW), dtype=torch.uint8, device=d)
+        self._ids = torch.empty((B, 1), dtype=torch.int32, device=d)
+        self._one = torch.ones(B, dtype=torch.int32, device=d)
+        self._caps = torch.empty(B, dtype=torch.int32, device=d)
+        self.counter_acc = torch.zeros(4, dtype=torch.int64, device=d)
+        q_idx, q = self.next_queries()
+        self.q_idx_in.copy_(q_idx)
+        self.q_in.copy_(q)
+        s = torch.cuda.Stream(d)
+        s.wait_stream(torch.cuda.current_stream(d))
+        with torch.cuda.stream(s):
+            self._device_step(overlap, gather_ctas)  # eager: sets up attrs / maps
+        torch.cuda.current_stream(d).wait_stream(s)
+        torch.cuda.synchronize(d)
+        eager_counts = self.step_counts().clone()
+        self.history += 1
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._device_step(overlap, gather_ctas)
+        self.counter_acc.zero_()
+        return eager_counts  # access counts of the eager step (graph buffers are unwritten)
+
+    def step(self, q_idx: torch.Tensor, q: torch.Tensor, new_rows: torch.Tensor):
+        """One decode step through the captured graph: inputs land in the graph's
+        static buffers (two device copies), then a single graph launch."""
+        self.q_idx_in.copy_(q_idx, non_blocking=True)
+        self.q_in.copy_(q, non_blocking=True)
+        self.rows_in.copy_(new_rows, non_blocking=True)
+        self.graph.replay()
+        self.history += 1
+        return self.out, self.lse
+
+    def step_counts(self) -> torch.Tensor:
+        """[B, 4] access counts of the last step (hits, misses, evicted, transient)."""
+        return self.acc.counts
 
     def append_token(self, new_rows: torch.Tensor | None = None, new_keys: torch.Tensor | None = None):
         """Each request admits its generated token (cache.py:191-195 order: grow, append)."""
@@ -146,12 +254,14 @@ class DSADecodeLayer:
         pos = self.history
         self.history += 1
         self.pool.grow(pool_capacity(self.rho, self.history))
-        ids = torch.full((B, 1), pos, dtype=torch.int32, device=d)
-        one = torch.ones(B, dtype=torch.int32, device=d)
-        slots = self.pool.append(ids, one)
+        if getattr(self, "_ids", None) is None:
+            self._ids = torch.empty((B, 1), dtype=torch.int32, device=d)
+            self._one = torch.ones(B, dtype=torch.int32, device=d)
+        self._ids.fill_(pos)
+        slots = self.pool.append(self._ids, self._one)
         if new_rows is None:
             new_rows = random_latent_rows(B, d, self.gen).view(B, 1, ROW)
-        write_generated(self.pool, self.store, ids, one, slots, new_rows)
+        write_generated(self.pool, self.store, self._ids, self._one, slots, new_rows)
         if new_keys is not None:
             self.k_cache[:, pos] = new_keys
         self.lens += 1

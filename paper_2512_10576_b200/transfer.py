@@ -99,14 +99,18 @@ class HostLatentStore:
 
 
 def gather(pool: PoolSet, store: HostLatentStore, acc: AccessBatch, begin: int = 0,
-           store_begin: int | None = None, max_ctas: int = 32, stream=None) -> None:
-    """Copy every miss row host[pool][miss_id] -> slot store[pool][miss_row] (K4)."""
+           store_begin: int | None = None, max_ctas: int = 32, exclusive: bool = False,
+           stream=None) -> None:
+    """Copy every miss row host[pool][miss_id] -> slot store[pool][miss_row] (K4),
+    dequantising to the slot format on the way.  ``exclusive`` keeps the gather off
+    SMs that run attention CTAs (overlapped schedule)."""
     num = acc.counts.shape[0]
     sb = begin if store_begin is None else store_begin
+    flags = _lib.ESS_GATHER_EXCLUSIVE_SM if exclusive else 0
     _lib.check(_lib.load().ess_gather(
         pool.handle, begin, num, store.pool_ptr(sb), store.rows_per_pool,
         acc.miss_ids.data_ptr(), acc.miss_row.data_ptr(), acc.counts.data_ptr(),
-        acc.miss_ids.stride(0), max_ctas, _lib.stream_handle(stream)), "ess_gather")
+        acc.miss_ids.stride(0), max_ctas, flags, _lib.stream_handle(stream)), "ess_gather")
 
 
 def write_generated(pool: PoolSet, store: HostLatentStore, ids: torch.Tensor, m: torch.Tensor,

@@ -30,7 +30,7 @@ def test_decode_layer_matches_oracle_chain(ctx, rho):
         torch.cuda.synchronize()
         logits = layer.logits.cpu().numpy()
         idx, cnt = layer.idx.cpu().numpy(), layer.cnt.cpu().numpy()
-        counts = layer.acc.counts.cpu().numpy()
+        counts = layer.step_counts().cpu().numpy()
         host = layer.store.host.numpy()
         o_all, l_all = out.float().cpu().numpy(), lse.cpu().numpy()
         qf = q.float().cpu().numpy()
@@ -53,4 +53,55 @@ def test_decode_layer_matches_oracle_chain(ctx, rho):
     out, cnt = layer.pool.lru_order()
     for b in range(B):
         assert out[b, :int(cnt[b])].tolist() == orc[b].lru_order()
+    layer.close()
+
+
+def test_graph_step_with_overlap_matches_oracle_chain():
+    """The product step — two micro-batches, gathers on a side stream, whole step
+    captured as a CUDA graph, history/capacity computed on device — stays bit-exact
+    on selections and cache accounting and within tolerance on attention."""
+    from paper_2512_10576_b200.cache import pool_capacity
+    from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows
+    B, K, ctx, rho = 4, 2048, 8192, 0.25
+    layer = DSADecodeLayer(B, ctx, rho, K, max_new_tokens=12, seed=3, drift=0.97)
+    windows = layer.prefill_warmup(windows=6, record=True)
+    orc = [olru.OraclePool(pool_capacity(rho, ctx)) for _ in range(B)]
+    for w in windows:
+        for b in range(B):
+            orc[b].warmup([w[b].tolist()])
+    hist = ctx
+
+    def mirror(check_attention, q=None, counts=None):
+        nonlocal hist
+        torch.cuda.synchronize()
+        logits = layer.logits.cpu().numpy()
+        idx, cnt = layer.idx.cpu().numpy(), layer.cnt.cpu().numpy()
+        counts = (layer.step_counts() if counts is None else counts).cpu().numpy()
+        host = layer.store.host.numpy()
+        for b in range(B):
+            want = dsa.topk_indices(logits[b], hist, K)
+            np.testing.assert_array_equal(idx[b, :cnt[b]], want)
+            r = orc[b].access_step(want.tolist())
+            assert counts[b, 0] == len(r.hit_ids) and counts[b, 1] == len(r.miss_ids)
+            if check_attention:
+                ref_o, ref_l = dsa.sparse_mla(q[b].float().cpu().numpy(), host[b, want], layer.sm_scale)
+                o = layer.out[b].float().cpu().numpy()
+                assert np.linalg.norm(o - ref_o) / np.linalg.norm(ref_o) <= 1e-2
+        hist += 1
+        for o in orc:
+            o.grow_capacity(pool_capacity(rho, hist))
+            o.append_generated([hist - 1])
+
+    eager = layer.capture(overlap="da")       # runs one eager step first
+    mirror(False, counts=eager)
+    for _ in range(3):
+        q_idx, q = layer.next_queries()
+        rows = random_latent_rows(B, "cuda", layer.gen).view(B, 1, 656)
+        layer.step(q_idx, q, rows)
+        mirror(True, q)
+    layer.pool.check()
+    out, cnt = layer.pool.lru_order()
+    for b in range(B):
+        assert out[b, :int(cnt[b])].tolist() == orc[b].lru_order()
+    assert int(layer.lens[0]) == hist
     layer.close()

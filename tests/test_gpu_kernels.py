@@ -204,3 +204,35 @@ def test_sparse_mla_rescale_path():
         # log-sum-exp tolerance is relative at this scale
         got_l = lse[b].cpu().numpy()
         assert (np.abs(got_l - ref_l) <= 1e-2 + 1e-3 * np.abs(ref_l)).all()
+
+
+@pytest.mark.parametrize("split", [(1900, 148), (0, 300), (2048, 0), (5, 1)])
+def test_split_attention_partial_then_resume(split):
+    """DA split: Attn0 over one row set -> workspace, Attn1 resumes
+    over the other set = attention over the union (merge_attn semantics)."""
+    from paper_2512_10576_b200.attention import SplitWorkspace, sparse_mla, DEFAULT_SM_SCALE
+    from paper_2512_10576_b200.cache import PoolSet
+    from paper_2512_10576_b200.decode import random_latent_rows
+    n1, n2 = split
+    B, cap = 3, 4096
+    pools = PoolSet(B, 8192, cap, cap, row_bytes=1152)
+    g = torch.Generator(device="cuda").manual_seed(17)
+    lat = [random_latent_rows(cap, "cuda", g) for _ in range(B)]
+    _fill_slots(pools, lat, cap)
+    perm = torch.stack([torch.randperm(cap, device="cuda", generator=g)[:n1 + n2] for _ in range(B)]).int()
+    rows1 = torch.zeros((B, 2048), dtype=torch.int32, device="cuda")
+    rows2 = torch.zeros((B, 2048), dtype=torch.int32, device="cuda")
+    rows1[:, :n1] = perm[:, :n1]
+    rows2[:, :n2] = perm[:, n1:]
+    counts = torch.tensor([[n1, n2, 0, 0]] * B, dtype=torch.int32, device="cuda")
+    q = (torch.randn((B, 128, 576), device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    ws = SplitWorkspace(B, "cuda")
+    sparse_mla(pools, q, rows1, counts[:, 0], workspace=ws, mode="partial")
+    out, lse = sparse_mla(pools, q, rows2, counts[:, 1], workspace=ws, mode="resume")
+    out, lse = out.float().cpu().numpy(), lse.cpu().numpy()
+    for b in range(B):
+        rows = lat[b].cpu().numpy()[perm[b].cpu().numpy()]
+        ref_o, ref_l = dsa.sparse_mla(q[b].float().cpu().numpy(), rows, DEFAULT_SM_SCALE)
+        rel = np.linalg.norm(out[b] - ref_o) / max(np.linalg.norm(ref_o), 1e-12)
+        assert rel <= 1e-2, (split, b, rel)
+        assert np.abs(lse[b] - ref_l).max() <= 1e-2
