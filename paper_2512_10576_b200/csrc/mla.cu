@@ -211,20 +211,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         x[j] = (i * NB + j < n) ? __uint_as_float(s[j]) * scale_log2 : -INFINITY;
         mt = fmaxf(mt, x[j]);
       }
+      // PV(i-1) accumulates into O: wait for it before O may be rescaled.  Waited on
+      // every tile so each p_empty phase has exactly one waiter (synccheck-clean).
+      if (i > 0) {
+        mbar_wait(&c.p_empty, (i & 1) ^ 1);
+        tc_fence_after();
+      }
       // warp-uniform decision (tcgen05.ld/st are .sync.aligned); a lane whose own
       // max did not grow rescales by alpha = 1
       if (__any_sync(0xffffffffu, mt > m_run + RESCALE_THRESHOLD) || (i == 0 && !resume)) {
         const float m_new = fmaxf(mt, m_run);
         const float alpha = exp2f(m_run - m_new);  // 0 when m_run = -inf
         l_run *= alpha;
-        if (i > 0 || resume) {
-          // O holds PV(i-1) (or the resumed state): wait for it, then rescale.  P(i)
-          // itself goes to the other S buffer, so without a rescale there is nothing
-          // to wait for; the barrier is never more than one phase ahead here.
-          if (i > 0) {
-            mbar_wait(&c.p_empty, (i & 1) ^ 1);
-            tc_fence_after();
-          }
+        if (i > 0 || resume) {  // O holds PV(i-1) or the resumed state
 #pragma unroll 1
           for (int cc = 0; cc < V_HALF / 32; cc++) {
             uint32_t o[32];
