@@ -202,32 +202,40 @@ def run_steps(layer, inputs, new_rows, overlap, counts=None):
 
 def kernel_breakdown(layer, inputs, new_rows):
     """Sequential steps with CUDA events around every kernel of the path (one stream,
-    no overlap): per-kernel device time for the roofline and the gather GB/s."""
+    no overlap): per-kernel device time for the roofline and the gather GB/s.  Each
+    timed kernel is preceded by a GPU sleep so host launch latency never leaks into
+    the events (the GPU is always behind the host)."""
     import torch
     from paper_2512_10576_b200.attention import sparse_mla
     from paper_2512_10576_b200.indexer import indexer_logits, topk
     from paper_2512_10576_b200.transfer import gather
     names = ["indexer", "topk", "cache", "gather", "sparse_mla", "append"]
-    evs, counts = [], []
+    ms = {n: 0.0 for n in names}
+    counts = []
+    acc = None
+
+    def timed(name, fn):
+        torch.cuda._sleep(2_000_000)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        r = fn()
+        e1.record()
+        timed.ev.append((name, e0, e1))
+        return r
+    timed.ev = []
     for t, (q_idx, q) in enumerate(inputs):
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
-        ev[0].record()
-        indexer_logits(q_idx, layer.w, layer.k_cache, layer.k_scale, layer.lens, out=layer.logits)
-        ev[1].record()
-        topk(layer.logits, layer.lens, layer.K, out=layer.idx, count=layer.cnt)
-        ev[2].record()
-        acc = layer.pool.access(layer.idx, layer.cnt)
-        ev[3].record()
-        gather(layer.pool, layer.store, acc, max_ctas=layer.gather_ctas)
-        ev[4].record()
-        sparse_mla(layer.pool, q, acc.sel_row, layer.cnt, layer.sm_scale, out=layer.out, lse=layer.lse)
-        ev[5].record()
-        layer.append_token(new_rows=new_rows[t])
-        ev[6].record()
-        evs.append(ev)
+        timed("indexer", lambda: indexer_logits(q_idx, layer.w, layer.k_cache, layer.k_scale,
+                                                layer.lens, out=layer.logits))
+        timed("topk", lambda: topk(layer.logits, layer.lens, layer.K, out=layer.idx, count=layer.cnt))
+        acc = timed("cache", lambda: layer.pool.access(layer.idx, layer.cnt, out=acc))
+        timed("gather", lambda: gather(layer.pool, layer.store, acc, max_ctas=layer.gather_ctas))
+        timed("sparse_mla", lambda: sparse_mla(layer.pool, q, acc.sel_row, layer.cnt, layer.sm_scale,
+                                               out=layer.out, lse=layer.lse))
+        timed("append", lambda: layer._append_device(new_rows[t]))  # the graph's device-side append
         counts.append(acc.counts.clone())
     torch.cuda.synchronize()
-    ms = {n: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / len(evs) for i, n in enumerate(names)}
+    for name, e0, e1 in timed.ev:
+        ms[name] += e0.elapsed_time(e1) / len(inputs)
     return ms, torch.stack(counts)
 
 
@@ -294,22 +302,23 @@ def run_ours(args, cfg):
         with open(tfile) as f:
             traffic = json.load(f).get("indexer_dram_bytes_per_launch")
 
-    # e2e: through the public API with host buffers: H2D of the step's queries from pinned
-    # memory, the step, D2H of the attention output, every step
+    # e2e: through the public API with host buffers: every step copies its queries H2D
+    # from pinned memory and its attention output D2H (layer.step_host: copy stream,
+    # double-buffered staging, so transfers of step t overlap compute of t-1 / t+1)
     h_in = [(qi.cpu().pin_memory(), q.cpu().pin_memory()) for qi, q in inputs[W:W + K]]
-    h_out = torch.empty(layer.out.shape, dtype=layer.out.dtype).pin_memory()
+    h_out = [torch.empty(layer.out.shape, dtype=layer.out.dtype).pin_memory() for _ in range(K)]
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for t in range(K):
-        layer.step(h_in[t][0], h_in[t][1], new_rows[W + t])  # H2D into the graph inputs
-        h_out.copy_(layer.out, non_blocking=True)
+        layer.step_host(h_in[t][0], h_in[t][1], new_rows[W + t], h_out[t])
+    layer._ds.synchronize()
     e1.record()
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1) / K
     e2e_tok, e2e_t = aggregate(B * K, e2e_ms * K / 1e3, device=dev)
     h2d = h_in[0][0].numel() + h_in[0][1].numel() * 2
-    d2h = h_out.numel() * 2
+    d2h = h_out[0].numel() * 2
 
     line = None
     if rank == 0:

@@ -106,6 +106,15 @@ int ess_pool_access(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d
  * slot (may be NULL)                                     (SparsePool.append_generated) */
 int ess_pool_append(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_ids,
                     const int32_t *d_m, int32_t stride, int32_t *d_slot_out, void *stream);
+/* the decode step's tail in one launch (cache.py:191-195, :137-138, :122-134): per pool,
+ * with h = d_hist[i] (history length) and m = d_m ? d_m[i] : 1 generated tokens:
+ * grow capacity to max(1, floor(rho * (h + m))), admit ids h..h+m-1 at top recency
+ * (LRU evictions counted), write each 656-B source row (d_src_rows [num][src_stride])
+ * to the host store (D2H) and, dequantised, to its slot; d_hist[i] += m.              */
+int ess_pool_admit(ess_pool *pool, int32_t begin, int32_t num, int32_t *d_hist,
+                   const int32_t *d_m, double rho, const void *d_src_rows, int32_t src_stride,
+                   void *d_host_rows, int64_t host_pool_stride_rows, int32_t *d_slot_out,
+                   void *stream);
 /* least- to most-recent resident ids: d_out [num][cap_max], d_count [num]
  *                                                 (SparsePool.lru_order, cache.py:55-57) */
 int ess_pool_lru_order(ess_pool *pool, int32_t begin, int32_t num, int32_t *d_out,

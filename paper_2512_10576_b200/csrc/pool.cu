@@ -737,6 +737,84 @@ __global__ void write_generated_kernel(PoolView pv, int begin, const int32_t *id
   }
 }
 
+// The decode step's tail for one pool in one launch (cache.py:191-195 order): grow the
+// capacity to max(1, floor(rho * (h + m))) (cache.py:137-138, f64 as in Python), admit
+// the m generated ids h..h+m-1 at top recency (evicting LRU, counted; cache.py:122-134),
+// write each new 656-B row back to the host store (D2H) and, dequantised,
+// into its slot, and advance the history h (the request's length) by m.
+__global__ void __launch_bounds__(NTA) pool_admit_kernel(PoolView pv, int begin, int32_t *hist,
+                                                        const int32_t *m_arr, double rho,
+                                                        const uint8_t *src, int src_stride,
+                                                        uint8_t *host, int64_t host_stride,
+                                                        int32_t *slot_out) {
+  __shared__ unsigned long long red[NTA / 32 + 1];
+  __shared__ int slots[64];
+  const int b = blockIdx.x, p = begin + b;
+  PoolMeta *meta = pv.meta + p;
+  int32_t *slot_of = pv.slot_of + (int64_t)p * pv.max_ids;
+  int32_t *slot_id = pv.slot_id + (int64_t)p * pv.cap_max;
+  uint32_t *key = pv.key + (int64_t)p * pv.cap_max;
+  const int h = hist[b];
+  const int M = m_arr ? m_arr[b] : 1;
+  const int64_t want = (int64_t)floor(rho * (double)(h + M));
+  const int newcap = (int)(want < 1 ? 1 : want);
+  int code = 0;
+  if (M < 0 || M > 64 || (int64_t)h + M > pv.max_ids) code = ESS_ERR_ARG;
+  else if (newcap < meta->cap) code = ESS_ERR_SHRINK;
+  else if (newcap > pv.cap_max) code = ESS_ERR_CAPACITY;
+  else if ((int64_t)h <= meta->watermark) code = ESS_ERR_DUPLICATE;
+  if (code) {
+    if (threadIdx.x == 0) ess_set_status(pv.status, code);
+    return;
+  }
+  const int cap = newcap;
+  int size = meta->size;
+  uint32_t clk = meta->clk;
+  int64_t evictions = 0;
+  for (int i = 0; i < M; i++) {
+    int s;
+    if (size >= cap) {  // LRU resident -> evicted; its slot takes the new id
+      s = argmin_key(key, cap, red);
+      if (threadIdx.x == 0) slot_of[slot_id[s]] = -1;
+      evictions++;
+    } else {            // smallest free slot (free keys == slot index < any stamp)
+      s = argmin_key(key, cap, red);
+      size++;
+    }
+    if (threadIdx.x == 0) {
+      slot_of[h + i] = s;
+      slot_id[s] = h + i;
+      key[s] = clk;
+      slots[i] = s;
+    }
+    clk++;
+    __syncthreads();
+  }
+  // rows: host write-back + dequantised slot fill, one warp per row
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = warp; i < M; i += NTA / 32) {
+    const uint8_t *sr = src + ((int64_t)b * src_stride + i) * ESS_LATENT_ROW_BYTES;
+    uint4 v0 = reinterpret_cast<const uint4 *>(sr)[lane];
+    uint4 v1 = lane + 32 < ROW_CHUNKS ? reinterpret_cast<const uint4 *>(sr)[lane + 32] : make_uint4(0, 0, 0, 0);
+    if (host) {
+      uint8_t *hp = host + ((int64_t)b * host_stride + h + i) * ESS_LATENT_ROW_BYTES;
+      st_v4(hp + lane * 16, v0);
+      if (lane + 32 < ROW_CHUNKS) st_v4(hp + (lane + 32) * 16, v1);
+    }
+    if (pv.rows)
+      dequant_row_to_slot(v0, v1, lane, pv.rows + ((int64_t)p * pv.rows_per_pool + slots[i]) * pv.row_bytes);
+    if (slot_out && lane == 0) slot_out[(int64_t)b * src_stride + i] = slots[i];
+  }
+  if (threadIdx.x == 0) {
+    meta->cap = cap;
+    meta->size = size;
+    meta->clk = clk;
+    meta->watermark = h + M - 1 > meta->watermark ? h + M - 1 : meta->watermark;
+    meta->evictions += evictions;
+    hist[b] = h + M;
+  }
+}
+
 __global__ void pool_lookup_kernel(PoolView pv, int p, const int32_t *ids, int n, int32_t *out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -993,6 +1071,20 @@ int ess_gather(ess_pool *p, int32_t begin, int32_t num, const void *d_host_rows,
   gather_kernel<<<max_ctas, NTG, smem, (cudaStream_t)stream>>>(
       view(p), begin, num, (const uint8_t *)d_host_rows, host_pool_stride_rows, d_miss_ids,
       d_miss_row, d_counts, stride);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+int ess_pool_admit(ess_pool *p, int32_t begin, int32_t num, int32_t *d_hist, const int32_t *d_m,
+                   double rho, const void *d_src_rows, int32_t src_stride, void *d_host_rows,
+                   int64_t host_pool_stride_rows, int32_t *d_slot_out, void *stream) {
+  if (!range_ok(p, begin, num) || !d_hist || !d_src_rows || src_stride < 1 || !(rho > 0.0) ||
+      rho > 1.0)
+    return rho > 0.0 && rho <= 1.0 ? ESS_ERR_ARG : ESS_ERR_RATIO;
+  if (num == 0) return ESS_OK;
+  pool_admit_kernel<<<num, NTA, 0, (cudaStream_t)stream>>>(
+      view(p), begin, d_hist, d_m, rho, (const uint8_t *)d_src_rows, src_stride,
+      (uint8_t *)d_host_rows, host_pool_stride_rows, d_slot_out);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }

@@ -192,13 +192,10 @@ class DSADecodeLayer:
         """append_token with every per-step scalar derived on the device: the new id is
         each request's history length and the capacity floor(rho * (history + 1))
         (cache.py:137-138, :191-195) — float64, bit-identical to math.floor."""
-        B = self.B
-        self._ids.copy_(self.lens.view(B, 1))
-        self._caps.copy_(torch.floor(self.lens.double().add(1).mul(self.rho)).clamp_min(1).to(torch.int32))
-        self.pool.grow(self._caps)
-        slots = self.pool.append(self._ids, self._one)
-        write_generated(self.pool, self.store, self._ids, self._one, slots, new_rows)
-        self.lens += 1
+        _lib.check(_lib.load().ess_pool_admit(
+            self.pool.handle, 0, self.B, self.lens.data_ptr(), None, float(self.rho),
+            new_rows.data_ptr(), new_rows.stride(0) // ROW, self.store.pool_ptr(0),
+            self.store.rows_per_pool, None, _lib.stream_handle()), "ess_pool_admit")
 
     def _device_step(self, overlap: str, gather_ctas: int) -> None:
         self.attend(self.q_idx_in, self.q_in, gather_ctas=gather_ctas, overlap=overlap)
@@ -243,6 +240,54 @@ class DSADecodeLayer:
         self.graph.replay()
         self.history += 1
         return self.out, self.lse
+
+    def step_host(self, h_q_idx: torch.Tensor, h_q: torch.Tensor, new_rows: torch.Tensor,
+                  h_out: torch.Tensor) -> None:
+        """One step with the queries in pinned host memory and the attention output
+        returned to pinned host memory.  H2D and D2H run on a copy stream into
+        double-buffered device staging, so step t's transfers overlap steps t-1 / t+1
+        while every step still moves its own inputs and result over the host link.
+        Asynchronous: synchronise before reading ``h_out``."""
+        d = self.device
+        if getattr(self, "_cs", None) is None:
+            self._cs = torch.cuda.Stream(d)    # H2D copies
+            self._ds = torch.cuda.Stream(d)    # D2H copies (other PCIe direction)
+            self._stage = [(torch.empty_like(self.q_idx_in), torch.empty_like(self.q_in),
+                            torch.empty_like(self.out)) for _ in range(2)]
+            self._ev = [{k: torch.cuda.Event() for k in ("in_ready", "in_free", "out_ready", "out_free")}
+                        for _ in range(2)]
+            self._slot = 0
+        main, cs, ds = torch.cuda.current_stream(d), self._cs, self._ds
+        s = self._slot
+        self._slot ^= 1
+        st_qi, st_q, st_out = self._stage[s]
+        ev = self._ev[s]
+        cs.wait_event(ev["in_free"])           # staging slot s no longer read by main
+        with torch.cuda.stream(cs):
+            st_qi.copy_(h_q_idx, non_blocking=True)
+            st_q.copy_(h_q, non_blocking=True)
+            ev["in_ready"].record(cs)
+        main.wait_event(ev["in_ready"])
+        self.q_idx_in.copy_(st_qi)
+        self.q_in.copy_(st_q)
+        self.rows_in.copy_(new_rows)
+        ev["in_free"].record(main)
+        self.graph.replay()
+        self.history += 1
+        main.wait_event(ev["out_free"])        # previous D2H from this slot finished
+        st_out.copy_(self.out)
+        ev["out_ready"].record(main)
+        ds.wait_event(ev["out_ready"])
+        with torch.cuda.stream(ds):
+            h_out.copy_(st_out, non_blocking=True)
+            ev["out_free"].record(ds)
+
+    def host_sync(self) -> None:
+        """Wait for every outstanding step_host transfer."""
+        for s in ("_cs", "_ds"):
+            if getattr(self, s, None) is not None:
+                getattr(self, s).synchronize()
+        torch.cuda.synchronize(self.device)
 
     def step_counts(self) -> torch.Tensor:
         """[B, 4] access counts of the last step (hits, misses, evicted, transient)."""
