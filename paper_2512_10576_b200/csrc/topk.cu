@@ -5,148 +5,321 @@
 //   emit them ascending by index — the canonical selection-set form of
 //   AccessTrace (trace.py:31-46).  len <= k returns 0..len-1 (scenario.py:110-112).
 //
-// One 1024-thread CTA per row.  Scores map to order-preserving u32 keys (-0.0 is
-// canonicalised to +0.0 so IEEE-equal scores are equal keys).  Four 8-bit radix
-// passes find the exact k-th largest key T; a final ordered compaction takes every
-// key > T plus the first (k - #greater) keys == T in index order.  Rows are read
-// with 16-B loads straight from L2 (K1 has just written them).
+// One CLN-CTA thread-block cluster per row (CLN in {1,2,4,8}, the smallest whose slice
+// fits shared memory: 1 up to 40K tokens, 4 at 128K); CTA r owns the r-th
+// contiguous slice of the row, staged once as order-preserving u32 keys in shared
+// memory (-0.0 canonicalised to +0.0 so IEEE-equal scores are equal keys).
+//
+// Exact k-th largest key T in three radix digits, 12 + 10 + 10 bits:
+//   1. the 12-bit histogram (sign, exponent, 3 mantissa bits) is built while the slice
+//      is staged; every CTA sums the CLN histograms through distributed shared memory
+//      (DSMEM) and all agree on the digit d1 without a global round trip;
+//   2. the keys whose first digit is >= d1 (the < k keys above the bin plus the bin
+//      itself, about k per row) are compacted in row order into a u16 list;
+//   3. the two 10-bit passes and the ordered emit touch only that list.
+// Full-slice passes: stage, count, compact.  A list longer than LCAP (mass ties) makes
+// that CTA fall back to full-slice passes.  The emit takes every key > T plus the first
+// (k - #greater) keys == T in index order; CTA r's output offset is the cluster prefix
+// of the (greater, equal) counts of CTAs 0..r-1.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace {
 
-constexpr int NT = 1024;
+constexpr int NT = 1024;                  // threads per CTA
+constexpr int NW = NT / 32;
 constexpr int VEC = 4;
-constexpr int TILE = NT * VEC;
+constexpr int SLICE_MAX = 40 * 1024;      // keys per CTA (160 KB of shared memory)
+constexpr int LCAP = 12 * 1024;           // list entries per CTA (u16, 24 KB)
+constexpr int D1_BITS = 12, D1_BINS = 1 << D1_BITS, D1_SHIFT = 32 - D1_BITS;
+constexpr int DR_BITS = 10, DR_BINS = 1 << DR_BITS;
+static_assert(DR_BINS == NT, "one 10-bit bin per thread");
 
 __device__ __forceinline__ uint32_t score_key(float f) {
   uint32_t u = __float_as_uint(f + 0.0f);  // -0 -> +0
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+template <int CLN>
+__device__ __forceinline__ void cluster_sync() {
+  if constexpr (CLN > 1) cg::this_cluster().sync();
+  else __syncthreads();
+}
+
+// bin i summed over the cluster's histograms
+template <int CLN>
+__device__ __forceinline__ int cluster_bin(int *hist, int i) {
+  if constexpr (CLN == 1) {
+    return hist[i];
+  } else {
+    cg::cluster_group cl = cg::this_cluster();
+    int v = 0;
+#pragma unroll
+    for (int r = 0; r < CLN; r++) v += cl.map_shared_rank(hist, r)[i];
+    return v;
+  }
+}
+
+// Digit holding the rem-th largest key (bins scanned from the top, summed over the
+// cluster); thread t owns NB/NT consecutive bins.  Leaves (digit, rank inside the bin)
+// in scal and syncs the CTA.
+template <int NB, int CLN>
+__device__ __forceinline__ void pick_digit(int *hist, int rem, int *wbuf, int *scal) {
+  constexpr int BPT = NB / NT;
+  int loc[BPT], sum = 0;
+#pragma unroll
+  for (int j = 0; j < BPT; j++) {
+    loc[j] = cluster_bin<CLN>(hist, NB - 1 - (threadIdx.x * BPT + j));
+    sum += loc[j];
+  }
+  int tot;
+  int c = block_exclusive_scan<NT>(sum, wbuf, &tot);
+  if (c < rem && rem <= c + sum) {
+#pragma unroll
+    for (int j = 0; j < BPT; j++) {
+      if (c + loc[j] >= rem) {
+        scal[0] = NB - 1 - (threadIdx.x * BPT + j);
+        scal[1] = rem - c;
+        break;
+      }
+      c += loc[j];
+    }
+  }
+  __syncthreads();
+}
+
+// Fallback helpers over warp-contiguous runs [lo, hi) of the staged slice.
+__device__ __forceinline__ void run_counts(const uint32_t *skey, int lo, int hi, uint32_t T,
+                                           int &g, int &q) {
+  const int lane = threadIdx.x & 31;
+  g = 0;
+  q = 0;
+  for (int i = lo; i < hi; i += 32) {
+    const int j = i + lane;
+    const uint32_t key = j < hi ? skey[j] : 0u;
+    g += __popc(__ballot_sync(0xffffffffu, j < hi && key > T));
+    q += __popc(__ballot_sync(0xffffffffu, j < hi && key == T));
+  }
+}
+
+__device__ __forceinline__ void run_emit(const uint32_t *skey, int lo, int hi, uint32_t T,
+                                         int need_eq, int gb, int eb, int idx_base,
+                                         int32_t *__restrict__ o) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int i = lo; i < hi; i += 32) {
+    const int j = i + lane;
+    const uint32_t key = j < hi ? skey[j] : 0u;
+    const bool gt = j < hi && key > T, eq = j < hi && key == T;
+    const uint32_t mg = __ballot_sync(0xffffffffu, gt), me = __ballot_sync(0xffffffffu, eq);
+    const int e = eb + __popc(me & lt);
+    if (gt || (eq && e < need_eq)) o[gb + __popc(mg & lt) + min(e, need_eq)] = idx_base + j;
+    gb += __popc(mg);
+    eb += __popc(me);
+  }
+}
+
+template <int CLN>
+__host__ __device__ __forceinline__ int64_t slice_cap(int64_t ld) {  // keys, 4-aligned
+  return (((ld + CLN - 1) / CLN) + 3) & ~3LL;
+}
+
+template <int CLN>
 __global__ void __launch_bounds__(NT, 1)
     topk_kernel(const float *__restrict__ logits, int64_t ld, const int32_t *__restrict__ lens,
                 int k, int32_t *__restrict__ out, int out_ld, int32_t *__restrict__ counts) {
-  __shared__ int hist[256];
-  __shared__ int wbuf[NT / 32];
+  extern __shared__ uint32_t skey[];  // slice_cap keys, then LCAP u16 list entries
+  uint16_t *list = reinterpret_cast<uint16_t *>(skey + slice_cap<CLN>(ld));
+  __shared__ int hist[D1_BINS];
+  __shared__ int wbuf[NW];
   __shared__ int scal[2];
-  const int b = blockIdx.x;
+  __shared__ int part[2];  // this CTA's (greater, equal) totals, read by later ranks
+  int rank = 0;
+  if constexpr (CLN > 1) rank = (int)cg::this_cluster().block_rank();
+  const int b = blockIdx.x / CLN;
   const int len = lens[b];
   const float *row = logits + (int64_t)b * ld;
   int32_t *o = out + (int64_t)b * out_ld;
-  if (len <= k) {
-    for (int i = threadIdx.x; i < len; i += NT) o[i] = i;
-    if (threadIdx.x == 0) counts[b] = len < 0 ? 0 : len;
+  const int chunk = (((len + CLN - 1) / CLN) + 3) & ~3;
+  const int beg = min(len, rank * chunk), end = min(len, beg + chunk);
+  const int n = end - beg;
+  if (len <= k) {  // whole row, ascending (uniform across the cluster: no cluster sync)
+    for (int i = beg + threadIdx.x; i < end; i += NT) o[i] = i;
+    if (rank == 0 && threadIdx.x == 0) counts[b] = len < 0 ? 0 : len;
     return;
   }
-  const bool vec_ok = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(logits) & 15) == 0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int i = threadIdx.x; i < D1_BINS; i += NT) hist[i] = 0;
+  __syncthreads();
 
-  // ---- radix select of the k-th largest key ------------------------------------
-  uint32_t prefix = 0, mask = 0;
-  int rem = k;  // rank (1-based, from the top) still to locate inside the bucket
-  for (int shift = 24; shift >= 0; shift -= 8) {
-    for (int i = threadIdx.x; i < 256; i += NT) hist[i] = 0;
-    __syncthreads();
-    if (vec_ok) {
-      for (int i0 = threadIdx.x * VEC; i0 < len; i0 += TILE) {
-        float4 v = *reinterpret_cast<const float4 *>(row + i0);
-        float a[4] = {v.x, v.y, v.z, v.w};
+  // ---- stage the slice as keys + first-digit histogram (8 loads in flight) ----------
+  const float *src = row + beg;
+  const bool vec_ok = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(logits) & 15) == 0);
+  {
+    constexpr int U = 8;
+    const int n4 = vec_ok ? (n & ~3) : 0;
+    for (int i0 = threadIdx.x * VEC; i0 < n4; i0 += NT * VEC * U) {
+      float4 v[U];
 #pragma unroll
-        for (int e = 0; e < 4; e++) {
-          if (i0 + e < len) {
-            uint32_t key = score_key(a[e]);
-            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
-          }
-        }
+      for (int u = 0; u < U; u++) {
+        const int i = i0 + u * NT * VEC;
+        if (i < n4) v[u] = __ldg(reinterpret_cast<const float4 *>(src + i));
       }
-    } else {
-      for (int i = threadIdx.x; i < len; i += NT) {
-        uint32_t key = score_key(row[i]);
-        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      // bins from the top: lane 0 owns digits 255..248, lane 31 owns 7..0
-      const int lane = threadIdx.x;
-      int loc[8], sum = 0;
 #pragma unroll
-      for (int j = 0; j < 8; j++) {
-        loc[j] = hist[255 - (lane * 8 + j)];
-        sum += loc[j];
-      }
-      int incl = sum;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += y;
-      }
-      int c = incl - sum;
-      if (c < rem && rem <= incl) {
-#pragma unroll
-        for (int j = 0; j < 8; j++) {
-          if (c + loc[j] >= rem) {
-            scal[0] = 255 - (lane * 8 + j);
-            scal[1] = rem - c;
-            break;
-          }
-          c += loc[j];
+      for (int u = 0; u < U; u++) {
+        const int i = i0 + u * NT * VEC;
+        if (i < n4) {
+          const uint4 kk = make_uint4(score_key(v[u].x), score_key(v[u].y), score_key(v[u].z),
+                                      score_key(v[u].w));
+          *reinterpret_cast<uint4 *>(skey + i) = kk;
+          atomicAdd(&hist[kk.x >> D1_SHIFT], 1);
+          atomicAdd(&hist[kk.y >> D1_SHIFT], 1);
+          atomicAdd(&hist[kk.z >> D1_SHIFT], 1);
+          atomicAdd(&hist[kk.w >> D1_SHIFT], 1);
         }
       }
     }
+    for (int i = n4 + threadIdx.x; i < n; i += NT) {
+      const uint32_t key = score_key(src[i]);
+      skey[i] = key;
+      atomicAdd(&hist[key >> D1_SHIFT], 1);
+    }
+  }
+  cluster_sync<CLN>();  // every slice histogram complete and visible cluster-wide
+  pick_digit<D1_BINS, CLN>(hist, k, wbuf, scal);
+  const uint32_t d1 = (uint32_t)scal[0];
+  int rem = scal[1];
+  cluster_sync<CLN>();  // peers finished reading our histogram before it is reused
+
+  // ---- list = slice keys with first digit >= d1, in row order -----------------------
+  const int cw = (((n + NW - 1) / NW) + 31) & ~31;
+  const int lo = min(n, warp * cw), hi = min(n, lo + cw);
+  int cnt = 0;
+  for (int i = lo; i < hi; i += 32) {
+    const int j = i + lane;
+    cnt += __popc(__ballot_sync(0xffffffffu, j < hi && (skey[j] >> D1_SHIFT) >= d1));
+  }
+  int m;
+  int base = block_exclusive_scan<NT>(lane ? 0 : cnt, wbuf, &m);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  const bool use_l = m <= LCAP;
+  if (use_l) {
+    for (int i = lo; i < hi; i += 32) {
+      const int j = i + lane;
+      const bool c = j < hi && (skey[j] >> D1_SHIFT) >= d1;
+      const uint32_t mc = __ballot_sync(0xffffffffu, c);
+      if (c) list[base + __popc(mc & lt)] = (uint16_t)j;
+      base += __popc(mc);
+    }
+  }
+
+  // ---- two 10-bit digits inside bin d1 ------------------------------------------------
+  uint32_t prefix = d1 << D1_SHIFT, mask = ~0u << D1_SHIFT;
+  for (int shift = DR_BITS; shift >= 0; shift -= DR_BITS) {
+    hist[threadIdx.x] = 0;
     __syncthreads();
+    const int len2 = use_l ? m : n;
+    for (int i = threadIdx.x; i < len2; i += NT) {
+      const uint32_t key = skey[use_l ? list[i] : i];
+      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & (DR_BINS - 1)], 1);
+    }
+    cluster_sync<CLN>();
+    pick_digit<DR_BINS, CLN>(hist, rem, wbuf, scal);
     prefix |= (uint32_t)scal[0] << shift;
-    mask |= 0xFFu << shift;
+    mask |= (uint32_t)(DR_BINS - 1) << shift;
     rem = scal[1];
-    __syncthreads();
+    cluster_sync<CLN>();
   }
   const uint32_t T = prefix;
-  const int need_eq = rem;        // keys == T to take, in index order
-  const int n_gt = k - need_eq;   // keys > T (all taken)
-  (void)n_gt;
+  const int need_eq = rem;  // keys == T to take, in index order over the whole row
 
-  // ---- ordered compaction ---------------------------------------------------------
-  int base_gt = 0, base_eq = 0;
-  for (int t0 = 0; t0 < len; t0 += TILE) {
-    const int i0 = t0 + threadIdx.x * VEC;
-    uint32_t keys[VEC];
-#pragma unroll
-    for (int e = 0; e < VEC; e++) keys[e] = 0;
-    if (vec_ok && i0 + VEC <= len) {
-      float4 v = *reinterpret_cast<const float4 *>(row + i0);
-      keys[0] = score_key(v.x);
-      keys[1] = score_key(v.y);
-      keys[2] = score_key(v.z);
-      keys[3] = score_key(v.w);
-    } else {
-#pragma unroll
-      for (int e = 0; e < VEC; e++)
-        if (i0 + e < len) keys[e] = score_key(row[i0 + e]);
-    }
-    int cg = 0, ce = 0;
-#pragma unroll
-    for (int e = 0; e < VEC; e++) {
-      bool valid = i0 + e < len;
-      cg += valid && keys[e] > T;
-      ce += valid && keys[e] == T;
-    }
-    int tot;
-    int ex = block_exclusive_scan<NT>(cg | (ce << 16), wbuf, &tot);
-    int gb = base_gt + (ex & 0xFFFF), eb = base_eq + (ex >> 16);
-#pragma unroll
-    for (int e = 0; e < VEC; e++) {
-      if (i0 + e >= len) break;
-      if (keys[e] > T) {
-        o[gb + min(eb, need_eq)] = i0 + e;
-        gb++;
-      } else if (keys[e] == T) {
-        if (eb < need_eq) o[gb + eb] = i0 + e;
-        eb++;
+  // ---- this slice's (greater, equal) counts and their cluster prefix ------------------
+  int gb = 0, eb = 0, fb_ex = 0;
+  if (use_l) {
+    if constexpr (CLN > 1) {
+      int g = 0, q = 0;
+      for (int i = threadIdx.x; i < m; i += NT) {
+        const uint32_t key = skey[list[i]];
+        g += key > T;
+        q += key == T;
+      }
+      int tot;
+      block_exclusive_scan<NT>(g | (q << 16), wbuf, &tot);
+      if (threadIdx.x == 0) {
+        part[0] = tot & 0xFFFF;
+        part[1] = tot >> 16;
       }
     }
-    base_gt += tot & 0xFFFF;
-    base_eq += tot >> 16;
+  } else {
+    int g, q, tot;
+    run_counts(skey, lo, hi, T, g, q);
+    fb_ex = block_exclusive_scan<NT>(lane ? 0 : (g | (q << 16)), wbuf, &tot);
+    fb_ex = __shfl_sync(0xffffffffu, fb_ex, 0);
+    if (threadIdx.x == 0) {
+      part[0] = tot & 0xFFFF;
+      part[1] = tot >> 16;
+    }
   }
-  if (threadIdx.x == 0) counts[b] = k;
+  if constexpr (CLN > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    for (int r = 0; r < rank; r++) {
+      const int *pc = cl.map_shared_rank(part, r);
+      gb += pc[0];
+      eb += pc[1];
+    }
+    cl.sync();  // keep shared memory alive until every peer has read our counts
+  }
+
+  // ---- ordered emit: every key > T and the first need_eq keys == T --------------------
+  if (use_l) {
+    for (int c0 = 0; c0 < m; c0 += NT) {
+      const int i = c0 + threadIdx.x;
+      const int j = i < m ? list[i] : 0;
+      const uint32_t key = i < m ? skey[j] : 0u;
+      const bool gt = i < m && key > T, eq = i < m && key == T;
+      int tot;
+      const int ex = block_exclusive_scan<NT>((int)gt | ((int)eq << 16), wbuf, &tot);
+      const int e = eb + (ex >> 16);
+      if (gt || (eq && e < need_eq)) o[gb + (ex & 0xFFFF) + min(e, need_eq)] = beg + j;
+      gb += tot & 0xFFFF;
+      eb += tot >> 16;
+    }
+  } else {
+    run_emit(skey, lo, hi, T, need_eq, gb + (fb_ex & 0xFFFF), eb + (fb_ex >> 16), beg, o);
+  }
+  if (rank == 0 && threadIdx.x == 0) counts[b] = k;
+}
+
+template <int CLN>
+int launch_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch, int32_t k,
+                int32_t *d_idx, int32_t idx_ld, int32_t *d_count, cudaStream_t stream) {
+  const size_t smem = (size_t)slice_cap<CLN>(ld) * sizeof(uint32_t) + LCAP * sizeof(uint16_t);
+  static bool attr = false;  // per instantiation: opt in to the largest slice once
+  if (!attr) {
+    ESS_CUDA_TRY(cudaFuncSetAttribute(topk_kernel<CLN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(SLICE_MAX * sizeof(uint32_t) + LCAP * sizeof(uint16_t))));
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)batch * CLN);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CLN;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, topk_kernel<CLN>, d_logits, ld, d_len, (int)k, d_idx,
+                                  (int)idx_ld, d_count));
+  return ESS_OK;
 }
 
 }  // namespace
@@ -157,8 +330,21 @@ extern "C" int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len,
   if (!d_logits || !d_len || !d_idx || !d_count || batch < 0 || k < 1 || idx_ld < k || ld < 1)
     return ESS_ERR_ARG;
   if (batch == 0) return ESS_OK;
-  topk_kernel<<<batch, NT, 0, (cudaStream_t)stream>>>(d_logits, ld, d_len, k, d_idx, idx_ld,
-                                                      d_count);
+  // Cluster size: the smallest that fits a slice in shared memory.  Growing it to fill
+  // idle SMs does not pay: 1024-thread CTAs are register-limited to one per SM and the
+  // DSMEM histogram sums cost more than the shorter slices save (profiles/README.md).
+  int cln = 1;
+  while (cln < 8 && (ld + cln - 1) / cln > SLICE_MAX) cln *= 2;
+  if ((ld + cln - 1) / cln > SLICE_MAX) return ESS_ERR_ARG;  // rows longer than 320K tokens
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc;
+  switch (cln) {
+    case 1: rc = launch_topk<1>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, s); break;
+    case 2: rc = launch_topk<2>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, s); break;
+    case 4: rc = launch_topk<4>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, s); break;
+    default: rc = launch_topk<8>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, s); break;
+  }
+  if (rc != ESS_OK) return rc;
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }

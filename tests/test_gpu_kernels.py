@@ -24,7 +24,10 @@ def e4m3(x):
 
 # ---------------------------------------------------------------------------- K2
 @pytest.mark.parametrize("lens", [[32768, 4096, 2049, 2048, 100, 0, 131072, 5001],
-                                  [32768] * 16])
+                                  [32768] * 16, [49000, 20000, 2049, 1, 0, 3000],
+                                  [2500] * 80,
+                                  [40960 + 4099 * i for i in range(10)],  # 2-CTA clusters
+                                  [200000, 170000, 3000, 2049]])  # 8-CTA clusters
 def test_topk_matches_oracle(lens):
     from paper_2512_10576_b200.indexer import topk
     g = torch.Generator(device="cuda").manual_seed(7)
