@@ -41,6 +41,25 @@ constexpr int QS_BYTES = QS_BLKS * HEADS * 128;    // 49152
 constexpr int KV_BLK_BYTES = NB * 128;             // 4096
 constexpr int KV_BYTES = NBLK * KV_BLK_BYTES;      // 36864
 constexpr int KS = 4;                              // KV ring depth
+#ifndef ESS_MLA_LOAD_LAG
+#define ESS_MLA_LOAD_LAG 1
+#endif
+#ifndef ESS_MLA_DBG_NOLOAD  // timing-only switches for scratch builds (scripts/variant_lib.sh)
+#define ESS_MLA_DBG_NOLOAD 0
+#endif
+#ifndef ESS_MLA_DBG_NOMMA
+#define ESS_MLA_DBG_NOMMA 0
+#endif
+#ifndef ESS_MLA_DBG_ALLSS
+#define ESS_MLA_DBG_ALLSS 0
+#endif
+#ifndef ESS_MLA_DBG_NOSOFT
+#define ESS_MLA_DBG_NOSOFT 0
+#endif
+constexpr int LOAD_LAG = ESS_MLA_LOAD_LAG;         // tiles in flight per loader beyond the newest
+// the MMA warp issues S(i+1) before PV(i) frees slot i, so a loader may run at most
+// KS - 2 tiles ahead of its newest complete tile
+static_assert(LOAD_LAG >= 1 && LOAD_LAG <= KS - 2, "loader lag must leave the MMA a lookahead slot");
 constexpr int MAX_N = ESS_MAX_REQUEST;
 constexpr int NSOFT = 4, NLOAD = 4;
 constexpr int MMA_WARP = NSOFT, LOAD0 = NSOFT + 1;
@@ -49,12 +68,15 @@ constexpr int ROWS_PER_LOADER = NB / NLOAD;         // 8
 constexpr int SLOT_CHUNKS = ESS_SLOT_ROW_BYTES / 16; // 72
 constexpr uint32_t TM_O = 0, TM_S = 256, TM_Q = 320;
 constexpr float RESCALE_THRESHOLD = 8.0f;
-constexpr uint32_t IDESC_S = make_idesc(0 /*f16*/, 0 /*f16*/, HEADS, NB, 0, 0);
+#ifndef ESS_MLA_DBG_SN
+#define ESS_MLA_DBG_SN NB
+#endif
+constexpr uint32_t IDESC_S = make_idesc(0 /*f16*/, 0 /*f16*/, HEADS, ESS_MLA_DBG_SN, 0, 0);
 constexpr uint32_t IDESC_PV = make_idesc(0, 0, HEADS, V_HALF, 0, 1 /*B MN-major*/);
 
 struct Ctrl {
   uint64_t kv_full[KS], kv_empty[KS];
-  uint64_t s_full[2], s_free[2], p_full, p_empty, o_done;
+  uint64_t s_full[2], p_full, p_empty, o_done;
   uint32_t tmem;
 };
 constexpr size_t SMEM_BYTES = 1024 + QS_BYTES + KS * KV_BYTES + MAX_N * 4 + sizeof(Ctrl);
@@ -120,10 +142,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(&c.kv_full[i], NLOAD);
       mbar_init(&c.kv_empty[i], 1);
     }
-    for (int i = 0; i < 2; i++) {
-      mbar_init(&c.s_full[i], 1);
-      mbar_init(&c.s_free[i], 1);
-    }
+    for (int i = 0; i < 2; i++) mbar_init(&c.s_full[i], 1);
     mbar_init(&c.p_full, NSOFT);
     mbar_init(&c.p_empty, 1);
     mbar_init(&c.o_done, 1);
@@ -201,6 +220,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int sb = i & 1;
       mbar_wait(&c.s_full[sb], (i >> 1) & 1);
       tc_fence_after();
+#if ESS_MLA_DBG_NOSOFT
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c.p_full);
+      continue;
+#endif
       uint32_t s[32];
       tmem_ld_32x32b_x32(tmem + lane_base + TM_S + sb * NB, s);
       tmem_ld_wait();
@@ -211,18 +235,21 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         x[j] = (i * NB + j < n) ? __uint_as_float(s[j]) * scale_log2 : -INFINITY;
         mt = fmaxf(mt, x[j]);
       }
-      // PV(i-1) accumulates into O: wait for it before O may be rescaled.  Waited on
-      // every tile so each p_empty phase has exactly one waiter (synccheck-clean).
-      if (i > 0) {
-        mbar_wait(&c.p_empty, (i & 1) ^ 1);
-        tc_fence_after();
-      }
       // warp-uniform decision (tcgen05.ld/st are .sync.aligned); a lane whose own
       // max did not grow rescales by alpha = 1
       if (__any_sync(0xffffffffu, mt > m_run + RESCALE_THRESHOLD) || (i == 0 && !resume)) {
         const float m_new = fmaxf(mt, m_run);
         const float alpha = exp2f(m_run - m_new);  // 0 when m_run = -inf
         l_run *= alpha;
+        // PV(i-1) accumulates into O: wait for it before O is rescaled.  Only rescale
+        // tiles wait, keeping the MMA round trip off the per-tile path.  The parity
+        // is unambiguous: the s_full(i) commit tracks every earlier MMA, PV(i-2)
+        // included, and PV(i) needs this tile's P, so p_empty has completed phase
+        // i-2 and not phase i.
+        if (i > 0) {
+          mbar_wait(&c.p_empty, (i & 1) ^ 1);
+          tc_fence_after();
+        }
         if (i > 0 || resume) {  // O holds PV(i-1) or the resumed state
 #pragma unroll 1
           for (int cc = 0; cc < V_HALF / 32; cc++) {
@@ -316,8 +343,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint32_t qsaddr = smem_u32(sq);
       auto issue_s = [&](int i) {
         const int kb = i % KS, sb = i & 1;
+        // S(i) overwrites S/P buffer sb, last read by PV(i-2) as its A operand.  No
+        // wait: softmax(i-2) finished with the buffer before p_full(i-2), PV(i-2) was
+        // issued before this S(i), and one thread's tcgen05.mma ops execute in issue
+        // order — waiting for PV(i-2) to complete would idle the tensor pipe each tile.
         mbar_wait(&c.kv_full[kb], (i / KS) & 1);
-        mbar_wait(&c.s_free[sb], ((i >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t kvaddr = smem_u32(skv + kb * KV_BYTES);
         const uint32_t d = tmem + TM_S + sb * NB;
@@ -326,7 +356,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
           for (int kk = 0; kk < 4; kk++) {
             uint64_t bd = sw128_desc(kvaddr + blk * KV_BLK_BYTES + kk * 32, 16, 1024);
-            mma_f16_ts(d, tmem + TM_Q + (blk * 4 + kk) * 8, bd, IDESC_S, (blk | kk) ? 1u : 0u);
+#if ESS_MLA_DBG_ALLSS
+            mma_f16_ss(d, sw128_desc(qsaddr + (blk % QS_BLKS) * (HEADS * 128) + kk * 32, 16, 1024), bd,
+                       IDESC_S, (blk | kk) ? 1u : 0u);
+#else
+            if (!ESS_MLA_DBG_NOMMA)
+              mma_f16_ts(d, tmem + TM_Q + (blk * 4 + kk) * 8, bd, IDESC_S, (blk | kk) ? 1u : 0u);
+#endif
           }
         }
 #pragma unroll 1
@@ -335,7 +371,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           for (int kk = 0; kk < 4; kk++) {
             uint64_t ad = sw128_desc(qsaddr + (blk - QT_BLKS) * (HEADS * 128) + kk * 32, 16, 1024);
             uint64_t bd = sw128_desc(kvaddr + blk * KV_BLK_BYTES + kk * 32, 16, 1024);
-            mma_f16_ss(d, ad, bd, IDESC_S, 1u);
+            if (!ESS_MLA_DBG_NOMMA) mma_f16_ss(d, ad, bd, IDESC_S, 1u);
           }
         }
         tc_commit(&c.s_full[sb]);
@@ -350,12 +386,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int kk = 0; kk < NB / 16; kk++) {
           uint64_t bd = sw128_desc(vaddr + kk * 16 * 128, KV_BLK_BYTES, 1024);
-          mma_f16_ts(tmem + TM_O, tmem + TM_S + sb * NB + kk * 8, bd, IDESC_PV,
-                     (i | kk) || resume ? 1u : 0u);
+          if (!ESS_MLA_DBG_NOMMA)
+            mma_f16_ts(tmem + TM_O, tmem + TM_S + sb * NB + kk * 8, bd, IDESC_PV,
+                       (i | kk) || resume ? 1u : 0u);
         }
         tc_commit(&c.p_empty);
         tc_commit(&c.kv_empty[kb]);
-        tc_commit(&c.s_free[sb]);
         if (i == ntiles - 1) tc_commit(&c.o_done);
       }
     }
@@ -385,21 +421,19 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 #pragma unroll
         for (int k = 0; k < 3; k++) {
           const int ch = lane + 32 * k;
-          if (ch < SLOT_CHUNKS)
+          if (ch < SLOT_CHUNKS && !ESS_MLA_DBG_NOLOAD)
             cp_async16(kv + (ch >> 3) * KV_BLK_BYTES + r * 128 + (((ch & 7) ^ (r & 7)) << 4),
                        src + ch * 16, ok ? 16u : 0u);
         }
       }
       cp_async_commit();
-      if (i > 0) {
-        cp_async_wait<1>();
-        signal(i - 1);
+      if (i >= LOAD_LAG) {
+        cp_async_wait<LOAD_LAG>();
+        signal(i - LOAD_LAG);
       }
     }
-    if (ntiles > 0) {
-      cp_async_wait<0>();
-      signal(ntiles - 1);
-    }
+    cp_async_wait<0>();
+    for (int i = max(0, ntiles - LOAD_LAG); i < ntiles; i++) signal(i);
   }
   tc_fence_before();
   __syncthreads();

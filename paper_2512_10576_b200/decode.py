@@ -143,7 +143,7 @@ class DSADecodeLayer:
                            hit_row=acc.hit_row[a:b])
         return self.pool.access(self.idx[a:b], self.cnt[a:b], begin=a, out=view)
 
-    def attend(self, q_idx, q, gather_ctas: int = 32, overlap: str = "da"):
+    def attend(self, q_idx, q, gather_ctas: int = 32, overlap: str = "da", new_rows=None):
         """K1..K5 for every request of the layer.
 
         overlap="da" is the paper's DA schedule (the reference
@@ -152,6 +152,12 @@ class DSADecodeLayer:
         attention pass 1 (Attn0) runs over the rows that were already resident; pass 2
         (Attn1) resumes the online softmax over the fetched rows once the gather lands
         — the merge is the resume itself.  overlap="none" runs K4 then one K5 pass.
+
+        ``new_rows`` (DA only) also admits this step's generated rows, on a third
+        stream right after the cache manager: admission touches no row the step reads
+        (its LRU victim is never one of the rows K3 just stamped, and the new token id
+        is outside the selection), so it hides under the gather instead of trailing
+        the step.  The LRU state afterwards is the same as access-then-append.
         """
         B = self.B
         if self.acc is None:
@@ -174,6 +180,14 @@ class DSADecodeLayer:
         ready = torch.cuda.Event()
         ready.record(main)
         side.wait_event(ready)
+        if new_rows is not None:
+            if getattr(self, "_adm", None) is None:
+                self._adm = torch.cuda.Stream(self.device)
+            self._adm.wait_event(ready)
+            with torch.cuda.stream(self._adm):
+                self._append_device(new_rows)
+            admitted = torch.cuda.Event()
+            admitted.record(self._adm)
         with torch.cuda.stream(side):
             # attention takes 2 CTAs per request (one SM each); the gather gets the rest
             free_sms = torch.cuda.get_device_properties(self.device).multi_processor_count - 2 * B
@@ -185,6 +199,8 @@ class DSADecodeLayer:
         main.wait_event(done)
         sparse_mla(self.pool, q, acc.miss_row, acc.counts[:, 1], self.sm_scale, out=self.out,
                    lse=self.lse, workspace=self._ws, mode="resume")
+        if new_rows is not None:
+            main.wait_event(admitted)
         return self.out, self.lse
 
     # -- whole-step CUDA graph ------------------------------------------------------------
@@ -198,9 +214,15 @@ class DSADecodeLayer:
             self.store.rows_per_pool, None, _lib.stream_handle()), "ess_pool_admit")
 
     def _device_step(self, overlap: str, gather_ctas: int) -> None:
-        self.attend(self.q_idx_in, self.q_in, gather_ctas=gather_ctas, overlap=overlap)
+        # admission overlaps attention only while every pool holds more than K rows:
+        # a smaller pool keeps part of the selection in rows the admission may evict
+        # (capacity only grows with history, so this holds for every later replay)
+        early = overlap == "da" and math.floor(self.rho * self.history) > self.K
+        self.attend(self.q_idx_in, self.q_in, gather_ctas=gather_ctas, overlap=overlap,
+                    new_rows=self.rows_in if early else None)
         self.counter_acc += self.step_counts().sum(0, dtype=torch.int64)
-        self._append_device(self.rows_in)
+        if not early:
+            self._append_device(self.rows_in)
 
     def capture(self, overlap: str = "da", gather_ctas: int = 32) -> None:
         """Record one full decode step (K1..K5 for every micro-batch, the side-stream

@@ -1,0 +1,35 @@
+"""Time K5 (sparse MLA) alone at the C2 shape: B=64, 2048 of 8192 slot rows each."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2512_10576_b200 import _lib
+if len(sys.argv) > 1:
+    _lib.LIB_PATH = os.path.abspath(sys.argv[1])  # a scratch variant build
+from paper_2512_10576_b200.attention import sparse_mla
+from paper_2512_10576_b200.cache import PoolSet
+
+B, cap, n = 64, 8192, 2048
+pools = PoolSet(B, 32768, cap, cap, row_bytes=1152)
+g = torch.Generator(device="cuda").manual_seed(0)
+rv = pools.rows_view()
+rv.copy_((torch.randn(rv.shape, device="cuda", generator=g) * 0.5).half())
+sel = torch.stack([torch.randperm(cap, device="cuda", generator=g)[:n] for _ in range(B)]).int()
+cnt = torch.full((B,), n, dtype=torch.int32, device="cuda")
+q = (torch.randn((B, 128, 576), device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+out, lse = sparse_mla(pools, q, sel, cnt)
+for _ in range(3):
+    sparse_mla(pools, q, sel, cnt, out=out, lse=lse)
+torch.cuda.synchronize()
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+ts = []
+for _ in range(int(os.environ.get("ITERS", "10"))):
+    flush.zero_()
+    torch.cuda._sleep(1_000_000)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(); sparse_mla(pools, q, sel, cnt, out=out, lse=lse); b.record()
+    torch.cuda.synchronize()
+    ts.append(a.elapsed_time(b) * 1e3)
+ts.sort()
+byt = B * n * 1152
+print(f"{os.path.basename(_lib.LIB_PATH)} sparse_mla B={B} n={n}: median {ts[len(ts)//2]:.1f} us, min {ts[0]:.1f} us, "
+      f"{byt / ts[len(ts)//2] / 1e3:.0f} GB/s unique rows")
