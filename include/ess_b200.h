@@ -144,6 +144,13 @@ int ess_gather(ess_pool *pool, int32_t begin, int32_t num, const void *d_host_ro
                int64_t host_pool_stride_rows, const int32_t *d_miss_ids,
                const int32_t *d_miss_row, const int32_t *d_counts, int32_t stride,
                int32_t max_ctas, int32_t flags, void *stream);
+/* as ess_gather, and every landed row also adds 1 (release, GPU scope) to
+ * d_landed[pool - begin] — the per-request arrival counters ess_sparse_mla_da
+ * waits on.  The caller zeroes d_landed [num] before the launch. */
+int ess_gather_signal(ess_pool *pool, int32_t begin, int32_t num, const void *d_host_rows,
+                      int64_t host_pool_stride_rows, const int32_t *d_miss_ids,
+                      const int32_t *d_miss_row, const int32_t *d_counts, int32_t stride,
+                      int32_t *d_landed, int32_t max_ctas, int32_t flags, void *stream);
 /* D2H write-back + slot fill of generated rows (cache.py:122-134):
  * src rows [num][stride][656] -> host_rows[pool][id] and slot store[pool][slot] */
 int ess_write_generated(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_ids,
@@ -182,6 +189,18 @@ int ess_sparse_mla(ess_pool *pool, int32_t pool_begin, const void *d_q,
                    const int32_t *d_sel_row, int32_t sel_stride, const int32_t *d_count,
                    int32_t count_stride, int32_t batch, float sm_scale, void *d_out,
                    float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags, void *stream);
+/* The DA schedule in one launch: attention over the resident rows d_hit_row[b][0:h)
+ * and then, once d_landed[b] reaches m, over the fetched rows d_miss_row[b][0:m)
+ * (h, m = d_counts[b * count_stride + 0 / 1], the access counts of
+ * ess_pool_access), while ess_gather_signal lands those rows on other SMs.  Same
+ * out / lse as ess_sparse_mla over the union.  Its 2 * batch CTAs spin on the
+ * counters, so the gather must be co-resident: batch <= (SMs - 8) / 2, with the
+ * gather given the remaining SMs (ESS_GATHER_EXCLUSIVE_SM).  d_landed [batch] must
+ * be zero at the first call; the kernel leaves it zero again for the next step.  */
+int ess_sparse_mla_da(ess_pool *pool, int32_t pool_begin, const void *d_q,
+                      const int32_t *d_hit_row, const int32_t *d_miss_row, int32_t row_stride,
+                      const int32_t *d_counts, int32_t count_stride, int32_t *d_landed,
+                      int32_t batch, float sm_scale, void *d_out, float *d_lse, void *stream);
 
 #ifdef __cplusplus
 }

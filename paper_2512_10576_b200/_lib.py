@@ -37,10 +37,12 @@ SIGNATURES = {
     "ess_pool_status": ([V, PI32], ctypes.c_int),
     "ess_pool_info": ([V, PI32, PI64, PI32, PI32, PI64, PV], ctypes.c_int),
     "ess_gather": ([V, I32, I32, V, I64, V, V, V, I32, I32, I32, V], ctypes.c_int),
+    "ess_gather_signal": ([V, I32, I32, V, I64, V, V, V, I32, V, I32, I32, V], ctypes.c_int),
     "ess_write_generated": ([V, I32, I32, V, V, V, I32, V, V, I64, V], ctypes.c_int),
     "ess_indexer_logits": ([V, V, V, V, V, I32, I64, V, V], ctypes.c_int),
     "ess_topk": ([V, I64, V, I32, I32, V, I32, V, V], ctypes.c_int),
     "ess_sparse_mla": ([V, I32, V, V, I32, V, I32, I32, F32, V, V, V, V, I32, V], ctypes.c_int),
+    "ess_sparse_mla_da": ([V, I32, V, V, V, I32, V, I32, V, I32, F32, V, V, V], ctypes.c_int),
 }
 
 ESS_OK = 0

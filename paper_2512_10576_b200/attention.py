@@ -61,3 +61,32 @@ def sparse_mla(pool: PoolSet, q: torch.Tensor, sel_row: torch.Tensor, count: tor
         count.data_ptr(), count.stride(0), B, float(sm_scale), _lib.ptr(out), _lib.ptr(lse),
         ws_o, ws_ml, flags, _lib.stream_handle()), "ess_sparse_mla")
     return out, lse
+
+
+def sparse_mla_da(pool: PoolSet, q: torch.Tensor, acc, landed: torch.Tensor,
+                  sm_scale: float = DEFAULT_SM_SCALE, pool_begin: int = 0,
+                  out: torch.Tensor | None = None, lse: torch.Tensor | None = None):
+    """The DA schedule as one launch: attention over the resident
+    rows ``acc.hit_row[b, :counts[b, 0]]``, then — once ``landed[b]`` reaches
+    ``counts[b, 1]`` — over the fetched rows ``acc.miss_row[b, :counts[b, 1]]`` that a
+    concurrent ``gather(..., landed=landed)`` is writing.  Same (out, lse) as
+    ``sparse_mla`` over the union; no workspace round trip, no second prologue.
+    The gather must run concurrently on the SMs this launch leaves free.  ``landed``
+    starts zeroed; the kernel leaves it zero again for the next step."""
+    _lib.require_cuda(q)
+    B = q.shape[0]
+    if q.shape != (B, HEADS, QK_DIM) or q.dtype != torch.bfloat16:
+        raise ValueError("q must be [B, 128, 576] bfloat16")
+    if acc.hit_row.stride(0) != acc.miss_row.stride(0):
+        raise ValueError("hit_row and miss_row must share a row stride")
+    if landed.dtype != torch.int32 or landed.numel() < B:
+        raise ValueError("landed must be int32 with one counter per request")
+    if out is None:
+        out = torch.empty((B, HEADS, V_DIM), dtype=torch.bfloat16, device=q.device)
+    if lse is None:
+        lse = torch.empty((B, HEADS), dtype=torch.float32, device=q.device)
+    _lib.check(_lib.load().ess_sparse_mla_da(
+        pool.handle, pool_begin, q.data_ptr(), acc.hit_row.data_ptr(), acc.miss_row.data_ptr(),
+        acc.hit_row.stride(0), acc.counts.data_ptr(), acc.counts.stride(0), landed.data_ptr(), B,
+        float(sm_scale), out.data_ptr(), lse.data_ptr(), _lib.stream_handle()), "ess_sparse_mla_da")
+    return out, lse

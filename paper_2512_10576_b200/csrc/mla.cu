@@ -37,7 +37,8 @@ constexpr int NB = 32;                    // KV rows per tile
 constexpr int NBLK = QK_DIM / 64;         // 9 dim-blocks of 64 (128 B of f16)
 constexpr int QT_BLKS = 6;                // q blocks held in TMEM (dims 0..383)
 constexpr int QS_BLKS = NBLK - QT_BLKS;   // q blocks in shared memory (dims 384..575)
-constexpr int QS_BYTES = QS_BLKS * HEADS * 128;    // 49152
+constexpr int QBLK_BYTES = HEADS * 128;            // one [128 heads][64 dims] block
+constexpr int QS_BYTES = QS_BLKS * QBLK_BYTES;     // 49152
 constexpr int KV_BLK_BYTES = NB * 128;             // 4096
 constexpr int KV_BYTES = NBLK * KV_BLK_BYTES;      // 36864
 constexpr int KS = 4;                              // KV ring depth
@@ -68,6 +69,7 @@ constexpr int ROWS_PER_LOADER = NB / NLOAD;         // 8
 constexpr int SLOT_CHUNKS = ESS_SLOT_ROW_BYTES / 16; // 72
 constexpr uint32_t TM_O = 0, TM_S = 256, TM_Q = 320;
 constexpr float RESCALE_THRESHOLD = 8.0f;
+constexpr int MLA_AWAIT = 4;  // internal flag of ess_sparse_mla_da
 #ifndef ESS_MLA_DBG_SN
 #define ESS_MLA_DBG_SN NB
 #endif
@@ -76,12 +78,10 @@ constexpr uint32_t IDESC_PV = make_idesc(0, 0, HEADS, V_HALF, 0, 1 /*B MN-major*
 
 struct Ctrl {
   uint64_t kv_full[KS], kv_empty[KS];
-  uint64_t s_full[2], p_full, p_empty, o_done;
+  uint64_t s_full[2], p_full, p_empty, o_done, q_full;
   uint32_t tmem;
 };
 constexpr size_t SMEM_BYTES = 1024 + QS_BYTES + KS * KV_BYTES + MAX_N * 4 + sizeof(Ctrl);
-
-__device__ __forceinline__ uint32_t sw128(uint32_t o) { return o ^ (((o >> 7) & 7u) << 4); }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -107,6 +107,31 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Arrival counter of the fused DA schedule: the low 24 bits count rows the gather has
+// landed (release adds); each of the request's two CTAs adds LANDED_TAG once it no
+// longer needs the counter, and the second one resets it to 0 for the next step (the
+// next gather starts only after this kernel completed).
+constexpr int LANDED_TAG = 1 << 24;
+__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// One lane polls (acquire, GPU scope) until target rows landed, then every lane
+// acquires once itself, so the slot rows published before the gather's release adds
+// are visible to its cp.async.cg loads.
+__device__ __forceinline__ void wait_landed(const int32_t *p, int target) {
+  if ((threadIdx.x & 31) == 0) {
+    uint32_t spins = 0;
+    while ((ld_acquire(p) & (LANDED_TAG - 1)) < target) {
+      if (++spins > ESS_SPIN_LIMIT) __trap();
+      __nanosleep(256);
+    }
+  }
+  __syncwarp();
+  (void)ld_acquire(p);
+}
+
 __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
@@ -118,8 +143,9 @@ __device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_
 }
 
 __global__ void __launch_bounds__(NTHREADS, 1)
-    sparse_mla_kernel(const uint8_t *__restrict__ rows, const uint16_t *__restrict__ q,
+    sparse_mla_kernel(const __grid_constant__ CUtensorMap tm_q, const uint8_t *__restrict__ rows,
                       int64_t rows_per_pool, int pool_begin, const int32_t *__restrict__ sel_row,
+                      const int32_t *__restrict__ sel2, int32_t *landed,
                       int sel_stride, const int32_t *__restrict__ counts, int count_stride,
                       float sm_scale, uint16_t *__restrict__ out, float *__restrict__ lse,
                       float *__restrict__ ws_o, float *__restrict__ ws_ml, int flags) {
@@ -132,10 +158,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int v = blockIdx.x;  // output half
   const int b = blockIdx.y;
-  const int n = min(counts[(int64_t)b * count_stride], MAX_N);
   const bool partial = flags & ESS_MLA_PARTIAL, resume = flags & ESS_MLA_RESUME;
+  // fused DA: rows sel_row[0:n1) are resident, sel2[0:n2) land during the kernel
+  const bool await = flags & MLA_AWAIT;
+  const int n1 = min(counts[(int64_t)b * count_stride], MAX_N);
+  const int n2 = await ? min(counts[(int64_t)b * count_stride + 1], MAX_N - n1) : 0;
+  const int n = n1 + n2;
   const int ntiles = (n + NB - 1) / NB;
-  const uint16_t *qb = q + (int64_t)b * HEADS * QK_DIM;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < KS; i++) {
@@ -146,6 +175,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     mbar_init(&c.p_full, NSOFT);
     mbar_init(&c.p_empty, 1);
     mbar_init(&c.o_done, 1);
+    mbar_init(&c.q_full, 1);
     fence_barrier_init();
   }
   if (warp == MMA_WARP) tmem_alloc<512>(&c.tmem);
@@ -155,16 +185,35 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const uint32_t tmem = c.tmem;
 
   // ---- prologue: q -> TMEM (dims 0..383) and smem (384..575); slot ids -> smem ----
+  // Nine TMA box loads of [128 heads][64 dims] bf16 (SW128): blocks 6..8 land in their
+  // final shared-memory place and are converted to f16 in place; blocks 0..5 land in
+  // the still-empty KV ring, where each head's 128-B row is read bank-conflict free
+  // (the swizzle spreads the 8 lanes of a phase over 8 chunks) and stored to TMEM.
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&c.q_full, HEADS * QK_DIM * 2);
+    for (int blk = 0; blk < NBLK; blk++)
+      tma_load_2d(blk < QT_BLKS ? skv + blk * QBLK_BYTES : sq + (blk - QT_BLKS) * QBLK_BYTES, &tm_q,
+                  &c.q_full, blk * 64, b * HEADS);
+  }
+  if (warp >= LOAD0) {
+    const int32_t *sel = sel_row + (int64_t)b * sel_stride;
+    for (int j = threadIdx.x - LOAD0 * 32; j < n1; j += NLOAD * 32) ssel[j] = __ldg(sel + j);
+    if (await) {
+      const int32_t *s2 = sel2 + (int64_t)b * sel_stride;
+      for (int j = threadIdx.x - LOAD0 * 32; j < n2; j += NLOAD * 32) ssel[n1 + j] = __ldg(s2 + j);
+    }
+  }
+  mbar_wait(&c.q_full, 0);
   if (warp < NSOFT) {
     const int h = warp * 32 + lane;
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    const uint4 *src = reinterpret_cast<const uint4 *>(qb + (int64_t)h * QK_DIM);
 #pragma unroll 1
-    for (int cc = 0; cc < QT_BLKS; cc++) {  // 64 dims = 32 columns per chunk
+    for (int cc = 0; cc < QT_BLKS; cc++) {  // 64 dims = 32 columns per block
+      const uint8_t *rowp = skv + cc * QBLK_BYTES + h * 128;
       uint32_t r[32];
 #pragma unroll
       for (int k = 0; k < 8; k++) {
-        uint4 y = cvt8_bf16_f16(__ldg(src + cc * 8 + k));
+        uint4 y = cvt8_bf16_f16(*reinterpret_cast<const uint4 *>(rowp + ((k ^ (h & 7)) << 4)));
         r[4 * k] = y.x;
         r[4 * k + 1] = y.y;
         r[4 * k + 2] = y.z;
@@ -174,16 +223,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     tmem_st_wait();
   } else {
-    // warps 4-8: slot ids, then q dims 384..575 into SW128 smem
+    // warps 4-8: q dims 384..575 to f16 in place (16-B units keep their SW128 position)
     constexpr int NT = NTHREADS - NSOFT * 32;
-    const int t = threadIdx.x - NSOFT * 32;
-    const int32_t *sel = sel_row + (int64_t)b * sel_stride;
-    for (int j = t; j < n; j += NT) ssel[j] = __ldg(sel + j);
-    for (int it = t; it < HEADS * QS_BLKS * 8; it += NT) {
-      const int h = it / (QS_BLKS * 8), ch = it % (QS_BLKS * 8);  // 8-element chunk
-      uint4 y = cvt8_bf16_f16(__ldg(reinterpret_cast<const uint4 *>(qb + (int64_t)h * QK_DIM + 384) + ch));
-      *reinterpret_cast<uint4 *>(sq + (ch >> 3) * (HEADS * 128) + sw128((uint32_t)h * 128 + (ch & 7) * 16)) = y;
-    }
+    uint4 *qs = reinterpret_cast<uint4 *>(sq);
+    for (int u = threadIdx.x - NSOFT * 32; u < QS_BYTES / 16; u += NT) qs[u] = cvt8_bf16_f16(qs[u]);
     fence_proxy_async_smem();
   }
   tc_fence_before();
@@ -197,25 +240,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     const int64_t hrow = (int64_t)b * HEADS + h;
     float *wso = ws_o ? ws_o + hrow * ESS_MLA_V_DIM + v * V_HALF : nullptr;
-    float m_run = -INFINITY, l_run = 0.f;
-    if (resume) {  // continue from pass 1: running max / sum and this CTA's O half
-      m_run = ws_ml[hrow * 2 + 0];
-      l_run = ws_ml[hrow * 2 + 1];
-#pragma unroll 1
-      for (int cc = 0; cc < V_HALF / 32; cc++) {
-        uint32_t o[32];
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float4 f = *reinterpret_cast<const float4 *>(wso + cc * 32 + j);
-          o[j] = __float_as_uint(f.x);
-          o[j + 1] = __float_as_uint(f.y);
-          o[j + 2] = __float_as_uint(f.z);
-          o[j + 3] = __float_as_uint(f.w);
-        }
-        tmem_st_32x32b_x32(tmem + lane_base + TM_O + cc * 32, o);
-      }
-      tmem_st_wait();
-    }
+    float m_run = -INFINITY, l_run = 0.f;  // resume starts a fresh partial, merged at the end
     for (int i = 0; i < ntiles; i++) {
       const int sb = i & 1;
       mbar_wait(&c.s_full[sb], (i >> 1) & 1);
@@ -237,7 +262,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
       // warp-uniform decision (tcgen05.ld/st are .sync.aligned); a lane whose own
       // max did not grow rescales by alpha = 1
-      if (__any_sync(0xffffffffu, mt > m_run + RESCALE_THRESHOLD) || (i == 0 && !resume)) {
+      if (__any_sync(0xffffffffu, mt > m_run + RESCALE_THRESHOLD) || i == 0) {
         const float m_new = fmaxf(mt, m_run);
         const float alpha = exp2f(m_run - m_new);  // 0 when m_run = -inf
         l_run *= alpha;
@@ -250,7 +275,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mbar_wait(&c.p_empty, (i & 1) ^ 1);
           tc_fence_after();
         }
-        if (i > 0 || resume) {  // O holds PV(i-1) or the resumed state
+        if (i > 0) {  // O holds PV(i-1)
 #pragma unroll 1
           for (int cc = 0; cc < V_HALF / 32; cc++) {
             uint32_t o[32];
@@ -281,7 +306,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (lane == 0) mbar_arrive(&c.p_full);
     }
     // ---------------- epilogue ---------------------------------------------------
-    const bool have_o = ntiles > 0 || resume;  // TMEM O holds a valid accumulator
+    const bool have_o = ntiles > 0;  // TMEM O holds a valid accumulator
     if (ntiles > 0) {
       mbar_wait(&c.o_done, 0);
       tc_fence_after();
@@ -309,21 +334,63 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         ws_ml[hrow * 2 + 1] = l_run;
       }
     } else {
+      // final output.  Resume mode merges this pass's O (TMEM) with pass 1's
+      // unnormalised state from the workspace, streamed with a one-chunk prefetch:
+      // out = (O0 a0 + O1 a1) / (l0 a0 + l1 a1), a_k = 2^(m_k - max(m0, m1)).
+      float m = m_run, l = l_run, a0 = 0.f, a1 = have_o ? 1.f : 0.f;
+      if (resume) {
+        const float m0 = ws_ml[hrow * 2 + 0], l0 = ws_ml[hrow * 2 + 1];
+        m = fmaxf(m0, m_run);
+        a0 = m0 == -INFINITY ? 0.f : exp2f(m0 - m);
+        a1 = (have_o && m_run != -INFINITY) ? exp2f(m_run - m) : 0.f;
+        l = l0 * a0 + l_run * a1;
+      }
       uint16_t *ob = out + hrow * ESS_MLA_V_DIM + v * V_HALF;
-      if (have_o && l_run > 0.f) {
-        const float inv = 1.f / l_run;
+      if (l > 0.f) {
+        const float inv = 1.f / l, c0 = a0 * inv, c1 = a1 * inv;
+        // the KV ring is idle once o_done fired: stage this head's workspace half
+        // (1 KB) there as [16-B unit][head], all 64 copies in flight at once
+        const uint4 *wst = reinterpret_cast<const uint4 *>(skv);
+        if (resume) {
+          const uint32_t st = smem_u32(skv);
+#pragma unroll 8
+          for (int k = 0; k < V_HALF / 4; k++) cp_async16(st + (k * HEADS + h) * 16, wso + 4 * k, 16u);
+          cp_async_commit();
+          cp_async_wait<0>();
+        }
 #pragma unroll 1
         for (int cc = 0; cc < V_HALF / 32; cc++) {
+          float4 w[8];
+#pragma unroll
+          for (int j = 0; j < 8; j++) {
+            if (resume) {
+              const uint4 u = wst[(cc * 8 + j) * HEADS + h];
+              w[j] = make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z),
+                                 __uint_as_float(u.w));
+            } else {
+              w[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
           uint32_t o[32];
-          tmem_ld_32x32b_x32(tmem + lane_base + TM_O + cc * 32, o);
-          tmem_ld_wait();
+          if (have_o) {
+            tmem_ld_32x32b_x32(tmem + lane_base + TM_O + cc * 32, o);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; j++) o[j] = 0u;
+          }
 #pragma unroll
           for (int j = 0; j < 32; j += 8) {
+            const float4 p = w[j / 4], q4 = w[j / 4 + 1];
+            __nv_bfloat162 t0 = __floats2bfloat162_rn(__uint_as_float(o[j]) * c1 + p.x * c0,
+                                                      __uint_as_float(o[j + 1]) * c1 + p.y * c0);
+            __nv_bfloat162 t1 = __floats2bfloat162_rn(__uint_as_float(o[j + 2]) * c1 + p.z * c0,
+                                                      __uint_as_float(o[j + 3]) * c1 + p.w * c0);
+            __nv_bfloat162 t2 = __floats2bfloat162_rn(__uint_as_float(o[j + 4]) * c1 + q4.x * c0,
+                                                      __uint_as_float(o[j + 5]) * c1 + q4.y * c0);
+            __nv_bfloat162 t3 = __floats2bfloat162_rn(__uint_as_float(o[j + 6]) * c1 + q4.z * c0,
+                                                      __uint_as_float(o[j + 7]) * c1 + q4.w * c0);
             uint4 pk;
-            __nv_bfloat162 t0 = __floats2bfloat162_rn(__uint_as_float(o[j]) * inv, __uint_as_float(o[j + 1]) * inv);
-            __nv_bfloat162 t1 = __floats2bfloat162_rn(__uint_as_float(o[j + 2]) * inv, __uint_as_float(o[j + 3]) * inv);
-            __nv_bfloat162 t2 = __floats2bfloat162_rn(__uint_as_float(o[j + 4]) * inv, __uint_as_float(o[j + 5]) * inv);
-            __nv_bfloat162 t3 = __floats2bfloat162_rn(__uint_as_float(o[j + 6]) * inv, __uint_as_float(o[j + 7]) * inv);
             pk.x = *reinterpret_cast<uint32_t *>(&t0);
             pk.y = *reinterpret_cast<uint32_t *>(&t1);
             pk.z = *reinterpret_cast<uint32_t *>(&t2);
@@ -331,7 +398,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             *reinterpret_cast<uint4 *>(ob + cc * 32 + j) = pk;
           }
         }
-        if (v == 0) lse[hrow] = (m_run + log2f(l_run)) * 0.6931471805599453f;
+        if (v == 0) lse[hrow] = (m + log2f(l)) * 0.6931471805599453f;
       } else {
         for (int j = 0; j < V_HALF; j += 8) *reinterpret_cast<uint4 *>(ob + j) = make_uint4(0, 0, 0, 0);
         if (v == 0) lse[hrow] = -INFINITY;
@@ -387,8 +454,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         for (int kk = 0; kk < NB / 16; kk++) {
           uint64_t bd = sw128_desc(vaddr + kk * 16 * 128, KV_BLK_BYTES, 1024);
           if (!ESS_MLA_DBG_NOMMA)
-            mma_f16_ts(tmem + TM_O, tmem + TM_S + sb * NB + kk * 8, bd, IDESC_PV,
-                       (i | kk) || resume ? 1u : 0u);
+            mma_f16_ts(tmem + TM_O, tmem + TM_S + sb * NB + kk * 8, bd, IDESC_PV, (i | kk) ? 1u : 0u);
         }
         tc_commit(&c.p_empty);
         tc_commit(&c.kv_empty[kb]);
@@ -408,9 +474,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&c.kv_full[i % KS]);
     };
+    bool pending = n2 > 0;  // fetched rows not yet known to have landed
     for (int i = 0; i < ntiles; i++) {
       const int kb = i % KS;
       mbar_wait(&c.kv_empty[kb], ((i / KS) & 1) ^ 1);
+      if (pending && (i + 1) * NB > n1) {  // first tile holding fetched rows
+        wait_landed(landed + b, n2);
+        pending = false;
+      }
       const uint32_t kv = kv0 + kb * KV_BYTES;
 #pragma unroll
       for (int rr = 0; rr < ROWS_PER_LOADER; rr++) {
@@ -438,7 +509,56 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (await && threadIdx.x == 0) {  // this CTA's loaders are past their waits
+    if (atomicAdd(landed + b, LANDED_TAG) >= LANDED_TAG) atomicExch(landed + b, 0);
+  }
   if (warp == MMA_WARP) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+
+namespace {
+
+int launch_mla(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_t *d_sel_row,
+               const int32_t *d_sel2, int32_t *d_landed, int32_t sel_stride,
+               const int32_t *d_count, int32_t count_stride, int32_t batch, float sm_scale,
+               void *d_out, float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags,
+               void *stream) {
+  // q as a [batch * 128 heads][576] bf16 tensor, boxes of [128 heads][64 dims], SW128
+  struct QMap {
+    const void *base = nullptr;
+    int32_t batch = 0;
+    CUtensorMap map;
+  };
+  static thread_local QMap qm;
+  alignas(64) CUtensorMap tq;
+  if (qm.base == d_q && qm.batch == batch) {
+    tq = qm.map;
+  } else {
+    if (!ess_make_tmap_2d(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, d_q, QK_DIM, (uint64_t)batch * HEADS,
+                          QK_DIM * 2, 64, HEADS, CU_TENSOR_MAP_SWIZZLE_128B))
+      return ESS_ERR_CUDA;
+    qm.base = d_q;
+    qm.batch = batch;
+    qm.map = tq;
+  }
+  static bool attr = false;
+  if (!attr) {
+    ESS_CUDA_TRY(cudaFuncSetAttribute(sparse_mla_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)SMEM_BYTES));
+    attr = true;
+  }
+  dim3 grid(2, batch);
+  sparse_mla_kernel<<<grid, NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
+      tq, pool->rows, pool->rows_per_pool, pool_begin, d_sel_row, d_sel2, d_landed, sel_stride,
+      d_count, count_stride, sm_scale, (uint16_t *)d_out, d_lse, d_ws_o, d_ws_ml, flags);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+bool pool_ok(ess_pool *pool, int32_t pool_begin, int32_t batch) {
+  return pool && pool->rows && pool->row_bytes == ESS_SLOT_ROW_BYTES && batch >= 0 &&
+         pool_begin >= 0 && (int64_t)pool_begin + batch <= pool->P;
 }
 
 }  // namespace
@@ -450,24 +570,29 @@ extern "C" int ess_sparse_mla(ess_pool *pool, int32_t pool_begin, const void *d_
                               void *stream) {
   if ((flags & (ESS_MLA_PARTIAL | ESS_MLA_RESUME)) && (!d_ws_o || !d_ws_ml)) return ESS_ERR_ARG;
   if ((flags & ESS_MLA_PARTIAL) && (flags & ESS_MLA_RESUME)) return ESS_ERR_ARG;
-  if (!pool || !pool->rows || pool->row_bytes != ESS_SLOT_ROW_BYTES || !d_q || !d_sel_row ||
-      !d_count || count_stride < 1 || (!(flags & ESS_MLA_PARTIAL) && (!d_out || !d_lse)) ||
-      batch < 0 || pool_begin < 0 ||
-      (int64_t)pool_begin + batch > pool->P || sel_stride < 1 ||
+  if (flags & ~(ESS_MLA_PARTIAL | ESS_MLA_RESUME)) return ESS_ERR_ARG;
+  if (!pool_ok(pool, pool_begin, batch) || !d_q || !d_sel_row || !d_count || count_stride < 1 ||
+      (!(flags & ESS_MLA_PARTIAL) && (!d_out || !d_lse)) || sel_stride < 1 ||
       (reinterpret_cast<uintptr_t>(d_q) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15))
     return ESS_ERR_ARG;
   if (batch == 0) return ESS_OK;
-  static bool attr = false;
-  if (!attr) {
-    ESS_CUDA_TRY(cudaFuncSetAttribute(sparse_mla_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)SMEM_BYTES));
-    attr = true;
-  }
-  dim3 grid(2, batch);
-  sparse_mla_kernel<<<grid, NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
-      pool->rows, (const uint16_t *)d_q, pool->rows_per_pool, pool_begin, d_sel_row,
-      sel_stride, d_count, count_stride, sm_scale, (uint16_t *)d_out, d_lse, d_ws_o, d_ws_ml,
-      flags);
-  ESS_CUDA_TRY(cudaGetLastError());
-  return ESS_OK;
+  return launch_mla(pool, pool_begin, d_q, d_sel_row, nullptr, nullptr, sel_stride, d_count,
+                    count_stride, batch, sm_scale, d_out, d_lse, d_ws_o, d_ws_ml, flags, stream);
+}
+
+extern "C" int ess_sparse_mla_da(ess_pool *pool, int32_t pool_begin, const void *d_q,
+                                 const int32_t *d_hit_row, const int32_t *d_miss_row,
+                                 int32_t row_stride, const int32_t *d_counts, int32_t count_stride,
+                                 int32_t *d_landed, int32_t batch, float sm_scale,
+                                 void *d_out, float *d_lse, void *stream) {
+  if (!pool_ok(pool, pool_begin, batch) || !d_q || !d_hit_row || !d_miss_row || !d_counts ||
+      !d_landed || !d_out || !d_lse || row_stride < 1 || count_stride < 2 ||
+      (reinterpret_cast<uintptr_t>(d_q) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15))
+    return ESS_ERR_ARG;
+  if (batch == 0) return ESS_OK;
+  // every CTA may spin on the arrival counters: all of them and the gather must fit at once
+  if (2 * batch > ess_sm_count() - 8) return ESS_ERR_ARG;
+  return launch_mla(pool, pool_begin, d_q, d_hit_row, d_miss_row, d_landed, row_stride, d_counts,
+                    count_stride, batch, sm_scale, d_out, d_lse, nullptr, nullptr, MLA_AWAIT,
+                    stream);
 }

@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
                                                      const int32_t *__restrict__ miss_ids,
                                                      const int32_t *__restrict__ miss_row,
                                                      const int32_t *__restrict__ counts,
-                                                     int stride) {
+                                                     int stride, int32_t *landed) {
   extern __shared__ int pref[];  // [num + 1]
   __shared__ int wbuf[NTG / 32];
   int run = 0;
@@ -677,14 +677,32 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
   const int gwarp = blockIdx.x * (NTG / 32) + (threadIdx.x >> 5);
   const int nwarps = gridDim.x * (NTG / 32);
   const int64_t rb = pv.row_bytes;
-  for (int g0 = gwarp * GROWS; g0 < total; g0 += nwarps * GROWS) {
+  // each warp owns a contiguous run of the flattened miss list (it spans few pools),
+  // so arrival counts are published once per pool change and at the end: one fence
+  // each instead of one per iteration, which would stall the host-link pipeline
+  const int per = (total + nwarps - 1) / nwarps;
+  const int gbeg = min(total, gwarp * per), gend = min(total, gbeg + per);
+  int cur_pool = -1, tally = 0;
+  auto publish = [&]() {
+    if (landed && tally > 0) {
+      __threadfence();  // every lane's slot stores before the release add
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(landed + cur_pool), "r"(tally)
+                     : "memory");
+    }
+    tally = 0;
+  };
+  for (int g0 = gbeg; g0 < gend; g0 += GROWS) {
     const uint8_t *src[GROWS];
     uint8_t *dst[GROWS];
+    int pool_of[GROWS];
 #pragma unroll
     for (int r = 0; r < GROWS; r++) {
       int g = g0 + r;
       src[r] = nullptr;
-      if (g < total) {
+      pool_of[r] = 0;
+      if (g < gend) {
         int lo = 0, hi = num - 1;  // last pool with pref <= g
         while (lo < hi) {
           int mid = (lo + hi + 1) >> 1;
@@ -695,6 +713,7 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
         int row = miss_row[(int64_t)lo * stride + j];
         src[r] = host + ((int64_t)lo * host_stride + id) * ESS_LATENT_ROW_BYTES;
         dst[r] = pv.rows + ((int64_t)(begin + lo) * pv.rows_per_pool + row) * rb;
+        pool_of[r] = lo;
       }
     }
     // all 16-B PCIe loads of the warp's rows in flight first, then dequantise
@@ -708,9 +727,17 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
       }
     }
 #pragma unroll
-    for (int r = 0; r < GROWS; r++)
-      if (src[r]) dequant_row_to_slot(v[r][0], v[r][1], lane, dst[r]);
+    for (int r = 0; r < GROWS; r++) {
+      if (!src[r]) continue;
+      if (pool_of[r] != cur_pool) {  // rows of the previous pool are all stored
+        publish();
+        cur_pool = pool_of[r];
+      }
+      dequant_row_to_slot(v[r][0], v[r][1], lane, dst[r]);
+      tally++;
+    }
   }
+  publish();
 }
 
 // generated rows (656-B latent format) -> host store (D2H through the mapped alias)
@@ -1053,6 +1080,14 @@ int ess_gather(ess_pool *p, int32_t begin, int32_t num, const void *d_host_rows,
                int64_t host_pool_stride_rows, const int32_t *d_miss_ids,
                const int32_t *d_miss_row, const int32_t *d_counts, int32_t stride,
                int32_t max_ctas, int32_t flags, void *stream) {
+  return ess_gather_signal(p, begin, num, d_host_rows, host_pool_stride_rows, d_miss_ids,
+                           d_miss_row, d_counts, stride, nullptr, max_ctas, flags, stream);
+}
+
+int ess_gather_signal(ess_pool *p, int32_t begin, int32_t num, const void *d_host_rows,
+                      int64_t host_pool_stride_rows, const int32_t *d_miss_ids,
+                      const int32_t *d_miss_row, const int32_t *d_counts, int32_t stride,
+                      int32_t *d_landed, int32_t max_ctas, int32_t flags, void *stream) {
   if (!range_ok(p, begin, num) || !p->rows || !d_host_rows || !d_miss_ids || !d_miss_row ||
       !d_counts || stride < 1 || max_ctas < 1)
     return ESS_ERR_ARG;
@@ -1070,7 +1105,7 @@ int ess_gather(ess_pool *p, int32_t begin, int32_t num, const void *d_host_rows,
   }
   gather_kernel<<<max_ctas, NTG, smem, (cudaStream_t)stream>>>(
       view(p), begin, num, (const uint8_t *)d_host_rows, host_pool_stride_rows, d_miss_ids,
-      d_miss_row, d_counts, stride);
+      d_miss_row, d_counts, stride, d_landed);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }

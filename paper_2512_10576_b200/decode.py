@@ -28,7 +28,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _lib
-from .attention import DEFAULT_SM_SCALE, SplitWorkspace, sparse_mla
+from .attention import DEFAULT_SM_SCALE, SplitWorkspace, sparse_mla, sparse_mla_da
 from .cache import AccessBatch, PoolSet, pool_capacity
 from .indexer import indexer_logits, topk
 from .transfer import HostLatentStore, gather, write_generated
@@ -67,6 +67,7 @@ class DSADecodeLayer:
         self.device = torch.device(device if device is not None else "cuda")
         self.B, self.ctx, self.rho, self.K = batch, context_len, sparse_ratio, topk_k
         self.drift, self.sm_scale = drift, sm_scale
+        self.fuse_da = True  # DA as one K5 launch waiting on the gather (when it fits)
         self.Lmax = ((context_len + max_new_tokens + 127) // 128) * 128
         self.gen = torch.Generator(device=self.device).manual_seed(seed)
         d, g, B = self.device, self.gen, batch
@@ -176,7 +177,12 @@ class DSADecodeLayer:
         if getattr(self, "_side", None) is None:
             self._side = torch.cuda.Stream(self.device, priority=-1)
             self._ws = SplitWorkspace(B, self.device)
+            self._landed = torch.zeros(B, dtype=torch.int32, device=self.device)
         side = self._side
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        # one fused K5 launch when its 2B CTAs and the gather fit the GPU at once (its
+        # CTAs wait for the gather's arrival counters); two passes + merge otherwise
+        fused = self.fuse_da and 2 * B <= sms - 8
         ready = torch.cuda.Event()
         ready.record(main)
         side.wait_event(ready)
@@ -190,10 +196,16 @@ class DSADecodeLayer:
             admitted.record(self._adm)
         with torch.cuda.stream(side):
             # attention takes 2 CTAs per request (one SM each); the gather gets the rest
-            free_sms = torch.cuda.get_device_properties(self.device).multi_processor_count - 2 * B
-            gather(self.pool, self.store, acc, max_ctas=max(8, free_sms), exclusive=True)
+            gather(self.pool, self.store, acc, max_ctas=max(8, sms - 2 * B), exclusive=True,
+                   landed=self._landed if fused else None)
         done = torch.cuda.Event()
         done.record(side)
+        if fused:
+            sparse_mla_da(self.pool, q, acc, self._landed, self.sm_scale, out=self.out, lse=self.lse)
+            main.wait_event(done)
+            if new_rows is not None:
+                main.wait_event(admitted)
+            return self.out, self.lse
         sparse_mla(self.pool, q, acc.hit_row, acc.counts[:, 0], self.sm_scale,
                    workspace=self._ws, mode="partial")
         main.wait_event(done)

@@ -100,17 +100,21 @@ class HostLatentStore:
 
 def gather(pool: PoolSet, store: HostLatentStore, acc: AccessBatch, begin: int = 0,
            store_begin: int | None = None, max_ctas: int = 32, exclusive: bool = False,
-           stream=None) -> None:
+           stream=None, landed: torch.Tensor | None = None) -> None:
     """Copy every miss row host[pool][miss_id] -> slot store[pool][miss_row] (K4),
     dequantising to the slot format on the way.  ``exclusive`` keeps the gather off
-    SMs that run attention CTAs (overlapped schedule)."""
+    SMs that run attention CTAs (overlapped schedule).  ``landed`` (int32 [num],
+    zero before the step; sparse_mla_da re-zeroes it) counts each request's landed rows."""
     num = acc.counts.shape[0]
     sb = begin if store_begin is None else store_begin
     flags = _lib.ESS_GATHER_EXCLUSIVE_SM if exclusive else 0
-    _lib.check(_lib.load().ess_gather(
+    if landed is not None and (landed.dtype != torch.int32 or landed.numel() < num):
+        raise ValueError("landed must be int32 with one counter per request")
+    _lib.check(_lib.load().ess_gather_signal(
         pool.handle, begin, num, store.pool_ptr(sb), store.rows_per_pool,
         acc.miss_ids.data_ptr(), acc.miss_row.data_ptr(), acc.counts.data_ptr(),
-        acc.miss_ids.stride(0), max_ctas, flags, _lib.stream_handle(stream)), "ess_gather")
+        acc.miss_ids.stride(0), _lib.ptr(landed), max_ctas, flags, _lib.stream_handle(stream)),
+        "ess_gather")
 
 
 def write_generated(pool: PoolSet, store: HostLatentStore, ids: torch.Tensor, m: torch.Tensor,

@@ -5,10 +5,11 @@ import torch
 from paper_2512_10576_b200 import _lib
 if len(sys.argv) > 1:
     _lib.LIB_PATH = os.path.abspath(sys.argv[1])  # a scratch variant build
-from paper_2512_10576_b200.attention import sparse_mla
+from paper_2512_10576_b200.attention import SplitWorkspace, sparse_mla
 from paper_2512_10576_b200.cache import PoolSet
 
-B, cap, n = 64, 8192, 2048
+B, cap, n = 64, 8192, int(os.environ.get("N", 2048))
+MODE = os.environ.get("MODE", "full")
 pools = PoolSet(B, 32768, cap, cap, row_bytes=1152)
 g = torch.Generator(device="cuda").manual_seed(0)
 rv = pools.rows_view()
@@ -17,8 +18,12 @@ sel = torch.stack([torch.randperm(cap, device="cuda", generator=g)[:n] for _ in 
 cnt = torch.full((B,), n, dtype=torch.int32, device="cuda")
 q = (torch.randn((B, 128, 576), device="cuda", generator=g) * 0.5).to(torch.bfloat16)
 out, lse = sparse_mla(pools, q, sel, cnt)
+ws = SplitWorkspace(B, "cuda")
+sparse_mla(pools, q, sel, cnt, workspace=ws, mode="partial")
+run = lambda: sparse_mla(pools, q, sel, cnt, out=out, lse=lse, workspace=ws if MODE != "full" else None,
+                         mode=MODE)  # noqa: E731
 for _ in range(3):
-    sparse_mla(pools, q, sel, cnt, out=out, lse=lse)
+    run()
 torch.cuda.synchronize()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 ts = []
@@ -26,10 +31,10 @@ for _ in range(int(os.environ.get("ITERS", "10"))):
     flush.zero_()
     torch.cuda._sleep(1_000_000)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(); sparse_mla(pools, q, sel, cnt, out=out, lse=lse); b.record()
+    a.record(); run(); b.record()
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b) * 1e3)
 ts.sort()
 byt = B * n * 1152
-print(f"{os.path.basename(_lib.LIB_PATH)} sparse_mla B={B} n={n}: median {ts[len(ts)//2]:.1f} us, min {ts[0]:.1f} us, "
+print(f"{os.path.basename(_lib.LIB_PATH)} sparse_mla {MODE} B={B} n={n}: median {ts[len(ts)//2]:.1f} us, min {ts[0]:.1f} us, "
       f"{byt / ts[len(ts)//2] / 1e3:.0f} GB/s unique rows")

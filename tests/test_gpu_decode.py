@@ -12,12 +12,15 @@ from oracle import lru as olru
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("ctx,rho", [(8192, 0.25), (4096, 0.25)])
-def test_decode_layer_matches_oracle_chain(ctx, rho):
+@pytest.mark.parametrize("ctx,rho,fuse", [(8192, 0.25, True), (4096, 0.25, True), (8192, 0.25, False)])
+def test_decode_layer_matches_oracle_chain(ctx, rho, fuse):
+    """fuse: the DA schedule as one K5 launch waiting on the gather's arrival counters
+    (sparse_mla_da) vs. two K5 passes merged through the workspace."""
     from paper_2512_10576_b200.cache import pool_capacity
     from paper_2512_10576_b200.decode import DSADecodeLayer
     B, K = 3, 2048
     layer = DSADecodeLayer(B, ctx, rho, K, max_new_tokens=8, seed=1, drift=0.97)
+    layer.fuse_da = fuse
     windows = layer.prefill_warmup(windows=8, record=True)
     orc = [olru.OraclePool(pool_capacity(rho, ctx)) for _ in range(B)]
     for w in windows:
