@@ -35,6 +35,11 @@ extern "C" {
 #endif
 
 #define ESS_LATENT_ROW_BYTES 656
+/* host latent store row pitch: 656-B rows on 64-B boundaries.  The host link moves
+ * 64-B read requests; an unaligned 656-B row straddles 12 of them, an aligned one 11
+ * (+6% zero-copy gather bandwidth, measured; profiles/README.md).  Rows of the host
+ * store are addressed as d_host_rows + (pool * host_pool_stride_rows + id) * pitch. */
+#define ESS_HOST_ROW_PITCH 704
 #define ESS_SLOT_ROW_BYTES 1152 /* 576 x f16 */
 #define ESS_NOPE_DIM 512
 #define ESS_ROPE_DIM 64
@@ -137,7 +142,7 @@ int ess_pool_info(ess_pool *pool, int32_t *num_pools, int64_t *max_ids, int32_t 
  *      transfer_time(..., "h2d") cost term, costmodel.py:173-186) ------------------ */
 /* copies every miss row host_rows[pool][miss_id] -> slot store[pool][miss_row]
  * with 16-B loads through the device alias of registered host memory.  Pool i
- * of the range reads host rows at d_host_rows + i*host_pool_stride_rows*656. */
+ * of the range reads host rows at d_host_rows + (i*host_pool_stride_rows + id)*704. */
 #define ESS_GATHER_EXCLUSIVE_SM 1        /* run only on SMs no attention CTA occupies */
 #define ESS_GATHER_EXCLUSIVE_SMEM (64 * 1024)
 int ess_gather(ess_pool *pool, int32_t begin, int32_t num, const void *d_host_rows,

@@ -53,6 +53,7 @@ ESS_MLA_PARTIAL, ESS_MLA_RESUME = 1, 2
 ESS_GATHER_EXCLUSIVE_SM = 1
 MAX_REQUEST = 2048
 LATENT_ROW_BYTES = 656   # host store / transfer format (e4m3 NoPE + scales + bf16 RoPE)
+HOST_ROW_PITCH = 704     # host store row pitch (64-B aligned rows; ESS_HOST_ROW_PITCH)
 SLOT_ROW_BYTES = 1152    # GPU slot store format (576 x f16, dequantised on admission)
 
 _lib = None

@@ -340,6 +340,18 @@ __device__ __forceinline__ uint4 ld_nc_v4(const void *p) {
                : "l"(p));
   return r;
 }
+#ifndef ESS_HOST_PREFETCH
+#define ESS_HOST_PREFETCH "L2::256B"
+#endif
+// host-link (zero-copy) variant: the L2 fetch-size hint turns a warp's 16-B lane loads
+// into fewer, larger PCIe read requests
+__device__ __forceinline__ uint4 ld_host_v4(const void *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate." ESS_HOST_PREFETCH ".v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
 __device__ __forceinline__ uint4 ld_volatile_v4(const void *p) {
   // system-scope data (mapped host memory): bypass L1, no caching assumptions
   uint4 r;

@@ -31,6 +31,7 @@ constexpr int MAXR = ESS_MAX_REQUEST;    // 2048 ids per call
 constexpr int EPT = MAXR / NT;           // elements per thread (contiguous)
 constexpr int ROW_CHUNKS = ESS_LATENT_ROW_BYTES / 16;  // 41 x 16 B
 
+
 enum { MODE_ACCESS = 0, MODE_WARMUP = 1 };
 
 struct StepSmem {
@@ -711,7 +712,7 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
         int j = g - pref[lo];
         int id = miss_ids[(int64_t)lo * stride + j];
         int row = miss_row[(int64_t)lo * stride + j];
-        src[r] = host + ((int64_t)lo * host_stride + id) * ESS_LATENT_ROW_BYTES;
+        src[r] = host + ((int64_t)lo * host_stride + id) * ESS_HOST_ROW_PITCH;
         dst[r] = pv.rows + ((int64_t)(begin + lo) * pv.rows_per_pool + row) * rb;
         pool_of[r] = lo;
       }
@@ -722,8 +723,8 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
     for (int r = 0; r < GROWS; r++) {
       v[r][1] = make_uint4(0, 0, 0, 0);
       if (src[r]) {
-        v[r][0] = ld_nc_v4(src[r] + lane * 16);
-        if (lane + 32 < ROW_CHUNKS) v[r][1] = ld_nc_v4(src[r] + (lane + 32) * 16);
+        v[r][0] = ld_host_v4(src[r] + lane * 16);
+        if (lane + 32 < ROW_CHUNKS) v[r][1] = ld_host_v4(src[r] + (lane + 32) * 16);
       }
     }
 #pragma unroll
@@ -756,7 +757,7 @@ __global__ void write_generated_kernel(PoolView pv, int begin, const int32_t *id
     uint4 v0 = reinterpret_cast<const uint4 *>(sr)[lane];
     uint4 v1 = lane + 32 < ROW_CHUNKS ? reinterpret_cast<const uint4 *>(sr)[lane + 32] : make_uint4(0, 0, 0, 0);
     if (host) {
-      uint8_t *h = host + ((int64_t)b * host_stride + id) * LB;
+      uint8_t *h = host + ((int64_t)b * host_stride + id) * ESS_HOST_ROW_PITCH;
       st_v4(h + lane * 16, v0);
       if (lane + 32 < ROW_CHUNKS) st_v4(h + (lane + 32) * 16, v1);
     }
@@ -824,7 +825,7 @@ __global__ void __launch_bounds__(NTA) pool_admit_kernel(PoolView pv, int begin,
     uint4 v0 = reinterpret_cast<const uint4 *>(sr)[lane];
     uint4 v1 = lane + 32 < ROW_CHUNKS ? reinterpret_cast<const uint4 *>(sr)[lane + 32] : make_uint4(0, 0, 0, 0);
     if (host) {
-      uint8_t *hp = host + ((int64_t)b * host_stride + h + i) * ESS_LATENT_ROW_BYTES;
+      uint8_t *hp = host + ((int64_t)b * host_stride + h + i) * ESS_HOST_ROW_PITCH;
       st_v4(hp + lane * 16, v0);
       if (lane + 32 < ROW_CHUNKS) st_v4(hp + (lane + 32) * 16, v1);
     }

@@ -66,29 +66,33 @@ def transfer_time(model: TransferModel, blocks: int, direction: str) -> float:
 
 
 class HostLatentStore:
-    """[pools, rows_per_pool, 656] bytes of page-locked, device-mapped host memory."""
+    """[pools, rows_per_pool] latent rows of 656 B in page-locked, device-mapped host
+    memory, laid out at the ESS_HOST_ROW_PITCH (704-B) pitch so every row starts on a
+    64-B host-link request boundary.  ``host`` is the [pools, rows, 656] view."""
 
-    def __init__(self, num_pools: int, rows_per_pool: int, row_bytes: int = LATENT_BLOCK_BYTES):
+    def __init__(self, num_pools: int, rows_per_pool: int):
         _lib.require_cuda()
-        self.num_pools, self.rows_per_pool, self.row_bytes = num_pools, rows_per_pool, row_bytes
-        self.host = torch.empty((num_pools, rows_per_pool, row_bytes), dtype=torch.uint8)
+        self.num_pools, self.rows_per_pool = num_pools, rows_per_pool
+        self.row_bytes, self.pitch = LATENT_BLOCK_BYTES, _lib.HOST_ROW_PITCH
+        self._buf = torch.empty((num_pools, rows_per_pool, self.pitch), dtype=torch.uint8)
+        self.host = self._buf[:, :, :self.row_bytes]
         alias = ctypes.c_void_p()
-        _lib.check(_lib.load().ess_host_register(self.host.data_ptr(), self.host.numel(),
+        _lib.check(_lib.load().ess_host_register(self._buf.data_ptr(), self._buf.numel(),
                                                  ctypes.byref(alias)), "ess_host_register")
         self.device_ptr = alias.value
         self._registered = True
 
     @property
     def nbytes(self) -> int:
-        return self.host.numel()
+        return self._buf.numel()
 
     def pool_ptr(self, begin: int) -> int:
-        return self.device_ptr + begin * self.rows_per_pool * self.row_bytes
+        return self.device_ptr + begin * self.rows_per_pool * self.pitch
 
     def close(self):
         if getattr(self, "_registered", False):
             torch.cuda.synchronize()
-            _lib.load().ess_host_unregister(self.host.data_ptr())
+            _lib.load().ess_host_unregister(self._buf.data_ptr())
             self._registered = False
 
     def __del__(self):

@@ -3,6 +3,9 @@ Also times a plain cudaMemcpy H2D of the same bytes for the link's DMA rate."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
+from paper_2512_10576_b200 import _lib
+if len(sys.argv) > 1:
+    _lib.LIB_PATH = os.path.abspath(sys.argv[1])  # a scratch variant build
 from paper_2512_10576_b200.cache import AccessBatch, PoolSet
 from paper_2512_10576_b200.transfer import HostLatentStore, gather
 
@@ -34,7 +37,7 @@ for ctas in [int(c) for c in os.environ.get("CTAS", "8,20,40,80,148,296").split(
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b) * 1e3)
         ts.sort()
-        print(f"gather ctas={ctas:4d} M={M}: median {ts[5]:.1f} us  {byt / ts[5] / 1e3:.1f} GB/s")
+        print(f"{os.path.basename(_lib.LIB_PATH)} gather ctas={ctas:4d} M={M}: median {ts[5]:.1f} us  {byt / ts[5] / 1e3:.1f} GB/s")
 hbuf = torch.empty(byt, dtype=torch.uint8).pin_memory()
 dbuf = torch.empty(byt, dtype=torch.uint8, device="cuda")
 for _ in range(3):

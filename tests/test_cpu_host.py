@@ -36,6 +36,18 @@ def test_library_exports_every_header_symbol():
     assert "only grow" in _lib.status_text(_lib.ESS_ERR_SHRINK)
 
 
+def test_header_constants_match_python_mirror():
+    src = open(os.path.join(ROOT, "include", "ess_b200.h")).read()
+    defs = dict(re.findall(r"#define (ESS_[A-Z0-9_]+) \(?(-?[0-9]+)", src))
+    assert int(defs["ESS_LATENT_ROW_BYTES"]) == _lib.LATENT_ROW_BYTES == 656
+    assert int(defs["ESS_SLOT_ROW_BYTES"]) == _lib.SLOT_ROW_BYTES
+    assert int(defs["ESS_HOST_ROW_PITCH"]) == _lib.HOST_ROW_PITCH
+    assert _lib.HOST_ROW_PITCH % 64 == 0 and _lib.HOST_ROW_PITCH >= _lib.LATENT_ROW_BYTES
+    assert int(defs["ESS_MLA_PARTIAL"]) == _lib.ESS_MLA_PARTIAL
+    assert int(defs["ESS_MLA_RESUME"]) == _lib.ESS_MLA_RESUME
+    assert int(defs["ESS_GATHER_EXCLUSIVE_SM"]) == _lib.ESS_GATHER_EXCLUSIVE_SM
+
+
 def test_status_mapping():
     with pytest.raises(ValueError, match="duplicate"):
         _lib.check(_lib.ESS_ERR_DUPLICATE)
