@@ -258,6 +258,7 @@ def run_ours(args, cfg):
     layer = DSADecodeLayer(B, L, rho, TOPK, max_new_tokens=total + K + 16, device=dev,
                            seed=1234 + rank, drift=args.drift)
     layer.gather_ctas = args.gather_ctas
+    layer.micro = args.micro
     layer.prefill_warmup(windows=32)
     inputs = [layer.next_queries() for _ in range(total)]
     new_rows = [random_latent_rows(B, dev, layer.gen).view(B, 1, 656) for _ in range(total)]
@@ -269,7 +270,7 @@ def run_ours(args, cfg):
     for t in range(1, W):
         layer.step(inputs[t][0], inputs[t][1], new_rows[t])
     torch.cuda.synchronize()
-    layer.counter_acc.zero_()
+    hits0, misses0 = layer.access_totals()
     if world > 1:
         dist.barrier()
     # timed region: K product steps (graph replays incl. input copies), device clock
@@ -287,7 +288,7 @@ def run_ours(args, cfg):
     layer.pool.check("bench")
     tokens_total, t_max = aggregate(B * K, step_ms * K / 1e3, device=dev)
     value = tokens_total / t_max
-    hits, misses = layer.counter_acc[:2].tolist()
+    hits, misses = (x - y for x, y in zip(layer.access_totals(), (hits0, misses0)))
 
     # per-kernel breakdown (sequential, separate steps) for the roofline
     ktimes, bcounts = kernel_breakdown(layer, inputs[W + K:], new_rows[W + K:])
@@ -331,6 +332,7 @@ def run_ours(args, cfg):
             "config": {"workload": cfg["workload"], "layers": 1, "batch_per_gpu": B,
                        "context_len": L, "sparse_ratio": rho, "topk": TOPK, "query_drift": args.drift,
                        "overlap": args.overlap,
+                       "micro_batches": args.micro if args.overlap == "dba" else 1,
                        "parallelism": f"dp{world} (requests sharded, no collective)",
                        "l2": "inputs larger than L2 (indexer keys + slot pool > 600 MB/GPU)"},
             "e2e": {"value": e2e_tok / e2e_t, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
@@ -341,7 +343,8 @@ def run_ours(args, cfg):
                          "algorithmic_bytes_per_launch": idx_bytes},
             "cpu_baseline": {"value": cpu_v, "unit": "tokens/s", "cores": cpu_threads, "kind": "port",
                              "sample": cpu_sample},
-            "gpu_launches": (9 if args.overlap == "da" else 8) * K,
+            # our kernels per step: K1, K2, K3, K4 per micro-batch + fused K5 + admission
+            "gpu_launches": (4 * (args.micro if args.overlap == "dba" else 1) + 2) * K,
             "cuda_graph": True,
             "clocks": clocks.summary(),
             "kernels_ms": ktimes,
@@ -389,7 +392,7 @@ def run_ceiling(args, cfg, dev):
     for t in range(1, args.warmup):
         layer.step(inputs[t][0], inputs[t][1], new_rows[t])
     torch.cuda.synchronize()
-    layer.counter_acc.zero_()
+    hits0, misses0 = layer.access_totals()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for t in range(args.warmup, total):
@@ -397,7 +400,7 @@ def run_ceiling(args, cfg, dev):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
-    c = layer.counter_acc.tolist()
+    c = [x - y for x, y in zip(layer.access_totals(), (hits0, misses0))]
     layer.pool.check("ceiling")
     layer.close()
     return {"value": B / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms,
@@ -413,7 +416,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--drift", type=float, default=0.97)
     ap.add_argument("--gather-ctas", type=int, default=32)
-    ap.add_argument("--overlap", default="da", choices=["da", "none"])
+    ap.add_argument("--overlap", default="dba", choices=["dba", "da", "none"])
+    ap.add_argument("--micro", type=int, default=2, help="DBA micro-batches per step")
     ap.add_argument("--breakdown-steps", type=int, default=5)
     ap.add_argument("--no-ceiling", dest="ceiling", action="store_false")
     args = ap.parse_args()

@@ -73,6 +73,9 @@ const char *ess_status_string(int status);
 /* cudaHostRegister(mapped) + device alias: the host latent store (UVA gather source) */
 int ess_host_register(void *host_ptr, size_t bytes, void **d_alias);
 int ess_host_unregister(void *host_ptr);
+/* diagnostic: write the device global timer (ns) to *d_dst in stream order; works
+ * inside captured CUDA graphs (step timelines) */
+int ess_timestamp(uint64_t *d_dst, void *stream);
 
 /* ---- K3 cache manager: replaces offsim.cache.SparsePool (cache.py:29-134) ------ */
 /* num_pools pools over ids [0, max_ids), each with up to cap_max slots.  When
@@ -145,6 +148,7 @@ int ess_pool_info(ess_pool *pool, int32_t *num_pools, int64_t *max_ids, int32_t 
  * of the range reads host rows at d_host_rows + (i*host_pool_stride_rows + id)*704. */
 #define ESS_GATHER_EXCLUSIVE_SM 1        /* run only on SMs no attention CTA occupies */
 #define ESS_GATHER_EXCLUSIVE_SMEM (64 * 1024)
+#define ESS_GATHER_BULK 2                /* rows via cp.async.bulk into a smem ring, not 16-B loads */
 int ess_gather(ess_pool *pool, int32_t begin, int32_t num, const void *d_host_rows,
                int64_t host_pool_stride_rows, const int32_t *d_miss_ids,
                const int32_t *d_miss_row, const int32_t *d_counts, int32_t stride,
@@ -170,6 +174,11 @@ int ess_write_generated(ess_pool *pool, int32_t begin, int32_t num, const int32_
 int ess_indexer_logits(const void *d_q, const float *d_w, const void *d_k,
                        const float *d_kscale, const int32_t *d_len, int32_t batch,
                        int64_t k_ld, float *d_logits, void *stream);
+/* same, on at most max_ctas SMs (0 = all): leaves SMs free for a concurrent
+ * host-link gather (the DBA micro-batch schedule) */
+int ess_indexer_logits_ex(const void *d_q, const float *d_w, const void *d_k,
+                          const float *d_kscale, const int32_t *d_len, int32_t batch,
+                          int64_t k_ld, float *d_logits, int32_t max_ctas, void *stream);
 
 /* ---- K2 top-k (op "indexer_topk") ---------------------------------------------- */
 /* per row: the k largest logits[b][0:len[b]) by (score desc, index asc), written

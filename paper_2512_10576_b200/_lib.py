@@ -22,6 +22,7 @@ SIGNATURES = {
     "ess_status_string": ([ctypes.c_int], ctypes.c_char_p),
     "ess_host_register": ([V, SZ, PV], ctypes.c_int),
     "ess_host_unregister": ([V], ctypes.c_int),
+    "ess_timestamp": ([V, V], ctypes.c_int),
     "ess_pool_create": ([PV, I32, I64, I32, I32, I32], ctypes.c_int),
     "ess_pool_destroy": ([V], ctypes.c_int),
     "ess_pool_reset": ([V, I32, I32, V, V], ctypes.c_int),
@@ -40,6 +41,7 @@ SIGNATURES = {
     "ess_gather_signal": ([V, I32, I32, V, I64, V, V, V, I32, V, I32, I32, V], ctypes.c_int),
     "ess_write_generated": ([V, I32, I32, V, V, V, I32, V, V, I64, V], ctypes.c_int),
     "ess_indexer_logits": ([V, V, V, V, V, I32, I64, V, V], ctypes.c_int),
+    "ess_indexer_logits_ex": ([V, V, V, V, V, I32, I64, V, I32, V], ctypes.c_int),
     "ess_topk": ([V, I64, V, I32, I32, V, I32, V, V], ctypes.c_int),
     "ess_sparse_mla": ([V, I32, V, V, I32, V, I32, I32, F32, V, V, V, V, I32, V], ctypes.c_int),
     "ess_sparse_mla_da": ([V, I32, V, V, V, I32, V, I32, V, I32, F32, V, V, V], ctypes.c_int),
@@ -51,6 +53,7 @@ ESS_ERR_NOMEM, ESS_ERR_RATIO, ESS_ERR_ARG, ESS_ERR_CUDA, ESS_ERR_CLOCK = -4, -5,
 ESS_ACCESS_SORT_EVICTED = 1
 ESS_MLA_PARTIAL, ESS_MLA_RESUME = 1, 2
 ESS_GATHER_EXCLUSIVE_SM = 1
+ESS_GATHER_BULK = 2
 MAX_REQUEST = 2048
 LATENT_ROW_BYTES = 656   # host store / transfer format (e4m3 NoPE + scales + bf16 RoPE)
 HOST_ROW_PITCH = 704     # host store row pitch (64-B aligned rows; ESS_HOST_ROW_PITCH)

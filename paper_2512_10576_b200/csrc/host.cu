@@ -79,6 +79,21 @@ int ess_host_register(void *host_ptr, size_t bytes, void **d_alias) {
   return ESS_OK;
 }
 
+// Diagnostic: one thread writes the device's global nanosecond timer to *d_dst, in
+// stream order (usable inside captured CUDA graphs, where events cannot be timed).
+__global__ void timestamp_kernel(uint64_t *dst) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *dst = t;
+}
+
+int ess_timestamp(uint64_t *d_dst, void *stream) {
+  if (!d_dst) return ESS_ERR_ARG;
+  timestamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(d_dst);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
 int ess_host_unregister(void *host_ptr) {
   if (!host_ptr) return ESS_ERR_ARG;
   ESS_CUDA_TRY(cudaHostUnregister(host_ptr));

@@ -258,6 +258,14 @@ bool make_map(CUtensorMap *m, const void *base, uint64_t rows, uint32_t box_rows
 extern "C" int ess_indexer_logits(const void *d_q, const float *d_w, const void *d_k,
                                   const float *d_kscale, const int32_t *d_len, int32_t batch,
                                   int64_t k_ld, float *d_logits, void *stream) {
+  return ess_indexer_logits_ex(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, 0, stream);
+}
+
+extern "C" int ess_indexer_logits_ex(const void *d_q, const float *d_w, const void *d_k,
+                                     const float *d_kscale, const int32_t *d_len, int32_t batch,
+                                     int64_t k_ld, float *d_logits, int32_t max_ctas,
+                                     void *stream) {
+  if (max_ctas < 0) return ESS_ERR_ARG;
   if (!d_q || !d_w || !d_k || !d_kscale || !d_len || !d_logits || batch < 0 ||
       batch > MAX_BATCH || k_ld < TILE_M || (k_ld % TILE_M) != 0 ||
       (reinterpret_cast<uintptr_t>(d_k) & 15) || (reinterpret_cast<uintptr_t>(d_q) & 15) ||
@@ -275,7 +283,8 @@ extern "C" int ess_indexer_logits(const void *d_q, const float *d_w, const void 
                                       (int)SMEM_BYTES));
     attr = true;
   }
-  indexer_kernel<<<ess_sm_count(), NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
+  const int ctas = max_ctas > 0 && max_ctas < ess_sm_count() ? max_ctas : ess_sm_count();
+  indexer_kernel<<<ctas, NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
       tk, tq, d_w, d_kscale, d_len, batch, k_ld, d_logits);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;

@@ -741,6 +741,103 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
   publish();
 }
 
+// K4, bulk-copy form (ESS_GATHER_BULK): each warp streams its contiguous run of the
+// flattened miss list through a ring of GB_RING 656-B shared-memory row buffers filled
+// by one-instruction `cp.async.bulk` copies straight from the mapped host store (one
+// 656-B request per row instead of 41 x 16-B loads), then dequantises from shared
+// memory into the slot rows.  Same outputs and arrival counters as gather_kernel.
+constexpr int GB_RING = 8;
+constexpr int GB_ROW = ESS_LATENT_ROW_BYTES;  // 656 = 41 x 16 B
+
+__device__ __forceinline__ int gather_locate(const int *pref, int num, int g) {
+  int lo = 0, hi = num - 1;  // last pool with pref <= g
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (pref[mid] <= g) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(NTG) gather_bulk_kernel(PoolView pv, int begin, int num,
+                                                          const uint8_t *host, int64_t host_stride,
+                                                          const int32_t *__restrict__ miss_ids,
+                                                          const int32_t *__restrict__ miss_row,
+                                                          const int32_t *__restrict__ counts,
+                                                          int stride, int32_t *landed) {
+  extern __shared__ __align__(128) uint8_t gsm[];
+  constexpr int NW = NTG / 32;
+  uint8_t *ring = gsm;                                                   // [NW][GB_RING][656]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(gsm + NW * GB_RING * GB_ROW);  // [NW][GB_RING]
+  int *pref = reinterpret_cast<int *>(bars + NW * GB_RING);             // [num + 1]
+  __shared__ int wbuf[NW];
+  int run = 0;
+  for (int c0 = 0; c0 < num; c0 += NTG) {
+    int i = c0 + threadIdx.x;
+    int v = i < num ? counts[i * 4 + 1] : 0;
+    int tot;
+    int ex = block_exclusive_scan<NTG>(v, wbuf, &tot);
+    if (i < num) pref[i] = run + ex;
+    run += tot;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint8_t *myring = ring + warp * GB_RING * GB_ROW;
+  uint64_t *mybar = bars + warp * GB_RING;
+  if (threadIdx.x == 0) pref[num] = run;
+  if (lane == 0) {
+    for (int k = 0; k < GB_RING; k++) mbar_init(&mybar[k], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int total = run;
+  const int gwarp = blockIdx.x * NW + warp;
+  const int nwarps = gridDim.x * NW;
+  const int64_t rb = pv.row_bytes;
+  const int per = (total + nwarps - 1) / nwarps;
+  const int gbeg = min(total, gwarp * per), gend = min(total, gbeg + per);
+  const int n = gend - gbeg;
+  auto issue = [&](int k) {  // lane 0: row gbeg + k -> ring buffer k % GB_RING
+    const int g = gbeg + k;
+    const int lo = gather_locate(pref, num, g);
+    const int id = miss_ids[(int64_t)lo * stride + (g - pref[lo])];
+    uint64_t *bar = &mybar[k % GB_RING];
+    mbar_arrive_expect_tx(bar, GB_ROW);
+    bulk_load(myring + (k % GB_RING) * GB_ROW, host + ((int64_t)lo * host_stride + id) * ESS_HOST_ROW_PITCH,
+              GB_ROW, bar);
+  };
+  if (lane == 0)
+    for (int k = 0; k < min(n, GB_RING); k++) issue(k);
+  int cur_pool = -1, tally = 0;
+  auto publish = [&]() {
+    if (landed && tally > 0) {
+      __threadfence();
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(landed + cur_pool), "r"(tally)
+                     : "memory");
+    }
+    tally = 0;
+  };
+  for (int k = 0; k < n; k++) {
+    const int slot = k % GB_RING;
+    const int g = gbeg + k;
+    const int lo = gather_locate(pref, num, g);
+    const int row = miss_row[(int64_t)lo * stride + (g - pref[lo])];
+    mbar_wait(&mybar[slot], (k / GB_RING) & 1);
+    const uint4 *buf = reinterpret_cast<const uint4 *>(myring + slot * GB_ROW);
+    const uint4 v0 = buf[lane];
+    const uint4 v1 = lane + 32 < ROW_CHUNKS ? buf[lane + 32] : make_uint4(0, 0, 0, 0);
+    __syncwarp();
+    if (lane == 0 && k + GB_RING < n) issue(k + GB_RING);
+    if (lo != cur_pool) {
+      publish();
+      cur_pool = lo;
+    }
+    dequant_row_to_slot(v0, v1, lane, pv.rows + ((int64_t)(begin + lo) * pv.rows_per_pool + row) * rb);
+    tally++;
+  }
+  publish();
+}
+
 // generated rows (656-B latent format) -> host store (D2H through the mapped alias)
 // and, dequantised, their slots
 __global__ void write_generated_kernel(PoolView pv, int begin, const int32_t *ids,
@@ -1093,18 +1190,20 @@ int ess_gather_signal(ess_pool *p, int32_t begin, int32_t num, const void *d_hos
       !d_counts || stride < 1 || max_ctas < 1)
     return ESS_ERR_ARG;
   if (num == 0) return ESS_OK;
-  size_t smem = sizeof(int) * (num + 1);
+  const bool bulk = (flags & ESS_GATHER_BULK) != 0;
+  const size_t ring = bulk ? (size_t)(NTG / 32) * GB_RING * (GB_ROW + 8) : 0;
+  size_t smem = ring + sizeof(int) * (num + 1);
   // ESS_GATHER_EXCLUSIVE_SM: reserve enough shared memory that a gather CTA can never
   // share an SM with a K5 CTA (~205 KB), so the long-latency host-link loads do not
   // compete with attention for the SM's L1 miss tracking — the gather runs on the SMs
   // attention leaves idle.
   if ((flags & ESS_GATHER_EXCLUSIVE_SM) && smem < ESS_GATHER_EXCLUSIVE_SMEM)
     smem = ESS_GATHER_EXCLUSIVE_SMEM;
+  auto kern = bulk ? gather_bulk_kernel : gather_kernel;
   if (smem > 48 * 1024) {
-    ESS_CUDA_TRY(cudaFuncSetAttribute(gather_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
+    ESS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   }
-  gather_kernel<<<max_ctas, NTG, smem, (cudaStream_t)stream>>>(
+  kern<<<max_ctas, NTG, smem, (cudaStream_t)stream>>>(
       view(p), begin, num, (const uint8_t *)d_host_rows, host_pool_stride_rows, d_miss_ids,
       d_miss_row, d_counts, stride, d_landed);
   ESS_CUDA_TRY(cudaGetLastError());

@@ -68,6 +68,7 @@ class DSADecodeLayer:
         self.B, self.ctx, self.rho, self.K = batch, context_len, sparse_ratio, topk_k
         self.drift, self.sm_scale = drift, sm_scale
         self.fuse_da = True  # DA as one K5 launch waiting on the gather (when it fits)
+        self.micro = 2       # DBA micro-batches per step (overlap="dba")
         self.Lmax = ((context_len + max_new_tokens + 127) // 128) * 128
         self.gen = torch.Generator(device=self.device).manual_seed(seed)
         d, g, B = self.device, self.gen, batch
@@ -132,46 +133,62 @@ class DSADecodeLayer:
         return rec
 
     # -- the decode step -------------------------------------------------------------------
-    def _select(self, q_idx, a, b):
+    def _select(self, q_idx, a, b, max_ctas: int = 0):
         """K1 -> K2 -> K3 for requests [a, b) on the current stream, writing into the
         step's shared access buffers (row slices)."""
         indexer_logits(q_idx[a:b], self.w[a:b], self.k_cache[a:b], self.k_scale[a:b],
-                       self.lens[a:b], out=self.logits[a:b])
+                       self.lens[a:b], out=self.logits[a:b], max_ctas=max_ctas)
         topk(self.logits[a:b], self.lens[a:b], self.K, out=self.idx[a:b], count=self.cnt[a:b])
+        return self.pool.access(self.idx[a:b], self.cnt[a:b], begin=a, out=self._acc_view(a, b))
+
+    def _acc_view(self, a, b):
         acc = self.acc
-        view = AccessBatch(counts=acc.counts[a:b], sel_row=acc.sel_row[a:b],
+        return AccessBatch(counts=acc.counts[a:b], sel_row=acc.sel_row[a:b],
                            miss_ids=acc.miss_ids[a:b], miss_row=acc.miss_row[a:b],
                            hit_row=acc.hit_row[a:b])
-        return self.pool.access(self.idx[a:b], self.cnt[a:b], begin=a, out=view)
 
-    def attend(self, q_idx, q, gather_ctas: int = 32, overlap: str = "da", new_rows=None):
+    def micro_batches(self, n: int):
+        """[a, b) request ranges of the DBA split (contiguous, sizes differ by <= 1)."""
+        n = max(1, min(n, self.B))
+        edges = [self.B * i // n for i in range(n + 1)]
+        return [(edges[i], edges[i + 1]) for i in range(n)]
+
+    def attend(self, q_idx, q, gather_ctas: int = 32, overlap: str = "dba", new_rows=None,
+               micro: int = 2):
         """K1..K5 for every request of the layer.
 
         overlap="da" is the paper's DA schedule (the reference
         models it as span DAGs, pipeline.py:125-141): right after the cache manager,
         the host-link miss gather (K4) runs on a high-priority side stream while
-        attention pass 1 (Attn0) runs over the rows that were already resident; pass 2
-        (Attn1) resumes the online softmax over the fetched rows once the gather lands
-        — the merge is the resume itself.  overlap="none" runs K4 then one K5 pass.
+        attention over the rows that were already resident (Attn0) runs on the main
+        stream; the fetched rows are attended once they land (Attn1) — the merge is
+        the resumed online softmax.  overlap="none" runs K4 then one K5 pass.
 
-        ``new_rows`` (DA only) also admits this step's generated rows, on a third
-        stream right after the cache manager: admission touches no row the step reads
-        (its LRU victim is never one of the rows K3 just stamped, and the new token id
-        is outside the selection), so it hides under the gather instead of trailing
-        the step.  The LRU state afterwards is the same as access-then-append.
+        overlap="dba" adds the paper's batch split (DBA; pipeline.py
+        :144-167): the requests are cut into ``micro`` contiguous micro-batches whose
+        K1 -> K2 -> K3 run back to back; micro-batch i's gather starts as soon as its
+        cache manager is done and overlaps micro-batch i+1's indexer, which runs on the
+        SMs the gather leaves free.  Attention is still one launch over all requests
+        (Attn0 for every request right away, Attn1 per request as its rows land).
+
+        ``new_rows`` (DA/DBA) also admits this step's generated rows, on a third
+        stream right after the last cache manager: admission touches no row the step
+        reads (its LRU victim is never one of the rows K3 just stamped, and the new
+        token id is outside the selection), so it hides under the gather instead of
+        trailing the step.  The LRU state afterwards is the same as access-then-append.
         """
         B = self.B
         if self.acc is None:
             z = lambda: torch.empty((B, self.K), dtype=torch.int32, device=self.device)  # noqa: E731
             self.acc = AccessBatch(counts=torch.empty((B, 4), dtype=torch.int32, device=self.device),
                                    sel_row=z(), miss_ids=z(), miss_row=z(), hit_row=z())
-        self._select(q_idx, 0, B)
         acc = self.acc
         if overlap == "none":
+            self._select(q_idx, 0, B)
             gather(self.pool, self.store, acc, max_ctas=gather_ctas)
             sparse_mla(self.pool, q, acc.sel_row, self.cnt, self.sm_scale, out=self.out, lse=self.lse)
             return self.out, self.lse
-        if overlap != "da":
+        if overlap not in ("da", "dba"):
             raise ValueError(f"unknown overlap schedule {overlap!r}")
         main = torch.cuda.current_stream(self.device)
         if getattr(self, "_side", None) is None:
@@ -183,9 +200,18 @@ class DSADecodeLayer:
         # one fused K5 launch when its 2B CTAs and the gather fit the GPU at once (its
         # CTAs wait for the gather's arrival counters); two passes + merge otherwise
         fused = self.fuse_da and 2 * B <= sms - 8
-        ready = torch.cuda.Event()
-        ready.record(main)
-        side.wait_event(ready)
+        gsms = max(8, sms - 2 * B)  # attention takes 2 CTAs per request (one SM each)
+        ranges = self.micro_batches(micro if overlap == "dba" else 1)
+        ready = None
+        for i, (a, b) in enumerate(ranges):
+            # later micro-batches' indexers leave the gather's SMs free
+            self._select(q_idx, a, b, max_ctas=sms - gsms if i > 0 else 0)
+            ready = torch.cuda.Event()
+            ready.record(main)
+            side.wait_event(ready)
+            with torch.cuda.stream(side):
+                gather(self.pool, self.store, self._acc_view(a, b), begin=a, max_ctas=gsms,
+                       exclusive=True, landed=self._landed[a:b] if fused else None)
         if new_rows is not None:
             if getattr(self, "_adm", None) is None:
                 self._adm = torch.cuda.Stream(self.device)
@@ -194,10 +220,6 @@ class DSADecodeLayer:
                 self._append_device(new_rows)
             admitted = torch.cuda.Event()
             admitted.record(self._adm)
-        with torch.cuda.stream(side):
-            # attention takes 2 CTAs per request (one SM each); the gather gets the rest
-            gather(self.pool, self.store, acc, max_ctas=max(8, sms - 2 * B), exclusive=True,
-                   landed=self._landed if fused else None)
         done = torch.cuda.Event()
         done.record(side)
         if fused:
@@ -229,14 +251,19 @@ class DSADecodeLayer:
         # admission overlaps attention only while every pool holds more than K rows:
         # a smaller pool keeps part of the selection in rows the admission may evict
         # (capacity only grows with history, so this holds for every later replay)
-        early = overlap == "da" and math.floor(self.rho * self.history) > self.K
+        early = overlap in ("da", "dba") and math.floor(self.rho * self.history) > self.K
         self.attend(self.q_idx_in, self.q_in, gather_ctas=gather_ctas, overlap=overlap,
-                    new_rows=self.rows_in if early else None)
-        self.counter_acc += self.step_counts().sum(0, dtype=torch.int64)
+                    new_rows=self.rows_in if early else None, micro=self.micro)
         if not early:
             self._append_device(self.rows_in)
 
-    def capture(self, overlap: str = "da", gather_ctas: int = 32) -> None:
+    def access_totals(self) -> tuple[int, int]:
+        """(hits, misses) summed over the layer's pools since creation (the pools'
+        own counters, cache.py:41-43): the difference across a run gives its hit rate."""
+        c = self.pool.counters()
+        return int(c[:, 2].sum()), int(c[:, 3].sum())
+
+    def capture(self, overlap: str = "dba", gather_ctas: int = 32) -> None:
         """Record one full decode step (K1..K5 for every micro-batch, the side-stream
         gathers, grow/append/write-back) as a CUDA graph; ``step`` replays it.  The
         first (eager) step also runs here — it advances the state like any step."""
@@ -247,7 +274,6 @@ class DSADecodeLayer:
         self._ids = torch.empty((B, 1), dtype=torch.int32, device=d)
         self._one = torch.ones(B, dtype=torch.int32, device=d)
         self._caps = torch.empty(B, dtype=torch.int32, device=d)
-        self.counter_acc = torch.zeros(4, dtype=torch.int64, device=d)
         q_idx, q = self.next_queries()
         self.q_idx_in.copy_(q_idx)
         self.q_in.copy_(q)
@@ -262,7 +288,6 @@ class DSADecodeLayer:
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self._device_step(overlap, gather_ctas)
-        self.counter_acc.zero_()
         return eager_counts  # access counts of the eager step (graph buffers are unwritten)
 
     def step(self, q_idx: torch.Tensor, q: torch.Tensor, new_rows: torch.Tensor):

@@ -19,13 +19,14 @@ TOPK = 2048
 
 def indexer_logits(q_fp8: torch.Tensor, w: torch.Tensor, k_cache: torch.Tensor,
                    k_scale: torch.Tensor, lens: torch.Tensor,
-                   out: torch.Tensor | None = None) -> torch.Tensor:
+                   out: torch.Tensor | None = None, max_ctas: int = 0) -> torch.Tensor:
     """logits[b, s] = k_scale[b, s] * sum_h w[b, h] * relu(q[b, h] . k[b, s]) for s < lens[b].
 
     q_fp8 [B, 64, 128] and k_cache [B, Lmax, 128] hold e4m3 bytes (uint8 or
     float8_e4m3fn), w [B, 64] f32, k_scale [B, Lmax] f32, lens [B] int32.
     Lmax must be a multiple of 128 and k_cache 16-byte aligned (TMA).
-    Entries at s >= lens[b] are left untouched.
+    Entries at s >= lens[b] are left untouched.  ``max_ctas`` > 0 caps the
+    persistent grid (SMs left free for a concurrent gather); 0 = every SM.
     """
     _lib.require_cuda(k_cache)
     B, Lmax, D = k_cache.shape
@@ -33,9 +34,9 @@ def indexer_logits(q_fp8: torch.Tensor, w: torch.Tensor, k_cache: torch.Tensor,
         raise ValueError("expected q [B,64,128], w [B,64], k [B,Lmax,128]")
     if out is None:
         out = torch.empty((B, Lmax), dtype=torch.float32, device=k_cache.device)
-    _lib.check(_lib.load().ess_indexer_logits(
+    _lib.check(_lib.load().ess_indexer_logits_ex(
         q_fp8.data_ptr(), w.data_ptr(), k_cache.data_ptr(), k_scale.data_ptr(), lens.data_ptr(),
-        B, Lmax, out.data_ptr(), _lib.stream_handle()), "ess_indexer_logits")
+        B, Lmax, out.data_ptr(), max_ctas, _lib.stream_handle()), "ess_indexer_logits")
     return out
 
 

@@ -13,6 +13,7 @@
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import torch
@@ -21,6 +22,8 @@ from . import _lib
 from .cache import AccessBatch, PoolSet
 
 LATENT_BLOCK_BYTES = 656
+# K4 form: 16-B zero-copy loads (False) or cp.async.bulk row copies into a smem ring (True)
+GATHER_BULK = os.environ.get("ESS_GATHER_BULK", "0") == "1"
 PER_CALL_EFFECTIVE_H2D_GBS = 0.79
 PER_CALL_EFFECTIVE_D2H_GBS = 0.23
 
@@ -104,7 +107,7 @@ class HostLatentStore:
 
 def gather(pool: PoolSet, store: HostLatentStore, acc: AccessBatch, begin: int = 0,
            store_begin: int | None = None, max_ctas: int = 32, exclusive: bool = False,
-           stream=None, landed: torch.Tensor | None = None) -> None:
+           stream=None, landed: torch.Tensor | None = None, bulk: bool | None = None) -> None:
     """Copy every miss row host[pool][miss_id] -> slot store[pool][miss_row] (K4),
     dequantising to the slot format on the way.  ``exclusive`` keeps the gather off
     SMs that run attention CTAs (overlapped schedule).  ``landed`` (int32 [num],
@@ -112,6 +115,8 @@ def gather(pool: PoolSet, store: HostLatentStore, acc: AccessBatch, begin: int =
     num = acc.counts.shape[0]
     sb = begin if store_begin is None else store_begin
     flags = _lib.ESS_GATHER_EXCLUSIVE_SM if exclusive else 0
+    if GATHER_BULK if bulk is None else bulk:
+        flags |= _lib.ESS_GATHER_BULK
     if landed is not None and (landed.dtype != torch.int32 or landed.numel() < num):
         raise ValueError("landed must be int32 with one counter per request")
     _lib.check(_lib.load().ess_gather_signal(

@@ -21,23 +21,28 @@ acc = AccessBatch(counts=torch.zeros((B, 4), dtype=torch.int32, device="cuda"), 
                   miss_ids=z(), miss_row=z(), hit_row=z())
 acc.counts[:, 1] = M
 for b in range(B):
-    acc.miss_ids[b, :M] = torch.randperm(hist, device="cuda", generator=g)[:M].int()
+    if os.environ.get("SEQ") == "1":  # contiguous host rows (page locality probe)
+        acc.miss_ids[b, :M] = torch.arange(M, device="cuda", dtype=torch.int32) + 1000
+    elif os.environ.get("SORTED") == "1":
+        acc.miss_ids[b, :M] = torch.randperm(hist, device="cuda", generator=g)[:M].sort().values.int()
+    else:
+        acc.miss_ids[b, :M] = torch.randperm(hist, device="cuda", generator=g)[:M].int()
     acc.miss_row[b, :M] = torch.randperm(cap, device="cuda", generator=g)[:M].int()
 byt = B * M * 656
 for ctas in [int(c) for c in os.environ.get("CTAS", "8,20,40,80,148,296").split(",")]:
-    for excl in (False,):
+    for bulk in (False, True):
         for _ in range(3):
-            gather(pools, store, acc, max_ctas=ctas, exclusive=excl)
+            gather(pools, store, acc, max_ctas=ctas, bulk=bulk)
         torch.cuda.synchronize()
         ts = []
         for _ in range(10):
             torch.cuda._sleep(1_000_000)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record(); gather(pools, store, acc, max_ctas=ctas, exclusive=excl); b.record()
+            a.record(); gather(pools, store, acc, max_ctas=ctas, bulk=bulk); b.record()
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b) * 1e3)
         ts.sort()
-        print(f"{os.path.basename(_lib.LIB_PATH)} gather ctas={ctas:4d} M={M}: median {ts[5]:.1f} us  {byt / ts[5] / 1e3:.1f} GB/s")
+        print(f"{'bulk' if bulk else 'ld16'} gather ctas={ctas:4d} M={M}: median {ts[5]:.1f} us  {byt / ts[5] / 1e3:.1f} GB/s")
 hbuf = torch.empty(byt, dtype=torch.uint8).pin_memory()
 dbuf = torch.empty(byt, dtype=torch.uint8, device="cuda")
 for _ in range(3):

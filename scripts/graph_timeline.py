@@ -1,0 +1,91 @@
+"""Device timeline of the CAPTURED decode step (the graph bench.py replays): every
+stage of DSADecodeLayer.attend is followed by an ess_timestamp node on the stream it
+ran on, so the graph records where each stage ended (globaltimer, ns).  The stamp
+nodes add ~1-2 us each to the chain; read shares, not absolutes.
+Env: CONFIG=c2|c4, STEPS."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_2512_10576_b200 import _lib, decode  # noqa: E402
+from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows  # noqa: E402
+
+CFG = {"c2": (64, 32768, 0.25), "c4": (64, 131072, 0.1)}[os.environ.get("CONFIG", "c2")]
+B, ctx, rho = CFG
+layer = DSADecodeLayer(B, ctx, rho, 2048, max_new_tokens=96, seed=1234, drift=0.97)
+layer.prefill_warmup(windows=32)
+stamps = torch.zeros(64, dtype=torch.int64, device="cuda")
+names = []
+
+
+def mark(name):
+    i = len(names)
+    names.append(name)
+    _lib.check(_lib.load().ess_timestamp(stamps[i:].data_ptr(), _lib.stream_handle()), "ts")
+
+
+def wrap(mod, fn_name, label):
+    f = getattr(mod, fn_name)
+
+    def g(*a, **k):
+        r = f(*a, **k)
+        mark(label)
+        return r
+    setattr(mod, fn_name, g)
+
+
+wrap(decode, "indexer_logits", "K1 indexer")
+wrap(decode, "topk", "K2 topk")
+wrap(decode, "gather", "K4 gather (side)")
+wrap(decode, "sparse_mla_da", "K5 fused DA")
+wrap(decode, "sparse_mla", "K5 pass")
+acc_f = decode.PoolSet.access
+
+
+def access(self, *a, **k):
+    r = acc_f(self, *a, **k)
+    mark("K3 cache")
+    return r
+
+
+decode.PoolSet.access = access
+adm_f = DSADecodeLayer._append_device
+
+
+def append_dev(self, *a, **k):
+    r = adm_f(self, *a, **k)
+    mark("admit")
+    return r
+
+
+DSADecodeLayer._append_device = append_dev
+dev_step = DSADecodeLayer._device_step
+
+
+def device_step(self, *a, **k):
+    mark("start")
+    dev_step(self, *a, **k)
+    mark("end")
+
+
+DSADecodeLayer._device_step = device_step
+names.clear()
+layer.micro = int(os.environ.get("MICRO", 2))
+layer.capture(os.environ.get("OVERLAP", "dba"), 32)  # eager step (stamps 0..n-1), then the graph (stamps n..2n-1)
+n = len(names) // 2
+gnames = names[n:]
+steps = int(os.environ.get("STEPS", 6))
+for t in range(steps):
+    q_idx, q = layer.next_queries()
+    rows = random_latent_rows(B, "cuda", layer.gen).view(B, 1, 656)
+    torch.cuda.synchronize()
+    layer.step(q_idx, q, rows)
+    torch.cuda.synchronize()
+    if t >= steps - 3:
+        s = stamps.cpu().tolist()[n:2 * n]
+        m = int(layer.step_counts()[:, 1].sum())
+        print(f"step {t}: misses {m}  " + "  ".join(f"{nm}={(s[i] - s[0]) / 1e3:.1f}"
+                                                  for i, nm in enumerate(gnames) if i))

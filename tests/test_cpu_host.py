@@ -46,6 +46,7 @@ def test_header_constants_match_python_mirror():
     assert int(defs["ESS_MLA_PARTIAL"]) == _lib.ESS_MLA_PARTIAL
     assert int(defs["ESS_MLA_RESUME"]) == _lib.ESS_MLA_RESUME
     assert int(defs["ESS_GATHER_EXCLUSIVE_SM"]) == _lib.ESS_GATHER_EXCLUSIVE_SM
+    assert int(defs["ESS_GATHER_BULK"]) == _lib.ESS_GATHER_BULK
 
 
 def test_status_mapping():

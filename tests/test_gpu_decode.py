@@ -12,8 +12,10 @@ from oracle import lru as olru
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("ctx,rho,fuse", [(8192, 0.25, True), (4096, 0.25, True), (8192, 0.25, False)])
-def test_decode_layer_matches_oracle_chain(ctx, rho, fuse):
+@pytest.mark.parametrize("ctx,rho,fuse,overlap", [(8192, 0.25, True, "dba"), (4096, 0.25, True, "dba"),
+                                                  (8192, 0.25, False, "dba"), (8192, 0.25, True, "da"),
+                                                  (8192, 0.25, True, "none")])
+def test_decode_layer_matches_oracle_chain(ctx, rho, fuse, overlap):
     """fuse: the DA schedule as one K5 launch waiting on the gather's arrival counters
     (sparse_mla_da) vs. two K5 passes merged through the workspace."""
     from paper_2512_10576_b200.cache import pool_capacity
@@ -29,7 +31,7 @@ def test_decode_layer_matches_oracle_chain(ctx, rho, fuse):
     hist = ctx
     for step in range(4):
         q_idx, q = layer.next_queries()
-        out, lse = layer.attend(q_idx, q)
+        out, lse = layer.attend(q_idx, q, overlap=overlap)
         torch.cuda.synchronize()
         logits = layer.logits.cpu().numpy()
         idx, cnt = layer.idx.cpu().numpy(), layer.cnt.cpu().numpy()
@@ -59,7 +61,8 @@ def test_decode_layer_matches_oracle_chain(ctx, rho, fuse):
     layer.close()
 
 
-def test_graph_step_with_overlap_matches_oracle_chain():
+@pytest.mark.parametrize("overlap,micro", [("dba", 2), ("dba", 3), ("da", 1)])
+def test_graph_step_with_overlap_matches_oracle_chain(overlap, micro):
     """The product step — two micro-batches, gathers on a side stream, whole step
     captured as a CUDA graph, history/capacity computed on device — stays bit-exact
     on selections and cache accounting and within tolerance on attention."""
@@ -95,7 +98,8 @@ def test_graph_step_with_overlap_matches_oracle_chain():
             o.grow_capacity(pool_capacity(rho, hist))
             o.append_generated([hist - 1])
 
-    eager = layer.capture(overlap="da")       # runs one eager step first
+    layer.micro = micro
+    eager = layer.capture(overlap=overlap)    # runs one eager step first
     mirror(False, counts=eager)
     for _ in range(3):
         q_idx, q = layer.next_queries()

@@ -112,7 +112,8 @@ def _fill_slots(pools, rows_u8_per_pool, count):
         rv[b, :count].copy_(torch.as_tensor(dsa.slot_rows(rows.cpu().numpy()), device="cuda"))
 
 
-def test_gather_and_write_back_are_exact():
+@pytest.mark.parametrize("bulk", [False, True], ids=["ld16", "bulk"])
+def test_gather_and_write_back_are_exact(bulk):
     """K4 reads 656-B rows over the host link and admits them dequantised; the slot
     row must equal the oracle's f16(f32(e4m3) * scale) ++ f16(bf16) bit for bit."""
     from paper_2512_10576_b200.cache import PoolSet
@@ -127,7 +128,7 @@ def test_gather_and_write_back_are_exact():
     sets = np.stack([rng.choice(4000, size=1000, replace=False) for _ in range(P)]).astype(np.int32)
     acc = pools.access(torch.as_tensor(sets, device="cuda"),
                        torch.full((P,), 1000, dtype=torch.int32, device="cuda"))
-    gather(pools, store, acc)
+    gather(pools, store, acc, bulk=bulk)
     rows = pools.rows_view().cpu().numpy()
     sel = acc.sel_row.cpu().numpy()
     host = store.host.numpy()
