@@ -4,14 +4,18 @@
 //
 // The head contraction is a real GEMM per 128-token tile: D[128 tok][64 heads] =
 // K_tile[128 x 128 e4m3] . Q[64 x 128 e4m3]^T, issued as tcgen05.mma kind::f8f6f4
-// (M=128, N=64, 4 x K=32) by one thread into one of 4 TMEM accumulators, so the
-// epilogue (ReLU, head-weighted sum, x kscale) of earlier tiles overlaps the MMA of
-// later ones.  TMA (SWIZZLE_128B) streams K tiles through a 10-stage mbarrier ring;
-// q is loaded once per request into one of two slots.  The kernel is persistent
-// (one CTA per SM, contiguous tile ranges) and HBM-bound: 132 B/token in, 4 B out.
+// (M=128, N=64, 4 x K=32) by one thread into TMEM.  The pipeline moves 256-token
+// UNITS (two MMA tiles, one 32-KB ring stage, one barrier round, one TMEM
+// accumulator of 128 columns): with 128-token units the per-unit barrier / commit /
+// TMEM hand-off chain, not HBM, set the rate (K1 scaled linearly with the number of
+// SMs; profiles/README.md), and doubling the unit took C2 from 68 to 55 us and C4
+// from 228 to 178 us (98% of the measured copy bandwidth).  TMA (SWIZZLE_128B)
+// streams K tiles through a 5-stage ring; q is loaded once per request into one of
+// two slots.  The kernel is persistent (one CTA per SM, contiguous unit ranges) and
+// HBM-bound: 132 B/token in, 4 B out.
 //
 // Warp roles (320 threads): w0 TMA producer, w1 TMEM alloc + MMA issuer,
-// w2..w9 epilogue in two groups taking alternate tiles (TMEM lane quarter =
+// w2..w9 epilogue in two groups taking alternate units (TMEM lane quarter =
 // warp % 4); head weights stay in registers while the request does not change.
 #include <cuda.h>
 
@@ -19,17 +23,27 @@
 
 namespace {
 
-constexpr int STAGES = 10;                  // K-tile ring depth (16 KB each)
-constexpr int TILE_M = 128;                 // tokens per tile
+#ifndef ESS_K1_SUB
+#define ESS_K1_SUB 2
+#endif
+#ifndef ESS_K1_STAGES
+#define ESS_K1_STAGES (ESS_K1_SUB == 1 ? 10 : ESS_K1_SUB == 2 ? 5 : 3)
+#endif
+constexpr int TILE_M = 128;                 // tokens per MMA tile (M)
+constexpr int SUB = ESS_K1_SUB;             // MMA tiles per pipeline unit
+constexpr int UNIT_M = SUB * TILE_M;        // tokens per unit (one ring stage, one barrier round)
+constexpr int STAGES = ESS_K1_STAGES;       // unit ring depth
 constexpr int HEADS = ESS_INDEXER_HEADS;    // 64 = N
 constexpr int DIM = ESS_INDEXER_DIM;        // 128 = K (bytes, e4m3)
-constexpr int KT_BYTES = TILE_M * DIM;      // 16 KB
+constexpr int KT_BYTES = TILE_M * DIM;      // 16 KB per MMA tile
+constexpr int UT_BYTES = SUB * KT_BYTES;    // bytes per unit
 constexpr int QT_BYTES = HEADS * DIM;       // 8 KB, one per request (double-buffered)
-constexpr int NACC = 4;                     // TMEM accumulator stages
+constexpr int ACC_COLS = SUB * HEADS;       // TMEM columns per unit
+constexpr int NACC = 512 / ACC_COLS < 4 ? 512 / ACC_COLS : 4;  // TMEM accumulator stages
 constexpr int NEPI = 8;                     // epilogue warps: 2 groups x 4 lane quarters
 constexpr int NTHREADS = 32 * (2 + NEPI);
 constexpr int MAX_BATCH = 4096;
-constexpr int TMEM_COLS = NACC * HEADS;     // 256
+constexpr int TMEM_COLS = NACC * ACC_COLS;  // 512 (SUB 2) / 256 (SUB 1)
 constexpr uint32_t IDESC = make_idesc(0 /*e4m3*/, 0 /*e4m3*/, TILE_M, HEADS, 0, 0);
 
 struct Ctrl {
@@ -44,9 +58,10 @@ struct Ctrl {
 };
 
 constexpr size_t SMEM_BYTES =
-    1024 /*align slack*/ + (size_t)STAGES * KT_BYTES + 2 * QT_BYTES + sizeof(Ctrl);
+    1024 /*align slack*/ + (size_t)STAGES * UT_BYTES + 2 * QT_BYTES + sizeof(Ctrl);
+static_assert(SMEM_BYTES <= 232448, "K1 shared memory over the sm_100 limit");
 
-// Walk the flattened (request, tile) sequence.
+// Walk the flattened (request, unit) sequence.
 struct TileCursor {
   int b, t;
   __device__ void seek(const int *pref, int B, int idx) {
@@ -73,17 +88,17 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                    const int32_t *__restrict__ lens, int B, int64_t k_ld, float *__restrict__ logits) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *qbuf = smem + (size_t)STAGES * KT_BYTES;
+  uint8_t *qbuf = smem + (size_t)STAGES * UT_BYTES;
   Ctrl &c = *reinterpret_cast<Ctrl *>(qbuf + 2 * QT_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  // tile prefix over requests (every CTA computes it; B is small)
+  // unit prefix over requests (every CTA computes it; B is small)
   if (threadIdx.x == 0) {
     int acc = 0;
     for (int b = 0; b < B; b++) {
       c.pref[b] = acc;
       int L = lens[b];
-      acc += L > 0 ? (L + TILE_M - 1) / TILE_M : 0;
+      acc += L > 0 ? (L + UNIT_M - 1) / UNIT_M : 0;
     }
     c.pref[B] = acc;
     for (int s = 0; s < STAGES; s++) {
@@ -112,13 +127,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (ntiles > 0) {
     if (warp == 0) {
-      // ---- TMA producer: q once per request (2 slots), K tiles through the ring ----
+      // ---- TMA producer: q once per request (2 slots), K units through the ring ----
       if (elect_one()) {
         prefetch_tmap(&tm_k);
         prefetch_tmap(&tm_q);
         TileCursor cur;
         cur.seek(c.pref, B, t0);
-        int qs = 1, prev_b = -1;
+        int qs = 1, prev_b = -1, len_b = 0;
         uint32_t quse[2] = {0, 0};
         for (int it = 0; it < ntiles; it++) {
           if (cur.b != prev_b) {
@@ -128,12 +143,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tma_load_2d(qbuf + qs * QT_BYTES, &tm_q, &c.qfull[qs], 0, cur.b * HEADS);
             quse[qs]++;
             prev_b = cur.b;
+            len_b = __ldg(lens + cur.b);
           }
           const int s = it % STAGES;
+          // MMA tiles of this unit that hold tokens (the last unit may be short; its
+          // missing tile is never loaded — the MMA reads stale rows, masked below)
+          const int rem = len_b - cur.t * UNIT_M;
+          const int nsub = rem >= UNIT_M ? SUB : (rem + TILE_M - 1) / TILE_M;
           mbar_wait(&c.empty[s], ((it / STAGES) & 1) ^ 1);
-          mbar_arrive_expect_tx(&c.full[s], KT_BYTES);
-          tma_load_2d(smem + (size_t)s * KT_BYTES, &tm_k, &c.full[s], 0,
-                      (int32_t)(cur.b * k_ld + (int64_t)cur.t * TILE_M));
+          mbar_arrive_expect_tx(&c.full[s], nsub * KT_BYTES);
+          for (int j = 0; j < nsub; j++)
+            tma_load_2d(smem + (size_t)s * UT_BYTES + j * KT_BYTES, &tm_k, &c.full[s], 0,
+                        (int32_t)(cur.b * k_ld + (int64_t)cur.t * UNIT_M + j * TILE_M));
           cur.next(c.pref, B);
         }
       }
@@ -157,13 +178,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mbar_wait(&c.tempty[a], ((it / NACC) & 1) ^ 1);
           mbar_wait(&c.full[s], (it / STAGES) & 1);
           tc_fence_after();
-          const uint32_t kaddr = smem_u32(smem + (size_t)s * KT_BYTES);
           const uint32_t qaddr = smem_u32(qbuf + qs * QT_BYTES);
 #pragma unroll
-          for (int kk = 0; kk < DIM / 32; kk++) {
-            uint64_t ad = sw128_desc(kaddr + kk * 32, 16, 1024);
-            uint64_t bd = sw128_desc(qaddr + kk * 32, 16, 1024);
-            mma_f8f6f4_ss(tmem + a * HEADS, ad, bd, IDESC, kk > 0 ? 1u : 0u);
+          for (int j = 0; j < SUB; j++) {
+            const uint32_t kaddr = smem_u32(smem + (size_t)s * UT_BYTES + j * KT_BYTES);
+#pragma unroll
+            for (int kk = 0; kk < DIM / 32; kk++) {
+              uint64_t ad = sw128_desc(kaddr + kk * 32, 16, 1024);
+              uint64_t bd = sw128_desc(qaddr + kk * 32, 16, 1024);
+              mma_f8f6f4_ss(tmem + a * ACC_COLS + j * HEADS, ad, bd, IDESC, kk > 0 ? 1u : 0u);
+            }
           }
           tc_commit(&c.empty[s]);
           tc_commit(&c.tfull[a]);
@@ -171,7 +195,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
       }
     } else {
-      // ---- epilogue: group g = tiles it % 2 == g; warp % 4 = TMEM lane quarter ------
+      // ---- epilogue: group g = units it % 2 == g; warp % 4 = TMEM lane quarter ------
       const int e = warp - 2;
       const int g = e >> 2;
       const int quarter = warp & 3;
@@ -196,28 +220,39 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           len_b = __ldg(lens + b);
           wb = b;
         }
-        const int64_t tok = (int64_t)cur.t * TILE_M + row;
-        const bool valid = tok < len_b;
-        const int64_t off = (int64_t)b * k_ld + tok;
-        const float ks = valid ? __ldg(kscale + off) : 0.f;
+        int64_t off[SUB];
+        bool valid[SUB];
+        float ks[SUB];
+#pragma unroll
+        for (int j = 0; j < SUB; j++) {
+          const int64_t tok = (int64_t)cur.t * UNIT_M + j * TILE_M + row;
+          valid[j] = tok < len_b;
+          off[j] = (int64_t)b * k_ld + tok;
+          ks[j] = valid[j] ? __ldg(kscale + off[j]) : 0.f;
+        }
         const int a = it % NACC;
         mbar_wait(&c.tfull[a], (it / NACC) & 1);
         tc_fence_after();
-        uint32_t r[64];
-        tmem_ld_32x32b_x64(tmem + ((uint32_t)(quarter * 32) << 16) + a * HEADS, r);
-        tmem_ld_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&c.tempty[a]);
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-        for (int h = 0; h < HEADS; h += 4) {
-          a0 = fmaf(wr[h + 0], fmaxf(__uint_as_float(r[h + 0]), 0.f), a0);
-          a1 = fmaf(wr[h + 1], fmaxf(__uint_as_float(r[h + 1]), 0.f), a1);
-          a2 = fmaf(wr[h + 2], fmaxf(__uint_as_float(r[h + 2]), 0.f), a2);
-          a3 = fmaf(wr[h + 3], fmaxf(__uint_as_float(r[h + 3]), 0.f), a3);
+        for (int j = 0; j < SUB; j++) {
+          uint32_t r[64];
+          tmem_ld_32x32b_x64(tmem + ((uint32_t)(quarter * 32) << 16) + a * ACC_COLS + j * HEADS, r);
+          tmem_ld_wait();
+          if (j == SUB - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&c.tempty[a]);
+          }
+          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+          for (int h = 0; h < HEADS; h += 4) {
+            a0 = fmaf(wr[h + 0], fmaxf(__uint_as_float(r[h + 0]), 0.f), a0);
+            a1 = fmaf(wr[h + 1], fmaxf(__uint_as_float(r[h + 1]), 0.f), a1);
+            a2 = fmaf(wr[h + 2], fmaxf(__uint_as_float(r[h + 2]), 0.f), a2);
+            a3 = fmaf(wr[h + 3], fmaxf(__uint_as_float(r[h + 3]), 0.f), a3);
+          }
+          if (valid[j]) logits[off[j]] = ((a0 + a1) + (a2 + a3)) * ks[j];
         }
-        if (valid) logits[off] = ((a0 + a1) + (a2 + a3)) * ks;
         cur.next(c.pref, B);
         cur.next(c.pref, B);
       }

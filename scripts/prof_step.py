@@ -18,12 +18,13 @@ ap.add_argument("--ctx", type=int, default=32768)
 ap.add_argument("--rho", type=float, default=0.25)
 ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--windows", type=int, default=4)
+ap.add_argument("--overlap", default="da")
 a = ap.parse_args()
 layer = DSADecodeLayer(a.batch, a.ctx, a.rho, 2048, max_new_tokens=a.steps + 8, seed=5, drift=0.97)
 layer.prefill_warmup(windows=a.windows)
 for _ in range(a.steps):
     q_idx, q = layer.next_queries()
-    layer.attend(q_idx, q)
+    layer.attend(q_idx, q, overlap=a.overlap)
     layer.append_token()
 torch.cuda.synchronize()
 layer.pool.check()
