@@ -73,6 +73,14 @@ const char *ess_status_string(int status);
 /* cudaHostRegister(mapped) + device alias: the host latent store (UVA gather source) */
 int ess_host_register(void *host_ptr, size_t bytes, void **d_alias);
 int ess_host_unregister(void *host_ptr);
+/* allocate + register the host latent store: 2-MB aligned, transparent huge pages
+ * (ESS_HOST_HUGEPAGES), bound to numa_node when >= 0; *placed reports which of the
+ * two took effect.  Free with ess_host_free(host_ptr, bytes). */
+#define ESS_HOST_HUGEPAGES 1
+#define ESS_HOST_NUMA_BOUND 2
+int ess_host_alloc(size_t bytes, int32_t flags, int32_t numa_node, void **host_ptr, void **d_alias,
+                   int32_t *placed);
+int ess_host_free(void *host_ptr, size_t bytes);
 /* diagnostic: write the device global timer (ns) to *d_dst in stream order; works
  * inside captured CUDA graphs (step timelines) */
 int ess_timestamp(uint64_t *d_dst, void *stream);

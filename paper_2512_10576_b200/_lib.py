@@ -23,6 +23,8 @@ SIGNATURES = {
     "ess_host_register": ([V, SZ, PV], ctypes.c_int),
     "ess_host_unregister": ([V], ctypes.c_int),
     "ess_timestamp": ([V, V], ctypes.c_int),
+    "ess_host_alloc": ([SZ, I32, I32, PV, PV, PI32], ctypes.c_int),
+    "ess_host_free": ([V, SZ], ctypes.c_int),
     "ess_pool_create": ([PV, I32, I64, I32, I32, I32], ctypes.c_int),
     "ess_pool_destroy": ([V], ctypes.c_int),
     "ess_pool_reset": ([V, I32, I32, V, V], ctypes.c_int),
@@ -54,6 +56,7 @@ ESS_ACCESS_SORT_EVICTED = 1
 ESS_MLA_PARTIAL, ESS_MLA_RESUME = 1, 2
 ESS_GATHER_EXCLUSIVE_SM = 1
 ESS_GATHER_BULK = 2
+ESS_HOST_HUGEPAGES, ESS_HOST_NUMA_BOUND = 1, 2
 MAX_REQUEST = 2048
 LATENT_ROW_BYTES = 656   # host store / transfer format (e4m3 NoPE + scales + bf16 RoPE)
 HOST_ROW_PITCH = 704     # host store row pitch (64-B aligned rows; ESS_HOST_ROW_PITCH)

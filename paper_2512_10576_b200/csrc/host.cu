@@ -1,5 +1,9 @@
 // Library-level entry points: version, status strings, pinned host registration,
 // and the shared host helpers (tensor-map encoding, SM count).
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include <cstring>
 #include <mutex>
 
@@ -92,6 +96,58 @@ int ess_timestamp(uint64_t *d_dst, void *stream) {
   timestamp_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(d_dst);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
+}
+
+// The host latent store, allocated here rather than by the caller: 2-MB aligned anonymous
+// memory, transparent huge pages requested (madvise) so the GPU's zero-copy row reads
+// walk few IOMMU / page-table entries across a multi-GB store, optionally bound to the
+// GPU's NUMA node (mbind; one NUMA-local host pool per GPU), then
+// page-locked and mapped into the device address space.
+namespace {
+constexpr size_t kHugePage = 2u << 20;
+size_t host_span(size_t bytes) { return (bytes + kHugePage - 1) / kHugePage * kHugePage; }
+}  // namespace
+
+int ess_host_alloc(size_t bytes, int32_t flags, int32_t numa_node, void **host_ptr, void **d_alias,
+                   int32_t *placed) {
+  if (!bytes || !host_ptr || !d_alias) return ESS_ERR_ARG;
+  const size_t span = host_span(bytes);
+  void *raw = mmap(nullptr, span + kHugePage, PROT_READ | PROT_WRITE,
+                   MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
+  if (raw == MAP_FAILED) return ESS_ERR_NOMEM;
+  uintptr_t a = (reinterpret_cast<uintptr_t>(raw) + kHugePage - 1) & ~(uintptr_t)(kHugePage - 1);
+  uint8_t *p = reinterpret_cast<uint8_t *>(a);
+  const size_t head = a - reinterpret_cast<uintptr_t>(raw);
+  if (head) munmap(raw, head);
+  const size_t tail = kHugePage - head;
+  if (tail) munmap(p + span, tail);
+  int got = 0;
+  if ((flags & ESS_HOST_HUGEPAGES) && madvise(p, span, MADV_HUGEPAGE) == 0) got |= ESS_HOST_HUGEPAGES;
+  if (numa_node >= 0 && numa_node < 64) {
+    unsigned long mask = 1ul << numa_node;
+    // MPOL_BIND = 2; the pages are first touched by cudaHostRegister below
+    if (syscall(SYS_mbind, p, span, 2, &mask, 64, 0) == 0) got |= ESS_HOST_NUMA_BOUND;
+  }
+  cudaError_t e = cudaHostRegister(p, span, cudaHostRegisterMapped | cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    munmap(p, span);
+    return e == cudaErrorMemoryAllocation ? ESS_ERR_NOMEM : ESS_ERR_CUDA;
+  }
+  if (cudaHostGetDevicePointer(d_alias, p, 0) != cudaSuccess) {
+    cudaHostUnregister(p);
+    munmap(p, span);
+    return ESS_ERR_CUDA;
+  }
+  *host_ptr = p;
+  if (placed) *placed = got;
+  return ESS_OK;
+}
+
+int ess_host_free(void *host_ptr, size_t bytes) {
+  if (!host_ptr || !bytes) return ESS_ERR_ARG;
+  const cudaError_t e = cudaHostUnregister(host_ptr);
+  munmap(host_ptr, host_span(bytes));
+  return e == cudaSuccess ? ESS_OK : ESS_ERR_CUDA;
 }
 
 int ess_host_unregister(void *host_ptr) {

@@ -10,10 +10,13 @@
 // the whole TMEM of one SM, so each request runs on two CTAs that own 256 output
 // dims each and both compute the full score tile S.  Per CTA (512 TMEM columns):
 //   O      [0,256)    fp32 accumulator, 128 heads x 256 dims
-//   S0/S1  [256,320)  fp32 scores, 32 rows each; P (f16) overwrites the first 16
+//   S0..S2 [256,352)  fp32 scores, 32 rows each; P (f16) overwrites the first 16
 //                     columns of its S buffer and feeds PV straight from TMEM
-//   Qt     [320,512)  q dims 0..383 as f16 pairs: the A operand of S from TMEM
-// Shared memory: q dims 384..575 (SW128 K-major, 48 KB), a 4-deep ring of KV tiles
+//   Qt     [352,512)  q dims 0..319 as f16 pairs: the A operand of S from TMEM
+// Three S buffers let the MMA warp issue S(i+1) and S(i+2) before PV(i), so the
+// softmax of tile i and the p_full -> PV hand-off hide behind two score tiles on
+// the tensor pipe (with two buffers that per-tile round trip set K5's rate).
+// Shared memory: q dims 320..575 (SW128 K-major, 64 KB), a 4-deep ring of KV tiles
 // (32 rows x 576 f16, SW128: 9 blocks of [32 rows][64 dims]) filled by 16-B
 // cp.async straight into the swizzled positions (TMA tile::gather4 moves only
 // 4 x 128 B per instruction and was instruction-rate bound here), and the
@@ -35,16 +38,21 @@ constexpr int QK_DIM = ESS_MLA_QK_DIM;    // 576
 constexpr int V_HALF = 256;               // output dims per CTA
 constexpr int NB = 32;                    // KV rows per tile
 constexpr int NBLK = QK_DIM / 64;         // 9 dim-blocks of 64 (128 B of f16)
-constexpr int QT_BLKS = 6;                // q blocks held in TMEM (dims 0..383)
-constexpr int QS_BLKS = NBLK - QT_BLKS;   // q blocks in shared memory (dims 384..575)
+#ifndef ESS_MLA_NSB
+#define ESS_MLA_NSB 2
+#endif
+#ifndef ESS_MLA_QT_BLKS
+#define ESS_MLA_QT_BLKS 6
+#endif
+constexpr int QT_BLKS = ESS_MLA_QT_BLKS;  // q blocks held in TMEM (dims 0..64*QT_BLKS-1)
+constexpr int QS_BLKS = NBLK - QT_BLKS;   // q blocks in shared memory (dims 320..575)
+constexpr int NSB = ESS_MLA_NSB;          // S/P buffers: S(i+NSB-1) is issued before PV(i)
+constexpr int LOOKAHEAD = NSB - 1;
 constexpr int QBLK_BYTES = HEADS * 128;            // one [128 heads][64 dims] block
-constexpr int QS_BYTES = QS_BLKS * QBLK_BYTES;     // 49152
+constexpr int QS_BYTES = QS_BLKS * QBLK_BYTES;     // 65536
 constexpr int KV_BLK_BYTES = NB * 128;             // 4096
 constexpr int KV_BYTES = NBLK * KV_BLK_BYTES;      // 36864
 constexpr int KS = 4;                              // KV ring depth
-#ifndef ESS_MLA_LOAD_LAG
-#define ESS_MLA_LOAD_LAG 1
-#endif
 #ifndef ESS_MLA_DBG_NOLOAD  // timing-only switches for scratch builds (scripts/variant_lib.sh)
 #define ESS_MLA_DBG_NOLOAD 0
 #endif
@@ -57,17 +65,17 @@ constexpr int KS = 4;                              // KV ring depth
 #ifndef ESS_MLA_DBG_NOSOFT
 #define ESS_MLA_DBG_NOSOFT 0
 #endif
-constexpr int LOAD_LAG = ESS_MLA_LOAD_LAG;         // tiles in flight per loader beyond the newest
-// the MMA warp issues S(i+1) before PV(i) frees slot i, so a loader may run at most
-// KS - 2 tiles ahead of its newest complete tile
-static_assert(LOAD_LAG >= 1 && LOAD_LAG <= KS - 2, "loader lag must leave the MMA a lookahead slot");
+// the MMA warp issues S(i+LOOKAHEAD) before PV(i) frees slot i: the ring must hold
+// tiles i..i+LOOKAHEAD at once
+static_assert(KS >= LOOKAHEAD + 1, "KV ring too shallow for the S lookahead");
 constexpr int MAX_N = ESS_MAX_REQUEST;
 constexpr int NSOFT = 4, NLOAD = 4;
 constexpr int MMA_WARP = NSOFT, LOAD0 = NSOFT + 1;
 constexpr int NTHREADS = 32 * (NSOFT + 1 + NLOAD);  // 288
 constexpr int ROWS_PER_LOADER = NB / NLOAD;         // 8
 constexpr int SLOT_CHUNKS = ESS_SLOT_ROW_BYTES / 16; // 72
-constexpr uint32_t TM_O = 0, TM_S = 256, TM_Q = 320;
+constexpr uint32_t TM_O = 0, TM_S = 256, TM_Q = TM_S + NSB * NB;  // Q: [352, 512)
+static_assert(TM_Q + QT_BLKS * 32 <= 512, "TMEM budget");
 constexpr float RESCALE_THRESHOLD = 8.0f;
 constexpr int MLA_AWAIT = 4;  // internal flag of ess_sparse_mla_da
 #ifndef ESS_MLA_DBG_SN
@@ -78,7 +86,7 @@ constexpr uint32_t IDESC_PV = make_idesc(0, 0, HEADS, V_HALF, 0, 1 /*B MN-major*
 
 struct Ctrl {
   uint64_t kv_full[KS], kv_empty[KS];
-  uint64_t s_full[2], p_full, p_empty, o_done, q_full;
+  uint64_t s_full[NSB], p_full[NSB], pv_done[NSB], o_done, q_full;
   uint32_t tmem;
 };
 constexpr size_t SMEM_BYTES = 1024 + QS_BYTES + KS * KV_BYTES + MAX_N * 4 + sizeof(Ctrl);
@@ -104,6 +112,11 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32
                : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// arrive on an mbarrier when every cp.async this thread issued so far has completed
+// (the arrive counts toward the barrier's expected count)
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
@@ -151,7 +164,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                       float *__restrict__ ws_o, float *__restrict__ ws_ml, int flags) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t *sq = smem;                        // q dims 384..575, 3 SW128 blocks
+  uint8_t *sq = smem;                        // q dims 320..575, 4 SW128 blocks
   uint8_t *skv = sq + QS_BYTES;              // KS f16 KV tiles
   int32_t *ssel = reinterpret_cast<int32_t *>(skv + KS * KV_BYTES);
   Ctrl &c = *reinterpret_cast<Ctrl *>(ssel + MAX_N);
@@ -168,12 +181,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < KS; i++) {
-      mbar_init(&c.kv_full[i], NLOAD);
+      mbar_init(&c.kv_full[i], NLOAD * 32);  // one cp.async completion arrive per loader thread
       mbar_init(&c.kv_empty[i], 1);
     }
-    for (int i = 0; i < 2; i++) mbar_init(&c.s_full[i], 1);
-    mbar_init(&c.p_full, NSOFT);
-    mbar_init(&c.p_empty, 1);
+    for (int i = 0; i < NSB; i++) {
+      mbar_init(&c.s_full[i], 1);
+      mbar_init(&c.p_full[i], NSOFT);
+      mbar_init(&c.pv_done[i], 1);
+    }
     mbar_init(&c.o_done, 1);
     mbar_init(&c.q_full, 1);
     fence_barrier_init();
@@ -184,9 +199,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_after();
   const uint32_t tmem = c.tmem;
 
-  // ---- prologue: q -> TMEM (dims 0..383) and smem (384..575); slot ids -> smem ----
-  // Nine TMA box loads of [128 heads][64 dims] bf16 (SW128): blocks 6..8 land in their
-  // final shared-memory place and are converted to f16 in place; blocks 0..5 land in
+  // ---- prologue: q -> TMEM (dims 0..319) and smem (320..575); slot ids -> smem ----
+  // Nine TMA box loads of [128 heads][64 dims] bf16 (SW128): blocks 5..8 land in their
+  // final shared-memory place and are converted to f16 in place; blocks 0..4 land in
   // the still-empty KV ring, where each head's 128-B row is read bank-conflict free
   // (the swizzle spreads the 8 lanes of a phase over 8 chunks) and stored to TMEM.
   if (threadIdx.x == 0) {
@@ -223,7 +238,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     tmem_st_wait();
   } else {
-    // warps 4-8: q dims 384..575 to f16 in place (16-B units keep their SW128 position)
+    // warps 4-8: q dims 320..575 to f16 in place (16-B units keep their SW128 position)
     constexpr int NT = NTHREADS - NSOFT * 32;
     uint4 *qs = reinterpret_cast<uint4 *>(sq);
     for (int u = threadIdx.x - NSOFT * 32; u < QS_BYTES / 16; u += NT) qs[u] = cvt8_bf16_f16(qs[u]);
@@ -242,12 +257,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     float *wso = ws_o ? ws_o + hrow * ESS_MLA_V_DIM + v * V_HALF : nullptr;
     float m_run = -INFINITY, l_run = 0.f;  // resume starts a fresh partial, merged at the end
     for (int i = 0; i < ntiles; i++) {
-      const int sb = i & 1;
-      mbar_wait(&c.s_full[sb], (i >> 1) & 1);
+      const int sb = i % NSB;
+      mbar_wait(&c.s_full[sb], (i / NSB) & 1);
       tc_fence_after();
 #if ESS_MLA_DBG_NOSOFT
       __syncwarp();
-      if (lane == 0) mbar_arrive(&c.p_full);
+      if (lane == 0) mbar_arrive(&c.p_full[sb]);
       continue;
 #endif
       uint32_t s[32];
@@ -267,12 +282,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const float alpha = exp2f(m_run - m_new);  // 0 when m_run = -inf
         l_run *= alpha;
         // PV(i-1) accumulates into O: wait for it before O is rescaled.  Only rescale
-        // tiles wait, keeping the MMA round trip off the per-tile path.  The parity
-        // is unambiguous: the s_full(i) commit tracks every earlier MMA, PV(i-2)
-        // included, and PV(i) needs this tile's P, so p_empty has completed phase
-        // i-2 and not phase i.
+        // tiles wait, keeping the MMA round trip off the per-tile path.  pv_done[k % 3]
+        // completes its phase k / 3 when PV(k) is done; the parity is unambiguous: the
+        // s_full(i) commit tracks every MMA issued before S(i), PV(i-3) included, so
+        // that barrier's previous phase (PV(i-4)) is complete, and PV(i+2) needs a P
+        // this warp has not produced yet.
         if (i > 0) {
-          mbar_wait(&c.p_empty, (i & 1) ^ 1);
+          mbar_wait(&c.pv_done[(i - 1) % NSB], ((i - 1) / NSB) & 1);
           tc_fence_after();
         }
         if (i > 0) {  // O holds PV(i-1)
@@ -303,7 +319,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&c.p_full);
+      if (lane == 0) mbar_arrive(&c.p_full[sb]);
     }
     // ---------------- epilogue ---------------------------------------------------
     const bool have_o = ntiles > 0;  // TMEM O holds a valid accumulator
@@ -407,47 +423,45 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   } else if (warp == MMA_WARP) {
     // ---------------- MMA issuer --------------------------------------------------
     if (elect_one() && ntiles > 0) {
-      const uint32_t qsaddr = smem_u32(sq);
+      const uint64_t abase = sw128_desc(smem_u32(sq), 16, 1024);
       auto issue_s = [&](int i) {
-        const int kb = i % KS, sb = i & 1;
-        // S(i) overwrites S/P buffer sb, last read by PV(i-2) as its A operand.  No
-        // wait: softmax(i-2) finished with the buffer before p_full(i-2), PV(i-2) was
+        const int kb = i % KS, sb = i % NSB;
+        // S(i) overwrites S/P buffer sb, last read by PV(i-3) as its A operand.  No
+        // wait: softmax(i-3) finished with the buffer before p_full(i-3), PV(i-3) was
         // issued before this S(i), and one thread's tcgen05.mma ops execute in issue
-        // order — waiting for PV(i-2) to complete would idle the tensor pipe each tile.
+        // order — waiting for PV(i-3) to complete would idle the tensor pipe each tile.
         mbar_wait(&c.kv_full[kb], (i / KS) & 1);
+        fence_proxy_async_smem();  // cp.async (generic proxy) rows -> tensor-core reads
         tc_fence_after();
-        const uint32_t kvaddr = smem_u32(skv + kb * KV_BYTES);
         const uint32_t d = tmem + TM_S + sb * NB;
-#pragma unroll 1
-        for (int blk = 0; blk < QT_BLKS; blk++) {
+        // descriptors as base + compile-time offsets (the 14-bit address field cannot
+        // carry: shared memory ends below 2^18 B), so the fully unrolled 36-MMA
+        // sequence issues back to back instead of rebuilding each descriptor
+        const uint64_t bbase = sw128_desc(smem_u32(skv + kb * KV_BYTES), 16, 1024);
+#pragma unroll
+        for (int blk = 0; blk < NBLK; blk++) {
 #pragma unroll
           for (int kk = 0; kk < 4; kk++) {
-            uint64_t bd = sw128_desc(kvaddr + blk * KV_BLK_BYTES + kk * 32, 16, 1024);
-#if ESS_MLA_DBG_ALLSS
-            mma_f16_ss(d, sw128_desc(qsaddr + (blk % QS_BLKS) * (HEADS * 128) + kk * 32, 16, 1024), bd,
-                       IDESC_S, (blk | kk) ? 1u : 0u);
-#else
-            if (!ESS_MLA_DBG_NOMMA)
-              mma_f16_ts(d, tmem + TM_Q + (blk * 4 + kk) * 8, bd, IDESC_S, (blk | kk) ? 1u : 0u);
-#endif
-          }
-        }
-#pragma unroll 1
-        for (int blk = QT_BLKS; blk < NBLK; blk++) {
-#pragma unroll
-          for (int kk = 0; kk < 4; kk++) {
-            uint64_t ad = sw128_desc(qsaddr + (blk - QT_BLKS) * (HEADS * 128) + kk * 32, 16, 1024);
-            uint64_t bd = sw128_desc(kvaddr + blk * KV_BLK_BYTES + kk * 32, 16, 1024);
-            if (!ESS_MLA_DBG_NOMMA) mma_f16_ss(d, ad, bd, IDESC_S, 1u);
+            const uint64_t bd = bbase + (uint64_t)((blk * KV_BLK_BYTES + kk * 32) >> 4);
+            const uint32_t acc = (blk | kk) ? 1u : 0u;
+            if (ESS_MLA_DBG_NOMMA) continue;
+            if (ESS_MLA_DBG_ALLSS || blk >= QT_BLKS) {
+              const int qb = ESS_MLA_DBG_ALLSS ? blk % QS_BLKS : blk - QT_BLKS;
+              mma_f16_ss(d, abase + (uint64_t)((qb * HEADS * 128 + kk * 32) >> 4), bd, IDESC_S, acc);
+            } else {
+              mma_f16_ts(d, tmem + TM_Q + (blk * 4 + kk) * 8, bd, IDESC_S, acc);
+            }
           }
         }
         tc_commit(&c.s_full[sb]);
       };
-      issue_s(0);
+      // two score tiles in flight ahead of PV: the softmax of tile i and the
+      // p_full -> PV hand-off overlap S(i+1) and S(i+2) on the tensor pipe
+      for (int i = 0; i < LOOKAHEAD && i < ntiles; i++) issue_s(i);
       for (int i = 0; i < ntiles; i++) {
-        if (i + 1 < ntiles) issue_s(i + 1);
-        const int kb = i % KS, sb = i & 1;
-        mbar_wait(&c.p_full, i & 1);
+        if (i + LOOKAHEAD < ntiles) issue_s(i + LOOKAHEAD);
+        const int kb = i % KS, sb = i % NSB;
+        mbar_wait(&c.p_full[sb], (i / NSB) & 1);
         tc_fence_after();
         const uint32_t vaddr = smem_u32(skv + kb * KV_BYTES) + (uint32_t)(4 * v) * KV_BLK_BYTES;
 #pragma unroll
@@ -456,7 +470,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           if (!ESS_MLA_DBG_NOMMA)
             mma_f16_ts(tmem + TM_O, tmem + TM_S + sb * NB + kk * 8, bd, IDESC_PV, (i | kk) ? 1u : 0u);
         }
-        tc_commit(&c.p_empty);
+        tc_commit(&c.pv_done[sb]);
         tc_commit(&c.kv_empty[kb]);
         if (i == ntiles - 1) tc_commit(&c.o_done);
       }
@@ -469,11 +483,6 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int w = warp - LOAD0;
     const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b) * rows_per_pool * ESS_SLOT_ROW_BYTES;
     const uint32_t kv0 = smem_u32(skv);
-    auto signal = [&](int i) {
-      fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&c.kv_full[i % KS]);
-    };
     bool pending = n2 > 0;  // fetched rows not yet known to have landed
     for (int i = 0; i < ntiles; i++) {
       const int kb = i % KS;
@@ -497,14 +506,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                        src + ch * 16, ok ? 16u : 0u);
         }
       }
-      cp_async_commit();
-      if (i >= LOAD_LAG) {
-        cp_async_wait<LOAD_LAG>();
-        signal(i - LOAD_LAG);
-      }
+      // tile i is full once every loader thread's copies landed: each thread's
+      // completion arrives on kv_full by itself, so no loader waits on its own copies
+      // and the ring runs as far ahead as the free slots allow
+      cp_async_arrive_noinc(&c.kv_full[kb]);
     }
     cp_async_wait<0>();
-    for (int i = max(0, ntiles - LOAD_LAG); i < ntiles; i++) signal(i);
   }
   tc_fence_before();
   __syncthreads();

@@ -62,7 +62,7 @@ class DSADecodeLayer:
 
     def __init__(self, batch: int, context_len: int, sparse_ratio: float, topk_k: int = 2048,
                  max_new_tokens: int = 64, device=None, seed: int = 0, drift: float = 0.95,
-                 sm_scale: float = DEFAULT_SM_SCALE):
+                 sm_scale: float = DEFAULT_SM_SCALE, hugepages: bool = True):
         _lib.require_cuda()
         self.device = torch.device(device if device is not None else "cuda")
         self.B, self.ctx, self.rho, self.K = batch, context_len, sparse_ratio, topk_k
@@ -78,7 +78,7 @@ class DSADecodeLayer:
         self.k_cache = _e4m3(torch.randn((B, self.Lmax, 128), device=d, generator=g) * 8.0)
         self.k_scale = torch.rand((B, self.Lmax), device=d, generator=g) * 0.5 + 0.75
         # host latent store (pinned, mapped) + GPU slot pool
-        self.store = HostLatentStore(B, self.Lmax)
+        self.store = HostLatentStore(B, self.Lmax, hugepages=hugepages, device=self.device)
         for b in range(B):  # fill through the GPU: random rows copied into pinned memory
             self.store.host[b].copy_(random_latent_rows(self.Lmax, d, g), non_blocking=False)
         self.cap0 = pool_capacity(sparse_ratio, context_len)

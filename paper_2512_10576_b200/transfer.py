@@ -68,26 +68,47 @@ def transfer_time(model: TransferModel, blocks: int, direction: str) -> float:
     return us
 
 
+def gpu_numa_node(device=None) -> int | None:
+    """NUMA node of the GPU's PCI function (sysfs), None when unknown."""
+    try:
+        props = torch.cuda.get_device_properties(device if device is not None else torch.cuda.current_device())
+        bus = f"{props.pci_domain_id:04x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+        with open(f"/sys/bus/pci/devices/{bus}/numa_node") as f:
+            node = int(f.read().strip())
+        return node if node >= 0 else None
+    except (OSError, ValueError, AttributeError, RuntimeError):
+        return None
+
+
 class HostLatentStore:
     """[pools, rows_per_pool] latent rows of 656 B in page-locked, device-mapped host
     memory, laid out at the ESS_HOST_ROW_PITCH (704-B) pitch so every row starts on a
     64-B host-link request boundary.  ``host`` is the [pools, rows, 656] view."""
 
-    def __init__(self, num_pools: int, rows_per_pool: int):
+    def __init__(self, num_pools: int, rows_per_pool: int, hugepages: bool = True,
+                 numa_node: int | None = None, device=None):
         _lib.require_cuda()
         self.num_pools, self.rows_per_pool = num_pools, rows_per_pool
         self.row_bytes, self.pitch = LATENT_BLOCK_BYTES, _lib.HOST_ROW_PITCH
-        self._buf = torch.empty((num_pools, rows_per_pool, self.pitch), dtype=torch.uint8)
+        n = num_pools * rows_per_pool * self.pitch
+        node = gpu_numa_node(device) if numa_node is None else numa_node
+        hp, alias, placed = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int32(0)
+        _lib.check(_lib.load().ess_host_alloc(n, _lib.ESS_HOST_HUGEPAGES if hugepages else 0,
+                                              -1 if node is None else node, ctypes.byref(hp),
+                                              ctypes.byref(alias), ctypes.byref(placed)),
+                   "ess_host_alloc")
+        self._host_ptr, self._nbytes = hp.value, n
+        self.hugepages = bool(placed.value & _lib.ESS_HOST_HUGEPAGES)
+        self.numa_node = node if placed.value & _lib.ESS_HOST_NUMA_BOUND else None
+        raw = (ctypes.c_uint8 * n).from_address(hp.value)
+        self._buf = torch.frombuffer(raw, dtype=torch.uint8).view(num_pools, rows_per_pool, self.pitch)
         self.host = self._buf[:, :, :self.row_bytes]
-        alias = ctypes.c_void_p()
-        _lib.check(_lib.load().ess_host_register(self._buf.data_ptr(), self._buf.numel(),
-                                                 ctypes.byref(alias)), "ess_host_register")
         self.device_ptr = alias.value
         self._registered = True
 
     @property
     def nbytes(self) -> int:
-        return self._buf.numel()
+        return self._nbytes
 
     def pool_ptr(self, begin: int) -> int:
         return self.device_ptr + begin * self.rows_per_pool * self.pitch
@@ -95,8 +116,9 @@ class HostLatentStore:
     def close(self):
         if getattr(self, "_registered", False):
             torch.cuda.synchronize()
-            _lib.load().ess_host_unregister(self._buf.data_ptr())
             self._registered = False
+            self.host = self._buf = None
+            _lib.load().ess_host_free(self._host_ptr, self._nbytes)
 
     def __del__(self):
         try:

@@ -9,10 +9,11 @@ if len(sys.argv) > 1:
 from paper_2512_10576_b200.cache import AccessBatch, PoolSet
 from paper_2512_10576_b200.transfer import HostLatentStore, gather
 
-B, cap, hist = 64, 8192, 32768
+B, cap, hist = 64, 8192, int(os.environ.get("HIST", 32768))
 M = int(os.environ.get("M", 120))
 pools = PoolSet(B, hist, cap, cap, row_bytes=1152)
-store = HostLatentStore(B, hist)
+store = HostLatentStore(B, hist, hugepages=os.environ.get("HP", "1") == "1")
+print(f"host store {store.nbytes / 2**30:.2f} GiB hugepages={store.hugepages} numa={store.numa_node}")
 store.host.random_(0, 256)
 g = torch.Generator(device="cuda").manual_seed(0)
 K = 2048
