@@ -148,9 +148,16 @@ class DSADecodeLayer:
                            hit_row=acc.hit_row[a:b])
 
     def micro_batches(self, n: int):
-        """[a, b) request ranges of the DBA split (contiguous, sizes differ by <= 1)."""
+        """[a, b) request ranges of the DBA split: contiguous; the first holds
+        ``first_frac`` of the batch when set (a small first micro-batch starts the
+        host-link gather early), the rest split evenly."""
         n = max(1, min(n, self.B))
-        edges = [self.B * i // n for i in range(n + 1)]
+        ff = getattr(self, "first_frac", None)
+        if n == 1 or not ff:
+            edges = [self.B * i // n for i in range(n + 1)]
+        else:
+            f = min(self.B - (n - 1), max(1, round(self.B * ff)))
+            edges = [0] + [f + (self.B - f) * i // (n - 1) for i in range(n)]
         return [(edges[i], edges[i + 1]) for i in range(n)]
 
     def attend(self, q_idx, q, gather_ctas: int = 32, overlap: str = "dba", new_rows=None,
@@ -202,16 +209,32 @@ class DSADecodeLayer:
         fused = self.fuse_da and 2 * B <= sms - 8
         gsms = max(8, sms - 2 * B)  # attention takes 2 CTAs per request (one SM each)
         ranges = self.micro_batches(micro if overlap == "dba" else 1)
+        if getattr(self, "_sel", None) is None:
+            self._sel = torch.cuda.Stream(self.device)
+        sel = self._sel
         ready = None
+        prev = 0  # requests of the previous micro-batch (its K2/K3 run beside this K1)
         for i, (a, b) in enumerate(ranges):
-            # later micro-batches' indexers leave the gather's SMs free
-            self._select(q_idx, a, b, max_ctas=sms - gsms if i > 0 else 0)
-            ready = torch.cuda.Event()
-            ready.record(main)
+            # K1 of micro-batch i on the main stream; its top-k and cache manager on the
+            # selection stream, so they overlap the NEXT micro-batch's indexer, which
+            # leaves SMs free for them (one per request) and for the running gather
+            ctas = 0 if i == 0 else sms - gsms - prev
+            indexer_logits(q_idx[a:b], self.w[a:b], self.k_cache[a:b], self.k_scale[a:b],
+                           self.lens[a:b], out=self.logits[a:b], max_ctas=ctas)
+            scored = torch.cuda.Event()
+            scored.record(main)
+            sel.wait_event(scored)
+            with torch.cuda.stream(sel):
+                topk(self.logits[a:b], self.lens[a:b], self.K, out=self.idx[a:b], count=self.cnt[a:b])
+                self.pool.access(self.idx[a:b], self.cnt[a:b], begin=a, out=self._acc_view(a, b))
+                ready = torch.cuda.Event()
+                ready.record(sel)
             side.wait_event(ready)
             with torch.cuda.stream(side):
                 gather(self.pool, self.store, self._acc_view(a, b), begin=a, max_ctas=gsms,
                        exclusive=True, landed=self._landed[a:b] if fused else None)
+            prev = b - a
+        main.wait_event(ready)  # attention reads every micro-batch's selections
         if new_rows is not None:
             if getattr(self, "_adm", None) is None:
                 self._adm = torch.cuda.Stream(self.device)
