@@ -30,6 +30,24 @@ constexpr int NT = 1024;                 // threads per pool CTA
 constexpr int MAXR = ESS_MAX_REQUEST;    // 2048 ids per call
 constexpr int EPT = MAXR / NT;           // elements per thread (contiguous)
 constexpr int ROW_CHUNKS = ESS_LATENT_ROW_BYTES / 16;  // 41 x 16 B
+#ifdef ESS_POOL_PROF  // scratch builds: per-phase globaltimer stamps of K3 (thread 0)
+__device__ unsigned long long g_pool_prof[256][16];
+#define PPROF(i)                                                              \
+  do {                                                                        \
+    __syncthreads();                                                          \
+    if (threadIdx.x == 0 && blockIdx.x < 256) {                               \
+      unsigned long long tt;                                                  \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                  \
+      g_pool_prof[blockIdx.x][i] = tt;                                        \
+    }                                                                         \
+  } while (0)
+#else
+#define PPROF(i) \
+  do {           \
+  } while (0)
+#endif
+constexpr int POOL_STAGED = 1 << 30;     // internal access flag: stage keys/slot ids in smem
+constexpr size_t STAGE_SMEM_MAX = 180 * 1024;
 
 
 enum { MODE_ACCESS = 0, MODE_WARMUP = 1 };
@@ -64,6 +82,16 @@ PoolView view(const ess_pool *p) {
                   p->max_ids, p->cap_max, p->row_bytes, p->staging, p->rows_per_pool};
 }
 
+// Histogram add with warp aggregation: lanes hitting the same bin add once (popc).
+// Stamps are clustered (a recent clock window), so the high-digit passes would
+// otherwise serialise 1024 shared-memory atomics on one or two bins.
+__device__ __forceinline__ void hist_add_warp(int *hist, uint32_t bin, bool active) {
+  const unsigned am = __ballot_sync(0xffffffffu, active);
+  if (!active) return;
+  const unsigned peers = __match_any_sync(am, bin);
+  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], __popc(peers));
+}
+
 // k-th smallest (1-based) of keys[0:cnt) — keys are unique, so exactly kth keys
 // are <= the result.  4 passes of 8-bit digits, histogram in shared memory.
 __device__ uint32_t select_kth_smallest(const uint32_t *__restrict__ keys, int cnt, int kth,
@@ -73,9 +101,10 @@ __device__ uint32_t select_kth_smallest(const uint32_t *__restrict__ keys, int c
   for (int shift = 24; shift >= 0; shift -= 8) {
     for (int i = threadIdx.x; i < 256; i += NT) sm.hist[i] = 0;
     __syncthreads();
-    for (int s = threadIdx.x; s < cnt; s += NT) {
-      uint32_t k = keys[s];
-      if ((k & mask) == prefix) atomicAdd(&sm.hist[(k >> shift) & 255u], 1);
+    for (int s0 = 0; s0 < cnt; s0 += NT) {  // uniform trip count: warp-collective adds
+      const int s = s0 + threadIdx.x;
+      const uint32_t k = s < cnt ? keys[s] : 0u;
+      hist_add_warp(sm.hist, (k >> shift) & 255u, s < cnt && (k & mask) == prefix);
     }
     __syncthreads();
     if (threadIdx.x < 32) {
@@ -112,6 +141,117 @@ __device__ uint32_t select_kth_smallest(const uint32_t *__restrict__ keys, int c
     __syncthreads();
   }
   return prefix;
+}
+
+// k-th smallest (1-based) of the unique keys[0:cnt) via two passes of 11-bit digits
+// over a narrow key range.  Free slots (key = slot index < ESS_CLOCK_BASE) come first
+// in key order; they are counted, and the select then runs over whichever class holds
+// the k-th key: the free slots (range < cap) or the residents, whose stamps span a
+// recent clock window.  2048-bin histograms live in `h` (2048 ints of shared memory).
+// Returns false (T untouched) when that class spans 2^22 or more; the caller then
+// falls back to select_kth_smallest.
+__device__ bool select_kth_narrow(const uint32_t *__restrict__ keys, int cnt, int kth, StepSmem &sm,
+                                  int *h, uint32_t *T) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  uint32_t mn = 0xFFFFFFFFu, mx = 0u;
+  int nfree = 0;
+  for (int s = t; s < cnt; s += NT) {
+    const uint32_t k = keys[s];
+    if (k < ESS_CLOCK_BASE) {
+      nfree++;
+    } else {
+      mn = min(mn, k);
+      mx = max(mx, k);
+    }
+  }
+  mn = __reduce_min_sync(0xffffffffu, mn);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  nfree = __reduce_add_sync(0xffffffffu, nfree);
+  uint32_t *red = reinterpret_cast<uint32_t *>(sm.hist);  // [0,32) min, [32,64) max, [64,96) free
+  if (lane == 0) {
+    red[warp] = mn;
+    red[32 + warp] = mx;
+    red[64 + warp] = (uint32_t)nfree;
+  }
+  __syncthreads();
+  mn = __reduce_min_sync(0xffffffffu, red[lane]);
+  mx = __reduce_max_sync(0xffffffffu, red[32 + lane]);
+  nfree = (int)__reduce_add_sync(0xffffffffu, red[64 + lane]);
+  __syncthreads();  // red aliases the histogram zeroed below
+  // the class holding the k-th key: [lo, hi] and the rank inside it
+  uint32_t lo, hi;
+  int rem = kth;
+  if (kth <= nfree) {
+    lo = 0;
+    hi = ESS_CLOCK_BASE - 1;
+    mx = (uint32_t)cnt;  // free keys are slot indices < cnt
+  } else {
+    lo = mn;
+    hi = 0xFFFFFFFFu;
+    rem = kth - nfree;
+  }
+  const uint32_t range = kth <= nfree ? (uint32_t)cnt : mx - mn;
+  if (range >> 22) return false;  // uniform: every thread read the same values
+  const int bits = 32 - __clz((int)(range | 1u));
+  const int shift = bits > 11 ? bits - 11 : 0;
+  uint32_t prefix = 0;
+  for (int pass = 0; pass < (shift ? 2 : 1); pass++) {
+    for (int i = t; i < 2048; i += NT) h[i] = 0;
+    __syncthreads();
+    for (int s = t; s < cnt; s += NT) {
+      const uint32_t k = keys[s];
+      const uint32_t rel = k - lo;
+      const bool in = k >= lo && k <= hi;
+      const bool on = in && (pass == 0 || (rel >> shift) == prefix);
+      // plain atomics: 2048 bins spread the clustered stamps enough (merging equal-bin
+      // lane runs or match_any aggregation measured slower here)
+      if (on) atomicAdd(&h[pass == 0 ? rel >> shift : rel & ((1u << shift) - 1u)], 1);
+    }
+    __syncthreads();
+    const int v0 = h[2 * t], v1 = h[2 * t + 1];
+    int tot;
+    const int ex = block_exclusive_scan<NT>(v0 + v1, sm.warp, &tot);
+    if (ex < rem && rem <= ex + v0 + v1) {
+      const bool first = rem <= ex + v0;
+      sm.scal[0] = 2 * t + (first ? 0 : 1);
+      sm.scal[1] = rem - ex - (first ? 0 : v0);
+    }
+    __syncthreads();
+    prefix = pass == 0 ? (uint32_t)sm.scal[0] : (prefix << shift) | (uint32_t)sm.scal[0];
+    rem = sm.scal[1];
+    __syncthreads();
+  }
+  *T = lo + prefix;
+  return true;
+}
+
+// Ascending slot indices s < cnt with keys[s] <= T into out[0:MAXR): warp ballots per
+// 32-slot group, one block scan over the (chunk, warp) counts (in `c`, 2048 ints), a
+// second ballot pass writes.  cnt <= 64 * NT.
+__device__ void compact_le(const uint32_t *__restrict__ keys, int cnt, uint32_t T, StepSmem &sm,
+                           int *c, int *out) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int nch = (cnt + NT - 1) / NT;
+  for (int ch = 0; ch < nch; ch++) {
+    const int s = ch * NT + t;
+    const unsigned bal = __ballot_sync(0xffffffffu, s < cnt && keys[s] <= T);
+    if (lane == 0) c[ch * 32 + warp] = __popc(bal);
+  }
+  for (int i = nch * 32 + t; i < 2048; i += NT) c[i] = 0;
+  __syncthreads();
+  const int v0 = c[2 * t], v1 = c[2 * t + 1];
+  int tot;
+  const int ex = block_exclusive_scan<NT>(v0 + v1, sm.warp, &tot);
+  c[2 * t] = ex;
+  c[2 * t + 1] = ex + v0;
+  __syncthreads();
+  for (int ch = 0; ch < nch; ch++) {
+    const int s = ch * NT + t;
+    const bool f = s < cnt && keys[s] <= T;
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    const int pos = c[ch * 32 + warp] + __popc(bal & ((1u << lane) - 1u));
+    if (f && pos < MAXR) out[pos] = s;
+  }
 }
 
 // Ascending bitonic sort of sm.ev[0:n), n <= MAXR.
@@ -177,6 +317,7 @@ __global__ void __launch_bounds__(NT, 1)
                      int out_stride, int flags,
                      int64_t *inserted_out) {
   __shared__ StepSmem sm;
+  extern __shared__ uint32_t stage_smem[];  // [cap_max] keys (STAGED)
   const int t = threadIdx.x;
   const int b = blockIdx.x;
   const int p = begin + b;
@@ -189,16 +330,36 @@ __global__ void __launch_bounds__(NT, 1)
   const int size0 = meta->size;
   const uint32_t clk = meta->clk;
   const int64_t out_base = (int64_t)b * out_stride;
+  PPROF(0);
+  // STAGED: the pool's keys are copied to shared memory once, so the victim
+  // select's passes and its compaction read on-chip
+  // instead of paying an HBM round trip per pass (the state is evicted from L2 by
+  // the indexer stream between steps).  Global copies stay authoritative: every
+  // write below goes to both.
+  const bool staged = (flags & POOL_STAGED) != 0;
+  uint32_t *skey = stage_smem;
+  const uint32_t *kread = staged ? skey : key;
+  const int32_t *sread = slot_id;
 
   // ---- load + validate -------------------------------------------------------
   bool bad = n < 0 || n > MAXR || (uint64_t)clk + (uint64_t)n > 0xFFFFFF00ull;
-  int hflag[EPT];
+  int hflag[EPT], xs[EPT];
+#pragma unroll
+  for (int e = 0; e < EPT; e++) {
+    const int i = t * EPT + e;
+    xs[e] = (!bad && i < n) ? req[(int64_t)b * req_stride + i] : 0;
+  }
+  // the key staging loads go out while the requested ids are in flight
+  if (staged) {
+#pragma unroll 4
+    for (int s2 = t; s2 < cap; s2 += NT) skey[s2] = key[s2];
+  }
 #pragma unroll
   for (int e = 0; e < EPT; e++) {
     int i = t * EPT + e;
     hflag[e] = 0;
     if (!bad && i < n) {
-      int x = req[(int64_t)b * req_stride + i];
+      int x = xs[e];
       if (x < 0 || x >= pv.max_ids) {
         bad = true;
       } else {
@@ -217,6 +378,7 @@ __global__ void __launch_bounds__(NT, 1)
     return;
   }
 
+  PPROF(1);
   // ---- hit / miss split in requested order (cache.py:98-99) ---------------------
   int nh_local = 0;
 #pragma unroll
@@ -240,6 +402,7 @@ __global__ void __launch_bounds__(NT, 1)
     }
   }
 
+  PPROF(2);
   int nev = 0;
   int64_t inserted = 0;
   if (MODE == MODE_WARMUP) {
@@ -298,22 +461,36 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
     for (int e = 0; e < EPT; e++) {
       int i = t * EPT + e;
-      if (i < n && hflag[e])
-        key[sm.slot[i]] = (MODE == MODE_ACCESS) ? clk + hrank[e] : clk + i;
+      if (i < n && hflag[e]) {
+        const uint32_t st = (MODE == MODE_ACCESS) ? clk + hrank[e] : clk + i;
+        key[sm.slot[i]] = st;
+        if (staged) skey[sm.slot[i]] = st;
+      }
     }
     __syncthreads();
+    PPROF(3);
     if (nmiss > 0) {
-      const uint32_t T = select_kth_smallest(key, cap, nmiss, sm);
-      int base = 0;
-      for (int s0 = 0; s0 < cap; s0 += NT) {
-        int s = s0 + t;
-        int f = (s < cap && key[s] <= T) ? 1 : 0;
-        int tot;
-        int pos = block_exclusive_scan<NT>(f, sm.warp, &tot);
-        if (f && base + pos < MAXR) sm.sel[base + pos] = s;
-        base += tot;
+      // sm.ev is free until the victims are listed: it serves as the 2048-bin
+      // histogram of the narrow select and the count table of the compaction
+      uint32_t T;
+      if (!select_kth_narrow(kread, cap, nmiss, sm, sm.ev, &T)) T = select_kth_smallest(kread, cap, nmiss, sm);
+      PPROF(4);
+      // the nmiss selected slots in ascending order (exactly nmiss keys are <= T)
+      if (cap <= 64 * NT) {
+        compact_le(kread, cap, T, sm, sm.ev, sm.sel);
+      } else {
+        int base = 0;
+        for (int s0 = 0; s0 < cap; s0 += NT) {
+          int s2 = s0 + t;
+          int f = (s2 < cap && kread[s2] <= T) ? 1 : 0;
+          int tot;
+          int pos = block_exclusive_scan<NT>(f, sm.warp, &tot);
+          if (f && base + pos < MAXR) sm.sel[base + pos] = s2;
+          base += tot;
+        }
       }
       __syncthreads();
+      PPROF(5);
       // victims: selected slots that were occupied (least recent first is not needed:
       // the set is what matters, evicted_ids is reported sorted, cache.py:120)
       int ef[EPT], eid[EPT], ne_local = 0;
@@ -322,7 +499,7 @@ __global__ void __launch_bounds__(NT, 1)
         int j = t * EPT + e;
         ef[e] = 0;
         if (j < nmiss) {
-          int old = slot_id[sm.sel[j]];
+          int old = sread[sm.sel[j]];
           eid[e] = old;
           ef[e] = old >= 0;
           ne_local += ef[e];
@@ -428,6 +605,7 @@ __global__ void __launch_bounds__(NT, 1)
   }
   __syncthreads();
 
+  PPROF(6);
   // ---- outputs + counters -----------------------------------------------------
   if (MODE == MODE_ACCESS) {
     if (sel_row_out) {
@@ -449,6 +627,7 @@ __global__ void __launch_bounds__(NT, 1)
       for (int j = t; j < nev; j += NT) ev_out[out_base + j] = sm.ev[j];
     }
   }
+  PPROF(7);
   if (t == 0) {
     if (MODE == MODE_ACCESS) {
       meta->hits += nhit;
@@ -1094,12 +1273,31 @@ int ess_pool_access(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_re
       out_stride < 1)
     return ESS_ERR_ARG;
   if (num == 0) return ESS_OK;
-  pool_step_kernel<MODE_ACCESS><<<num, NT, 0, (cudaStream_t)stream>>>(
+  if (flags & POOL_STAGED) return ESS_ERR_ARG;
+  const size_t stage = (size_t)p->cap_max * 4;
+  size_t smem = 0;
+  if (stage <= STAGE_SMEM_MAX) {
+    static size_t attr = 0;  // largest opt-in so far
+    if (stage > attr) {
+      ESS_CUDA_TRY(cudaFuncSetAttribute(pool_step_kernel<MODE_ACCESS>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage));
+      attr = stage;
+    }
+    smem = stage;
+    flags |= POOL_STAGED;
+  }
+  pool_step_kernel<MODE_ACCESS><<<num, NT, smem, (cudaStream_t)stream>>>(
       view(p), begin, d_req, d_n, req_stride, d_hit_ids, d_miss_ids, d_evicted_ids, d_sel_row,
       d_hit_row, d_miss_row, d_counts, out_stride, flags, nullptr);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }
+
+#ifdef ESS_POOL_PROF
+int ess_debug_pool_prof(unsigned long long *host) {
+  return cudaMemcpyFromSymbol(host, g_pool_prof, sizeof(g_pool_prof)) == cudaSuccess ? 0 : -7;
+}
+#endif
 
 int ess_pool_append(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_ids,
                     const int32_t *d_m, int32_t stride, int32_t *d_slot_out, void *stream) {
