@@ -27,6 +27,26 @@
 
 namespace cg = cooperative_groups;
 
+#ifdef ESS_TOPK_PROF  // scratch builds: per-phase globaltimer stamps (thread 0 of each CTA)
+__device__ unsigned long long g_topk_prof[1024][8];
+#define KPROF(i)                                                             \
+  do {                                                                       \
+    __syncthreads();                                                         \
+    if (threadIdx.x == 0 && blockIdx.x < 1024) {                             \
+      unsigned long long tt;                                                 \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                 \
+      g_topk_prof[blockIdx.x][i] = tt;                                       \
+    }                                                                        \
+  } while (0)
+extern "C" int ess_debug_topk_prof(unsigned long long *host) {
+  return cudaMemcpyFromSymbol(host, g_topk_prof, sizeof(g_topk_prof)) == cudaSuccess ? 0 : -7;
+}
+#else
+#define KPROF(i) \
+  do {           \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr int NT = 1024;                  // threads per CTA
@@ -153,6 +173,7 @@ __global__ void __launch_bounds__(NT, 1)
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
+  KPROF(0);
   for (int i = threadIdx.x; i < D1_BINS; i += NT) hist[i] = 0;
   __syncthreads();
 
@@ -189,34 +210,60 @@ __global__ void __launch_bounds__(NT, 1)
       atomicAdd(&hist[key >> D1_SHIFT], 1);
     }
   }
+  KPROF(1);
   cluster_sync<CLN>();  // every slice histogram complete and visible cluster-wide
   pick_digit<D1_BINS, CLN>(hist, k, wbuf, scal);
   const uint32_t d1 = (uint32_t)scal[0];
   int rem = scal[1];
   cluster_sync<CLN>();  // peers finished reading our histogram before it is reused
 
+  KPROF(2);
   // ---- list = slice keys with first digit >= d1, in row order -----------------------
   const int cw = (((n + NW - 1) / NW) + 31) & ~31;
   const int lo = min(n, warp * cw), hi = min(n, lo + cw);
+  // the list pass: warp-contiguous runs of whole 128-key chunks (n rounds up to a
+  // multiple of 4 inside the slice allocation; keys past n are masked by hi4 = n)
+  const int cw4 = (((n + NW - 1) / NW) + 127) & ~127;
+  const int lo4 = min(n, warp * cw4), hi4 = min(n, lo4 + cw4);
+  // 128-key chunks: each lane reads 4 consecutive keys with one 16-B shared load and
+  // the 4 ballots (one per vector slot) give every key's rank in row order
   int cnt = 0;
-  for (int i = lo; i < hi; i += 32) {
-    const int j = i + lane;
-    cnt += __popc(__ballot_sync(0xffffffffu, j < hi && (skey[j] >> D1_SHIFT) >= d1));
+#pragma unroll 2
+  for (int i = lo4; i < hi4; i += 128) {
+    const int j = i + lane * 4;
+    const uint4 kv = *reinterpret_cast<const uint4 *>(skey + j);
+    const uint32_t b0 = __ballot_sync(0xffffffffu, j + 0 < hi4 && (kv.x >> D1_SHIFT) >= d1);
+    const uint32_t b1 = __ballot_sync(0xffffffffu, j + 1 < hi4 && (kv.y >> D1_SHIFT) >= d1);
+    const uint32_t b2 = __ballot_sync(0xffffffffu, j + 2 < hi4 && (kv.z >> D1_SHIFT) >= d1);
+    const uint32_t b3 = __ballot_sync(0xffffffffu, j + 3 < hi4 && (kv.w >> D1_SHIFT) >= d1);
+    cnt += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
   }
   int m;
   int base = block_exclusive_scan<NT>(lane ? 0 : cnt, wbuf, &m);
   base = __shfl_sync(0xffffffffu, base, 0);
   const bool use_l = m <= LCAP;
   if (use_l) {
-    for (int i = lo; i < hi; i += 32) {
-      const int j = i + lane;
-      const bool c = j < hi && (skey[j] >> D1_SHIFT) >= d1;
-      const uint32_t mc = __ballot_sync(0xffffffffu, c);
-      if (c) list[base + __popc(mc & lt)] = (uint16_t)j;
-      base += __popc(mc);
+#pragma unroll 2
+    for (int i = lo4; i < hi4; i += 128) {
+      const int j = i + lane * 4;
+      const uint4 kv = *reinterpret_cast<const uint4 *>(skey + j);
+      const bool c0 = j + 0 < hi4 && (kv.x >> D1_SHIFT) >= d1;
+      const bool c1 = j + 1 < hi4 && (kv.y >> D1_SHIFT) >= d1;
+      const bool c2 = j + 2 < hi4 && (kv.z >> D1_SHIFT) >= d1;
+      const bool c3 = j + 3 < hi4 && (kv.w >> D1_SHIFT) >= d1;
+      const uint32_t b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
+      const uint32_t b2 = __ballot_sync(0xffffffffu, c2), b3 = __ballot_sync(0xffffffffu, c3);
+      int pos = base + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+      if (c0) list[pos++] = (uint16_t)(j + 0);
+      if (c1) list[pos++] = (uint16_t)(j + 1);
+      if (c2) list[pos++] = (uint16_t)(j + 2);
+      if (c3) list[pos++] = (uint16_t)(j + 3);
+      base += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
     }
   }
 
+
+  KPROF(3);
   // ---- two 10-bit digits inside bin d1 ------------------------------------------------
   uint32_t prefix = d1 << D1_SHIFT, mask = ~0u << D1_SHIFT;
   for (int shift = DR_BITS; shift >= 0; shift -= DR_BITS) {
@@ -237,6 +284,7 @@ __global__ void __launch_bounds__(NT, 1)
   const uint32_t T = prefix;
   const int need_eq = rem;  // keys == T to take, in index order over the whole row
 
+  KPROF(4);
   // ---- this slice's (greater, equal) counts and their cluster prefix ------------------
   int gb = 0, eb = 0, fb_ex = 0;
   if (use_l) {
@@ -275,6 +323,7 @@ __global__ void __launch_bounds__(NT, 1)
     cl.sync();  // keep shared memory alive until every peer has read our counts
   }
 
+  KPROF(5);
   // ---- ordered emit: every key > T and the first need_eq keys == T --------------------
   if (use_l) {
     for (int c0 = 0; c0 < m; c0 += NT) {
@@ -292,6 +341,7 @@ __global__ void __launch_bounds__(NT, 1)
   } else {
     run_emit(skey, lo, hi, T, need_eq, gb + (fb_ex & 0xFFFF), eb + (fb_ex >> 16), beg, o);
   }
+  KPROF(6);
   if (rank == 0 && threadIdx.x == 0) counts[b] = k;
 }
 
