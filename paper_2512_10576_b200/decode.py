@@ -25,6 +25,7 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass, field
 
+import numpy as np
 import torch
 
 from . import _lib
@@ -396,3 +397,50 @@ class DSADecodeLayer:
     def close(self):
         self.pool.close()
         self.store.close()
+
+
+class SelectionRecorder:
+    """Live K2 selections -> ESSTRACE v1 (format trace.py:238-287,
+    SPEC.md:194).  Attach one recorder to the decode layers of a model (one trace
+    layer per DSADecodeLayer); after each decode step ``record()`` copies every
+    request's selection set to the host.  ``trace(b)`` is request b's AccessTrace, so
+    ``offsim trace stats`` computes the Eq. (1) step-to-step similarity
+    (trace.py:164-196) of model-driven runs and ``offsim simulate --trace`` / ``replay``
+    re-run the cache manager on them.  Diagnostic / export path: it synchronises, so
+    it stays outside timed regions."""
+
+    def __init__(self, layers):
+        self.layers = list(layers)
+        if not self.layers:
+            raise ValueError("no layers to record")
+        l0 = self.layers[0]
+        self.B, self.ctx, self.K = l0.B, l0.ctx, l0.K
+        if any((l.B, l.ctx, l.K) != (self.B, self.ctx, self.K) for l in self.layers):
+            raise ValueError("layers must share batch, context and top-k")
+        self.steps = [[] for _ in range(self.B)]       # [b][t] -> list over layers
+        self.windows = None                              # [b][layer][window]
+
+    def prefill(self, windows_per_layer) -> None:
+        """``windows_per_layer[l]`` = DSADecodeLayer.prefill_warmup(record=True) of layer l."""
+        if len(windows_per_layer) != len(self.layers):
+            raise ValueError("one window list per layer")
+        self.windows = [[[np.asarray(w[b], dtype=np.int64) for w in windows_per_layer[l]]
+                         for l in range(len(self.layers))] for b in range(self.B)]
+
+    def record(self) -> None:
+        """Append the selections of the step just run (one accepted token per step)."""
+        sel = [(l.idx.cpu().numpy(), l.cnt.cpu().numpy()) for l in self.layers]
+        for b in range(self.B):
+            self.steps[b].append([idx[b, :cnt[b]].astype(np.int64) for idx, cnt in sel])
+
+    def trace(self, b: int):
+        from .trace import AccessTrace, StepAccess
+        tr = AccessTrace(num_layers=len(self.layers), context_len=self.ctx, topk=self.K,
+                         steps=[StepAccess(layers=s, tokens_accepted=1) for s in self.steps[b]],
+                         prefill_windows=self.windows[b] if self.windows is not None else None)
+        tr.check()
+        return tr
+
+    def write(self, b: int, path) -> None:
+        from .trace import write_trace
+        write_trace(self.trace(b), path)
