@@ -34,6 +34,10 @@ CONFIGS = {
     "c2": dict(batch=64, context_len=32768, sparse_ratio=0.25, micro=2, first=0.25,
                workload="C2: one DSA layer decode, batch 64/GPU, ctx 32K, 25% GPU slot pool"),
     # configs[3]: ctx 128K, batch 64/GPU, 10% slot pool
+    # configs[2]: the full 61-layer attention path, global batch 128 over 8 GPUs = 16/GPU
+    "c3": dict(batch=16, context_len=32768, sparse_ratio=0.25, micro=2, first=0.5, layers=61,
+               workload="C3: 61-layer decode step (attention path), batch 16/GPU "
+                        "(global 128 over 8 GPUs), ctx 32K, 25% GPU slot pool"),
     "c4": dict(batch=64, context_len=131072, sparse_ratio=0.10, micro=3, first=0.375,
                workload="C4: one DSA layer decode, batch 64/GPU, ctx 128K, 10% GPU slot pool"),
 }
@@ -382,6 +386,76 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def run_model(args, cfg):
+    """Multi-layer configs (C3): the whole num_layers-layer step as one CUDA graph,
+    device-timed like run_ours; per-layer breakdown, e2e and the CPU leg are the
+    single-layer configs' (C2 is the same layer shape at 4x the batch)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2512_10576_b200.decode import DSADecodeModel, random_latent_rows
+    from paper_2512_10576_b200.dp import aggregate
+
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    B, L, rho, NL = cfg["batch"], cfg["context_len"], cfg["sparse_ratio"], cfg["layers"]
+    W, K = args.warmup, args.steps
+    t_setup = time.perf_counter()
+    model = DSADecodeModel(NL, B, L, rho, TOPK, max_new_tokens=W + K + 8, device=dev,
+                           seed=1234 + 100003 * rank, drift=args.drift)
+    model.set_schedule(args.micro, args.first)
+    model.prefill_warmup(windows=32)
+    rows = random_latent_rows(B, dev).view(B, 1, 656)
+    model.capture(args.overlap, args.gather_ctas)
+    queries = [model.next_queries() for _ in range(W + K)]
+    for t in range(1, W):
+        model.step(queries[t], rows)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+    h0, m0 = model.access_totals()
+    if world > 1:
+        dist.barrier()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clocks:
+        torch.cuda.synchronize()
+        start.record()
+        for t in range(W, W + K):
+            model.step(queries[t], rows)
+        end.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = start.elapsed_time(end) / K
+    model.check("bench")
+    h, m = (x - y for x, y in zip(model.access_totals(), (h0, m0)))
+    tokens_total, t_max = aggregate(B * K, step_ms * K / 1e3, device=dev)
+    model.close()
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": tokens_total / t_max, "unit": "tokens/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": t_max * 1e3 / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "e4m3/f16/f32",
+            "data": "synthetic (random-weight DeepSeek-V3.2-Exp DSA shapes, drifting queries)",
+            "config": {"workload": cfg["workload"], "layers": NL, "batch_per_gpu": B,
+                       "context_len": L, "sparse_ratio": rho, "topk": TOPK,
+                       "query_drift": args.drift, "overlap": args.overlap,
+                       "micro_batches": args.micro, "first_micro_batch_share": args.first,
+                       "parallelism": f"dp{world} (requests sharded, no collective)",
+                       "l2": "inputs larger than L2"},
+            "us_per_layer": step_ms * 1e3 / NL, "hit_rate": h / max(1, h + m),
+            "misses_per_request_layer_step": m / (B * K * NL),
+            "gpu_launches": (4 * (args.micro if args.overlap == "dba" else 1) + 2) * NL * K,
+            "cuda_graph": True, "clocks": clocks.summary(), "setup_s": setup_s,
+            "e2e": None, "note": "secondary config: per-kernel roofline, e2e and CPU leg on c2/c4"}),
+            flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def run_ceiling(args, cfg, dev):
     """Same kernels with the whole latent cache in HBM (rho = 1, full history preloaded):
     every selection hits and the gather moves nothing (SURVEY §8d ceiling).  It runs the
@@ -452,6 +526,8 @@ def main():
         args.first = cfg["first"] if args.micro == cfg["micro"] else None
     if args.impl == "reference":
         run_reference(args, cfg)
+    elif cfg.get("layers", 1) > 1:
+        run_model(args, cfg)
     else:
         run_ours(args, cfg)
 

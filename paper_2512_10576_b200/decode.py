@@ -287,10 +287,8 @@ class DSADecodeLayer:
         c = self.pool.counters()
         return int(c[:, 2].sum()), int(c[:, 3].sum())
 
-    def capture(self, overlap: str = "dba", gather_ctas: int = 32) -> None:
-        """Record one full decode step (K1..K5 for every micro-batch, the side-stream
-        gathers, grow/append/write-back) as a CUDA graph; ``step`` replays it.  The
-        first (eager) step also runs here — it advances the state like any step."""
+    def _alloc_static(self) -> None:
+        """The graph's static input buffers, filled with the next queries."""
         B, d = self.B, self.device
         self.q_idx_in = torch.empty((B, 64, 128), dtype=torch.uint8, device=d)
         self.q_in = torch.empty((B, 128, 576), dtype=torch.bfloat16, device=d)
@@ -301,6 +299,13 @@ class DSADecodeLayer:
         q_idx, q = self.next_queries()
         self.q_idx_in.copy_(q_idx)
         self.q_in.copy_(q)
+
+    def capture(self, overlap: str = "dba", gather_ctas: int = 32) -> None:
+        """Record one full decode step (K1..K5 for every micro-batch, the side-stream
+        gathers, grow/append/write-back) as a CUDA graph; ``step`` replays it.  The
+        first (eager) step also runs here — it advances the state like any step."""
+        d = self.device
+        self._alloc_static()
         s = torch.cuda.Stream(d)
         s.wait_stream(torch.cuda.current_stream(d))
         with torch.cuda.stream(s):
@@ -397,6 +402,80 @@ class DSADecodeLayer:
     def close(self):
         self.pool.close()
         self.store.close()
+
+
+class DSADecodeModel:
+    """The attention path of a full decode step (BASELINE configs[2], "C3"): ``num_layers``
+    DSA layers back to back, each with its own indexer key cache, LRU pools, slot store
+    and host latent store (one pool per (request, layer)).  Layer l+1
+    starts only once layer l's attention output exists (its inputs would be computed
+    from it in the real model), so overlap stays inside a layer (DA / DBA); the whole
+    step is one CUDA graph.  Projections, MoE and the dense MLP are outside this path
+    (DESIGN.md §12); every layer's queries are synthetic inputs."""
+
+    def __init__(self, num_layers: int, batch: int, context_len: int, sparse_ratio: float,
+                 topk_k: int = 2048, max_new_tokens: int = 64, device=None, seed: int = 0,
+                 drift: float = 0.97, hugepages: bool = True):
+        self.layers = [DSADecodeLayer(batch, context_len, sparse_ratio, topk_k, max_new_tokens,
+                                      device=device, seed=seed + 7919 * i, drift=drift,
+                                      hugepages=hugepages) for i in range(num_layers)]
+        self.B, self.device = batch, self.layers[0].device
+
+    def set_schedule(self, micro: int = 2, first_frac: float | None = None) -> None:
+        for layer in self.layers:
+            layer.micro, layer.first_frac = micro, first_frac
+
+    def prefill_warmup(self, windows: int = 32) -> None:
+        for layer in self.layers:
+            layer.prefill_warmup(windows=windows)
+
+    def next_queries(self):
+        return [layer.next_queries() for layer in self.layers]
+
+    def capture(self, overlap: str = "dba", gather_ctas: int = 32) -> None:
+        """One eager step (advances the state), then the whole step captured as a graph."""
+        d = self.device
+        for layer in self.layers:
+            layer._alloc_static()
+        s = torch.cuda.Stream(d)
+        s.wait_stream(torch.cuda.current_stream(d))
+        with torch.cuda.stream(s):
+            for layer in self.layers:
+                layer._device_step(overlap, gather_ctas)
+        torch.cuda.current_stream(d).wait_stream(s)
+        torch.cuda.synchronize(d)
+        for layer in self.layers:
+            layer.history += 1
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            for layer in self.layers:
+                layer._device_step(overlap, gather_ctas)
+
+    def step(self, queries, new_rows) -> None:
+        """queries: per layer (q_idx, q); new_rows: per layer [B, 1, 656] (or one shared)."""
+        for i, (layer, (q_idx, q)) in enumerate(zip(self.layers, queries)):
+            layer.q_idx_in.copy_(q_idx, non_blocking=True)
+            layer.q_in.copy_(q, non_blocking=True)
+            layer.rows_in.copy_(new_rows[i] if isinstance(new_rows, (list, tuple)) else new_rows,
+                                non_blocking=True)
+        self.graph.replay()
+        for layer in self.layers:
+            layer.history += 1
+
+    def access_totals(self) -> tuple[int, int]:
+        h = m = 0
+        for layer in self.layers:
+            a, b = layer.access_totals()
+            h, m = h + a, m + b
+        return h, m
+
+    def check(self, what: str = "model") -> None:
+        for i, layer in enumerate(self.layers):
+            layer.pool.check(f"{what} layer {i}")
+
+    def close(self) -> None:
+        for layer in self.layers:
+            layer.close()
 
 
 class SelectionRecorder:

@@ -112,3 +112,61 @@ def test_graph_step_with_overlap_matches_oracle_chain(overlap, micro):
         assert out[b, :int(cnt[b])].tolist() == orc[b].lru_order()
     assert int(layer.lens[0]) == hist
     layer.close()
+
+
+def test_multilayer_model_graph_matches_oracle_per_layer():
+    """C3's DSADecodeModel: layers run back to back inside one CUDA graph; every layer
+    keeps its own pools and host store and stays bit-exact on selections and cache
+    accounting, within tolerance on attention."""
+    from paper_2512_10576_b200.cache import pool_capacity
+    from paper_2512_10576_b200.decode import DSADecodeModel, random_latent_rows
+    NL, B, K, ctx, rho = 3, 2, 2048, 8192, 0.25
+    model = DSADecodeModel(NL, B, ctx, rho, K, max_new_tokens=8, seed=11)
+    model.set_schedule(2, None)
+    orcs = []
+    for layer in model.layers:
+        wins = layer.prefill_warmup(windows=4, record=True)
+        orc = [olru.OraclePool(pool_capacity(rho, ctx)) for _ in range(B)]
+        for w in wins:
+            for b in range(B):
+                orc[b].warmup([w[b].tolist()])
+        orcs.append(orc)
+    hist = ctx
+
+    def mirror(check_attention, qs=None):
+        nonlocal hist
+        torch.cuda.synchronize()
+        for li, layer in enumerate(model.layers):
+            logits = layer.logits.cpu().numpy()
+            idx, cnt = layer.idx.cpu().numpy(), layer.cnt.cpu().numpy()
+            counts = layer.step_counts().cpu().numpy()
+            host = layer.store.host.numpy()
+            for b in range(B):
+                want = dsa.topk_indices(logits[b], hist, K)
+                np.testing.assert_array_equal(idx[b, :cnt[b]], want)
+                r = orcs[li][b].access_step(want.tolist())
+                assert counts[b, 1] == len(r.miss_ids), (li, b)
+                if check_attention:
+                    q = qs[li][1]
+                    ref_o, _ = dsa.sparse_mla(q[b].float().cpu().numpy(), host[b, want], layer.sm_scale)
+                    o = layer.out[b].float().cpu().numpy()
+                    assert np.linalg.norm(o - ref_o) / np.linalg.norm(ref_o) <= 1e-2
+        hist += 1
+        for orc in orcs:
+            for o in orc:
+                o.grow_capacity(pool_capacity(rho, hist))
+                o.append_generated([hist - 1])
+
+    model.capture("dba")
+    mirror(False)
+    rows = random_latent_rows(B, "cuda").view(B, 1, 656)
+    for _ in range(2):
+        qs = model.next_queries()
+        model.step(qs, rows)
+        mirror(True, qs)
+    model.check()
+    for li, layer in enumerate(model.layers):
+        out, cnt = layer.pool.lru_order()
+        for b in range(B):
+            assert out[b, :int(cnt[b])].tolist() == orcs[li][b].lru_order()
+    model.close()
