@@ -206,6 +206,8 @@ int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t ba
  *   ESS_MLA_RESUME   start from the workspace state and finish (Attn1: fetched rows
  *                    + the merge)                                                   */
 #define ESS_MLA_PARTIAL 1
+#define ESS_MLA_SPLIT_SHIFT 8   /* flags bits 8..11: KV splits - 1 (full mode; ws sized batch*splits) */
+#define ESS_MLA_MAX_SPLIT 8
 #define ESS_MLA_RESUME 2
 int ess_sparse_mla(ess_pool *pool, int32_t pool_begin, const void *d_q,
                    const int32_t *d_sel_row, int32_t sel_stride, const int32_t *d_count,
@@ -223,6 +225,16 @@ int ess_sparse_mla_da(ess_pool *pool, int32_t pool_begin, const void *d_q,
                       const int32_t *d_hit_row, const int32_t *d_miss_row, int32_t row_stride,
                       const int32_t *d_counts, int32_t count_stride, int32_t *d_landed,
                       int32_t batch, float sm_scale, void *d_out, float *d_lse, void *stream);
+/* same with the rows of each request split into nsplit contiguous shares (2 * nsplit
+ * CTAs per request; small batches), partial states in d_ws_o [batch*nsplit][128][512]
+ * f32 / d_ws_ml [batch*nsplit][128][2] f32, merged by a combine kernel on the stream.
+ * nsplit = 1 is ess_sparse_mla_da.  2 * batch * nsplit <= SMs - 8.                */
+int ess_sparse_mla_da_split(ess_pool *pool, int32_t pool_begin, const void *d_q,
+                            const int32_t *d_hit_row, const int32_t *d_miss_row,
+                            int32_t row_stride, const int32_t *d_counts, int32_t count_stride,
+                            int32_t *d_landed, int32_t batch, float sm_scale, void *d_out,
+                            float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t nsplit,
+                            void *stream);
 
 #ifdef __cplusplus
 }

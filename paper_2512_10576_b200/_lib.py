@@ -47,6 +47,8 @@ SIGNATURES = {
     "ess_topk": ([V, I64, V, I32, I32, V, I32, V, V], ctypes.c_int),
     "ess_sparse_mla": ([V, I32, V, V, I32, V, I32, I32, F32, V, V, V, V, I32, V], ctypes.c_int),
     "ess_sparse_mla_da": ([V, I32, V, V, V, I32, V, I32, V, I32, F32, V, V, V], ctypes.c_int),
+    "ess_sparse_mla_da_split": ([V, I32, V, V, V, I32, V, I32, V, I32, F32, V, V, V, V, I32, V],
+                                ctypes.c_int),
 }
 
 ESS_OK = 0
@@ -54,6 +56,7 @@ ESS_ERR_CAPACITY, ESS_ERR_SHRINK, ESS_ERR_DUPLICATE = -1, -2, -3
 ESS_ERR_NOMEM, ESS_ERR_RATIO, ESS_ERR_ARG, ESS_ERR_CUDA, ESS_ERR_CLOCK = -4, -5, -6, -7, -8
 ESS_ACCESS_SORT_EVICTED = 1
 ESS_MLA_PARTIAL, ESS_MLA_RESUME = 1, 2
+ESS_MLA_SPLIT_SHIFT, ESS_MLA_MAX_SPLIT = 8, 8
 ESS_GATHER_EXCLUSIVE_SM = 1
 ESS_GATHER_BULK = 2
 ESS_HOST_HUGEPAGES, ESS_HOST_NUMA_BOUND = 1, 2

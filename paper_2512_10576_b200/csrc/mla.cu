@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                       const int32_t *__restrict__ sel2, int32_t *landed,
                       int sel_stride, const int32_t *__restrict__ counts, int count_stride,
                       float sm_scale, uint16_t *__restrict__ out, float *__restrict__ lse,
-                      float *__restrict__ ws_o, float *__restrict__ ws_ml, int flags) {
+                      float *__restrict__ ws_o, float *__restrict__ ws_ml, int flags, int nsplit) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sq = smem;                        // q dims 320..575, 4 SW128 blocks
@@ -170,13 +170,22 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   Ctrl &c = *reinterpret_cast<Ctrl *>(ssel + MAX_N);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int v = blockIdx.x;  // output half
-  const int b = blockIdx.y;
+  const int split = blockIdx.y % nsplit;     // KV split: a contiguous share of the rows
+  const int b = blockIdx.y / nsplit;
   const bool partial = flags & ESS_MLA_PARTIAL, resume = flags & ESS_MLA_RESUME;
-  // fused DA: rows sel_row[0:n1) are resident, sel2[0:n2) land during the kernel
+  // split CTAs leave unnormalised partial states in the workspace; a combine kernel
+  // merges them (small batches: 2 * nsplit CTAs per request fill the GPU)
+  const bool to_ws = partial || nsplit > 1;
+  // fused DA: rows sel_row[0:n1t) are resident, sel2[0:n2t) land during the kernel; the
+  // CTA attends rows [r0, r0 + n) of their concatenation
   const bool await = flags & MLA_AWAIT;
-  const int n1 = min(counts[(int64_t)b * count_stride], MAX_N);
-  const int n2 = await ? min(counts[(int64_t)b * count_stride + 1], MAX_N - n1) : 0;
-  const int n = n1 + n2;
+  const int n1t = min(counts[(int64_t)b * count_stride], MAX_N);
+  const int n2t = await ? min(counts[(int64_t)b * count_stride + 1], MAX_N - n1t) : 0;
+  const int chunk = ((n1t + n2t + nsplit - 1) / nsplit + NB - 1) / NB * NB;
+  const int r0 = min(n1t + n2t, split * chunk);
+  const int n = min(n1t + n2t, r0 + chunk) - r0;
+  const int n1 = max(0, min(n, n1t - r0));   // resident rows of this share
+  const bool fetched = r0 + n > n1t;         // the share holds fetched rows
   const int ntiles = (n + NB - 1) / NB;
 
   if (threadIdx.x == 0) {
@@ -212,10 +221,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   }
   if (warp >= LOAD0) {
     const int32_t *sel = sel_row + (int64_t)b * sel_stride;
-    for (int j = threadIdx.x - LOAD0 * 32; j < n1; j += NLOAD * 32) ssel[j] = __ldg(sel + j);
-    if (await) {
-      const int32_t *s2 = sel2 + (int64_t)b * sel_stride;
-      for (int j = threadIdx.x - LOAD0 * 32; j < n2; j += NLOAD * 32) ssel[n1 + j] = __ldg(s2 + j);
+    const int32_t *s2 = await ? sel2 + (int64_t)b * sel_stride : nullptr;
+    for (int j = threadIdx.x - LOAD0 * 32; j < n; j += NLOAD * 32) {
+      const int g = r0 + j;
+      ssel[j] = g < n1t ? __ldg(sel + g) : __ldg(s2 + (g - n1t));
     }
   }
   mbar_wait(&c.q_full, 0);
@@ -254,7 +263,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int h = warp * 32 + lane;
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     const int64_t hrow = (int64_t)b * HEADS + h;
-    float *wso = ws_o ? ws_o + hrow * ESS_MLA_V_DIM + v * V_HALF : nullptr;
+    const int64_t wrow = (int64_t)(b * nsplit + split) * HEADS + h;  // workspace row
+    float *wso = ws_o ? ws_o + wrow * ESS_MLA_V_DIM + v * V_HALF : nullptr;
     float m_run = -INFINITY, l_run = 0.f;  // resume starts a fresh partial, merged at the end
     for (int i = 0; i < ntiles; i++) {
       const int sb = i % NSB;
@@ -327,8 +337,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_wait(&c.o_done, 0);
       tc_fence_after();
     }
-    if (partial) {
-      // pass 1 of the split attention: unnormalised O and (max, sum) to the workspace
+    if (to_ws) {
+      // pass 1 of the split attention / a KV split: unnormalised O and (max, sum) to
+      // the workspace
 #pragma unroll 1
       for (int cc = 0; cc < V_HALF / 32; cc++) {
         uint32_t o[32];
@@ -346,8 +357,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                           __uint_as_float(o[j + 2]), __uint_as_float(o[j + 3]));
       }
       if (v == 0) {
-        ws_ml[hrow * 2 + 0] = m_run;
-        ws_ml[hrow * 2 + 1] = l_run;
+        ws_ml[wrow * 2 + 0] = m_run;
+        ws_ml[wrow * 2 + 1] = l_run;
       }
     } else {
       // final output.  Resume mode merges this pass's O (TMEM) with pass 1's
@@ -483,12 +494,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int w = warp - LOAD0;
     const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b) * rows_per_pool * ESS_SLOT_ROW_BYTES;
     const uint32_t kv0 = smem_u32(skv);
-    bool pending = n2 > 0;  // fetched rows not yet known to have landed
+    bool pending = fetched && n2t > 0;  // fetched rows not yet known to have landed
     for (int i = 0; i < ntiles; i++) {
       const int kb = i % KS;
       mbar_wait(&c.kv_empty[kb], ((i / KS) & 1) ^ 1);
       if (pending && (i + 1) * NB > n1) {  // first tile holding fetched rows
-        wait_landed(landed + b, n2);
+        wait_landed(landed + b, n2t);
         pending = false;
       }
       const uint32_t kv = kv0 + kb * KV_BYTES;
@@ -517,9 +528,73 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   __syncthreads();
   tc_fence_after();
   if (await && threadIdx.x == 0) {  // this CTA's loaders are past their waits
-    if (atomicAdd(landed + b, LANDED_TAG) >= LANDED_TAG) atomicExch(landed + b, 0);
+    // the request's last CTA (of 2 * nsplit) to get here resets the counter
+    if (atomicAdd(landed + b, LANDED_TAG) >= (2 * nsplit - 1) * LANDED_TAG) atomicExch(landed + b, 0);
   }
   if (warp == MMA_WARP) tmem_dealloc<512>(tmem);
+}
+
+// KV-split merge (the reference's merge_attn, costmodel.py:26): per (request, head),
+// out = sum_s 2^(m_s - m) O_s / sum_s 2^(m_s - m) l_s with m = max_s m_s (exp2 domain,
+// as the kernel's online softmax), lse = (m + log2 l) ln 2.  One warp per head, each
+// lane 16 of the 512 output dims.
+__global__ void __launch_bounds__(128) mla_combine_kernel(const float *__restrict__ ws_o,
+                                                          const float *__restrict__ ws_ml, int nsplit,
+                                                          uint16_t *__restrict__ out,
+                                                          float *__restrict__ lse) {
+  const int b = blockIdx.x, h = blockIdx.y * 4 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  float ms[ESS_MLA_MAX_SPLIT], ls[ESS_MLA_MAX_SPLIT];
+  float m = -INFINITY;
+#pragma unroll
+  for (int s = 0; s < ESS_MLA_MAX_SPLIT; s++) {
+    if (s < nsplit) {
+      const int64_t r = (int64_t)(b * nsplit + s) * HEADS + h;
+      ms[s] = ws_ml[r * 2];
+      ls[s] = ws_ml[r * 2 + 1];
+      if (ls[s] > 0.f) m = fmaxf(m, ms[s]);
+    }
+  }
+  float l = 0.f, wgt[ESS_MLA_MAX_SPLIT];
+#pragma unroll
+  for (int s = 0; s < ESS_MLA_MAX_SPLIT; s++) {
+    wgt[s] = (s < nsplit && ls[s] > 0.f) ? exp2f(ms[s] - m) : 0.f;
+    if (s < nsplit) l += ls[s] * wgt[s];
+  }
+  const int64_t hrow = (int64_t)b * HEADS + h;
+  uint16_t *ob = out + hrow * ESS_MLA_V_DIM + lane * 16;
+  if (!(l > 0.f)) {
+    reinterpret_cast<uint4 *>(ob)[0] = make_uint4(0, 0, 0, 0);
+    reinterpret_cast<uint4 *>(ob)[1] = make_uint4(0, 0, 0, 0);
+    if (lane == 0) lse[hrow] = -INFINITY;
+    return;
+  }
+  const float inv = 1.f / l;
+  float acc[16];
+#pragma unroll
+  for (int j = 0; j < 16; j++) acc[j] = 0.f;
+#pragma unroll
+  for (int s = 0; s < ESS_MLA_MAX_SPLIT; s++) {
+    if (s >= nsplit || wgt[s] == 0.f) continue;
+    const float4 *src = reinterpret_cast<const float4 *>(
+        ws_o + ((int64_t)(b * nsplit + s) * HEADS + h) * ESS_MLA_V_DIM + lane * 16);
+#pragma unroll
+    for (int q4 = 0; q4 < 4; q4++) {
+      const float4 x = src[q4];
+      acc[4 * q4 + 0] += x.x * wgt[s];
+      acc[4 * q4 + 1] += x.y * wgt[s];
+      acc[4 * q4 + 2] += x.z * wgt[s];
+      acc[4 * q4 + 3] += x.w * wgt[s];
+    }
+  }
+  uint32_t pk[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) {
+    __nv_bfloat162 t = __floats2bfloat162_rn(acc[2 * j] * inv, acc[2 * j + 1] * inv);
+    pk[j] = *reinterpret_cast<uint32_t *>(&t);
+  }
+  reinterpret_cast<uint4 *>(ob)[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  reinterpret_cast<uint4 *>(ob)[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+  if (lane == 0) lse[hrow] = (m + log2f(l)) * 0.6931471805599453f;
 }
 
 }  // namespace
@@ -530,7 +605,7 @@ int launch_mla(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_
                const int32_t *d_sel2, int32_t *d_landed, int32_t sel_stride,
                const int32_t *d_count, int32_t count_stride, int32_t batch, float sm_scale,
                void *d_out, float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags,
-               void *stream) {
+               int32_t nsplit, void *stream) {
   // q as a [batch * 128 heads][576] bf16 tensor, boxes of [128 heads][64 dims], SW128
   struct QMap {
     const void *base = nullptr;
@@ -555,11 +630,16 @@ int launch_mla(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_
                                       (int)SMEM_BYTES));
     attr = true;
   }
-  dim3 grid(2, batch);
+  dim3 grid(2, batch * nsplit);
   sparse_mla_kernel<<<grid, NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
       tq, pool->rows, pool->rows_per_pool, pool_begin, d_sel_row, d_sel2, d_landed, sel_stride,
-      d_count, count_stride, sm_scale, (uint16_t *)d_out, d_lse, d_ws_o, d_ws_ml, flags);
+      d_count, count_stride, sm_scale, (uint16_t *)d_out, d_lse, d_ws_o, d_ws_ml, flags, nsplit);
   ESS_CUDA_TRY(cudaGetLastError());
+  if (nsplit > 1) {
+    mla_combine_kernel<<<dim3(batch, HEADS / 4), 128, 0, (cudaStream_t)stream>>>(
+        d_ws_o, d_ws_ml, nsplit, (uint16_t *)d_out, d_lse);
+    ESS_CUDA_TRY(cudaGetLastError());
+  }
   return ESS_OK;
 }
 
@@ -575,16 +655,21 @@ extern "C" int ess_sparse_mla(ess_pool *pool, int32_t pool_begin, const void *d_
                               int32_t count_stride, int32_t batch, float sm_scale, void *d_out,
                               float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags,
                               void *stream) {
+  const int nsplit = ((flags >> ESS_MLA_SPLIT_SHIFT) & 0xF) + 1;
+  flags &= ~(0xF << ESS_MLA_SPLIT_SHIFT);
+  if (nsplit > ESS_MLA_MAX_SPLIT) return ESS_ERR_ARG;
   if ((flags & (ESS_MLA_PARTIAL | ESS_MLA_RESUME)) && (!d_ws_o || !d_ws_ml)) return ESS_ERR_ARG;
   if ((flags & ESS_MLA_PARTIAL) && (flags & ESS_MLA_RESUME)) return ESS_ERR_ARG;
   if (flags & ~(ESS_MLA_PARTIAL | ESS_MLA_RESUME)) return ESS_ERR_ARG;
+  if (nsplit > 1 && (flags || !d_ws_o || !d_ws_ml)) return ESS_ERR_ARG;  // split: full mode only
   if (!pool_ok(pool, pool_begin, batch) || !d_q || !d_sel_row || !d_count || count_stride < 1 ||
       (!(flags & ESS_MLA_PARTIAL) && (!d_out || !d_lse)) || sel_stride < 1 ||
       (reinterpret_cast<uintptr_t>(d_q) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15))
     return ESS_ERR_ARG;
   if (batch == 0) return ESS_OK;
   return launch_mla(pool, pool_begin, d_q, d_sel_row, nullptr, nullptr, sel_stride, d_count,
-                    count_stride, batch, sm_scale, d_out, d_lse, d_ws_o, d_ws_ml, flags, stream);
+                    count_stride, batch, sm_scale, d_out, d_lse, d_ws_o, d_ws_ml, flags, nsplit,
+                    stream);
 }
 
 extern "C" int ess_sparse_mla_da(ess_pool *pool, int32_t pool_begin, const void *d_q,
@@ -592,14 +677,26 @@ extern "C" int ess_sparse_mla_da(ess_pool *pool, int32_t pool_begin, const void 
                                  int32_t row_stride, const int32_t *d_counts, int32_t count_stride,
                                  int32_t *d_landed, int32_t batch, float sm_scale,
                                  void *d_out, float *d_lse, void *stream) {
+  return ess_sparse_mla_da_split(pool, pool_begin, d_q, d_hit_row, d_miss_row, row_stride, d_counts,
+                                 count_stride, d_landed, batch, sm_scale, d_out, d_lse, nullptr,
+                                 nullptr, 1, stream);
+}
+
+extern "C" int ess_sparse_mla_da_split(ess_pool *pool, int32_t pool_begin, const void *d_q,
+                                       const int32_t *d_hit_row, const int32_t *d_miss_row,
+                                       int32_t row_stride, const int32_t *d_counts,
+                                       int32_t count_stride, int32_t *d_landed, int32_t batch,
+                                       float sm_scale, void *d_out, float *d_lse, float *d_ws_o,
+                                       float *d_ws_ml, int32_t nsplit, void *stream) {
   if (!pool_ok(pool, pool_begin, batch) || !d_q || !d_hit_row || !d_miss_row || !d_counts ||
       !d_landed || !d_out || !d_lse || row_stride < 1 || count_stride < 2 ||
-      (reinterpret_cast<uintptr_t>(d_q) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15))
+      (reinterpret_cast<uintptr_t>(d_q) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15) ||
+      nsplit < 1 || nsplit > ESS_MLA_MAX_SPLIT || (nsplit > 1 && (!d_ws_o || !d_ws_ml)))
     return ESS_ERR_ARG;
   if (batch == 0) return ESS_OK;
   // every CTA may spin on the arrival counters: all of them and the gather must fit at once
-  if (2 * batch > ess_sm_count() - 8) return ESS_ERR_ARG;
+  if (2 * batch * nsplit > ess_sm_count() - 8) return ESS_ERR_ARG;
   return launch_mla(pool, pool_begin, d_q, d_hit_row, d_miss_row, d_landed, row_stride, d_counts,
-                    count_stride, batch, sm_scale, d_out, d_lse, nullptr, nullptr, MLA_AWAIT,
-                    stream);
+                    count_stride, batch, sm_scale, d_out, d_lse, d_ws_o, d_ws_ml, MLA_AWAIT,
+                    nsplit, stream);
 }

@@ -70,6 +70,8 @@ class DSADecodeLayer:
         self.drift, self.sm_scale = drift, sm_scale
         self.fuse_da = True  # DA as one K5 launch waiting on the gather (when it fits)
         self.micro = 2       # DBA micro-batches per step (overlap="dba")
+        self.max_split = 4   # fused K5: KV splits per request at small batch
+        self.min_gather_sms = 20
         self.Lmax = ((context_len + max_new_tokens + 127) // 128) * 128
         self.gen = torch.Generator(device=self.device).manual_seed(seed)
         d, g, B = self.device, self.gen, batch
@@ -208,7 +210,14 @@ class DSADecodeLayer:
         # one fused K5 launch when its 2B CTAs and the gather fit the GPU at once (its
         # CTAs wait for the gather's arrival counters); two passes + merge otherwise
         fused = self.fuse_da and 2 * B <= sms - 8
-        gsms = max(8, sms - 2 * B)  # attention takes 2 CTAs per request (one SM each)
+        # small batches: spread each request's rows over 2 * split CTAs (KV split +
+        # combine) while leaving the gather its SMs; attention takes one SM per CTA
+        split = 1
+        if fused:
+            split = max(1, min(self.max_split, (sms - 8 - self.min_gather_sms) // (2 * B)))
+        gsms = max(8, sms - 2 * B * split)
+        if split > 1 and getattr(self, "_ws_split", None) is None:
+            self._ws_split = SplitWorkspace(B, self.device, splits=split)
         ranges = self.micro_batches(micro if overlap == "dba" else 1)
         if getattr(self, "_sel", None) is None:
             self._sel = torch.cuda.Stream(self.device)
@@ -247,7 +256,8 @@ class DSADecodeLayer:
         done = torch.cuda.Event()
         done.record(side)
         if fused:
-            sparse_mla_da(self.pool, q, acc, self._landed, self.sm_scale, out=self.out, lse=self.lse)
+            sparse_mla_da(self.pool, q, acc, self._landed, self.sm_scale, out=self.out, lse=self.lse,
+                          split=split, workspace=self._ws_split if split > 1 else None)
             main.wait_event(done)
             if new_rows is not None:
                 main.wait_event(admitted)

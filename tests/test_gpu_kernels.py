@@ -154,9 +154,12 @@ def test_gather_and_write_back_are_exact(bulk):
 
 
 # ---------------------------------------------------------------------------- K5
+@pytest.mark.parametrize("split", [1, 2, 3, 4])
 @pytest.mark.parametrize("counts", [[2048, 1000, 17, 1], [2048] * 3])
-def test_sparse_mla_matches_oracle(counts):
-    from paper_2512_10576_b200.attention import sparse_mla, DEFAULT_SM_SCALE
+def test_sparse_mla_matches_oracle(counts, split):
+    """split > 1: each request's rows on 2 * split CTAs, partial states merged by the
+    combine kernel (small-batch path) — same tolerance as one pass."""
+    from paper_2512_10576_b200.attention import SplitWorkspace, sparse_mla, DEFAULT_SM_SCALE
     from paper_2512_10576_b200.cache import PoolSet
     from paper_2512_10576_b200.decode import random_latent_rows
     B, cap = len(counts), 4096
@@ -167,7 +170,8 @@ def test_sparse_mla_matches_oracle(counts):
     sel = torch.stack([torch.randperm(cap, device="cuda", generator=g)[:2048] for _ in range(B)]).int()
     cnt = torch.tensor(counts, dtype=torch.int32, device="cuda")
     q = (torch.randn((B, 128, 576), device="cuda", generator=g) * 0.5).to(torch.bfloat16)
-    out, lse = sparse_mla(pools, q, sel, cnt)
+    ws = SplitWorkspace(B, "cuda", splits=split) if split > 1 else None
+    out, lse = sparse_mla(pools, q, sel, cnt, workspace=ws, split=split)
     out, lse = out.float().cpu().numpy(), lse.cpu().numpy()
     qf = q.float().cpu().numpy()
     for b, n in enumerate(counts):
