@@ -38,11 +38,28 @@ CONFIGS = {
     "c3": dict(batch=16, context_len=32768, sparse_ratio=0.25, micro=2, first=0.5, layers=61,
                workload="C3: 61-layer decode step (attention path), batch 16/GPU "
                         "(global 128 over 8 GPUs), ctx 32K, 25% GPU slot pool"),
+    # configs[4]: mixed-length batch, context log-uniform over [8K, 128K] (seeded per rank);
+    # the pool-size / hit-rate sweep is scripts/sweep_c5.py
+    "c5": dict(batch=64, context_len=(8192, 131072), sparse_ratio=0.25, micro=3, first=0.375,
+               workload="C5: one DSA layer decode, batch 64/GPU of mixed 8K-128K contexts "
+                        "(log-uniform), 25% GPU slot pool"),
     "c4": dict(batch=64, context_len=131072, sparse_ratio=0.10, micro=3, first=0.375,
                workload="C4: one DSA layer decode, batch 64/GPU, ctx 128K, 10% GPU slot pool"),
 }
 TOPK = 2048
 METRIC = "decode tokens/s/GPU at 32K/128K ctx, latent cache offloaded; H2D gather GB/s"
+
+
+def request_lengths(cfg, n, seed=0):
+    """Per-request context lengths: the config's single length, or (C5) a seeded
+    log-uniform draw over [lo, hi] — the mixed 8K-128K batch of BASELINE configs[4]."""
+    L = cfg["context_len"]
+    if isinstance(L, int):
+        return [L] * n
+    import numpy as np
+    lo, hi = L
+    rng = np.random.default_rng(seed)
+    return [int(x) for x in np.exp(rng.uniform(np.log(lo), np.log(hi), size=n)).round()]
 
 
 def measured_peaks():
@@ -120,10 +137,12 @@ def cpu_reference_rate(cfg, budget_s: float = 12.0, seed: int = 0):
     from oracle import lru as olru
 
     rng = np.random.default_rng(seed)
-    L, K, rho = cfg["context_len"], TOPK, cfg["sparse_ratio"]
+    K, rho = TOPK, cfg["sparse_ratio"]
+    sample_lens = request_lengths(cfg, cfg["batch"], seed=seed + 17)
     e4 = lambda a: np.clip(np.round(a), -6, 6).astype(np.int8).view(np.uint8)  # noqa: E731
     n_req, t_total = 0, 0.0
     while n_req < 1 or (t_total < budget_s and n_req < cfg["batch"]):
+        L = sample_lens[n_req % len(sample_lens)]
         k = e4(rng.standard_normal((L, 128)) * 2)
         q = e4(rng.standard_normal((64, 128)) * 2)
         w = rng.standard_normal(64).astype(np.float32) / 8
@@ -166,7 +185,9 @@ def run_reference(args, cfg):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
             "config": {"workload": cfg["workload"], "layers": 1, "batch_per_gpu": cfg["batch"],
-                       "context_len": cfg["context_len"], "sparse_ratio": cfg["sparse_ratio"],
+                       "context_len": cfg["context_len"] if isinstance(cfg["context_len"], int)
+                       else "mixed {}-{} log-uniform".format(*cfg["context_len"]),
+                       "sparse_ratio": cfg["sparse_ratio"],
                        "topk": TOPK},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
                              "sample": sample},
@@ -259,7 +280,9 @@ def run_ours(args, cfg):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     peaks, peak_kind = measured_peaks()
-    B, L, rho = cfg["batch"], cfg["context_len"], cfg["sparse_ratio"]
+    B, rho = cfg["batch"], cfg["sparse_ratio"]
+    lens = request_lengths(cfg, B, seed=rank)
+    L = lens if not isinstance(cfg["context_len"], int) else cfg["context_len"]
     W, K, NB = args.warmup, args.steps, args.breakdown_steps
     total = W + K + NB
     layer = DSADecodeLayer(B, L, rho, TOPK, max_new_tokens=total + K + 16, device=dev,
@@ -311,7 +334,7 @@ def run_ours(args, cfg):
         return
     # per-kernel breakdown (sequential, separate steps) for the roofline
     ktimes, bcounts = kernel_breakdown(layer, inputs[W + K:], new_rows[W + K:])
-    lens_mean = L + W + K + (NB - 1) / 2
+    lens_mean = sum(lens) / B + W + K + (NB - 1) / 2
     idx_bytes = B * lens_mean * (132 + 4) + B * (64 * 128 + 64 * 4)
     achieved = idx_bytes / (ktimes["indexer"] * 1e-3) / 1e9
     gather_bytes = bcounts[:, :, 1].sum().item() * 656 / NB
@@ -349,7 +372,9 @@ def run_ours(args, cfg):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "e4m3/f16/f32",
             "data": "synthetic (random-weight DeepSeek-V3.2-Exp DSA shapes, drifting queries)",
             "config": {"workload": cfg["workload"], "layers": 1, "batch_per_gpu": B,
-                       "context_len": L, "sparse_ratio": rho, "topk": TOPK, "query_drift": args.drift,
+                       "context_len": L if isinstance(L, int)
+                       else "mixed {}-{} log-uniform, mean {:.0f}".format(*cfg["context_len"], sum(lens) / B),
+                       "sparse_ratio": rho, "topk": TOPK, "query_drift": args.drift,
                        "overlap": args.overlap,
                        "micro_batches": args.micro if args.overlap == "dba" else 1,
                        "first_micro_batch_share": args.first if args.overlap == "dba" else None,
@@ -465,18 +490,21 @@ def run_ceiling(args, cfg, dev):
     from paper_2512_10576_b200.cache import AccessBatch
     from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows
     from paper_2512_10576_b200.transfer import gather
-    B, L = cfg["batch"], cfg["context_len"]
+    B = cfg["batch"]
+    lens = request_lengths(cfg, B, seed=int(os.environ.get("RANK", "0")))
+    L = lens if not isinstance(cfg["context_len"], int) else cfg["context_len"]
     total = args.warmup + args.steps
     layer = DSADecodeLayer(B, L, 1.0, TOPK, max_new_tokens=total + 8, device=dev, seed=99,
                            drift=args.drift)
     layer.gather_ctas = args.gather_ctas
-    full = torch.arange(L, dtype=torch.int32, device=dev)
-    for c0 in range(0, L, 2048):
+    full = torch.arange(max(lens), dtype=torch.int32, device=dev)
+    for c0 in range(0, max(lens), 2048):
         ids = full[c0:c0 + 2048].expand(B, -1).contiguous()
-        layer.pool.warmup(ids, torch.full((B,), ids.shape[1], dtype=torch.int32, device=dev))
+        nb = torch.tensor([min(2048, max(0, n - c0)) for n in lens], dtype=torch.int32, device=dev)
+        layer.pool.warmup(ids, nb)
         slots = torch.stack([layer.pool.lookup(b, ids[b]) for b in range(B)])
         cnt = torch.zeros((B, 4), dtype=torch.int32, device=dev)
-        cnt[:, 1] = ids.shape[1]
+        cnt[:, 1] = nb
         gather(layer.pool, layer.store, AccessBatch(cnt, None, ids, slots.contiguous()), max_ctas=148)
     inputs = [layer.next_queries() for _ in range(total)]
     new_rows = [random_latent_rows(B, dev, layer.gen).view(B, 1, 656) for _ in range(total)]
@@ -512,6 +540,7 @@ def main():
     ap.add_argument("--micro", type=int, default=None, help="DBA micro-batches per step (default: per config)")
     ap.add_argument("--first", type=float, default=None,
                     help="DBA: fraction of the batch in the first micro-batch (default: per config)")
+    ap.add_argument("--rho", type=float, default=None, help="override the config's GPU slot-pool ratio")
     ap.add_argument("--quick", action="store_true",
                     help="schedule sweeps: skip the CPU baseline, e2e and per-kernel breakdown")
     ap.add_argument("--breakdown-steps", type=int, default=5)
@@ -519,7 +548,9 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.rho is not None:
+        cfg["sparse_ratio"] = args.rho
     if args.micro is None:
         args.micro = cfg["micro"]
     if args.first is None:

@@ -155,7 +155,8 @@ __device__ bool select_kth_narrow(const uint32_t *__restrict__ keys, int cnt, in
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   uint32_t mn = 0xFFFFFFFFu, mx = 0u;
   int nfree = 0;
-  for (int s = t; s < cnt; s += NT) {
+#pragma unroll 8
+  for (int s = t; s < cnt; s += NT) {  // unrolled: keys may be in global memory (big pools)
     const uint32_t k = keys[s];
     if (k < ESS_CLOCK_BASE) {
       nfree++;
@@ -198,6 +199,7 @@ __device__ bool select_kth_narrow(const uint32_t *__restrict__ keys, int cnt, in
   for (int pass = 0; pass < (shift ? 2 : 1); pass++) {
     for (int i = t; i < 2048; i += NT) h[i] = 0;
     __syncthreads();
+#pragma unroll 8
     for (int s = t; s < cnt; s += NT) {
       const uint32_t k = keys[s];
       const uint32_t rel = k - lo;
@@ -478,15 +480,20 @@ __global__ void __launch_bounds__(NT, 1)
       // the nmiss selected slots in ascending order (exactly nmiss keys are <= T)
       if (cap <= 64 * NT) {
         compact_le(kread, cap, T, sm, sm.ev, sm.sel);
-      } else {
-        int base = 0;
-        for (int s0 = 0; s0 < cap; s0 += NT) {
-          int s2 = s0 + t;
-          int f = (s2 < cap && kread[s2] <= T) ? 1 : 0;
-          int tot;
-          int pos = block_exclusive_scan<NT>(f, sm.warp, &tot);
-          if (f && base + pos < MAXR) sm.sel[base + pos] = s2;
-          base += tot;
+      } else {  // very large pools: contiguous runs per thread, still one block scan
+        const int per = (cap + NT - 1) / NT;
+        const int s0 = min(cap, t * per), s1 = min(cap, s0 + per);
+        int f = 0;
+#pragma unroll 8
+        for (int s2 = s0; s2 < s1; s2++) f += kread[s2] <= T;
+        int tot;
+        int pos = block_exclusive_scan<NT>(f, sm.warp, &tot);
+        for (int s2 = s0; s2 < s1 && f > 0; s2++) {
+          if (kread[s2] <= T) {
+            if (pos < MAXR) sm.sel[pos] = s2;
+            pos++;
+            f--;
+          }
         }
       }
       __syncthreads();
@@ -697,8 +704,30 @@ constexpr int NTA = 256;
 
 // block-wide argmin of key[0:cap) -> slot (keys unique)
 __device__ int argmin_key(const uint32_t *key, int cap, unsigned long long *red) {
+  // 16-B loads, several in flight per thread: the scan is latency-bound otherwise
+  // (the key array sits in HBM; the indexer stream evicts it from L2 every step).
+  // Plain (coherent) loads: thread 0 rewrites a key between the scans of one launch.
   unsigned long long best = ~0ull;
-  for (int s = threadIdx.x; s < cap; s += NTA) {
+  const int head = min(cap, (int)((4 - ((reinterpret_cast<uintptr_t>(key) >> 2) & 3)) & 3));
+  const int body = (cap - head) & ~3;
+  if ((int)threadIdx.x < head) {
+    unsigned long long v = ((unsigned long long)key[threadIdx.x] << 32) | threadIdx.x;
+    best = v < best ? v : best;
+  }
+  const uint4 *k4 = reinterpret_cast<const uint4 *>(key + head);
+#pragma unroll 4
+  for (int j = threadIdx.x * 4; j < body; j += NTA * 4) {
+    const uint4 q = k4[j >> 2];
+    const unsigned s = (unsigned)(head + j);
+    const unsigned long long v0 = ((unsigned long long)q.x << 32) | s;
+    const unsigned long long v1 = ((unsigned long long)q.y << 32) | (s + 1);
+    const unsigned long long v2 = ((unsigned long long)q.z << 32) | (s + 2);
+    const unsigned long long v3 = ((unsigned long long)q.w << 32) | (s + 3);
+    const unsigned long long a = v0 < v1 ? v0 : v1, c = v2 < v3 ? v2 : v3;
+    const unsigned long long m = a < c ? a : c;
+    best = m < best ? m : best;
+  }
+  for (int s = head + body + threadIdx.x; s < cap; s += NTA) {
     unsigned long long v = ((unsigned long long)key[s] << 32) | (unsigned)s;
     best = v < best ? v : best;
   }

@@ -61,11 +61,21 @@ class StepStats:
 class DSADecodeLayer:
     """Device-resident state + buffers for one layer over ``batch`` requests."""
 
-    def __init__(self, batch: int, context_len: int, sparse_ratio: float, topk_k: int = 2048,
+    def __init__(self, batch: int, context_len, sparse_ratio: float, topk_k: int = 2048,
                  max_new_tokens: int = 64, device=None, seed: int = 0, drift: float = 0.95,
                  sm_scale: float = DEFAULT_SM_SCALE, hugepages: bool = True):
+        """``context_len``: one length for every request, or a sequence of ``batch``
+        per-request lengths (mixed batches, C5); each request's pool holds
+        floor(rho * its own history) rows (cache.py:137-138)."""
         _lib.require_cuda()
         self.device = torch.device(device if device is not None else "cuda")
+        if isinstance(context_len, (list, tuple, np.ndarray)):
+            self.ctx_lens = [int(x) for x in context_len]
+            if len(self.ctx_lens) != batch or min(self.ctx_lens) < 1:
+                raise ValueError("need one positive context length per request")
+        else:
+            self.ctx_lens = [int(context_len)] * batch
+        context_len = max(self.ctx_lens)
         self.B, self.ctx, self.rho, self.K = batch, context_len, sparse_ratio, topk_k
         self.drift, self.sm_scale = drift, sm_scale
         self.fuse_da = True  # DA as one K5 launch waiting on the gather (when it fits)
@@ -75,8 +85,8 @@ class DSADecodeLayer:
         self.Lmax = ((context_len + max_new_tokens + 127) // 128) * 128
         self.gen = torch.Generator(device=self.device).manual_seed(seed)
         d, g, B = self.device, self.gen, batch
-        self.lens = torch.full((B,), context_len, dtype=torch.int32, device=d)
-        self.history = context_len
+        self.lens = torch.tensor(self.ctx_lens, dtype=torch.int32, device=d)
+        self.history = context_len  # the longest request's history (= ctx + steps)
         # indexer key cache (HBM): e4m3 keys + f32 per-token scale
         self.k_cache = _e4m3(torch.randn((B, self.Lmax, 128), device=d, generator=g) * 8.0)
         self.k_scale = torch.rand((B, self.Lmax), device=d, generator=g) * 0.5 + 0.75
@@ -84,10 +94,11 @@ class DSADecodeLayer:
         self.store = HostLatentStore(B, self.Lmax, hugepages=hugepages, device=self.device)
         for b in range(B):  # fill through the GPU: random rows copied into pinned memory
             self.store.host[b].copy_(random_latent_rows(self.Lmax, d, g), non_blocking=False)
-        self.cap0 = pool_capacity(sparse_ratio, context_len)
+        caps = [pool_capacity(sparse_ratio, n) for n in self.ctx_lens]
+        self.cap0 = min(caps)
         self.cap_max = pool_capacity(sparse_ratio, self.Lmax)
         staging = topk_k if self.cap0 < topk_k else 0
-        self.pool = PoolSet(B, self.Lmax, self.cap_max, self.cap0, row_bytes=_lib.SLOT_ROW_BYTES,
+        self.pool = PoolSet(B, self.Lmax, self.cap_max, caps, row_bytes=_lib.SLOT_ROW_BYTES,
                             staging_rows=staging, device=d)
         # drifting queries
         self._zi = torch.randn((B, 64, 128), device=d, generator=g)
@@ -285,7 +296,8 @@ class DSADecodeLayer:
         # admission overlaps attention only while every pool holds more than K rows:
         # a smaller pool keeps part of the selection in rows the admission may evict
         # (capacity only grows with history, so this holds for every later replay)
-        early = overlap in ("da", "dba") and math.floor(self.rho * self.history) > self.K
+        hist_min = min(self.ctx_lens) + self.history - self.ctx
+        early = overlap in ("da", "dba") and math.floor(self.rho * hist_min) > self.K
         self.attend(self.q_idx_in, self.q_in, gather_ctas=gather_ctas, overlap=overlap,
                     new_rows=self.rows_in if early else None, micro=self.micro)
         if not early:
@@ -394,19 +406,19 @@ class DSADecodeLayer:
     def append_token(self, new_rows: torch.Tensor | None = None, new_keys: torch.Tensor | None = None):
         """Each request admits its generated token (cache.py:191-195 order: grow, append)."""
         B, d = self.B, self.device
-        pos = self.history
+        steps = self.history - self.ctx + 1   # tokens generated after this one
         self.history += 1
-        self.pool.grow(pool_capacity(self.rho, self.history))
+        self.pool.grow([pool_capacity(self.rho, n + steps) for n in self.ctx_lens])
         if getattr(self, "_ids", None) is None:
             self._ids = torch.empty((B, 1), dtype=torch.int32, device=d)
             self._one = torch.ones(B, dtype=torch.int32, device=d)
-        self._ids.fill_(pos)
+        self._ids.copy_(self.lens.view(B, 1))  # the new id of request b is its history length
         slots = self.pool.append(self._ids, self._one)
         if new_rows is None:
             new_rows = random_latent_rows(B, d, self.gen).view(B, 1, ROW)
         write_generated(self.pool, self.store, self._ids, self._one, slots, new_rows)
         if new_keys is not None:
-            self.k_cache[:, pos] = new_keys
+            self.k_cache[torch.arange(B, device=d), self.lens.long()] = new_keys
         self.lens += 1
 
     def close(self):
@@ -524,7 +536,7 @@ class SelectionRecorder:
 
     def trace(self, b: int):
         from .trace import AccessTrace, StepAccess
-        tr = AccessTrace(num_layers=len(self.layers), context_len=self.ctx, topk=self.K,
+        tr = AccessTrace(num_layers=len(self.layers), context_len=self.layers[0].ctx_lens[b], topk=self.K,
                          steps=[StepAccess(layers=s, tokens_accepted=1) for s in self.steps[b]],
                          prefill_windows=self.windows[b] if self.windows is not None else None)
         tr.check()

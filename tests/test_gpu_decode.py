@@ -170,3 +170,53 @@ def test_multilayer_model_graph_matches_oracle_per_layer():
         for b in range(B):
             assert out[b, :int(cnt[b])].tolist() == orcs[li][b].lru_order()
     model.close()
+
+
+@pytest.mark.parametrize("overlap", ["dba", "none"])
+def test_mixed_length_batch_matches_oracle(overlap):
+    """C5-style batch: per-request context lengths (and so per-request pool capacities);
+    graph-captured product steps stay bit-exact on selections and cache accounting."""
+    from paper_2512_10576_b200.cache import pool_capacity
+    from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows
+    lens = [9000, 4100, 16384, 2500]   # one request below the 4 x 2048 pool floor
+    B, K, rho = len(lens), 2048, 0.25
+    layer = DSADecodeLayer(B, lens, rho, K, max_new_tokens=8, seed=21, drift=0.97)
+    wins = layer.prefill_warmup(windows=4, record=True)
+    orc = [olru.OraclePool(pool_capacity(rho, n)) for n in lens]
+    for w in wins:
+        for b in range(B):
+            orc[b].warmup([w[b].tolist()])
+    hist = list(lens)
+
+    def mirror(check_attention, q=None):
+        torch.cuda.synchronize()
+        logits = layer.logits.cpu().numpy()
+        idx, cnt = layer.idx.cpu().numpy(), layer.cnt.cpu().numpy()
+        counts = layer.step_counts().cpu().numpy()
+        host = layer.store.host.numpy()
+        for b in range(B):
+            want = dsa.topk_indices(logits[b], hist[b], K)
+            np.testing.assert_array_equal(idx[b, :cnt[b]], want)
+            r = orc[b].access_step(want.tolist())
+            assert counts[b, 0] == len(r.hit_ids) and counts[b, 1] == len(r.miss_ids), b
+            if check_attention:
+                ref_o, _ = dsa.sparse_mla(q[b].float().cpu().numpy(), host[b, want], layer.sm_scale)
+                o = layer.out[b].float().cpu().numpy()
+                assert np.linalg.norm(o - ref_o) / np.linalg.norm(ref_o) <= 1e-2
+        for b in range(B):
+            hist[b] += 1
+            orc[b].grow_capacity(pool_capacity(rho, hist[b]))
+            orc[b].append_generated([hist[b] - 1])
+
+    layer.capture(overlap=overlap)
+    mirror(False)
+    for _ in range(3):
+        q_idx, q = layer.next_queries()
+        layer.step(q_idx, q, random_latent_rows(B, "cuda", layer.gen).view(B, 1, 656))
+        mirror(True, q)
+    layer.pool.check()
+    out, cnt = layer.pool.lru_order()
+    for b in range(B):
+        assert out[b, :int(cnt[b])].tolist() == orc[b].lru_order()
+    assert layer.lens.tolist() == hist
+    layer.close()
