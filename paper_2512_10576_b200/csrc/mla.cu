@@ -31,6 +31,25 @@
 
 #include "common.cuh"
 
+#ifdef ESS_MLA_TRACE  // scratch builds: per-tile globaltimer stamps of CTA (0, 0)
+__device__ unsigned long long g_mla_trace[8][72];
+#define MTRACE(ev, i)                                                                  \
+  do {                                                                                 \
+    if (blockIdx.x == 0 && blockIdx.y == 0 && (i) < 72) {                              \
+      unsigned long long tt;                                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                           \
+      g_mla_trace[ev][i] = tt;                                                         \
+    }                                                                                  \
+  } while (0)
+extern "C" int ess_debug_mla_trace(unsigned long long *host) {
+  return cudaMemcpyFromSymbol(host, g_mla_trace, sizeof(g_mla_trace)) == cudaSuccess ? 0 : -7;
+}
+#else
+#define MTRACE(ev, i) \
+  do {                \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr int HEADS = ESS_MLA_HEADS;      // 128 = M
@@ -104,6 +123,19 @@ __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uin
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
+}
+
+// 2^x in one MUFU op (ftz: subnormal results flush to 0, far below f16 P's range)
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// (lo, hi) -> f16x2, round to nearest, one instruction
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
 }
 
 // 16-B async global -> shared copy (L1 bypass); src_bytes = 0 zero-fills
@@ -269,6 +301,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int i = 0; i < ntiles; i++) {
       const int sb = i % NSB;
       mbar_wait(&c.s_full[sb], (i / NSB) & 1);
+      if (threadIdx.x == 0) MTRACE(2, i);  // softmax sees S(i)
       tc_fence_after();
 #if ESS_MLA_DBG_NOSOFT
       __syncwarp();
@@ -278,13 +311,18 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       uint32_t s[32];
       tmem_ld_32x32b_x32(tmem + lane_base + TM_S + sb * NB, s);
       tmem_ld_wait();
+      // raw scores; the scale folds into the exp2 argument (one FFMA per score)
       float x[32];
-      float mt = -INFINITY;
+      const int lim = n - i * NB;  // valid columns of this tile (uniform)
 #pragma unroll
-      for (int j = 0; j < NB; j++) {
-        x[j] = (i * NB + j < n) ? __uint_as_float(s[j]) * scale_log2 : -INFINITY;
-        mt = fmaxf(mt, x[j]);
+      for (int j = 0; j < NB; j++) x[j] = j < lim ? __uint_as_float(s[j]) : -INFINITY;
+      float m0 = fmaxf(x[0], x[1]), m1 = fmaxf(x[2], x[3]);
+#pragma unroll
+      for (int j = 4; j < NB; j += 4) {
+        m0 = fmaxf(m0, fmaxf(x[j], x[j + 1]));
+        m1 = fmaxf(m1, fmaxf(x[j + 2], x[j + 3]));
       }
+      const float mt = fmaxf(m0, m1) * scale_log2;
       // warp-uniform decision (tcgen05.ld/st are .sync.aligned); a lane whose own
       // max did not grow rescales by alpha = 1
       if (__any_sync(0xffffffffu, mt > m_run + RESCALE_THRESHOLD) || i == 0) {
@@ -314,22 +352,32 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         }
         m_run = m_new;
       }
-      // P (f16 pairs) over the first 16 columns of this S buffer
+      // P (f16 pairs) over the first 16 columns of this S buffer: p = 2^(x*scale - m)
+      // (ex2.approx, one MUFU op), packed two per cvt; l sums the unrounded values in
+      // four independent chains (the f16 rounding of P is below the tolerance budget)
       uint32_t p[16];
-      float lsum = 0.f;
+      float ls0 = 0.f, ls1 = 0.f, ls2 = 0.f, ls3 = 0.f;
+      const float nm = -m_run;
 #pragma unroll
-      for (int e = 0; e < 16; e++) {
-        __half2 p2 = __floats2half2_rn(exp2f(x[2 * e] - m_run), exp2f(x[2 * e + 1] - m_run));
-        float2 f = __half22float2(p2);
-        lsum += f.x + f.y;
-        p[e] = *reinterpret_cast<uint32_t *>(&p2);
+      for (int e = 0; e < 16; e += 2) {
+        const float e0 = fast_exp2(fmaf(x[2 * e], scale_log2, nm));
+        const float e1 = fast_exp2(fmaf(x[2 * e + 1], scale_log2, nm));
+        const float e2 = fast_exp2(fmaf(x[2 * e + 2], scale_log2, nm));
+        const float e3 = fast_exp2(fmaf(x[2 * e + 3], scale_log2, nm));
+        p[e] = pack_f16x2(e0, e1);
+        p[e + 1] = pack_f16x2(e2, e3);
+        ls0 += e0;
+        ls1 += e1;
+        ls2 += e2;
+        ls3 += e3;
       }
-      l_run += lsum;
+      l_run += (ls0 + ls1) + (ls2 + ls3);
       tmem_st_32x32b_x16(tmem + lane_base + TM_S + sb * NB, p);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&c.p_full[sb]);
+      if (threadIdx.x == 0) MTRACE(3, i);  // softmax warp 0 arrived P(i)
     }
     // ---------------- epilogue ---------------------------------------------------
     const bool have_o = ntiles > 0;  // TMEM O holds a valid accumulator
@@ -442,6 +490,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         // issued before this S(i), and one thread's tcgen05.mma ops execute in issue
         // order — waiting for PV(i-3) to complete would idle the tensor pipe each tile.
         mbar_wait(&c.kv_full[kb], (i / KS) & 1);
+        MTRACE(0, i);  // tile i rows in smem (MMA view)
         fence_proxy_async_smem();  // cp.async (generic proxy) rows -> tensor-core reads
         tc_fence_after();
         const uint32_t d = tmem + TM_S + sb * NB;
@@ -465,6 +514,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
         tc_commit(&c.s_full[sb]);
+        MTRACE(1, i);  // S(i) issued
       };
       // two score tiles in flight ahead of PV: the softmax of tile i and the
       // p_full -> PV hand-off overlap S(i+1) and S(i+2) on the tensor pipe
@@ -473,6 +523,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (i + LOOKAHEAD < ntiles) issue_s(i + LOOKAHEAD);
         const int kb = i % KS, sb = i % NSB;
         mbar_wait(&c.p_full[sb], (i / NSB) & 1);
+        MTRACE(4, i);  // MMA sees P(i)
         tc_fence_after();
         const uint32_t vaddr = smem_u32(skv + kb * KV_BYTES) + (uint32_t)(4 * v) * KV_BLK_BYTES;
 #pragma unroll
@@ -482,6 +533,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             mma_f16_ts(tmem + TM_O, tmem + TM_S + sb * NB + kk * 8, bd, IDESC_PV, (i | kk) ? 1u : 0u);
         }
         tc_commit(&c.pv_done[sb]);
+        MTRACE(5, i);  // PV(i) issued
         tc_commit(&c.kv_empty[kb]);
         if (i == ntiles - 1) tc_commit(&c.o_done);
       }
