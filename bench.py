@@ -242,8 +242,10 @@ def kernel_breakdown(layer, inputs, new_rows):
     counts = []
     acc = None
 
-    def timed(name, fn):
+    def timed(name, fn, warm=None):
         torch.cuda._sleep(2_000_000)
+        if warm is not None:  # an idempotent untimed launch first (host link out of idle)
+            warm()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         r = fn()
@@ -256,7 +258,10 @@ def kernel_breakdown(layer, inputs, new_rows):
                                                 layer.lens, out=layer.logits))
         timed("topk", lambda: topk(layer.logits, layer.lens, layer.K, out=layer.idx, count=layer.cnt))
         acc = timed("cache", lambda: layer.pool.access(layer.idx, layer.cnt, out=acc))
-        timed("gather", lambda: gather(layer.pool, layer.store, acc, max_ctas=layer.gather_ctas))
+        # the gather is idempotent (same rows into the same slots): re-running it first
+        # keeps the measurement off the idle host link's wake-up
+        g = lambda: gather(layer.pool, layer.store, acc, max_ctas=layer.gather_ctas)  # noqa: E731
+        timed("gather", g, warm=g)
         timed("sparse_mla", lambda: sparse_mla(layer.pool, q, acc.sel_row, layer.cnt, layer.sm_scale,
                                                out=layer.out, lse=layer.lse))
         timed("append", lambda: layer._append_device(new_rows[t]))  # the graph's device-side append

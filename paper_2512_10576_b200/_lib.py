@@ -11,7 +11,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libess_b200.so")
+# ESS_LIB overrides the library path (scratch variant builds for A/B timing)
+LIB_PATH = os.environ.get("ESS_LIB") or os.path.join(_HERE, "libess_b200.so")
 
 V, I32, I64, F32, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_float, ctypes.c_size_t
 PI32, PI64, PV = ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_void_p)

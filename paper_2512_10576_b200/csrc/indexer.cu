@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (elect_one()) {
         prefetch_tmap(&tm_k);
         prefetch_tmap(&tm_q);
+        const uint64_t kpol = l2_policy_evict_first();
         TileCursor cur;
         cur.seek(c.pref, B, t0);
         int qs = 1, prev_b = -1, len_b = 0;
@@ -153,8 +154,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           mbar_wait(&c.empty[s], ((it / STAGES) & 1) ^ 1);
           mbar_arrive_expect_tx(&c.full[s], nsub * KT_BYTES);
           for (int j = 0; j < nsub; j++)
+#ifndef ESS_K1_NO_EVICT_FIRST
+            // keys are streamed once: evict-first keeps L2 for the logits K2 reads next
+            tma_load_2d_hint(smem + (size_t)s * UT_BYTES + j * KT_BYTES, &tm_k, &c.full[s], 0,
+                             (int32_t)(cur.b * k_ld + (int64_t)cur.t * UNIT_M + j * TILE_M), kpol);
+#else
             tma_load_2d(smem + (size_t)s * UT_BYTES + j * KT_BYTES, &tm_k, &c.full[s], 0,
                         (int32_t)(cur.b * k_ld + (int64_t)cur.t * UNIT_M + j * TILE_M));
+#endif
           cur.next(c.pref, B);
         }
       }

@@ -23,6 +23,7 @@ q_t = a q_{t-1} + sqrt(1-a^2) eps, which sets the step-to-step selection overlap
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -82,6 +83,7 @@ class DSADecodeLayer:
         self.micro = 2       # DBA micro-batches per step (overlap="dba")
         self.max_split = 4   # fused K5: KV splits per request at small batch
         self.min_gather_sms = 20
+        self.early_gather_sms = int(os.environ.get("ESS_EARLY_GATHER_SMS", "20"))
         self.Lmax = ((context_len + max_new_tokens + 127) // 128) * 128
         self.gen = torch.Generator(device=self.device).manual_seed(seed)
         d, g, B = self.device, self.gen, batch
@@ -239,7 +241,11 @@ class DSADecodeLayer:
             # K1 of micro-batch i on the main stream; its top-k and cache manager on the
             # selection stream, so they overlap the NEXT micro-batch's indexer, which
             # leaves SMs free for them (one per request) and for the running gather
-            ctas = 0 if i == 0 else sms - gsms - prev
+            # gathers of earlier micro-batches run beside the next indexer, not beside
+            # attention, and may take more SMs (early_gather_sms) than the last one
+            g_i = gsms if i == len(ranges) - 1 else max(gsms, self.early_gather_sms)
+            g_prev = 0 if i == 0 else (gsms if i - 1 == len(ranges) - 1 else max(gsms, self.early_gather_sms))
+            ctas = 0 if i == 0 else sms - g_prev - prev
             indexer_logits(q_idx[a:b], self.w[a:b], self.k_cache[a:b], self.k_scale[a:b],
                            self.lens[a:b], out=self.logits[a:b], max_ctas=ctas)
             scored = torch.cuda.Event()
@@ -252,7 +258,7 @@ class DSADecodeLayer:
                 ready.record(sel)
             side.wait_event(ready)
             with torch.cuda.stream(side):
-                gather(self.pool, self.store, self._acc_view(a, b), begin=a, max_ctas=gsms,
+                gather(self.pool, self.store, self._acc_view(a, b), begin=a, max_ctas=g_i,
                        exclusive=True, landed=self._landed[a:b] if fused else None)
             prev = b - a
         main.wait_event(ready)  # attention reads every micro-batch's selections
