@@ -72,6 +72,12 @@ constexpr int QS_BYTES = QS_BLKS * QBLK_BYTES;     // 65536
 constexpr int KV_BLK_BYTES = NB * 128;             // 4096
 constexpr int KV_BYTES = NBLK * KV_BLK_BYTES;      // 36864
 constexpr int KS = 4;                              // KV ring depth
+// Loader completion: 1 = each thread's cp.async completion arrives on the tile barrier
+// (cp.async.mbarrier.arrive.noinc); 0 = wait_group + proxy fence + one arrive per warp,
+// the form compute-sanitizer's racecheck models (same speed at two S buffers).
+#ifndef ESS_MLA_ASYNC_ARRIVE
+#define ESS_MLA_ASYNC_ARRIVE 0
+#endif
 #ifndef ESS_MLA_DBG_NOLOAD  // timing-only switches for scratch builds (scripts/variant_lib.sh)
 #define ESS_MLA_DBG_NOLOAD 0
 #endif
@@ -87,6 +93,9 @@ constexpr int KS = 4;                              // KV ring depth
 // the MMA warp issues S(i+LOOKAHEAD) before PV(i) frees slot i: the ring must hold
 // tiles i..i+LOOKAHEAD at once
 static_assert(KS >= LOOKAHEAD + 1, "KV ring too shallow for the S lookahead");
+// wait_group loader: tile j is signalled after tile j+1 is issued, i.e. once slot
+// (j+1) % KS is free; S(i+LOOKAHEAD) must not wait for PV(i) -> KS >= LOOKAHEAD + 3
+static_assert(ESS_MLA_ASYNC_ARRIVE || KS >= LOOKAHEAD + 3, "KV ring too shallow for the lagged loader");
 constexpr int MAX_N = ESS_MAX_REQUEST;
 constexpr int NSOFT = 4, NLOAD = 4;
 constexpr int MMA_WARP = NSOFT, LOAD0 = NSOFT + 1;
@@ -222,7 +231,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < KS; i++) {
-      mbar_init(&c.kv_full[i], NLOAD * 32);  // one cp.async completion arrive per loader thread
+      // async-arrive: one cp.async completion arrive per loader thread; else one per warp
+      mbar_init(&c.kv_full[i], ESS_MLA_ASYNC_ARRIVE ? NLOAD * 32 : NLOAD);
       mbar_init(&c.kv_empty[i], 1);
     }
     for (int i = 0; i < NSB; i++) {
@@ -302,6 +312,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int sb = i % NSB;
       mbar_wait(&c.s_full[sb], (i / NSB) & 1);
       if (threadIdx.x == 0) MTRACE(2, i);  // softmax sees S(i)
+      // observe PV(i - NSB)'s pv_done phase: s_full(i) tracks it (issued before S(i)), so
+      // this never stalls; every phase gets a waiter (compute-sanitizer synccheck)
+      if (i >= NSB) mbar_wait(&c.pv_done[sb], ((i - NSB) / NSB) & 1);
       tc_fence_after();
 #if ESS_MLA_DBG_NOSOFT
       __syncwarp();
@@ -383,6 +396,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const bool have_o = ntiles > 0;  // TMEM O holds a valid accumulator
     if (ntiles > 0) {
       mbar_wait(&c.o_done, 0);
+      for (int k = max(0, ntiles - NSB); k < ntiles; k++)  // the last PV phases (all done)
+        mbar_wait(&c.pv_done[k % NSB], (k / NSB) & 1);
       tc_fence_after();
     }
     if (to_ws) {
@@ -546,6 +561,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int w = warp - LOAD0;
     const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b) * rows_per_pool * ESS_SLOT_ROW_BYTES;
     const uint32_t kv0 = smem_u32(skv);
+    [[maybe_unused]] auto signal = [&](int i) {
+      fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&c.kv_full[i % KS]);
+    };
     bool pending = fetched && n2t > 0;  // fetched rows not yet known to have landed
     for (int i = 0; i < ntiles; i++) {
       const int kb = i % KS;
@@ -569,12 +589,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                        src + ch * 16, ok ? 16u : 0u);
         }
       }
+#if ESS_MLA_ASYNC_ARRIVE
       // tile i is full once every loader thread's copies landed: each thread's
       // completion arrives on kv_full by itself, so no loader waits on its own copies
       // and the ring runs as far ahead as the free slots allow
       cp_async_arrive_noinc(&c.kv_full[kb]);
+#else
+      // one commit group per tile, signalled one tile later (wait_group 1: two tiles
+      // in flight per warp); the generic->async proxy fence precedes the arrive
+      cp_async_commit();
+      if (i >= 1) {
+        cp_async_wait<1>();
+        signal(i - 1);
+      }
+#endif
     }
     cp_async_wait<0>();
+#if !ESS_MLA_ASYNC_ARRIVE
+    if (ntiles > 0) signal(ntiles - 1);
+#endif
   }
   tc_fence_before();
   __syncthreads();

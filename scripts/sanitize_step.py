@@ -1,15 +1,30 @@
-"""Small decode workload for compute-sanitizer (memcheck / racecheck / synccheck)."""
-import os, sys
+"""Small decode workloads for compute-sanitizer (memcheck / racecheck / synccheck):
+the oversize path (ctx 4K, cap 1024 < K) and the normal path (mixed 9K-13K contexts,
+early admission), each under the none / DA / DBA schedules; small batches take the
+split fused K5 + combine; plus the bulk-copy gather variant."""
+import os
+import sys
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import torch
-from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows
+import torch  # noqa: E402
+
+from paper_2512_10576_b200 import transfer  # noqa: E402
+from paper_2512_10576_b200.decode import DSADecodeLayer  # noqa: E402
+
 B = int(os.environ.get("B", 2))
-layer = DSADecodeLayer(B, 4096, 0.25, 2048, max_new_tokens=8, seed=1, drift=0.9)
-layer.prefill_warmup(windows=2)
-for overlap in ("none", "da"):
+for ctx in (4096, [9000 + 1500 * b for b in range(B)]):
+    layer = DSADecodeLayer(B, ctx, 0.25, 2048, max_new_tokens=8, seed=1, drift=0.9)
+    layer.prefill_warmup(windows=2)
+    for overlap in ("none", "da", "dba"):
+        q_idx, q = layer.next_queries()
+        layer.attend(q_idx, q, overlap=overlap)
+        layer.append_token()
+    transfer.GATHER_BULK = True
     q_idx, q = layer.next_queries()
-    layer.attend(q_idx, q, overlap=overlap)
+    layer.attend(q_idx, q, overlap="none")
     layer.append_token()
-torch.cuda.synchronize()
-layer.pool.check()
+    transfer.GATHER_BULK = False
+    torch.cuda.synchronize()
+    layer.pool.check()
+    layer.close()
 print("sanitize workload done")
