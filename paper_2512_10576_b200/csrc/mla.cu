@@ -155,7 +155,7 @@ __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 // arrive on an mbarrier when every cp.async this thread issued so far has completed
 // (the arrive counts toward the barrier's expected count)
-__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
+[[maybe_unused]] __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 template <int N>
