@@ -39,7 +39,9 @@ extern "C" {
  * 64-B read requests; an unaligned 656-B row straddles 12 of them, an aligned one 11
  * (+6% zero-copy gather bandwidth, measured; profiles/README.md).  Rows of the host
  * store are addressed as d_host_rows + (pool * host_pool_stride_rows + id) * pitch. */
+#ifndef ESS_HOST_ROW_PITCH  /* scratch builds may override (A/B of the host layout) */
 #define ESS_HOST_ROW_PITCH 704
+#endif
 #define ESS_SLOT_ROW_BYTES 1152 /* 576 x f16 */
 #define ESS_NOPE_DIM 512
 #define ESS_ROPE_DIM 64

@@ -63,7 +63,9 @@ ESS_GATHER_BULK = 2
 ESS_HOST_HUGEPAGES, ESS_HOST_NUMA_BOUND = 1, 2
 MAX_REQUEST = 2048
 LATENT_ROW_BYTES = 656   # host store / transfer format (e4m3 NoPE + scales + bf16 RoPE)
-HOST_ROW_PITCH = 704     # host store row pitch (64-B aligned rows; ESS_HOST_ROW_PITCH)
+# host store row pitch (64-B aligned rows; ESS_HOST_ROW_PITCH); the env override pairs with
+# a scratch library built with the same -DESS_HOST_ROW_PITCH
+HOST_ROW_PITCH = int(os.environ.get("ESS_HOST_ROW_PITCH", "704"))
 SLOT_ROW_BYTES = 1152    # GPU slot store format (576 x f16, dequantised on admission)
 
 _lib = None
