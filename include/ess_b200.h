@@ -120,6 +120,17 @@ int ess_pool_access(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d
                     int32_t *d_miss_ids, int32_t *d_evicted_ids, int32_t *d_sel_row,
                     int32_t *d_hit_row, int32_t *d_miss_row, int32_t *d_counts,
                     int32_t out_stride, int32_t flags, void *stream);
+/* Early-gather split of ess_pool_access (needs staging_rows >= 2048 and n <= capacity):
+ * ess_pool_split is the read-only hit/miss split — hit rows, miss ids and STAGING rows
+ * (cap_max + j) for the misses, counts (hits, misses) — so the host-link gather can
+ * start at once; ess_pool_access with d_miss_row = a settle-slot buffer then updates
+ * the LRU state and reports each miss's final slot; ess_pool_settle copies the fetched
+ * rows from staging into those slots (after the gather, concurrently with attention). */
+int ess_pool_split(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_req,
+                   const int32_t *d_n, int32_t req_stride, int32_t *d_hit_row, int32_t *d_miss_ids,
+                   int32_t *d_miss_row, int32_t *d_counts, int32_t out_stride, void *stream);
+int ess_pool_settle(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_slot,
+                    const int32_t *d_counts, int32_t stride, void *stream);
 /* admit generated ids at top recency; d_slot_out [num][stride] gets each id's
  * slot (may be NULL)                                     (SparsePool.append_generated) */
 int ess_pool_append(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_ids,

@@ -33,6 +33,8 @@ SIGNATURES = {
     "ess_pool_warmup": ([V, I32, I32, V, V, I32, V, V], ctypes.c_int),
     "ess_pool_access": ([V, I32, I32, V, V, I32, V, V, V, V, V, V, V, I32, I32, V], ctypes.c_int),
     "ess_pool_append": ([V, I32, I32, V, V, I32, V, V], ctypes.c_int),
+    "ess_pool_split": ([V, I32, I32, V, V, I32, V, V, V, V, I32, V], ctypes.c_int),
+    "ess_pool_settle": ([V, I32, I32, V, V, I32, V], ctypes.c_int),
     "ess_pool_admit": ([V, I32, I32, V, V, ctypes.c_double, V, I32, V, I64, V, V], ctypes.c_int),
     "ess_pool_lru_order": ([V, I32, I32, V, V, V], ctypes.c_int),
     "ess_pool_counters": ([V, I32, I32, V, V], ctypes.c_int),

@@ -157,6 +157,24 @@ class PoolSet:
             out.counts.data_ptr(), stride, flags, _lib.stream_handle()))
         return out
 
+    def split(self, req: torch.Tensor, n: torch.Tensor, out: AccessBatch, begin: int = 0) -> AccessBatch:
+        """Early-gather K3a: read-only hit/miss split; misses point at staging rows
+        (needs staging_rows >= 2048; see ess_pool_split)."""
+        num = req.shape[0]
+        self._range(begin, num)
+        _lib.check(self._L.ess_pool_split(
+            self._h, begin, num, req.data_ptr(), n.data_ptr(), req.stride(0), out.hit_row.data_ptr(),
+            out.miss_ids.data_ptr(), out.miss_row.data_ptr(), out.counts.data_ptr(),
+            out.miss_ids.stride(0), _lib.stream_handle()), "ess_pool_split")
+        return out
+
+    def settle(self, slots: torch.Tensor, counts: torch.Tensor, begin: int = 0) -> None:
+        """Fetched miss rows: staging -> their final slots (ess_pool_settle)."""
+        num = slots.shape[0]
+        self._range(begin, num)
+        _lib.check(self._L.ess_pool_settle(self._h, begin, num, slots.data_ptr(), counts.data_ptr(),
+                                           slots.stride(0), _lib.stream_handle()), "ess_pool_settle")
+
     def append(self, ids: torch.Tensor, m: torch.Tensor, begin: int = 0,
                slots: torch.Tensor | None = None) -> torch.Tensor:
         num = ids.shape[0]

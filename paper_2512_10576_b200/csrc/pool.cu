@@ -843,6 +843,72 @@ __global__ void pool_lru_order_kernel(PoolView pv, int begin, int32_t *out, int3
   if (blockIdx.y == 0 && threadIdx.x == 0) count[b] = pv.meta[p].size;
 }
 
+// ---- early-gather split of K3 -----------------------------------------------------
+// "K3a": the hit/miss split alone (read-only on the LRU state: one slot_of lookup per
+// requested id).  Misses are pointed at per-pool staging rows cap_max + j, so the host
+// link gather can start before victim selection; the full access ("K3b") then updates
+// the LRU state exactly as one access would and reports each miss's final slot, and a
+// settle pass moves the fetched rows from staging into those slots.  Victims are never
+// requested ids (n <= cap), so K5 reads hits in place and misses from staging while
+// the settle writes only victim slots.
+__global__ void __launch_bounds__(NT) pool_split_kernel(PoolView pv, int begin,
+                                                        const int32_t *__restrict__ req,
+                                                        const int32_t *__restrict__ req_n,
+                                                        int req_stride, int32_t *hit_row_out,
+                                                        int32_t *miss_out, int32_t *miss_row_out,
+                                                        int32_t *counts_out, int out_stride) {
+  __shared__ int wbuf[NT / 32];
+  const int t = threadIdx.x, b = blockIdx.x, p = begin + b;
+  const int n = min(max(req_n[b], 0), MAXR);
+  const int32_t *slot_of = pv.slot_of + (int64_t)p * pv.max_ids;
+  int x[EPT], s[EPT], h = 0;
+#pragma unroll
+  for (int e = 0; e < EPT; e++) {
+    const int i = t * EPT + e;
+    x[e] = i < n ? req[(int64_t)b * req_stride + i] : -1;
+  }
+#pragma unroll
+  for (int e = 0; e < EPT; e++) {
+    s[e] = (x[e] >= 0 && x[e] < pv.max_ids) ? slot_of[x[e]] : -1;  // bad ids: K3b flags them
+    h += (t * EPT + e < n) && s[e] >= 0;
+  }
+  int nhit;
+  int hr = block_exclusive_scan<NT>(h, wbuf, &nhit);
+  const int64_t ob = (int64_t)b * out_stride;
+#pragma unroll
+  for (int e = 0; e < EPT; e++) {
+    const int i = t * EPT + e;
+    if (i >= n) continue;
+    if (s[e] >= 0) {
+      hit_row_out[ob + hr++] = s[e];
+    } else {
+      const int j = i - hr;
+      miss_out[ob + j] = x[e];
+      miss_row_out[ob + j] = pv.cap_max + j;
+    }
+  }
+  if (t == 0) {
+    counts_out[b * 4 + 0] = nhit;
+    counts_out[b * 4 + 1] = n - nhit;
+    counts_out[b * 4 + 2] = 0;
+    counts_out[b * 4 + 3] = 0;
+  }
+}
+
+// settle: staging row cap_max + j -> final slot slot[j] (< 0: not admitted), one warp
+// per row, for the counts[b*4+1] misses of each pool
+__global__ void pool_settle_kernel(PoolView pv, int begin, const int32_t *__restrict__ slot,
+                                   const int32_t *__restrict__ counts, int stride) {
+  const int b = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int m = counts[b * 4 + 1];
+  uint8_t *base = pv.rows + (int64_t)(begin + b) * pv.rows_per_pool * pv.row_bytes;
+  for (int j = blockIdx.y * (blockDim.x / 32) + warp; j < m; j += gridDim.y * (blockDim.x / 32)) {
+    const int s = slot[(int64_t)b * stride + j];
+    if (s >= 0) copy_row(base + (int64_t)(pv.cap_max + j) * pv.row_bytes, base + (int64_t)s * pv.row_bytes,
+                         lane, pv.row_bytes);
+  }
+}
+
 __global__ void pool_counters_kernel(PoolView pv, int begin, int num, int64_t *out) {
   int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= num) return;
@@ -1288,6 +1354,30 @@ int ess_pool_warmup(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_id
   pool_step_kernel<MODE_WARMUP><<<num, NT, 0, (cudaStream_t)stream>>>(
       view(p), begin, d_ids, d_n, stride, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
       nullptr, 0, 0, d_inserted);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+int ess_pool_split(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_req, const int32_t *d_n,
+                   int32_t req_stride, int32_t *d_hit_row, int32_t *d_miss_ids, int32_t *d_miss_row,
+                   int32_t *d_counts, int32_t out_stride, void *stream) {
+  if (!range_ok(p, begin, num) || !d_req || !d_n || !d_hit_row || !d_miss_ids || !d_miss_row ||
+      !d_counts || out_stride < 1 || req_stride < 0 || p->staging < MAXR)
+    return ESS_ERR_ARG;
+  if (num == 0) return ESS_OK;
+  pool_split_kernel<<<num, NT, 0, (cudaStream_t)stream>>>(view(p), begin, d_req, d_n, req_stride,
+                                                           d_hit_row, d_miss_ids, d_miss_row,
+                                                           d_counts, out_stride);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+int ess_pool_settle(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_slot,
+                    const int32_t *d_counts, int32_t stride, void *stream) {
+  if (!range_ok(p, begin, num) || !p->rows || !d_slot || !d_counts || stride < 1) return ESS_ERR_ARG;
+  if (num == 0) return ESS_OK;
+  pool_settle_kernel<<<dim3(num, 4), 256, 0, (cudaStream_t)stream>>>(view(p), begin, d_slot, d_counts,
+                                                                     stride);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }

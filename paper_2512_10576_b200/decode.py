@@ -99,7 +99,10 @@ class DSADecodeLayer:
         caps = [pool_capacity(sparse_ratio, n) for n in self.ctx_lens]
         self.cap0 = min(caps)
         self.cap_max = pool_capacity(sparse_ratio, self.Lmax)
-        staging = topk_k if self.cap0 < topk_k else 0
+        # early gather (DA/DBA): misses land in per-pool staging rows while the cache
+        # manager still selects victims; needs every pool to hold a whole selection
+        self.early_gather = self.cap0 >= topk_k and os.environ.get("ESS_EARLY_GATHER", "1") == "1"
+        staging = topk_k if (self.cap0 < topk_k or self.early_gather) else 0
         self.pool = PoolSet(B, self.Lmax, self.cap_max, caps, row_bytes=_lib.SLOT_ROW_BYTES,
                             staging_rows=staging, device=d)
         # drifting queries
@@ -205,6 +208,8 @@ class DSADecodeLayer:
             z = lambda: torch.empty((B, self.K), dtype=torch.int32, device=self.device)  # noqa: E731
             self.acc = AccessBatch(counts=torch.empty((B, 4), dtype=torch.int32, device=self.device),
                                    sel_row=z(), miss_ids=z(), miss_row=z(), hit_row=z())
+            self._settle = z()
+            self._counts_b = torch.empty((B, 4), dtype=torch.int32, device=self.device)
         acc = self.acc
         if overlap == "none":
             self._select(q_idx, 0, B)
@@ -234,7 +239,8 @@ class DSADecodeLayer:
         ranges = self.micro_batches(micro if overlap == "dba" else 1)
         if getattr(self, "_sel", None) is None:
             self._sel = torch.cuda.Stream(self.device)
-        sel = self._sel
+            self._lru = torch.cuda.Stream(self.device)
+        sel, lru = self._sel, self._lru
         ready = None
         prev = 0  # requests of the previous micro-batch (its K2/K3 run beside this K1)
         for i, (a, b) in enumerate(ranges):
@@ -253,19 +259,43 @@ class DSADecodeLayer:
             sel.wait_event(scored)
             with torch.cuda.stream(sel):
                 topk(self.logits[a:b], self.lens[a:b], self.K, out=self.idx[a:b], count=self.cnt[a:b])
-                self.pool.access(self.idx[a:b], self.cnt[a:b], begin=a, out=self._acc_view(a, b))
+                if self.early_gather:
+                    # K3a: hit/miss split only (misses -> staging rows); the gather starts now
+                    self.pool.split(self.idx[a:b], self.cnt[a:b], out=self._acc_view(a, b), begin=a)
+                else:
+                    self.pool.access(self.idx[a:b], self.cnt[a:b], begin=a, out=self._acc_view(a, b))
                 ready = torch.cuda.Event()
                 ready.record(sel)
             side.wait_event(ready)
             with torch.cuda.stream(side):
                 gather(self.pool, self.store, self._acc_view(a, b), begin=a, max_ctas=g_i,
                        exclusive=True, landed=self._landed[a:b] if fused else None)
+                fetched = torch.cuda.Event()
+                fetched.record(side)
+            if self.early_gather:
+                # K3b (the LRU update proper, reporting each miss's final slot) and the
+                # settle (staging -> final slots, after the gather) on their own stream, so
+                # neither delays the next micro-batch's selection or gather
+                lru.wait_event(ready)
+                with torch.cuda.stream(lru):
+                    self.pool.access(self.idx[a:b], self.cnt[a:b], begin=a, out=AccessBatch(
+                        counts=self._counts_b[a:b], sel_row=None, miss_ids=None,
+                        miss_row=self._settle[a:b], hit_row=None))
+                    lru_ready = torch.cuda.Event()
+                    lru_ready.record(lru)
+                    lru.wait_event(fetched)
+                    self.pool.settle(self._settle[a:b], self.acc.counts[a:b], begin=a)
+            else:
+                lru_ready = ready
             prev = b - a
+        if self.early_gather:
+            settled = torch.cuda.Event()
+            settled.record(lru)
         main.wait_event(ready)  # attention reads every micro-batch's selections
         if new_rows is not None:
             if getattr(self, "_adm", None) is None:
                 self._adm = torch.cuda.Stream(self.device)
-            self._adm.wait_event(ready)
+            self._adm.wait_event(lru_ready)  # the final LRU state of every micro-batch
             with torch.cuda.stream(self._adm):
                 self._append_device(new_rows)
             admitted = torch.cuda.Event()
@@ -276,6 +306,8 @@ class DSADecodeLayer:
             sparse_mla_da(self.pool, q, acc, self._landed, self.sm_scale, out=self.out, lse=self.lse,
                           split=split, workspace=self._ws_split if split > 1 else None)
             main.wait_event(done)
+            if self.early_gather:
+                main.wait_event(settled)
             if new_rows is not None:
                 main.wait_event(admitted)
             return self.out, self.lse
@@ -284,6 +316,8 @@ class DSADecodeLayer:
         main.wait_event(done)
         sparse_mla(self.pool, q, acc.miss_row, acc.counts[:, 1], self.sm_scale, out=self.out,
                    lse=self.lse, workspace=self._ws, mode="resume")
+        if self.early_gather:
+            main.wait_event(settled)
         if new_rows is not None:
             main.wait_event(admitted)
         return self.out, self.lse
