@@ -40,7 +40,7 @@ CONFIGS = {
                         "(global 128 over 8 GPUs), ctx 32K, 25% GPU slot pool"),
     # configs[4]: mixed-length batch, context log-uniform over [8K, 128K] (seeded per rank);
     # the pool-size / hit-rate sweep is scripts/sweep_c5.py
-    "c5": dict(batch=64, context_len=(8192, 131072), sparse_ratio=0.25, micro=3, first=0.375,
+    "c5": dict(batch=64, context_len=(8192, 131072), sparse_ratio=0.25, micro=2, first=0.375,
                workload="C5: one DSA layer decode, batch 64/GPU of mixed 8K-128K contexts "
                         "(log-uniform), 25% GPU slot pool"),
     "c4": dict(batch=64, context_len=131072, sparse_ratio=0.10, micro=3, first=0.375,
