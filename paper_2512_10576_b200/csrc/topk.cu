@@ -22,6 +22,7 @@
 // (k - #greater) keys == T in index order; CTA r's output offset is the cluster prefix
 // of the (greater, equal) counts of CTAs 0..r-1.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -385,6 +386,13 @@ extern "C" int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len,
   // DSMEM histogram sums cost more than the shorter slices save (profiles/README.md).
   int cln = 1;
   while (cln < 8 && (ld + cln - 1) / cln > SLICE_MAX) cln *= 2;
+  // A/B switch (scratch timing): a minimum cluster size per row
+  static const int min_cln = [] {
+    const char *e = getenv("ESS_TOPK_MIN_CLUSTER");
+    int v = e ? atoi(e) : 1;
+    return v == 2 || v == 4 || v == 8 ? v : 1;
+  }();
+  while (cln < min_cln) cln *= 2;
   if ((ld + cln - 1) / cln > SLICE_MAX) return ESS_ERR_ARG;  // rows longer than 320K tokens
   cudaStream_t s = (cudaStream_t)stream;
   int rc;
