@@ -244,3 +244,61 @@ def test_split_attention_partial_then_resume(split):
         rel = np.linalg.norm(out[b] - ref_o) / max(np.linalg.norm(ref_o), 1e-12)
         assert rel <= 1e-2, (split, b, rel)
         assert np.abs(lse[b] - ref_l).max() <= 1e-2
+
+
+def test_early_gather_split_access_settle_matches_plain_access():
+    """Early-gather form of K3 + K4: the read-only split (misses -> staging rows), the
+    gather into staging, the LRU update reporting final slots and the settle copy end in
+    the same pool state and slot contents as one plain access + gather."""
+    from paper_2512_10576_b200.cache import AccessBatch, PoolSet
+    from paper_2512_10576_b200.decode import random_latent_rows
+    from paper_2512_10576_b200.transfer import HostLatentStore, gather
+    P, ids, cap, K = 3, 9000, 2500, 2048
+    store = HostLatentStore(P, ids)
+    for p in range(P):
+        store.host[p].copy_(random_latent_rows(ids, "cuda"))
+    a = PoolSet(P, ids, cap, cap, row_bytes=1152, staging_rows=K)
+    b = PoolSet(P, ids, cap, cap, row_bytes=1152, staging_rows=K)
+    rng = np.random.default_rng(3)
+    z = lambda: torch.zeros((P, K), dtype=torch.int32, device="cuda")  # noqa: E731
+    for step in range(4):
+        sets = [np.sort(rng.choice(6000 + 500 * step, size=K, replace=False)) for _ in range(P)]
+        req = torch.as_tensor(np.stack(sets).astype(np.int32), device="cuda")
+        n = torch.full((P,), K, dtype=torch.int32, device="cuda")
+        ra = a.access(req, n, lists=True)
+        gather(a, store, ra)
+        sb = AccessBatch(counts=torch.zeros((P, 4), dtype=torch.int32, device="cuda"), sel_row=z(),
+                         miss_ids=z(), miss_row=z(), hit_row=z())
+        b.split(req, n, out=sb)
+        settle, cb = z(), torch.zeros((P, 4), dtype=torch.int32, device="cuda")
+        gather(b, store, sb)
+        b.access(req, n, out=AccessBatch(counts=cb, sel_row=None, miss_ids=None, miss_row=settle,
+                                         hit_row=None))
+        b.settle(settle, sb.counts)
+        torch.cuda.synchronize()
+        a.check()
+        b.check()
+        ca, cs = ra.counts.cpu().numpy(), sb.counts.cpu().numpy()
+        np.testing.assert_array_equal(ca[:, :2], cs[:, :2])
+        np.testing.assert_array_equal(cb.cpu().numpy()[:, :2], cs[:, :2])
+        for p in range(P):
+            m = int(ca[p, 1])
+            np.testing.assert_array_equal(ra.miss_ids[p, :m].cpu().numpy(), sb.miss_ids[p, :m].cpu().numpy())
+            # staging rows for the misses, the plain access's slots for its misses
+            assert sb.miss_row[p, :m].tolist() == list(range(b.cap_max, b.cap_max + m))
+            np.testing.assert_array_equal(settle[p, :m].cpu().numpy(), ra.miss_row[p, :m].cpu().numpy())
+        oa, na = a.lru_order()
+        ob, nb = b.lru_order()
+        np.testing.assert_array_equal(na.cpu().numpy(), nb.cpu().numpy())
+        for p in range(P):
+            assert oa[p, :int(na[p])].tolist() == ob[p, :int(nb[p])].tolist()
+    ra_rows, rb_rows = a.rows_view().cpu().numpy(), b.rows_view().cpu().numpy()
+    for p in range(P):
+        order = oa[p, :int(na[p])].cpu().numpy()
+        sa = a.lookup(p, torch.as_tensor(order, device="cuda")).cpu().numpy()
+        sbl = b.lookup(p, torch.as_tensor(order, device="cuda")).cpu().numpy()
+        np.testing.assert_array_equal(sa, sbl)
+        np.testing.assert_array_equal(ra_rows[p, sa].view(np.uint16), rb_rows[p, sbl].view(np.uint16))
+    a.close()
+    b.close()
+    store.close()
