@@ -167,6 +167,14 @@ def _cpu_pool(workers):
     return _cpu_pool.p
 
 
+def _cpu_pool_close():
+    p = getattr(_cpu_pool, "p", None)
+    if p is not None:
+        p.close()
+        p.join()
+        del _cpu_pool.p
+
+
 def cpu_reference_rate(cfg, budget_s: float = 12.0, seed: int = 0):
     """The CPU oracle on every host core: rounds of one request per core (one decode step
     each, the config's shapes), wall-clock timed.  Returns (tokens/s, sample, cores)."""
@@ -201,6 +209,7 @@ def run_reference(args, cfg):
         v, sample, threads = cpu_reference_rate(cfg, budget_s=5.0)
         vals.append(v)
     el = time.perf_counter() - t0
+    _cpu_pool_close()
     value = statistics.mean(vals)
     line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps,
@@ -393,6 +402,7 @@ def run_ours(args, cfg):
     line = None
     if rank == 0:
         cpu_v, cpu_sample, cpu_threads = cpu_reference_rate(cfg, budget_s=12.0)
+        _cpu_pool_close()
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": t_max * 1e3 / K,

@@ -47,11 +47,27 @@ acc_f = decode.PoolSet.access
 
 def access(self, *a, **k):
     r = acc_f(self, *a, **k)
-    mark("K3 cache")
+    mark("K3(b) LRU")
     return r
 
 
 decode.PoolSet.access = access
+split_f, settle_f = decode.PoolSet.split, decode.PoolSet.settle
+
+
+def split(self, *a, **k):
+    r = split_f(self, *a, **k)
+    mark("K3a split")
+    return r
+
+
+def settle(self, *a, **k):
+    r = settle_f(self, *a, **k)
+    mark("settle")
+    return r
+
+
+decode.PoolSet.split, decode.PoolSet.settle = split, settle
 adm_f = DSADecodeLayer._append_device
 
 
