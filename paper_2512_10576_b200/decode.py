@@ -343,6 +343,20 @@ class DSADecodeLayer:
         if not early:
             self._append_device(self.rows_in)
 
+    def launches_per_step(self, overlap: str) -> int:
+        """Kernels of this library one captured step launches (the graph's kernel nodes):
+        per micro-batch K1, K2, K3 (or K3a + K3b with the early gather), K4 (+ settle);
+        then K5 (+ the KV-split combine) and the admission."""
+        if overlap == "none":
+            return 6  # K1, K2, K3, K4, K5, admission
+        micro = self.micro if overlap == "dba" else 1
+        per_mb = 6 if self.early_gather else 4
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        fused = self.fuse_da and 2 * self.B <= sms - 8
+        split = max(1, min(self.max_split, (sms - 8 - self.min_gather_sms) // (2 * self.B))) if fused else 1
+        k5 = (1 + (split > 1)) if fused else 2
+        return per_mb * micro + k5 + 1
+
     def access_totals(self) -> tuple[int, int]:
         """(hits, misses) summed over the layer's pools since creation (the pools'
         own counters, cache.py:41-43): the difference across a run gives its hit rate."""
