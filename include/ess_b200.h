@@ -72,6 +72,8 @@ typedef struct ess_pool ess_pool;
 /* ---- library ---------------------------------------------------------------- */
 const char *ess_version(void);
 const char *ess_status_string(int status);
+/* ESS_HOST_ROW_PITCH as compiled into this library */
+int ess_host_row_pitch(void);
 /* cudaHostRegister(mapped) + device alias: the host latent store (UVA gather source) */
 int ess_host_register(void *host_ptr, size_t bytes, void **d_alias);
 int ess_host_unregister(void *host_ptr);

@@ -21,6 +21,7 @@ PI32, PI64, PV = ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
 SIGNATURES = {
     "ess_version": ([], ctypes.c_char_p),
     "ess_status_string": ([ctypes.c_int], ctypes.c_char_p),
+    "ess_host_row_pitch": ([], ctypes.c_int),
     "ess_host_register": ([V, SZ, PV], ctypes.c_int),
     "ess_host_unregister": ([V], ctypes.c_int),
     "ess_timestamp": ([V, V], ctypes.c_int),
@@ -85,6 +86,9 @@ def load():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = res
+        if L.ess_host_row_pitch() != HOST_ROW_PITCH:
+            raise ImportError(f"{LIB_PATH} was built with host row pitch {L.ess_host_row_pitch()}, "
+                              f"the Python side uses {HOST_ROW_PITCH} (ESS_HOST_ROW_PITCH)")
         _lib = L
     return _lib
 

@@ -59,6 +59,10 @@ extern "C" {
 
 const char *ess_version(void) { return "ess_b200 0.1 sm_100a"; }
 
+// the host latent store row pitch this library was compiled with (the Python side
+// lays the store out with its own constant and must agree)
+int ess_host_row_pitch(void) { return ESS_HOST_ROW_PITCH; }
+
 const char *ess_status_string(int status) {
   switch (status) {
     case ESS_OK: return "ok";

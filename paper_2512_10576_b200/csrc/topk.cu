@@ -50,6 +50,10 @@ extern "C" int ess_debug_topk_prof(unsigned long long *host) {
 
 namespace {
 
+#ifndef ESS_TOPK_LIST_UNROLL
+#define ESS_TOPK_LIST_UNROLL 2
+#endif
+constexpr int LIST_UNROLL = ESS_TOPK_LIST_UNROLL;
 constexpr int NT = 1024;                  // threads per CTA
 constexpr int NW = NT / 32;
 constexpr int VEC = 4;
@@ -229,7 +233,7 @@ __global__ void __launch_bounds__(NT, 1)
   // 128-key chunks: each lane reads 4 consecutive keys with one 16-B shared load and
   // the 4 ballots (one per vector slot) give every key's rank in row order
   int cnt = 0;
-#pragma unroll 2
+#pragma unroll LIST_UNROLL
   for (int i = lo4; i < hi4; i += 128) {
     const int j = i + lane * 4;
     const uint4 kv = *reinterpret_cast<const uint4 *>(skey + j);
@@ -243,8 +247,11 @@ __global__ void __launch_bounds__(NT, 1)
   int base = block_exclusive_scan<NT>(lane ? 0 : cnt, wbuf, &m);
   base = __shfl_sync(0xffffffffu, base, 0);
   const bool use_l = m <= LCAP;
+#ifdef ESS_TOPK_PROF
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_topk_prof[blockIdx.x][7] = (unsigned long long)m;
+#endif
   if (use_l) {
-#pragma unroll 2
+#pragma unroll LIST_UNROLL
     for (int i = lo4; i < hi4; i += 128) {
       const int j = i + lane * 4;
       const uint4 kv = *reinterpret_cast<const uint4 *>(skey + j);

@@ -27,3 +27,4 @@ names = ["stage+hist12", "pick d1", "list compact", "2x10-bit digits", "counts",
 for i, nm in enumerate(names):
     print(f"{nm:18s} mean {d[:, i].mean():6.2f} us  max {d[:, i].max():6.2f}")
 print(f"total mean {(a[:, 6] - a[:, 0]).mean() / 1e3:.2f} us; span {(a[:, 6].max() - a[:, 0].min()) / 1e3:.2f} us")
+print("list sizes m (first 8 rows):", [int(x) for x in np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8)[:8, 7]])
