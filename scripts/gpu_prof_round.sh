@@ -5,7 +5,7 @@ cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
 mkdir -p gpurun_out
 NCU=/usr/local/cuda/bin/ncu
 timeout 900 $NCU --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
-  --log-file gpurun_out/launches_bench.csv python bench.py --steps 3 --warmup 3 --breakdown-steps 1 --no-ceiling \
+  --target-processes application-only --log-file gpurun_out/launches_bench.csv python bench.py --quick --steps 3 --warmup 3 \
   > gpurun_out/launches_bench.log 2>&1
 echo "launch list exit=$?"
 # skip counts: prof_step runs 4 warm-up windows (K1/K2/K3 each) + 1 prefill gather,
