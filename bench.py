@@ -35,7 +35,7 @@ CONFIGS = {
                workload="C2: one DSA layer decode, batch 64/GPU, ctx 32K, 25% GPU slot pool"),
     # configs[3]: ctx 128K, batch 64/GPU, 10% slot pool
     # configs[2]: the full 61-layer attention path, global batch 128 over 8 GPUs = 16/GPU
-    "c3": dict(batch=16, context_len=32768, sparse_ratio=0.25, micro=2, first=0.5, layers=61,
+    "c3": dict(batch=16, context_len=32768, sparse_ratio=0.25, micro=1, first=None, layers=61,
                workload="C3: 61-layer decode step (attention path), batch 16/GPU "
                         "(global 128 over 8 GPUs), ctx 32K, 25% GPU slot pool"),
     # configs[4]: mixed-length batch, context log-uniform over [8K, 128K] (seeded per rank);
