@@ -170,6 +170,15 @@ class DSADecodeLayer:
         """[a, b) request ranges of the DBA split: contiguous; the first holds
         ``first_frac`` of the batch when set (a small first micro-batch starts the
         host-link gather early), the rest split evenly."""
+        sizes = getattr(self, "mb_sizes", None) or (
+            [int(x) for x in os.environ["ESS_MB_SIZES"].split(",")] if os.environ.get("ESS_MB_SIZES") else None)
+        if sizes and n > 1:  # explicit micro-batch sizes (must cover the batch)
+            if sum(sizes) != self.B or min(sizes) < 1:
+                raise ValueError(f"micro-batch sizes {sizes} do not partition {self.B} requests")
+            edges = [0]
+            for z in sizes:
+                edges.append(edges[-1] + z)
+            return [(edges[i], edges[i + 1]) for i in range(len(sizes))]
         n = max(1, min(n, self.B))
         ff = getattr(self, "first_frac", None)
         if n == 1 or not ff:
