@@ -75,6 +75,9 @@ constexpr int KS = 4;                              // KV ring depth
 // Loader completion: 1 = each thread's cp.async completion arrives on the tile barrier
 // (cp.async.mbarrier.arrive.noinc); 0 = wait_group + proxy fence + one arrive per warp,
 // the form compute-sanitizer's racecheck models (same speed at two S buffers).
+#ifndef ESS_MLA_SPIN  // 1: spin with test_wait on the per-tile S / P hand-offs
+#define ESS_MLA_SPIN 0
+#endif
 #ifndef ESS_MLA_ASYNC_ARRIVE
 #define ESS_MLA_ASYNC_ARRIVE 0
 #endif
@@ -310,7 +313,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     float m_run = -INFINITY, l_run = 0.f;  // resume starts a fresh partial, merged at the end
     for (int i = 0; i < ntiles; i++) {
       const int sb = i % NSB;
+#if ESS_MLA_SPIN
+      mbar_spin(&c.s_full[sb], (i / NSB) & 1);
+#else
       mbar_wait(&c.s_full[sb], (i / NSB) & 1);
+#endif
       if (threadIdx.x == 0) MTRACE(2, i);  // softmax sees S(i)
       // observe PV(i - NSB)'s pv_done phase: s_full(i) tracks it (issued before S(i)), so
       // this never stalls; every phase gets a waiter (compute-sanitizer synccheck)
@@ -537,7 +544,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       for (int i = 0; i < ntiles; i++) {
         if (i + LOOKAHEAD < ntiles) issue_s(i + LOOKAHEAD);
         const int kb = i % KS, sb = i % NSB;
+#if ESS_MLA_SPIN
+        mbar_spin(&c.p_full[sb], (i / NSB) & 1);
+#else
         mbar_wait(&c.p_full[sb], (i / NSB) & 1);
+#endif
         MTRACE(4, i);  // MMA sees P(i)
         tc_fence_after();
         const uint32_t vaddr = smem_u32(skv + kb * KV_BYTES) + (uint32_t)(4 * v) * KV_BLK_BYTES;
