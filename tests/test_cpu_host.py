@@ -196,3 +196,34 @@ def test_dp_aggregate_two_gloo_ranks():
         p.join(timeout=60)
     assert sorted(res[0][1] + res[1][1]) == list(range(64))
     assert all(r[2] == 64 and r[3] == 1.5 for r in res)
+
+
+def test_micro_batch_partitions():
+    """DBA request ranges: contiguous, covering the batch, first-share / explicit sizes."""
+    import types
+    from paper_2512_10576_b200.decode import DSADecodeLayer
+    mb = DSADecodeLayer.micro_batches
+    o = types.SimpleNamespace(B=64, first_frac=None, mb_sizes=None)
+    assert mb(o, 1) == [(0, 64)]
+    assert mb(o, 2) == [(0, 32), (32, 64)]
+    o.first_frac = 0.25
+    assert mb(o, 2) == [(0, 16), (16, 64)]
+    assert mb(o, 3) == [(0, 16), (16, 40), (40, 64)]
+    o.mb_sizes = [8, 16, 40]
+    assert mb(o, 3) == [(0, 8), (8, 24), (24, 64)]
+    o.mb_sizes = [8, 8]
+    with pytest.raises(ValueError):
+        mb(o, 2)
+    o = types.SimpleNamespace(B=3, first_frac=0.9, mb_sizes=None)
+    r = mb(o, 3)
+    assert r[0][0] == 0 and r[-1][1] == 3 and all(a < b for a, b in r)
+
+
+def test_bench_request_lengths():
+    """C5's mixed batch: seeded log-uniform lengths within the configured range."""
+    import bench
+    lens = bench.request_lengths(bench.CONFIGS["c5"], 64, seed=0)
+    assert len(lens) == 64 and min(lens) >= 8192 and max(lens) <= 131072
+    assert lens == bench.request_lengths(bench.CONFIGS["c5"], 64, seed=0)
+    assert lens != bench.request_lengths(bench.CONFIGS["c5"], 64, seed=1)
+    assert bench.request_lengths(bench.CONFIGS["c2"], 4) == [32768] * 4
