@@ -29,7 +29,7 @@
 namespace cg = cooperative_groups;
 
 #ifdef ESS_TOPK_PROF  // scratch builds: per-phase globaltimer stamps (thread 0 of each CTA)
-__device__ unsigned long long g_topk_prof[1024][8];
+__device__ unsigned long long g_topk_prof[1024][12];
 #define KPROF(i)                                                             \
   do {                                                                       \
     __syncthreads();                                                         \
@@ -243,8 +243,10 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t b3 = __ballot_sync(0xffffffffu, j + 3 < hi4 && (kv.w >> D1_SHIFT) >= d1);
     cnt += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
   }
+  KPROF(8);
   int m;
   int base = block_exclusive_scan<NT>(lane ? 0 : cnt, wbuf, &m);
+  KPROF(9);
   base = __shfl_sync(0xffffffffu, base, 0);
   const bool use_l = m <= LCAP;
 #ifdef ESS_TOPK_PROF

@@ -19,12 +19,15 @@ indexer_logits(q_idx, layer.w, layer.k_cache, layer.k_scale, layer.lens, out=lay
 for _ in range(2):
     topk(layer.logits, layer.lens, layer.K, out=layer.idx, count=layer.cnt)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * (1024 * 8))()
+buf = (ctypes.c_ulonglong * (1024 * 12))()
 _lib.load().ess_debug_topk_prof(buf)
-a = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8)[:B, :7].astype(np.int64)
+full = np.frombuffer(buf, dtype=np.uint64).reshape(1024, 12)[:B].astype(np.int64)
+a = full[:, :7]
 d = np.diff(a, axis=1) / 1e3
 names = ["stage+hist12", "pick d1", "list compact", "2x10-bit digits", "counts", "emit"]
 for i, nm in enumerate(names):
     print(f"{nm:18s} mean {d[:, i].mean():6.2f} us  max {d[:, i].max():6.2f}")
 print(f"total mean {(a[:, 6] - a[:, 0]).mean() / 1e3:.2f} us; span {(a[:, 6].max() - a[:, 0].min()) / 1e3:.2f} us")
-print("list sizes m (first 8 rows):", [int(x) for x in np.frombuffer(buf, dtype=np.uint64).reshape(1024, 8)[:8, 7]])
+print("list sizes m (first 8 rows):", [int(x) for x in full[:8, 7]])
+print(f"list: pass1 {((full[:, 8] - full[:, 2]) / 1e3).mean():.2f} us, scan {((full[:, 9] - full[:, 8]) / 1e3).mean():.2f} us, "
+      f"pass2 {((full[:, 3] - full[:, 9]) / 1e3).mean():.2f} us")
