@@ -49,6 +49,7 @@ SIGNATURES = {
     "ess_indexer_logits": ([V, V, V, V, V, I32, I64, V, V], ctypes.c_int),
     "ess_indexer_logits_ex": ([V, V, V, V, V, I32, I64, V, I32, V], ctypes.c_int),
     "ess_topk": ([V, I64, V, I32, I32, V, I32, V, V], ctypes.c_int),
+    "ess_topk_split": ([V, I64, V, I32, I32, V, I32, V, V, I32, V, V, V, V, I32, V], ctypes.c_int),
     "ess_sparse_mla": ([V, I32, V, V, I32, V, I32, I32, F32, V, V, V, V, I32, V], ctypes.c_int),
     "ess_sparse_mla_da": ([V, I32, V, V, V, I32, V, I32, V, I32, F32, V, V, V], ctypes.c_int),
     "ess_sparse_mla_da_split": ([V, I32, V, V, V, I32, V, I32, V, I32, F32, V, V, V, V, I32, V],

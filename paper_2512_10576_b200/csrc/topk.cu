@@ -152,10 +152,61 @@ __host__ __device__ __forceinline__ int64_t slice_cap(int64_t ld) {  // keys, 4-
   return (((ld + CLN - 1) / CLN) + 3) & ~3LL;
 }
 
+// Optional fused epilogue (single-CTA rows): the early-gather hit/miss split of the cache
+// manager (ess_pool_split) on the selection this CTA just emitted, saving a launch and
+// the id reload.  slot_of already points at the first pool of the batch.
+struct SplitArgs {
+  const int32_t *slot_of;  // nullptr: no split
+  int64_t max_ids;
+  int32_t cap_max;
+  int32_t *hit_row, *miss_ids, *miss_row, *counts;
+  int32_t out_stride;
+};
+
+__device__ __forceinline__ void split_tail(int b, const int32_t *o, int n, const SplitArgs &sp,
+                                           int *wbuf) {
+  __syncthreads();  // the emitted ids (global, this CTA's writes) are visible block-wide
+  const int t = threadIdx.x;
+  const int32_t *so = sp.slot_of + (int64_t)b * sp.max_ids;
+  int x[2], sl[2], h = 0;
+#pragma unroll
+  for (int e = 0; e < 2; e++) {
+    const int i = t * 2 + e;
+    x[e] = i < n ? o[i] : -1;
+  }
+#pragma unroll
+  for (int e = 0; e < 2; e++) {
+    sl[e] = (x[e] >= 0 && x[e] < sp.max_ids) ? so[x[e]] : -1;
+    h += (t * 2 + e < n) && sl[e] >= 0;
+  }
+  int nhit;
+  int hr = block_exclusive_scan<NT>(h, wbuf, &nhit);
+  const int64_t ob = (int64_t)b * sp.out_stride;
+#pragma unroll
+  for (int e = 0; e < 2; e++) {
+    const int i = t * 2 + e;
+    if (i >= n) continue;
+    if (sl[e] >= 0) {
+      sp.hit_row[ob + hr++] = sl[e];
+    } else {
+      const int j = i - hr;
+      sp.miss_ids[ob + j] = x[e];
+      sp.miss_row[ob + j] = sp.cap_max + j;  // per-pool staging row
+    }
+  }
+  if (t == 0) {
+    sp.counts[b * 4 + 0] = nhit;
+    sp.counts[b * 4 + 1] = n - nhit;
+    sp.counts[b * 4 + 2] = 0;
+    sp.counts[b * 4 + 3] = 0;
+  }
+}
+
 template <int CLN>
 __global__ void __launch_bounds__(NT, 1)
     topk_kernel(const float *__restrict__ logits, int64_t ld, const int32_t *__restrict__ lens,
-                int k, int32_t *__restrict__ out, int out_ld, int32_t *__restrict__ counts) {
+                int k, int32_t *__restrict__ out, int out_ld, int32_t *__restrict__ counts,
+                SplitArgs sp) {
   extern __shared__ uint32_t skey[];  // slice_cap keys, then LCAP u16 list entries
   uint16_t *list = reinterpret_cast<uint16_t *>(skey + slice_cap<CLN>(ld));
   __shared__ int hist[D1_BINS];
@@ -174,6 +225,8 @@ __global__ void __launch_bounds__(NT, 1)
   if (len <= k) {  // whole row, ascending (uniform across the cluster: no cluster sync)
     for (int i = beg + threadIdx.x; i < end; i += NT) o[i] = i;
     if (rank == 0 && threadIdx.x == 0) counts[b] = len < 0 ? 0 : len;
+    if constexpr (CLN == 1)
+      if (sp.slot_of) split_tail(b, o, max(len, 0), sp, wbuf);
     return;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -353,11 +406,14 @@ __global__ void __launch_bounds__(NT, 1)
   }
   KPROF(6);
   if (rank == 0 && threadIdx.x == 0) counts[b] = k;
+  if constexpr (CLN == 1)
+    if (sp.slot_of) split_tail(b, o, k, sp, wbuf);
 }
 
 template <int CLN>
 int launch_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch, int32_t k,
-                int32_t *d_idx, int32_t idx_ld, int32_t *d_count, cudaStream_t stream) {
+                int32_t *d_idx, int32_t idx_ld, int32_t *d_count, cudaStream_t stream,
+                SplitArgs sp = SplitArgs{}) {
   const size_t smem = (size_t)slice_cap<CLN>(ld) * sizeof(uint32_t) + LCAP * sizeof(uint16_t);
   static bool attr = false;  // per instantiation: opt in to the largest slice once
   if (!attr) {
@@ -378,7 +434,7 @@ int launch_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t
   cfg.attrs = at;
   cfg.numAttrs = 1;
   ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, topk_kernel<CLN>, d_logits, ld, d_len, (int)k, d_idx,
-                                  (int)idx_ld, d_count));
+                                  (int)idx_ld, d_count, sp));
   return ESS_OK;
 }
 
@@ -411,6 +467,43 @@ extern "C" int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len,
     case 4: rc = launch_topk<4>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, s); break;
     default: rc = launch_topk<8>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, s); break;
   }
+  if (rc != ESS_OK) return rc;
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+// Top-k fused with the early-gather hit/miss split (ess_pool_split) of pools
+// [pool_begin, pool_begin + batch): one launch when each row fits one CTA, else the
+// top-k and then the split kernel.
+extern "C" int ess_topk_split(const float *d_logits, int64_t ld, const int32_t *d_len,
+                              int32_t batch, int32_t k, int32_t *d_idx, int32_t idx_ld,
+                              int32_t *d_count, ess_pool *pool, int32_t pool_begin,
+                              int32_t *d_hit_row, int32_t *d_miss_ids, int32_t *d_miss_row,
+                              int32_t *d_counts, int32_t out_stride, void *stream) {
+  if (!pool || pool_begin < 0 || (int64_t)pool_begin + batch > pool->P || !d_hit_row ||
+      !d_miss_ids || !d_miss_row || !d_counts || out_stride < 1 || k > 2 * NT ||
+      pool->staging < k)
+    return ESS_ERR_ARG;
+  if (ld > SLICE_MAX) {  // cluster rows: two launches
+    int rc = ess_topk(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, stream);
+    if (rc != ESS_OK) return rc;
+    return ess_pool_split(pool, pool_begin, batch, d_idx, d_count, idx_ld, d_hit_row, d_miss_ids,
+                          d_miss_row, d_counts, out_stride, stream);
+  }
+  if (!d_logits || !d_len || !d_idx || !d_count || batch < 0 || k < 1 || idx_ld < k || ld < 1)
+    return ESS_ERR_ARG;
+  if (batch == 0) return ESS_OK;
+  SplitArgs sp;
+  sp.slot_of = pool->slot_of + (int64_t)pool_begin * pool->max_ids;
+  sp.max_ids = pool->max_ids;
+  sp.cap_max = pool->cap_max;
+  sp.hit_row = d_hit_row;
+  sp.miss_ids = d_miss_ids;
+  sp.miss_row = d_miss_row;
+  sp.counts = d_counts;
+  sp.out_stride = out_stride;
+  int rc = launch_topk<1>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count,
+                          (cudaStream_t)stream, sp);
   if (rc != ESS_OK) return rc;
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;

@@ -32,7 +32,7 @@ import torch
 from . import _lib
 from .attention import DEFAULT_SM_SCALE, SplitWorkspace, sparse_mla, sparse_mla_da
 from .cache import AccessBatch, PoolSet, pool_capacity
-from .indexer import indexer_logits, topk
+from .indexer import indexer_logits, topk, topk_split
 from .transfer import HostLatentStore, gather, write_generated
 
 ROW = 656
@@ -267,11 +267,13 @@ class DSADecodeLayer:
             scored.record(main)
             sel.wait_event(scored)
             with torch.cuda.stream(sel):
-                topk(self.logits[a:b], self.lens[a:b], self.K, out=self.idx[a:b], count=self.cnt[a:b])
                 if self.early_gather:
-                    # K3a: hit/miss split only (misses -> staging rows); the gather starts now
-                    self.pool.split(self.idx[a:b], self.cnt[a:b], out=self._acc_view(a, b), begin=a)
+                    # K2 + K3a (the hit/miss split; misses -> staging rows) in one launch:
+                    # the gather starts right after the top-k
+                    topk_split(self.logits[a:b], self.lens[a:b], self.K, self.idx[a:b], self.cnt[a:b],
+                               self.pool, self._acc_view(a, b), begin=a)
                 else:
+                    topk(self.logits[a:b], self.lens[a:b], self.K, out=self.idx[a:b], count=self.cnt[a:b])
                     self.pool.access(self.idx[a:b], self.cnt[a:b], begin=a, out=self._acc_view(a, b))
                 ready = torch.cuda.Event()
                 ready.record(sel)
@@ -359,7 +361,8 @@ class DSADecodeLayer:
         if overlap == "none":
             return 6  # K1, K2, K3, K4, K5, admission
         micro = self.micro if overlap == "dba" else 1
-        per_mb = 6 if self.early_gather else 4
+        # early gather: K2 + K3a fused when a row fits one CTA (<= 40K tokens), + K3b, settle
+        per_mb = (5 if self.Lmax <= 40 * 1024 else 6) if self.early_gather else 4
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         fused = self.fuse_da and 2 * self.B <= sms - 8
         split = max(1, min(self.max_split, (sms - 8 - self.min_gather_sms) // (2 * self.B))) if fused else 1

@@ -55,3 +55,18 @@ def topk(logits: torch.Tensor, lens: torch.Tensor, k: int = TOPK,
                                     out.data_ptr(), out.stride(0), count.data_ptr(),
                                     _lib.stream_handle()), "ess_topk")
     return out, count
+
+
+def topk_split(logits: torch.Tensor, lens: torch.Tensor, k: int, out: torch.Tensor, count: torch.Tensor,
+               pool, acc, begin: int = 0):
+    """K2 fused with the early-gather hit/miss split of pools [begin, begin + B)
+    (ess_topk_split): selection ids into ``out``/``count``; hit rows, miss ids, staging
+    rows and counts into ``acc`` (an AccessBatch of row slices)."""
+    _lib.require_cuda(logits)
+    B, ld = logits.shape
+    _lib.check(_lib.load().ess_topk_split(
+        logits.data_ptr(), logits.stride(0), lens.data_ptr(), B, k, out.data_ptr(), out.stride(0),
+        count.data_ptr(), pool.handle, begin, acc.hit_row.data_ptr(), acc.miss_ids.data_ptr(),
+        acc.miss_row.data_ptr(), acc.counts.data_ptr(), acc.miss_ids.stride(0),
+        _lib.stream_handle()), "ess_topk_split")
+    return out, count

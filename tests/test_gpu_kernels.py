@@ -302,3 +302,45 @@ def test_early_gather_split_access_settle_matches_plain_access():
     a.close()
     b.close()
     store.close()
+
+
+@pytest.mark.parametrize("lens", [[32768, 4096, 2049, 2048, 1000], [131072, 40000]])
+def test_topk_split_fused_matches_topk_then_split(lens):
+    """K2 with the fused hit/miss split (one launch for rows <= 40K, two otherwise) gives
+    the same selection and the same hit rows / miss ids / staging rows / counts as top-k
+    followed by ess_pool_split."""
+    from paper_2512_10576_b200.cache import AccessBatch, PoolSet
+    from paper_2512_10576_b200.indexer import topk, topk_split
+    B, K = len(lens), 2048
+    ld = ((max(lens) + 127) // 128) * 128
+    g = torch.Generator(device="cuda").manual_seed(5)
+    logits = torch.randn((B, ld), device="cuda", generator=g)
+    ln = torch.tensor(lens, dtype=torch.int32, device="cuda")
+    cap = 4096
+    pool = PoolSet(B, ld, cap, cap, row_bytes=1152, staging_rows=K)
+    rng = np.random.default_rng(1)
+    for b, n in enumerate(lens):  # make a random part of the history resident
+        w = rng.choice(n, size=min(n, 2000), replace=False).astype(np.int32)
+        ids = torch.as_tensor(w, device="cuda").view(1, -1)
+        pool.warmup(ids, torch.tensor([ids.shape[1]], dtype=torch.int32, device="cuda"), begin=b)
+    z = lambda: torch.full((B, K), -7, dtype=torch.int32, device="cuda")  # noqa: E731
+    mk = lambda: AccessBatch(counts=torch.zeros((B, 4), dtype=torch.int32, device="cuda"),  # noqa: E731
+                             sel_row=None, miss_ids=z(), miss_row=z(), hit_row=z())
+    i1, c1 = topk(logits, ln, K)
+    r1 = mk()
+    pool.split(i1, c1, out=r1)
+    i2, c2 = torch.empty_like(i1), torch.empty_like(c1)
+    r2 = mk()
+    topk_split(logits, ln, K, i2, c2, pool, r2)
+    torch.cuda.synchronize()
+    assert torch.equal(c1, c2)
+    for b in range(B):
+        n = int(c1[b])
+        assert torch.equal(i1[b, :n], i2[b, :n])
+        h, m = int(r1.counts[b, 0]), int(r1.counts[b, 1])
+        assert h + m == n and h > 0
+        assert torch.equal(r1.counts[b], r2.counts[b])
+        assert torch.equal(r1.hit_row[b, :h], r2.hit_row[b, :h])
+        assert torch.equal(r1.miss_ids[b, :m], r2.miss_ids[b, :m])
+        assert torch.equal(r1.miss_row[b, :m], r2.miss_row[b, :m])
+    pool.close()
