@@ -387,6 +387,12 @@ __device__ __forceinline__ uint4 ld_host_v4(const void *p) {
                : "l"(p));
   return r;
 }
+// 32-B host-link load (sm_100 256-bit LDG)
+__device__ __forceinline__ void ld_host_v8(const void *p, uint4 &a, uint4 &b) {
+  asm volatile("ld.global.nc.L1::no_allocate." ESS_HOST_PREFETCH ".v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+               : "l"(p));
+}
 __device__ __forceinline__ uint4 ld_volatile_v4(const void *p) {
   // system-scope data (mapped host memory): bypass L1, no caching assumptions
   uint4 r;

@@ -925,6 +925,13 @@ __global__ void pool_counters_kernel(PoolView pv, int begin, int num, int64_t *o
 }
 
 // ---- K4: zero-copy gather of miss rows ------------------------
+#ifndef ESS_GATHER_LD256
+#define ESS_GATHER_LD256 0
+#endif
+__device__ __forceinline__ uint4 shfl_v4(uint4 x, int src) {
+  return make_uint4(__shfl_sync(0xffffffffu, x.x, src), __shfl_sync(0xffffffffu, x.y, src),
+                    __shfl_sync(0xffffffffu, x.z, src), __shfl_sync(0xffffffffu, x.w, src));
+}
 constexpr int NTG = 256;
 constexpr int GROWS = 4;  // rows per warp iteration -> 8 x 16-B loads in flight per lane
 
@@ -991,8 +998,25 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
         pool_of[r] = lo;
       }
     }
-    // all 16-B PCIe loads of the warp's rows in flight first, then dequantise
+    // all PCIe loads of the warp's rows in flight first, then dequantise
     uint4 v[GROWS][2];
+#if ESS_GATHER_LD256
+    // 32-B loads (lanes 0-19 two chunks each, lane 20 the last chunk), then shuffles put
+    // chunk l in lane l (v0) and chunk 32+l in lane l (v1) as the dequant expects
+#pragma unroll
+    for (int r = 0; r < GROWS; r++) {
+      uint4 a0 = make_uint4(0, 0, 0, 0), a1 = make_uint4(0, 0, 0, 0);
+      if (src[r]) {
+        if (lane < ROW_CHUNKS / 2) ld_host_v8(src[r] + lane * 32, a0, a1);
+        else if (lane == ROW_CHUNKS / 2) a0 = ld_host_v4(src[r] + lane * 32);
+      }
+      const int s0 = lane >> 1, s1 = 16 + (lane >> 1);
+      const uint4 t0 = shfl_v4(a0, s0), t1 = shfl_v4(a1, s0);
+      const uint4 u0 = shfl_v4(a0, s1), u1 = shfl_v4(a1, s1);
+      v[r][0] = (lane & 1) ? t1 : t0;
+      v[r][1] = (lane + 32 < ROW_CHUNKS) ? ((lane & 1) ? u1 : u0) : make_uint4(0, 0, 0, 0);
+    }
+#else
 #pragma unroll
     for (int r = 0; r < GROWS; r++) {
       v[r][1] = make_uint4(0, 0, 0, 0);
@@ -1001,6 +1025,7 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
         if (lane + 32 < ROW_CHUNKS) v[r][1] = ld_host_v4(src[r] + (lane + 32) * 16);
       }
     }
+#endif
 #pragma unroll
     for (int r = 0; r < GROWS; r++) {
       if (!src[r]) continue;
