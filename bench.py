@@ -47,6 +47,7 @@ CONFIGS = {
                workload="C4: one DSA layer decode, batch 64/GPU, ctx 128K, 10% GPU slot pool"),
 }
 TOPK = 2048
+LINK_ROW_BYTES = 64 * ((656 + 63) // 64)  # a 64-B aligned 656-B row in 64-B read completions
 METRIC = "decode tokens/s/GPU at 32K/128K ctx, latent cache offloaded; H2D gather GB/s"
 
 
@@ -415,6 +416,7 @@ def run_ours(args, cfg):
     h2d = h_in[0][0].numel() + h_in[0][1].numel() * 2
     d2h = h_out[0].numel() * 2
 
+    gather_gbs = gather_bytes / (ktimes["gather"] * 1e-3) / 1e9 if ktimes["gather"] else None
     line = None
     if rank == 0:
         cpu_v, cpu_sample, cpu_threads = cpu_reference_rate(cfg, budget_s=12.0)
@@ -447,9 +449,15 @@ def run_ours(args, cfg):
             "cuda_graph": True,
             "clocks": clocks.summary(),
             "kernels_ms": ktimes,
+            # useful bytes = 656 per miss; on the link each 64-B-aligned row (704-B host
+            # pitch) moves as 11 64-B read completions = 704 B
             "gather": {"bytes_per_step": gather_bytes,
-                       "gbs": gather_bytes / (ktimes["gather"] * 1e-3) / 1e9 if ktimes["gather"] else None,
+                       "gbs": gather_gbs,
+                       "link_bytes_per_row": LINK_ROW_BYTES,
+                       "link_gbs": gather_gbs * LINK_ROW_BYTES / 656 if gather_gbs else None,
                        "host_link_peak_gbs": link_peak,
+                       "frac_of_link_peak": (gather_gbs * LINK_ROW_BYTES / 656 / link_peak
+                                             if gather_gbs and link_peak else None),
                        "paper_flashtrans_gbs": 37.0},
             "hit_rate": hits / max(1, hits + misses),
             "misses_per_request_step": misses / (B * K),

@@ -932,8 +932,14 @@ __device__ __forceinline__ uint4 shfl_v4(uint4 x, int src) {
   return make_uint4(__shfl_sync(0xffffffffu, x.x, src), __shfl_sync(0xffffffffu, x.y, src),
                     __shfl_sync(0xffffffffu, x.z, src), __shfl_sync(0xffffffffu, x.w, src));
 }
-constexpr int NTG = 256;
-constexpr int GROWS = 4;  // rows per warp iteration -> 8 x 16-B loads in flight per lane
+#ifndef ESS_GATHER_NTG
+#define ESS_GATHER_NTG 256
+#endif
+constexpr int NTG = ESS_GATHER_NTG;
+#ifndef ESS_GATHER_GROWS
+#define ESS_GATHER_GROWS 4
+#endif
+constexpr int GROWS = ESS_GATHER_GROWS;  // rows per warp iteration -> 8 x 16-B loads in flight per lane
 
 __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int num,
                                                      const uint8_t *host, int64_t host_stride,
