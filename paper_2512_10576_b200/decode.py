@@ -84,6 +84,7 @@ class DSADecodeLayer:
         self.max_split = 4   # fused K5: KV splits per request at small batch
         self.min_gather_sms = 20
         self.early_gather_sms = int(os.environ.get("ESS_EARLY_GATHER_SMS", "20"))
+        self.late_k1_ctas = int(os.environ.get("ESS_LATE_K1_CTAS", "0"))
         self.Lmax = ((context_len + max_new_tokens + 127) // 128) * 128
         self.gen = torch.Generator(device=self.device).manual_seed(seed)
         d, g, B = self.device, self.gen, batch
@@ -261,6 +262,8 @@ class DSADecodeLayer:
             g_i = gsms if i == len(ranges) - 1 else max(gsms, self.early_gather_sms)
             g_prev = 0 if i == 0 else (gsms if i - 1 == len(ranges) - 1 else max(gsms, self.early_gather_sms))
             ctas = 0 if i == 0 else sms - g_prev - prev
+            if i > 0 and self.late_k1_ctas:  # cap: less HBM pressure beside the gather
+                ctas = min(ctas, self.late_k1_ctas)
             indexer_logits(q_idx[a:b], self.w[a:b], self.k_cache[a:b], self.k_scale[a:b],
                            self.lens[a:b], out=self.logits[a:b], max_ctas=ctas)
             scored = torch.cuda.Event()
