@@ -55,13 +55,16 @@ namespace {
 constexpr int HEADS = ESS_MLA_HEADS;      // 128 = M
 constexpr int QK_DIM = ESS_MLA_QK_DIM;    // 576
 constexpr int V_HALF = 256;               // output dims per CTA
-constexpr int NB = 32;                    // KV rows per tile
+#ifndef ESS_MLA_NB
+#define ESS_MLA_NB 32
+#endif
+constexpr int NB = ESS_MLA_NB;            // KV rows per tile (32, or 64: half the tiles)
 constexpr int NBLK = QK_DIM / 64;         // 9 dim-blocks of 64 (128 B of f16)
 #ifndef ESS_MLA_NSB
 #define ESS_MLA_NSB 2
 #endif
 #ifndef ESS_MLA_QT_BLKS
-#define ESS_MLA_QT_BLKS 6
+#define ESS_MLA_QT_BLKS (ESS_MLA_NB == 64 ? 4 : 6)
 #endif
 constexpr int QT_BLKS = ESS_MLA_QT_BLKS;  // q blocks held in TMEM (dims 0..64*QT_BLKS-1)
 constexpr int QS_BLKS = NBLK - QT_BLKS;   // q blocks in shared memory (dims 320..575)
@@ -71,7 +74,10 @@ constexpr int QBLK_BYTES = HEADS * 128;            // one [128 heads][64 dims] b
 constexpr int QS_BYTES = QS_BLKS * QBLK_BYTES;     // 65536
 constexpr int KV_BLK_BYTES = NB * 128;             // 4096
 constexpr int KV_BYTES = NBLK * KV_BLK_BYTES;      // 36864
-constexpr int KS = 4;                              // KV ring depth
+constexpr int KS = NB == 64 ? 2 : 4;               // KV ring depth
+// 64-row tiles: the selected slot ids are read from global memory per tile (no room
+// for the 8-KB id copy in shared memory)
+constexpr bool SSEL_SMEM = NB != 64;
 // Loader completion: 1 = each thread's cp.async completion arrives on the tile barrier
 // (cp.async.mbarrier.arrive.noinc); 0 = wait_group + proxy fence + one arrive per warp,
 // the form compute-sanitizer's racecheck models (same speed at two S buffers).
@@ -79,7 +85,7 @@ constexpr int KS = 4;                              // KV ring depth
 #define ESS_MLA_SPIN 0
 #endif
 #ifndef ESS_MLA_ASYNC_ARRIVE
-#define ESS_MLA_ASYNC_ARRIVE 0
+#define ESS_MLA_ASYNC_ARRIVE (ESS_MLA_NB == 64 ? 1 : 0)
 #endif
 #ifndef ESS_MLA_DBG_NOLOAD  // timing-only switches for scratch builds (scripts/variant_lib.sh)
 #define ESS_MLA_DBG_NOLOAD 0
@@ -120,7 +126,8 @@ struct Ctrl {
   uint64_t s_full[NSB], p_full[NSB], pv_done[NSB], o_done, q_full;
   uint32_t tmem;
 };
-constexpr size_t SMEM_BYTES = 1024 + QS_BYTES + KS * KV_BYTES + MAX_N * 4 + sizeof(Ctrl);
+constexpr size_t SMEM_BYTES = 1024 + QS_BYTES + KS * KV_BYTES + (SSEL_SMEM ? MAX_N * 4 : 0) + sizeof(Ctrl);
+static_assert(SMEM_BYTES <= 232448, "K5 shared memory over the sm_100 limit");
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -211,7 +218,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t *sq = smem;                        // q dims 320..575, 4 SW128 blocks
   uint8_t *skv = sq + QS_BYTES;              // KS f16 KV tiles
   int32_t *ssel = reinterpret_cast<int32_t *>(skv + KS * KV_BYTES);
-  Ctrl &c = *reinterpret_cast<Ctrl *>(ssel + MAX_N);
+  Ctrl &c = *reinterpret_cast<Ctrl *>(ssel + (SSEL_SMEM ? MAX_N : 0));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int v = blockIdx.x;  // output half
   const int split = blockIdx.y % nsplit;     // KV split: a contiguous share of the rows
@@ -264,7 +271,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tma_load_2d(blk < QT_BLKS ? skv + blk * QBLK_BYTES : sq + (blk - QT_BLKS) * QBLK_BYTES, &tm_q,
                   &c.q_full, blk * 64, b * HEADS);
   }
-  if (warp >= LOAD0) {
+  if (SSEL_SMEM && warp >= LOAD0) {
     const int32_t *sel = sel_row + (int64_t)b * sel_stride;
     const int32_t *s2 = await ? sel2 + (int64_t)b * sel_stride : nullptr;
     for (int j = threadIdx.x - LOAD0 * 32; j < n; j += NLOAD * 32) {
@@ -328,11 +335,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (lane == 0) mbar_arrive(&c.p_full[sb]);
       continue;
 #endif
-      uint32_t s[32];
-      tmem_ld_32x32b_x32(tmem + lane_base + TM_S + sb * NB, s);
+      uint32_t s[NB];
+      if constexpr (NB == 64) tmem_ld_32x32b_x64(tmem + lane_base + TM_S + sb * NB, *reinterpret_cast<uint32_t(*)[64]>(s));
+      else tmem_ld_32x32b_x32(tmem + lane_base + TM_S + sb * NB, *reinterpret_cast<uint32_t(*)[32]>(s));
       tmem_ld_wait();
       // raw scores; the scale folds into the exp2 argument (one FFMA per score)
-      float x[32];
+      float x[NB];
       const int lim = n - i * NB;  // valid columns of this tile (uniform)
 #pragma unroll
       for (int j = 0; j < NB; j++) x[j] = j < lim ? __uint_as_float(s[j]) : -INFINITY;
@@ -375,11 +383,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       // P (f16 pairs) over the first 16 columns of this S buffer: p = 2^(x*scale - m)
       // (ex2.approx, one MUFU op), packed two per cvt; l sums the unrounded values in
       // four independent chains (the f16 rounding of P is below the tolerance budget)
-      uint32_t p[16];
+      uint32_t p[NB / 2];
       float ls0 = 0.f, ls1 = 0.f, ls2 = 0.f, ls3 = 0.f;
       const float nm = -m_run;
 #pragma unroll
-      for (int e = 0; e < 16; e += 2) {
+      for (int e = 0; e < NB / 2; e += 2) {
         const float e0 = fast_exp2(fmaf(x[2 * e], scale_log2, nm));
         const float e1 = fast_exp2(fmaf(x[2 * e + 1], scale_log2, nm));
         const float e2 = fast_exp2(fmaf(x[2 * e + 2], scale_log2, nm));
@@ -392,7 +400,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         ls3 += e3;
       }
       l_run += (ls0 + ls1) + (ls2 + ls3);
-      tmem_st_32x32b_x16(tmem + lane_base + TM_S + sb * NB, p);
+      if constexpr (NB == 64) tmem_st_32x32b_x32(tmem + lane_base + TM_S + sb * NB, *reinterpret_cast<const uint32_t(*)[32]>(p));
+      else tmem_st_32x32b_x16(tmem + lane_base + TM_S + sb * NB, *reinterpret_cast<const uint32_t(*)[16]>(p));
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
@@ -591,7 +600,15 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int r = w * ROWS_PER_LOADER + rr;
         const int j = i * NB + r;
         const bool ok = j < n;
-        const uint8_t *src = pool_rows + (int64_t)ssel[ok ? j : 0] * ESS_SLOT_ROW_BYTES;
+        int sid;
+        if constexpr (SSEL_SMEM) {
+          sid = ssel[ok ? j : 0];
+        } else {  // the id straight from global (L2-resident; warp-uniform per row)
+          const int g = r0 + (ok ? j : 0);
+          sid = g < n1t ? __ldg(sel_row + (int64_t)b * sel_stride + g)
+                        : __ldg(sel2 + (int64_t)b * sel_stride + (g - n1t));
+        }
+        const uint8_t *src = pool_rows + (int64_t)sid * ESS_SLOT_ROW_BYTES;
 #pragma unroll
         for (int k = 0; k < 3; k++) {
           const int ch = lane + 32 * k;
