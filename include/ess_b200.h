@@ -208,8 +208,8 @@ int ess_indexer_logits_ex(const void *d_q, const float *d_w, const void *d_k,
  * ascending to d_idx [B][idx_ld]; d_count[b] = min(k, len[b]) (scenario.py:110-112) */
 int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
              int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count, void *stream);
-/* top-k fused with ess_pool_split on the emitted selection (one launch for rows of up
- * to 40K tokens, else ess_topk + ess_pool_split): pools [pool_begin, pool_begin+batch) */
+/* top-k fused with ess_pool_split on the emitted selection, one launch (for cluster
+ * rows > 40K tokens, rank 0 of each cluster splits): pools [pool_begin, pool_begin+batch) */
 int ess_topk_split(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
                    int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count, ess_pool *pool,
                    int32_t pool_begin, int32_t *d_hit_row, int32_t *d_miss_ids,

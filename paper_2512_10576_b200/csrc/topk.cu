@@ -152,7 +152,7 @@ __host__ __device__ __forceinline__ int64_t slice_cap(int64_t ld) {  // keys, 4-
   return (((ld + CLN - 1) / CLN) + 3) & ~3LL;
 }
 
-// Optional fused epilogue (single-CTA rows): the early-gather hit/miss split of the cache
+// Optional fused epilogue: the early-gather hit/miss split of the cache
 // manager (ess_pool_split) on the selection this CTA just emitted, saving a launch and
 // the id reload.  slot_of already points at the first pool of the batch.
 struct SplitArgs {
@@ -225,8 +225,14 @@ __global__ void __launch_bounds__(NT, 1)
   if (len <= k) {  // whole row, ascending (uniform across the cluster: no cluster sync)
     for (int i = beg + threadIdx.x; i < end; i += NT) o[i] = i;
     if (rank == 0 && threadIdx.x == 0) counts[b] = len < 0 ? 0 : len;
-    if constexpr (CLN == 1)
-      if (sp.slot_of) split_tail(b, o, max(len, 0), sp, wbuf);
+    if (sp.slot_of) {
+      if constexpr (CLN > 1) {
+        cg::this_cluster().sync();  // every rank's ids written (release / acquire)
+        if (rank == 0) split_tail(b, o, max(len, 0), sp, wbuf);
+      } else {
+        split_tail(b, o, max(len, 0), sp, wbuf);
+      }
+    }
     return;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -406,8 +412,14 @@ __global__ void __launch_bounds__(NT, 1)
   }
   KPROF(6);
   if (rank == 0 && threadIdx.x == 0) counts[b] = k;
-  if constexpr (CLN == 1)
-    if (sp.slot_of) split_tail(b, o, k, sp, wbuf);
+  if (sp.slot_of) {
+    if constexpr (CLN > 1) {
+      cg::this_cluster().sync();  // every rank's part of the selection written
+      if (rank == 0) split_tail(b, o, k, sp, wbuf);
+    } else {
+      split_tail(b, o, k, sp, wbuf);
+    }
+  }
 }
 
 template <int CLN>
@@ -473,8 +485,8 @@ extern "C" int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len,
 }
 
 // Top-k fused with the early-gather hit/miss split (ess_pool_split) of pools
-// [pool_begin, pool_begin + batch): one launch when each row fits one CTA, else the
-// top-k and then the split kernel.
+// [pool_begin, pool_begin + batch) in one launch (cluster rows: rank 0 splits after a
+// cluster barrier).
 extern "C" int ess_topk_split(const float *d_logits, int64_t ld, const int32_t *d_len,
                               int32_t batch, int32_t k, int32_t *d_idx, int32_t idx_ld,
                               int32_t *d_count, ess_pool *pool, int32_t pool_begin,
@@ -484,15 +496,12 @@ extern "C" int ess_topk_split(const float *d_logits, int64_t ld, const int32_t *
       !d_miss_ids || !d_miss_row || !d_counts || out_stride < 1 || k > 2 * NT ||
       pool->staging < k)
     return ESS_ERR_ARG;
-  if (ld > SLICE_MAX) {  // cluster rows: two launches
-    int rc = ess_topk(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, stream);
-    if (rc != ESS_OK) return rc;
-    return ess_pool_split(pool, pool_begin, batch, d_idx, d_count, idx_ld, d_hit_row, d_miss_ids,
-                          d_miss_row, d_counts, out_stride, stream);
-  }
   if (!d_logits || !d_len || !d_idx || !d_count || batch < 0 || k < 1 || idx_ld < k || ld < 1)
     return ESS_ERR_ARG;
   if (batch == 0) return ESS_OK;
+  int cln = 1;
+  while (cln < 8 && (ld + cln - 1) / cln > SLICE_MAX) cln *= 2;
+  if ((ld + cln - 1) / cln > SLICE_MAX) return ESS_ERR_ARG;
   SplitArgs sp;
   sp.slot_of = pool->slot_of + (int64_t)pool_begin * pool->max_ids;
   sp.max_ids = pool->max_ids;
@@ -502,8 +511,15 @@ extern "C" int ess_topk_split(const float *d_logits, int64_t ld, const int32_t *
   sp.miss_row = d_miss_row;
   sp.counts = d_counts;
   sp.out_stride = out_stride;
-  int rc = launch_topk<1>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count,
-                          (cudaStream_t)stream, sp);
+  // cluster rows: rank 0 of each cluster runs the split after a cluster barrier
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  switch (cln) {
+    case 1: rc = launch_topk<1>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, st, sp); break;
+    case 2: rc = launch_topk<2>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, st, sp); break;
+    case 4: rc = launch_topk<4>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, st, sp); break;
+    default: rc = launch_topk<8>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, st, sp); break;
+  }
   if (rc != ESS_OK) return rc;
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;

@@ -364,8 +364,8 @@ class DSADecodeLayer:
         if overlap == "none":
             return 6  # K1, K2, K3, K4, K5, admission
         micro = self.micro if overlap == "dba" else 1
-        # early gather: K2 + K3a fused when a row fits one CTA (<= 40K tokens), + K3b, settle
-        per_mb = (5 if self.Lmax <= 40 * 1024 else 6) if self.early_gather else 4
+        # early gather: K2 + K3a fused, + K3b, settle
+        per_mb = 5 if self.early_gather else 4
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         fused = self.fuse_da and 2 * self.B <= sms - 8
         split = max(1, min(self.max_split, (sms - 8 - self.min_gather_sms) // (2 * self.B))) if fused else 1

@@ -12,7 +12,7 @@ from paper_2512_10576_b200 import transfer  # noqa: E402
 from paper_2512_10576_b200.decode import DSADecodeLayer  # noqa: E402
 
 B = int(os.environ.get("B", 2))
-for ctx in (4096, [9000 + 1500 * b for b in range(B)]):
+for ctx in (4096, [9000 + 1500 * b for b in range(B)], [45000 + 5000 * b for b in range(B)]):
     layer = DSADecodeLayer(B, ctx, 0.25, 2048, max_new_tokens=8, seed=1, drift=0.9)
     layer.prefill_warmup(windows=2)
     for overlap in ("none", "da", "dba"):
