@@ -295,7 +295,9 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll LIST_UNROLL
   for (int i = lo4; i < hi4; i += 128) {
     const int j = i + lane * 4;
-    const uint4 kv = *reinterpret_cast<const uint4 *>(skey + j);
+    // lanes past the run read nothing (slice_cap is 4-aligned, so j < hi4 keeps the
+    // 16-B read inside the staged slice, never into the list behind it)
+    const uint4 kv = j < hi4 ? *reinterpret_cast<const uint4 *>(skey + j) : make_uint4(0, 0, 0, 0);
     const uint32_t b0 = __ballot_sync(0xffffffffu, j + 0 < hi4 && (kv.x >> D1_SHIFT) >= d1);
     const uint32_t b1 = __ballot_sync(0xffffffffu, j + 1 < hi4 && (kv.y >> D1_SHIFT) >= d1);
     const uint32_t b2 = __ballot_sync(0xffffffffu, j + 2 < hi4 && (kv.z >> D1_SHIFT) >= d1);
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll LIST_UNROLL
     for (int i = lo4; i < hi4; i += 128) {
       const int j = i + lane * 4;
-      const uint4 kv = *reinterpret_cast<const uint4 *>(skey + j);
+      const uint4 kv = j < hi4 ? *reinterpret_cast<const uint4 *>(skey + j) : make_uint4(0, 0, 0, 0);
       const bool c0 = j + 0 < hi4 && (kv.x >> D1_SHIFT) >= d1;
       const bool c1 = j + 1 < hi4 && (kv.y >> D1_SHIFT) >= d1;
       const bool c2 = j + 2 < hi4 && (kv.z >> D1_SHIFT) >= d1;
