@@ -13,7 +13,8 @@ import torch  # noqa: E402
 from paper_2512_10576_b200 import _lib, decode  # noqa: E402
 from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows  # noqa: E402
 
-CFG = {"c2": (64, 32768, 0.25), "c4": (64, 131072, 0.1)}[os.environ.get("CONFIG", "c2")]
+CFG = {"c2": (64, 32768, 0.25), "c4": (64, 131072, 0.1),
+       "c3": (16, 32768, 0.25)}[os.environ.get("CONFIG", "c2")]  # c3: one layer of C3
 B, ctx, rho = CFG
 layer = DSADecodeLayer(B, ctx, rho, 2048, max_new_tokens=96, seed=1234, drift=0.97)
 layer.prefill_warmup(windows=32)
@@ -39,6 +40,7 @@ def wrap(mod, fn_name, label):
 
 wrap(decode, "indexer_logits", "K1 indexer")
 wrap(decode, "topk", "K2 topk")
+wrap(decode, "topk_split", "K2+K3a topk+split")
 wrap(decode, "gather", "K4 gather (side)")
 wrap(decode, "sparse_mla_da", "K5 fused DA")
 wrap(decode, "sparse_mla", "K5 pass")
