@@ -246,9 +246,10 @@ int ess_sparse_mla_da(ess_pool *pool, int32_t pool_begin, const void *d_q,
                       const int32_t *d_hit_row, const int32_t *d_miss_row, int32_t row_stride,
                       const int32_t *d_counts, int32_t count_stride, int32_t *d_landed,
                       int32_t batch, float sm_scale, void *d_out, float *d_lse, void *stream);
-/* same with the rows of each request split into nsplit contiguous shares (2 * nsplit
- * CTAs per request; small batches), partial states in d_ws_o [batch*nsplit][128][512]
- * f32 / d_ws_ml [batch*nsplit][128][2] f32, merged by a combine kernel on the stream.
+/* same with the rows of each request split into nsplit shares, each an equal slice of the
+ * resident rows and of the fetched rows (2 * nsplit CTAs per request; small batches),
+ * partial states in d_ws_o [batch*nsplit][128][512] f32 / d_ws_ml [batch*nsplit][128][2]
+ * f32, merged by a combine kernel on the stream.
  * nsplit = 1 is ess_sparse_mla_da.  2 * batch * nsplit <= SMs - 8.                */
 int ess_sparse_mla_da_split(ess_pool *pool, int32_t pool_begin, const void *d_q,
                             const int32_t *d_hit_row, const int32_t *d_miss_row,

@@ -221,22 +221,24 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   Ctrl &c = *reinterpret_cast<Ctrl *>(ssel + (SSEL_SMEM ? MAX_N : 0));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int v = blockIdx.x;  // output half
-  const int split = blockIdx.y % nsplit;     // KV split: a contiguous share of the rows
+  const int split = blockIdx.y % nsplit;     // KV split: one share of the rows
   const int b = blockIdx.y / nsplit;
   const bool partial = flags & ESS_MLA_PARTIAL, resume = flags & ESS_MLA_RESUME;
   // split CTAs leave unnormalised partial states in the workspace; a combine kernel
   // merges them (small batches: 2 * nsplit CTAs per request fill the GPU)
   const bool to_ws = partial || nsplit > 1;
-  // fused DA: rows sel_row[0:n1t) are resident, sel2[0:n2t) land during the kernel; the
-  // CTA attends rows [r0, r0 + n) of their concatenation
+  // fused DA: rows sel_row[0:n1t) are resident, sel2[0:n2t) land during the kernel
   const bool await = flags & MLA_AWAIT;
   const int n1t = min(counts[(int64_t)b * count_stride], MAX_N);
   const int n2t = await ? min(counts[(int64_t)b * count_stride + 1], MAX_N - n1t) : 0;
-  const int chunk = ((n1t + n2t + nsplit - 1) / nsplit + NB - 1) / NB * NB;
-  const int r0 = min(n1t + n2t, split * chunk);
-  const int n = min(n1t + n2t, r0 + chunk) - r0;
-  const int n1 = max(0, min(n, n1t - r0));   // resident rows of this share
-  const bool fetched = r0 + n > n1t;         // the share holds fetched rows
+  // Each share takes an equal slice of the resident rows AND of the fetched rows (its list is
+  // [hits h0..h1) ++ [misses m0..m1)), so every share overlaps its own hits with the gather
+  // and the post-arrival tail is ~n2t/nsplit rows instead of all of them in the last share.
+  const int h0 = n1t * split / nsplit, h1 = n1t * (split + 1) / nsplit;
+  const int m0 = n2t * split / nsplit, m1 = n2t * (split + 1) / nsplit;
+  const int n1 = h1 - h0;                    // resident rows of this share
+  const int n = n1 + (m1 - m0);
+  const bool fetched = m1 > m0;              // the share holds fetched rows
   const int ntiles = (n + NB - 1) / NB;
 
   if (threadIdx.x == 0) {
@@ -275,8 +277,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     const int32_t *sel = sel_row + (int64_t)b * sel_stride;
     const int32_t *s2 = await ? sel2 + (int64_t)b * sel_stride : nullptr;
     for (int j = threadIdx.x - LOAD0 * 32; j < n; j += NLOAD * 32) {
-      const int g = r0 + j;
-      ssel[j] = g < n1t ? __ldg(sel + g) : __ldg(s2 + (g - n1t));
+      ssel[j] = j < n1 ? __ldg(sel + h0 + j) : __ldg(s2 + m0 + (j - n1));
     }
   }
   mbar_wait(&c.q_full, 0);
@@ -604,9 +605,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if constexpr (SSEL_SMEM) {
           sid = ssel[ok ? j : 0];
         } else {  // the id straight from global (L2-resident; warp-uniform per row)
-          const int g = r0 + (ok ? j : 0);
-          sid = g < n1t ? __ldg(sel_row + (int64_t)b * sel_stride + g)
-                        : __ldg(sel2 + (int64_t)b * sel_stride + (g - n1t));
+          const int jj = ok ? j : 0;
+          sid = jj < n1 ? __ldg(sel_row + (int64_t)b * sel_stride + h0 + jj)
+                        : __ldg(sel2 + (int64_t)b * sel_stride + m0 + (jj - n1));
         }
         const uint8_t *src = pool_rows + (int64_t)sid * ESS_SLOT_ROW_BYTES;
 #pragma unroll
