@@ -61,6 +61,24 @@ constexpr size_t SMEM_BYTES =
     1024 /*align slack*/ + (size_t)STAGES * UT_BYTES + 2 * QT_BYTES + sizeof(Ctrl);
 static_assert(SMEM_BYTES <= 232448, "K1 shared memory over the sm_100 limit");
 
+#ifdef ESS_K1_PROF  // scratch builds: per-CTA globaltimer stamps (entry, setup, first unit, end)
+__device__ unsigned long long g_k1_prof[160][6];
+__device__ __forceinline__ void k1_stamp(int i) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+#ifdef ESS_K1_PROF_FULLGRID  // the latest full-grid launch (the step's first micro-batch)
+  if (blockIdx.x < 160 && gridDim.x >= 148) g_k1_prof[blockIdx.x][i] = t;
+#else  // first launch after a reset wins (the step launches K1 once per micro-batch)
+  if (blockIdx.x < 160 && g_k1_prof[blockIdx.x][i] == 0) g_k1_prof[blockIdx.x][i] = t;
+#endif
+}
+#define K1PROF(i) k1_stamp(i)
+#else
+#define K1PROF(i) \
+  do {            \
+  } while (0)
+#endif
+
 // Walk the flattened (request, unit) sequence.
 struct TileCursor {
   int b, t;
@@ -91,16 +109,28 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   uint8_t *qbuf = smem + (size_t)STAGES * UT_BYTES;
   Ctrl &c = *reinterpret_cast<Ctrl *>(qbuf + 2 * QT_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) K1PROF(0);
 
-  // unit prefix over requests (every CTA computes it; B is small)
-  if (threadIdx.x == 0) {
+  // unit prefix over requests (every CTA computes it): warp 0, 32 requests per round
+  // (a serial loop of dependent-latency loads cost ~27 ns per request)
+  if (warp == 0) {
     int acc = 0;
-    for (int b = 0; b < B; b++) {
-      c.pref[b] = acc;
-      int L = lens[b];
-      acc += L > 0 ? (L + UNIT_M - 1) / UNIT_M : 0;
+    for (int b0 = 0; b0 < B; b0 += 32) {
+      const int b = b0 + lane;
+      const int L = b < B ? __ldg(lens + b) : 0;
+      const int u = L > 0 ? (L + UNIT_M - 1) / UNIT_M : 0;
+      int x = u;  // inclusive warp scan
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+      }
+      if (b < B) c.pref[b] = acc + x - u;
+      acc += __shfl_sync(0xffffffffu, x, 31);
     }
-    c.pref[B] = acc;
+    if (lane == 0) c.pref[B] = acc;
+  }
+  if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; s++) {
       mbar_init(&c.full[s], 1);
       mbar_init(&c.empty[s], 1);
@@ -119,6 +149,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) K1PROF(1);
   const uint32_t tmem = c.tmem;
   const int total = c.pref[B];
   const int t0 = (int)((int64_t)total * blockIdx.x / gridDim.x);
@@ -240,6 +271,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const int a = it % NACC;
         mbar_wait(&c.tfull[a], (it / NACC) & 1);
         tc_fence_after();
+        if (it == 0 && threadIdx.x == 64) K1PROF(2);
 #pragma unroll
         for (int j = 0; j < SUB; j++) {
           uint32_t r[64];
@@ -265,10 +297,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       }
     }
   }
+  if (threadIdx.x == 64) K1PROF(3);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
+  if (threadIdx.x == 32) K1PROF(4);
 }
 
 // 2D uint8 tensor [rows][128 B], box [box_rows][128 B], 128-B swizzle.  The last
@@ -296,6 +330,16 @@ bool make_map(CUtensorMap *m, const void *base, uint64_t rows, uint32_t box_rows
 }
 
 }  // namespace
+
+#ifdef ESS_K1_PROF
+extern "C" int ess_debug_k1_prof(unsigned long long *host) {
+  return cudaMemcpyFromSymbol(host, g_k1_prof, sizeof(g_k1_prof)) == cudaSuccess ? 0 : -7;
+}
+extern "C" int ess_debug_k1_prof_reset() {
+  static unsigned long long zero[160][6];
+  return cudaMemcpyToSymbol(g_k1_prof, zero, sizeof(zero)) == cudaSuccess ? 0 : -7;
+}
+#endif
 
 extern "C" int ess_indexer_logits(const void *d_q, const float *d_w, const void *d_k,
                                   const float *d_kscale, const int32_t *d_len, int32_t batch,
