@@ -61,14 +61,15 @@ def test_decode_layer_matches_oracle_chain(ctx, rho, fuse, overlap):
     layer.close()
 
 
-@pytest.mark.parametrize("overlap,micro", [("dba", 2), ("dba", 3), ("da", 1)])
-def test_graph_step_with_overlap_matches_oracle_chain(overlap, micro):
+@pytest.mark.parametrize("overlap,micro,B", [("dba", 2, 4), ("dba", 3, 4), ("da", 1, 4), ("dba", 2, 40)])
+def test_graph_step_with_overlap_matches_oracle_chain(overlap, micro, B):
     """The product step — two micro-batches, gathers on a side stream, whole step
     captured as a CUDA graph, history/capacity computed on device — stays bit-exact
-    on selections and cache accounting and within tolerance on attention."""
+    on selections and cache accounting and within tolerance on attention (B = 4: K5
+    KV-split shares; B = 40: one share per request)."""
     from paper_2512_10576_b200.cache import pool_capacity
     from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows
-    B, K, ctx, rho = 4, 2048, 8192, 0.25
+    K, ctx, rho = 2048, 8192, 0.25
     layer = DSADecodeLayer(B, ctx, rho, K, max_new_tokens=12, seed=3, drift=0.97)
     windows = layer.prefill_warmup(windows=6, record=True)
     orc = [olru.OraclePool(pool_capacity(rho, ctx)) for _ in range(B)]
