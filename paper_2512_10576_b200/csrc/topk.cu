@@ -12,8 +12,9 @@
 //
 // Exact k-th largest key T in three radix digits, 12 + 10 + 10 bits:
 //   1. the 12-bit histogram (sign, exponent, 3 mantissa bits) is built while the slice
-//      is staged; every CTA sums the CLN histograms through distributed shared memory
-//      (DSMEM) and all agree on the digit d1 without a global round trip;
+//      is staged; every CTA pushes its nonzero bins into every rank's summed histogram
+//      (distributed shared memory reductions) and all agree on the digit d1 without a
+//      global round trip;
 //   2. the keys whose first digit is >= d1 (the < k keys above the bin plus the bin
 //      itself, about k per row) are compacted in row order into a u16 list;
 //   3. the two 10-bit passes and the ordered emit touch only that list.
@@ -74,30 +75,36 @@ __device__ __forceinline__ void cluster_sync() {
   else __syncthreads();
 }
 
-// bin i summed over the cluster's histograms
-template <int CLN>
-__device__ __forceinline__ int cluster_bin(int *hist, int i) {
-  if constexpr (CLN == 1) {
-    return hist[i];
-  } else {
-    cg::cluster_group cl = cg::this_cluster();
-    int v = 0;
-#pragma unroll
-    for (int r = 0; r < CLN; r++) v += cl.map_shared_rank(hist, r)[i];
-    return v;
-  }
+// Cluster rows sum their histograms by pushing: every CTA adds its counts into every
+// rank's `csum` with remote shared-memory reductions (only nonzero bins for the 12-bit
+// digit, one add per candidate key for the 10-bit digits), then each CTA picks from its
+// own csum.  Pulling every bin of every peer (4 B DSMEM loads) cost 4 / 10 us at 2 / 4
+// CTAs per row; pushes are fire-and-forget and skip the empty bins.
+__device__ __forceinline__ uint32_t cluster_addr(const void *p, int rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(p)), "r"(rank));
+  return a;
+}
+__device__ __forceinline__ void cluster_red_add(uint32_t addr, int v) {
+  asm volatile("red.relaxed.cluster.shared::cluster.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-// Digit holding the rem-th largest key (bins scanned from the top, summed over the
-// cluster); thread t owns NB/NT consecutive bins.  Leaves (digit, rank inside the bin)
+// Digit holding the rem-th largest key of a histogram (bins scanned from the top);
+// thread t owns NB/NT consecutive bins.  Leaves (digit, rank inside the bin)
 // in scal and syncs the CTA.
-template <int NB, int CLN>
+template <int NB>
 __device__ __forceinline__ void pick_digit(int *hist, int rem, int *wbuf, int *scal) {
   constexpr int BPT = NB / NT;
   int loc[BPT], sum = 0;
 #pragma unroll
   for (int j = 0; j < BPT; j++) {
-    loc[j] = cluster_bin<CLN>(hist, NB - 1 - (threadIdx.x * BPT + j));
+    loc[j] = hist[NB - 1 - (threadIdx.x * BPT + j)];
     sum += loc[j];
   }
   int tot;
@@ -210,6 +217,7 @@ __global__ void __launch_bounds__(NT, 1)
   extern __shared__ uint32_t skey[];  // slice_cap keys, then LCAP u16 list entries
   uint16_t *list = reinterpret_cast<uint16_t *>(skey + slice_cap<CLN>(ld));
   __shared__ int hist[D1_BINS];
+  __shared__ int csum[CLN > 1 ? D1_BINS : 1];  // cluster rows: histogram summed over ranks
   __shared__ int wbuf[NW];
   __shared__ int scal[2];
   __shared__ int part[2];  // this CTA's (greater, equal) totals, read by later ranks
@@ -239,6 +247,10 @@ __global__ void __launch_bounds__(NT, 1)
   const uint32_t lt = (1u << lane) - 1u;
   KPROF(0);
   for (int i = threadIdx.x; i < D1_BINS; i += NT) hist[i] = 0;
+  if constexpr (CLN > 1) {
+    for (int i = threadIdx.x; i < D1_BINS; i += NT) csum[i] = 0;
+    cluster_arrive();  // csum zeroed; peers push into it after the matching wait
+  }
   __syncthreads();
 
   // ---- stage the slice as keys + first-digit histogram (8 loads in flight) ----------
@@ -275,11 +287,27 @@ __global__ void __launch_bounds__(NT, 1)
     }
   }
   KPROF(1);
-  cluster_sync<CLN>();  // every slice histogram complete and visible cluster-wide
-  pick_digit<D1_BINS, CLN>(hist, k, wbuf, scal);
+  if constexpr (CLN > 1) {
+    __syncthreads();  // this slice's histogram complete
+    cluster_wait();   // every rank's csum zeroed
+    uint32_t rb[CLN];
+#pragma unroll
+    for (int r = 0; r < CLN; r++) rb[r] = cluster_addr(csum, r);
+    for (int i = threadIdx.x; i < D1_BINS; i += NT) {
+      const int v = hist[i];
+      if (v) {
+#pragma unroll
+        for (int r = 0; r < CLN; r++) cluster_red_add(rb[r] + 4 * i, v);
+      }
+    }
+    cluster_sync<CLN>();  // every push landed
+    pick_digit<D1_BINS>(csum, k, wbuf, scal);
+  } else {
+    __syncthreads();
+    pick_digit<D1_BINS>(hist, k, wbuf, scal);
+  }
   const uint32_t d1 = (uint32_t)scal[0];
   int rem = scal[1];
-  cluster_sync<CLN>();  // peers finished reading our histogram before it is reused
 
   KPROF(2);
   // ---- list = slice keys with first digit >= d1, in row order -----------------------
@@ -338,19 +366,36 @@ __global__ void __launch_bounds__(NT, 1)
   // ---- two 10-bit digits inside bin d1 ------------------------------------------------
   uint32_t prefix = d1 << D1_SHIFT, mask = ~0u << D1_SHIFT;
   for (int shift = DR_BITS; shift >= 0; shift -= DR_BITS) {
-    hist[threadIdx.x] = 0;
-    __syncthreads();
     const int len2 = use_l ? m : n;
-    for (int i = threadIdx.x; i < len2; i += NT) {
-      const uint32_t key = skey[use_l ? list[i] : i];
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & (DR_BINS - 1)], 1);
+    if constexpr (CLN > 1) {
+      csum[threadIdx.x] = 0;  // after this CTA's previous pick (it ends in a CTA barrier)
+      cluster_sync<CLN>();    // every rank zeroed and done picking from its csum
+      uint32_t rb[CLN];
+#pragma unroll
+      for (int r = 0; r < CLN; r++) rb[r] = cluster_addr(csum, r);
+      for (int i = threadIdx.x; i < len2; i += NT) {
+        const uint32_t key = skey[use_l ? list[i] : i];
+        if ((key & mask) == prefix) {
+          const uint32_t off = 4u * ((key >> shift) & (DR_BINS - 1));
+#pragma unroll
+          for (int r = 0; r < CLN; r++) cluster_red_add(rb[r] + off, 1);
+        }
+      }
+      cluster_sync<CLN>();  // every push landed
+      pick_digit<DR_BINS>(csum, rem, wbuf, scal);
+    } else {
+      hist[threadIdx.x] = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < len2; i += NT) {
+        const uint32_t key = skey[use_l ? list[i] : i];
+        if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & (DR_BINS - 1)], 1);
+      }
+      __syncthreads();
+      pick_digit<DR_BINS>(hist, rem, wbuf, scal);
     }
-    cluster_sync<CLN>();
-    pick_digit<DR_BINS, CLN>(hist, rem, wbuf, scal);
     prefix |= (uint32_t)scal[0] << shift;
     mask |= (uint32_t)(DR_BINS - 1) << shift;
     rem = scal[1];
-    cluster_sync<CLN>();
   }
   const uint32_t T = prefix;
   const int need_eq = rem;  // keys == T to take, in index order over the whole row
