@@ -60,6 +60,7 @@ constexpr int NW = NT / 32;
 constexpr int VEC = 4;
 constexpr int SLICE_MAX = 40 * 1024;      // keys per CTA (160 KB of shared memory)
 constexpr int LCAP = 12 * 1024;           // list entries per CTA (u16, 24 KB)
+constexpr int RCAP = LCAP / (NT / 32);    // per-warp list segment (one-pass list)
 constexpr int D1_BITS = 12, D1_BINS = 1 << D1_BITS, D1_SHIFT = 32 - D1_BITS;
 constexpr int DR_BITS = 10, DR_BINS = 1 << DR_BITS;
 static_assert(DR_BINS == NT, "one 10-bit bin per thread");
@@ -214,7 +215,7 @@ __global__ void __launch_bounds__(NT, 1)
     topk_kernel(const float *__restrict__ logits, int64_t ld, const int32_t *__restrict__ lens,
                 int k, int32_t *__restrict__ out, int out_ld, int32_t *__restrict__ counts,
                 SplitArgs sp) {
-  extern __shared__ uint32_t skey[];  // slice_cap keys, then LCAP u16 list entries
+  extern __shared__ uint32_t skey[];  // slice_cap keys, then LCAP u16 list entries + NW trash
   uint16_t *list = reinterpret_cast<uint16_t *>(skey + slice_cap<CLN>(ld));
   __shared__ int hist[D1_BINS];
   __shared__ int csum[CLN > 1 ? D1_BINS : 1];  // cluster rows: histogram summed over ranks
@@ -317,8 +318,12 @@ __global__ void __launch_bounds__(NT, 1)
   // multiple of 4 inside the slice allocation; keys past n are masked by hi4 = n)
   const int cw4 = (((n + NW - 1) / NW) + 127) & ~127;
   const int lo4 = min(n, warp * cw4), hi4 = min(n, lo4 + cw4);
-  // 128-key chunks: each lane reads 4 consecutive keys with one 16-B shared load and
-  // the 4 ballots (one per vector slot) give every key's rank in row order
+  // One pass: each warp appends its run's candidates to its own segment of the list
+  // (RCAP entries), so no block-wide scan or second pass is needed; segments in warp
+  // order are in row order.  128-key chunks: each lane reads 4 consecutive keys with
+  // one 16-B shared load and the 4 ballots give every key's rank in row order.
+  uint16_t *myseg = list + warp * RCAP;
+  const int trash = LCAP + warp - warp * RCAP;  // list[LCAP + warp], relative to myseg
   int cnt = 0;
 #pragma unroll LIST_UNROLL
   for (int i = lo4; i < hi4; i += 128) {
@@ -326,55 +331,73 @@ __global__ void __launch_bounds__(NT, 1)
     // lanes past the run read nothing (slice_cap is 4-aligned, so j < hi4 keeps the
     // 16-B read inside the staged slice, never into the list behind it)
     const uint4 kv = j < hi4 ? *reinterpret_cast<const uint4 *>(skey + j) : make_uint4(0, 0, 0, 0);
-    const uint32_t b0 = __ballot_sync(0xffffffffu, j + 0 < hi4 && (kv.x >> D1_SHIFT) >= d1);
-    const uint32_t b1 = __ballot_sync(0xffffffffu, j + 1 < hi4 && (kv.y >> D1_SHIFT) >= d1);
-    const uint32_t b2 = __ballot_sync(0xffffffffu, j + 2 < hi4 && (kv.z >> D1_SHIFT) >= d1);
-    const uint32_t b3 = __ballot_sync(0xffffffffu, j + 3 < hi4 && (kv.w >> D1_SHIFT) >= d1);
+    const bool c0 = j + 0 < hi4 && (kv.x >> D1_SHIFT) >= d1;
+    const bool c1 = j + 1 < hi4 && (kv.y >> D1_SHIFT) >= d1;
+    const bool c2 = j + 2 < hi4 && (kv.z >> D1_SHIFT) >= d1;
+    const bool c3 = j + 3 < hi4 && (kv.w >> D1_SHIFT) >= d1;
+    const uint32_t b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
+    const uint32_t b2 = __ballot_sync(0xffffffffu, c2), b3 = __ballot_sync(0xffffffffu, c3);
+    // branch-free: non-candidates (and overflow) store to this warp's trash entry
+    const int p0 = cnt + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+    const int p1 = p0 + c0, p2 = p1 + c1, p3 = p2 + c2;
+    myseg[c0 && p0 < RCAP ? p0 : trash] = (uint16_t)(j + 0);
+    myseg[c1 && p1 < RCAP ? p1 : trash] = (uint16_t)(j + 1);
+    myseg[c2 && p2 < RCAP ? p2 : trash] = (uint16_t)(j + 2);
+    myseg[c3 && p3 < RCAP ? p3 : trash] = (uint16_t)(j + 3);
     cnt += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
   }
   KPROF(8);
-  int m;
-  int base = block_exclusive_scan<NT>(lane ? 0 : cnt, wbuf, &m);
-  KPROF(9);
-  base = __shfl_sync(0xffffffffu, base, 0);
-  const bool use_l = m <= LCAP;
-#ifdef ESS_TOPK_PROF
-  if (threadIdx.x == 0 && blockIdx.x < 1024) g_topk_prof[blockIdx.x][7] = (unsigned long long)m;
-#endif
-  if (use_l) {
+  // a segment overflowed (candidates bunched in one run, e.g. sorted rows): one
+  // contiguous list from the per-warp counts (scan + second pass), or, past LCAP
+  // entries (mass ties), full-slice passes
+  const bool seg = !__syncthreads_or(cnt > RCAP);
+  int m = 0;
+  bool use_l = true;
+  if (!seg) {
+    int base = block_exclusive_scan<NT>(lane ? 0 : cnt, wbuf, &m);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    use_l = m <= LCAP;
+    if (use_l) {
 #pragma unroll LIST_UNROLL
-    for (int i = lo4; i < hi4; i += 128) {
-      const int j = i + lane * 4;
-      const uint4 kv = j < hi4 ? *reinterpret_cast<const uint4 *>(skey + j) : make_uint4(0, 0, 0, 0);
-      const bool c0 = j + 0 < hi4 && (kv.x >> D1_SHIFT) >= d1;
-      const bool c1 = j + 1 < hi4 && (kv.y >> D1_SHIFT) >= d1;
-      const bool c2 = j + 2 < hi4 && (kv.z >> D1_SHIFT) >= d1;
-      const bool c3 = j + 3 < hi4 && (kv.w >> D1_SHIFT) >= d1;
-      const uint32_t b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
-      const uint32_t b2 = __ballot_sync(0xffffffffu, c2), b3 = __ballot_sync(0xffffffffu, c3);
-      int pos = base + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
-      if (c0) list[pos++] = (uint16_t)(j + 0);
-      if (c1) list[pos++] = (uint16_t)(j + 1);
-      if (c2) list[pos++] = (uint16_t)(j + 2);
-      if (c3) list[pos++] = (uint16_t)(j + 3);
-      base += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+      for (int i = lo4; i < hi4; i += 128) {
+        const int j = i + lane * 4;
+        const uint4 kv = j < hi4 ? *reinterpret_cast<const uint4 *>(skey + j) : make_uint4(0, 0, 0, 0);
+        const bool c0 = j + 0 < hi4 && (kv.x >> D1_SHIFT) >= d1;
+        const bool c1 = j + 1 < hi4 && (kv.y >> D1_SHIFT) >= d1;
+        const bool c2 = j + 2 < hi4 && (kv.z >> D1_SHIFT) >= d1;
+        const bool c3 = j + 3 < hi4 && (kv.w >> D1_SHIFT) >= d1;
+        const uint32_t b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
+        const uint32_t b2 = __ballot_sync(0xffffffffu, c2), b3 = __ballot_sync(0xffffffffu, c3);
+        int pos = base + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+        if (c0) list[pos++] = (uint16_t)(j + 0);
+        if (c1) list[pos++] = (uint16_t)(j + 1);
+        if (c2) list[pos++] = (uint16_t)(j + 2);
+        if (c3) list[pos++] = (uint16_t)(j + 3);
+        base += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+      }
     }
   }
-
+#ifdef ESS_TOPK_PROF
+  if (threadIdx.x == 0 && blockIdx.x < 1024) g_topk_prof[blockIdx.x][7] = (unsigned long long)(seg ? 0 : m);
+#endif
+  KPROF(9);
+  // the candidates: this warp's segment (seg), the contiguous list, or the whole slice
+  const int len2 = seg ? cnt : (use_l ? m : n);
+  const int i0 = seg ? lane : threadIdx.x, istep = seg ? 32 : NT;
+  auto cand = [&](int i) -> int { return seg ? myseg[i] : (use_l ? list[i] : i); };
 
   KPROF(3);
   // ---- two 10-bit digits inside bin d1 ------------------------------------------------
   uint32_t prefix = d1 << D1_SHIFT, mask = ~0u << D1_SHIFT;
   for (int shift = DR_BITS; shift >= 0; shift -= DR_BITS) {
-    const int len2 = use_l ? m : n;
     if constexpr (CLN > 1) {
       csum[threadIdx.x] = 0;  // after this CTA's previous pick (it ends in a CTA barrier)
       cluster_sync<CLN>();    // every rank zeroed and done picking from its csum
       uint32_t rb[CLN];
 #pragma unroll
       for (int r = 0; r < CLN; r++) rb[r] = cluster_addr(csum, r);
-      for (int i = threadIdx.x; i < len2; i += NT) {
-        const uint32_t key = skey[use_l ? list[i] : i];
+      for (int i = i0; i < len2; i += istep) {
+        const uint32_t key = skey[cand(i)];
         if ((key & mask) == prefix) {
           const uint32_t off = 4u * ((key >> shift) & (DR_BINS - 1));
 #pragma unroll
@@ -386,8 +409,8 @@ __global__ void __launch_bounds__(NT, 1)
     } else {
       hist[threadIdx.x] = 0;
       __syncthreads();
-      for (int i = threadIdx.x; i < len2; i += NT) {
-        const uint32_t key = skey[use_l ? list[i] : i];
+      for (int i = i0; i < len2; i += istep) {
+        const uint32_t key = skey[cand(i)];
         if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & (DR_BINS - 1)], 1);
       }
       __syncthreads();
@@ -403,7 +426,26 @@ __global__ void __launch_bounds__(NT, 1)
   KPROF(4);
   // ---- this slice's (greater, equal) counts and their cluster prefix ------------------
   int gb = 0, eb = 0, fb_ex = 0;
-  if (use_l) {
+  if (seg) {  // per-warp counts; their prefix orders the segments' emits
+    int g = 0, q = 0;
+    for (int i = lane; i < cnt; i += 32) {
+      const uint32_t key = skey[myseg[i]];
+      g += key > T;
+      q += key == T;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      g += __shfl_xor_sync(0xffffffffu, g, d);
+      q += __shfl_xor_sync(0xffffffffu, q, d);
+    }
+    int tot;
+    fb_ex = block_exclusive_scan<NT>(lane ? 0 : (g | (q << 16)), wbuf, &tot);
+    fb_ex = __shfl_sync(0xffffffffu, fb_ex, 0);
+    if (threadIdx.x == 0) {
+      part[0] = tot & 0xFFFF;
+      part[1] = tot >> 16;
+    }
+  } else if (use_l) {
     if constexpr (CLN > 1) {
       int g = 0, q = 0;
       for (int i = threadIdx.x; i < m; i += NT) {
@@ -441,7 +483,20 @@ __global__ void __launch_bounds__(NT, 1)
 
   KPROF(5);
   // ---- ordered emit: every key > T and the first need_eq keys == T --------------------
-  if (use_l) {
+  if (seg) {
+    int gw = gb + (fb_ex & 0xFFFF), ew = eb + (fb_ex >> 16);
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      const int i = c0 + lane;
+      const int j = i < cnt ? myseg[i] : 0;
+      const uint32_t key = i < cnt ? skey[j] : 0u;
+      const bool gt = i < cnt && key > T, eq = i < cnt && key == T;
+      const uint32_t mg = __ballot_sync(0xffffffffu, gt), me = __ballot_sync(0xffffffffu, eq);
+      const int e = ew + __popc(me & lt);
+      if (gt || (eq && e < need_eq)) o[gw + __popc(mg & lt) + min(e, need_eq)] = beg + j;
+      gw += __popc(mg);
+      ew += __popc(me);
+    }
+  } else if (use_l) {
     for (int c0 = 0; c0 < m; c0 += NT) {
       const int i = c0 + threadIdx.x;
       const int j = i < m ? list[i] : 0;
@@ -473,11 +528,11 @@ template <int CLN>
 int launch_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch, int32_t k,
                 int32_t *d_idx, int32_t idx_ld, int32_t *d_count, cudaStream_t stream,
                 SplitArgs sp = SplitArgs{}) {
-  const size_t smem = (size_t)slice_cap<CLN>(ld) * sizeof(uint32_t) + LCAP * sizeof(uint16_t);
+  const size_t smem = (size_t)slice_cap<CLN>(ld) * sizeof(uint32_t) + (LCAP + NW) * sizeof(uint16_t);
   static bool attr = false;  // per instantiation: opt in to the largest slice once
   if (!attr) {
     ESS_CUDA_TRY(cudaFuncSetAttribute(topk_kernel<CLN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(SLICE_MAX * sizeof(uint32_t) + LCAP * sizeof(uint16_t))));
+                                      (int)(SLICE_MAX * sizeof(uint32_t) + (LCAP + NW) * sizeof(uint16_t))));
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};

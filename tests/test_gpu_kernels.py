@@ -44,6 +44,22 @@ def test_topk_matches_oracle(lens):
         np.testing.assert_array_equal(idx[b, :cnt[b]], want)
 
 
+@pytest.mark.parametrize("n", [32768, 40000, 131072])
+def test_topk_sorted_rows(n):
+    """Candidates bunched at the end of the row (ascending scores) overflow the one-pass
+    list's per-warp segments; descending rows bunch them at the start."""
+    from paper_2512_10576_b200.indexer import topk
+    up = torch.arange(n, device="cuda", dtype=torch.float32) / n
+    logits = torch.stack([up, up.flip(0), torch.round(up * 50)])
+    L = torch.full((3,), n, dtype=torch.int32, device="cuda")
+    idx, cnt = topk(logits, L, 2048)
+    idx, cnt, host = idx.cpu().numpy(), cnt.cpu().numpy(), logits.cpu().numpy()
+    for b in range(3):
+        want = dsa.topk_indices(host[b], n, 2048)
+        assert cnt[b] == len(want)
+        np.testing.assert_array_equal(idx[b, :cnt[b]], want)
+
+
 def test_topk_all_equal_row():
     from paper_2512_10576_b200.indexer import topk
     logits = torch.zeros((2, 40000), device="cuda")
