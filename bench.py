@@ -331,6 +331,10 @@ def run_ours(args, cfg):
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     dev, agg_dev = init_ranks(local, world)
+    # launch loop and pinned staging on the GPU's NUMA node (ESS_BIND_NUMA=0: off);
+    # the CPU baseline below gets the full affinity back
+    from paper_2512_10576_b200.transfer import bind_to_gpu_node
+    prev_aff, bound_node = bind_to_gpu_node(dev) if os.environ.get("ESS_BIND_NUMA", "1") == "1" else (None, None)
     peaks, peak_kind = measured_peaks()
     B, rho = cfg["batch"], cfg["sparse_ratio"]
     lens = request_lengths(cfg, B, seed=rank)
@@ -418,6 +422,8 @@ def run_ours(args, cfg):
 
     gather_gbs = gather_bytes / (ktimes["gather"] * 1e-3) / 1e9 if ktimes["gather"] else None
     line = None
+    if prev_aff is not None:
+        os.sched_setaffinity(0, prev_aff)
     if rank == 0:
         cpu_v, cpu_sample, cpu_threads = cpu_reference_rate(cfg, budget_s=12.0)
         _cpu_pool_close()
@@ -434,7 +440,8 @@ def run_ours(args, cfg):
                        "micro_batches": args.micro if args.overlap == "dba" else 1,
                        "first_micro_batch_share": args.first if args.overlap == "dba" else None,
                        "parallelism": f"dp{world} (requests sharded, no collective)",
-                       "l2": "inputs larger than L2 (indexer keys + slot pool > 600 MB/GPU)"},
+                       "l2": "inputs larger than L2 (indexer keys + slot pool > 600 MB/GPU)",
+                       "host_numa_node": bound_node},
             "e2e": {"value": e2e_tok / e2e_t, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
             "roofline": {"bound": "hbm", "kernel": "indexer (K1)", "achieved": achieved,

@@ -80,6 +80,31 @@ def gpu_numa_node(device=None) -> int | None:
         return None
 
 
+def bind_to_gpu_node(device=None) -> tuple[set | None, int | None]:
+    """Pin this process's threads to the CPUs of the GPU's NUMA node, so the step's
+    launch loop runs next to the GPU and pinned staging buffers are placed on that
+    node (first touch).  Returns (previous affinity, node) for ``os.sched_setaffinity``
+    to restore; (None, None) when the node or its CPU list is unknown."""
+    node = gpu_numa_node(device)
+    if node is None or not hasattr(os, "sched_setaffinity"):
+        return None, None
+    try:
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        prev = os.sched_getaffinity(0)
+        cpus &= prev
+        if not cpus:
+            return None, None
+        os.sched_setaffinity(0, cpus)
+        return prev, node
+    except (OSError, ValueError):
+        return None, None
+
+
 class HostLatentStore:
     """[pools, rows_per_pool] latent rows of 656 B in page-locked, device-mapped host
     memory, laid out at the ESS_HOST_ROW_PITCH (704-B) pitch so every row starts on a
