@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(NT, 1)
     topk_kernel(const float *__restrict__ logits, int64_t ld, const int32_t *__restrict__ lens,
                 int k, int32_t *__restrict__ out, int out_ld, int32_t *__restrict__ counts,
                 SplitArgs sp) {
-  extern __shared__ uint32_t skey[];  // slice_cap keys, then LCAP u16 list entries + NW trash
+  extern __shared__ uint32_t skey[];  // slice_cap keys, then LCAP u16 list entries + NT trash
   uint16_t *list = reinterpret_cast<uint16_t *>(skey + slice_cap<CLN>(ld));
   __shared__ int hist[D1_BINS];
   __shared__ int csum[CLN > 1 ? D1_BINS : 1];  // cluster rows: histogram summed over ranks
@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(NT, 1)
   // order are in row order.  128-key chunks: each lane reads 4 consecutive keys with
   // one 16-B shared load and the 4 ballots give every key's rank in row order.
   uint16_t *myseg = list + warp * RCAP;
-  const int trash = LCAP + warp - warp * RCAP;  // list[LCAP + warp], relative to myseg
+  const int trash = LCAP + threadIdx.x - warp * RCAP;  // list[LCAP + thread], relative to myseg
   int cnt = 0;
 #pragma unroll LIST_UNROLL
   for (int i = lo4; i < hi4; i += 128) {
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(NT, 1)
     const bool c3 = j + 3 < hi4 && (kv.w >> D1_SHIFT) >= d1;
     const uint32_t b0 = __ballot_sync(0xffffffffu, c0), b1 = __ballot_sync(0xffffffffu, c1);
     const uint32_t b2 = __ballot_sync(0xffffffffu, c2), b3 = __ballot_sync(0xffffffffu, c3);
-    // branch-free: non-candidates (and overflow) store to this warp's trash entry
+    // branch-free: non-candidates (and overflow) store to this thread's trash entry
     const int p0 = cnt + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
     const int p1 = p0 + c0, p2 = p1 + c1, p3 = p2 + c2;
     myseg[c0 && p0 < RCAP ? p0 : trash] = (uint16_t)(j + 0);
@@ -528,11 +528,11 @@ template <int CLN>
 int launch_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch, int32_t k,
                 int32_t *d_idx, int32_t idx_ld, int32_t *d_count, cudaStream_t stream,
                 SplitArgs sp = SplitArgs{}) {
-  const size_t smem = (size_t)slice_cap<CLN>(ld) * sizeof(uint32_t) + (LCAP + NW) * sizeof(uint16_t);
+  const size_t smem = (size_t)slice_cap<CLN>(ld) * sizeof(uint32_t) + (LCAP + NT) * sizeof(uint16_t);
   static bool attr = false;  // per instantiation: opt in to the largest slice once
   if (!attr) {
     ESS_CUDA_TRY(cudaFuncSetAttribute(topk_kernel<CLN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(SLICE_MAX * sizeof(uint32_t) + (LCAP + NW) * sizeof(uint16_t))));
+                                      (int)(SLICE_MAX * sizeof(uint32_t) + (LCAP + NT) * sizeof(uint16_t))));
     attr = true;
   }
   cudaLaunchConfig_t cfg = {};
