@@ -43,7 +43,7 @@ CONFIGS = {
     "c5": dict(batch=64, context_len=(8192, 131072), sparse_ratio=0.25, micro=2, first=0.375,
                workload="C5: one DSA layer decode, batch 64/GPU of mixed 8K-128K contexts "
                         "(log-uniform), 25% GPU slot pool"),
-    "c4": dict(batch=64, context_len=131072, sparse_ratio=0.10, micro=3, first=0.375,
+    "c4": dict(batch=64, context_len=131072, sparse_ratio=0.10, micro=3, first=0.1875,
                workload="C4: one DSA layer decode, batch 64/GPU, ctx 128K, 10% GPU slot pool"),
 }
 TOPK = 2048
