@@ -16,10 +16,11 @@
 //      (distributed shared memory reductions) and all agree on the digit d1 without a
 //      global round trip;
 //   2. the keys whose first digit is >= d1 (the < k keys above the bin plus the bin
-//      itself, about k per row) are compacted in row order into a u16 list;
-//   3. the two 10-bit passes and the ordered emit touch only that list.
-// Full-slice passes: stage, count, compact.  A list longer than LCAP (mass ties) makes
-// that CTA fall back to full-slice passes.  The emit takes every key > T plus the first
+//      itself, about k per row) are appended in one pass to per-warp u16 list segments
+//      (in warp order = row order); a segment overflow falls back to one contiguous list;
+//   3. the two 10-bit passes and the ordered emit (per warp segment) touch only the list.
+// Full-slice passes: stage, list.  A list longer than LCAP (mass ties) makes that CTA
+// fall back to full-slice passes.  The emit takes every key > T plus the first
 // (k - #greater) keys == T in index order; CTA r's output offset is the cluster prefix
 // of the (greater, equal) counts of CTAs 0..r-1.
 #include <cooperative_groups.h>
