@@ -222,7 +222,8 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ int csum[CLN > 1 ? D1_BINS : 1];  // cluster rows: histogram summed over ranks
   __shared__ int wbuf[NW];
   __shared__ int scal[2];
-  __shared__ int part[2];  // this CTA's (greater, equal) totals, read by later ranks
+  __shared__ int part[2];  // this CTA's (greater, equal) totals
+  __shared__ int pre[2];   // cluster rows: (greater, equal) totals of the lower ranks (pushed)
   int rank = 0;
   if constexpr (CLN > 1) rank = (int)cg::this_cluster().block_rank();
   const int b = blockIdx.x / CLN;
@@ -251,7 +252,8 @@ __global__ void __launch_bounds__(NT, 1)
   for (int i = threadIdx.x; i < D1_BINS; i += NT) hist[i] = 0;
   if constexpr (CLN > 1) {
     for (int i = threadIdx.x; i < D1_BINS; i += NT) csum[i] = 0;
-    cluster_arrive();  // csum zeroed; peers push into it after the matching wait
+    if (threadIdx.x < 2) pre[threadIdx.x] = 0;
+    cluster_arrive();  // csum / pre zeroed; peers push into them after the matching wait
   }
   __syncthreads();
 
@@ -390,13 +392,19 @@ __global__ void __launch_bounds__(NT, 1)
   KPROF(3);
   // ---- two 10-bit digits inside bin d1 ------------------------------------------------
   uint32_t prefix = d1 << D1_SHIFT, mask = ~0u << D1_SHIFT;
+  if constexpr (CLN > 1) {
+    // both 10-bit passes' sums (csum[0:1024], csum[1024:2048]) zeroed after this CTA's
+    // first-digit pick; one cluster barrier covers the zeroing and every rank's pick
+    csum[threadIdx.x] = 0;
+    csum[DR_BINS + threadIdx.x] = 0;
+    cluster_sync<CLN>();
+  }
   for (int shift = DR_BITS; shift >= 0; shift -= DR_BITS) {
     if constexpr (CLN > 1) {
-      csum[threadIdx.x] = 0;  // after this CTA's previous pick (it ends in a CTA barrier)
-      cluster_sync<CLN>();    // every rank zeroed and done picking from its csum
+      int *dsum = csum + (shift ? 0 : DR_BINS);  // this pass's buffer (no peer reads it yet)
       uint32_t rb[CLN];
 #pragma unroll
-      for (int r = 0; r < CLN; r++) rb[r] = cluster_addr(csum, r);
+      for (int r = 0; r < CLN; r++) rb[r] = cluster_addr(dsum, r);
       for (int i = i0; i < len2; i += istep) {
         const uint32_t key = skey[cand(i)];
         if ((key & mask) == prefix) {
@@ -406,7 +414,7 @@ __global__ void __launch_bounds__(NT, 1)
         }
       }
       cluster_sync<CLN>();  // every push landed
-      pick_digit<DR_BINS>(csum, rem, wbuf, scal);
+      pick_digit<DR_BINS>(dsum, rem, wbuf, scal);
     } else {
       hist[threadIdx.x] = 0;
       __syncthreads();
@@ -472,14 +480,18 @@ __global__ void __launch_bounds__(NT, 1)
     }
   }
   if constexpr (CLN > 1) {
-    cg::cluster_group cl = cg::this_cluster();
-    cl.sync();
-    for (int r = 0; r < rank; r++) {
-      const int *pc = cl.map_shared_rank(part, r);
-      gb += pc[0];
-      eb += pc[1];
+    // add this slice's totals into every higher rank's prefix, one barrier, read ours
+    __syncthreads();  // part written
+    if (threadIdx.x == 0) {
+      for (int r = rank + 1; r < CLN; r++) {
+        const uint32_t a = cluster_addr(pre, r);
+        cluster_red_add(a, part[0]);
+        cluster_red_add(a + 4, part[1]);
+      }
     }
-    cl.sync();  // keep shared memory alive until every peer has read our counts
+    cluster_sync<CLN>();
+    gb = pre[0];
+    eb = pre[1];
   }
 
   KPROF(5);
