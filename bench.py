@@ -322,10 +322,29 @@ def kernel_breakdown(layer, inputs, new_rows):
     return ms, torch.stack(counts)
 
 
+def product_layer(cfg, dev, steps, drift=0.97, rank=0, micro=None, first=None, gather_ctas=32,
+                  record=False):
+    """The benchmarked product layer of a single-layer config, set up exactly as the timed
+    run uses it (the parity tests at the benchmarked shapes build it through here):
+    per-request lengths, pools at floor(rho * history), the DBA micro-batch split and the
+    32-window prefill warm-up.  Returns (layer, lens, windows or None)."""
+    from paper_2512_10576_b200.decode import DSADecodeLayer
+    B, rho = cfg["batch"], cfg["sparse_ratio"]
+    lens = request_lengths(cfg, B, seed=rank)
+    L = lens if not isinstance(cfg["context_len"], int) else cfg["context_len"]
+    layer = DSADecodeLayer(B, L, rho, TOPK, max_new_tokens=steps + 16, device=dev,
+                           seed=1234 + rank, drift=drift)
+    layer.gather_ctas = gather_ctas
+    layer.micro = cfg["micro"] if micro is None else micro
+    layer.first_frac = (cfg["first"] if layer.micro == cfg["micro"] else None) if first is None else first
+    windows = layer.prefill_warmup(windows=32, record=record)
+    return layer, lens, (windows if record else None)
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
-    from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows
+    from paper_2512_10576_b200.decode import random_latent_rows
     from paper_2512_10576_b200.dp import aggregate
 
     rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
@@ -337,16 +356,11 @@ def run_ours(args, cfg):
     prev_aff, bound_node = bind_to_gpu_node(dev) if os.environ.get("ESS_BIND_NUMA", "1") == "1" else (None, None)
     peaks, peak_kind = measured_peaks()
     B, rho = cfg["batch"], cfg["sparse_ratio"]
-    lens = request_lengths(cfg, B, seed=rank)
-    L = lens if not isinstance(cfg["context_len"], int) else cfg["context_len"]
     W, K, NB = args.warmup, args.steps, args.breakdown_steps
     total = W + K + NB
-    layer = DSADecodeLayer(B, L, rho, TOPK, max_new_tokens=total + K + 16, device=dev,
-                           seed=1234 + rank, drift=args.drift)
-    layer.gather_ctas = args.gather_ctas
-    layer.micro = args.micro
-    layer.first_frac = args.first
-    layer.prefill_warmup(windows=32)
+    layer, lens, _ = product_layer(cfg, dev, total + K, drift=args.drift, rank=rank, micro=args.micro,
+                                   first=args.first, gather_ctas=args.gather_ctas)
+    L = lens if not isinstance(cfg["context_len"], int) else cfg["context_len"]
     inputs = [layer.next_queries() for _ in range(total)]
     new_rows = [random_latent_rows(B, dev, layer.gen).view(B, 1, 656) for _ in range(total)]
     torch.cuda.synchronize()
@@ -554,9 +568,7 @@ def run_ceiling(args, cfg, dev):
     sequential schedule, the fastest one when there is nothing to overlap (the DBA
     split only pays when a gather has to hide), so the ceiling is the strict one."""
     import torch
-    from paper_2512_10576_b200.cache import AccessBatch
     from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows
-    from paper_2512_10576_b200.transfer import gather
     B = cfg["batch"]
     lens = request_lengths(cfg, B, seed=int(os.environ.get("RANK", "0")))
     L = lens if not isinstance(cfg["context_len"], int) else cfg["context_len"]
@@ -564,15 +576,7 @@ def run_ceiling(args, cfg, dev):
     layer = DSADecodeLayer(B, L, 1.0, TOPK, max_new_tokens=total + 8, device=dev, seed=99,
                            drift=args.drift)
     layer.gather_ctas = args.gather_ctas
-    full = torch.arange(max(lens), dtype=torch.int32, device=dev)
-    for c0 in range(0, max(lens), 2048):
-        ids = full[c0:c0 + 2048].expand(B, -1).contiguous()
-        nb = torch.tensor([min(2048, max(0, n - c0)) for n in lens], dtype=torch.int32, device=dev)
-        layer.pool.warmup(ids, nb)
-        slots = torch.stack([layer.pool.lookup(b, ids[b]) for b in range(B)])
-        cnt = torch.zeros((B, 4), dtype=torch.int32, device=dev)
-        cnt[:, 1] = nb
-        gather(layer.pool, layer.store, AccessBatch(cnt, None, ids, slots.contiguous()), max_ctas=148)
+    layer.preload_full_history()
     inputs = [layer.next_queries() for _ in range(total)]
     new_rows = [random_latent_rows(B, dev, layer.gen).view(B, 1, 656) for _ in range(total)]
     layer.capture("none", args.gather_ctas)  # all-HBM: its fastest schedule, nothing to gather

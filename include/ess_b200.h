@@ -205,7 +205,9 @@ int ess_indexer_logits_ex(const void *d_q, const float *d_w, const void *d_k,
 
 /* ---- K2 top-k (op "indexer_topk") ---------------------------------------------- */
 /* per row: the k largest logits[b][0:len[b]) by (score desc, index asc), written
- * ascending to d_idx [B][idx_ld]; d_count[b] = min(k, len[b]) (scenario.py:110-112) */
+ * ascending to d_idx [B][idx_ld]; d_count[b] = min(k, len[b]) (scenario.py:110-112);
+ * 1 <= k <= ESS_TOPK_MAX_K */
+#define ESS_TOPK_MAX_K 65535
 int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
              int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count, void *stream);
 /* top-k fused with ess_pool_split on the emitted selection, one launch (for cluster

@@ -137,3 +137,19 @@ def sparse_mla(q: np.ndarray, rows_u8: np.ndarray, sm_scale: float):
     out = (p / denom) @ k_nope.astype(np.float64)
     lse = (np.log(denom) + m)[:, 0]
     return out.astype(np.float32), lse.astype(np.float32)
+
+
+def sparse_mla_on_slot_rows(q: np.ndarray, slot_f16: np.ndarray, sm_scale: float):
+    """fp64 attention over rows ALREADY in the kernel's operand precision: slot_f16
+    [n, 576] f16 (= slot_rows(), the exact K / V values K5's tensor cores multiply;
+    V = the first 512 columns).  The K5 tests compare against this, so the tolerance
+    only has to cover K5's own roundings (P to f16, the bf16 output), not the f16
+    dequantisation of the rows."""
+    K = np.asarray(slot_f16, np.float64)
+    s = (np.asarray(q, np.float64) @ K.T) * sm_scale
+    m = s.max(axis=1, keepdims=True)
+    p = np.exp(s - m)
+    denom = p.sum(axis=1, keepdims=True)
+    out = (p / denom) @ K[:, :NOPE_DIM]
+    lse = (np.log(denom) + m)[:, 0]
+    return out.astype(np.float32), lse.astype(np.float32)

@@ -127,3 +127,23 @@ def require_cuda(t=None) -> None:
         raise RuntimeError("ess_b200 needs a CUDA device (sm_100a); no CPU fallback exists")
     if t is not None and not t.is_cuda:
         raise ValueError("tensor must be on the CUDA device")
+
+
+def check_tensor(t, name: str, dtypes, shape=None, contiguous: bool = True, device=None) -> None:
+    """Argument validation of the ctypes wrappers: the kernels address tensors through
+    raw pointers and the strides they are given, so a wrong dtype, shape or layout must
+    be refused here (ValueError), never reach the device."""
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise ValueError(f"{name} must be a torch.Tensor")
+    if not isinstance(dtypes, (tuple, list)):
+        dtypes = (dtypes,)
+    if t.dtype not in dtypes:
+        raise ValueError(f"{name} has dtype {t.dtype}, expected one of {list(dtypes)}")
+    if shape is not None:
+        if len(shape) != t.dim() or any(w is not None and w != g for w, g in zip(shape, t.shape)):
+            raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if contiguous and not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if not t.is_cuda or (device is not None and t.device != device):
+        raise ValueError(f"{name} must be on the CUDA device {device or ''}".rstrip())

@@ -21,7 +21,9 @@ int ess_record_cuda_error(cudaError_t e);
 bool ess_make_tmap_2d(CUtensorMap *m, CUtensorMapDataType dtype, const void *base,
                       uint64_t inner, uint64_t rows, uint64_t row_stride_bytes,
                       uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle swizzle);
-int ess_sm_count();
+int ess_sm_count();  // of the current device
+// raise `func`'s dynamic shared-memory limit to >= bytes on the current device (cached)
+int ess_smem_optin(const void *func, size_t bytes);
 
 // Per-pool mutable scalars (one 64-byte record per pool).  Recency is a strictly
 // increasing 32-bit clock; free slots carry key == slot index (< cap_max) and
@@ -64,28 +66,29 @@ __device__ __forceinline__ void ess_set_status(int32_t *status, int32_t code) {
 // Exclusive block scan over NT threads (NT multiple of 32, <= 1024).
 // `warp_buf` needs NT/32 ints.  All threads must call.  Returns exclusive prefix;
 // *total gets the block sum.
-template <int NT>
-__device__ __forceinline__ int block_exclusive_scan(int v, int *warp_buf, int *total) {
+// T = int, or uint32_t for packed multi-field counts (modular adds, logical shifts).
+template <int NT, typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T *warp_buf, T *total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int x = v;
+  T x = v;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    int y = __shfl_up_sync(0xffffffffu, x, o);
+    T y = __shfl_up_sync(0xffffffffu, x, o);
     if (lane >= o) x += y;
   }
   if (lane == 31) warp_buf[warp] = x;
   __syncthreads();
   if (warp == 0) {
-    int s = lane < NT / 32 ? warp_buf[lane] : 0;
+    T s = lane < NT / 32 ? warp_buf[lane] : T(0);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, s, o);
+      T y = __shfl_up_sync(0xffffffffu, s, o);
       if (lane >= o) s += y;
     }
     if (lane < NT / 32) warp_buf[lane] = s;
   }
   __syncthreads();
-  int base = warp ? warp_buf[warp - 1] : 0;
+  T base = warp ? warp_buf[warp - 1] : T(0);
   *total = warp_buf[NT / 32 - 1];
   __syncthreads();
   return base + x - v;

@@ -5,7 +5,9 @@
 #include <unistd.h>
 
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "common.cuh"
 
@@ -44,15 +46,36 @@ bool ess_make_tmap_2d(CUtensorMap *m, CUtensorMapDataType dtype, const void *bas
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Per-device state (a process may drive several GPUs, one stream per caller thread):
+// the SM count and each kernel's dynamic shared-memory opt-in are per device.
 int ess_sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  constexpr int MAXDEV = 64;
+  static int n[MAXDEV] = {};  // benign race: every writer stores the same value
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= MAXDEV) dev = 0;
+  if (!n[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
   }
-  return n;
+  return n[dev];
+}
+
+int ess_smem_optin(const void *func, size_t bytes) {
+  // no shortcut below 48 KB: the default dynamic limit is 48 KB minus the kernel's
+  // static shared memory, so a kernel with large static storage needs the opt-in too
+  if (bytes == 0) return ESS_OK;
+  static std::mutex mu;
+  static std::map<std::pair<const void *, int>, size_t> done;  // (kernel, device) -> bytes
+  int dev = 0;
+  ESS_CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  size_t &have = done[{func, dev}];
+  if (have >= bytes) return ESS_OK;
+  ESS_CUDA_TRY(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  have = bytes;
+  return ESS_OK;
 }
 
 extern "C" {

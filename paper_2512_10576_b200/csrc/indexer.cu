@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     int acc = 0;
     for (int b0 = 0; b0 < B; b0 += 32) {
       const int b = b0 + lane;
-      const int L = b < B ? __ldg(lens + b) : 0;
+      const int L = b < B ? min(__ldg(lens + b), (int)k_ld) : 0;
       const int u = L > 0 ? (L + UNIT_M - 1) / UNIT_M : 0;
       int x = u;  // inclusive warp scan
 #pragma unroll
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tma_load_2d(qbuf + qs * QT_BYTES, &tm_q, &c.qfull[qs], 0, cur.b * HEADS);
             quse[qs]++;
             prev_b = cur.b;
-            len_b = __ldg(lens + cur.b);
+            len_b = min(__ldg(lens + cur.b), (int)k_ld);
           }
           const int s = it % STAGES;
           // MMA tiles of this unit that hold tokens (the last unit may be short; its
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             wr[4 * h4 + 2] = v.z;
             wr[4 * h4 + 3] = v.w;
           }
-          len_b = __ldg(lens + b);
+          len_b = min(__ldg(lens + b), (int)k_ld);
           wb = b;
         }
         int64_t off[SUB];
@@ -363,12 +363,7 @@ extern "C" int ess_indexer_logits_ex(const void *d_q, const float *d_w, const vo
   alignas(64) CUtensorMap tq;
   if (!make_map(&tk, d_k, (uint64_t)batch * (uint64_t)k_ld, TILE_M, kc)) return ESS_ERR_CUDA;
   if (!make_map(&tq, d_q, (uint64_t)batch * HEADS, HEADS, qc)) return ESS_ERR_CUDA;
-  static bool attr = false;
-  if (!attr) {
-    ESS_CUDA_TRY(cudaFuncSetAttribute(indexer_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)SMEM_BYTES));
-    attr = true;
-  }
+  if (int rc = ess_smem_optin((const void *)indexer_kernel, SMEM_BYTES)) return rc;
   const int ctas = max_ctas > 0 && max_ctas < ess_sm_count() ? max_ctas : ess_sm_count();
   indexer_kernel<<<ctas, NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
       tk, tq, d_w, d_kscale, d_len, batch, k_ld, d_logits);

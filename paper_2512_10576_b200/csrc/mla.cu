@@ -738,12 +738,7 @@ int launch_mla(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_
     qm.batch = batch;
     qm.map = tq;
   }
-  static bool attr = false;
-  if (!attr) {
-    ESS_CUDA_TRY(cudaFuncSetAttribute(sparse_mla_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)SMEM_BYTES));
-    attr = true;
-  }
+  if (int rc = ess_smem_optin((const void *)sparse_mla_kernel, SMEM_BYTES)) return rc;
   dim3 grid(2, batch * nsplit);
   sparse_mla_kernel<<<grid, NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
       tq, pool->rows, pool->rows_per_pool, pool_begin, d_sel_row, d_sel2, d_landed, sel_stride,

@@ -1427,12 +1427,7 @@ int ess_pool_access(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_re
   const size_t stage = (size_t)p->cap_max * 4;
   size_t smem = 0;
   if (stage <= STAGE_SMEM_MAX) {
-    static size_t attr = 0;  // largest opt-in so far
-    if (stage > attr) {
-      ESS_CUDA_TRY(cudaFuncSetAttribute(pool_step_kernel<MODE_ACCESS>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)stage));
-      attr = stage;
-    }
+    if (int rc = ess_smem_optin((const void *)pool_step_kernel<MODE_ACCESS>, stage)) return rc;
     smem = stage;
     flags |= POOL_STAGED;
   }
@@ -1548,9 +1543,7 @@ int ess_gather_signal(ess_pool *p, int32_t begin, int32_t num, const void *d_hos
   if ((flags & ESS_GATHER_EXCLUSIVE_SM) && smem < ESS_GATHER_EXCLUSIVE_SMEM)
     smem = ESS_GATHER_EXCLUSIVE_SMEM;
   auto kern = bulk ? gather_bulk_kernel : gather_kernel;
-  if (smem > 48 * 1024) {
-    ESS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  }
+  if (int rc = ess_smem_optin((const void *)kern, smem)) return rc;
   kern<<<max_ctas, NTG, smem, (cudaStream_t)stream>>>(
       view(p), begin, num, (const uint8_t *)d_host_rows, host_pool_stride_rows, d_miss_ids,
       d_miss_row, d_counts, stride, d_landed);

@@ -71,6 +71,12 @@ __device__ __forceinline__ uint32_t score_key(float f) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
+// (greater, equal) counts packed as g | q << 16 in an unsigned word: g < k <= 65535 and
+// a CTA holds at most SLICE_MAX (40K) keys, so neither field carries into the other and
+// the logical >> 16 never sign-extends (a signed pack broke at 32K equal keys).
+__device__ __forceinline__ uint32_t pack_gq(uint32_t g, uint32_t q) { return g | (q << 16); }
+static_assert(SLICE_MAX < 65536, "equal-count field of pack_gq");
+
 template <int CLN>
 __device__ __forceinline__ void cluster_sync() {
   if constexpr (CLN > 1) cg::this_cluster().sync();
@@ -221,13 +227,14 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ int hist[D1_BINS];
   __shared__ int csum[CLN > 1 ? D1_BINS : 1];  // cluster rows: histogram summed over ranks
   __shared__ int wbuf[NW];
+  uint32_t *uwbuf = reinterpret_cast<uint32_t *>(wbuf);  // packed-count scans
   __shared__ int scal[2];
   __shared__ int part[2];  // this CTA's (greater, equal) totals
   __shared__ int pre[2];   // cluster rows: (greater, equal) totals of the lower ranks (pushed)
   int rank = 0;
   if constexpr (CLN > 1) rank = (int)cg::this_cluster().block_rank();
   const int b = blockIdx.x / CLN;
-  const int len = lens[b];
+  const int len = (int)min((int64_t)lens[b], ld);  // a len past the row stride reads no further
   const float *row = logits + (int64_t)b * ld;
   int32_t *o = out + (int64_t)b * out_ld;
   const int chunk = (((len + CLN - 1) / CLN) + 3) & ~3;
@@ -434,7 +441,8 @@ __global__ void __launch_bounds__(NT, 1)
 
   KPROF(4);
   // ---- this slice's (greater, equal) counts and their cluster prefix ------------------
-  int gb = 0, eb = 0, fb_ex = 0;
+  int gb = 0, eb = 0;
+  uint32_t fb_ex = 0;  // packed (greater, equal) prefix of the lower warps
   if (seg) {  // per-warp counts; their prefix orders the segments' emits
     int g = 0, q = 0;
     for (int i = lane; i < cnt; i += 32) {
@@ -447,12 +455,12 @@ __global__ void __launch_bounds__(NT, 1)
       g += __shfl_xor_sync(0xffffffffu, g, d);
       q += __shfl_xor_sync(0xffffffffu, q, d);
     }
-    int tot;
-    fb_ex = block_exclusive_scan<NT>(lane ? 0 : (g | (q << 16)), wbuf, &tot);
+    uint32_t tot;
+    fb_ex = block_exclusive_scan<NT>(lane ? 0u : pack_gq(g, q), uwbuf, &tot);
     fb_ex = __shfl_sync(0xffffffffu, fb_ex, 0);
     if (threadIdx.x == 0) {
-      part[0] = tot & 0xFFFF;
-      part[1] = tot >> 16;
+      part[0] = (int)(tot & 0xFFFFu);
+      part[1] = (int)(tot >> 16);
     }
   } else if (use_l) {
     if constexpr (CLN > 1) {
@@ -462,21 +470,22 @@ __global__ void __launch_bounds__(NT, 1)
         g += key > T;
         q += key == T;
       }
-      int tot;
-      block_exclusive_scan<NT>(g | (q << 16), wbuf, &tot);
+      uint32_t tot;
+      block_exclusive_scan<NT>(pack_gq(g, q), uwbuf, &tot);
       if (threadIdx.x == 0) {
-        part[0] = tot & 0xFFFF;
-        part[1] = tot >> 16;
+        part[0] = (int)(tot & 0xFFFFu);
+        part[1] = (int)(tot >> 16);
       }
     }
   } else {
-    int g, q, tot;
+    int g, q;
+    uint32_t tot;
     run_counts(skey, lo, hi, T, g, q);
-    fb_ex = block_exclusive_scan<NT>(lane ? 0 : (g | (q << 16)), wbuf, &tot);
+    fb_ex = block_exclusive_scan<NT>(lane ? 0u : pack_gq(g, q), uwbuf, &tot);
     fb_ex = __shfl_sync(0xffffffffu, fb_ex, 0);
     if (threadIdx.x == 0) {
-      part[0] = tot & 0xFFFF;
-      part[1] = tot >> 16;
+      part[0] = (int)(tot & 0xFFFFu);
+      part[1] = (int)(tot >> 16);
     }
   }
   if constexpr (CLN > 1) {
@@ -497,7 +506,7 @@ __global__ void __launch_bounds__(NT, 1)
   KPROF(5);
   // ---- ordered emit: every key > T and the first need_eq keys == T --------------------
   if (seg) {
-    int gw = gb + (fb_ex & 0xFFFF), ew = eb + (fb_ex >> 16);
+    int gw = gb + (int)(fb_ex & 0xFFFFu), ew = eb + (int)(fb_ex >> 16);
     for (int c0 = 0; c0 < cnt; c0 += 32) {
       const int i = c0 + lane;
       const int j = i < cnt ? myseg[i] : 0;
@@ -515,15 +524,15 @@ __global__ void __launch_bounds__(NT, 1)
       const int j = i < m ? list[i] : 0;
       const uint32_t key = i < m ? skey[j] : 0u;
       const bool gt = i < m && key > T, eq = i < m && key == T;
-      int tot;
-      const int ex = block_exclusive_scan<NT>((int)gt | ((int)eq << 16), wbuf, &tot);
-      const int e = eb + (ex >> 16);
-      if (gt || (eq && e < need_eq)) o[gb + (ex & 0xFFFF) + min(e, need_eq)] = beg + j;
-      gb += tot & 0xFFFF;
-      eb += tot >> 16;
+      uint32_t tot;
+      const uint32_t ex = block_exclusive_scan<NT>(pack_gq(gt, eq), uwbuf, &tot);
+      const int e = eb + (int)(ex >> 16);
+      if (gt || (eq && e < need_eq)) o[gb + (int)(ex & 0xFFFFu) + min(e, need_eq)] = beg + j;
+      gb += (int)(tot & 0xFFFFu);
+      eb += (int)(tot >> 16);
     }
   } else {
-    run_emit(skey, lo, hi, T, need_eq, gb + (fb_ex & 0xFFFF), eb + (fb_ex >> 16), beg, o);
+    run_emit(skey, lo, hi, T, need_eq, gb + (int)(fb_ex & 0xFFFFu), eb + (int)(fb_ex >> 16), beg, o);
   }
   KPROF(6);
   if (rank == 0 && threadIdx.x == 0) counts[b] = k;
@@ -542,12 +551,10 @@ int launch_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t
                 int32_t *d_idx, int32_t idx_ld, int32_t *d_count, cudaStream_t stream,
                 SplitArgs sp = SplitArgs{}) {
   const size_t smem = (size_t)slice_cap<CLN>(ld) * sizeof(uint32_t) + (LCAP + NT) * sizeof(uint16_t);
-  static bool attr = false;  // per instantiation: opt in to the largest slice once
-  if (!attr) {
-    ESS_CUDA_TRY(cudaFuncSetAttribute(topk_kernel<CLN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(SLICE_MAX * sizeof(uint32_t) + (LCAP + NT) * sizeof(uint16_t))));
-    attr = true;
-  }
+  // per (instantiation, device): opt in to the largest slice
+  if (int rc = ess_smem_optin((const void *)topk_kernel<CLN>,
+                              SLICE_MAX * sizeof(uint32_t) + (LCAP + NT) * sizeof(uint16_t)))
+    return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)batch * CLN);
   cfg.blockDim = dim3(NT);
@@ -570,7 +577,8 @@ int launch_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t
 extern "C" int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
                         int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count,
                         void *stream) {
-  if (!d_logits || !d_len || !d_idx || !d_count || batch < 0 || k < 1 || idx_ld < k || ld < 1)
+  if (!d_logits || !d_len || !d_idx || !d_count || batch < 0 || k < 1 || k > ESS_TOPK_MAX_K ||
+      idx_ld < k || ld < 1)
     return ESS_ERR_ARG;
   if (batch == 0) return ESS_OK;
   // Cluster size: the smallest that fits a slice in shared memory.  Growing it to fill

@@ -152,6 +152,25 @@ class DSADecodeLayer:
         self.pool.check("prefill_warmup")
         return rec
 
+    def preload_full_history(self) -> None:
+        """The all-HBM ceiling's state: every request's whole history made
+        resident in its pool (needs sparse_ratio = 1) and its slot rows filled from the
+        host store, so every selection hits and no step gathers anything."""
+        if self.cap0 < max(self.ctx_lens):
+            raise ValueError("preload_full_history needs a pool that holds the whole history (rho = 1)")
+        B, d = self.B, self.device
+        full = torch.arange(self.ctx, dtype=torch.int32, device=d)
+        for c0 in range(0, self.ctx, _lib.MAX_REQUEST):
+            ids = full[c0:c0 + _lib.MAX_REQUEST].expand(B, -1).contiguous()
+            nb = torch.tensor([min(_lib.MAX_REQUEST, max(0, n - c0)) for n in self.ctx_lens],
+                              dtype=torch.int32, device=d)
+            self.pool.warmup(ids, nb)
+            slots = torch.stack([self.pool.lookup(b, ids[b]) for b in range(B)])
+            cnt = torch.zeros((B, 4), dtype=torch.int32, device=d)
+            cnt[:, 1] = nb
+            gather(self.pool, self.store, AccessBatch(cnt, None, ids, slots.contiguous()), max_ctas=148)
+        self.pool.check("preload_full_history")
+
     # -- the decode step -------------------------------------------------------------------
     def _select(self, q_idx, a, b, max_ctas: int = 0):
         """K1 -> K2 -> K3 for requests [a, b) on the current stream, writing into the
@@ -413,12 +432,22 @@ class DSADecodeLayer:
     def step(self, q_idx: torch.Tensor, q: torch.Tensor, new_rows: torch.Tensor):
         """One decode step through the captured graph: inputs land in the graph's
         static buffers (two device copies), then a single graph launch."""
+        self._check_room()
         self.q_idx_in.copy_(q_idx, non_blocking=True)
         self.q_in.copy_(q, non_blocking=True)
         self.rows_in.copy_(new_rows, non_blocking=True)
         self.graph.replay()
         self.history += 1
         return self.out, self.lse
+
+    def _check_room(self) -> None:
+        """A replayed step admits one generated id per request at its history length;
+        past Lmax the admission kernel latches ESS_ERR_ARG and stops advancing, so the
+        host refuses the step before it is launched (the device status is the backstop,
+        read by ``pool.check``)."""
+        if self.history + 1 > self.Lmax:
+            raise ValueError(f"decode step {self.history - self.ctx + 1} exceeds max_new_tokens: "
+                             f"history {self.history} + 1 > Lmax {self.Lmax}")
 
     def step_host(self, h_q_idx: torch.Tensor, h_q: torch.Tensor, new_rows: torch.Tensor,
                   h_out: torch.Tensor) -> None:
@@ -428,6 +457,7 @@ class DSADecodeLayer:
         while every step still moves its own inputs and result over the host link.
         Asynchronous: synchronise before reading ``h_out``."""
         d = self.device
+        self._check_room()
         if getattr(self, "_cs", None) is None:
             self._cs = torch.cuda.Stream(d)    # H2D copies
             self._ds = torch.cuda.Stream(d)    # D2H copies (other PCIe direction)
@@ -544,6 +574,8 @@ class DSADecodeModel:
 
     def step(self, queries, new_rows) -> None:
         """queries: per layer (q_idx, q); new_rows: per layer [B, 1, 656] (or one shared)."""
+        for layer in self.layers:
+            layer._check_room()
         for i, (layer, (q_idx, q)) in enumerate(zip(self.layers, queries)):
             layer.q_idx_in.copy_(q_idx, non_blocking=True)
             layer.q_in.copy_(q, non_blocking=True)

@@ -29,11 +29,21 @@ def indexer_logits(q_fp8: torch.Tensor, w: torch.Tensor, k_cache: torch.Tensor,
     persistent grid (SMs left free for a concurrent gather); 0 = every SM.
     """
     _lib.require_cuda(k_cache)
+    if k_cache.dim() != 3:
+        raise ValueError("expected k [B,Lmax,128]")
     B, Lmax, D = k_cache.shape
-    if D != DIM or q_fp8.shape != (B, HEADS, DIM) or w.shape != (B, HEADS):
-        raise ValueError("expected q [B,64,128], w [B,64], k [B,Lmax,128]")
+    if D != DIM or Lmax % 128:
+        raise ValueError("expected k [B,Lmax,128] with Lmax a multiple of 128")
+    dev = k_cache.device
+    fp8 = (torch.uint8, torch.float8_e4m3fn)
+    _lib.check_tensor(k_cache, "k_cache", fp8, device=dev)
+    _lib.check_tensor(q_fp8, "q_fp8", fp8, (B, HEADS, DIM), device=dev)
+    _lib.check_tensor(w, "w", torch.float32, (B, HEADS), device=dev)
+    _lib.check_tensor(k_scale, "k_scale", torch.float32, (B, Lmax), device=dev)
+    _lib.check_tensor(lens, "lens", torch.int32, (B,), device=dev)
     if out is None:
-        out = torch.empty((B, Lmax), dtype=torch.float32, device=k_cache.device)
+        out = torch.empty((B, Lmax), dtype=torch.float32, device=dev)
+    _lib.check_tensor(out, "out", torch.float32, (B, Lmax), device=dev)
     _lib.check(_lib.load().ess_indexer_logits_ex(
         q_fp8.data_ptr(), w.data_ptr(), k_cache.data_ptr(), k_scale.data_ptr(), lens.data_ptr(),
         B, Lmax, out.data_ptr(), max_ctas, _lib.stream_handle()), "ess_indexer_logits")
@@ -46,11 +56,12 @@ def topk(logits: torch.Tensor, lens: torch.Tensor, k: int = TOPK,
 
     Returns (idx [B, k] int32, count [B] int32) with count = min(k, lens)."""
     _lib.require_cuda(logits)
-    B, ld = logits.shape
+    B, ld = _check_topk_args(logits, lens, k)
     if out is None:
         out = torch.empty((B, k), dtype=torch.int32, device=logits.device)
     if count is None:
         count = torch.empty(B, dtype=torch.int32, device=logits.device)
+    _check_topk_out(out, count, B, k, logits.device)
     _lib.check(_lib.load().ess_topk(logits.data_ptr(), logits.stride(0), lens.data_ptr(), B, k,
                                     out.data_ptr(), out.stride(0), count.data_ptr(),
                                     _lib.stream_handle()), "ess_topk")
@@ -63,10 +74,34 @@ def topk_split(logits: torch.Tensor, lens: torch.Tensor, k: int, out: torch.Tens
     (ess_topk_split): selection ids into ``out``/``count``; hit rows, miss ids, staging
     rows and counts into ``acc`` (an AccessBatch of row slices)."""
     _lib.require_cuda(logits)
-    B, ld = logits.shape
+    B, ld = _check_topk_args(logits, lens, k)
+    _check_topk_out(out, count, B, k, logits.device)
+    for name in ("hit_row", "miss_ids", "miss_row"):
+        t = getattr(acc, name)
+        _lib.check_tensor(t, f"acc.{name}", torch.int32, (B, None), contiguous=False, device=logits.device)
+        if t.stride(1) != 1 or t.stride(0) != acc.miss_ids.stride(0) or t.shape[1] < k:
+            raise ValueError(f"acc.{name} rows must be unit-stride, share one row stride and hold k ids")
+    _lib.check_tensor(acc.counts, "acc.counts", torch.int32, (B, 4), device=logits.device)
     _lib.check(_lib.load().ess_topk_split(
         logits.data_ptr(), logits.stride(0), lens.data_ptr(), B, k, out.data_ptr(), out.stride(0),
         count.data_ptr(), pool.handle, begin, acc.hit_row.data_ptr(), acc.miss_ids.data_ptr(),
         acc.miss_row.data_ptr(), acc.counts.data_ptr(), acc.miss_ids.stride(0),
         _lib.stream_handle()), "ess_topk_split")
     return out, count
+
+
+def _check_topk_args(logits, lens, k):
+    if logits.dim() != 2 or logits.dtype != torch.float32 or logits.stride(1) != 1 or not logits.is_cuda:
+        raise ValueError("logits must be a CUDA float32 [B, ld] tensor with unit column stride")
+    B, ld = logits.shape
+    _lib.check_tensor(lens, "lens", torch.int32, (B,), device=logits.device)
+    if not 1 <= k <= 65535:
+        raise ValueError("k must be in [1, 65535]")
+    return B, ld
+
+
+def _check_topk_out(out, count, B, k, device):
+    _lib.check_tensor(out, "out", torch.int32, (B, None), contiguous=False, device=device)
+    if out.stride(1) != 1 or out.shape[1] < k:
+        raise ValueError("out must be int32 [B, >= k] with unit column stride")
+    _lib.check_tensor(count, "count", torch.int32, (B,), device=device)

@@ -60,12 +60,26 @@ def test_topk_sorted_rows(n):
         np.testing.assert_array_equal(idx[b, :cnt[b]], want)
 
 
-def test_topk_all_equal_row():
+@pytest.mark.parametrize("n", [40000, 40960, 65536, 131072, 200000])
+def test_topk_all_equal_row(n):
+    """Mass ties: every key equal, so the first k ids win (index asc).  Rows past 32K
+    equal keys once overflowed a signed packed (greater, equal) count and wrote ids
+    before the row; the output rows sit between sentinel guard rows that must survive."""
     from paper_2512_10576_b200.indexer import topk
-    logits = torch.zeros((2, 40000), device="cuda")
-    L = torch.tensor([40000, 39999], dtype=torch.int32, device="cuda")
-    idx, cnt = topk(logits, L, 2048)
-    assert (idx.cpu().numpy() == np.arange(2048)).all()
+    K, G = 2048, 4
+    logits = torch.zeros((3, n), device="cuda")
+    logits[2, n // 2:] = 1.0  # half the row tied above the rest
+    L = torch.tensor([n, n - 1, n], dtype=torch.int32, device="cuda")
+    buf = torch.full((G + 3 + G, K), -12345, dtype=torch.int32, device="cuda")
+    idx = buf[G:G + 3]
+    cnt = torch.empty(3, dtype=torch.int32, device="cuda")
+    topk(logits, L, K, out=idx, count=cnt)
+    torch.cuda.synchronize()
+    got = buf.cpu().numpy()
+    assert (got[:G] == -12345).all() and (got[G + 3:] == -12345).all(), "writes outside the output rows"
+    assert (got[G] == np.arange(K)).all() and (got[G + 1] == np.arange(K)).all()
+    assert (got[G + 2] == np.arange(n // 2, n // 2 + K)).all()
+    assert cnt.cpu().tolist() == [K, K, K]
 
 
 # ---------------------------------------------------------------------------- K1
@@ -122,10 +136,40 @@ def test_indexer_then_topk_exact_regime_end_to_end():
 
 # ---------------------------------------------------------------------------- K4
 def _fill_slots(pools, rows_u8_per_pool, count):
-    """Test setup: write the slot-store (f16) form of 656-B latent rows."""
+    """Test setup: write 656-B latent rows into the slot store in its format (the
+    dequantised f16 form, or the raw FP8 row when the store keeps 656-B rows)."""
     rv = pools.rows_view()
     for b, rows in enumerate(rows_u8_per_pool):
-        rv[b, :count].copy_(torch.as_tensor(dsa.slot_rows(rows.cpu().numpy()), device="cuda"))
+        if pools.row_bytes == 656:
+            rv[b, :count].copy_(rows[:count])
+        else:
+            rv[b, :count].copy_(torch.as_tensor(dsa.slot_rows(rows.cpu().numpy()), device="cuda"))
+
+
+def _slot_ref(q, rows_u8, sm):
+    """fp64 attention over the exact f16 operands K5 multiplies (dsa.slot_rows)."""
+    return dsa.sparse_mla_on_slot_rows(q, dsa.slot_rows(rows_u8), sm)
+
+
+def _bf16(x):
+    return torch.as_tensor(x).to(torch.bfloat16).float().numpy()
+
+
+# K5 tolerances against _slot_ref (same operands): the output is bf16 (relative
+# rounding <= 2^-9 per element, ~1.6e-3 rel-L2), P is rounded to f16 (2^-11).  So:
+# rel-L2 to the exact result <= 3e-3, and to the exact result ROUNDED to bf16 <= 1.2e-3
+# (away from rounding ties only K5's own f16-P / f32-sum error remains); lse to 1e-3.
+K5_REL = 3e-3
+K5_REL_BF16 = 1.2e-3
+K5_LSE = 1e-3
+
+
+def _check_k5(o, lse, ref_o, ref_l, what):
+    rel = np.linalg.norm(o - ref_o) / max(np.linalg.norm(ref_o), 1e-12)
+    relb = np.linalg.norm(o - _bf16(ref_o)) / max(np.linalg.norm(ref_o), 1e-12)
+    assert rel <= K5_REL, (what, "rel-L2", rel)
+    assert relb <= K5_REL_BF16, (what, "rel-L2 vs bf16(ref)", relb)
+    assert np.abs(lse - ref_l).max() <= K5_LSE + 1e-6 * np.abs(ref_l).max(), (what, "lse")
 
 
 @pytest.mark.parametrize("bulk", [False, True], ids=["ld16", "bulk"])
@@ -192,12 +236,79 @@ def test_sparse_mla_matches_oracle(counts, split):
     qf = q.float().cpu().numpy()
     for b, n in enumerate(counts):
         rows = lat[b].cpu().numpy()[sel[b, :n].cpu().numpy()]
+        ref_o, ref_l = _slot_ref(qf[b], rows, DEFAULT_SM_SCALE)
+        _check_k5(out[b], lse[b], ref_o, ref_l, (b, n, split))
+        # and against the unrounded dequantised rows (the end-to-end tolerance)
         ref_o, ref_l = dsa.sparse_mla(qf[b], rows, DEFAULT_SM_SCALE)
-        err = out[b] - ref_o
-        rel = np.linalg.norm(err) / max(np.linalg.norm(ref_o), 1e-12)
+        rel = np.linalg.norm(out[b] - ref_o) / max(np.linalg.norm(ref_o), 1e-12)
         assert rel <= 1e-2, (b, n, rel)
-        assert np.abs(err).max() <= 2e-2 * max(np.abs(ref_o).max(), 1e-6), (b, n)
-        assert np.abs(lse[b] - ref_l).max() <= 1e-2, (b, n)
+
+
+@pytest.mark.parametrize("n", [2048, 2047, 33, 1])
+def test_sparse_mla_counts_every_row_once(n):
+    """Exact row accounting: q = 0 makes every score 0, so the softmax is uniform and
+    out = (sum of the selected V rows) / n exactly.  Each slot row is one-hot in a
+    slot-dependent NoPE dim (value 1.0), so out[:, d] = (#selected rows hashed to d) / n
+    — a dropped, duplicated or wrong row changes some dim by 1/n: compared bit for bit
+    (for n = 2048 every count / n is exact in bf16)."""
+    from paper_2512_10576_b200.attention import sparse_mla
+    from paper_2512_10576_b200.cache import PoolSet
+    B, cap = 2, 4096
+    pools = PoolSet(B, 8192, cap, cap, row_bytes=_lib_slot_bytes())
+    dims = (np.arange(cap) * 37 + 11) % 512
+    rows = np.zeros((cap, 656), np.uint8)
+    rows[np.arange(cap), dims] = 0x38                               # e4m3 1.0
+    rows[:, 512:528] = np.ones((cap, 4), np.float32).view(np.uint8)  # scales 1.0
+    lat = [torch.as_tensor(rows, device="cuda")] * B
+    _fill_slots(pools, lat, cap)
+    g = torch.Generator(device="cuda").manual_seed(23)
+    sel = torch.stack([torch.randperm(cap, device="cuda", generator=g)[:2048] for _ in range(B)]).int()
+    cnt = torch.full((B,), n, dtype=torch.int32, device="cuda")
+    q = torch.zeros((B, 128, 576), dtype=torch.bfloat16, device="cuda")
+    out, lse = sparse_mla(pools, q, sel, cnt)
+    out, lse = out.float().cpu().numpy(), lse.cpu().numpy()
+    for b in range(B):
+        want = np.broadcast_to(np.bincount(dims[sel[b, :n].cpu().numpy()], minlength=512) / n, (128, 512))
+        if n == 2048:  # count / 2^11 is exact in bf16: bit for bit
+            np.testing.assert_array_equal(out[b], _bf16(want))
+        else:  # one bf16 ulp of double rounding allowed; one row more or less is >= 1/count
+            np.testing.assert_allclose(out[b], want, rtol=8e-3, atol=0)
+        np.testing.assert_allclose(lse[b], np.log(n), rtol=1e-6)
+    pools.close()
+
+
+def test_sparse_mla_dominant_row():
+    """One selected row outscores the rest by > 40 nats for every head, so the output is
+    that row's V (to bf16 rounding); a dropped or shifted row (the ring's first, last or
+    middle slot) would replace it with a blend of the others."""
+    from paper_2512_10576_b200.attention import sparse_mla
+    from paper_2512_10576_b200.cache import PoolSet
+    from paper_2512_10576_b200.decode import random_latent_rows
+    B, cap = 3, 4096
+    pools = PoolSet(B, 8192, cap, cap, row_bytes=_lib_slot_bytes())
+    g = torch.Generator(device="cuda").manual_seed(29)
+    lat = [random_latent_rows(cap, "cuda", g) for _ in range(B)]
+    _fill_slots(pools, lat, cap)
+    sel = torch.stack([torch.randperm(cap, device="cuda", generator=g)[:2048] for _ in range(B)]).int()
+    cnt = torch.full((B,), 2048, dtype=torch.int32, device="cuda")
+    pick = [0, 1023, 2047]  # position of the dominant row in the selection
+    q = torch.empty((B, 128, 576), dtype=torch.bfloat16, device="cuda")
+    for b in range(B):
+        k = torch.as_tensor(dsa.slot_rows(lat[b][sel[b, pick[b]]].cpu().numpy()[None])[0].astype(np.float32))
+        q[b] = (k / k.norm() * 600.0).to(torch.bfloat16).expand(128, -1)
+    out, lse = sparse_mla(pools, q, sel, cnt)
+    for b in range(B):
+        rows = lat[b].cpu().numpy()[sel[b].cpu().numpy()]
+        ref_o, ref_l = _slot_ref(q[b].float().cpu().numpy(), rows, 1.0 / 192 ** 0.5)
+        v = dsa.slot_rows(rows[pick[b]][None])[0, :512].astype(np.float32)
+        assert np.abs(ref_o - v).max() <= 1e-3 * np.abs(v).max()  # the setup is one-hot
+        _check_k5(out[b].float().cpu().numpy(), lse[b].cpu().numpy(), ref_o, ref_l, b)
+    pools.close()
+
+
+def _lib_slot_bytes():
+    from paper_2512_10576_b200 import _lib
+    return _lib.SLOT_ROW_BYTES
 
 
 def test_sparse_mla_rescale_path():
