@@ -43,10 +43,12 @@ def _e4m3(x: torch.Tensor) -> torch.Tensor:
 
 
 def random_latent_rows(n: int, device, gen=None) -> torch.Tensor:
-    """[n, 656] latent rows: e4m3 NoPE (values ~N(0,1)*32 quantised), positive
-    group scales ~1/32, bf16 RoPE ~N(0,1)."""
+    """[n, 656] latent rows in DeepSeek-V3.2's FP8 KV-cache format: e4m3 NoPE (values
+    ~N(0,1)*32 quantised), one power-of-two scale per 128-element group (2^-6..2^-4,
+    the UE8M0-style scales FlashMLA's FP8 sparse decode expects — it matches the oracle
+    only for those, profiles/r02_thirdparty_probe.json), bf16 RoPE ~N(0,1)."""
     nope = _e4m3(torch.randn((n, 512), device=device, generator=gen) * 32.0)
-    scales = (torch.rand((n, 4), device=device, generator=gen) * 0.5 + 0.75) / 32.0
+    scales = torch.exp2(torch.randint(-6, -3, (n, 4), device=device, generator=gen).float())
     rope = torch.randn((n, 64), device=device, generator=gen).to(torch.bfloat16)
     return torch.cat([nope, scales.view(torch.uint8), rope.view(torch.uint8)], dim=1)
 
