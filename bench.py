@@ -31,19 +31,19 @@ CONFIGS = {
     # micro / first: the DBA split (micro-batches, share of the first one), tuned per
     # workload on B200: a small first micro-batch starts the host-link
     # gather early; more micro-batches pay when the gather dominates (C4)
-    "c2": dict(batch=64, context_len=32768, sparse_ratio=0.25, micro=2, first=0.25,
+    "c2": dict(name="c2", batch=64, context_len=32768, sparse_ratio=0.25, micro=2, first=0.25,
                workload="C2: one DSA layer decode, batch 64/GPU, ctx 32K, 25% GPU slot pool"),
     # configs[3]: ctx 128K, batch 64/GPU, 10% slot pool
     # configs[2]: the full 61-layer attention path, global batch 128 over 8 GPUs = 16/GPU
-    "c3": dict(batch=16, context_len=32768, sparse_ratio=0.25, micro=1, first=None, layers=61,
+    "c3": dict(name="c3", batch=16, context_len=32768, sparse_ratio=0.25, micro=1, first=None, layers=61,
                workload="C3: 61-layer decode step (attention path), batch 16/GPU "
                         "(global 128 over 8 GPUs), ctx 32K, 25% GPU slot pool"),
     # configs[4]: mixed-length batch, context log-uniform over [8K, 128K] (seeded per rank);
     # the pool-size / hit-rate sweep is scripts/sweep_c5.py
-    "c5": dict(batch=64, context_len=(8192, 131072), sparse_ratio=0.25, micro=2, first=0.375,
+    "c5": dict(name="c5", batch=64, context_len=(8192, 131072), sparse_ratio=0.25, micro=2, first=0.375,
                workload="C5: one DSA layer decode, batch 64/GPU of mixed 8K-128K contexts "
                         "(log-uniform), 25% GPU slot pool"),
-    "c4": dict(batch=64, context_len=131072, sparse_ratio=0.10, micro=3, first=0.1875,
+    "c4": dict(name="c4", batch=64, context_len=131072, sparse_ratio=0.10, micro=3, first=0.1875,
                workload="C4: one DSA layer decode, batch 64/GPU, ctx 128K, 10% GPU slot pool"),
 }
 TOPK = 2048
@@ -287,10 +287,22 @@ def kernel_breakdown(layer, inputs, new_rows):
     from paper_2512_10576_b200.attention import sparse_mla
     from paper_2512_10576_b200.indexer import indexer_logits, topk
     from paper_2512_10576_b200.transfer import gather
+    from paper_2512_10576_b200.cache import AccessBatch
     names = ["indexer", "topk", "cache", "gather", "sparse_mla", "append"]
     ms = {n: 0.0 for n in names}
     counts = []
     acc = layer.acc  # preallocated step buffers (no allocation inside a timed region)
+    # link wake-up before each timed gather: 32 rows per pool that no step selects (ids
+    # at the end of the store, past every history) into the pool's staging rows — so the
+    # timed gather reads its own, cold miss list rather than re-reading warm rows
+    wake = None
+    if layer.pool.staging_rows >= 32:
+        B, d = layer.B, layer.device
+        ids = torch.arange(layer.Lmax - 32, layer.Lmax, dtype=torch.int32, device=d).repeat(B, 1)
+        rows = torch.arange(layer.pool.cap_max, layer.pool.cap_max + 32, dtype=torch.int32, device=d).repeat(B, 1)
+        cnt = torch.zeros((B, 4), dtype=torch.int32, device=d)
+        cnt[:, 1] = 32
+        wake = AccessBatch(cnt, None, ids.contiguous(), rows.contiguous())
 
     def timed(name, fn, warm=None):
         torch.cuda._sleep(2_000_000)
@@ -308,10 +320,9 @@ def kernel_breakdown(layer, inputs, new_rows):
                                                 layer.lens, out=layer.logits))
         timed("topk", lambda: topk(layer.logits, layer.lens, layer.K, out=layer.idx, count=layer.cnt))
         acc = timed("cache", lambda: layer.pool.access(layer.idx, layer.cnt, out=acc))
-        # the gather is idempotent (same rows into the same slots): re-running it first
-        # keeps the measurement off the idle host link's wake-up
         g = lambda: gather(layer.pool, layer.store, acc, max_ctas=layer.gather_ctas)  # noqa: E731
-        timed("gather", g, warm=g)
+        w = (lambda: gather(layer.pool, layer.store, wake, max_ctas=layer.gather_ctas)) if wake else None
+        timed("gather", g, warm=w)
         timed("sparse_mla", lambda: sparse_mla(layer.pool, q, acc.sel_row, layer.cnt, layer.sm_scale,
                                                out=layer.out, lse=layer.lse))
         timed("append", lambda: layer._append_device(new_rows[t]))  # the graph's device-side append
@@ -319,18 +330,24 @@ def kernel_breakdown(layer, inputs, new_rows):
     torch.cuda.synchronize()
     for name, e0, e1 in timed.ev:
         ms[name] += e0.elapsed_time(e1) / len(inputs)
-    return ms, torch.stack(counts)
+    return ms, torch.stack(counts), q
 
 
 def product_layer(cfg, dev, steps, drift=0.97, rank=0, micro=None, first=None, gather_ctas=32,
-                  record=False):
+                  record=False, world=1):
     """The benchmarked product layer of a single-layer config, set up exactly as the timed
-    run uses it (the parity tests at the benchmarked shapes build it through here):
-    per-request lengths, pools at floor(rho * history), the DBA micro-batch split and the
+    run uses it (the parity tests at the benchmarked shapes build it through here): this
+    rank's share of the global request set (dp.shard_requests: round-robin, LPT by length
+    for mixed batches), pools at floor(rho * history), the DBA micro-batch split and the
     32-window prefill warm-up.  Returns (layer, lens, windows or None)."""
     from paper_2512_10576_b200.decode import DSADecodeLayer
-    B, rho = cfg["batch"], cfg["sparse_ratio"]
-    lens = request_lengths(cfg, B, seed=rank)
+    from paper_2512_10576_b200.dp import shard_requests
+    rho = cfg["sparse_ratio"]
+    glob = request_lengths(cfg, cfg["batch"] * world, seed=0)
+    mixed = not isinstance(cfg["context_len"], int)
+    mine = shard_requests(len(glob), world, rank, glob if mixed else None)
+    lens = [glob[i] for i in mine]
+    B = len(lens)
     L = lens if not isinstance(cfg["context_len"], int) else cfg["context_len"]
     layer = DSADecodeLayer(B, L, rho, TOPK, max_new_tokens=steps + 16, device=dev,
                            seed=1234 + rank, drift=drift)
@@ -341,30 +358,92 @@ def product_layer(cfg, dev, steps, drift=0.97, rank=0, micro=None, first=None, g
     return layer, lens, (windows if record else None)
 
 
-def run_ours(args, cfg):
+def host_info(bound_node):
+    """CPU model, NUMA layout and the GPU's node (BASELINE.md §3 asks for them beside
+    the CPU baseline; SURVEY §8e's one-NUMA-local-host-pool-per-GPU placement)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        nodes = len([d for d in os.listdir("/sys/devices/system/node") if d.startswith("node")])
+    except OSError:
+        nodes = None
+    return {"cpu_model": model, "cpus": os.cpu_count(), "numa_nodes": nodes, "gpu_numa_node": bound_node}
+
+
+def selection_similarity(layer, inputs, new_rows, steps=4):
+    """Eq. (1) step-to-step overlap r (offsim trace.py:164-177, |K_{t-1} & K_t| / |K_t|) of
+    the product layer's live K2 selections over a few extra (untimed) steps, averaged over
+    requests and step pairs."""
+    import numpy as np
+    prev, rs = None, []
+    for t in range(steps):
+        layer.step(inputs[t][0], inputs[t][1], new_rows[t])
+        idx, cnt = layer.idx.cpu().numpy(), layer.cnt.cpu().numpy()
+        cur = [idx[b, :cnt[b]] for b in range(layer.B)]
+        if prev is not None:
+            rs += [len(np.intersect1d(p, c, assume_unique=True)) / len(c) for p, c in zip(prev, cur) if len(c)]
+        prev = cur
+    return float(np.mean(rs))
+
+
+def flashmla_bar(layer, q, sel_row, counts, k5_ms):
+    """The speed bar for K5: FlashMLA's sm100 FP8 sparse decode (DeepSeek's V3.2 DSA kernel,
+    vLLM's build) over the same number of requests / selected rows / slot indices, its 656-B
+    rows in one HBM cache of the pool's size.  Returns (us, K5 speed-up) or None."""
+    import torch
+    sys.path.insert(0, os.path.join(ROOT, "scripts"))
+    try:
+        import thirdparty as tp
+        if not tp.flashmla_available():
+            return None
+        B, rows = layer.B, layer.pool.rows_per_pool
+        cache = torch.randint(0, 120, (B * rows, 656), dtype=torch.uint8, device=layer.device)
+        cache[:, 512:528] = torch.full((B * rows, 4), 2.0 ** -5, device=layer.device).view(torch.uint8)
+        n = counts.clone()
+        kp = (int(n.max()) + 63) // 64 * 64
+        idx = (sel_row[:, :kp].clamp(0, rows - 1) + torch.arange(B, device=layer.device).view(B, 1) * rows)
+        idx = idx.int().contiguous()
+        _, _, meta = tp.flashmla_sparse_decode(q, cache, idx, layer.sm_scale, lengths=n)
+        for _ in range(3):
+            tp.flashmla_sparse_decode(q, cache, idx, layer.sm_scale, lengths=n, meta=meta)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(2_000_000)
+        e0.record()
+        for _ in range(10):
+            tp.flashmla_sparse_decode(q, cache, idx, layer.sm_scale, lengths=n, meta=meta)
+        e1.record()
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) / 10 * 1e3
+        del cache
+        return {"flashmla_us": us, "k5_us": k5_ms * 1e3, "k5_speedup_vs_flashmla": us / (k5_ms * 1e3)}
+    except Exception as e:  # comparator unavailable: say so, never fail the bench
+        return {"error": repr(e)[:200]}
+
+
+def measure(args, cfg, dev, rank, world, agg_dev, drift, full, peaks, peak_kind, link_peak=None):
+    """One single-layer workload: the product step (graph replays, device clock) and, when
+    ``full``, the per-kernel breakdown (K1 roofline, cold-list gather GB/s, K5 vs FlashMLA),
+    the Eq. (1) similarity and the e2e host-buffer run.  Returns (record, layer-free)."""
     import torch
     import torch.distributed as dist
     from paper_2512_10576_b200.decode import random_latent_rows
     from paper_2512_10576_b200.dp import aggregate
 
-    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    dev, agg_dev = init_ranks(local, world)
-    # launch loop and pinned staging on the GPU's NUMA node (ESS_BIND_NUMA=0: off);
-    # the CPU baseline below gets the full affinity back
-    from paper_2512_10576_b200.transfer import bind_to_gpu_node
-    prev_aff, bound_node = bind_to_gpu_node(dev) if os.environ.get("ESS_BIND_NUMA", "1") == "1" else (None, None)
-    peaks, peak_kind = measured_peaks()
-    B, rho = cfg["batch"], cfg["sparse_ratio"]
     W, K, NB = args.warmup, args.steps, args.breakdown_steps
-    total = W + K + NB
-    layer, lens, _ = product_layer(cfg, dev, total + K, drift=args.drift, rank=rank, micro=args.micro,
-                                   first=args.first, gather_ctas=args.gather_ctas)
-    L = lens if not isinstance(cfg["context_len"], int) else cfg["context_len"]
+    total = W + K + NB + 4
+    layer, lens, _ = product_layer(cfg, dev, total + K, drift=drift, rank=rank, micro=args.micro,
+                                   first=args.first, gather_ctas=args.gather_ctas, world=world)
+    B = layer.B
     inputs = [layer.next_queries() for _ in range(total)]
     new_rows = [random_latent_rows(B, dev, layer.gen).view(B, 1, 656) for _ in range(total)]
     torch.cuda.synchronize()
-
     # warm-up (untimed): capture the whole step as one CUDA graph (its first, eager
     # execution is a real step), then W-1 graph replays
     layer.capture(args.overlap, args.gather_ctas)
@@ -388,106 +467,154 @@ def run_ours(args, cfg):
     step_ms = start.elapsed_time(end) / K
     layer.pool.check("bench")
     tokens_total, t_max = aggregate(B * K, step_ms * K / 1e3, device=agg_dev)
-    value = tokens_total / t_max
     hits, misses = (x - y for x, y in zip(layer.access_totals(), (hits0, misses0)))
-
-    gpu_launches = layer.launches_per_step(args.overlap) * K
-    if args.quick:  # schedule sweeps: the device-timed product steps only
+    rec = {"value": tokens_total / t_max, "unit": "tokens/s", "ms_per_step": t_max * 1e3 / K,
+           "batch_per_gpu": B, "query_drift": drift, "hit_rate": hits / max(1, hits + misses),
+           "misses_per_request_step": misses / (B * K), "clocks": clocks.summary(),
+           "gpu_launches": layer.launches_per_step(args.overlap) * K,
+           "micro_batches": layer.micro_batches(layer.micro) if args.overlap == "dba" else [(0, B)],
+           "context_len": cfg["context_len"] if isinstance(cfg["context_len"], int)
+           else "mixed {}-{} log-uniform, mean {:.0f}".format(*cfg["context_len"], sum(lens) / B)}
+    # Eq. (1) selection similarity r over 4 more (untimed) steps
+    rec["similarity_r"] = selection_similarity(layer, inputs[W + K:W + K + 4], new_rows[W + K:W + K + 4])
+    if args.quick or not full:
         layer.close()
+        return rec
+    # per-kernel breakdown (sequential, separate steps) for the roofline
+    ktimes, bcounts, bq = kernel_breakdown(layer, inputs[W + K + 4:W + K + 4 + NB],
+                                           new_rows[W + K + 4:W + K + 4 + NB])
+    lens_mean = sum(lens) / B + W + K + 4 + (NB - 1) / 2
+    idx_bytes = B * lens_mean * (132 + 4) + B * (64 * 128 + 64 * 4)
+    achieved = idx_bytes / (ktimes["indexer"] * 1e-3) / 1e9
+    gather_bytes = bcounts[:, :, 1].sum().item() * 656 / NB
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"traffic_{cfg['name']}.json")
+    if os.path.exists(tfile):
+        with open(tfile) as f:
+            traffic = json.load(f).get("indexer_dram_bytes_per_launch")
+    gather_gbs = gather_bytes / (ktimes["gather"] * 1e-3) / 1e9 if ktimes["gather"] else None
+    rec["kernels_ms"] = ktimes
+    rec["roofline"] = {"bound": "hbm", "kernel": "indexer (K1)", "achieved": achieved,
+                       "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                       "traffic": traffic, "peak_kind": peak_kind,
+                       "algorithmic_bytes_per_launch": idx_bytes}
+    k5_flop = 2 * 128 * (576 + 512) * bcounts[:, :, :2].sum().item() / NB
+    rec["k5"] = {"tflops": k5_flop / (ktimes["sparse_mla"] * 1e-3) / 1e12,
+                 "frac_of_bf16_peak": k5_flop / (ktimes["sparse_mla"] * 1e-3) / 1e12 / peaks["bf16_tflops"],
+                 "bar": flashmla_bar(layer, bq, layer.acc.sel_row, layer.cnt, ktimes["sparse_mla"])}
+    # useful bytes = 656 per miss; on the link each 64-B-aligned row (704-B host pitch)
+    # moves as 11 64-B read completions = 704 B.  Timed on the step's own (cold) miss list.
+    rec["gather"] = {"bytes_per_step": gather_bytes, "gbs": gather_gbs,
+                     "host_link_peak_gbs": link_peak,
+                     "frac_of_link_peak": gather_gbs / link_peak if gather_gbs and link_peak else None,
+                     "link_bytes_per_row": LINK_ROW_BYTES,
+                     "link_gbs": gather_gbs * LINK_ROW_BYTES / 656 if gather_gbs else None,
+                     "link_frac_of_link_peak": (gather_gbs * LINK_ROW_BYTES / 656 / link_peak
+                                                if gather_gbs and link_peak else None),
+                     "miss_list": "cold: the breakdown step's own misses, after a gather of other rows",
+                     "paper_flashtrans_gbs": 37.0}
+    # e2e: through the public API with host buffers: every step copies its queries H2D
+    # from pinned memory and its attention output D2H (layer.step_host: copy stream,
+    # double-buffered staging, so transfers of step t overlap compute of t-1 / t+1)
+    if args.e2e:
+        h_in = [(qi.cpu().pin_memory(), q.cpu().pin_memory()) for qi, q in inputs[W:W + K]]
+        h_out = [torch.empty(layer.out.shape, dtype=layer.out.dtype).pin_memory() for _ in range(K)]
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for t in range(K):
+            layer.step_host(h_in[t][0], h_in[t][1], new_rows[W + t], h_out[t])
+        layer._ds.synchronize()
+        e1.record()
+        torch.cuda.synchronize()
+        e2e_ms = e0.elapsed_time(e1) / K
+        e2e_tok, e2e_t = aggregate(B * K, e2e_ms * K / 1e3, device=agg_dev)
+        rec["e2e"] = {"value": e2e_tok / e2e_t, "unit": "tokens/s",
+                      "h2d_bytes_per_step": h_in[0][0].numel() + h_in[0][1].numel() * 2,
+                      "d2h_bytes_per_step": h_out[0].numel() * 2}
+    layer.close()
+    return rec
+
+
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev, agg_dev = init_ranks(local, world)
+    # launch loop and pinned staging on the GPU's NUMA node (ESS_BIND_NUMA=0: off);
+    # the CPU baseline below gets the full affinity back
+    from paper_2512_10576_b200.transfer import bind_to_gpu_node
+    prev_aff, bound_node = bind_to_gpu_node(dev) if os.environ.get("ESS_BIND_NUMA", "1") == "1" else (None, None)
+    peaks, peak_kind = measured_peaks()
+    link_peak = host_link_peak_gbs(dev)
+    main = measure(args, cfg, dev, rank, world, agg_dev, args.drift, True, peaks, peak_kind, link_peak)
+    if args.quick:
         if rank == 0:
-            print(json.dumps({"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
-                              "ms_per_step": t_max * 1e3 / K, "quick": True,
+            print(json.dumps({"metric": METRIC, "value": main["value"], "unit": "tokens/s", "n_gpus": world,
+                              "ms_per_step": main["ms_per_step"], "quick": True,
                               "micro_batches": args.micro, "first": args.first,
-                              "hit_rate": hits / max(1, hits + misses)}), flush=True)
+                              "hit_rate": main["hit_rate"], "similarity_r": main["similarity_r"]}), flush=True)
         if world > 1:
             dist.barrier()
             dist.destroy_process_group()
         return
-    # per-kernel breakdown (sequential, separate steps) for the roofline
-    ktimes, bcounts = kernel_breakdown(layer, inputs[W + K:], new_rows[W + K:])
-    lens_mean = sum(lens) / B + W + K + (NB - 1) / 2
-    idx_bytes = B * lens_mean * (132 + 4) + B * (64 * 128 + 64 * 4)
-    achieved = idx_bytes / (ktimes["indexer"] * 1e-3) / 1e9
-    gather_bytes = bcounts[:, :, 1].sum().item() * 656 / NB
-    link_peak = host_link_peak_gbs(dev) if rank == 0 else None
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
-    if os.path.exists(tfile):
-        with open(tfile) as f:
-            traffic = json.load(f).get("indexer_dram_bytes_per_launch")
-
-    # e2e: through the public API with host buffers: every step copies its queries H2D
-    # from pinned memory and its attention output D2H (layer.step_host: copy stream,
-    # double-buffered staging, so transfers of step t overlap compute of t-1 / t+1)
-    h_in = [(qi.cpu().pin_memory(), q.cpu().pin_memory()) for qi, q in inputs[W:W + K]]
-    h_out = [torch.empty(layer.out.shape, dtype=layer.out.dtype).pin_memory() for _ in range(K)]
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for t in range(K):
-        layer.step_host(h_in[t][0], h_in[t][1], new_rows[W + t], h_out[t])
-    layer._ds.synchronize()
-    e1.record()
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / K
-    e2e_tok, e2e_t = aggregate(B * K, e2e_ms * K / 1e3, device=agg_dev)
-    h2d = h_in[0][0].numel() + h_in[0][1].numel() * 2
-    d2h = h_out[0].numel() * 2
-
-    gather_gbs = gather_bytes / (ktimes["gather"] * 1e-3) / 1e9 if ktimes["gather"] else None
-    line = None
+    ceiling = run_ceiling(args, cfg, dev) if (args.ceiling and world == 1) else None
+    subs = {}
+    if args.sub and world == 1:
+        # the metric's other half (128K, BASELINE configs[3]) and a lower-locality row
+        c4 = dict(CONFIGS["c4"])
+        a4 = argparse.Namespace(**{**vars(args), "micro": c4["micro"], "first": c4["first"], "e2e": False})
+        subs["c4"] = measure(a4, c4, dev, rank, world, agg_dev, args.drift, True, peaks, peak_kind, link_peak)
+        if args.ceiling:
+            subs["c4"]["all_hbm_ceiling"] = run_ceiling(a4, c4, dev)
+            subs["c4"]["all_hbm_ceiling"]["frac_of_ceiling"] = (
+                subs["c4"]["value"] / subs["c4"]["all_hbm_ceiling"]["value"])
+        lo = argparse.Namespace(**{**vars(args), "e2e": False})
+        subs[f"{cfg['name']}_drift_0.9"] = measure(lo, cfg, dev, rank, world, agg_dev, 0.9, False, peaks,
+                                                   peak_kind, link_peak)
+        if ceiling:
+            r = subs[f"{cfg['name']}_drift_0.9"]
+            r["frac_of_ceiling"] = r["value"] / ceiling["value"]
     if prev_aff is not None:
         os.sched_setaffinity(0, prev_aff)
+    line = None
     if rank == 0:
         cpu_v, cpu_sample, cpu_threads = cpu_reference_rate(cfg, budget_s=12.0)
         _cpu_pool_close()
         line = {
-            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
-            "steps": K, "warmup": W, "ms_per_step": t_max * 1e3 / K,
+            "metric": METRIC, "value": main["value"], "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": main["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "e4m3/f16/f32",
             "data": "synthetic (random-weight DeepSeek-V3.2-Exp DSA shapes, drifting queries)",
-            "config": {"workload": cfg["workload"], "layers": 1, "batch_per_gpu": B,
-                       "context_len": L if isinstance(L, int)
-                       else "mixed {}-{} log-uniform, mean {:.0f}".format(*cfg["context_len"], sum(lens) / B),
-                       "sparse_ratio": rho, "topk": TOPK, "query_drift": args.drift,
-                       "overlap": args.overlap,
-                       "micro_batches": args.micro if args.overlap == "dba" else 1,
-                       "first_micro_batch_share": args.first if args.overlap == "dba" else None,
-                       "parallelism": f"dp{world} (requests sharded, no collective)",
+            "config": {"workload": cfg["workload"], "layers": 1, "batch_per_gpu": main["batch_per_gpu"],
+                       "context_len": main["context_len"], "sparse_ratio": cfg["sparse_ratio"],
+                       "topk": TOPK, "query_drift": args.drift, "overlap": args.overlap,
+                       "micro_batches": main["micro_batches"],
+                       "parallelism": f"dp{world} (requests sharded by dp.shard_requests, no collective)",
                        "l2": "inputs larger than L2 (indexer keys + slot pool > 600 MB/GPU)",
-                       "host_numa_node": bound_node},
-            "e2e": {"value": e2e_tok / e2e_t, "unit": "tokens/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h},
-            "roofline": {"bound": "hbm", "kernel": "indexer (K1)", "achieved": achieved,
-                         "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                         "traffic": traffic, "peak_kind": peak_kind,
-                         "algorithmic_bytes_per_launch": idx_bytes},
+                       "host": host_info(bound_node)},
+            "e2e": main.get("e2e"),
+            "roofline": main["roofline"],
             "cpu_baseline": {"value": cpu_v, "unit": "tokens/s", "cores": cpu_threads, "kind": "port",
                              "sample": cpu_sample},
-            # our kernels per step: K1, K2, K3, K4 per micro-batch + fused K5 + admission
             # this library's kernels per step (graph kernel nodes; DSADecodeLayer.launches_per_step)
-            "gpu_launches": gpu_launches,
+            "gpu_launches": main["gpu_launches"],
             "cuda_graph": True,
-            "clocks": clocks.summary(),
-            "kernels_ms": ktimes,
-            # useful bytes = 656 per miss; on the link each 64-B-aligned row (704-B host
-            # pitch) moves as 11 64-B read completions = 704 B
-            "gather": {"bytes_per_step": gather_bytes,
-                       "gbs": gather_gbs,
-                       "link_bytes_per_row": LINK_ROW_BYTES,
-                       "link_gbs": gather_gbs * LINK_ROW_BYTES / 656 if gather_gbs else None,
-                       "host_link_peak_gbs": link_peak,
-                       "frac_of_link_peak": (gather_gbs * LINK_ROW_BYTES / 656 / link_peak
-                                             if gather_gbs and link_peak else None),
-                       "paper_flashtrans_gbs": 37.0},
-            "hit_rate": hits / max(1, hits + misses),
-            "misses_per_request_step": misses / (B * K),
+            "clocks": main["clocks"],
+            "kernels_ms": main["kernels_ms"],
+            "k5": main["k5"],
+            "gather": main["gather"],
+            "hit_rate": main["hit_rate"],
+            "misses_per_request_step": main["misses_per_request_step"],
+            "similarity_r": main["similarity_r"],
         }
-    if args.ceiling and world == 1:
-        line["all_hbm_ceiling"] = run_ceiling(args, cfg, dev)
-        line["all_hbm_ceiling"]["frac_of_ceiling"] = value / line["all_hbm_ceiling"]["value"]
-    layer.close()
-    if rank == 0:
+        if ceiling:
+            line["all_hbm_ceiling"] = ceiling
+            line["all_hbm_ceiling"]["frac_of_ceiling"] = main["value"] / ceiling["value"]
+        if subs:
+            line["sub"] = subs
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -616,6 +743,9 @@ def main():
                     help="schedule sweeps: skip the CPU baseline, e2e and per-kernel breakdown")
     ap.add_argument("--breakdown-steps", type=int, default=5)
     ap.add_argument("--no-ceiling", dest="ceiling", action="store_false")
+    ap.add_argument("--no-sub", dest="sub", action="store_false",
+                    help="skip the sub-records (C4 at 128K + its ceiling, drift 0.9); N=1 only")
+    ap.add_argument("--no-e2e", dest="e2e", action="store_false")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")

@@ -16,9 +16,12 @@
  *   latent row   656 B = [0,512) e4m3 NoPE | [512,528) 4 x f32 group scales |
  *                [528,656) 64 x bf16 RoPE          (scenario.py:25, costmodel.py:31)
  *                — the host store and every H2D/D2H transfer use this format
- *   slot row     1152 B = 576 x f16: dequantised NoPE (e4m3 x scale) ++ RoPE; the
- *                GPU slot store holds attention-ready rows, dequantised once when
- *                a row is admitted (gather / write-back), never per step
+ *   slot row     one of two formats, chosen per pool set at ess_pool_create:
+ *                656 B  (ESS_SLOT_ROW_BYTES_FP8) the latent row itself — the slot store
+ *                       costs exactly the latent bytes it caches; K5 dequantises in
+ *                       shared memory (FP8 sparse MLA on a cta_group::2 CTA pair)
+ *                1152 B (ESS_SLOT_ROW_BYTES) 576 x f16: dequantised NoPE (e4m3 x scale)
+ *                       ++ RoPE, dequantised once on admission
  *   indexer key  128 B e4m3 + f32 scale per token (separate arrays)
  *                                                   (scenario.py:26, :30-33)
  *   pools        P = layers x requests independent LRU pools, pool id = l*B + b
@@ -42,7 +45,8 @@ extern "C" {
 #ifndef ESS_HOST_ROW_PITCH  /* scratch builds may override (A/B of the host layout) */
 #define ESS_HOST_ROW_PITCH 704
 #endif
-#define ESS_SLOT_ROW_BYTES 1152 /* 576 x f16 */
+#define ESS_SLOT_ROW_BYTES 1152 /* 576 x f16: the dequantised slot format */
+#define ESS_SLOT_ROW_BYTES_FP8 656 /* the raw latent row as the slot format (K5 dequantises on chip) */
 #define ESS_NOPE_DIM 512
 #define ESS_ROPE_DIM 64
 #define ESS_INDEXER_HEADS 64
@@ -91,7 +95,8 @@ int ess_timestamp(uint64_t *d_dst, void *stream);
 
 /* ---- K3 cache manager: replaces offsim.cache.SparsePool (cache.py:29-134) ------ */
 /* num_pools pools over ids [0, max_ids), each with up to cap_max slots.  When
- * row_bytes == ESS_SLOT_ROW_BYTES the pool also owns its GPU slot store: per pool
+ * row_bytes is ESS_SLOT_ROW_BYTES_FP8 or ESS_SLOT_ROW_BYTES the pool also owns its GPU
+ * slot store in that format: per pool
  * cap_max slot rows + staging_rows transient rows (oversize requests,
  * cache.py:103-111).  row_bytes == 0: bookkeeping only (replay). */
 int ess_pool_create(ess_pool **out, int32_t num_pools, int64_t max_ids, int32_t cap_max,

@@ -70,7 +70,12 @@ LATENT_ROW_BYTES = 656   # host store / transfer format (e4m3 NoPE + scales + bf
 # host store row pitch (64-B aligned rows; ESS_HOST_ROW_PITCH); the env override pairs with
 # a scratch library built with the same -DESS_HOST_ROW_PITCH
 HOST_ROW_PITCH = int(os.environ.get("ESS_HOST_ROW_PITCH", "704"))
-SLOT_ROW_BYTES = 1152    # GPU slot store format (576 x f16, dequantised on admission)
+# GPU slot store formats (include/ess_b200.h): the raw 656-B latent row, dequantised in
+# shared memory by the CTA-pair FP8 K5 (mla2.cu), or 576 x f16 dequantised on admission
+# (mla.cu).  ESS_SLOT_FORMAT picks the decode layer's default.
+SLOT_ROW_BYTES_FP8, SLOT_ROW_BYTES_F16 = 656, 1152
+SLOT_FORMATS = {"fp8": SLOT_ROW_BYTES_FP8, "f16": SLOT_ROW_BYTES_F16}
+SLOT_ROW_BYTES = SLOT_FORMATS[os.environ.get("ESS_SLOT_FORMAT", "f16")]
 
 _lib = None
 

@@ -218,13 +218,16 @@ class PoolSet:
         return p.value or 0
 
     def rows_view(self) -> torch.Tensor:
-        """The slot store as a [P, rows_per_pool, 576] float16 tensor (aliasing view):
-        dequantised NoPE (512) ++ RoPE (64) per slot row."""
+        """The slot store as an aliasing view: [P, rows_per_pool, 656] uint8 raw latent rows
+        (FP8 slot format), or [P, rows_per_pool, 576] float16 dequantised NoPE (512) ++
+        RoPE (64) rows (f16 slot format)."""
         if not self.row_bytes:
             raise ValueError("pool set has no slot store")
         n = self.num_pools * self.rows_per_pool * self.row_bytes
-        return _wrap_device(self.rows_ptr(), n, self.device, self).view(torch.float16).view(
-            self.num_pools, self.rows_per_pool, self.row_bytes // 2)
+        raw = _wrap_device(self.rows_ptr(), n, self.device, self)
+        if self.row_bytes == _lib.SLOT_ROW_BYTES_FP8:
+            return raw.view(self.num_pools, self.rows_per_pool, self.row_bytes)
+        return raw.view(torch.float16).view(self.num_pools, self.rows_per_pool, self.row_bytes // 2)
 
     def status(self) -> int:
         st = ctypes.c_int32(0)

@@ -713,6 +713,12 @@ __global__ void __launch_bounds__(128) mla_combine_kernel(const float *__restric
 
 }  // namespace
 
+int ess_launch_mla_fp8(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_t *d_sel_row,
+                       const int32_t *d_sel2, int32_t *d_landed, int32_t sel_stride,
+                       const int32_t *d_count, int32_t count_stride, int32_t batch, float sm_scale,
+                       void *d_out, float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags,
+                       int32_t nsplit, void *stream);  // mla2.cu
+
 namespace {
 
 int launch_mla(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_t *d_sel_row,
@@ -720,6 +726,18 @@ int launch_mla(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_
                const int32_t *d_count, int32_t count_stride, int32_t batch, float sm_scale,
                void *d_out, float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags,
                int32_t nsplit, void *stream) {
+  if (pool->row_bytes == ESS_SLOT_ROW_BYTES_FP8) {  // raw-row slots: the CTA-pair FP8 kernel
+    int rc = ess_launch_mla_fp8(pool, pool_begin, d_q, d_sel_row, d_sel2, d_landed, sel_stride, d_count,
+                                count_stride, batch, sm_scale, d_out, d_lse, d_ws_o, d_ws_ml, flags, nsplit,
+                                stream);
+    if (rc != ESS_OK) return rc;
+    if (nsplit > 1) {
+      mla_combine_kernel<<<dim3(batch, HEADS / 4), 128, 0, (cudaStream_t)stream>>>(
+          d_ws_o, d_ws_ml, nsplit, (uint16_t *)d_out, d_lse);
+      ESS_CUDA_TRY(cudaGetLastError());
+    }
+    return ESS_OK;
+  }
   // q as a [batch * 128 heads][576] bf16 tensor, boxes of [128 heads][64 dims], SW128
   struct QMap {
     const void *base = nullptr;
@@ -753,7 +771,8 @@ int launch_mla(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_
 }
 
 bool pool_ok(ess_pool *pool, int32_t pool_begin, int32_t batch) {
-  return pool && pool->rows && pool->row_bytes == ESS_SLOT_ROW_BYTES && batch >= 0 &&
+  return pool && pool->rows &&
+         (pool->row_bytes == ESS_SLOT_ROW_BYTES || pool->row_bytes == ESS_SLOT_ROW_BYTES_FP8) && batch >= 0 &&
          pool_begin >= 0 && (int64_t)pool_begin + batch <= pool->P;
 }
 

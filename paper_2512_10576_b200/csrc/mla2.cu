@@ -1,0 +1,666 @@
+// K5, FP8 slot rows: sparse MLA decode over 656-B latent rows (op "sparse_mla",
+// costmodel.py:18-27) on a CTA pair with cta_group::2 MMAs.
+//
+// Why a second K5.  The f16-slot kernel (mla.cu) runs a request on two CTAs that each
+// own 256 output dims and BOTH compute the full 128-head score tile (1.53x the
+// algorithmic MMA work), and it reads 1152-B dequantised rows (1.76x the 656-B wire
+// bytes; the slot store costs 1.76x the latent bytes it caches).  Here:
+//   * the slot store keeps the raw 656-B row (512 e4m3 NoPE, 4 f32 group scales,
+//     64 bf16 RoPE, scenario.py:25) — a 25% pool costs 25% of the latent bytes — and
+//     the kernel dequantises in shared memory: f16(e4m3) x f16(scale) in one HMUL2
+//     (exact for the power-of-two group scales of DeepSeek-V3.2's FP8 cache; for other
+//     scales one f16 rounding of the scale, < 1 f16 ulp from oracle.dsa.slot_rows);
+//   * the pair splits the HEADS (CTA r owns heads 64r..64r+63) and every MMA is
+//     cta_group::2 with M = 128: S = Q K^T has each CTA supply its 64 q rows and half
+//     of the tile's 32 K rows (N = 32), so each score is computed once; O += P V has
+//     each CTA supply its 64 P rows and half of each 256-dim V block (N = 256, two
+//     instructions for 512 dims).  Per-SM tensor work is the algorithmic 285 MFLOP per
+//     request instead of 436.
+//
+// TMEM per CTA (cta_group::2 "2x2" layout: a 64 x N accumulator spans 128 lanes x N/2
+// columns, lanes 64..127 holding columns N/2..N-1):
+//   O   [0,256)    two 64 x 256 accumulators (dims 0..255, 256..511)
+//   S   [256,320)  four 64 x 32 score buffers (16 columns each): S(i+3) issues before PV(i)
+//   Q   [320,512)  q dims 0..383 as f16 pairs, duplicated over both lane halves (the
+//                  A-from-TMEM layout of cta_group::2)
+// Thread t of the softmax warps owns head 64r + t%64 and tile tokens [16u, 16u+16),
+// u = t/64; the pair's two threads of a head exchange their tile max through shared
+// memory.  Shared memory per CTA: q dims 384..575 (3 SW128 blocks), a 3-deep staging
+// ring of raw rows (own 16 rows whole + the other 16 rows' V bytes of this CTA's dims),
+// 3 S tiles [16 rows][576] and 4 V tiles [32 rows][256 dims] in SW128 f16, 4 P tiles
+// [64 heads][32 tokens].
+//
+// Warp roles (320 threads): w0-3 softmax + epilogue, w4 TMEM alloc + MMA issue (rank 0
+// only issues), w5 row loader (cp.async.bulk per row / row part), w6-9 dequantisers.
+// The rank-0 CTA's barriers gate the MMAs: the peer's dequantisers and softmax warps
+// arrive on them remotely; MMA completion is multicast to both CTAs' barriers.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+
+namespace {
+
+constexpr int HEADS = ESS_MLA_HEADS;   // 128 = M of every MMA (64 per CTA)
+constexpr int HH = HEADS / 2;          // heads per CTA
+constexpr int NB = 32;                 // tokens per tile (N of S)
+constexpr int NH = NB / 2;             // tokens per CTA half
+constexpr int NBLK = ESS_MLA_QK_DIM / 64;  // 9 dim-blocks of 64
+constexpr int QT_BLKS = 6;             // q blocks in TMEM (dims 0..383)
+constexpr int QS_BLKS = NBLK - QT_BLKS;    // 3 in shared memory (384..575)
+constexpr int NSB = 4;                 // TMEM S buffers / P tiles
+constexpr int LOOKAHEAD = NSB - 1;     // S(i+3) issues before PV(i)
+constexpr int KSS = 3;                 // S tiles
+constexpr int KSV = 4;                 // V tiles
+constexpr int NST = 3;                 // staging stages
+constexpr int ROW = ESS_LATENT_ROW_BYTES;  // 656
+constexpr int OTHER = 272;             // other half's row part: 2 x 128 B NoPE + 16 B scales
+constexpr int STG_OWN = NH * ROW;      // 10496
+constexpr int STG_BYTES = STG_OWN + NH * OTHER;  // 14848
+constexpr int QBLK = HH * 128;         // [64 heads][64 dims] f16 = 8 KB
+constexpr int S_BLK = NH * 128;        // [16 rows][64 dims] = 2 KB
+constexpr int S_TILE = NBLK * S_BLK;   // 18 KB
+constexpr int V_BLK = NB * 128;        // [32 rows][64 dims] = 4 KB
+constexpr int V_TILE = 4 * V_BLK;      // 16 KB: this CTA's 256 of the 512 V dims
+constexpr int P_TILE = HH * 128;       // [64 heads][32 tokens] f16 in 128-B SW128 rows
+constexpr int NSOFT = 4, MMA_WARP = 4, LOAD_WARP = 5, CONV0 = 6, NCONV = 4;
+constexpr int NTHREADS = 32 * (CONV0 + NCONV);  // 320
+constexpr uint32_t TM_O = 0, TM_S = 256, TM_Q = 320;
+static_assert(TM_Q + QT_BLKS * 32 <= 512, "TMEM budget");
+constexpr float RESCALE_THRESHOLD = 8.0f;
+constexpr int MLA_AWAIT = 4;           // internal flag (as in mla.cu)
+constexpr int LANDED_TAG = 1 << 24;
+constexpr uint32_t IDESC_S = make_idesc(0, 0, HEADS, NB, 0, 0);
+constexpr uint32_t IDESC_PV = make_idesc(0, 0, HEADS, 256, 0, 1 /* B MN-major */);
+
+struct Ctrl {
+  uint64_t stg_full[NST], stg_empty[NST];
+  uint64_t s_full[KSS], s_empty[KSS];   // s_full/v_full/p_full: rank 0's gate the MMAs
+  uint64_t v_full[KSV], v_empty[KSV];
+  uint64_t s_ready[NSB], p_full[NSB], pv_done[NSB];
+  uint64_t o_done, q_full;
+  uint32_t tmem;
+  float xm[2][2][HH];                   // pair max / sum exchange (double-buffered)
+};
+constexpr size_t OFF_Q = 0;
+constexpr size_t OFF_S = OFF_Q + QS_BLKS * QBLK;
+constexpr size_t OFF_V = OFF_S + KSS * S_TILE;
+constexpr size_t OFF_P = OFF_V + KSV * V_TILE;
+constexpr size_t OFF_STG = OFF_P + NSB * P_TILE;
+constexpr size_t OFF_CTRL = OFF_STG + NST * STG_BYTES;
+constexpr size_t SMEM_BYTES = 1024 + OFF_CTRL + sizeof(Ctrl);
+static_assert(SMEM_BYTES <= 232448, "K5 (FP8) shared memory over the sm_100 limit");
+static_assert(QT_BLKS * QBLK <= KSV * V_TILE, "q staging for TMEM fits the V ring");
+static_assert(OFF_S % 1024 == 0 && OFF_V % 1024 == 0 && OFF_P % 1024 == 0, "SW128 alignment");
+
+// ---- cta_group::2 PTX --------------------------------------------------------------
+__device__ __forceinline__ void mma2_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma2_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// completion of every prior tcgen05 op of this thread -> arrive on the barrier at the
+// same shared-memory offset in both CTAs of the pair
+__device__ __forceinline__ void commit2(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc2(uint32_t *dst) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(dst))
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc2(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(taddr) : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive (release, cluster scope) on the barrier at the same offset in CTA `rank`
+__device__ __forceinline__ void arrive_on(uint64_t *bar, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ void softmax_bar() {  // the 4 softmax warps only
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st_x32(uint32_t taddr, const uint32_t (&r)[32]) { tmem_st_32x32b_x32(taddr, r); }
+__device__ __forceinline__ void tmem_ld_x16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// bf16 pair -> f16 pair, saturating at +-65504 (no silent inf from the narrower range)
+__device__ __forceinline__ uint32_t bf16x2_to_f16x2_sat(uint32_t v) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(__uint_as_float(v & 0xFFFF0000u)),
+      "f"(__uint_as_float(v << 16)));
+  return r;
+}
+__device__ __forceinline__ uint4 cvt8_bf16_f16_sat(uint4 x) {
+  return make_uint4(bf16x2_to_f16x2_sat(x.x), bf16x2_to_f16x2_sat(x.y), bf16x2_to_f16x2_sat(x.z),
+                    bf16x2_to_f16x2_sat(x.w));
+}
+// 16 e4m3 (one uint4) x f16 scale pair -> 16 f16 (two uint4): exact e4m3 -> f16, one HMUL2
+__device__ __forceinline__ void deq16(uint4 v, uint32_t s2, uint4 &a, uint4 &c) {
+  const __half2 sc = *reinterpret_cast<const __half2 *>(&s2);
+  auto m = [&](uint32_t w16) {
+    uint32_t h = cvt_e4m3x2_f16x2((uint16_t)w16);
+    __half2 r = __hmul2(*reinterpret_cast<__half2 *>(&h), sc);
+    return *reinterpret_cast<uint32_t *>(&r);
+  };
+  a = make_uint4(m(v.x & 0xFFFF), m(v.x >> 16), m(v.y & 0xFFFF), m(v.y >> 16));
+  c = make_uint4(m(v.z & 0xFFFF), m(v.z >> 16), m(v.w & 0xFFFF), m(v.w >> 16));
+}
+__device__ __forceinline__ uint32_t scale_f16x2(float s) {
+  __half2 h = __float2half2_rn(s);
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+__device__ __forceinline__ int ld_acquire(const int32_t *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_landed(const int32_t *p, int target) {
+  if ((threadIdx.x & 31) == 0) {
+    uint32_t spins = 0;
+    while ((ld_acquire(p) & (LANDED_TAG - 1)) < target) {
+      if (++spins > ESS_SPIN_LIMIT) __trap();
+      __nanosleep(256);
+    }
+  }
+  __syncwarp();
+  (void)ld_acquire(p);
+  fence_proxy_async_global();  // the gather's generic-proxy stores -> our bulk-copy reads
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1)
+    sparse_mla_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const uint8_t *__restrict__ rows,
+                          int64_t rows_per_pool, int pool_begin, const int32_t *__restrict__ sel_row,
+                          const int32_t *__restrict__ sel2, int32_t *landed, int sel_stride,
+                          const int32_t *__restrict__ counts, int count_stride, float sm_scale,
+                          uint16_t *__restrict__ out, float *__restrict__ lse, float *__restrict__ ws_o,
+                          float *__restrict__ ws_ml, int flags, int nsplit) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sq = smem + OFF_Q, *sS = smem + OFF_S, *sV = smem + OFF_V, *sP = smem + OFF_P;
+  uint8_t *stg = smem + OFF_STG;
+  Ctrl &c = *reinterpret_cast<Ctrl *>(smem + OFF_CTRL);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t r = cluster_rank();         // 0: issues the MMAs
+  const int split = blockIdx.y % nsplit;
+  const int b = blockIdx.y / nsplit;
+  const bool partial = flags & ESS_MLA_PARTIAL, resume = flags & ESS_MLA_RESUME;
+  const bool to_ws = partial || nsplit > 1;
+  const bool await = flags & MLA_AWAIT;
+  const int n1t = min(counts[(int64_t)b * count_stride], ESS_MAX_REQUEST);
+  const int n2t = await ? min(counts[(int64_t)b * count_stride + 1], ESS_MAX_REQUEST - n1t) : 0;
+  const int h0 = n1t * split / nsplit, h1 = n1t * (split + 1) / nsplit;
+  const int m0 = n2t * split / nsplit, m1 = n2t * (split + 1) / nsplit;
+  const int n1 = h1 - h0;
+  const int n = n1 + (m1 - m0);
+  const bool fetched = m1 > m0;
+  const int ntiles = (n + NB - 1) / NB;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NST; i++) {
+      mbar_init(&c.stg_full[i], 1);
+      mbar_init(&c.stg_empty[i], NCONV);
+    }
+    for (int i = 0; i < KSS; i++) {
+      mbar_init(&c.s_full[i], 2 * NCONV);
+      mbar_init(&c.s_empty[i], 1);
+    }
+    for (int i = 0; i < KSV; i++) {
+      mbar_init(&c.v_full[i], 2 * NCONV);
+      mbar_init(&c.v_empty[i], 1);
+    }
+    for (int i = 0; i < NSB; i++) {
+      mbar_init(&c.s_ready[i], 1);
+      mbar_init(&c.p_full[i], 2 * NSOFT);
+      mbar_init(&c.pv_done[i], 1);
+    }
+    mbar_init(&c.o_done, 1);
+    mbar_init(&c.q_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == MMA_WARP) tmem_alloc2(&c.tmem);
+
+  // ---- prologue: this CTA's 64 q rows -> TMEM (dims 0..383, duplicated over both lane
+  // halves) and shared memory (384..575); TMA boxes of [64 heads][64 dims] bf16 -------
+  __syncthreads();  // barriers initialised (q_full is waited on below)
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(&c.q_full, HH * ESS_MLA_QK_DIM * 2);
+    for (int blk = 0; blk < NBLK; blk++)
+      tma_load_2d(blk < QT_BLKS ? sV + blk * QBLK : sq + (blk - QT_BLKS) * QBLK, &tm_q, &c.q_full, blk * 64,
+                  b * HEADS + (int)r * HH);
+  }
+  mbar_wait(&c.q_full, 0);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = c.tmem;
+  if (warp < NSOFT) {
+    const int h = (warp * 32 + lane) & (HH - 1);
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+#pragma unroll 1
+    for (int cc = 0; cc < QT_BLKS; cc++) {
+      const uint8_t *rowp = sV + cc * QBLK + h * 128;
+      uint32_t v[32];
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const uint4 y = cvt8_bf16_f16_sat(*reinterpret_cast<const uint4 *>(rowp + ((k ^ (h & 7)) << 4)));
+        v[4 * k] = y.x;
+        v[4 * k + 1] = y.y;
+        v[4 * k + 2] = y.z;
+        v[4 * k + 3] = y.w;
+      }
+      tmem_st_x32(tmem + lane_base + TM_Q + cc * 32, v);
+    }
+    tmem_st_wait();
+  } else {
+    uint4 *qs = reinterpret_cast<uint4 *>(sq);
+    for (int u = threadIdx.x - NSOFT * 32; u < QS_BLKS * QBLK / 16; u += NTHREADS - NSOFT * 32)
+      qs[u] = cvt8_bf16_f16_sat(qs[u]);
+    fence_proxy_async_smem();
+  }
+  tc_fence_before();
+  __syncthreads();   // the V ring (q staging) is free again
+  cluster_sync_all();  // both CTAs: barriers initialised, q in TMEM / smem
+  tc_fence_after();
+  const float scale_log2 = sm_scale * 1.4426950408889634f;
+
+  if (warp < NSOFT) {
+    // ================= softmax / epilogue: thread = (head, token half) ===============
+    const int t = warp * 32 + lane;
+    const int h = t & (HH - 1), u = t >> 6;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const int64_t hrow = (int64_t)b * HEADS + (int)r * HH + h;
+    const int64_t wrow = (int64_t)(b * nsplit + split) * HEADS + (int)r * HH + h;
+    float *wso = ws_o ? ws_o + wrow * ESS_MLA_V_DIM : nullptr;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int i = 0; i < ntiles; i++) {
+      const int sb = i % NSB;
+      mbar_wait(&c.s_ready[sb], (i / NSB) & 1);
+      if (i >= NSB) mbar_wait(&c.pv_done[sb], ((i - NSB) / NSB) & 1);  // P tile sb free
+      tc_fence_after();
+      uint32_t sr[NH];
+      tmem_ld_x16(tmem + lane_base + TM_S + sb * NH, sr);
+      tmem_ld_wait();
+      float x[NH];
+      const int lim = n - i * NB - u * NH;  // valid tokens of this half
+#pragma unroll
+      for (int j = 0; j < NH; j++) x[j] = j < lim ? __uint_as_float(sr[j]) : -INFINITY;
+      float mx = fmaxf(x[0], x[1]);
+#pragma unroll
+      for (int j = 2; j < NH; j++) mx = fmaxf(mx, x[j]);
+      c.xm[i & 1][u][h] = mx;
+      softmax_bar();
+      const float mt = fmaxf(mx, c.xm[i & 1][u ^ 1][h]) * scale_log2;
+      // both threads of a head see the same (mt, m_run): the pair and the two warps
+      // holding the same heads (w, w+2) take the same, warp-uniform decision
+      if (__any_sync(0xffffffffu, mt > m_run + RESCALE_THRESHOLD) || i == 0) {
+        const float m_new = fmaxf(mt, m_run);
+        const float alpha = exp2f(m_run - m_new);
+        l_run *= alpha;
+        if (i > 0) {
+          mbar_wait(&c.pv_done[(i - 1) % NSB], ((i - 1) / NSB) & 1);  // O holds PV(i-1)
+          tc_fence_after();
+#pragma unroll 1
+          for (int cc = 0; cc < 8; cc++) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(tmem + lane_base + TM_O + cc * 32, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; j++) o[j] = __float_as_uint(__uint_as_float(o[j]) * alpha);
+            tmem_st_x32(tmem + lane_base + TM_O + cc * 32, o);
+          }
+          tmem_st_wait();
+        }
+        m_run = m_new;
+      }
+      uint32_t p[NH / 2];
+      float ls0 = 0.f, ls1 = 0.f;
+      const float nm = -m_run;
+#pragma unroll
+      for (int e = 0; e < NH / 2; e++) {
+        const float e0 = fast_exp2(fmaf(x[2 * e], scale_log2, nm));
+        const float e1 = fast_exp2(fmaf(x[2 * e + 1], scale_log2, nm));
+        p[e] = pack_f16x2(e0, e1);
+        ls0 += e0;
+        ls1 += e1;
+      }
+      l_run += ls0 + ls1;
+      // P row h, tokens [16u, 16u+16): logical 16-B chunks 2u, 2u+1 of the SW128 row
+      uint8_t *prow = sP + sb * P_TILE + h * 128;
+      *reinterpret_cast<uint4 *>(prow + (((2 * u) ^ (h & 7)) << 4)) = make_uint4(p[0], p[1], p[2], p[3]);
+      *reinterpret_cast<uint4 *>(prow + (((2 * u + 1) ^ (h & 7)) << 4)) = make_uint4(p[4], p[5], p[6], p[7]);
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_on(&c.p_full[sb], 0);
+    }
+    // ---------------- epilogue ----------------------------------------------------
+    const bool have_o = ntiles > 0;
+    if (have_o) {
+      mbar_wait(&c.o_done, 0);
+      for (int k = max(0, ntiles - NSB); k < ntiles; k++) mbar_wait(&c.pv_done[k % NSB], (k / NSB) & 1);
+      tc_fence_after();
+    }
+    c.xm[ntiles & 1][u][h] = l_run;  // the pair's sums
+    softmax_bar();
+    const float l_pair = l_run + c.xm[ntiles & 1][u ^ 1][h];
+    // this thread's 256 dims: columns [0,128) = dims 128u + c, [128,256) = 256 + 128u + c
+    auto dim_of = [&](int col) { return col < 128 ? 128 * u + col : 256 + 128 * u + (col - 128); };
+    if (to_ws) {
+#pragma unroll 1
+      for (int cc = 0; cc < 8; cc++) {
+        uint32_t o[32];
+        if (have_o) {
+          tmem_ld_32x32b_x32(tmem + lane_base + TM_O + cc * 32, o);
+          tmem_ld_wait();
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; j++) o[j] = 0u;
+        }
+        float *dst = wso + dim_of(cc * 32);
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4 *>(dst + j) = make_float4(__uint_as_float(o[j]), __uint_as_float(o[j + 1]),
+                                                             __uint_as_float(o[j + 2]), __uint_as_float(o[j + 3]));
+      }
+      if (u == 0) {
+        ws_ml[wrow * 2 + 0] = m_run;
+        ws_ml[wrow * 2 + 1] = l_pair;
+      }
+    } else {
+      float m = m_run, l = l_pair, a0 = 0.f, a1 = have_o ? 1.f : 0.f;
+      if (resume) {
+        const float mp = ws_ml[hrow * 2 + 0], lp = ws_ml[hrow * 2 + 1];
+        m = fmaxf(mp, m_run);
+        a0 = mp == -INFINITY ? 0.f : exp2f(mp - m);
+        a1 = (have_o && m_run != -INFINITY) ? exp2f(m_run - m) : 0.f;
+        l = lp * a0 + l_pair * a1;
+      }
+      uint16_t *ob = out + hrow * ESS_MLA_V_DIM;
+      const float *wsr = resume ? ws_o + hrow * ESS_MLA_V_DIM : nullptr;
+      if (l > 0.f) {
+        const float inv = 1.f / l, c0 = a0 * inv, c1 = a1 * inv;
+#pragma unroll 1
+        for (int cc = 0; cc < 8; cc++) {
+          uint32_t o[32];
+          if (have_o) {
+            tmem_ld_32x32b_x32(tmem + lane_base + TM_O + cc * 32, o);
+            tmem_ld_wait();
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; j++) o[j] = 0u;
+          }
+          const int d0 = dim_of(cc * 32);
+#pragma unroll
+          for (int j = 0; j < 32; j += 8) {
+            float w[8];
+#pragma unroll
+            for (int e = 0; e < 8; e++) w[e] = resume ? wsr[d0 + j + e] : 0.f;
+            uint4 pk;
+            uint32_t *pw = reinterpret_cast<uint32_t *>(&pk);
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+              __nv_bfloat162 tt = __floats2bfloat162_rn(__uint_as_float(o[j + 2 * e]) * c1 + w[2 * e] * c0,
+                                                        __uint_as_float(o[j + 2 * e + 1]) * c1 + w[2 * e + 1] * c0);
+              pw[e] = *reinterpret_cast<uint32_t *>(&tt);
+            }
+            *reinterpret_cast<uint4 *>(ob + d0 + j) = pk;
+          }
+        }
+        if (u == 0) lse[hrow] = (m + log2f(l)) * 0.6931471805599453f;
+      } else {
+        for (int cc = 0; cc < 8; cc++) {
+          const int d0 = dim_of(cc * 32);
+          for (int j = 0; j < 32; j += 8) *reinterpret_cast<uint4 *>(ob + d0 + j) = make_uint4(0, 0, 0, 0);
+        }
+        if (u == 0) lse[hrow] = -INFINITY;
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    // ================= MMA issue (rank 0; its instructions drive both SMs) ===========
+    if (r == 0 && elect_one() && ntiles > 0) {
+      const uint64_t qbase = sw128_desc(smem_u32(sq), 16, 1024);
+      const uint64_t sbase = sw128_desc(smem_u32(sS), 16, 1024);
+      const uint64_t vbase = sw128_desc(smem_u32(sV), V_BLK, 1024);
+      const uint64_t pbase = sw128_desc(smem_u32(sP), 16, 1024);
+      auto issue_s = [&](int i) {
+        const int ks = i % KSS, sb = i % NSB;
+        mbar_wait(&c.s_full[ks], (i / KSS) & 1);  // both CTAs' halves of tile i dequantised
+        tc_fence_after();
+        const uint32_t d = tmem + TM_S + sb * NH;
+#pragma unroll
+        for (int blk = 0; blk < NBLK; blk++) {
+#pragma unroll
+          for (int kk = 0; kk < 4; kk++) {
+            const uint64_t bd = sbase + (uint64_t)((ks * S_TILE + blk * S_BLK + kk * 32) >> 4);
+            const uint32_t acc = (blk | kk) ? 1u : 0u;
+            if (blk < QT_BLKS) mma2_ts(d, tmem + TM_Q + (blk * 4 + kk) * 8, bd, IDESC_S, acc);
+            else mma2_ss(d, qbase + (uint64_t)(((blk - QT_BLKS) * QBLK + kk * 32) >> 4), bd, IDESC_S, acc);
+          }
+        }
+        commit2(&c.s_ready[sb]);
+        commit2(&c.s_empty[ks]);
+      };
+      for (int i = 0; i < LOOKAHEAD && i < ntiles; i++) issue_s(i);
+      for (int i = 0; i < ntiles; i++) {
+        if (i + LOOKAHEAD < ntiles) issue_s(i + LOOKAHEAD);
+        const int sb = i % NSB, kv = i % KSV;
+        mbar_wait(&c.p_full[sb], (i / NSB) & 1);
+        mbar_wait(&c.v_full[kv], (i / KSV) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 2; kk++) {
+          const uint64_t ad = pbase + (uint64_t)((sb * P_TILE + kk * 32) >> 4);
+#pragma unroll
+          for (int hf = 0; hf < 2; hf++) {
+            const uint64_t bd = vbase + (uint64_t)((kv * V_TILE + 2 * hf * V_BLK + kk * 16 * 128) >> 4);
+            mma2_ss(tmem + TM_O + hf * 128, ad, bd, IDESC_PV, (i | kk) ? 1u : 0u);
+          }
+        }
+        commit2(&c.pv_done[sb]);
+        commit2(&c.v_empty[kv]);
+        if (i == ntiles - 1) commit2(&c.o_done);
+      }
+    }
+  } else if (warp == LOAD_WARP) {
+    // ================= row loader: one bulk copy per own row, three per other row ====
+    const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b) * rows_per_pool * ROW;
+    const int32_t *selh = sel_row + (int64_t)b * sel_stride + h0;
+    const int32_t *selm = await ? sel2 + (int64_t)b * sel_stride + m0 : nullptr;
+    bool pending = fetched && n2t > 0;
+    for (int i = 0; i < ntiles; i++) {
+      const int st = i % NST;
+      mbar_wait(&c.stg_empty[st], ((i / NST) & 1) ^ 1);
+      if (pending && (i + 1) * NB > n1) {
+        wait_landed(landed + b, n2t);
+        pending = false;
+      }
+      if (lane == 0) mbar_arrive_expect_tx(&c.stg_full[st], STG_BYTES);
+      __syncwarp();
+      const bool own = lane < NH;
+      const int tok = i * NB + (own ? (int)r * NH + lane : (1 - (int)r) * NH + (lane - NH));
+      const int j = tok < n ? tok : 0;  // padding rows re-read row 0 (masked by the softmax)
+      const int sid = j < n1 ? __ldg(selh + j) : __ldg(selm + (j - n1));
+      const uint8_t *src = pool_rows + (int64_t)sid * ROW;
+      uint8_t *dst = stg + st * STG_BYTES;
+      if (own) {
+        bulk_load(dst + lane * ROW, src, ROW, &c.stg_full[st]);
+      } else {
+        uint8_t *o = dst + STG_OWN + (lane - NH) * OTHER;
+        bulk_load(o, src + 128 * r, 128, &c.stg_full[st]);
+        bulk_load(o + 128, src + 256 + 128 * r, 128, &c.stg_full[st]);
+        bulk_load(o + 256, src + 512, 16, &c.stg_full[st]);
+      }
+    }
+  } else {
+    // ================= dequantisers (4 warps): staging -> S tile, V tile ==============
+    const int ct = threadIdx.x - CONV0 * 32;  // 0..127
+    for (int i = 0; i < ntiles; i++) {
+      const int st = i % NST, ks = i % KSS, kv = i % KSV;
+      mbar_wait(&c.stg_full[st], (i / NST) & 1);
+      if (i >= KSS) mbar_wait(&c.s_empty[ks], ((i - KSS) / KSS) & 1);
+      const uint8_t *src = stg + st * STG_BYTES;
+      // own 16 rows x (32 NoPE chunks + 8 RoPE chunks) -> S tile [16 rows][576] SW128
+      uint8_t *sd = sS + ks * S_TILE;
+#pragma unroll
+      for (int k = 0; k < (NH * 40) / 128; k++) {
+        const int it = ct + 128 * k;
+        const int row = it / 40, ch = it % 40;
+        const uint8_t *rp = src + row * ROW;
+        if (ch < 32) {
+          const uint4 v = *reinterpret_cast<const uint4 *>(rp + ch * 16);
+          const float s = *reinterpret_cast<const float *>(rp + 512 + 4 * (ch >> 3));
+          uint4 a, cc;
+          deq16(v, scale_f16x2(s), a, cc);
+          const int blk = ch >> 2, c0 = (ch & 3) * 2;  // 4 NoPE chunks per 64-dim block
+          uint8_t *dr = sd + blk * S_BLK + row * 128;
+          *reinterpret_cast<uint4 *>(dr + ((c0 ^ (row & 7)) << 4)) = a;
+          *reinterpret_cast<uint4 *>(dr + (((c0 + 1) ^ (row & 7)) << 4)) = cc;
+        } else {
+          const int rc = ch - 32;  // RoPE: 8 bf16 per chunk -> block 8, chunk rc
+          const uint4 v = *reinterpret_cast<const uint4 *>(rp + 528 + rc * 16);
+          *reinterpret_cast<uint4 *>(sd + 8 * S_BLK + row * 128 + ((rc ^ (row & 7)) << 4)) = cvt8_bf16_f16_sat(v);
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) arrive_on(&c.s_full[ks], 0);
+      // V: 32 tokens x this CTA's 256 NoPE dims (16 chunks) -> V tile [32][4 x 64] SW128
+      if (i >= KSV) mbar_wait(&c.v_empty[kv], ((i - KSV) / KSV) & 1);
+      uint8_t *vd = sV + kv * V_TILE;
+#pragma unroll
+      for (int k = 0; k < (NB * 16) / 128; k++) {
+        const int it = ct + 128 * k;
+        const int tok = it >> 4, ch = it & 15;  // ch < 8: dims 128r + 16ch; else 256 + 128r + 16(ch-8)
+        const bool own = (tok >> 4) == (int)r;
+        const int jr = tok & (NH - 1);
+        uint4 v;
+        float s;
+        if (own) {
+          const uint8_t *rp = src + jr * ROW;
+          const int cabs = (ch < 8 ? 8 * (int)r : 16 + 8 * (int)r) + (ch & 7);
+          v = *reinterpret_cast<const uint4 *>(rp + cabs * 16);
+          s = *reinterpret_cast<const float *>(rp + 512 + 4 * (cabs >> 3));
+        } else {
+          const uint8_t *rp = src + STG_OWN + jr * OTHER;
+          v = *reinterpret_cast<const uint4 *>(rp + ch * 16);
+          s = *reinterpret_cast<const float *>(rp + 256 + 4 * (ch < 8 ? (int)r : 2 + (int)r));
+        }
+        uint4 a, cc;
+        deq16(v, scale_f16x2(s), a, cc);
+        const int vb = ch >> 2, c0 = (ch & 3) * 2;
+        uint8_t *dr = vd + vb * V_BLK + tok * 128;
+        *reinterpret_cast<uint4 *>(dr + ((c0 ^ (tok & 7)) << 4)) = a;
+        *reinterpret_cast<uint4 *>(dr + (((c0 + 1) ^ (tok & 7)) << 4)) = cc;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        arrive_on(&c.v_full[kv], 0);
+        mbar_arrive(&c.stg_empty[st]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (await && threadIdx.x == 0) {
+    if (atomicAdd(landed + b, LANDED_TAG) >= (2 * nsplit - 1) * LANDED_TAG) atomicExch(landed + b, 0);
+  }
+  cluster_sync_all();  // no more remote arrives / peer operand reads; then free TMEM
+  tc_fence_after();
+  if (warp == MMA_WARP) tmem_dealloc2(tmem);
+}
+
+}  // namespace
+
+// launched by mla.cu's entry points when the pool keeps 656-B slot rows
+int ess_launch_mla_fp8(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_t *d_sel_row,
+                       const int32_t *d_sel2, int32_t *d_landed, int32_t sel_stride,
+                       const int32_t *d_count, int32_t count_stride, int32_t batch, float sm_scale,
+                       void *d_out, float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags,
+                       int32_t nsplit, void *stream) {
+  // q as a [batch * 128 heads][576] bf16 tensor, boxes of [64 heads][64 dims], SW128
+  struct QMap {
+    const void *base = nullptr;
+    int32_t batch = 0;
+    int dev = -1;
+    CUtensorMap map;
+  };
+  static thread_local QMap qm;
+  int dev = 0;
+  ESS_CUDA_TRY(cudaGetDevice(&dev));
+  alignas(64) CUtensorMap tq;
+  if (qm.base == d_q && qm.batch == batch && qm.dev == dev) {
+    tq = qm.map;
+  } else {
+    if (!ess_make_tmap_2d(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, d_q, ESS_MLA_QK_DIM, (uint64_t)batch * HEADS,
+                          ESS_MLA_QK_DIM * 2, 64, HH, CU_TENSOR_MAP_SWIZZLE_128B))
+      return ESS_ERR_CUDA;
+    qm.base = d_q;
+    qm.batch = batch;
+    qm.dev = dev;
+    qm.map = tq;
+  }
+  if (int rc = ess_smem_optin((const void *)sparse_mla_fp8_kernel, SMEM_BYTES)) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2, (unsigned)(batch * nsplit));
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, sparse_mla_fp8_kernel, tq, (const uint8_t *)pool->rows,
+                                  pool->rows_per_pool, (int)pool_begin, d_sel_row, d_sel2, d_landed,
+                                  (int)sel_stride, d_count, (int)count_stride, sm_scale, (uint16_t *)d_out,
+                                  d_lse, d_ws_o, d_ws_ml, (int)flags, (int)nsplit));
+  return ESS_OK;
+}

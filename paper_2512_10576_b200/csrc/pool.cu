@@ -310,6 +310,18 @@ __device__ __forceinline__ void dequant_row_to_slot(uint4 v0, uint4 v1, int lane
   if (lane >= 1 && lane <= 8) st_v4(dst + 1024 + (lane - 1) * 16, cvt8_bf16_f16(v1));
 }
 
+// The slot row of a 656-B latent row held by a warp, in the pool's slot format: the raw
+// row (ESS_SLOT_ROW_BYTES_FP8: K5 dequantises in shared memory) or the dequantised f16
+// row (ESS_SLOT_ROW_BYTES).
+__device__ __forceinline__ void store_slot_row(uint4 v0, uint4 v1, int lane, uint8_t *dst, int row_bytes) {
+  if (row_bytes == ESS_SLOT_ROW_BYTES_FP8) {
+    st_v4(dst + lane * 16, v0);
+    if (lane + 32 < ESS_LATENT_ROW_BYTES / 16) st_v4(dst + (lane + 32) * 16, v1);
+  } else {
+    dequant_row_to_slot(v0, v1, lane, dst);
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(NT, 1)
     pool_step_kernel(PoolView pv, int begin, const int32_t *__restrict__ req,
@@ -1039,7 +1051,7 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
         publish();
         cur_pool = pool_of[r];
       }
-      dequant_row_to_slot(v[r][0], v[r][1], lane, dst[r]);
+      store_slot_row(v[r][0], v[r][1], lane, dst[r], (int)rb);
       tally++;
     }
   }
@@ -1137,7 +1149,7 @@ __global__ void __launch_bounds__(NTG) gather_bulk_kernel(PoolView pv, int begin
       publish();
       cur_pool = lo;
     }
-    dequant_row_to_slot(v0, v1, lane, pv.rows + ((int64_t)(begin + lo) * pv.rows_per_pool + row) * rb);
+    store_slot_row(v0, v1, lane, pv.rows + ((int64_t)(begin + lo) * pv.rows_per_pool + row) * rb, (int)rb);
     tally++;
   }
   publish();
@@ -1163,7 +1175,9 @@ __global__ void write_generated_kernel(PoolView pv, int begin, const int32_t *id
       st_v4(h + lane * 16, v0);
       if (lane + 32 < ROW_CHUNKS) st_v4(h + (lane + 32) * 16, v1);
     }
-    if (s >= 0) dequant_row_to_slot(v0, v1, lane, pv.rows + ((int64_t)(begin + b) * pv.rows_per_pool + s) * pv.row_bytes);
+    if (s >= 0)
+      store_slot_row(v0, v1, lane, pv.rows + ((int64_t)(begin + b) * pv.rows_per_pool + s) * pv.row_bytes,
+                     pv.row_bytes);
   }
 }
 
@@ -1232,7 +1246,8 @@ __global__ void __launch_bounds__(NTA) pool_admit_kernel(PoolView pv, int begin,
       if (lane + 32 < ROW_CHUNKS) st_v4(hp + (lane + 32) * 16, v1);
     }
     if (pv.rows)
-      dequant_row_to_slot(v0, v1, lane, pv.rows + ((int64_t)p * pv.rows_per_pool + slots[i]) * pv.row_bytes);
+      store_slot_row(v0, v1, lane, pv.rows + ((int64_t)p * pv.rows_per_pool + slots[i]) * pv.row_bytes,
+                     pv.row_bytes);
     if (slot_out && lane == 0) slot_out[(int64_t)b * src_stride + i] = slots[i];
   }
   if (threadIdx.x == 0) {
@@ -1294,7 +1309,7 @@ int ess_pool_create(ess_pool **out, int32_t num_pools, int64_t max_ids, int32_t 
                     int32_t row_bytes, int32_t staging_rows) {
   if (!out || num_pools < 1 || max_ids < 1 || max_ids > 0x7fffffff || cap_max < 1 ||
       cap_max > 0x00ffffff || staging_rows < 0 || row_bytes < 0 ||
-      (row_bytes && row_bytes != ESS_SLOT_ROW_BYTES))
+      (row_bytes && row_bytes != ESS_SLOT_ROW_BYTES && row_bytes != ESS_SLOT_ROW_BYTES_FP8))
     return ESS_ERR_ARG;
   // 64-B alignment for the embedded CUtensorMap
   ess_pool *p = (ess_pool *)aligned_alloc(64, (sizeof(ess_pool) + 63) & ~size_t(63));

@@ -1,4 +1,5 @@
-"""Time K5 (sparse MLA) alone at the C2 shape: B=64, 2048 of 8192 slot rows each."""
+"""Time K5 (sparse MLA) alone at the C2 shape: B=64, 2048 of 8192 slot rows each.
+FMT=656 (raw FP8 slot rows, the CTA-pair kernel) or 1152 (f16 slot rows)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -10,10 +11,16 @@ from paper_2512_10576_b200.cache import PoolSet
 
 B, cap, n = 64, 8192, int(os.environ.get("N", 2048))
 MODE = os.environ.get("MODE", "full")
-pools = PoolSet(B, 32768, cap, cap, row_bytes=1152)
+FMT = int(os.environ.get("FMT", "656"))
+pools = PoolSet(B, 32768, cap, cap, row_bytes=FMT)
 g = torch.Generator(device="cuda").manual_seed(0)
 rv = pools.rows_view()
-rv.copy_((torch.randn(rv.shape, device="cuda", generator=g) * 0.5).half())
+if FMT == 656:
+    from paper_2512_10576_b200.decode import random_latent_rows
+    for b in range(B):
+        rv[b].copy_(random_latent_rows(cap, "cuda", g))
+else:
+    rv.copy_((torch.randn(rv.shape, device="cuda", generator=g) * 0.5).half())
 sel = torch.stack([torch.randperm(cap, device="cuda", generator=g)[:n] for _ in range(B)]).int()
 cnt = torch.full((B,), n, dtype=torch.int32, device="cuda")
 q = (torch.randn((B, 128, 576), device="cuda", generator=g) * 0.5).to(torch.bfloat16)
@@ -35,6 +42,6 @@ for _ in range(int(os.environ.get("ITERS", "10"))):
     torch.cuda.synchronize()
     ts.append(a.elapsed_time(b) * 1e3)
 ts.sort()
-byt = B * n * 1152
-print(f"{os.path.basename(_lib.LIB_PATH)} sparse_mla {MODE} B={B} n={n}: median {ts[len(ts)//2]:.1f} us, min {ts[0]:.1f} us, "
+byt = B * n * FMT
+print(f"{os.path.basename(_lib.LIB_PATH)} sparse_mla fmt={FMT} {MODE} B={B} n={n}: median {ts[len(ts)//2]:.1f} us, min {ts[0]:.1f} us, "
       f"{byt / ts[len(ts)//2] / 1e3:.0f} GB/s unique rows")

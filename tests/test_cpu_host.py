@@ -40,7 +40,10 @@ def test_header_constants_match_python_mirror():
     src = open(os.path.join(ROOT, "include", "ess_b200.h")).read()
     defs = dict(re.findall(r"#define (ESS_[A-Z0-9_]+) \(?(-?[0-9]+)", src))
     assert int(defs["ESS_LATENT_ROW_BYTES"]) == _lib.LATENT_ROW_BYTES == 656
-    assert int(defs["ESS_SLOT_ROW_BYTES"]) == _lib.SLOT_ROW_BYTES
+    assert int(defs["ESS_SLOT_ROW_BYTES"]) == _lib.SLOT_ROW_BYTES_F16 == 1152
+    assert int(defs["ESS_SLOT_ROW_BYTES_FP8"]) == _lib.SLOT_ROW_BYTES_FP8 == 656
+    assert _lib.SLOT_ROW_BYTES in (656, 1152)
+    assert int(defs["ESS_TOPK_MAX_K"]) == 65535
     assert int(defs["ESS_HOST_ROW_PITCH"]) == _lib.HOST_ROW_PITCH
     assert _lib.HOST_ROW_PITCH % 64 == 0 and _lib.HOST_ROW_PITCH >= _lib.LATENT_ROW_BYTES
     assert int(defs["ESS_MLA_PARTIAL"]) == _lib.ESS_MLA_PARTIAL

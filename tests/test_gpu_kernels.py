@@ -172,8 +172,9 @@ def _check_k5(o, lse, ref_o, ref_l, what):
     assert np.abs(lse - ref_l).max() <= K5_LSE + 1e-6 * np.abs(ref_l).max(), (what, "lse")
 
 
+@pytest.mark.parametrize("fmt", [656, 1152], ids=["fp8slots", "f16slots"])
 @pytest.mark.parametrize("bulk", [False, True], ids=["ld16", "bulk"])
-def test_gather_and_write_back_are_exact(bulk):
+def test_gather_and_write_back_are_exact(bulk, fmt):
     """K4 reads 656-B rows over the host link and admits them dequantised; the slot
     row must equal the oracle's f16(f32(e4m3) * scale) ++ f16(bf16) bit for bit."""
     from paper_2512_10576_b200.cache import PoolSet
@@ -183,7 +184,7 @@ def test_gather_and_write_back_are_exact(bulk):
     store = HostLatentStore(P, ids)
     for p in range(P):
         store.host[p].copy_(random_latent_rows(ids, "cuda"))
-    pools = PoolSet(P, ids, cap, cap, row_bytes=1152, staging_rows=0)
+    pools = PoolSet(P, ids, cap, cap, row_bytes=fmt, staging_rows=0)
     rng = np.random.default_rng(0)
     sets = np.stack([rng.choice(4000, size=1000, replace=False) for _ in range(P)]).astype(np.int32)
     acc = pools.access(torch.as_tensor(sets, device="cuda"),
@@ -193,8 +194,8 @@ def test_gather_and_write_back_are_exact(bulk):
     sel = acc.sel_row.cpu().numpy()
     host = store.host.numpy()
     for p in range(P):
-        want = dsa.slot_rows(host[p, sets[p]])
-        np.testing.assert_array_equal(rows[p, sel[p]].view(np.uint16), want.view(np.uint16))
+        want = host[p, sets[p]] if fmt == 656 else dsa.slot_rows(host[p, sets[p]]).view(np.uint16)
+        np.testing.assert_array_equal(rows[p, sel[p]].view(want.dtype), want)
     # write-back of generated rows (append) lands in host store and (dequantised) slot
     new = torch.full((P, 1), 4500, dtype=torch.int32, device="cuda")
     one = torch.ones(P, dtype=torch.int32, device="cuda")
@@ -207,23 +208,27 @@ def test_gather_and_write_back_are_exact(bulk):
     srcn = src.cpu().numpy()
     for p in range(P):
         np.testing.assert_array_equal(store.host.numpy()[p, 4500], srcn[p, 0])
-        np.testing.assert_array_equal(rows[p, s[p]].view(np.uint16),
-                                      dsa.slot_rows(srcn[p, :1])[0].view(np.uint16))
+        want = srcn[p, 0] if fmt == 656 else dsa.slot_rows(srcn[p, :1])[0].view(np.uint16)
+        np.testing.assert_array_equal(rows[p, s[p]].view(want.dtype), want)
     pools.check()
     store.close()
 
 
 # ---------------------------------------------------------------------------- K5
+FMT = pytest.mark.parametrize("fmt", [656, 1152], ids=["fp8slots", "f16slots"])
+
+
+@FMT
 @pytest.mark.parametrize("split", [1, 2, 3, 4])
 @pytest.mark.parametrize("counts", [[2048, 1000, 17, 1], [2048] * 3])
-def test_sparse_mla_matches_oracle(counts, split):
+def test_sparse_mla_matches_oracle(counts, split, fmt):
     """split > 1: each request's rows on 2 * split CTAs, partial states merged by the
     combine kernel (small-batch path) — same tolerance as one pass."""
     from paper_2512_10576_b200.attention import SplitWorkspace, sparse_mla, DEFAULT_SM_SCALE
     from paper_2512_10576_b200.cache import PoolSet
     from paper_2512_10576_b200.decode import random_latent_rows
     B, cap = len(counts), 4096
-    pools = PoolSet(B, 8192, cap, cap, row_bytes=1152)
+    pools = PoolSet(B, 8192, cap, cap, row_bytes=fmt)
     g = torch.Generator(device="cuda").manual_seed(11)
     lat = [random_latent_rows(cap, "cuda", g) for _ in range(B)]
     _fill_slots(pools, lat, cap)
@@ -244,8 +249,9 @@ def test_sparse_mla_matches_oracle(counts, split):
         assert rel <= 1e-2, (b, n, rel)
 
 
+@FMT
 @pytest.mark.parametrize("n", [2048, 2047, 33, 1])
-def test_sparse_mla_counts_every_row_once(n):
+def test_sparse_mla_counts_every_row_once(n, fmt):
     """Exact row accounting: q = 0 makes every score 0, so the softmax is uniform and
     out = (sum of the selected V rows) / n exactly.  Each slot row is one-hot in a
     slot-dependent NoPE dim (value 1.0), so out[:, d] = (#selected rows hashed to d) / n
@@ -254,7 +260,7 @@ def test_sparse_mla_counts_every_row_once(n):
     from paper_2512_10576_b200.attention import sparse_mla
     from paper_2512_10576_b200.cache import PoolSet
     B, cap = 2, 4096
-    pools = PoolSet(B, 8192, cap, cap, row_bytes=_lib_slot_bytes())
+    pools = PoolSet(B, 8192, cap, cap, row_bytes=fmt)
     dims = (np.arange(cap) * 37 + 11) % 512
     rows = np.zeros((cap, 656), np.uint8)
     rows[np.arange(cap), dims] = 0x38                               # e4m3 1.0
@@ -277,7 +283,8 @@ def test_sparse_mla_counts_every_row_once(n):
     pools.close()
 
 
-def test_sparse_mla_dominant_row():
+@FMT
+def test_sparse_mla_dominant_row(fmt):
     """One selected row outscores the rest by > 40 nats for every head, so the output is
     that row's V (to bf16 rounding); a dropped or shifted row (the ring's first, last or
     middle slot) would replace it with a blend of the others."""
@@ -285,7 +292,7 @@ def test_sparse_mla_dominant_row():
     from paper_2512_10576_b200.cache import PoolSet
     from paper_2512_10576_b200.decode import random_latent_rows
     B, cap = 3, 4096
-    pools = PoolSet(B, 8192, cap, cap, row_bytes=_lib_slot_bytes())
+    pools = PoolSet(B, 8192, cap, cap, row_bytes=fmt)
     g = torch.Generator(device="cuda").manual_seed(29)
     lat = [random_latent_rows(cap, "cuda", g) for _ in range(B)]
     _fill_slots(pools, lat, cap)
@@ -311,13 +318,14 @@ def _lib_slot_bytes():
     return _lib.SLOT_ROW_BYTES
 
 
-def test_sparse_mla_rescale_path():
+@FMT
+def test_sparse_mla_rescale_path(fmt):
     """Scores that grow tile by tile force the lazy O rescale (> 2^8 jumps)."""
     from paper_2512_10576_b200.attention import sparse_mla
     from paper_2512_10576_b200.cache import PoolSet
     from paper_2512_10576_b200.decode import random_latent_rows
     B, n = 2, 2048
-    pools = PoolSet(B, 4096, n, n, row_bytes=1152)
+    pools = PoolSet(B, 4096, n, n, row_bytes=fmt)
     g = torch.Generator(device="cuda").manual_seed(2)
     lat = []
     for b in range(B):
@@ -341,8 +349,9 @@ def test_sparse_mla_rescale_path():
         assert (np.abs(got_l - ref_l) <= 1e-2 + 1e-3 * np.abs(ref_l)).all()
 
 
+@FMT
 @pytest.mark.parametrize("split", [(1900, 148), (0, 300), (2048, 0), (5, 1)])
-def test_split_attention_partial_then_resume(split):
+def test_split_attention_partial_then_resume(split, fmt):
     """DA split: Attn0 over one row set -> workspace, Attn1 resumes
     over the other set = attention over the union (merge_attn semantics)."""
     from paper_2512_10576_b200.attention import SplitWorkspace, sparse_mla, DEFAULT_SM_SCALE
@@ -350,7 +359,7 @@ def test_split_attention_partial_then_resume(split):
     from paper_2512_10576_b200.decode import random_latent_rows
     n1, n2 = split
     B, cap = 3, 4096
-    pools = PoolSet(B, 8192, cap, cap, row_bytes=1152)
+    pools = PoolSet(B, 8192, cap, cap, row_bytes=fmt)
     g = torch.Generator(device="cuda").manual_seed(17)
     lat = [random_latent_rows(cap, "cuda", g) for _ in range(B)]
     _fill_slots(pools, lat, cap)
@@ -373,7 +382,8 @@ def test_split_attention_partial_then_resume(split):
         assert np.abs(lse[b] - ref_l).max() <= 1e-2
 
 
-def test_early_gather_split_access_settle_matches_plain_access():
+@FMT
+def test_early_gather_split_access_settle_matches_plain_access(fmt):
     """Early-gather form of K3 + K4: the read-only split (misses -> staging rows), the
     gather into staging, the LRU update reporting final slots and the settle copy end in
     the same pool state and slot contents as one plain access + gather."""
@@ -384,8 +394,8 @@ def test_early_gather_split_access_settle_matches_plain_access():
     store = HostLatentStore(P, ids)
     for p in range(P):
         store.host[p].copy_(random_latent_rows(ids, "cuda"))
-    a = PoolSet(P, ids, cap, cap, row_bytes=1152, staging_rows=K)
-    b = PoolSet(P, ids, cap, cap, row_bytes=1152, staging_rows=K)
+    a = PoolSet(P, ids, cap, cap, row_bytes=fmt, staging_rows=K)
+    b = PoolSet(P, ids, cap, cap, row_bytes=fmt, staging_rows=K)
     rng = np.random.default_rng(3)
     z = lambda: torch.zeros((P, K), dtype=torch.int32, device="cuda")  # noqa: E731
     for step in range(4):
@@ -425,7 +435,7 @@ def test_early_gather_split_access_settle_matches_plain_access():
         sa = a.lookup(p, torch.as_tensor(order, device="cuda")).cpu().numpy()
         sbl = b.lookup(p, torch.as_tensor(order, device="cuda")).cpu().numpy()
         np.testing.assert_array_equal(sa, sbl)
-        np.testing.assert_array_equal(ra_rows[p, sa].view(np.uint16), rb_rows[p, sbl].view(np.uint16))
+        np.testing.assert_array_equal(ra_rows[p, sa], rb_rows[p, sbl])
     a.close()
     b.close()
     store.close()
