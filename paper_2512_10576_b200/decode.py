@@ -538,11 +538,18 @@ class DSADecodeModel:
 
     def __init__(self, num_layers: int, batch: int, context_len: int, sparse_ratio: float,
                  topk_k: int = 2048, max_new_tokens: int = 64, device=None, seed: int = 0,
-                 drift: float = 0.97, hugepages: bool = True):
+                 drift=0.97, hugepages: bool = True):
+        """``drift``: one query-drift coefficient for every layer, or one per layer (real
+        models' layers differ in step-to-step selection similarity, hence in misses —
+        what the layer-wise plan keys on)."""
+        drifts = list(drift) if isinstance(drift, (list, tuple, np.ndarray)) else [drift] * num_layers
+        if len(drifts) != num_layers:
+            raise ValueError(f"{len(drifts)} drift values for {num_layers} layers")
         self.layers = [DSADecodeLayer(batch, context_len, sparse_ratio, topk_k, max_new_tokens,
-                                      device=device, seed=seed + 7919 * i, drift=drift,
+                                      device=device, seed=seed + 7919 * i, drift=float(drifts[i]),
                                       hugepages=hugepages) for i in range(num_layers)]
         self.B, self.device = batch, self.layers[0].device
+        self.plan = None
 
     def set_schedule(self, micro: int = 2, first_frac: float | None = None) -> None:
         for layer in self.layers:
@@ -555,24 +562,44 @@ class DSADecodeModel:
     def next_queries(self):
         return [layer.next_queries() for layer in self.layers]
 
-    def capture(self, overlap: str = "dba", gather_ctas: int = 32) -> None:
-        """One eager step (advances the state), then the whole step captured as a graph."""
+    def capture(self, overlap: str = "dba", gather_ctas: int = 32, plan=None) -> None:
+        """One eager step (advances the state), then the whole step captured as a graph.
+
+        ``plan`` (a ``plan.LayerPlan``, pipeline.py:177-195): each layer is recorded with
+        its own strategy — ``"dba"`` micro-batched with the schedule's ``micro``,
+        ``"da"`` one batch, ``"none"`` sequential — instead of ``overlap`` for all."""
         d = self.device
+        if plan is not None:
+            plan.check(len(self.layers))
+        self.plan = plan
+        ovs = list(plan.strategies) if plan is not None else [overlap] * len(self.layers)
         for layer in self.layers:
             layer._alloc_static()
         s = torch.cuda.Stream(d)
         s.wait_stream(torch.cuda.current_stream(d))
         with torch.cuda.stream(s):
-            for layer in self.layers:
-                layer._device_step(overlap, gather_ctas)
+            for layer, ov in zip(self.layers, ovs):
+                layer._device_step(ov, gather_ctas)
         torch.cuda.current_stream(d).wait_stream(s)
         torch.cuda.synchronize(d)
         for layer in self.layers:
             layer.history += 1
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            for layer in self.layers:
-                layer._device_step(overlap, gather_ctas)
+            for layer, ov in zip(self.layers, ovs):
+                layer._device_step(ov, gather_ctas)
+        self._overlaps = ovs
+
+    def plan_layers(self, threshold: float, meter=None, source: str = "live miss means"):
+        """The layer-wise plan from the model's running miss means (``plan.MissMeter``:
+        the pools' own counters since its snapshot), pipeline.py:190-195."""
+        from .plan import MissMeter, plan_from_means
+        meter = meter if meter is not None else MissMeter(self)
+        return plan_from_means(meter.means(), threshold, source)
+
+    def launches_per_step(self) -> int:
+        """This library's kernel nodes in the captured step (each layer's own schedule)."""
+        return sum(layer.launches_per_step(ov) for layer, ov in zip(self.layers, self._overlaps))
 
     def step(self, queries, new_rows) -> None:
         """queries: per layer (q_idx, q); new_rows: per layer [B, 1, 656] (or one shared)."""

@@ -11,7 +11,7 @@ from paper_2512_10576_b200.transfer import HostLatentStore, gather
 
 B, cap, hist = 64, 8192, int(os.environ.get("HIST", 32768))
 M = int(os.environ.get("M", 120))
-pools = PoolSet(B, hist, cap, cap, row_bytes=1152)
+pools = PoolSet(B, hist, cap, cap, row_bytes=int(os.environ.get("FMT", "1152")))
 store = HostLatentStore(B, hist, hugepages=os.environ.get("HP", "1") == "1")
 print(f"host store {store.nbytes / 2**30:.2f} GiB hugepages={store.hugepages} numa={store.numa_node}")
 store.host.random_(0, 256)

@@ -119,10 +119,25 @@ def test_multilayer_model_graph_matches_oracle_per_layer():
     """C3's DSADecodeModel: layers run back to back inside one CUDA graph; every layer
     keeps its own pools and host store and stays bit-exact on selections and cache
     accounting, within tolerance on attention."""
+    _model_chain(plan_theta=False)
+
+
+def test_layer_plan_mixed_schedules_match_oracle_per_layer():
+    """§8f.2 layer-wise plan (pipeline.py:190-195): layers with different query drift
+    (so different miss means) run two uniform DA steps, the plan from the pools' live
+    miss means puts DBA on the high-miss layers and DA elsewhere, and the graph
+    re-captured with that mixed plan stays bit-exact per layer on selections, cache
+    accounting and LRU order, within tolerance on attention."""
+    _model_chain(plan_theta=True)
+
+
+def _model_chain(plan_theta):
     from paper_2512_10576_b200.cache import pool_capacity
     from paper_2512_10576_b200.decode import DSADecodeModel, random_latent_rows
+    from paper_2512_10576_b200.plan import MissMeter
     NL, B, K, ctx, rho = 3, 2, 2048, 8192, 0.25
-    model = DSADecodeModel(NL, B, ctx, rho, K, max_new_tokens=8, seed=11)
+    drift = [0.99, 0.85, 0.95] if plan_theta else 0.97
+    model = DSADecodeModel(NL, B, ctx, rho, K, max_new_tokens=12, seed=11, drift=drift)
     model.set_schedule(2, None)
     orcs = []
     for layer in model.layers:
@@ -158,13 +173,29 @@ def test_multilayer_model_graph_matches_oracle_per_layer():
                 o.grow_capacity(pool_capacity(rho, hist))
                 o.append_generated([hist - 1])
 
-    model.capture("dba")
+    model.capture("da" if plan_theta else "dba")
     mirror(False)
+    meter = MissMeter(model)
     rows = random_latent_rows(B, "cuda").view(B, 1, 656)
     for _ in range(2):
         qs = model.next_queries()
         model.step(qs, rows)
         mirror(True, qs)
+    if plan_theta:
+        means = meter.means()
+        assert len(set(means.tolist())) == NL, means
+        theta = float(np.sort(means)[1])   # the two higher-miss layers get DBA
+        plan = model.plan_layers(theta, meter)
+        assert plan.counts() == {"dba": 2, "da": 1}, (means, plan)
+        assert plan.strategies[int(np.argmin(means))] == "da"
+        model.capture(plan=plan)
+        assert model.launches_per_step() == sum(
+            l.launches_per_step(o) for l, o in zip(model.layers, plan.strategies))
+        mirror(False)
+        for _ in range(2):
+            qs = model.next_queries()
+            model.step(qs, rows)
+            mirror(True, qs)
     model.check()
     for li, layer in enumerate(model.layers):
         out, cnt = layer.pool.lru_order()
