@@ -105,7 +105,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                    const float *__restrict__ w, const float *__restrict__ kscale,
                    const int32_t *__restrict__ lens, int B, int64_t k_ld, float *__restrict__ logits) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // offset from the shared array itself (keeps the shared address space: LDS/STS, not generic)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *qbuf = smem + (size_t)STAGES * UT_BYTES;
   Ctrl &c = *reinterpret_cast<Ctrl *>(qbuf + 2 * QT_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

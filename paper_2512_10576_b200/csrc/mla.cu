@@ -214,7 +214,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                       float sm_scale, uint16_t *__restrict__ out, float *__restrict__ lse,
                       float *__restrict__ ws_o, float *__restrict__ ws_ml, int flags, int nsplit) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // offset from the shared array itself (keeps the shared address space: LDS/STS, not generic)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sq = smem;                        // q dims 320..575, 4 SW128 blocks
   uint8_t *skv = sq + QS_BYTES;              // KS f16 KV tiles
   int32_t *ssel = reinterpret_cast<int32_t *>(skv + KS * KV_BYTES);

@@ -49,10 +49,18 @@ constexpr int NBLK = ESS_MLA_QK_DIM / 64;  // 9 dim-blocks of 64
 constexpr int QT_BLKS = 6;             // q blocks in TMEM (dims 0..383)
 constexpr int QS_BLKS = NBLK - QT_BLKS;    // 3 in shared memory (384..575)
 constexpr int NSB = 4;                 // TMEM S buffers / P tiles
-constexpr int LOOKAHEAD = NSB - 1;     // S(i+3) issues before PV(i)
-constexpr int KSS = 3;                 // S tiles
-constexpr int KSV = 4;                 // V tiles
-constexpr int NST = 3;                 // staging stages
+#ifndef ESS_MLA2_KSS  // ring depths (scratch builds sweep them; smem-bound)
+#define ESS_MLA2_KSS 2
+#define ESS_MLA2_KSV 4
+#define ESS_MLA2_NST 4
+#endif
+#ifndef ESS_MLA2_DEQ_LAG
+#define ESS_MLA2_DEQ_LAG 1
+#endif
+constexpr int DEQ_LAG = ESS_MLA2_DEQ_LAG;  // S dequantisation leads V by this many tiles
+constexpr int KSS = ESS_MLA2_KSS;      // S tiles
+constexpr int KSV = ESS_MLA2_KSV;      // V tiles
+constexpr int NST = ESS_MLA2_NST;      // staging stages
 constexpr int ROW = ESS_LATENT_ROW_BYTES;  // 656
 constexpr int OTHER = 272;             // other half's row part: 2 x 128 B NoPE + 16 B scales
 constexpr int STG_OWN = NH * ROW;      // 10496
@@ -63,10 +71,17 @@ constexpr int S_TILE = NBLK * S_BLK;   // 18 KB
 constexpr int V_BLK = NB * 128;        // [32 rows][64 dims] = 4 KB
 constexpr int V_TILE = 4 * V_BLK;      // 16 KB: this CTA's 256 of the 512 V dims
 constexpr int P_TILE = HH * 128;       // [64 heads][32 tokens] f16 in 128-B SW128 rows
-constexpr int NSOFT = 4, MMA_WARP = 4, LOAD_WARP = 5, CONV0 = 6, NCONV = 4;
-constexpr int NTHREADS = 32 * (CONV0 + NCONV);  // 320
+#ifndef ESS_MLA2_NLOAD
+#define ESS_MLA2_NLOAD 4
+#endif
+constexpr int NSOFT = 4, MMA_WARP = 4, LOAD0 = 5, NLOAD = ESS_MLA2_NLOAD, CONV0 = LOAD0 + NLOAD, NCONV = 4;
+constexpr int NTHREADS = 32 * (CONV0 + NCONV);  // 416
+constexpr int NLT = NLOAD * 32;                 // loader threads
+constexpr int OWN_CHUNKS = ROW / 16;            // 41 16-B chunks per own row
+constexpr int OTHER_CHUNKS = OTHER / 16;        // 17 per other row
 constexpr uint32_t TM_O = 0, TM_S = 256, TM_Q = 320;
 static_assert(TM_Q + QT_BLKS * 32 <= 512, "TMEM budget");
+static_assert(NST > DEQ_LAG, "staging ring must hold the V-lagged tiles");
 constexpr float RESCALE_THRESHOLD = 8.0f;
 constexpr int MLA_AWAIT = 4;           // internal flag (as in mla.cu)
 constexpr int LANDED_TAG = 1 << 24;
@@ -137,7 +152,7 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ void arrive_on(uint64_t *bar, uint32_t rank) {
   uint32_t a;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(bar)), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -194,6 +209,29 @@ __device__ __forceinline__ uint32_t scale_f16x2(float s) {
   __half2 h = __float2half2_rn(s);
   return *reinterpret_cast<uint32_t *>(&h);
 }
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+// arrive on the mbarrier once every cp.async this thread issued so far has completed
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ int ld_acquire(const int32_t *p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -212,6 +250,22 @@ __device__ __forceinline__ void wait_landed(const int32_t *p, int target) {
   fence_proxy_async_global();  // the gather's generic-proxy stores -> our bulk-copy reads
 }
 
+#ifdef ESS_MLA2_TRACE  // scratch builds: per-tile globaltimer stamps of request 0's CTA pair
+__device__ unsigned long long g_mla2_trace[2][10][72];
+#define M2TRACE(ev, i)                                                                 \
+  do {                                                                                 \
+    if (blockIdx.y == 0 && (i) < 72) {                                                 \
+      unsigned long long tt;                                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));                           \
+      g_mla2_trace[r][ev][i] = tt;                                                     \
+    }                                                                                  \
+  } while (0)
+#else
+#define M2TRACE(ev, i) \
+  do {                 \
+  } while (0)
+#endif
+
 __global__ void __launch_bounds__(NTHREADS, 1)
     sparse_mla_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const uint8_t *__restrict__ rows,
                           int64_t rows_per_pool, int pool_begin, const int32_t *__restrict__ sel_row,
@@ -220,7 +274,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                           uint16_t *__restrict__ out, float *__restrict__ lse, float *__restrict__ ws_o,
                           float *__restrict__ ws_ml, int flags, int nsplit) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // offset from the shared array itself (keeps the shared address space: LDS/STS, not generic)
+  uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *sq = smem + OFF_Q, *sS = smem + OFF_S, *sV = smem + OFF_V, *sP = smem + OFF_P;
   uint8_t *stg = smem + OFF_STG;
   Ctrl &c = *reinterpret_cast<Ctrl *>(smem + OFF_CTRL);
@@ -242,7 +297,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < NST; i++) {
-      mbar_init(&c.stg_full[i], 1);
+      mbar_init(&c.stg_full[i], NLOAD * 32);  // one cp.async completion arrive per loader thread
       mbar_init(&c.stg_empty[i], NCONV);
     }
     for (int i = 0; i < KSS; i++) {
@@ -320,6 +375,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int i = 0; i < ntiles; i++) {
       const int sb = i % NSB;
       mbar_wait(&c.s_ready[sb], (i / NSB) & 1);
+      if (t == 0) M2TRACE(4, i);
       if (i >= NSB) mbar_wait(&c.pv_done[sb], ((i - NSB) / NSB) & 1);  // P tile sb free
       tc_fence_after();
       uint32_t sr[NH];
@@ -377,6 +433,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) arrive_on(&c.p_full[sb], 0);
+      if (t == 0) M2TRACE(5, i);
     }
     // ---------------- epilogue ----------------------------------------------------
     const bool have_o = ntiles > 0;
@@ -469,8 +526,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint64_t pbase = sw128_desc(smem_u32(sP), 16, 1024);
       auto issue_s = [&](int i) {
         const int ks = i % KSS, sb = i % NSB;
-        mbar_wait(&c.s_full[ks], (i / KSS) & 1);  // both CTAs' halves of tile i dequantised
-        tc_fence_after();
+        tc_fence_after();  // s_full[ks] observed: both CTAs' halves of tile i dequantised
         const uint32_t d = tmem + TM_S + sb * NH;
 #pragma unroll
         for (int blk = 0; blk < NBLK; blk++) {
@@ -485,12 +541,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         commit2(&c.s_ready[sb]);
         commit2(&c.s_empty[ks]);
       };
-      for (int i = 0; i < LOOKAHEAD && i < ntiles; i++) issue_s(i);
-      for (int i = 0; i < ntiles; i++) {
-        if (i + LOOKAHEAD < ntiles) issue_s(i + LOOKAHEAD);
+      auto issue_pv = [&](int i) {
         const int sb = i % NSB, kv = i % KSV;
-        mbar_wait(&c.p_full[sb], (i / NSB) & 1);
-        mbar_wait(&c.v_full[kv], (i / KSV) & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 2; kk++) {
@@ -504,98 +556,175 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         commit2(&c.pv_done[sb]);
         commit2(&c.v_empty[kv]);
         if (i == ntiles - 1) commit2(&c.o_done);
+      };
+      // Issue whichever MMA group is ready, S ahead of PV by up to NSB tiles: S(ns) needs
+      // its dequantised K rows and a free TMEM S buffer (P(ns - NSB) seen, i.e.
+      // PV(ns - NSB) issued); PV(np) needs P(np) and V(np).  A fixed "S(i+3), then PV(i)"
+      // order made PV wait on rows three tiles ahead (and V dequantisation on PV).
+      int ns = 0, np = 0;
+      uint32_t spins = 0;
+      while (np < ntiles) {
+        bool progress = false;
+        if (ns < ntiles && ns < np + NSB && mbar_test_wait(&c.s_full[ns % KSS], (ns / KSS) & 1)) {
+          M2TRACE(6, ns);
+          issue_s(ns++);
+          progress = true;
+        }
+        if (np < ns && mbar_test_wait(&c.p_full[np % NSB], (np / NSB) & 1)) {
+          M2TRACE(7, np);
+          if (mbar_test_wait(&c.v_full[np % KSV], (np / KSV) & 1)) {
+            M2TRACE(8, np);
+            issue_pv(np++);
+            progress = true;
+          }
+        }
+        if (progress) spins = 0;
+        else if (++spins > ESS_SPIN_LIMIT) __trap();
       }
     }
-  } else if (warp == LOAD_WARP) {
-    // ================= row loader: one bulk copy per own row, three per other row ====
+  } else if (warp < LOAD0 + NLOAD) {
+    // ================= row loaders (2 warps): 16-B cp.async per chunk ===============
+    // Per tile this CTA stages its 16 own rows whole (41 chunks) and, of the other 16
+    // rows, the 17 chunks of its V dims (2 x 128 B NoPE + the 16-B scales).  Each
+    // thread's completion arrives on stg_full by itself (cp.async.mbarrier.arrive), so
+    // no loader waits on its own copies.  (One cp.async.bulk per row part throttled on
+    // the bulk-copy unit: 64 small copies per tile took 2.7 us.)
+    const int lt = threadIdx.x - LOAD0 * 32;  // 0..NLT-1
     const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b) * rows_per_pool * ROW;
     const int32_t *selh = sel_row + (int64_t)b * sel_stride + h0;
     const int32_t *selm = await ? sel2 + (int64_t)b * sel_stride + m0 : nullptr;
+    const uint32_t stg0 = smem_u32(stg);
     bool pending = fetched && n2t > 0;
+    // lane l holds the slot row of tile token l (padding tokens: row 0, zero-filled);
+    // the next tile's ids are loaded one tile ahead, off the copy issue's critical path
+    auto row_id = [&](int i) {
+      const int tl = i * NB + lane;
+      const int jl = tl < n ? tl : 0;
+      return jl < n1 ? __ldg(selh + jl) : (pending ? 0 : __ldg(selm + (jl - n1)));
+    };
+    int sid_next = ntiles > 0 && !(pending && NB > n1) ? row_id(0) : 0;
     for (int i = 0; i < ntiles; i++) {
       const int st = i % NST;
       mbar_wait(&c.stg_empty[st], ((i / NST) & 1) ^ 1);
+      int sidl = sid_next;
       if (pending && (i + 1) * NB > n1) {
-        wait_landed(landed + b, n2t);
+        wait_landed(landed + b, n2t);  // the fetched rows' slot ids are final only now
         pending = false;
+        sidl = row_id(i);
       }
-      if (lane == 0) mbar_arrive_expect_tx(&c.stg_full[st], STG_BYTES);
-      __syncwarp();
-      const bool own = lane < NH;
-      const int tok = i * NB + (own ? (int)r * NH + lane : (1 - (int)r) * NH + (lane - NH));
-      const int j = tok < n ? tok : 0;  // padding rows re-read row 0 (masked by the softmax)
-      const int sid = j < n1 ? __ldg(selh + j) : __ldg(selm + (j - n1));
-      const uint8_t *src = pool_rows + (int64_t)sid * ROW;
-      uint8_t *dst = stg + st * STG_BYTES;
-      if (own) {
-        bulk_load(dst + lane * ROW, src, ROW, &c.stg_full[st]);
-      } else {
-        uint8_t *o = dst + STG_OWN + (lane - NH) * OTHER;
-        bulk_load(o, src + 128 * r, 128, &c.stg_full[st]);
-        bulk_load(o + 128, src + 256 + 128 * r, 128, &c.stg_full[st]);
-        bulk_load(o + 256, src + 512, 16, &c.stg_full[st]);
+      if (lt == 0) M2TRACE(0, i);
+      if (i + 1 < ntiles && !(pending && (i + 2) * NB > n1)) sid_next = row_id(i + 1);
+      const uint32_t dst = stg0 + st * STG_BYTES;
+#pragma unroll
+      for (int k = 0; k < (NH * OWN_CHUNKS + NLT - 1) / NLT; k++) {
+        const int it = lt + NLT * k;
+        const int row = it < NH * OWN_CHUNKS ? it / OWN_CHUNKS : 0;
+        const int ch = it - row * OWN_CHUNKS;
+        const int tok = (int)r * NH + row;
+        const int sid = __shfl_sync(0xffffffffu, sidl, tok);
+        if (it < NH * OWN_CHUNKS)
+          cp_async16(dst + row * ROW + ch * 16, pool_rows + (int64_t)sid * ROW + ch * 16,
+                     i * NB + tok < n ? 16u : 0u);
       }
+#pragma unroll
+      for (int k = 0; k < (NH * OTHER_CHUNKS + NLT - 1) / NLT; k++) {
+        const int it = lt + NLT * k;
+        const int row = it < NH * OTHER_CHUNKS ? it / OTHER_CHUNKS : 0;
+        const int ch = it - row * OTHER_CHUNKS;
+        const int tok = (1 - (int)r) * NH + row;
+        const int sid = __shfl_sync(0xffffffffu, sidl, tok);
+        const int soff = ch < 8 ? 128 * (int)r + 16 * ch : (ch < 16 ? 256 + 128 * (int)r + 16 * (ch - 8) : 512);
+        if (it < NH * OTHER_CHUNKS)
+          cp_async16(dst + STG_OWN + row * OTHER + ch * 16, pool_rows + (int64_t)sid * ROW + soff,
+                     i * NB + tok < n ? 16u : 0u);
+      }
+      cp_async_arrive_noinc(&c.stg_full[st]);
+      if (lt == 0) M2TRACE(9, i);
     }
+    cp_async_wait_all();
   } else {
     // ================= dequantisers (4 warps): staging -> S tile, V tile ==============
+    // Loads of an item group are issued together before any convert / store, and the
+    // two 16-B halves of each dequantised chunk are stored in lane-dependent order so a
+    // quarter warp's SW128 stores hit 8 distinct bank groups.
     const int ct = threadIdx.x - CONV0 * 32;  // 0..127
-    for (int i = 0; i < ntiles; i++) {
-      const int st = i % NST, ks = i % KSS, kv = i % KSV;
+    const int wq = ct >> 5;                   // 0..3
+    const uint32_t stg0 = smem_u32(stg), sS0 = smem_u32(sS), sV0 = smem_u32(sV);
+    // S rows of tile j are dequantised DEQ_LAG tiles ahead of its V rows, so the score
+    // MMAs never wait behind a V tile that waits on an earlier PV
+    auto deq_s = [&](int i) {
+      const int st = i % NST, ks = i % KSS;
       mbar_wait(&c.stg_full[st], (i / NST) & 1);
+      if (ct == 0) M2TRACE(1, i);
       if (i >= KSS) mbar_wait(&c.s_empty[ks], ((i - KSS) / KSS) & 1);
-      const uint8_t *src = stg + st * STG_BYTES;
-      // own 16 rows x (32 NoPE chunks + 8 RoPE chunks) -> S tile [16 rows][576] SW128
-      uint8_t *sd = sS + ks * S_TILE;
+      const uint32_t src = stg0 + st * STG_BYTES;
+      const uint32_t sd = sS0 + ks * S_TILE;
+      {  // own rows' NoPE: rows wq + 4k, chunk = lane (16 dims); RoPE: row ct / 8, chunk ct % 8
+        uint4 v[4];
+        float sc[4];
 #pragma unroll
-      for (int k = 0; k < (NH * 40) / 128; k++) {
-        const int it = ct + 128 * k;
-        const int row = it / 40, ch = it % 40;
-        const uint8_t *rp = src + row * ROW;
-        if (ch < 32) {
-          const uint4 v = *reinterpret_cast<const uint4 *>(rp + ch * 16);
-          const float s = *reinterpret_cast<const float *>(rp + 512 + 4 * (ch >> 3));
-          uint4 a, cc;
-          deq16(v, scale_f16x2(s), a, cc);
-          const int blk = ch >> 2, c0 = (ch & 3) * 2;  // 4 NoPE chunks per 64-dim block
-          uint8_t *dr = sd + blk * S_BLK + row * 128;
-          *reinterpret_cast<uint4 *>(dr + ((c0 ^ (row & 7)) << 4)) = a;
-          *reinterpret_cast<uint4 *>(dr + (((c0 + 1) ^ (row & 7)) << 4)) = cc;
-        } else {
-          const int rc = ch - 32;  // RoPE: 8 bf16 per chunk -> block 8, chunk rc
-          const uint4 v = *reinterpret_cast<const uint4 *>(rp + 528 + rc * 16);
-          *reinterpret_cast<uint4 *>(sd + 8 * S_BLK + row * 128 + ((rc ^ (row & 7)) << 4)) = cvt8_bf16_f16_sat(v);
+        for (int k = 0; k < 4; k++) {
+          const uint32_t rp = src + (wq + 4 * k) * ROW;
+          v[k] = lds128(rp + lane * 16);
+          sc[k] = lds_f32(rp + 512 + 4 * (lane >> 3));
         }
+        const int rrow = ct >> 3, rc = ct & 7;
+        const uint4 rv = lds128(src + rrow * ROW + 528 + rc * 16);
+        const int blk = lane >> 2, c0 = (lane & 3) * 2, odd = blk & 1;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const int row = wq + 4 * k;
+          uint4 lo, hi;
+          deq16(v[k], scale_f16x2(sc[k]), lo, hi);
+          const uint32_t dr = sd + blk * S_BLK + row * 128;
+          const uint32_t a0 = dr + ((c0 ^ (row & 7)) << 4), a1 = dr + (((c0 + 1) ^ (row & 7)) << 4);
+          sts128(odd ? a1 : a0, odd ? hi : lo);
+          sts128(odd ? a0 : a1, odd ? lo : hi);
+        }
+        sts128(sd + 8 * S_BLK + rrow * 128 + ((rc ^ (rrow & 7)) << 4), cvt8_bf16_f16_sat(rv));
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) arrive_on(&c.s_full[ks], 0);
-      // V: 32 tokens x this CTA's 256 NoPE dims (16 chunks) -> V tile [32][4 x 64] SW128
+      if (ct == 0) M2TRACE(2, i);
+    };
+    auto deq_v = [&](int i) {
+      const int st = i % NST, kv = i % KSV;
+      const uint32_t src = stg0 + st * STG_BYTES;
+      // V: 32 tokens x this CTA's 256 NoPE dims (16 chunks) -> V tile [32][4 x 64] SW128;
+      // item k: token (ct / 16) + 8k (tokens 16r..16r+15 are this CTA's own rows), chunk ct % 16
       if (i >= KSV) mbar_wait(&c.v_empty[kv], ((i - KSV) / KSV) & 1);
-      uint8_t *vd = sV + kv * V_TILE;
+      const uint32_t vd = sV0 + kv * V_TILE;
+      const int ch = ct & 15;
+      {
+        uint4 v[4];
+        float sc[4];
 #pragma unroll
-      for (int k = 0; k < (NB * 16) / 128; k++) {
-        const int it = ct + 128 * k;
-        const int tok = it >> 4, ch = it & 15;  // ch < 8: dims 128r + 16ch; else 256 + 128r + 16(ch-8)
-        const bool own = (tok >> 4) == (int)r;
-        const int jr = tok & (NH - 1);
-        uint4 v;
-        float s;
-        if (own) {
-          const uint8_t *rp = src + jr * ROW;
-          const int cabs = (ch < 8 ? 8 * (int)r : 16 + 8 * (int)r) + (ch & 7);
-          v = *reinterpret_cast<const uint4 *>(rp + cabs * 16);
-          s = *reinterpret_cast<const float *>(rp + 512 + 4 * (cabs >> 3));
-        } else {
-          const uint8_t *rp = src + STG_OWN + jr * OTHER;
-          v = *reinterpret_cast<const uint4 *>(rp + ch * 16);
-          s = *reinterpret_cast<const float *>(rp + 256 + 4 * (ch < 8 ? (int)r : 2 + (int)r));
+        for (int k = 0; k < 4; k++) {
+          const int tok = (ct >> 4) + 8 * k;
+          const int jr = tok & (NH - 1);
+          if ((tok >> 4) == (int)r) {  // warp-uniform
+            const int cabs = (ch < 8 ? 8 * (int)r : 16 + 8 * (int)r) + (ch & 7);
+            const uint32_t rp = src + jr * ROW;
+            v[k] = lds128(rp + cabs * 16);
+            sc[k] = lds_f32(rp + 512 + 4 * (cabs >> 3));
+          } else {
+            const uint32_t rp = src + STG_OWN + jr * OTHER;
+            v[k] = lds128(rp + ch * 16);
+            sc[k] = lds_f32(rp + 256 + 4 * (ch < 8 ? (int)r : 2 + (int)r));
+          }
         }
-        uint4 a, cc;
-        deq16(v, scale_f16x2(s), a, cc);
-        const int vb = ch >> 2, c0 = (ch & 3) * 2;
-        uint8_t *dr = vd + vb * V_BLK + tok * 128;
-        *reinterpret_cast<uint4 *>(dr + ((c0 ^ (tok & 7)) << 4)) = a;
-        *reinterpret_cast<uint4 *>(dr + (((c0 + 1) ^ (tok & 7)) << 4)) = cc;
+        const int vb = ch >> 2, c0 = (ch & 3) * 2, odd = vb & 1;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const int tok = (ct >> 4) + 8 * k;
+          uint4 lo, hi;
+          deq16(v[k], scale_f16x2(sc[k]), lo, hi);
+          const uint32_t dr = vd + vb * V_BLK + tok * 128;
+          const uint32_t a0 = dr + ((c0 ^ (tok & 7)) << 4), a1 = dr + (((c0 + 1) ^ (tok & 7)) << 4);
+          sts128(odd ? a1 : a0, odd ? hi : lo);
+          sts128(odd ? a0 : a1, odd ? lo : hi);
+        }
       }
       fence_proxy_async_smem();
       __syncwarp();
@@ -603,6 +732,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         arrive_on(&c.v_full[kv], 0);
         mbar_arrive(&c.stg_empty[st]);
       }
+      if (ct == 0) M2TRACE(3, i);
+    };
+    for (int it = 0; it < ntiles + DEQ_LAG; it++) {
+      if (it < ntiles) deq_s(it);
+      if (it >= DEQ_LAG) deq_v(it - DEQ_LAG);
     }
   }
   tc_fence_before();
@@ -616,6 +750,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 }
 
 }  // namespace
+
+#ifdef ESS_MLA2_TRACE
+extern "C" int ess_debug_mla2_trace(unsigned long long *dst) {
+  return cudaMemcpyFromSymbol(dst, g_mla2_trace, sizeof(g_mla2_trace)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 // launched by mla.cu's entry points when the pool keeps 656-B slot rows
 int ess_launch_mla_fp8(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_t *d_sel_row,
