@@ -636,13 +636,33 @@ def run_model(args, cfg):
     B, L, rho, NL = cfg["batch"], cfg["context_len"], cfg["sparse_ratio"], cfg["layers"]
     W, K = args.warmup, args.steps
     t_setup = time.perf_counter()
-    model = DSADecodeModel(NL, B, L, rho, TOPK, max_new_tokens=W + K + 8, device=dev,
-                           seed=1234 + 100003 * rank, drift=args.drift)
+    drift = args.drift
+    if args.layer_drift:  # per-layer query drift, linearly spaced (layers differ in misses)
+        lo, hi = (float(x) for x in args.layer_drift.split(","))
+        drift = [lo + (hi - lo) * i / max(1, NL - 1) for i in range(NL)]
+    # uniform-schedule steps before the timed ones: they feed the plan's miss means (and
+    # with --pre-steps put uniform runs at the same decode position as planned ones)
+    plan_w = max(W if args.plan_theta is not None else 0, args.pre_steps)
+    model = DSADecodeModel(NL, B, L, rho, TOPK, max_new_tokens=W + K + plan_w + 8, device=dev,
+                           seed=1234 + 100003 * rank, drift=drift)
     model.set_schedule(args.micro, args.first)
     model.prefill_warmup(windows=32)
     rows = random_latent_rows(B, dev).view(B, 1, 656)
     model.capture(args.overlap, args.gather_ctas)
-    queries = [model.next_queries() for _ in range(W + K)]
+    queries = [model.next_queries() for _ in range(W + K + plan_w)]
+    plan = layer_means = None
+    if plan_w:
+        # the layer-wise plan (pipeline.py:190-195) from the pools' live miss means over
+        # W uniform-schedule steps, then the step re-captured with each layer's strategy
+        from paper_2512_10576_b200.plan import MissMeter
+        meter = MissMeter(model)
+        for t in range(plan_w):
+            model.step(queries[W + K + t], rows)
+        torch.cuda.synchronize()
+        layer_means = meter.means().tolist()
+        if args.plan_theta is not None:
+            plan = model.plan_layers(args.plan_theta, meter)
+            model.capture(plan=plan, gather_ctas=args.gather_ctas)
     for t in range(1, W):
         model.step(queries[t], rows)
     torch.cuda.synchronize()
@@ -664,7 +684,7 @@ def run_model(args, cfg):
     model.check("bench")
     h, m = (x - y for x, y in zip(model.access_totals(), (h0, m0)))
     tokens_total, t_max = aggregate(B * K, step_ms * K / 1e3, device=agg_dev)
-    launches = model.layers[0].launches_per_step(args.overlap) * NL * K
+    launches = model.launches_per_step() * K
     model.close()
     if rank == 0:
         print(json.dumps({
@@ -682,7 +702,11 @@ def run_model(args, cfg):
             "misses_per_request_layer_step": m / (B * K * NL),
             "gpu_launches": launches,
             "cuda_graph": True, "clocks": clocks.summary(), "setup_s": setup_s,
-            "e2e": None, "note": "secondary config: per-kernel roofline, e2e and CPU leg on c2/c4"}),
+            "e2e": None, "note": "secondary config: per-kernel roofline, e2e and CPU leg on c2/c4",
+            "layer_drift": args.layer_drift,
+            "pre_steps": plan_w, "layer_miss_means": layer_means,
+            "plan": None if plan is None else {
+                "theta": plan.threshold, "counts": plan.counts(), "strategies": plan.strategies}}),
             flush=True)
     if world > 1:
         dist.barrier()
@@ -746,6 +770,12 @@ def main():
     ap.add_argument("--no-sub", dest="sub", action="store_false",
                     help="skip the sub-records (C4 at 128K + its ceiling, drift 0.9); N=1 only")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--plan-theta", type=float, default=None,
+                    help="multi-layer configs: layer-wise DA/DBA plan at this miss threshold")
+    ap.add_argument("--pre-steps", type=int, default=0,
+                    help="multi-layer configs: untimed uniform-schedule steps before the timed ones")
+    ap.add_argument("--layer-drift", default=None,
+                    help="multi-layer configs: 'lo,hi' per-layer query drift, linearly spaced")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
