@@ -26,6 +26,8 @@
 // domain with lazy O rescaling when the running max grows by > 8), w4 TMEM alloc +
 // MMA issuer (S = Q K^T: M=128, N=32, 36 x K=16; O += P V: M=128, N=256, V read as
 // the MN-major view of the same tile), w5-8 row loaders.
+#include <cstdlib>
+
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -714,11 +716,11 @@ __global__ void __launch_bounds__(128) mla_combine_kernel(const float *__restric
 
 }  // namespace
 
-int ess_launch_mla_fp8(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_t *d_sel_row,
-                       const int32_t *d_sel2, int32_t *d_landed, int32_t sel_stride,
-                       const int32_t *d_count, int32_t count_stride, int32_t batch, float sm_scale,
-                       void *d_out, float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags,
-                       int32_t nsplit, void *stream);  // mla2.cu
+int ess_launch_mla_pair(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_t *d_sel_row,
+                        const int32_t *d_sel2, int32_t *d_landed, int32_t sel_stride,
+                        const int32_t *d_count, int32_t count_stride, int32_t batch, float sm_scale,
+                        void *d_out, float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags,
+                        int32_t nsplit, void *stream);  // mla2.cu
 
 namespace {
 
@@ -727,8 +729,13 @@ int launch_mla(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_
                const int32_t *d_count, int32_t count_stride, int32_t batch, float sm_scale,
                void *d_out, float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags,
                int32_t nsplit, void *stream) {
-  if (pool->row_bytes == ESS_SLOT_ROW_BYTES_FP8) {  // raw-row slots: the CTA-pair FP8 kernel
-    int rc = ess_launch_mla_fp8(pool, pool_begin, d_q, d_sel_row, d_sel2, d_landed, sel_stride, d_count,
+  // raw-row (FP8) slots: the CTA-pair kernel; f16 slots: the CTA pair when ESS_K5_PAIR=1
+  static const bool pair_f16 = [] {
+    const char *e = getenv("ESS_K5_PAIR");
+    return e && e[0] == '1';
+  }();
+  if (pool->row_bytes == ESS_SLOT_ROW_BYTES_FP8 || pair_f16) {
+    int rc = ess_launch_mla_pair(pool, pool_begin, d_q, d_sel_row, d_sel2, d_landed, sel_stride, d_count,
                                 count_stride, batch, sm_scale, d_out, d_lse, d_ws_o, d_ws_ml, flags, nsplit,
                                 stream);
     if (rc != ESS_OK) return rc;

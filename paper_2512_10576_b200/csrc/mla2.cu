@@ -88,10 +88,19 @@ constexpr int LANDED_TAG = 1 << 24;
 constexpr uint32_t IDESC_S = make_idesc(0, 0, HEADS, NB, 0, 0);
 constexpr uint32_t IDESC_PV = make_idesc(0, 0, HEADS, 256, 0, 1 /* B MN-major */);
 
+// f16 slot rows (1152 B, dequantised on admission): no staging or dequantisers; the
+// loaders cp.async each CTA's 16 own rows straight into an S tile and its 256 V dims of
+// all 32 rows into a V tile (one stage = both), 4 stages
+constexpr int F_NST = 4, F_NLOAD = 4;
+constexpr int F_NTHREADS = 32 * (LOAD0 + F_NLOAD);  // 288
+constexpr int F_ROW = ESS_SLOT_ROW_BYTES;           // 1152
+constexpr int MAXR = 4;                              // barrier array size of every ring
+static_assert(KSS <= MAXR && KSV <= MAXR && NST <= MAXR && F_NST <= MAXR, "ring barrier arrays");
 struct Ctrl {
-  uint64_t stg_full[NST], stg_empty[NST];
-  uint64_t s_full[KSS], s_empty[KSS];   // s_full/v_full/p_full: rank 0's gate the MMAs
-  uint64_t v_full[KSV], v_empty[KSV];
+  uint64_t stg_full[MAXR], stg_empty[MAXR];
+  uint64_t s_full[MAXR], s_empty[MAXR];   // s_full/v_full/p_full: rank 0's gate the MMAs
+  uint64_t v_full[MAXR], v_empty[MAXR];
+  uint64_t ld_full[MAXR];                 // f16 rows: this CTA's cp.async of a stage landed
   uint64_t s_ready[NSB], p_full[NSB], pv_done[NSB];
   uint64_t o_done, q_full;
   uint32_t tmem;
@@ -107,6 +116,12 @@ constexpr size_t SMEM_BYTES = 1024 + OFF_CTRL + sizeof(Ctrl);
 static_assert(SMEM_BYTES <= 232448, "K5 (FP8) shared memory over the sm_100 limit");
 static_assert(QT_BLKS * QBLK <= KSV * V_TILE, "q staging for TMEM fits the V ring");
 static_assert(OFF_S % 1024 == 0 && OFF_V % 1024 == 0 && OFF_P % 1024 == 0, "SW128 alignment");
+constexpr size_t F_OFF_V = OFF_S + F_NST * S_TILE;
+constexpr size_t F_OFF_P = F_OFF_V + F_NST * V_TILE;
+constexpr size_t F_OFF_CTRL = F_OFF_P + NSB * P_TILE;
+constexpr size_t F_SMEM_BYTES = 1024 + F_OFF_CTRL + sizeof(Ctrl);
+static_assert(F_SMEM_BYTES <= 232448, "K5 (f16 pair) shared memory over the sm_100 limit");
+static_assert(QT_BLKS * QBLK <= F_NST * V_TILE && F_OFF_V % 1024 == 0 && F_OFF_P % 1024 == 0, "f16 layout");
 
 // ---- cta_group::2 PTX --------------------------------------------------------------
 __device__ __forceinline__ void mma2_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -266,8 +281,9 @@ __device__ unsigned long long g_mla2_trace[2][10][72];
   } while (0)
 #endif
 
-__global__ void __launch_bounds__(NTHREADS, 1)
-    sparse_mla_fp8_kernel(const __grid_constant__ CUtensorMap tm_q, const uint8_t *__restrict__ rows,
+template <bool F16>
+__global__ void __launch_bounds__(F16 ? F_NTHREADS : NTHREADS, 1)
+    sparse_mla_pair_kernel(const __grid_constant__ CUtensorMap tm_q, const uint8_t *__restrict__ rows,
                           int64_t rows_per_pool, int pool_begin, const int32_t *__restrict__ sel_row,
                           const int32_t *__restrict__ sel2, int32_t *landed, int sel_stride,
                           const int32_t *__restrict__ counts, int count_stride, float sm_scale,
@@ -276,9 +292,12 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   // offset from the shared array itself (keeps the shared address space: LDS/STS, not generic)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t *sq = smem + OFF_Q, *sS = smem + OFF_S, *sV = smem + OFF_V, *sP = smem + OFF_P;
+  constexpr int KS_S = F16 ? F_NST : KSS, KS_V = F16 ? F_NST : KSV;  // S / V tile rings
+  constexpr int NTH = F16 ? F_NTHREADS : NTHREADS;
+  uint8_t *sq = smem + OFF_Q, *sS = smem + OFF_S, *sV = smem + (F16 ? F_OFF_V : OFF_V);
+  uint8_t *sP = smem + (F16 ? F_OFF_P : OFF_P);
   uint8_t *stg = smem + OFF_STG;
-  Ctrl &c = *reinterpret_cast<Ctrl *>(smem + OFF_CTRL);
+  Ctrl &c = *reinterpret_cast<Ctrl *>(smem + (F16 ? F_OFF_CTRL : OFF_CTRL));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t r = cluster_rank();         // 0: issues the MMAs
   const int split = blockIdx.y % nsplit;
@@ -295,7 +314,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   const bool fetched = m1 > m0;
   const int ntiles = (n + NB - 1) / NB;
 
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && F16) {
+    for (int i = 0; i < F_NST; i++) {
+      mbar_init(&c.ld_full[i], F_NLOAD * 32);  // one cp.async completion arrive per loader thread
+      mbar_init(&c.s_full[i], 1);              // rank 0: the peer's relay (its stage landed)
+      mbar_init(&c.v_empty[i], 1);             // PV(i) done: stage free in both CTAs
+    }
+  }
+  if (threadIdx.x == 0 && !F16) {
     for (int i = 0; i < NST; i++) {
       mbar_init(&c.stg_full[i], NLOAD * 32);  // one cp.async completion arrive per loader thread
       mbar_init(&c.stg_empty[i], NCONV);
@@ -308,6 +334,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       mbar_init(&c.v_full[i], 2 * NCONV);
       mbar_init(&c.v_empty[i], 1);
     }
+  }
+  if (threadIdx.x == 0) {
     for (int i = 0; i < NSB; i++) {
       mbar_init(&c.s_ready[i], 1);
       mbar_init(&c.p_full[i], 2 * NSOFT);
@@ -353,7 +381,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     tmem_st_wait();
   } else {
     uint4 *qs = reinterpret_cast<uint4 *>(sq);
-    for (int u = threadIdx.x - NSOFT * 32; u < QS_BLKS * QBLK / 16; u += NTHREADS - NSOFT * 32)
+    for (int u = threadIdx.x - NSOFT * 32; u < QS_BLKS * QBLK / 16; u += NTH - NSOFT * 32)
       qs[u] = cvt8_bf16_f16_sat(qs[u]);
     fence_proxy_async_smem();
   }
@@ -525,8 +553,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const uint64_t vbase = sw128_desc(smem_u32(sV), V_BLK, 1024);
       const uint64_t pbase = sw128_desc(smem_u32(sP), 16, 1024);
       auto issue_s = [&](int i) {
-        const int ks = i % KSS, sb = i % NSB;
-        tc_fence_after();  // s_full[ks] observed: both CTAs' halves of tile i dequantised
+        const int ks = i % KS_S, sb = i % NSB;
+        tc_fence_after();  // s_full[ks] observed: both CTAs' halves of tile i in shared memory
         const uint32_t d = tmem + TM_S + sb * NH;
 #pragma unroll
         for (int blk = 0; blk < NBLK; blk++) {
@@ -539,10 +567,10 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         }
         commit2(&c.s_ready[sb]);
-        commit2(&c.s_empty[ks]);
+        if (!F16) commit2(&c.s_empty[ks]);  // f16: the stage frees with its V tile (after PV)
       };
       auto issue_pv = [&](int i) {
-        const int sb = i % NSB, kv = i % KSV;
+        const int sb = i % NSB, kv = i % KS_V;
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 2; kk++) {
@@ -565,14 +593,16 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       uint32_t spins = 0;
       while (np < ntiles) {
         bool progress = false;
-        if (ns < ntiles && ns < np + NSB && mbar_test_wait(&c.s_full[ns % KSS], (ns / KSS) & 1)) {
+        if (ns < ntiles && ns < np + NSB && mbar_test_wait(&c.s_full[ns % KS_S], (ns / KS_S) & 1) &&
+            (!F16 || mbar_test_wait(&c.ld_full[ns % KS_S], (ns / KS_S) & 1))) {
           M2TRACE(6, ns);
+          if (F16) fence_proxy_async_smem();  // this CTA's cp.async rows -> tensor-core reads
           issue_s(ns++);
           progress = true;
         }
         if (np < ns && mbar_test_wait(&c.p_full[np % NSB], (np / NSB) & 1)) {
           M2TRACE(7, np);
-          if (mbar_test_wait(&c.v_full[np % KSV], (np / KSV) & 1)) {
+          if (F16 || mbar_test_wait(&c.v_full[np % KSV], (np / KSV) & 1)) {
             M2TRACE(8, np);
             issue_pv(np++);
             progress = true;
@@ -581,7 +611,66 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         if (progress) spins = 0;
         else if (++spins > ESS_SPIN_LIMIT) __trap();
       }
+    } else if (F16 && r == 1 && elect_one()) {
+      // relay: each stage this CTA's loaders filled -> rank 0's s_full (the MMA reads
+      // both CTAs' tiles); the proxy fence orders the cp.async writes before the MMA reads
+      for (int i = 0; i < ntiles; i++) {
+        mbar_wait(&c.ld_full[i % F_NST], (i / F_NST) & 1);
+        fence_proxy_async_smem();
+        arrive_on(&c.s_full[i % F_NST], 0);
+      }
     }
+  } else if (F16) {
+    // ================= f16 rows: 4 loader warps, cp.async straight into the tiles ===
+    // Per tile: the 16 own rows whole (72 chunks of 8 dims) -> S tile [16][9 x 64 dims];
+    // this CTA's 256 V dims (chunks 16r..16r+15 and 32+16r..32+16r+15) of all 32 rows ->
+    // V tile [32][4 x 64 dims]; SW128 positions (8 lanes = one 128-B row: no conflicts)
+    const int lt = threadIdx.x - LOAD0 * 32;  // 0..127
+    const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b) * rows_per_pool * F_ROW;
+    const int32_t *selh = sel_row + (int64_t)b * sel_stride + h0;
+    const int32_t *selm = await ? sel2 + (int64_t)b * sel_stride + m0 : nullptr;
+    const uint32_t sS0 = smem_u32(sS), sV0 = smem_u32(sV);
+    bool pending = fetched && n2t > 0;
+    auto row_id = [&](int i) {
+      const int tl = i * NB + lane;
+      const int jl = tl < n ? tl : 0;
+      return jl < n1 ? __ldg(selh + jl) : (pending ? 0 : __ldg(selm + (jl - n1)));
+    };
+    int sid_next = ntiles > 0 && !(pending && NB > n1) ? row_id(0) : 0;
+    for (int i = 0; i < ntiles; i++) {
+      const int st = i % F_NST;
+      mbar_wait(&c.v_empty[st], ((i / F_NST) & 1) ^ 1);
+      int sidl = sid_next;
+      if (pending && (i + 1) * NB > n1) {
+        wait_landed(landed + b, n2t);
+        pending = false;
+        sidl = row_id(i);
+      }
+      if (lt == 0) M2TRACE(0, i);
+      if (i + 1 < ntiles && !(pending && (i + 2) * NB > n1)) sid_next = row_id(i + 1);
+      const uint32_t sd = sS0 + st * S_TILE, vd = sV0 + st * V_TILE;
+#pragma unroll
+      for (int k = 0; k < NH * 72 / 128; k++) {  // 9
+        const int it = lt + 128 * k;
+        const int row = it / 72, ch = it - row * 72;
+        const int tok = (int)r * NH + row;
+        const int sid = __shfl_sync(0xffffffffu, sidl, tok);
+        cp_async16(sd + (ch >> 3) * S_BLK + row * 128 + (((ch & 7) ^ (row & 7)) << 4),
+                   pool_rows + (int64_t)sid * F_ROW + ch * 16, i * NB + tok < n ? 16u : 0u);
+      }
+#pragma unroll
+      for (int k = 0; k < NB * 32 / 128; k++) {  // 8
+        const int it = lt + 128 * k;
+        const int tok = it >> 5, cc = it & 31;
+        const int sid = __shfl_sync(0xffffffffu, sidl, tok);
+        const int ch = (cc < 16 ? 16 * (int)r : 32 + 16 * (int)r) + (cc & 15);
+        cp_async16(vd + (cc >> 3) * V_BLK + tok * 128 + (((cc & 7) ^ (tok & 7)) << 4),
+                   pool_rows + (int64_t)sid * F_ROW + ch * 16, i * NB + tok < n ? 16u : 0u);
+      }
+      cp_async_arrive_noinc(&c.ld_full[st]);
+      if (lt == 0) M2TRACE(9, i);
+    }
+    cp_async_wait_all();
   } else if (warp < LOAD0 + NLOAD) {
     // ================= row loaders (2 warps): 16-B cp.async per chunk ===============
     // Per tile this CTA stages its 16 own rows whole (41 chunks) and, of the other 16
@@ -642,7 +731,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       if (lt == 0) M2TRACE(9, i);
     }
     cp_async_wait_all();
-  } else {
+  } else if (!F16) {
     // ================= dequantisers (4 warps): staging -> S tile, V tile ==============
     // Loads of an item group are issued together before any convert / store, and the
     // two 16-B halves of each dequantised chunk are stored in lane-dependent order so a
@@ -757,12 +846,13 @@ extern "C" int ess_debug_mla2_trace(unsigned long long *dst) {
 }
 #endif
 
-// launched by mla.cu's entry points when the pool keeps 656-B slot rows
-int ess_launch_mla_fp8(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_t *d_sel_row,
-                       const int32_t *d_sel2, int32_t *d_landed, int32_t sel_stride,
-                       const int32_t *d_count, int32_t count_stride, int32_t batch, float sm_scale,
-                       void *d_out, float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags,
-                       int32_t nsplit, void *stream) {
+// launched by mla.cu's entry points: the FP8 kernel for 656-B slot rows, the f16 pair
+// kernel for 1152-B rows
+int ess_launch_mla_pair(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_t *d_sel_row,
+                        const int32_t *d_sel2, int32_t *d_landed, int32_t sel_stride,
+                        const int32_t *d_count, int32_t count_stride, int32_t batch, float sm_scale,
+                        void *d_out, float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags,
+                        int32_t nsplit, void *stream) {
   // q as a [batch * 128 heads][576] bf16 tensor, boxes of [64 heads][64 dims], SW128
   struct QMap {
     const void *base = nullptr;
@@ -785,11 +875,14 @@ int ess_launch_mla_fp8(ess_pool *pool, int32_t pool_begin, const void *d_q, cons
     qm.dev = dev;
     qm.map = tq;
   }
-  if (int rc = ess_smem_optin((const void *)sparse_mla_fp8_kernel, SMEM_BYTES)) return rc;
+  const bool f16 = pool->row_bytes == ESS_SLOT_ROW_BYTES;
+  const void *fn = f16 ? (const void *)sparse_mla_pair_kernel<true> : (const void *)sparse_mla_pair_kernel<false>;
+  const size_t smem = f16 ? F_SMEM_BYTES : SMEM_BYTES;
+  if (int rc = ess_smem_optin(fn, smem)) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(2, (unsigned)(batch * nsplit));
-  cfg.blockDim = dim3(NTHREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.blockDim = dim3(f16 ? F_NTHREADS : NTHREADS);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = (cudaStream_t)stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -798,9 +891,15 @@ int ess_launch_mla_fp8(ess_pool *pool, int32_t pool_begin, const void *d_q, cons
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, sparse_mla_fp8_kernel, tq, (const uint8_t *)pool->rows,
-                                  pool->rows_per_pool, (int)pool_begin, d_sel_row, d_sel2, d_landed,
-                                  (int)sel_stride, d_count, (int)count_stride, sm_scale, (uint16_t *)d_out,
-                                  d_lse, d_ws_o, d_ws_ml, (int)flags, (int)nsplit));
+  if (f16)
+    ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, sparse_mla_pair_kernel<true>, tq, (const uint8_t *)pool->rows,
+                                    pool->rows_per_pool, (int)pool_begin, d_sel_row, d_sel2, d_landed,
+                                    (int)sel_stride, d_count, (int)count_stride, sm_scale, (uint16_t *)d_out,
+                                    d_lse, d_ws_o, d_ws_ml, (int)flags, (int)nsplit));
+  else
+    ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, sparse_mla_pair_kernel<false>, tq, (const uint8_t *)pool->rows,
+                                    pool->rows_per_pool, (int)pool_begin, d_sel_row, d_sel2, d_landed,
+                                    (int)sel_stride, d_count, (int)count_stride, sm_scale, (uint16_t *)d_out,
+                                    d_lse, d_ws_o, d_ws_ml, (int)flags, (int)nsplit));
   return ESS_OK;
 }

@@ -14,11 +14,15 @@ from paper_2512_10576_b200.cache import PoolSet  # noqa: E402
 from paper_2512_10576_b200.decode import random_latent_rows  # noqa: E402
 
 B, cap, n = int(os.environ.get("B", 64)), 8192, 2048
-pools = PoolSet(B, 32768, cap, cap, row_bytes=656)
+FMT = int(os.environ.get("FMT", "656"))
+pools = PoolSet(B, 32768, cap, cap, row_bytes=FMT)
 g = torch.Generator(device="cuda").manual_seed(0)
 rv = pools.rows_view()
 for b in range(B):
-    rv[b].copy_(random_latent_rows(cap, "cuda", g))
+    if FMT == 656:
+        rv[b].copy_(random_latent_rows(cap, "cuda", g))
+    else:
+        rv[b].copy_((torch.randn(rv[b].shape, device="cuda", generator=g) * 0.5).half())
 sel = torch.stack([torch.randperm(cap, device="cuda", generator=g)[:n] for _ in range(B)]).int()
 cnt = torch.full((B,), n, dtype=torch.int32, device="cuda")
 q = (torch.randn((B, 128, 576), device="cuda", generator=g) * 0.5).to(torch.bfloat16)
