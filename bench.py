@@ -350,7 +350,7 @@ def product_layer(cfg, dev, steps, drift=0.97, rank=0, micro=None, first=None, g
     B = len(lens)
     L = lens if not isinstance(cfg["context_len"], int) else cfg["context_len"]
     layer = DSADecodeLayer(B, L, rho, TOPK, max_new_tokens=steps + 16, device=dev,
-                           seed=1234 + rank, drift=drift)
+                           seed=1234 + rank, drift=drift, slot_format=cfg.get("slot_format"))
     layer.gather_ctas = gather_ctas
     layer.micro = cfg["micro"] if micro is None else micro
     layer.first_frac = (cfg["first"] if layer.micro == cfg["micro"] else None) if first is None else first
@@ -470,6 +470,8 @@ def measure(args, cfg, dev, rank, world, agg_dev, drift, full, peaks, peak_kind,
     hits, misses = (x - y for x, y in zip(layer.access_totals(), (hits0, misses0)))
     rec = {"value": tokens_total / t_max, "unit": "tokens/s", "ms_per_step": t_max * 1e3 / K,
            "batch_per_gpu": B, "query_drift": drift, "hit_rate": hits / max(1, hits + misses),
+           "slot_row_bytes": layer.pool.row_bytes,
+           "slot_store_gb": layer.pool.num_pools * layer.pool.rows_per_pool * layer.pool.row_bytes / 1e9,
            "misses_per_request_step": misses / (B * K), "clocks": clocks.summary(),
            "gpu_launches": layer.launches_per_step(args.overlap) * K,
            "micro_batches": layer.micro_batches(layer.micro) if args.overlap == "dba" else [(0, B)],
@@ -571,6 +573,12 @@ def run_ours(args, cfg):
             subs["c4"]["all_hbm_ceiling"] = run_ceiling(a4, c4, dev)
             subs["c4"]["all_hbm_ceiling"]["frac_of_ceiling"] = (
                 subs["c4"]["value"] / subs["c4"]["all_hbm_ceiling"]["value"])
+        # the same workload with the 656-B FP8 slot format (K5 = the CTA-pair kernel that
+        # dequantises on chip): a 25% pool then costs 25% of the latent bytes
+        f8 = {**cfg, "slot_format": "fp8"}
+        a8 = argparse.Namespace(**{**vars(args), "e2e": False})
+        subs[f"{cfg['name']}_fp8_slots"] = measure(a8, f8, dev, rank, world, agg_dev, args.drift, True, peaks,
+                                                   peak_kind, link_peak)
         lo = argparse.Namespace(**{**vars(args), "e2e": False})
         subs[f"{cfg['name']}_drift_0.9"] = measure(lo, cfg, dev, rank, world, agg_dev, 0.9, False, peaks,
                                                    peak_kind, link_peak)
@@ -592,6 +600,7 @@ def run_ours(args, cfg):
                        "context_len": main["context_len"], "sparse_ratio": cfg["sparse_ratio"],
                        "topk": TOPK, "query_drift": args.drift, "overlap": args.overlap,
                        "micro_batches": main["micro_batches"],
+                       "slot_row_bytes": main["slot_row_bytes"], "slot_store_gb": main["slot_store_gb"],
                        "parallelism": f"dp{world} (requests sharded by dp.shard_requests, no collective)",
                        "l2": "inputs larger than L2 (indexer keys + slot pool > 600 MB/GPU)",
                        "host": host_info(bound_node)},

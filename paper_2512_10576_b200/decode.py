@@ -66,10 +66,12 @@ class DSADecodeLayer:
 
     def __init__(self, batch: int, context_len, sparse_ratio: float, topk_k: int = 2048,
                  max_new_tokens: int = 64, device=None, seed: int = 0, drift: float = 0.95,
-                 sm_scale: float = DEFAULT_SM_SCALE, hugepages: bool = True):
+                 sm_scale: float = DEFAULT_SM_SCALE, hugepages: bool = True, slot_format: str | None = None):
         """``context_len``: one length for every request, or a sequence of ``batch``
         per-request lengths (mixed batches, C5); each request's pool holds
-        floor(rho * its own history) rows (cache.py:137-138)."""
+        floor(rho * its own history) rows (cache.py:137-138).  ``slot_format``: the GPU
+        slot store's row format, "f16" (1152 B, dequantised on admission) or "fp8" (the
+        656-B latent row, dequantised by K5 on chip); default ESS_SLOT_FORMAT / f16."""
         _lib.require_cuda()
         self.device = torch.device(device if device is not None else "cuda")
         if isinstance(context_len, (list, tuple, np.ndarray)):
@@ -106,7 +108,10 @@ class DSADecodeLayer:
         # manager still selects victims; needs every pool to hold a whole selection
         self.early_gather = self.cap0 >= topk_k and os.environ.get("ESS_EARLY_GATHER", "1") == "1"
         staging = topk_k if (self.cap0 < topk_k or self.early_gather) else 0
-        self.pool = PoolSet(B, self.Lmax, self.cap_max, caps, row_bytes=_lib.SLOT_ROW_BYTES,
+        if slot_format is not None and slot_format not in _lib.SLOT_FORMATS:
+            raise ValueError(f"slot_format must be one of {sorted(_lib.SLOT_FORMATS)}")
+        row_bytes = _lib.SLOT_FORMATS[slot_format] if slot_format else _lib.SLOT_ROW_BYTES
+        self.pool = PoolSet(B, self.Lmax, self.cap_max, caps, row_bytes=row_bytes,
                             staging_rows=staging, device=d)
         # drifting queries
         self._zi = torch.randn((B, 64, 128), device=d, generator=g)
