@@ -127,6 +127,17 @@ int ess_pool_access(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d
                     int32_t *d_miss_ids, int32_t *d_evicted_ids, int32_t *d_sel_row,
                     int32_t *d_hit_row, int32_t *d_miss_row, int32_t *d_counts,
                     int32_t out_stride, int32_t flags, void *stream);
+/* MTP (qtok = mtp + 1 selection sets per pool per step: recency is updated
+ * by every selected set): pool i takes sets r = i*qtok + j, j = 0..qtok-1 (d_req row r at
+ * d_req + r*req_stride, n = d_n[r]) as qtok consecutive access_steps in one launch.
+ * d_sel_row is laid out like d_req (row r: the slot row of each id of set r); the
+ * hit / miss / evicted id and row lists of a pool's sets are appended in set order in
+ * its [out_stride >= qtok * req_stride] row; d_counts [num][4] are the sums. */
+int ess_pool_access_mtp(ess_pool *pool, int32_t begin, int32_t num, int32_t qtok,
+                        const int32_t *d_req, const int32_t *d_n, int32_t req_stride,
+                        int32_t *d_hit_ids, int32_t *d_miss_ids, int32_t *d_evicted_ids,
+                        int32_t *d_sel_row, int32_t *d_hit_row, int32_t *d_miss_row,
+                        int32_t *d_counts, int32_t out_stride, int32_t flags, void *stream);
 /* Early-gather split of ess_pool_access (needs staging_rows >= 2048 and n <= capacity):
  * ess_pool_split is the read-only hit/miss split — hit rows, miss ids and STAGING rows
  * (cap_max + j) for the misses, counts (hits, misses) — so the host-link gather can
@@ -208,6 +219,18 @@ int ess_indexer_logits_ex(const void *d_q, const float *d_w, const void *d_k,
                           const float *d_kscale, const int32_t *d_len, int32_t batch,
                           int64_t k_ld, float *d_logits, int32_t max_ctas, void *stream);
 
+/* MTP decode (mtp + 1 = qtok query tokens per request, pipeline.py:213-215):
+ * q [B][qtok][64][128] e4m3, w [B][qtok][64] f32, logits [B][qtok][k_ld] f32; every token
+ * of request b scores the same len[b] cached keys (the selection universe is the cache
+ * history, trace.py:151-154).  The keys are read once per request: one tcgen05 MMA with
+ * N = 64 * qtok per key tile.  1 <= qtok <= ESS_INDEXER_MAX_QTOK; qtok = 1 is
+ * ess_indexer_logits_ex. */
+#define ESS_INDEXER_MAX_QTOK 4
+int ess_indexer_logits_mtp(const void *d_q, const float *d_w, const void *d_k,
+                           const float *d_kscale, const int32_t *d_len, int32_t batch,
+                           int32_t qtok, int64_t k_ld, float *d_logits, int32_t max_ctas,
+                           void *stream);
+
 /* ---- K2 top-k (op "indexer_topk") ---------------------------------------------- */
 /* per row: the k largest logits[b][0:len[b]) by (score desc, index asc), written
  * ascending to d_idx [B][idx_ld]; d_count[b] = min(k, len[b]) (scenario.py:110-112);
@@ -215,6 +238,11 @@ int ess_indexer_logits_ex(const void *d_q, const float *d_w, const void *d_k,
 #define ESS_TOPK_MAX_K 65535
 int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
              int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count, void *stream);
+/* MTP: batch * qtok rows (request-major: row b*qtok + j is token j of request b), each
+ * the top-k of logits[row][0:len[b]) — the K2 half of ess_indexer_logits_mtp */
+int ess_topk_mtp(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
+                 int32_t qtok, int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count,
+                 void *stream);
 /* top-k fused with ess_pool_split on the emitted selection, one launch (for cluster
  * rows > 40K tokens, rank 0 of each cluster splits): pools [pool_begin, pool_begin+batch) */
 int ess_topk_split(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
@@ -236,6 +264,8 @@ int ess_topk_split(const float *d_logits, int64_t ld, const int32_t *d_len, int3
 #define ESS_MLA_PARTIAL 1
 #define ESS_MLA_SPLIT_SHIFT 8   /* flags bits 8..11: KV splits - 1 (full mode; ws sized batch*splits) */
 #define ESS_MLA_MAX_SPLIT 8
+#define ESS_MLA_QTOK_SHIFT 12   /* flags bits 12..14: qtok - 1 (MTP): batch = pools * qtok query-token
+                                  rows, row r attends in pool pool_begin + r / qtok (q row r, out row r) */
 #define ESS_MLA_RESUME 2
 int ess_sparse_mla(ess_pool *pool, int32_t pool_begin, const void *d_q,
                    const int32_t *d_sel_row, int32_t sel_stride, const int32_t *d_count,

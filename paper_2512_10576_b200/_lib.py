@@ -33,6 +33,7 @@ SIGNATURES = {
     "ess_pool_grow": ([V, I32, I32, V, V], ctypes.c_int),
     "ess_pool_warmup": ([V, I32, I32, V, V, I32, V, V], ctypes.c_int),
     "ess_pool_access": ([V, I32, I32, V, V, I32, V, V, V, V, V, V, V, I32, I32, V], ctypes.c_int),
+    "ess_pool_access_mtp": ([V, I32, I32, I32, V, V, I32, V, V, V, V, V, V, V, I32, I32, V], ctypes.c_int),
     "ess_pool_append": ([V, I32, I32, V, V, I32, V, V], ctypes.c_int),
     "ess_pool_split": ([V, I32, I32, V, V, I32, V, V, V, V, I32, V], ctypes.c_int),
     "ess_pool_settle": ([V, I32, I32, V, V, I32, V], ctypes.c_int),
@@ -48,7 +49,9 @@ SIGNATURES = {
     "ess_write_generated": ([V, I32, I32, V, V, V, I32, V, V, I64, V], ctypes.c_int),
     "ess_indexer_logits": ([V, V, V, V, V, I32, I64, V, V], ctypes.c_int),
     "ess_indexer_logits_ex": ([V, V, V, V, V, I32, I64, V, I32, V], ctypes.c_int),
+    "ess_indexer_logits_mtp": ([V, V, V, V, V, I32, I32, I64, V, I32, V], ctypes.c_int),
     "ess_topk": ([V, I64, V, I32, I32, V, I32, V, V], ctypes.c_int),
+    "ess_topk_mtp": ([V, I64, V, I32, I32, I32, V, I32, V, V], ctypes.c_int),
     "ess_topk_split": ([V, I64, V, I32, I32, V, I32, V, V, I32, V, V, V, V, I32, V], ctypes.c_int),
     "ess_sparse_mla": ([V, I32, V, V, I32, V, I32, I32, F32, V, V, V, V, I32, V], ctypes.c_int),
     "ess_sparse_mla_da": ([V, I32, V, V, V, I32, V, I32, V, I32, F32, V, V, V], ctypes.c_int),
@@ -62,6 +65,8 @@ ESS_ERR_NOMEM, ESS_ERR_RATIO, ESS_ERR_ARG, ESS_ERR_CUDA, ESS_ERR_CLOCK = -4, -5,
 ESS_ACCESS_SORT_EVICTED = 1
 ESS_MLA_PARTIAL, ESS_MLA_RESUME = 1, 2
 ESS_MLA_SPLIT_SHIFT, ESS_MLA_MAX_SPLIT = 8, 8
+ESS_MLA_QTOK_SHIFT = 12
+MAX_QTOK = 4  # ESS_INDEXER_MAX_QTOK: query tokens per request and step (MTP width + 1)
 ESS_GATHER_EXCLUSIVE_SM = 1
 ESS_GATHER_BULK = 2
 ESS_HOST_HUGEPAGES, ESS_HOST_NUMA_BOUND = 1, 2

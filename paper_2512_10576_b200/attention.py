@@ -34,7 +34,8 @@ class SplitWorkspace:
 def sparse_mla(pool: PoolSet, q: torch.Tensor, sel_row: torch.Tensor, count: torch.Tensor,
                sm_scale: float = DEFAULT_SM_SCALE, pool_begin: int = 0,
                out: torch.Tensor | None = None, lse: torch.Tensor | None = None,
-               workspace: SplitWorkspace | None = None, mode: str = "full", split: int = 1):
+               workspace: SplitWorkspace | None = None, mode: str = "full", split: int = 1,
+               qtok: int = 1):
     """out[b, h] = softmax_j(q[b, h] . K_j * sm_scale) V_j over rows sel_row[b, :count[b]]
     of pool (pool_begin + b)'s slot store.
 
@@ -44,6 +45,8 @@ def sparse_mla(pool: PoolSet, q: torch.Tensor, sel_row: torch.Tensor, count: tor
     continues from it over further rows and returns the merged result (Attn1 + merge).
     ``split`` > 1 (full mode) cuts each request's rows into that many shares on
     2 * split CTAs and merges them (``workspace`` with ``splits >= split``): small batches.
+    ``qtok`` > 1 (MTP): q rows are (request, query token) pairs, B = requests * qtok; row r
+    attends over sel_row[r, :count[r]] in pool pool_begin + r // qtok.
     """
     _lib.require_cuda(q)
     B = q.shape[0]
@@ -52,6 +55,9 @@ def sparse_mla(pool: PoolSet, q: torch.Tensor, sel_row: torch.Tensor, count: tor
     flags = {"full": 0, "partial": _lib.ESS_MLA_PARTIAL, "resume": _lib.ESS_MLA_RESUME}[mode]
     if flags and workspace is None:
         raise ValueError(f"mode {mode!r} needs a SplitWorkspace")
+    if not 1 <= qtok <= _lib.MAX_QTOK or B % qtok:
+        raise ValueError(f"qtok must be in [1, {_lib.MAX_QTOK}] and divide the {B} query rows")
+    flags |= (qtok - 1) << _lib.ESS_MLA_QTOK_SHIFT
     if not 1 <= split <= _lib.ESS_MLA_MAX_SPLIT:
         raise ValueError(f"split must be in [1, {_lib.ESS_MLA_MAX_SPLIT}]")
     if split > 1:

@@ -157,6 +157,43 @@ class PoolSet:
             out.counts.data_ptr(), stride, flags, _lib.stream_handle()))
         return out
 
+    def access_mtp(self, req: torch.Tensor, n: torch.Tensor, begin: int = 0, lists: bool = False,
+                   sort_evicted: bool = True, out: AccessBatch | None = None,
+                   sel_row: torch.Tensor | None = None) -> AccessBatch:
+        """MTP: ``qtok`` selection sets per pool, req [num, qtok, K] / n [num, qtok] (the
+        layout of ``indexer.topk_mtp``), taken as qtok consecutive access_steps per pool in
+        one launch — recency is updated by every selected set.  ``sel_row``
+        [num, qtok, K] gets each set's slot rows; the hit/miss/evicted lists of a pool's
+        sets are appended in set order in its [num, qtok*K] rows; counts are the sums."""
+        num, qtok, K = req.shape
+        self._range(begin, num)
+        if not 1 <= qtok <= _lib.MAX_QTOK:
+            raise ValueError(f"qtok must be in [1, {_lib.MAX_QTOK}]")
+        if not req.is_contiguous() or n.shape != (num, qtok) or not n.is_contiguous():
+            raise ValueError("req must be contiguous [num, qtok, K] and n [num, qtok]")
+        if out is None:
+            z = lambda: torch.empty((num, qtok * K), dtype=torch.int32, device=self.device)  # noqa: E731
+            out = AccessBatch(counts=torch.empty((num, 4), dtype=torch.int32, device=self.device),
+                              sel_row=None, miss_ids=z(), miss_row=z(), hit_row=z(),
+                              hit_ids=z() if lists else None, evicted_ids=z() if lists else None)
+        if sel_row is None:
+            sel_row = torch.empty((num, qtok, K), dtype=torch.int32, device=self.device)
+        if sel_row.shape != (num, qtok, K) or not sel_row.is_contiguous():
+            raise ValueError("sel_row must be contiguous [num, qtok, K]")
+        lists_ = [t for t in (out.miss_ids, out.miss_row, out.hit_row, out.hit_ids, out.evicted_ids)
+                  if t is not None]
+        stride = lists_[0].stride(0) if lists_ else qtok * K
+        if any(t.stride(0) != stride or t.stride(1) != 1 for t in lists_) or stride < qtok * K:
+            raise ValueError("list outputs must share a row stride >= qtok * K")
+        flags = _lib.ESS_ACCESS_SORT_EVICTED if sort_evicted else 0
+        _lib.check(self._L.ess_pool_access_mtp(
+            self._h, begin, num, qtok, req.data_ptr(), n.data_ptr(), K,
+            _lib.ptr(out.hit_ids), _lib.ptr(out.miss_ids), _lib.ptr(out.evicted_ids),
+            sel_row.data_ptr(), _lib.ptr(out.hit_row), _lib.ptr(out.miss_row),
+            out.counts.data_ptr(), stride, flags, _lib.stream_handle()), "ess_pool_access_mtp")
+        out.sel_row = sel_row
+        return out
+
     def split(self, req: torch.Tensor, n: torch.Tensor, out: AccessBatch, begin: int = 0) -> AccessBatch:
         """Early-gather K3a: read-only hit/miss split; misses point at staging rows
         (needs staging_rows >= 2048; see ess_pool_split)."""

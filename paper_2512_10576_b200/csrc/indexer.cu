@@ -30,36 +30,49 @@ namespace {
 #define ESS_K1_STAGES (ESS_K1_SUB == 1 ? 10 : ESS_K1_SUB == 2 ? 5 : 3)
 #endif
 constexpr int TILE_M = 128;                 // tokens per MMA tile (M)
-constexpr int SUB = ESS_K1_SUB;             // MMA tiles per pipeline unit
-constexpr int UNIT_M = SUB * TILE_M;        // tokens per unit (one ring stage, one barrier round)
-constexpr int STAGES = ESS_K1_STAGES;       // unit ring depth
-constexpr int HEADS = ESS_INDEXER_HEADS;    // 64 = N
+constexpr int HEADS = ESS_INDEXER_HEADS;    // 64 heads per query token
 constexpr int DIM = ESS_INDEXER_DIM;        // 128 = K (bytes, e4m3)
 constexpr int KT_BYTES = TILE_M * DIM;      // 16 KB per MMA tile
-constexpr int UT_BYTES = SUB * KT_BYTES;    // bytes per unit
-constexpr int QT_BYTES = HEADS * DIM;       // 8 KB, one per request (double-buffered)
-constexpr int ACC_COLS = SUB * HEADS;       // TMEM columns per unit
-constexpr int NACC = 512 / ACC_COLS < 4 ? 512 / ACC_COLS : 4;  // TMEM accumulator stages
 constexpr int NEPI = 8;                     // epilogue warps: 2 groups x 4 lane quarters
 constexpr int NTHREADS = 32 * (2 + NEPI);
 constexpr int MAX_BATCH = 4096;
-constexpr int TMEM_COLS = NACC * ACC_COLS;  // 512 (SUB 2) / 256 (SUB 1)
-constexpr uint32_t IDESC = make_idesc(0 /*e4m3*/, 0 /*e4m3*/, TILE_M, HEADS, 0, 0);
 
-struct Ctrl {
-  uint64_t full[STAGES];
-  uint64_t empty[STAGES];
-  uint64_t qfull[2];
-  uint64_t qempty[2];
-  uint64_t tfull[NACC];
-  uint64_t tempty[NACC];
-  uint32_t tmem;
-  int pref[MAX_BATCH + 1];
+// Per query-token count QT (1 = plain decode; QT = mtp + 1 query tokens per request,
+// pipeline.py:213-215): the QT tokens of a request share its key stream, so one MMA
+// with N = 64 * QT (all tokens' heads) consumes each key tile once — the indexer reads
+// the keys once per request whatever the MTP width.  QT = 1 keeps the 256-token units
+// (two MMA tiles per stage); QT > 1 has QT x the epilogue work per tile, so one tile
+// per unit already amortises the barrier chain.
+template <int QT>
+struct K1Cfg {
+  static constexpr int SUB = QT == 1 ? ESS_K1_SUB : 1;         // MMA tiles per unit
+  static constexpr int UNIT_M = SUB * TILE_M;                  // tokens per unit
+  static constexpr int STAGES = QT == 1 ? ESS_K1_STAGES : (QT == 2 ? 10 : 8);
+  static constexpr int N = HEADS * QT;                         // MMA N (all tokens' heads)
+  static constexpr int UT_BYTES = SUB * KT_BYTES;
+  static constexpr int QT_BYTES = N * DIM;                     // one request's q (x2 slots)
+  static constexpr int ACC_COLS = SUB * N;                     // TMEM columns per unit
+  static constexpr int NACC = 512 / ACC_COLS < 4 ? 512 / ACC_COLS : 4;
+  static constexpr int TMEM_USED = NACC * ACC_COLS;
+  static constexpr int TMEM_COLS = TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 : TMEM_USED <= 128 ? 128
+                                   : TMEM_USED <= 256 ? 256 : 512;
+  static constexpr uint32_t IDESC = make_idesc(0 /*e4m3*/, 0 /*e4m3*/, TILE_M, N, 0, 0);
+  struct Ctrl {
+    uint64_t full[STAGES];
+    uint64_t empty[STAGES];
+    uint64_t qfull[2];
+    uint64_t qempty[2];
+    uint64_t tfull[NACC];
+    uint64_t tempty[NACC];
+    uint32_t tmem;
+    int pref[MAX_BATCH + 1];
+    alignas(16) float wq[2][QT > 1 ? QT * HEADS : 4];  // QT > 1: each epilogue group's head weights
+  };
+  static constexpr size_t SMEM_BYTES =
+      1024 /*align slack*/ + (size_t)STAGES * UT_BYTES + 2 * QT_BYTES + sizeof(Ctrl);
+  static_assert(SMEM_BYTES <= 232448, "K1 shared memory over the sm_100 limit");
+  static_assert(N <= 256 && N % 16 == 0, "MMA N out of range");
 };
-
-constexpr size_t SMEM_BYTES =
-    1024 /*align slack*/ + (size_t)STAGES * UT_BYTES + 2 * QT_BYTES + sizeof(Ctrl);
-static_assert(SMEM_BYTES <= 232448, "K1 shared memory over the sm_100 limit");
 
 #ifdef ESS_K1_PROF  // scratch builds: per-CTA globaltimer stamps (entry, setup, first unit, end)
 __device__ unsigned long long g_k1_prof[160][6];
@@ -100,15 +113,23 @@ struct TileCursor {
   }
 };
 
+__device__ __forceinline__ void group_bar(int g) {  // the 128 threads of epilogue group g
+  asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+}
+
+template <int QT>
 __global__ void __launch_bounds__(NTHREADS, 1)
     indexer_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_q,
                    const float *__restrict__ w, const float *__restrict__ kscale,
                    const int32_t *__restrict__ lens, int B, int64_t k_ld, float *__restrict__ logits) {
+  using C = K1Cfg<QT>;
+  constexpr int SUB = C::SUB, UNIT_M = C::UNIT_M, STAGES = C::STAGES, NACC = C::NACC;
+  constexpr int UT_BYTES = C::UT_BYTES, QT_BYTES = C::QT_BYTES, ACC_COLS = C::ACC_COLS;
   extern __shared__ uint8_t smem_raw[];
   // offset from the shared array itself (keeps the shared address space: LDS/STS, not generic)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *qbuf = smem + (size_t)STAGES * UT_BYTES;
-  Ctrl &c = *reinterpret_cast<Ctrl *>(qbuf + 2 * QT_BYTES);
+  typename C::Ctrl &c = *reinterpret_cast<typename C::Ctrl *>(qbuf + 2 * QT_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) K1PROF(0);
 
@@ -146,7 +167,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc<TMEM_COLS>(&c.tmem);
+  if (warp == 1) tmem_alloc<C::TMEM_COLS>(&c.tmem);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -173,7 +194,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             qs ^= 1;
             mbar_wait(&c.qempty[qs], (quse[qs] & 1) ^ 1);
             mbar_arrive_expect_tx(&c.qfull[qs], QT_BYTES);
-            tma_load_2d(qbuf + qs * QT_BYTES, &tm_q, &c.qfull[qs], 0, cur.b * HEADS);
+            tma_load_2d(qbuf + qs * QT_BYTES, &tm_q, &c.qfull[qs], 0, cur.b * C::N);
             quse[qs]++;
             prev_b = cur.b;
             len_b = min(__ldg(lens + cur.b), (int)k_ld);
@@ -225,7 +246,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             for (int kk = 0; kk < DIM / 32; kk++) {
               uint64_t ad = sw128_desc(kaddr + kk * 32, 16, 1024);
               uint64_t bd = sw128_desc(qaddr + kk * 32, 16, 1024);
-              mma_f8f6f4_ss(tmem + a * ACC_COLS + j * HEADS, ad, bd, IDESC, kk > 0 ? 1u : 0u);
+              mma_f8f6f4_ss(tmem + a * ACC_COLS + j * C::N, ad, bd, C::IDESC, kk > 0 ? 1u : 0u);
             }
           }
           tc_commit(&c.empty[s]);
@@ -243,18 +264,25 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       cur.seek(c.pref, B, t0);
       if (g == 1) cur.next(c.pref, B);
       int wb = -1, len_b = 0;
-      float wr[HEADS];
+      float wr[QT == 1 ? HEADS : 1];  // QT = 1: head weights in registers
       for (int it = g; it < ntiles; it += 2) {
         const int b = cur.b;
-        if (b != wb) {  // head weights of this request, kept in registers
-          const float4 *src = reinterpret_cast<const float4 *>(w + (int64_t)b * HEADS);
+        if (b != wb) {  // head weights of this request
+          if constexpr (QT == 1) {
+            const float4 *src = reinterpret_cast<const float4 *>(w + (int64_t)b * HEADS);
 #pragma unroll
-          for (int h4 = 0; h4 < HEADS / 4; h4++) {
-            float4 v = __ldg(src + h4);
-            wr[4 * h4] = v.x;
-            wr[4 * h4 + 1] = v.y;
-            wr[4 * h4 + 2] = v.z;
-            wr[4 * h4 + 3] = v.w;
+            for (int h4 = 0; h4 < HEADS / 4; h4++) {
+              float4 v = __ldg(src + h4);
+              wr[4 * h4] = v.x;
+              wr[4 * h4 + 1] = v.y;
+              wr[4 * h4 + 2] = v.z;
+              wr[4 * h4 + 3] = v.w;
+            }
+          } else {  // QT x 64 weights: the group's shared-memory copy (broadcast reads)
+            group_bar(g);  // every thread of the group is done with the previous request
+            for (int i = (e - 4 * g) * 32 + lane; i < QT * HEADS; i += 128)
+              c.wq[g][i] = __ldg(w + (int64_t)b * QT * HEADS + i);
+            group_bar(g);
           }
           len_b = min(__ldg(lens + b), (int)k_ld);
           wb = b;
@@ -273,25 +301,53 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         mbar_wait(&c.tfull[a], (it / NACC) & 1);
         tc_fence_after();
         if (it == 0 && threadIdx.x == 64) K1PROF(2);
+        if constexpr (QT == 1) {
 #pragma unroll
-        for (int j = 0; j < SUB; j++) {
-          uint32_t r[64];
-          tmem_ld_32x32b_x64(tmem + ((uint32_t)(quarter * 32) << 16) + a * ACC_COLS + j * HEADS, r);
-          tmem_ld_wait();
-          if (j == SUB - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&c.tempty[a]);
-          }
-          float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+          for (int j = 0; j < SUB; j++) {
+            uint32_t r[64];
+            tmem_ld_32x32b_x64(tmem + ((uint32_t)(quarter * 32) << 16) + a * ACC_COLS + j * HEADS, r);
+            tmem_ld_wait();
+            if (j == SUB - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&c.tempty[a]);
+            }
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-          for (int h = 0; h < HEADS; h += 4) {
-            a0 = fmaf(wr[h + 0], fmaxf(__uint_as_float(r[h + 0]), 0.f), a0);
-            a1 = fmaf(wr[h + 1], fmaxf(__uint_as_float(r[h + 1]), 0.f), a1);
-            a2 = fmaf(wr[h + 2], fmaxf(__uint_as_float(r[h + 2]), 0.f), a2);
-            a3 = fmaf(wr[h + 3], fmaxf(__uint_as_float(r[h + 3]), 0.f), a3);
+            for (int h = 0; h < HEADS; h += 4) {
+              a0 = fmaf(wr[h + 0], fmaxf(__uint_as_float(r[h + 0]), 0.f), a0);
+              a1 = fmaf(wr[h + 1], fmaxf(__uint_as_float(r[h + 1]), 0.f), a1);
+              a2 = fmaf(wr[h + 2], fmaxf(__uint_as_float(r[h + 2]), 0.f), a2);
+              a3 = fmaf(wr[h + 3], fmaxf(__uint_as_float(r[h + 3]), 0.f), a3);
+            }
+            if (valid[j]) logits[off[j]] = ((a0 + a1) + (a2 + a3)) * ks[j];
           }
-          if (valid[j]) logits[off[j]] = ((a0 + a1) + (a2 + a3)) * ks[j];
+        } else {
+          // one MMA tile per unit: token jq's 64 heads are columns [jq*64, jq*64+64);
+          // logits row (b, jq) of [B][QT][k_ld]
+          const float4 *wq = reinterpret_cast<const float4 *>(c.wq[g]);
+          const int64_t tok = (int64_t)cur.t * UNIT_M + row;
+#pragma unroll 1
+          for (int jq = 0; jq < QT; jq++) {
+            uint32_t r[64];
+            tmem_ld_32x32b_x64(tmem + ((uint32_t)(quarter * 32) << 16) + a * ACC_COLS + jq * HEADS, r);
+            tmem_ld_wait();
+            if (jq == QT - 1) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&c.tempty[a]);
+            }
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+            for (int h = 0; h < HEADS; h += 4) {
+              const float4 wv = wq[jq * (HEADS / 4) + h / 4];
+              a0 = fmaf(wv.x, fmaxf(__uint_as_float(r[h + 0]), 0.f), a0);
+              a1 = fmaf(wv.y, fmaxf(__uint_as_float(r[h + 1]), 0.f), a1);
+              a2 = fmaf(wv.z, fmaxf(__uint_as_float(r[h + 2]), 0.f), a2);
+              a3 = fmaf(wv.w, fmaxf(__uint_as_float(r[h + 3]), 0.f), a3);
+            }
+            if (valid[0]) logits[((int64_t)b * QT + jq) * k_ld + tok] = ((a0 + a1) + (a2 + a3)) * ks[0];
+          }
         }
         cur.next(c.pref, B);
         cur.next(c.pref, B);
@@ -302,7 +358,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
+  if (warp == 1) tmem_dealloc<C::TMEM_COLS>(tmem);
   if (threadIdx.x == 32) K1PROF(4);
 }
 
@@ -348,26 +404,51 @@ extern "C" int ess_indexer_logits(const void *d_q, const float *d_w, const void 
   return ess_indexer_logits_ex(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, 0, stream);
 }
 
+namespace {
+
+template <int QT>
+int launch_indexer(const void *d_q, const float *d_w, const void *d_k, const float *d_kscale,
+                   const int32_t *d_len, int32_t batch, int64_t k_ld, float *d_logits,
+                   int32_t max_ctas, void *stream) {
+  using C = K1Cfg<QT>;
+  static thread_local MapCache kc, qc;
+  alignas(64) CUtensorMap tk;
+  alignas(64) CUtensorMap tq;
+  if (!make_map(&tk, d_k, (uint64_t)batch * (uint64_t)k_ld, TILE_M, kc)) return ESS_ERR_CUDA;
+  if (!make_map(&tq, d_q, (uint64_t)batch * C::N, C::N, qc)) return ESS_ERR_CUDA;
+  if (int rc = ess_smem_optin((const void *)indexer_kernel<QT>, C::SMEM_BYTES)) return rc;
+  const int ctas = max_ctas > 0 && max_ctas < ess_sm_count() ? max_ctas : ess_sm_count();
+  indexer_kernel<QT><<<ctas, NTHREADS, C::SMEM_BYTES, (cudaStream_t)stream>>>(
+      tk, tq, d_w, d_kscale, d_len, batch, k_ld, d_logits);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
+}  // namespace
+
 extern "C" int ess_indexer_logits_ex(const void *d_q, const float *d_w, const void *d_k,
                                      const float *d_kscale, const int32_t *d_len, int32_t batch,
                                      int64_t k_ld, float *d_logits, int32_t max_ctas,
                                      void *stream) {
-  if (max_ctas < 0) return ESS_ERR_ARG;
+  return ess_indexer_logits_mtp(d_q, d_w, d_k, d_kscale, d_len, batch, 1, k_ld, d_logits, max_ctas,
+                                stream);
+}
+
+extern "C" int ess_indexer_logits_mtp(const void *d_q, const float *d_w, const void *d_k,
+                                      const float *d_kscale, const int32_t *d_len, int32_t batch,
+                                      int32_t qtok, int64_t k_ld, float *d_logits, int32_t max_ctas,
+                                      void *stream) {
+  if (max_ctas < 0 || qtok < 1 || qtok > ESS_INDEXER_MAX_QTOK) return ESS_ERR_ARG;
   if (!d_q || !d_w || !d_k || !d_kscale || !d_len || !d_logits || batch < 0 ||
       batch > MAX_BATCH || k_ld < TILE_M || (k_ld % TILE_M) != 0 ||
       (reinterpret_cast<uintptr_t>(d_k) & 15) || (reinterpret_cast<uintptr_t>(d_q) & 15) ||
       (reinterpret_cast<uintptr_t>(d_w) & 15))
     return ESS_ERR_ARG;
   if (batch == 0) return ESS_OK;
-  static thread_local MapCache kc, qc;
-  alignas(64) CUtensorMap tk;
-  alignas(64) CUtensorMap tq;
-  if (!make_map(&tk, d_k, (uint64_t)batch * (uint64_t)k_ld, TILE_M, kc)) return ESS_ERR_CUDA;
-  if (!make_map(&tq, d_q, (uint64_t)batch * HEADS, HEADS, qc)) return ESS_ERR_CUDA;
-  if (int rc = ess_smem_optin((const void *)indexer_kernel, SMEM_BYTES)) return rc;
-  const int ctas = max_ctas > 0 && max_ctas < ess_sm_count() ? max_ctas : ess_sm_count();
-  indexer_kernel<<<ctas, NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
-      tk, tq, d_w, d_kscale, d_len, batch, k_ld, d_logits);
-  ESS_CUDA_TRY(cudaGetLastError());
-  return ESS_OK;
+  switch (qtok) {
+    case 1: return launch_indexer<1>(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, max_ctas, stream);
+    case 2: return launch_indexer<2>(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, max_ctas, stream);
+    case 3: return launch_indexer<3>(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, max_ctas, stream);
+    default: return launch_indexer<4>(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, max_ctas, stream);
+  }
 }

@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     // straight into the SW128 position; one commit group per tile, signalled one
     // tile later (wait_group 1) so two tiles are in flight per warp ----------------
     const int w = warp - LOAD0;
-    const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b) * rows_per_pool * ESS_SLOT_ROW_BYTES;
+    const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b / (((flags >> ESS_MLA_QTOK_SHIFT) & 7) + 1)) * rows_per_pool * ESS_SLOT_ROW_BYTES;
     const uint32_t kv0 = smem_u32(skv);
     [[maybe_unused]] auto signal = [&](int i) {
       fence_proxy_async_smem();  // cp.async (generic proxy) writes -> tensor-core reads
@@ -792,20 +792,23 @@ extern "C" int ess_sparse_mla(ess_pool *pool, int32_t pool_begin, const void *d_
                               float *d_lse, float *d_ws_o, float *d_ws_ml, int32_t flags,
                               void *stream) {
   const int nsplit = ((flags >> ESS_MLA_SPLIT_SHIFT) & 0xF) + 1;
+  const int qtok = ((flags >> ESS_MLA_QTOK_SHIFT) & 7) + 1;
   flags &= ~(0xF << ESS_MLA_SPLIT_SHIFT);
+  flags &= ~(7 << ESS_MLA_QTOK_SHIFT);
+  if (qtok > ESS_INDEXER_MAX_QTOK || batch % qtok) return ESS_ERR_ARG;
   if (nsplit > ESS_MLA_MAX_SPLIT) return ESS_ERR_ARG;
   if ((flags & (ESS_MLA_PARTIAL | ESS_MLA_RESUME)) && (!d_ws_o || !d_ws_ml)) return ESS_ERR_ARG;
   if ((flags & ESS_MLA_PARTIAL) && (flags & ESS_MLA_RESUME)) return ESS_ERR_ARG;
   if (flags & ~(ESS_MLA_PARTIAL | ESS_MLA_RESUME)) return ESS_ERR_ARG;
   if (nsplit > 1 && (flags || !d_ws_o || !d_ws_ml)) return ESS_ERR_ARG;  // split: full mode only
-  if (!pool_ok(pool, pool_begin, batch) || !d_q || !d_sel_row || !d_count || count_stride < 1 ||
+  if (!pool_ok(pool, pool_begin, batch / qtok) || !d_q || !d_sel_row || !d_count || count_stride < 1 ||
       (!(flags & ESS_MLA_PARTIAL) && (!d_out || !d_lse)) || sel_stride < 1 ||
       (reinterpret_cast<uintptr_t>(d_q) & 15) || (reinterpret_cast<uintptr_t>(d_out) & 15))
     return ESS_ERR_ARG;
   if (batch == 0) return ESS_OK;
   return launch_mla(pool, pool_begin, d_q, d_sel_row, nullptr, nullptr, sel_stride, d_count,
-                    count_stride, batch, sm_scale, d_out, d_lse, d_ws_o, d_ws_ml, flags, nsplit,
-                    stream);
+                    count_stride, batch, sm_scale, d_out, d_lse, d_ws_o, d_ws_ml,
+                    flags | ((qtok - 1) << ESS_MLA_QTOK_SHIFT), nsplit, stream);
 }
 
 extern "C" int ess_sparse_mla_da(ess_pool *pool, int32_t pool_begin, const void *d_q,

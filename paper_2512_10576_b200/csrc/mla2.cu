@@ -626,7 +626,7 @@ __global__ void __launch_bounds__(F16 ? F_NTHREADS : NTHREADS, 1)
     // this CTA's 256 V dims (chunks 16r..16r+15 and 32+16r..32+16r+15) of all 32 rows ->
     // V tile [32][4 x 64 dims]; SW128 positions (8 lanes = one 128-B row: no conflicts)
     const int lt = threadIdx.x - LOAD0 * 32;  // 0..127
-    const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b) * rows_per_pool * F_ROW;
+    const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b / (((flags >> ESS_MLA_QTOK_SHIFT) & 7) + 1)) * rows_per_pool * F_ROW;
     const int32_t *selh = sel_row + (int64_t)b * sel_stride + h0;
     const int32_t *selm = await ? sel2 + (int64_t)b * sel_stride + m0 : nullptr;
     const uint32_t sS0 = smem_u32(sS), sV0 = smem_u32(sV);
@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(F16 ? F_NTHREADS : NTHREADS, 1)
     // no loader waits on its own copies.  (One cp.async.bulk per row part throttled on
     // the bulk-copy unit: 64 small copies per tile took 2.7 us.)
     const int lt = threadIdx.x - LOAD0 * 32;  // 0..NLT-1
-    const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b) * rows_per_pool * ROW;
+    const uint8_t *pool_rows = rows + (int64_t)(pool_begin + b / (((flags >> ESS_MLA_QTOK_SHIFT) & 7) + 1)) * rows_per_pool * ROW;
     const int32_t *selh = sel_row + (int64_t)b * sel_stride + h0;
     const int32_t *selm = await ? sel2 + (int64_t)b * sel_stride + m0 : nullptr;
     const uint32_t stg0 = smem_u32(stg);

@@ -329,21 +329,28 @@ __global__ void __launch_bounds__(NT, 1)
                      int32_t *miss_out, int32_t *ev_out, int32_t *sel_row_out,
                      int32_t *hit_row_out, int32_t *miss_row_out, int32_t *counts_out,
                      int out_stride, int flags,
-                     int64_t *inserted_out) {
+                     int64_t *inserted_out, int qtok, int sel_stride) {
   __shared__ StepSmem sm;
   extern __shared__ uint32_t stage_smem[];  // [cap_max] keys (STAGED)
   const int t = threadIdx.x;
   const int b = blockIdx.x;
   const int p = begin + b;
-  const int n = req_n[b];
   PoolMeta *meta = pv.meta + p;
   int32_t *slot_of = pv.slot_of + (int64_t)p * pv.max_ids;
   int32_t *slot_id = pv.slot_id + (int64_t)p * pv.cap_max;
   uint32_t *key = pv.key + (int64_t)p * pv.cap_max;
+  // MTP (qtok > 1): the pool takes its request's qtok selection sets one after another,
+  // each a full access_step (recency updated by every selected set); the
+  // hit / miss / evicted lists of the sets are appended per pool, the counts summed.
+  int acc_hit = 0, acc_miss = 0, acc_ev = 0, acc_tr = 0;
+  for (int jq = 0; jq < qtok; jq++) {
+  const int n = req_n[(int64_t)b * qtok + jq];
+  const int32_t *reqj = req + ((int64_t)b * qtok + jq) * req_stride;
   const int cap = meta->cap;
   const int size0 = meta->size;
   const uint32_t clk = meta->clk;
   const int64_t out_base = (int64_t)b * out_stride;
+  const int64_t sel_base = ((int64_t)b * qtok + jq) * sel_stride;
   PPROF(0);
   // STAGED: the pool's keys are copied to shared memory once, so the victim
   // select's passes and its compaction read on-chip
@@ -361,10 +368,10 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
   for (int e = 0; e < EPT; e++) {
     const int i = t * EPT + e;
-    xs[e] = (!bad && i < n) ? req[(int64_t)b * req_stride + i] : 0;
+    xs[e] = (!bad && i < n) ? reqj[i] : 0;
   }
   // the key staging loads go out while the requested ids are in flight
-  if (staged) {
+  if (staged && jq == 0) {
 #pragma unroll 4
     for (int s2 = t; s2 < cap; s2 += NT) skey[s2] = key[s2];
   }
@@ -408,10 +415,10 @@ __global__ void __launch_bounds__(NT, 1)
     mrank[e] = i - hr;
     if (i < n) {
       if (hflag[e]) {
-        if (MODE == MODE_ACCESS && hit_out) hit_out[out_base + hr] = sm.id[i];
+        if (MODE == MODE_ACCESS && hit_out) hit_out[out_base + acc_hit + hr] = sm.id[i];
         hr++;
       } else if (MODE == MODE_ACCESS && miss_out) {
-        miss_out[out_base + (i - hrank[e])] = sm.id[i];
+        miss_out[out_base + acc_miss + (i - hrank[e])] = sm.id[i];
       }
     }
   }
@@ -541,9 +548,11 @@ __global__ void __launch_bounds__(NT, 1)
           int s = sm.sel[j];
           slot_of[sm.id[i]] = s;
           slot_id[s] = sm.id[i];
-          key[s] = (MODE == MODE_ACCESS) ? clk + nhit + j : clk + i;
+          const uint32_t st = (MODE == MODE_ACCESS) ? clk + nhit + j : clk + i;
+          key[s] = st;
+          if (staged) skey[s] = st;  // the staged copy stays exact for the next MTP set
           sm.slot[i] = s;
-          if (MODE == MODE_ACCESS && miss_row_out) miss_row_out[out_base + j] = s;
+          if (MODE == MODE_ACCESS && miss_row_out) miss_row_out[out_base + acc_miss + j] = s;
         }
       }
     }
@@ -614,12 +623,14 @@ __global__ void __launch_bounds__(NT, 1)
           slot_of[sm.id[i]] = s;
           slot_id[s] = sm.id[i];
         }
-        key[s] = (MODE == MODE_ACCESS) ? clk + (i - keep0) : clk + i;
+        const uint32_t st = (MODE == MODE_ACCESS) ? clk + (i - keep0) : clk + i;
+        key[s] = st;
+        if (staged) skey[s] = st;
         sm.slot[i] = s;
       } else {
         sm.slot[i] = pv.cap_max + i;  // transient: staging row
       }
-      if (MODE == MODE_ACCESS && miss_row_out && !hflag[e]) miss_row_out[out_base + mrank[e]] = sm.slot[i];
+      if (MODE == MODE_ACCESS && miss_row_out && !hflag[e]) miss_row_out[out_base + acc_miss + mrank[e]] = sm.slot[i];
     }
   }
   __syncthreads();
@@ -631,19 +642,19 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int e = 0; e < EPT; e++) {
         int i = t * EPT + e;
-        if (i < n) sel_row_out[out_base + i] = sm.slot[i];
+        if (i < n) sel_row_out[sel_base + i] = sm.slot[i];
       }
     }
     if (hit_row_out) {  // rows already resident before this step (attention pass 1)
 #pragma unroll
       for (int e = 0; e < EPT; e++) {
         int i = t * EPT + e;
-        if (i < n && hflag[e]) hit_row_out[out_base + hrank[e]] = sm.slot[i];
+        if (i < n && hflag[e]) hit_row_out[out_base + acc_hit + hrank[e]] = sm.slot[i];
       }
     }
     if (ev_out) {
       if (flags & ESS_ACCESS_SORT_EVICTED) sort_ids(sm, nev);
-      for (int j = t; j < nev; j += NT) ev_out[out_base + j] = sm.ev[j];
+      for (int j = t; j < nev; j += NT) ev_out[out_base + acc_ev + j] = sm.ev[j];
     }
   }
   PPROF(7);
@@ -652,11 +663,11 @@ __global__ void __launch_bounds__(NT, 1)
       meta->hits += nhit;
       meta->misses += nmiss;
       meta->evictions += nev;
-      if (counts_out) {
-        counts_out[b * 4 + 0] = nhit;
-        counts_out[b * 4 + 1] = nmiss;
-        counts_out[b * 4 + 2] = nev;
-        counts_out[b * 4 + 3] = n > cap ? n - cap : 0;
+      if (counts_out && jq == qtok - 1) {
+        counts_out[b * 4 + 0] = acc_hit + nhit;
+        counts_out[b * 4 + 1] = acc_miss + nmiss;
+        counts_out[b * 4 + 2] = acc_ev + nev;
+        counts_out[b * 4 + 3] = acc_tr + (n > cap ? n - cap : 0);
       }
     } else if (inserted_out) {
       inserted_out[b] += inserted;
@@ -669,6 +680,12 @@ __global__ void __launch_bounds__(NT, 1)
       meta->size = cap;
     }
   }
+  acc_hit += nhit;
+  acc_miss += nmiss;
+  acc_ev += nev;
+  acc_tr += n > cap ? n - cap : 0;
+  __syncthreads();  // the next set reads the pool state (meta, keys) this one wrote
+  }  // jq
 }
 
 __global__ void pool_reset_kernel(PoolView pv, int begin, int num, const int32_t *cap) {
@@ -1399,7 +1416,7 @@ int ess_pool_warmup(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_id
   if (num == 0) return ESS_OK;
   pool_step_kernel<MODE_WARMUP><<<num, NT, 0, (cudaStream_t)stream>>>(
       view(p), begin, d_ids, d_n, stride, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-      nullptr, 0, 0, d_inserted);
+      nullptr, 0, 0, d_inserted, 1, 0);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }
@@ -1428,11 +1445,12 @@ int ess_pool_settle(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_sl
   return ESS_OK;
 }
 
-int ess_pool_access(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_req,
-                    const int32_t *d_n, int32_t req_stride, int32_t *d_hit_ids,
-                    int32_t *d_miss_ids, int32_t *d_evicted_ids, int32_t *d_sel_row,
-                    int32_t *d_hit_row, int32_t *d_miss_row, int32_t *d_counts,
-                    int32_t out_stride, int32_t flags, void *stream) {
+static int pool_access_launch(ess_pool *p, int32_t begin, int32_t num, int32_t qtok,
+                              const int32_t *d_req, const int32_t *d_n, int32_t req_stride,
+                              int32_t *d_hit_ids, int32_t *d_miss_ids, int32_t *d_evicted_ids,
+                              int32_t *d_sel_row, int32_t sel_stride, int32_t *d_hit_row,
+                              int32_t *d_miss_row, int32_t *d_counts, int32_t out_stride,
+                              int32_t flags, void *stream) {
   if (!range_ok(p, begin, num) || !d_req || !d_n || req_stride < 0) return ESS_ERR_ARG;
   if ((d_hit_ids || d_miss_ids || d_evicted_ids || d_sel_row || d_hit_row || d_miss_row) &&
       out_stride < 1)
@@ -1448,9 +1466,33 @@ int ess_pool_access(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_re
   }
   pool_step_kernel<MODE_ACCESS><<<num, NT, smem, (cudaStream_t)stream>>>(
       view(p), begin, d_req, d_n, req_stride, d_hit_ids, d_miss_ids, d_evicted_ids, d_sel_row,
-      d_hit_row, d_miss_row, d_counts, out_stride, flags, nullptr);
+      d_hit_row, d_miss_row, d_counts, out_stride, flags, nullptr, qtok, sel_stride);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
+}
+
+int ess_pool_access(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_req,
+                    const int32_t *d_n, int32_t req_stride, int32_t *d_hit_ids,
+                    int32_t *d_miss_ids, int32_t *d_evicted_ids, int32_t *d_sel_row,
+                    int32_t *d_hit_row, int32_t *d_miss_row, int32_t *d_counts,
+                    int32_t out_stride, int32_t flags, void *stream) {
+  return pool_access_launch(p, begin, num, 1, d_req, d_n, req_stride, d_hit_ids, d_miss_ids,
+                            d_evicted_ids, d_sel_row, out_stride, d_hit_row, d_miss_row, d_counts,
+                            out_stride, flags, stream);
+}
+
+int ess_pool_access_mtp(ess_pool *p, int32_t begin, int32_t num, int32_t qtok, const int32_t *d_req,
+                        const int32_t *d_n, int32_t req_stride, int32_t *d_hit_ids,
+                        int32_t *d_miss_ids, int32_t *d_evicted_ids, int32_t *d_sel_row,
+                        int32_t *d_hit_row, int32_t *d_miss_row, int32_t *d_counts,
+                        int32_t out_stride, int32_t flags, void *stream) {
+  if (qtok < 1 || qtok > ESS_INDEXER_MAX_QTOK) return ESS_ERR_ARG;
+  if ((d_hit_ids || d_miss_ids || d_evicted_ids || d_hit_row || d_miss_row) &&
+      (int64_t)out_stride < (int64_t)qtok * req_stride)
+    return ESS_ERR_ARG;  // the appended lists of qtok sets must fit a pool's row
+  return pool_access_launch(p, begin, num, qtok, d_req, d_n, req_stride, d_hit_ids, d_miss_ids,
+                            d_evicted_ids, d_sel_row, req_stride, d_hit_row, d_miss_row, d_counts,
+                            out_stride, flags, stream);
 }
 
 #ifdef ESS_POOL_PROF

@@ -176,6 +176,7 @@ struct SplitArgs {
   int32_t cap_max;
   int32_t *hit_row, *miss_ids, *miss_row, *counts;
   int32_t out_stride;
+  int32_t len_div = 1;  // MTP: rows b*len_div .. b*len_div+len_div-1 share len[b]
 };
 
 __device__ __forceinline__ void split_tail(int b, const int32_t *o, int n, const SplitArgs &sp,
@@ -234,7 +235,7 @@ __global__ void __launch_bounds__(NT, 1)
   int rank = 0;
   if constexpr (CLN > 1) rank = (int)cg::this_cluster().block_rank();
   const int b = blockIdx.x / CLN;
-  const int len = (int)min((int64_t)lens[b], ld);  // a len past the row stride reads no further
+  const int len = (int)min((int64_t)lens[b / sp.len_div], ld);  // a len past the row stride reads no further
   const float *row = logits + (int64_t)b * ld;
   int32_t *o = out + (int64_t)b * out_ld;
   const int chunk = (((len + CLN - 1) / CLN) + 3) & ~3;
@@ -574,13 +575,14 @@ int launch_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t
 
 }  // namespace
 
-extern "C" int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
-                        int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count,
-                        void *stream) {
-  if (!d_logits || !d_len || !d_idx || !d_count || batch < 0 || k < 1 || k > ESS_TOPK_MAX_K ||
-      idx_ld < k || ld < 1)
+namespace {
+
+int topk_rows(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t rows, int32_t len_div,
+              int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count, void *stream) {
+  if (!d_logits || !d_len || !d_idx || !d_count || rows < 0 || k < 1 || k > ESS_TOPK_MAX_K ||
+      idx_ld < k || ld < 1 || len_div < 1)
     return ESS_ERR_ARG;
-  if (batch == 0) return ESS_OK;
+  if (rows == 0) return ESS_OK;
   // Cluster size: the smallest that fits a slice in shared memory.  Growing it to fill
   // idle SMs does not pay: 1024-thread CTAs are register-limited to one per SM and the
   // DSMEM histogram sums cost more than the shorter slices save (profiles/README.md).
@@ -595,16 +597,35 @@ extern "C" int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len,
   while (cln < min_cln) cln *= 2;
   if ((ld + cln - 1) / cln > SLICE_MAX) return ESS_ERR_ARG;  // rows longer than 320K tokens
   cudaStream_t s = (cudaStream_t)stream;
+  SplitArgs sp{};
+  sp.slot_of = nullptr;
+  sp.len_div = len_div;
   int rc;
   switch (cln) {
-    case 1: rc = launch_topk<1>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, s); break;
-    case 2: rc = launch_topk<2>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, s); break;
-    case 4: rc = launch_topk<4>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, s); break;
-    default: rc = launch_topk<8>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, s); break;
+    case 1: rc = launch_topk<1>(d_logits, ld, d_len, rows, k, d_idx, idx_ld, d_count, s, sp); break;
+    case 2: rc = launch_topk<2>(d_logits, ld, d_len, rows, k, d_idx, idx_ld, d_count, s, sp); break;
+    case 4: rc = launch_topk<4>(d_logits, ld, d_len, rows, k, d_idx, idx_ld, d_count, s, sp); break;
+    default: rc = launch_topk<8>(d_logits, ld, d_len, rows, k, d_idx, idx_ld, d_count, s, sp); break;
   }
   if (rc != ESS_OK) return rc;
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
+}
+
+}  // namespace
+
+extern "C" int ess_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
+                        int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count,
+                        void *stream) {
+  return topk_rows(d_logits, ld, d_len, batch, 1, k, d_idx, idx_ld, d_count, stream);
+}
+
+// MTP: batch * qtok rows (request-major), row b*qtok + j scored over len[b] tokens.
+extern "C" int ess_topk_mtp(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
+                            int32_t qtok, int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count,
+                            void *stream) {
+  if (qtok < 1 || qtok > ESS_INDEXER_MAX_QTOK || batch < 0) return ESS_ERR_ARG;
+  return topk_rows(d_logits, ld, d_len, batch * qtok, qtok, k, d_idx, idx_ld, d_count, stream);
 }
 
 // Top-k fused with the early-gather hit/miss split (ess_pool_split) of pools

@@ -148,6 +148,12 @@ class DSADecodeLayer:
             self.pool.warmup(self.idx, self.cnt)
             if record:
                 rec.append([self.idx[b, :int(self.cnt[b])].cpu().numpy() for b in range(self.B)])
+        self._fill_resident()
+        return rec
+
+    def _fill_resident(self) -> None:
+        """The prefill->decode handoff's data movement: every resident id's slot row is
+        filled from the host store (after the warm-up decided the residents)."""
         order, n = self.pool.lru_order()
         order = order[:, :self.cap_max].contiguous()
         slots = torch.stack([self.pool.lookup(b, order[b].clamp_min(0)) for b in range(self.B)])
@@ -157,7 +163,6 @@ class DSADecodeLayer:
         gather(self.pool, self.store, AccessBatch(counts=counts, sel_row=None, miss_ids=order,
                                                   miss_row=slots.contiguous()), max_ctas=148)
         self.pool.check("prefill_warmup")
-        return rec
 
     def preload_full_history(self) -> None:
         """The all-HBM ceiling's state: every request's whole history made

@@ -50,6 +50,65 @@ def indexer_logits(q_fp8: torch.Tensor, w: torch.Tensor, k_cache: torch.Tensor,
     return out
 
 
+def indexer_logits_mtp(q_fp8: torch.Tensor, w: torch.Tensor, k_cache: torch.Tensor,
+                       k_scale: torch.Tensor, lens: torch.Tensor,
+                       out: torch.Tensor | None = None, max_ctas: int = 0) -> torch.Tensor:
+    """MTP indexer: ``qtok`` = mtp + 1 query tokens per request (pipeline.py:213-215).
+
+    logits[b, j, s] = k_scale[b, s] * sum_h w[b, j, h] * relu(q[b, j, h] . k[b, s]), s < lens[b]
+    with q_fp8 [B, qtok, 64, 128] e4m3, w [B, qtok, 64] f32, out [B, qtok, Lmax] f32.
+    Every token of a request scores the same cached keys (the selection universe is the
+    cache history, trace.py:151-154); the keys are read once per request."""
+    _lib.require_cuda(k_cache)
+    if k_cache.dim() != 3 or q_fp8.dim() != 4:
+        raise ValueError("expected k [B,Lmax,128] and q [B,qtok,64,128]")
+    B, Lmax, D = k_cache.shape
+    qtok = q_fp8.shape[1]
+    if D != DIM or Lmax % 128:
+        raise ValueError("expected k [B,Lmax,128] with Lmax a multiple of 128")
+    if not 1 <= qtok <= _lib.MAX_QTOK:
+        raise ValueError(f"qtok must be in [1, {_lib.MAX_QTOK}]")
+    dev = k_cache.device
+    fp8 = (torch.uint8, torch.float8_e4m3fn)
+    _lib.check_tensor(k_cache, "k_cache", fp8, device=dev)
+    _lib.check_tensor(q_fp8, "q_fp8", fp8, (B, qtok, HEADS, DIM), device=dev)
+    _lib.check_tensor(w, "w", torch.float32, (B, qtok, HEADS), device=dev)
+    _lib.check_tensor(k_scale, "k_scale", torch.float32, (B, Lmax), device=dev)
+    _lib.check_tensor(lens, "lens", torch.int32, (B,), device=dev)
+    if out is None:
+        out = torch.empty((B, qtok, Lmax), dtype=torch.float32, device=dev)
+    _lib.check_tensor(out, "out", torch.float32, (B, qtok, Lmax), device=dev)
+    _lib.check(_lib.load().ess_indexer_logits_mtp(
+        q_fp8.data_ptr(), w.data_ptr(), k_cache.data_ptr(), k_scale.data_ptr(), lens.data_ptr(),
+        B, qtok, Lmax, out.data_ptr(), max_ctas, _lib.stream_handle()), "ess_indexer_logits_mtp")
+    return out
+
+
+def topk_mtp(logits: torch.Tensor, lens: torch.Tensor, k: int = TOPK,
+             out: torch.Tensor | None = None, count: torch.Tensor | None = None):
+    """Top-k of every query token's row: logits [B, qtok, ld] (indexer_logits_mtp),
+    row (b, j) over lens[b] tokens.  Returns (idx [B, qtok, k], count [B, qtok])."""
+    _lib.require_cuda(logits)
+    if logits.dim() != 3 or logits.dtype != torch.float32 or not logits.is_contiguous():
+        raise ValueError("logits must be a contiguous CUDA float32 [B, qtok, ld] tensor")
+    B, qtok, ld = logits.shape
+    if not 1 <= qtok <= _lib.MAX_QTOK:
+        raise ValueError(f"qtok must be in [1, {_lib.MAX_QTOK}]")
+    _lib.check_tensor(lens, "lens", torch.int32, (B,), device=logits.device)
+    if not 1 <= k <= 65535:
+        raise ValueError("k must be in [1, 65535]")
+    if out is None:
+        out = torch.empty((B, qtok, k), dtype=torch.int32, device=logits.device)
+    if count is None:
+        count = torch.empty((B, qtok), dtype=torch.int32, device=logits.device)
+    _lib.check_tensor(out, "out", torch.int32, (B, qtok, k), device=logits.device)
+    _lib.check_tensor(count, "count", torch.int32, (B, qtok), device=logits.device)
+    _lib.check(_lib.load().ess_topk_mtp(logits.data_ptr(), ld, lens.data_ptr(), B, qtok, k,
+                                        out.data_ptr(), k, count.data_ptr(), _lib.stream_handle()),
+               "ess_topk_mtp")
+    return out, count
+
+
 def topk(logits: torch.Tensor, lens: torch.Tensor, k: int = TOPK,
          out: torch.Tensor | None = None, count: torch.Tensor | None = None):
     """Top-k of each row logits[b, :lens[b]] by (score desc, index asc), ascending ids.
