@@ -579,6 +579,14 @@ def run_ours(args, cfg):
         a8 = argparse.Namespace(**{**vars(args), "e2e": False})
         subs[f"{cfg['name']}_fp8_slots"] = measure(a8, f8, dev, rank, world, agg_dev, args.drift, True, peaks,
                                                    peak_kind, link_peak)
+        if cfg["name"] == "c2" and args.mtp:
+            # MTP = 2, accept 1.7 (the paper's Table 2 32K setting) on the same shapes,
+            # beside its all-HBM ceiling (rho = 1, nothing to gather)
+            m = measure_mtp(args, cfg, dev, mtp=2, mean_accept=1.7)
+            mc = measure_mtp(args, cfg, dev, mtp=2, mean_accept=1.7, rho=1.0)
+            m["all_hbm_ceiling"] = {"value": mc["value"], "ms_per_step": mc["ms_per_step"],
+                                    "hit_rate": mc["hit_rate"], "frac_of_ceiling": m["value"] / mc["value"]}
+            subs["c2_mtp2"] = m
         lo = argparse.Namespace(**{**vars(args), "e2e": False})
         subs[f"{cfg['name']}_drift_0.9"] = measure(lo, cfg, dev, rank, world, agg_dev, 0.9, False, peaks,
                                                    peak_kind, link_peak)
@@ -722,6 +730,88 @@ def run_model(args, cfg):
         dist.destroy_process_group()
 
 
+def measure_mtp(args, cfg, dev, mtp=2, mean_accept=1.7, rho=None, overlap="dba", seed=4321):
+    """The MTP decode step (MTPDecodeLayer: mtp + 1 query tokens per request; the paper's
+    Table 2 setting MTP = 2, accept 1.7 at 32K): graph replays with
+    per-request accepted counts drawn as Poisson(mean - 1) + 1 capped at mtp + 1
+    (trace.py:127), device clock.  ``value`` counts accepted tokens (the reference's
+    OTPS x batch, costmodel.py:232-234); ``verified`` counts all query tokens."""
+    import numpy as np
+    import torch
+    from paper_2512_10576_b200.decode import random_latent_rows
+    from paper_2512_10576_b200.attention import sparse_mla
+    from paper_2512_10576_b200.indexer import indexer_logits_mtp, topk_mtp
+    from paper_2512_10576_b200.mtp import MTPDecodeLayer, draw_accepted
+    B, ctx = cfg["batch"], cfg["context_len"]
+    rho = cfg["sparse_ratio"] if rho is None else rho
+    W, K = args.warmup, args.steps
+    Q = mtp + 1
+    layer = MTPDecodeLayer(B, ctx, rho, TOPK, mtp=mtp, max_new_tokens=W + K + 8, device=dev, seed=seed,
+                           drift=args.drift)
+    layer.micro, layer.first_frac = cfg["micro"], cfg["first"]
+    if rho >= 1.0:
+        layer.preload_full_history()
+    else:
+        layer.prefill_warmup(windows=32)
+    rng = np.random.default_rng(seed)
+    total = W + K
+    acc_h = [draw_accepted(rng, B, mean_accept, Q) for _ in range(total)]
+    # each step starts where the previous one's accepted tokens end (query = f(position))
+    inputs = [layer.next_queries(None if t == 0 else acc_h[t - 1]) for t in range(total)]
+    rows = [random_latent_rows(B * Q, dev, layer.gen).view(B, Q, 656) for _ in range(total)]
+    acc_d = [torch.from_numpy(a).to(dev) for a in acc_h]
+    layer.capture(overlap if rho < 1.0 else "none", args.gather_ctas, accepted=acc_h[0])
+    for t in range(1, W):
+        layer.step(inputs[t][0], inputs[t][1], rows[t], acc_d[t], max_accepted=int(acc_h[t].max()))
+    torch.cuda.synchronize()
+    hits0, misses0 = layer.access_totals()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clocks:
+        torch.cuda.synchronize()
+        e0.record()
+        for t in range(W, total):
+            layer.step(inputs[t][0], inputs[t][1], rows[t], acc_d[t], max_accepted=int(acc_h[t].max()))
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    layer.pool.check("bench mtp")
+    hits, misses = (x - y for x, y in zip(layer.access_totals(), (hits0, misses0)))
+    accepted = float(sum(int(a.sum()) for a in acc_h[W:total]))
+    rec = {"value": accepted / (ms * 1e-3 * K), "unit": "accepted tokens/s", "ms_per_step": ms,
+           "verified_tokens_per_s": B * Q / (ms * 1e-3), "mtp": mtp, "mean_accept_drawn": accepted / (B * K),
+           "batch_per_gpu": B, "context_len": ctx, "sparse_ratio": rho,
+           "hit_rate": hits / max(1, hits + misses), "misses_per_request_step": misses / (B * K),
+           "gpu_launches": layer.launches_per_step(overlap if rho < 1.0 else "none") * K,
+           "clocks": clocks.summary()}
+    # the idempotent kernels alone on the last step's buffers (K1: the MTP indexer reads
+    # each request's keys once; K2: B * qtok rows; K5: B * qtok query rows)
+    L = int(layer.lens.float().mean())
+
+    def alone(fn, n=5):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n)]
+        for a, b in ev:
+            torch.cuda._sleep(1_000_000)
+            a.record()
+            fn()
+            b.record()
+        torch.cuda.synchronize()
+        return statistics.median(a.elapsed_time(b) for a, b in ev)
+    k1_ms = alone(lambda: indexer_logits_mtp(inputs[0][0], layer.w, layer.k_cache, layer.k_scale, layer.lens,
+                                             out=layer.logits))
+    rec["kernels_ms"] = {
+        "indexer": k1_ms,
+        "topk": alone(lambda: topk_mtp(layer.logits, layer.lens, TOPK, out=layer.idx, count=layer.cnt)),
+        "sparse_mla": alone(lambda: sparse_mla(layer.pool, layer.q_in.view(B * Q, 128, 576),
+                                               layer.sel_row.view(B * Q, TOPK), layer.cnt.view(B * Q),
+                                               layer.sm_scale, out=layer.out.view(B * Q, 128, 512),
+                                               lse=layer.lse.view(B * Q, 128), qtok=Q))}
+    k1_bytes = B * L * (132 + 4 * Q) + B * Q * (64 * 128 + 64 * 4)
+    rec["indexer"] = {"ms": k1_ms, "algorithmic_bytes": k1_bytes, "gbs": k1_bytes / (k1_ms * 1e-3) / 1e9,
+                      "tflops": 2 * 64 * 128 * Q * B * L / (k1_ms * 1e-3) / 1e12}
+    layer.close()
+    return rec
+
+
 def run_ceiling(args, cfg, dev):
     """Same kernels with the whole latent cache in HBM (rho = 1, full history preloaded):
     every selection hits and the gather moves nothing (SURVEY §8d ceiling).  It runs the
@@ -779,6 +869,8 @@ def main():
     ap.add_argument("--no-sub", dest="sub", action="store_false",
                     help="skip the sub-records (C4 at 128K + its ceiling, drift 0.9); N=1 only")
     ap.add_argument("--no-e2e", dest="e2e", action="store_false")
+    ap.add_argument("--no-mtp", dest="mtp", action="store_false", help="skip the MTP = 2 sub-record")
+    ap.add_argument("--mtp-only", action="store_true", help="print only the MTP sub-record (C2 shapes)")
     ap.add_argument("--plan-theta", type=float, default=None,
                     help="multi-layer configs: layer-wise DA/DBA plan at this miss threshold")
     ap.add_argument("--pre-steps", type=int, default=0,
@@ -795,7 +887,16 @@ def main():
         args.micro = cfg["micro"]
     if args.first is None:
         args.first = cfg["first"] if args.micro == cfg["micro"] else None
-    if args.impl == "reference":
+    if args.mtp_only:
+        import torch
+        dev = torch.device("cuda", 0)
+        torch.cuda.set_device(dev)
+        m = measure_mtp(args, cfg, dev, mtp=2, mean_accept=1.7)
+        mc = measure_mtp(args, cfg, dev, mtp=2, mean_accept=1.7, rho=1.0)
+        m["all_hbm_ceiling"] = {"value": mc["value"], "ms_per_step": mc["ms_per_step"],
+                                "frac_of_ceiling": m["value"] / mc["value"]}
+        print(json.dumps(m), flush=True)
+    elif args.impl == "reference":
         run_reference(args, cfg)
     elif cfg.get("layers", 1) > 1:
         run_model(args, cfg)

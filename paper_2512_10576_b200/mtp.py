@@ -31,13 +31,15 @@ C1-style oversize regime (cap < K) is served by the single-token layer.
 
 from __future__ import annotations
 
+import math
+
 import numpy as np
 import torch
 
 from . import _lib
 from .attention import sparse_mla
 from .cache import AccessBatch
-from .decode import ROW, DSADecodeLayer, random_latent_rows
+from .decode import ROW, DSADecodeLayer, _e4m3, random_latent_rows
 from .indexer import indexer_logits, indexer_logits_mtp, topk, topk_mtp
 from .transfer import gather
 
@@ -62,7 +64,10 @@ class MTPDecodeLayer(DSADecodeLayer):
         B, d, g, Q = self.B, self.device, self.gen, qtok
         self._zi = torch.randn((B, Q, 64, 128), device=d, generator=g)
         self._za = torch.randn((B, Q, 128, 576), device=d, generator=g)
-        self.w = (torch.randn((B, Q, 64), device=d, generator=g) / 8.0).contiguous()
+        # head weights: per request, the same for every position (as the single-token
+        # layer keeps them across steps), so a position's selection does not depend on
+        # which token slot of a step it occupies
+        self.w = (torch.randn((B, 1, 64), device=d, generator=g) / 8.0).expand(B, Q, 64).contiguous()
         self.logits = torch.empty((B, Q, self.Lmax), dtype=torch.float32, device=d)
         self.idx = torch.empty((B, Q, topk_k), dtype=torch.int32, device=d)
         self.cnt = torch.empty((B, Q), dtype=torch.int32, device=d)
@@ -74,8 +79,36 @@ class MTPDecodeLayer(DSADecodeLayer):
         self._idx1 = torch.empty((B, topk_k), dtype=torch.int32, device=d)
         self._cnt1 = torch.empty(B, dtype=torch.int32, device=d)
 
-    # next_queries (inherited) drifts every token's queries from its own previous-step
-    # value: q_idx [B, qtok, 64, 128] e4m3, q [B, qtok, 128, 576] bf16
+    def next_queries(self, advance=None):
+        """(q_idx [B, qtok, 64, 128] e4m3, q [B, qtok, 128, 576] bf16) of the next step.
+
+        The qtok tokens of a step are consecutive positions and a query is a function of
+        its position, drifting between adjacent positions as consecutive decode steps do
+        (Eq. (1)): q(p+1) = a q(p) + sqrt(1-a^2) eps.  A step starts ``advance[b]`` positions
+        after the previous one (the previous step's accepted tokens, default 1): its first
+        qtok - advance tokens are the previous step's last ones (same positions, same
+        queries), the rest continue the chain."""
+        B, Q, d = self.B, self.qtok, self.device
+        adv = torch.ones(B, dtype=torch.long, device=d) if advance is None else \
+            torch.as_tensor(np.asarray(advance), dtype=torch.long).to(d)
+        if adv.shape != (B,) or int(adv.min()) < 1 or int(adv.max()) > Q:
+            raise ValueError(f"advance must hold one value in [1, {Q}] per request")
+        a = self.drift
+        s = math.sqrt(max(0.0, 1.0 - a * a))
+        rows = torch.arange(B, device=d)
+        out = []
+        for old in (self._zi, self._za):
+            new = torch.empty_like(old)
+            prev = old[:, Q - 1]
+            for j in range(Q):
+                src = j + adv
+                chain = a * prev + s * torch.randn(prev.shape, device=d, generator=self.gen)
+                keep = (src < Q).view(B, *([1] * (old.dim() - 2)))
+                new[:, j] = torch.where(keep, old[rows, src.clamp(max=Q - 1)], chain)
+                prev = new[:, j]
+            out.append(new)
+        self._zi, self._za = out
+        return _e4m3(self._zi * 4.0), (self._za * 0.5).to(torch.bfloat16)
 
     def prefill_warmup(self, windows: int = 32, record: bool = False):
         rec = []
