@@ -66,6 +66,9 @@ extern "C" {
 #define ESS_ERR_ARG (-6)       /* id out of [0, max_ids), request too long, bad sizes  */
 #define ESS_ERR_CUDA (-7)      /* CUDA runtime / driver failure                        */
 #define ESS_ERR_CLOCK (-8)     /* 32-bit recency clock exhausted (> 4e9 touches)       */
+#define ESS_ERR_RANGE (-9)     /* a K5 operand (q, or a slot row's dequantised value)
+                                  outside the f16 range (|x| >= 65520): latched, the
+                                  output of that launch is not valid                  */
 
 #define ESS_CLOCK_BASE (1u << 24)   /* recency stamps start here; free slots key = slot index */
 

@@ -62,6 +62,7 @@ SIGNATURES = {
 ESS_OK = 0
 ESS_ERR_CAPACITY, ESS_ERR_SHRINK, ESS_ERR_DUPLICATE = -1, -2, -3
 ESS_ERR_NOMEM, ESS_ERR_RATIO, ESS_ERR_ARG, ESS_ERR_CUDA, ESS_ERR_CLOCK = -4, -5, -6, -7, -8
+ESS_ERR_RANGE = -9
 ESS_ACCESS_SORT_EVICTED = 1
 ESS_MLA_PARTIAL, ESS_MLA_RESUME = 1, 2
 ESS_MLA_SPLIT_SHIFT, ESS_MLA_MAX_SPLIT = 8, 8
@@ -113,7 +114,7 @@ def check(rc: int, what: str = "") -> None:
     if rc == ESS_OK:
         return
     msg = f"{what}: {status_text(rc)}" if what else status_text(rc)
-    if rc in (ESS_ERR_CAPACITY, ESS_ERR_SHRINK, ESS_ERR_DUPLICATE, ESS_ERR_RATIO, ESS_ERR_ARG):
+    if rc in (ESS_ERR_CAPACITY, ESS_ERR_SHRINK, ESS_ERR_DUPLICATE, ESS_ERR_RATIO, ESS_ERR_ARG, ESS_ERR_RANGE):
         raise ValueError(msg)
     if rc == ESS_ERR_NOMEM:
         raise MemoryError(msg)

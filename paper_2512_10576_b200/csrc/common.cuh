@@ -120,6 +120,23 @@ __device__ __forceinline__ uint4 cvt8_bf16_f16(uint4 x) {
                     bf16x2_to_f16x2(x.w));
 }
 
+// Range guard of the f16 operands (K5 computes in f16 on the tensor cores): a packed
+// f16 pair holding an inf / NaN — a bf16 source value of magnitude >= 65520 rounds to
+// inf — flags ESS_ERR_RANGE in the pool's status word instead of passing silently.
+__device__ __forceinline__ bool f16x2_nonfinite(uint32_t h) {
+  return ((h & 0x7C00u) == 0x7C00u) | ((h & 0x7C000000u) == 0x7C000000u);
+}
+__device__ __forceinline__ bool f16x8_nonfinite(uint4 v) {
+  return f16x2_nonfinite(v.x) | f16x2_nonfinite(v.y) | f16x2_nonfinite(v.z) | f16x2_nonfinite(v.w);
+}
+// a bf16 pair with a magnitude >= 65536 (or inf / NaN): outside what f16 represents
+__device__ __forceinline__ bool bf16x2_over_f16(uint32_t v) {
+  return ((v & 0x7FFFu) >= 0x4780u) | (((v >> 16) & 0x7FFFu) >= 0x4780u);
+}
+__device__ __forceinline__ bool bf16x8_over_f16(uint4 v) {
+  return bf16x2_over_f16(v.x) | bf16x2_over_f16(v.y) | bf16x2_over_f16(v.z) | bf16x2_over_f16(v.w);
+}
+
 // Bounded mbarrier / flag spin: trap instead of hanging the GPU on a protocol bug.
 #ifndef ESS_SPIN_LIMIT
 #define ESS_SPIN_LIMIT (1u << 26)

@@ -97,6 +97,7 @@ const char *ess_status_string(int status) {
     case ESS_ERR_ARG: return "invalid argument (id out of range, request too long, bad size)";
     case ESS_ERR_CUDA: return "CUDA error";
     case ESS_ERR_CLOCK: return "recency clock exhausted";
+    case ESS_ERR_RANGE: return "attention operand outside the f16 range (|x| >= 65520)";
     default: return "unknown status";
   }
 }

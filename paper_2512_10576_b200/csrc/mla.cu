@@ -214,7 +214,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
                       const int32_t *__restrict__ sel2, int32_t *landed,
                       int sel_stride, const int32_t *__restrict__ counts, int count_stride,
                       float sm_scale, uint16_t *__restrict__ out, float *__restrict__ lse,
-                      float *__restrict__ ws_o, float *__restrict__ ws_ml, int flags, int nsplit) {
+                      float *__restrict__ ws_o, float *__restrict__ ws_ml, int flags, int nsplit,
+                      int32_t *status) {
   extern __shared__ uint8_t smem_raw[];
   // offset from the shared array itself (keeps the shared address space: LDS/STS, not generic)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -291,22 +292,35 @@ __global__ void __launch_bounds__(NTHREADS, 1)
     for (int cc = 0; cc < QT_BLKS; cc++) {  // 64 dims = 32 columns per block
       const uint8_t *rowp = skv + cc * QBLK_BYTES + h * 128;
       uint32_t r[32];
+      bool bad = false;
 #pragma unroll
       for (int k = 0; k < 8; k++) {
         uint4 y = cvt8_bf16_f16(*reinterpret_cast<const uint4 *>(rowp + ((k ^ (h & 7)) << 4)));
+        bad |= f16x8_nonfinite(y);
         r[4 * k] = y.x;
         r[4 * k + 1] = y.y;
         r[4 * k + 2] = y.z;
         r[4 * k + 3] = y.w;
       }
       tmem_st_32x32b_x32(tmem + lane_base + TM_Q + cc * 32, r);
+#ifndef ESS_NO_RANGE_LATCH
+      if (bad) ess_set_status(status, ESS_ERR_RANGE);  // q outside the f16 range
+#endif
     }
     tmem_st_wait();
   } else {
     // warps 4-8: q dims 320..575 to f16 in place (16-B units keep their SW128 position)
     constexpr int NT = NTHREADS - NSOFT * 32;
     uint4 *qs = reinterpret_cast<uint4 *>(sq);
-    for (int u = threadIdx.x - NSOFT * 32; u < QS_BYTES / 16; u += NT) qs[u] = cvt8_bf16_f16(qs[u]);
+    bool bad = false;
+    for (int u = threadIdx.x - NSOFT * 32; u < QS_BYTES / 16; u += NT) {
+      const uint4 y = cvt8_bf16_f16(qs[u]);
+      bad |= f16x8_nonfinite(y);
+      qs[u] = y;
+    }
+#ifndef ESS_NO_RANGE_LATCH
+    if (bad) ess_set_status(status, ESS_ERR_RANGE);
+#endif
     fence_proxy_async_smem();
   }
   tc_fence_before();
@@ -456,8 +470,13 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         l = l0 * a0 + l_run * a1;
       }
       uint16_t *ob = out + hrow * ESS_MLA_V_DIM + v * V_HALF;
-      if (l > 0.f) {
-        const float inv = 1.f / l, c0 = a0 * inv, c1 = a1 * inv;
+      // Every lane runs the epilogue (tcgen05.ld is .sync.aligned: a per-lane branch
+      // around it would leave a partial warp — a hang when one head's l is NaN from an
+      // out-of-range operand).  l == 0 (no rows): zeros, lse -inf; l NaN: NaN out.
+      {
+        const bool pos = l > 0.f;
+        const float inv = 1.f / l;
+        const float c0 = pos ? a0 * inv : (l == l ? 0.f : l), c1 = pos ? a1 * inv : c0;
         // the KV ring is idle once o_done fired: stage this head's workspace half
         // (1 KB) there as [16-B unit][head], all 64 copies in flight at once
         const uint4 *wst = reinterpret_cast<const uint4 *>(skv);
@@ -508,10 +527,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             *reinterpret_cast<uint4 *>(ob + cc * 32 + j) = pk;
           }
         }
-        if (v == 0) lse[hrow] = (m + log2f(l)) * 0.6931471805599453f;
-      } else {
-        for (int j = 0; j < V_HALF; j += 8) *reinterpret_cast<uint4 *>(ob + j) = make_uint4(0, 0, 0, 0);
-        if (v == 0) lse[hrow] = -INFINITY;
+        if (v == 0) lse[hrow] = pos ? (m + log2f(l)) * 0.6931471805599453f : (l == l ? -INFINITY : l);
       }
     }
   } else if (warp == MMA_WARP) {
@@ -768,7 +784,8 @@ int launch_mla(ess_pool *pool, int32_t pool_begin, const void *d_q, const int32_
   dim3 grid(2, batch * nsplit);
   sparse_mla_kernel<<<grid, NTHREADS, SMEM_BYTES, (cudaStream_t)stream>>>(
       tq, pool->rows, pool->rows_per_pool, pool_begin, d_sel_row, d_sel2, d_landed, sel_stride,
-      d_count, count_stride, sm_scale, (uint16_t *)d_out, d_lse, d_ws_o, d_ws_ml, flags, nsplit);
+      d_count, count_stride, sm_scale, (uint16_t *)d_out, d_lse, d_ws_o, d_ws_ml, flags, nsplit,
+      pool->status);
   ESS_CUDA_TRY(cudaGetLastError());
   if (nsplit > 1) {
     mla_combine_kernel<<<dim3(batch, HEADS / 4), 128, 0, (cudaStream_t)stream>>>(

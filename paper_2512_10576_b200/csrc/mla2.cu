@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(F16 ? F_NTHREADS : NTHREADS, 1)
                           const int32_t *__restrict__ sel2, int32_t *landed, int sel_stride,
                           const int32_t *__restrict__ counts, int count_stride, float sm_scale,
                           uint16_t *__restrict__ out, float *__restrict__ lse, float *__restrict__ ws_o,
-                          float *__restrict__ ws_ml, int flags, int nsplit) {
+                          float *__restrict__ ws_ml, int flags, int nsplit, int32_t *status) {
   extern __shared__ uint8_t smem_raw[];
   // offset from the shared array itself (keeps the shared address space: LDS/STS, not generic)
   uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -368,21 +368,30 @@ __global__ void __launch_bounds__(F16 ? F_NTHREADS : NTHREADS, 1)
     for (int cc = 0; cc < QT_BLKS; cc++) {
       const uint8_t *rowp = sV + cc * QBLK + h * 128;
       uint32_t v[32];
+      bool bad = false;
 #pragma unroll
       for (int k = 0; k < 8; k++) {
-        const uint4 y = cvt8_bf16_f16_sat(*reinterpret_cast<const uint4 *>(rowp + ((k ^ (h & 7)) << 4)));
+        const uint4 x = *reinterpret_cast<const uint4 *>(rowp + ((k ^ (h & 7)) << 4));
+        bad |= bf16x8_over_f16(x);
+        const uint4 y = cvt8_bf16_f16_sat(x);
         v[4 * k] = y.x;
         v[4 * k + 1] = y.y;
         v[4 * k + 2] = y.z;
         v[4 * k + 3] = y.w;
       }
       tmem_st_x32(tmem + lane_base + TM_Q + cc * 32, v);
+      if (bad) ess_set_status(status, ESS_ERR_RANGE);  // q saturated: outside the f16 range
     }
     tmem_st_wait();
   } else {
     uint4 *qs = reinterpret_cast<uint4 *>(sq);
+    bool bad = false;
     for (int u = threadIdx.x - NSOFT * 32; u < QS_BLKS * QBLK / 16; u += NTH - NSOFT * 32)
+    {
+      bad |= bf16x8_over_f16(qs[u]);
       qs[u] = cvt8_bf16_f16_sat(qs[u]);
+    }
+    if (bad) ess_set_status(status, ESS_ERR_RANGE);
     fence_proxy_async_smem();
   }
   tc_fence_before();
@@ -507,8 +516,12 @@ __global__ void __launch_bounds__(F16 ? F_NTHREADS : NTHREADS, 1)
       }
       uint16_t *ob = out + hrow * ESS_MLA_V_DIM;
       const float *wsr = resume ? ws_o + hrow * ESS_MLA_V_DIM : nullptr;
-      if (l > 0.f) {
-        const float inv = 1.f / l, c0 = a0 * inv, c1 = a1 * inv;
+      // every lane runs the epilogue (tcgen05.ld is .sync.aligned; see mla.cu):
+      // l == 0 -> zeros, lse -inf; l NaN (out-of-range operands) -> NaN
+      {
+        const bool pos = l > 0.f;
+        const float inv = 1.f / l;
+        const float c0 = pos ? a0 * inv : (l == l ? 0.f : l), c1 = pos ? a1 * inv : c0;
 #pragma unroll 1
         for (int cc = 0; cc < 8; cc++) {
           uint32_t o[32];
@@ -536,13 +549,7 @@ __global__ void __launch_bounds__(F16 ? F_NTHREADS : NTHREADS, 1)
             *reinterpret_cast<uint4 *>(ob + d0 + j) = pk;
           }
         }
-        if (u == 0) lse[hrow] = (m + log2f(l)) * 0.6931471805599453f;
-      } else {
-        for (int cc = 0; cc < 8; cc++) {
-          const int d0 = dim_of(cc * 32);
-          for (int j = 0; j < 32; j += 8) *reinterpret_cast<uint4 *>(ob + d0 + j) = make_uint4(0, 0, 0, 0);
-        }
-        if (u == 0) lse[hrow] = -INFINITY;
+        if (u == 0) lse[hrow] = pos ? (m + log2f(l)) * 0.6931471805599453f : (l == l ? -INFINITY : l);
       }
     }
   } else if (warp == MMA_WARP) {
@@ -895,11 +902,11 @@ int ess_launch_mla_pair(ess_pool *pool, int32_t pool_begin, const void *d_q, con
     ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, sparse_mla_pair_kernel<true>, tq, (const uint8_t *)pool->rows,
                                     pool->rows_per_pool, (int)pool_begin, d_sel_row, d_sel2, d_landed,
                                     (int)sel_stride, d_count, (int)count_stride, sm_scale, (uint16_t *)d_out,
-                                    d_lse, d_ws_o, d_ws_ml, (int)flags, (int)nsplit));
+                                    d_lse, d_ws_o, d_ws_ml, (int)flags, (int)nsplit, pool->status));
   else
     ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, sparse_mla_pair_kernel<false>, tq, (const uint8_t *)pool->rows,
                                     pool->rows_per_pool, (int)pool_begin, d_sel_row, d_sel2, d_landed,
                                     (int)sel_stride, d_count, (int)count_stride, sm_scale, (uint16_t *)d_out,
-                                    d_lse, d_ws_o, d_ws_ml, (int)flags, (int)nsplit));
+                                    d_lse, d_ws_o, d_ws_ml, (int)flags, (int)nsplit, pool->status));
   return ESS_OK;
 }

@@ -289,7 +289,7 @@ __device__ __forceinline__ void copy_row(const uint8_t *src, uint8_t *dst, int l
 // 32+l in v1 — lane 0 has the four f32 group scales, lanes 1..8 the RoPE) ->
 // the 1152-B f16 slot row.  NoPE: f16(f32(e4m3) * scale), RoPE: f16(bf16) — both
 // single roundings, so the slot row is a pure function of the latent row.
-__device__ __forceinline__ void dequant_row_to_slot(uint4 v0, uint4 v1, int lane, uint8_t *dst) {
+__device__ __forceinline__ bool dequant_row_to_slot(uint4 v0, uint4 v1, int lane, uint8_t *dst) {
   const float s0 = __uint_as_float(__shfl_sync(0xffffffffu, v1.x, 0));
   const float s1 = __uint_as_float(__shfl_sync(0xffffffffu, v1.y, 0));
   const float s2 = __uint_as_float(__shfl_sync(0xffffffffu, v1.z, 0));
@@ -307,19 +307,27 @@ __device__ __forceinline__ void dequant_row_to_slot(uint4 v0, uint4 v1, int lane
   c.w = e4m3x2_scaled_f16x2((uint16_t)(v0.w >> 16), s);
   st_v4(dst + lane * 32, a);
   st_v4(dst + lane * 32 + 16, c);
-  if (lane >= 1 && lane <= 8) st_v4(dst + 1024 + (lane - 1) * 16, cvt8_bf16_f16(v1));
+  bool bad = f16x8_nonfinite(a) | f16x8_nonfinite(c);
+  if (lane >= 1 && lane <= 8) {
+    const uint4 r = cvt8_bf16_f16(v1);
+    st_v4(dst + 1024 + (lane - 1) * 16, r);
+    bad |= f16x8_nonfinite(r);
+  }
+  return bad;  // this lane wrote a value outside the f16 range
 }
 
 // The slot row of a 656-B latent row held by a warp, in the pool's slot format: the raw
 // row (ESS_SLOT_ROW_BYTES_FP8: K5 dequantises in shared memory) or the dequantised f16
 // row (ESS_SLOT_ROW_BYTES).
-__device__ __forceinline__ void store_slot_row(uint4 v0, uint4 v1, int lane, uint8_t *dst, int row_bytes) {
+// Returns true if this lane stored an f16 value outside the f16 range (the caller
+// latches ESS_ERR_RANGE).
+__device__ __forceinline__ bool store_slot_row(uint4 v0, uint4 v1, int lane, uint8_t *dst, int row_bytes) {
   if (row_bytes == ESS_SLOT_ROW_BYTES_FP8) {
     st_v4(dst + lane * 16, v0);
     if (lane + 32 < ESS_LATENT_ROW_BYTES / 16) st_v4(dst + (lane + 32) * 16, v1);
-  } else {
-    dequant_row_to_slot(v0, v1, lane, dst);
+    return false;
   }
+  return dequant_row_to_slot(v0, v1, lane, dst);
 }
 
 template <int MODE>
@@ -1068,7 +1076,7 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
         publish();
         cur_pool = pool_of[r];
       }
-      store_slot_row(v[r][0], v[r][1], lane, dst[r], (int)rb);
+      if (store_slot_row(v[r][0], v[r][1], lane, dst[r], (int)rb)) ess_set_status(pv.status, ESS_ERR_RANGE);
       tally++;
     }
   }
@@ -1166,7 +1174,7 @@ __global__ void __launch_bounds__(NTG) gather_bulk_kernel(PoolView pv, int begin
       publish();
       cur_pool = lo;
     }
-    store_slot_row(v0, v1, lane, pv.rows + ((int64_t)(begin + lo) * pv.rows_per_pool + row) * rb, (int)rb);
+    if (store_slot_row(v0, v1, lane, pv.rows + ((int64_t)(begin + lo) * pv.rows_per_pool + row) * rb, (int)rb)) ess_set_status(pv.status, ESS_ERR_RANGE);
     tally++;
   }
   publish();
@@ -1193,8 +1201,8 @@ __global__ void write_generated_kernel(PoolView pv, int begin, const int32_t *id
       if (lane + 32 < ROW_CHUNKS) st_v4(h + (lane + 32) * 16, v1);
     }
     if (s >= 0)
-      store_slot_row(v0, v1, lane, pv.rows + ((int64_t)(begin + b) * pv.rows_per_pool + s) * pv.row_bytes,
-                     pv.row_bytes);
+      if (store_slot_row(v0, v1, lane, pv.rows + ((int64_t)(begin + b) * pv.rows_per_pool + s) * pv.row_bytes,
+                     pv.row_bytes)) ess_set_status(pv.status, ESS_ERR_RANGE);
   }
 }
 
@@ -1263,8 +1271,8 @@ __global__ void __launch_bounds__(NTA) pool_admit_kernel(PoolView pv, int begin,
       if (lane + 32 < ROW_CHUNKS) st_v4(hp + (lane + 32) * 16, v1);
     }
     if (pv.rows)
-      store_slot_row(v0, v1, lane, pv.rows + ((int64_t)p * pv.rows_per_pool + slots[i]) * pv.row_bytes,
-                     pv.row_bytes);
+      if (store_slot_row(v0, v1, lane, pv.rows + ((int64_t)p * pv.rows_per_pool + slots[i]) * pv.row_bytes,
+                     pv.row_bytes)) ess_set_status(pv.status, ESS_ERR_RANGE);
     if (slot_out && lane == 0) slot_out[(int64_t)b * src_stride + i] = slots[i];
   }
   if (threadIdx.x == 0) {

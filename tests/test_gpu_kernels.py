@@ -481,3 +481,92 @@ def test_topk_split_fused_matches_topk_then_split(lens):
         assert torch.equal(r1.miss_ids[b, :m], r2.miss_ids[b, :m])
         assert torch.equal(r1.miss_row[b, :m], r2.miss_row[b, :m])
     pool.close()
+
+
+# ------------------------------------------------------------ f16 range guard (K4 / K5)
+@FMT
+def test_sparse_mla_flags_q_outside_f16_range(fmt):
+    """K5 multiplies f16 operands: a bf16 q element of magnitude >= 65520 has no f16
+    value, so the launch latches ESS_ERR_RANGE (ValueError at pool.check) instead of
+    returning silently wrong output; in-range q leaves the status clean."""
+    from paper_2512_10576_b200.attention import sparse_mla
+    from paper_2512_10576_b200.cache import PoolSet
+    from paper_2512_10576_b200.decode import random_latent_rows
+    B, cap = 2, 2048
+    pools = PoolSet(B, 4096, cap, cap, row_bytes=fmt)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    _fill_slots(pools, [random_latent_rows(cap, "cuda", g) for _ in range(B)], cap)
+    sel = torch.arange(cap, dtype=torch.int32, device="cuda").repeat(B, 1)
+    cnt = torch.full((B,), cap, dtype=torch.int32, device="cuda")
+    q = (torch.randn((B, 128, 576), device="cuda", generator=g) * 0.5).to(torch.bfloat16)
+    q[1, 7, 3] = 60000.0   # large but representable in f16: no error
+    sparse_mla(pools, q, sel, cnt)
+    pools.check("in range")
+    for bad in (70000.0, float("inf"), -1e6, 5e5):
+        q2 = q.clone()
+        q2[1, 100, 511 if bad > 0 else 560] = bad
+        sparse_mla(pools, q2, sel, cnt)
+        with pytest.raises(ValueError, match="f16 range"):
+            pools.check("q out of range")
+    pools.close()
+
+
+def test_gather_flags_slot_rows_outside_f16_range():
+    """The f16 slot format dequantises each fetched row once: a latent row whose RoPE
+    (bf16) or scaled NoPE value does not fit f16 latches ESS_ERR_RANGE in the gather."""
+    from paper_2512_10576_b200.cache import PoolSet
+    from paper_2512_10576_b200.decode import random_latent_rows
+    from paper_2512_10576_b200.transfer import HostLatentStore, gather
+    P, ids, cap = 2, 3000, 1024
+    store = HostLatentStore(P, ids)
+    for p in range(P):
+        store.host[p].copy_(random_latent_rows(ids, "cuda"))
+    h = store.host.numpy()
+    rope = h[1, 10, 528:].view(np.uint16)
+    rope[5] = 0x47C3   # bf16 99840: beyond f16
+    sc = h[0, 20, 512:528].view(np.float32)
+    sc[2] = 1024.0     # e4m3 values up to 448 x 1024: beyond f16 for |nope| > 64
+    for which, row_id in ((1, 10), (0, 20)):
+        pools = PoolSet(P, ids, cap, cap, row_bytes=1152)
+        sets = np.tile(np.arange(100, 200, dtype=np.int32), (P, 1))   # clean rows ...
+        sets[which, 0] = row_id                                       # ... and one bad one
+        acc = pools.access(torch.as_tensor(sets, device="cuda"),
+                           torch.full((P,), 100, dtype=torch.int32, device="cuda"))
+        gather(pools, store, acc)
+        with pytest.raises(ValueError, match="f16 range"):
+            pools.check("slot row out of range")
+        pools.close()
+    pools = PoolSet(P, ids, cap, cap, row_bytes=1152)   # rows 100.. are clean
+    sets = np.tile(np.arange(100, 400, dtype=np.int32), (P, 1))
+    acc = pools.access(torch.as_tensor(sets, device="cuda"), torch.full((P,), 300, dtype=torch.int32, device="cuda"))
+    gather(pools, store, acc)
+    pools.check("in range")
+    pools.close()
+    store.close()
+
+
+@FMT
+def test_sparse_mla_small_q_below_f16_normal_range(fmt):
+    """q of magnitude ~1e-6 (below f16's normal range, 6.1e-5: kept as f16 subnormals,
+    the smallest ~6e-8 flush to zero) still matches fp64 on the unrounded q within the
+    end-to-end tolerance: the scores are ~0 and the softmax near uniform."""
+    from paper_2512_10576_b200.attention import sparse_mla, DEFAULT_SM_SCALE
+    from paper_2512_10576_b200.cache import PoolSet
+    from paper_2512_10576_b200.decode import random_latent_rows
+    B, cap = 2, 2048
+    pools = PoolSet(B, 4096, cap, cap, row_bytes=fmt)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    lat = [random_latent_rows(cap, "cuda", g) for _ in range(B)]
+    _fill_slots(pools, lat, cap)
+    sel = torch.arange(cap, dtype=torch.int32, device="cuda").repeat(B, 1)
+    cnt = torch.full((B,), cap, dtype=torch.int32, device="cuda")
+    q = (torch.randn((B, 128, 576), device="cuda", generator=g) * 1e-6).to(torch.bfloat16)
+    out, lse = sparse_mla(pools, q, sel, cnt)
+    pools.check("small q")
+    qf = q.float().cpu().numpy()
+    for b in range(B):
+        ref_o, ref_l = dsa.sparse_mla(qf[b], lat[b].cpu().numpy(), DEFAULT_SM_SCALE)
+        o = out[b].float().cpu().numpy()
+        assert np.linalg.norm(o - ref_o) / np.linalg.norm(ref_o) <= 1e-2
+        assert np.abs(lse[b].cpu().numpy() - ref_l).max() <= 1e-2
+    pools.close()
