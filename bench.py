@@ -146,35 +146,61 @@ class ClockSampler:
 # -------------------------------------------------------------------------------------
 # CPU leg: the oracle port on host cores (cpu_baseline and --impl reference)
 # -------------------------------------------------------------------------------------
+CPU_WARM_WINDOWS = 4  # prefill windows per request in the CPU leg (the GPU layer uses 32)
+
+
 def _cpu_request(task):
-    """One request's decode step on one host core (oracle port): numpy indexer + top-k +
-    C LRU step + numpy sparse MLA, inputs of the config's shapes.  Returns seconds."""
-    L, rho, seed = task
+    """One request's decode step on one host core (oracle port), the GPU step's work in
+    order: numpy indexer -> top-k -> C LRU access step -> miss gather (the fetched 656-B
+    rows copied from the host store into the slot store) -> numpy sparse MLA over the
+    slot rows -> admission of the generated token (grow, append, row write-back).  The
+    pool is warmed first with prefill windows from the same drifting query process
+    (q_t = a q_{t-1} + sqrt(1-a^2) eps, the GPU layer's), untimed.  Returns (timed
+    seconds, hits, misses)."""
+    L, rho, seed, drift = task
     import numpy as np
     from threadpoolctl import threadpool_limits
 
     from oracle import dsa
     from oracle import lru as olru
 
+    import torch
+
+    def e4(a):  # e4m3 bytes, saturating (the GPU layer's _e4m3)
+        return torch.from_numpy(np.asarray(a, np.float32)).clamp(-448, 448).to(torch.float8_e4m3fn) \
+            .view(torch.uint8).numpy()
+
     rng = np.random.default_rng(seed)
-    e4 = lambda a: np.clip(np.round(a), -6, 6).astype(np.int8).view(np.uint8)  # noqa: E731
-    k = e4(rng.standard_normal((L, 128)) * 2)
-    q = e4(rng.standard_normal((64, 128)) * 2)
+    k = e4(rng.standard_normal((L, 128)) * 8)           # the GPU layer's key / query scales
     w = rng.standard_normal(64).astype(np.float32) / 8
-    ks = (rng.random(L).astype(np.float32) + 0.5)
-    rows = rng.integers(0, 120, size=(L, 656), dtype=np.uint8)
-    rows[:, 512:528] = np.full((L, 4), 0.03, np.float32).view(np.uint8)
-    rows[:, 528:] = 0
+    ks = (rng.random(L).astype(np.float32) * 0.5 + 0.75)
+    host = rng.integers(0, 120, size=(L + 1, 656), dtype=np.uint8)   # latent rows (+ the new one)
+    host[:, 512:528] = np.full((L + 1, 4), 0.03, np.float32).view(np.uint8)
+    host[:, 528:] = 0
+    slots = np.zeros_like(host)                                       # the slot store
+    a, sd = drift, float(np.sqrt(max(0.0, 1.0 - drift * drift)))
+    zi = rng.standard_normal((64, 128))
     qa = rng.standard_normal((128, 576)).astype(np.float32)
     pool = olru.OraclePool(olru.pool_capacity(rho, L))
-    pool.warmup([rng.choice(L, size=TOPK, replace=False)])
     with threadpool_limits(1):  # one core per request; requests run in parallel processes
+        for _ in range(CPU_WARM_WINDOWS):   # prefill -> decode handoff, untimed
+            zi = a * zi + sd * rng.standard_normal(zi.shape)
+            pool.warmup([dsa.topk_indices(dsa.indexer_logits(e4(zi * 4), w, k, ks, L), L, TOPK).tolist()])
+        res = pool.lru_order()
+        slots[res] = host[res]
+        zi = a * zi + sd * rng.standard_normal(zi.shape)
+        q = e4(zi * 4)
         t0 = time.perf_counter()
         logits = dsa.indexer_logits(q, w, k, ks, L)
         idx = dsa.topk_indices(logits, L, TOPK)
-        pool.access_step(idx.tolist())
-        dsa.sparse_mla(qa, rows[idx], 1.0 / 192 ** 0.5)
-        return time.perf_counter() - t0
+        r = pool.access_step(idx.tolist())
+        miss = np.asarray(r.miss_ids, dtype=np.int64)
+        slots[miss] = host[miss]                                      # K4: the miss gather
+        dsa.sparse_mla(qa, slots[idx], 1.0 / 192 ** 0.5)              # K5 over the slot rows
+        pool.grow_capacity(olru.pool_capacity(rho, L + 1))           # admission (cache.py:191-195)
+        pool.append_generated([L])
+        slots[L] = host[L]
+        return time.perf_counter() - t0, len(r.hit_ids), len(r.miss_ids)
 
 
 def _cpu_pool(workers):
@@ -182,7 +208,7 @@ def _cpu_pool(workers):
     if not hasattr(_cpu_pool, "p"):
         # spawn: the parent holds a CUDA context, which must not be forked
         _cpu_pool.p = mp.get_context("spawn").Pool(workers)
-        _cpu_pool.p.map(_cpu_request, [(4096, 0.25, i) for i in range(workers)])  # imports, oracle lib
+        _cpu_pool.p.map(_cpu_request, [(4096, 0.25, i, 0.97) for i in range(workers)])  # imports, oracle lib
     return _cpu_pool.p
 
 
@@ -194,25 +220,34 @@ def _cpu_pool_close():
         del _cpu_pool.p
 
 
-def cpu_reference_rate(cfg, budget_s: float = 12.0, seed: int = 0):
+def cpu_reference_rate(cfg, budget_s: float = 12.0, seed: int = 0, drift: float = 0.97):
     """The CPU oracle on every host core: rounds of one request per core (one decode step
-    each, the config's shapes), wall-clock timed.  Returns (tokens/s, sample, cores)."""
+    each, the config's shapes and query drift, after an untimed warm-up), timed per
+    request inside the worker.  Rate = cores / mean timed seconds per request-step (each
+    core runs one request at a time).  Returns (tokens/s, sample, cores, hit rate)."""
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     lens = request_lengths(cfg, max(cfg["batch"], cores), seed=seed + 17)
     pool = _cpu_pool(cores)
-    n_req, wall, rnd = 0, 0.0, 0
+    n_req, wall, rnd, times, hits, misses = 0, 0.0, 0, [], 0, 0
     while n_req < 1 or (wall < budget_s and n_req < 4 * max(cfg["batch"], cores)):
-        tasks = [(lens[(n_req + i) % len(lens)], cfg["sparse_ratio"], seed + 1000 * rnd + i)
+        tasks = [(lens[(n_req + i) % len(lens)], cfg["sparse_ratio"], seed + 1000 * rnd + i, drift)
                  for i in range(cores)]
         t0 = time.perf_counter()
-        pool.map(_cpu_request, tasks, chunksize=1)
+        for t, h, m in pool.map(_cpu_request, tasks, chunksize=1):
+            times.append(t)
+            hits += h
+            misses += m
         wall += time.perf_counter() - t0
         n_req += cores
         rnd += 1
-    sample = (f"{n_req} request-steps of the {cfg['workload']} workload, {cores} at a time (one per "
-              f"core, spawn processes, single-threaded BLAS): numpy indexer + top-k + C LRU step + "
-              f"numpy sparse MLA (oracle port), {wall:.2f} s wall")
-    return n_req / wall, sample, cores
+    mean_t = sum(times) / len(times)
+    hit_rate = hits / max(1, hits + misses)
+    sample = (f"{n_req} request-steps of the {cfg['workload']} workload at query drift {drift}, {cores} at a "
+              f"time (one per core, spawn processes, single-threaded BLAS), each after an untimed "
+              f"{CPU_WARM_WINDOWS}-window prefill warm-up: numpy indexer + top-k + C LRU step + miss gather "
+              f"into the slot store + numpy sparse MLA + admission (oracle port); mean {mean_t * 1e3:.1f} ms "
+              f"per request-step, hit rate {hit_rate:.3f}, {wall:.2f} s wall")
+    return cores / mean_t, sample, cores, hit_rate
 
 
 def run_reference(args, cfg):
@@ -221,11 +256,11 @@ def run_reference(args, cfg):
         return
     vals = []
     for _ in range(args.warmup):
-        cpu_reference_rate(cfg, budget_s=2.0)
+        cpu_reference_rate(cfg, budget_s=1.0, drift=args.drift)
     t0 = time.perf_counter()
-    sample = threads = None
-    for _ in range(args.steps):
-        v, sample, threads = cpu_reference_rate(cfg, budget_s=5.0)
+    sample = threads = hit_rate = None
+    for i in range(args.steps):
+        v, sample, threads, hit_rate = cpu_reference_rate(cfg, budget_s=3.0, seed=i, drift=args.drift)
         vals.append(v)
     el = time.perf_counter() - t0
     _cpu_pool_close()
@@ -238,7 +273,10 @@ def run_reference(args, cfg):
                        "context_len": cfg["context_len"] if isinstance(cfg["context_len"], int)
                        else "mixed {}-{} log-uniform".format(*cfg["context_len"]),
                        "sparse_ratio": cfg["sparse_ratio"],
-                       "topk": TOPK},
+                       "topk": TOPK, "query_drift": args.drift,
+                       "overlap": "none (one request per core, sequential K1..K5 + admission)",
+                       "prefill_windows": CPU_WARM_WINDOWS},
+            "hit_rate": hit_rate,
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
@@ -597,7 +635,7 @@ def run_ours(args, cfg):
         os.sched_setaffinity(0, prev_aff)
     line = None
     if rank == 0:
-        cpu_v, cpu_sample, cpu_threads = cpu_reference_rate(cfg, budget_s=12.0)
+        cpu_v, cpu_sample, cpu_threads, _ = cpu_reference_rate(cfg, budget_s=12.0, drift=args.drift)
         _cpu_pool_close()
         line = {
             "metric": METRIC, "value": main["value"], "unit": "tokens/s", "n_gpus": world,
