@@ -895,7 +895,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--drift", type=float, default=0.97)
     ap.add_argument("--gather-ctas", type=int, default=32)
-    ap.add_argument("--overlap", default="dba", choices=["dba", "da", "none"])
+    ap.add_argument("--overlap", default="dba", choices=["dba", "da", "none", "stream"])
     ap.add_argument("--micro", type=int, default=None, help="DBA micro-batches per step (default: per config)")
     ap.add_argument("--first", type=float, default=None,
                     help="DBA: fraction of the batch in the first micro-batch (default: per config)")

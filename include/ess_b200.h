@@ -202,6 +202,15 @@ int ess_gather_signal(ess_pool *pool, int32_t begin, int32_t num, const void *d_
                       int64_t host_pool_stride_rows, const int32_t *d_miss_ids,
                       const int32_t *d_miss_row, const int32_t *d_counts, int32_t stride,
                       int32_t *d_landed, int32_t max_ctas, int32_t flags, void *stream);
+/* The streamed step's gather: launched with the step, it takes request b once
+ * d_ready[b] != 0 (ess_topk_split_stream), warps claiming chunks of its miss list from
+ * d_claim[b] (zero at launch), every landed chunk added to d_landed[b] (release; may be
+ * NULL).  Requests are taken in order; rows as in ess_gather.  No ESS_GATHER_BULK. */
+int ess_gather_stream(ess_pool *pool, int32_t begin, int32_t num, const void *d_host_rows,
+                      int64_t host_pool_stride_rows, const int32_t *d_miss_ids,
+                      const int32_t *d_miss_row, const int32_t *d_counts, int32_t stride,
+                      const int32_t *d_ready, int32_t *d_claim, int32_t *d_landed, int32_t max_ctas,
+                      int32_t flags, void *stream);
 /* D2H write-back + slot fill of generated rows (cache.py:122-134):
  * src rows [num][stride][656] -> host_rows[pool][id] and slot store[pool][slot] */
 int ess_write_generated(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_ids,
@@ -234,6 +243,20 @@ int ess_indexer_logits_mtp(const void *d_q, const float *d_w, const void *d_k,
                            int32_t qtok, int64_t k_ld, float *d_logits, int32_t max_ctas,
                            void *stream);
 
+/* The streamed step (one CUDA graph, three concurrent kernels with per-request hand-off
+ * counters instead of micro-batches): the indexer processes requests in groups of
+ * `group` with the whole grid, and after storing its logits rows of request b every
+ * epilogue warp adds their number to d_done[b] (release).  group: requests per group in
+ * its low 16 bits, the first group's size in the high 16 bits (0: the same; a small first
+ * group starts the host link sooner).  d_done reaches min(len[b],
+ * k_ld) when b's logits are complete.  d_done [batch] zero at launch.  max_ctas must
+ * leave SMs for the concurrent ess_topk_split_stream and ess_gather_stream grids (all
+ * three must be co-resident). */
+int ess_indexer_logits_stream(const void *d_q, const float *d_w, const void *d_k,
+                              const float *d_kscale, const int32_t *d_len, int32_t batch,
+                              int64_t k_ld, float *d_logits, int32_t max_ctas, int32_t group,
+                              int32_t *d_done, void *stream);
+
 /* ---- K2 top-k (op "indexer_topk") ---------------------------------------------- */
 /* per row: the k largest logits[b][0:len[b]) by (score desc, index asc), written
  * ascending to d_idx [B][idx_ld]; d_count[b] = min(k, len[b]) (scenario.py:110-112);
@@ -252,6 +275,17 @@ int ess_topk_split(const float *d_logits, int64_t ld, const int32_t *d_len, int3
                    int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count, ess_pool *pool,
                    int32_t pool_begin, int32_t *d_hit_row, int32_t *d_miss_ids,
                    int32_t *d_miss_row, int32_t *d_counts, int32_t out_stride, void *stream);
+
+/* Streamed K2 + K3a: `ctas` persistent CTAs (ctas < 0: -ctas two-CTA clusters, one row
+ * per pair) take the requests in order; row b starts
+ * once d_done[b] == min(len[b], ld) (ess_indexer_logits_stream), then the top-k and the
+ * early-gather split of ess_topk_split run and d_ready[b] is set to 1 (release).  Rows
+ * up to 40K tokens (one CTA each); d_ready [batch] zero at launch. */
+int ess_topk_split_stream(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
+                          int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count, ess_pool *pool,
+                          int32_t pool_begin, int32_t *d_hit_row, int32_t *d_miss_ids,
+                          int32_t *d_miss_row, int32_t *d_counts, int32_t out_stride,
+                          const int32_t *d_done, int32_t *d_ready, int32_t ctas, void *stream);
 
 /* ---- K5 sparse MLA decode (ops "sparse_mla" + "merge_attn") --------------------- */
 /* out[b][h] = softmax_j(q[b][h] . K[j] * sm_scale) V[j] over the rows

@@ -50,6 +50,10 @@ SIGNATURES = {
     "ess_indexer_logits": ([V, V, V, V, V, I32, I64, V, V], ctypes.c_int),
     "ess_indexer_logits_ex": ([V, V, V, V, V, I32, I64, V, I32, V], ctypes.c_int),
     "ess_indexer_logits_mtp": ([V, V, V, V, V, I32, I32, I64, V, I32, V], ctypes.c_int),
+    "ess_indexer_logits_stream": ([V, V, V, V, V, I32, I64, V, I32, I32, V, V], ctypes.c_int),
+    "ess_topk_split_stream": ([V, I64, V, I32, I32, V, I32, V, V, I32, V, V, V, V, I32, V, V, I32, V],
+                              ctypes.c_int),
+    "ess_gather_stream": ([V, I32, I32, V, I64, V, V, V, I32, V, V, V, I32, I32, V], ctypes.c_int),
     "ess_topk": ([V, I64, V, I32, I32, V, I32, V, V], ctypes.c_int),
     "ess_topk_mtp": ([V, I64, V, I32, I32, I32, V, I32, V, V], ctypes.c_int),
     "ess_topk_split": ([V, I64, V, I32, I32, V, I32, V, V, I32, V, V, V, V, I32, V], ctypes.c_int),

@@ -137,10 +137,75 @@ __device__ __forceinline__ bool bf16x8_over_f16(uint4 v) {
   return bf16x2_over_f16(v.x) | bf16x2_over_f16(v.y) | bf16x2_over_f16(v.z) | bf16x2_over_f16(v.w);
 }
 
+// Cross-kernel hand-off flags of the streamed step (GPU scope): a producer kernel
+// publishes with a release add / store after its data stores, a consumer kernel polls
+// with acquire loads (one lane, bounded: trap instead of a hang) and then reads the data
+// through L2 (ld.global.cg), never through the non-coherent path.
+__device__ __forceinline__ int ess_ld_acquire(const int32_t *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void ess_red_release_add(int32_t *p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void ess_st_release(int32_t *p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // Bounded mbarrier / flag spin: trap instead of hanging the GPU on a protocol bug.
 #ifndef ESS_SPIN_LIMIT
 #define ESS_SPIN_LIMIT (1u << 26)
 #endif
+
+// Scratch builds (-DESS_STREAM_PROF): per-request globaltimer stamps of the streamed
+// step — [b][0] top-k start, [1] split published, [2] last gather chunk landed — read
+// by scripts/stream_timeline.py through ess_debug_stream_prof_{topk,gather}.
+#ifdef ESS_STREAM_PROF
+#define ESS_STREAM_PROF_READER(name)                                                           \
+  extern "C" int name(unsigned long long *host, int reset) {                                   \
+    if (reset) {                                                                               \
+      static unsigned long long zero[1024][4];                                                 \
+      return cudaMemcpyToSymbol(g_stream_prof, zero, sizeof(zero)) == cudaSuccess ? 0 : -7;    \
+    }                                                                                          \
+    return cudaMemcpyFromSymbol(host, g_stream_prof, sizeof(g_stream_prof)) == cudaSuccess ? 0 \
+                                                                                          : -7; \
+  }
+#endif
+#ifdef ESS_STREAM_PROF
+static __device__ unsigned long long g_stream_prof[1024][4];  // one copy per translation unit
+__device__ __forceinline__ unsigned long long ess_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define SPROF(b, i) (g_stream_prof[(b)][(i)] = ess_gtimer())
+#define SPROF_MAX(b, i) atomicMax(&g_stream_prof[(b)][(i)], ess_gtimer())
+#else
+#define SPROF(b, i) \
+  do {              \
+  } while (0)
+#define SPROF_MAX(b, i) \
+  do {                  \
+  } while (0)
+#endif
+
+// One lane polls (acquire, GPU scope, bounded) until *p >= target; then every lane
+// acquires once itself, so the producer's released stores are visible to the warp.
+// Exponential back-off (64 ns .. 1 us): many warps polling one flag must not turn its
+// L2 slice into a hot spot for the concurrent HBM-bound indexer.
+__device__ __forceinline__ void ess_warp_wait_geq(const int32_t *p, int target) {
+  if ((threadIdx.x & 31) == 0) {
+    uint32_t spins = 0, ns = 64;
+    while (ess_ld_acquire(p) < target) {
+      if (++spins > ESS_SPIN_LIMIT) __trap();
+      __nanosleep(ns);
+      ns = ns < 1024 ? 2 * ns : 1024;
+    }
+  }
+  __syncwarp();
+  (void)ess_ld_acquire(p);
+}
 
 // ---------------------------------------------------------------------------------
 // PTX wrappers: mbarrier, TMA, tcgen05 (sm_100a)

@@ -113,6 +113,62 @@ struct TileCursor {
   }
 };
 
+// The CTA's share of the flattened (request, unit) sequence.  Requests form groups of
+// `rg` (rg >= B: one group, the plain persistent split); the CTA takes its contiguous
+// slice of every group's units, group after group, so the whole grid finishes the
+// requests of group 0 first — the streamed step's top-k starts on them while the
+// indexer still runs (per-request completion counters, ess_indexer_logits_stream).
+struct UnitSeq {
+  int g, ngroups, rg, rg0, B, grid, cta, idx, end;
+  TileCursor cur;
+  // group gg: requests [b0, b1) — the first group has rg0 requests, the others rg
+  __device__ int group_begin(int gg) const { return gg == 0 ? 0 : min(B, rg0 + (gg - 1) * rg); }
+  __device__ bool slice(const int *pref, int gg, int &s, int &e) const {
+    const int b0 = group_begin(gg), b1 = group_begin(gg + 1);
+    const int u0 = pref[b0], tot = pref[b1] - u0;
+    s = u0 + (int)((int64_t)tot * cta / grid);
+    e = u0 + (int)((int64_t)tot * (cta + 1) / grid);
+    return s < e;
+  }
+  __device__ void open(const int *pref) {  // the first non-empty slice from group g on
+    for (; g < ngroups; g++) {
+      int s0, e0;
+      if (slice(pref, g, s0, e0)) {
+        idx = s0;
+        end = e0;
+        cur.seek(pref, B, s0);
+        return;
+      }
+    }
+  }
+  __device__ void start(const int *pref, int B_, int rg_, int rg0_) {
+    B = B_;
+    rg = rg_;
+    rg0 = rg0_ < rg_ ? rg0_ : rg_;
+    ngroups = 1 + (B - rg0 + rg - 1) / rg;
+    cta = blockIdx.x;
+    grid = gridDim.x;
+    g = 0;
+    open(pref);
+  }
+  __device__ int count(const int *pref) const {
+    int n = 0;
+    for (int gg = 0; gg < ngroups; gg++) {
+      int s0, e0;
+      if (slice(pref, gg, s0, e0)) n += e0 - s0;
+    }
+    return n;
+  }
+  __device__ void next(const int *pref) {
+    if (++idx < end) {
+      cur.next(pref, B);
+    } else {
+      g++;
+      open(pref);
+    }
+  }
+};
+
 __device__ __forceinline__ void group_bar(int g) {  // the 128 threads of epilogue group g
   asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
 }
@@ -121,7 +177,8 @@ template <int QT>
 __global__ void __launch_bounds__(NTHREADS, 1)
     indexer_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_q,
                    const float *__restrict__ w, const float *__restrict__ kscale,
-                   const int32_t *__restrict__ lens, int B, int64_t k_ld, float *__restrict__ logits) {
+                   const int32_t *__restrict__ lens, int B, int64_t k_ld, float *__restrict__ logits,
+                   int rg, int32_t *done) {
   using C = K1Cfg<QT>;
   constexpr int SUB = C::SUB, UNIT_M = C::UNIT_M, STAGES = C::STAGES, NACC = C::NACC;
   constexpr int UT_BYTES = C::UT_BYTES, QT_BYTES = C::QT_BYTES, ACC_COLS = C::ACC_COLS;
@@ -173,10 +230,9 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   tc_fence_after();
   if (threadIdx.x == 0) K1PROF(1);
   const uint32_t tmem = c.tmem;
-  const int total = c.pref[B];
-  const int t0 = (int)((int64_t)total * blockIdx.x / gridDim.x);
-  const int t1 = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
-  const int ntiles = t1 - t0;
+  UnitSeq seq0;
+  seq0.start(c.pref, B, rg & 0xFFFF, rg >> 16 ? rg >> 16 : rg & 0xFFFF);
+  const int ntiles = seq0.count(c.pref);
 
   if (ntiles > 0) {
     if (warp == 0) {
@@ -185,8 +241,8 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         prefetch_tmap(&tm_k);
         prefetch_tmap(&tm_q);
         const uint64_t kpol = l2_policy_evict_first();
-        TileCursor cur;
-        cur.seek(c.pref, B, t0);
+        UnitSeq seq = seq0;
+        const TileCursor &cur = seq.cur;
         int qs = 1, prev_b = -1, len_b = 0;
         uint32_t quse[2] = {0, 0};
         for (int it = 0; it < ntiles; it++) {
@@ -215,14 +271,14 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             tma_load_2d(smem + (size_t)s * UT_BYTES + j * KT_BYTES, &tm_k, &c.full[s], 0,
                         (int32_t)(cur.b * k_ld + (int64_t)cur.t * UNIT_M + j * TILE_M));
 #endif
-          cur.next(c.pref, B);
+          seq.next(c.pref);
         }
       }
     } else if (warp == 1) {
       // ---- MMA issuer ---------------------------------------------------------------
       if (elect_one()) {
-        TileCursor cur;
-        cur.seek(c.pref, B, t0);
+        UnitSeq seq = seq0;
+        const TileCursor &cur = seq.cur;
         int qs = 1, prev_b = -1;
         uint32_t quse[2] = {0, 0};
         for (int it = 0; it < ntiles; it++) {
@@ -251,7 +307,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
           tc_commit(&c.empty[s]);
           tc_commit(&c.tfull[a]);
-          cur.next(c.pref, B);
+          seq.next(c.pref);
         }
       }
     } else {
@@ -260,10 +316,11 @@ __global__ void __launch_bounds__(NTHREADS, 1)
       const int g = e >> 2;
       const int quarter = warp & 3;
       const int row = quarter * 32 + lane;
-      TileCursor cur;
-      cur.seek(c.pref, B, t0);
-      if (g == 1) cur.next(c.pref, B);
+      UnitSeq seq = seq0;
+      const TileCursor &cur = seq.cur;
+      if (g == 1) seq.next(c.pref);
       int wb = -1, len_b = 0;
+      int acc_b = seq.cur.b, acc_n = 0;  // streamed step: rows stored for request acc_b
       float wr[QT == 1 ? HEADS : 1];  // QT = 1: head weights in registers
       for (int it = g; it < ntiles; it += 2) {
         const int b = cur.b;
@@ -349,8 +406,31 @@ __global__ void __launch_bounds__(NTHREADS, 1)
             if (valid[0]) logits[((int64_t)b * QT + jq) * k_ld + tok] = ((a0 + a1) + (a2 + a3)) * ks[0];
           }
         }
-        cur.next(c.pref, B);
-        cur.next(c.pref, B);
+        if (done) {  // streamed step: count this warp's stored rows of request b
+#pragma unroll
+          for (int j = 0; j < SUB; j++) acc_n += __popc(__ballot_sync(0xffffffffu, valid[j]));
+        }
+        seq.next(c.pref);
+        seq.next(c.pref);
+        if (done && seq.cur.b != acc_b) {
+          // the warp leaves request acc_b (its slice is contiguous, so it never returns):
+          // publish its rows once (one release = one wait for the warp's stores, per
+          // request instead of per unit)
+          __syncwarp();
+          if (lane == 0 && acc_n) {
+            ess_red_release_add(done + acc_b, acc_n);
+            SPROF_MAX(acc_b, 3);
+          }
+          acc_b = seq.cur.b;
+          acc_n = 0;
+        }
+      }
+      if (done) {  // the warp's last request
+        __syncwarp();
+        if (lane == 0 && acc_n) {
+          ess_red_release_add(done + acc_b, acc_n);
+          SPROF_MAX(acc_b, 3);
+        }
       }
     }
   }
@@ -409,7 +489,7 @@ namespace {
 template <int QT>
 int launch_indexer(const void *d_q, const float *d_w, const void *d_k, const float *d_kscale,
                    const int32_t *d_len, int32_t batch, int64_t k_ld, float *d_logits,
-                   int32_t max_ctas, void *stream) {
+                   int32_t max_ctas, int32_t group, int32_t *d_done, void *stream) {
   using C = K1Cfg<QT>;
   static thread_local MapCache kc, qc;
   alignas(64) CUtensorMap tk;
@@ -419,7 +499,7 @@ int launch_indexer(const void *d_q, const float *d_w, const void *d_k, const flo
   if (int rc = ess_smem_optin((const void *)indexer_kernel<QT>, C::SMEM_BYTES)) return rc;
   const int ctas = max_ctas > 0 && max_ctas < ess_sm_count() ? max_ctas : ess_sm_count();
   indexer_kernel<QT><<<ctas, NTHREADS, C::SMEM_BYTES, (cudaStream_t)stream>>>(
-      tk, tq, d_w, d_kscale, d_len, batch, k_ld, d_logits);
+      tk, tq, d_w, d_kscale, d_len, batch, k_ld, d_logits, group > 0 ? group : batch, d_done);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }
@@ -446,9 +526,33 @@ extern "C" int ess_indexer_logits_mtp(const void *d_q, const float *d_w, const v
     return ESS_ERR_ARG;
   if (batch == 0) return ESS_OK;
   switch (qtok) {
-    case 1: return launch_indexer<1>(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, max_ctas, stream);
-    case 2: return launch_indexer<2>(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, max_ctas, stream);
-    case 3: return launch_indexer<3>(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, max_ctas, stream);
-    default: return launch_indexer<4>(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, max_ctas, stream);
+    case 1: return launch_indexer<1>(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, max_ctas, 0, nullptr, stream);
+    case 2: return launch_indexer<2>(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, max_ctas, 0, nullptr, stream);
+    case 3: return launch_indexer<3>(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, max_ctas, 0, nullptr, stream);
+    default: return launch_indexer<4>(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, max_ctas, 0, nullptr, stream);
   }
 }
+
+// Streamed step: requests in groups of `group`, the whole grid finishing each group
+// before the next; after storing its logits rows of a unit every epilogue warp adds the
+// number of rows it stored to d_done[b] (release, GPU scope), so d_done[b] reaches
+// min(len[b], k_ld) exactly when request b's logits are complete.  d_done [batch] must be
+// zero at launch.
+extern "C" int ess_indexer_logits_stream(const void *d_q, const float *d_w, const void *d_k,
+                                         const float *d_kscale, const int32_t *d_len, int32_t batch,
+                                         int64_t k_ld, float *d_logits, int32_t max_ctas, int32_t group,
+                                         int32_t *d_done, void *stream) {
+  if (max_ctas < 0 || group < 0 || !d_done) return ESS_ERR_ARG;
+  if (!d_q || !d_w || !d_k || !d_kscale || !d_len || !d_logits || batch < 0 ||
+      batch > MAX_BATCH || k_ld < TILE_M || (k_ld % TILE_M) != 0 ||
+      (reinterpret_cast<uintptr_t>(d_k) & 15) || (reinterpret_cast<uintptr_t>(d_q) & 15) ||
+      (reinterpret_cast<uintptr_t>(d_w) & 15))
+    return ESS_ERR_ARG;
+  if (batch == 0) return ESS_OK;
+  return launch_indexer<1>(d_q, d_w, d_k, d_kscale, d_len, batch, k_ld, d_logits, max_ctas, group, d_done,
+                           stream);
+}
+
+#ifdef ESS_STREAM_PROF
+ESS_STREAM_PROF_READER(ess_debug_stream_prof_k1)
+#endif

@@ -1083,6 +1083,68 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
   publish();
 }
 
+// K4, streamed form: the gather starts with the step and takes each request as soon as
+// the streamed top-k published its split (ready[b], acquire): warps claim GROWS-row
+// chunks of request b's miss list from claim[b] (atomic tickets, requests in order), so
+// every warp works on the earliest request that still has rows.  Each chunk's rows are
+// published on landed[b] (release) for the fused DA attention.  The lists were written
+// by a concurrent kernel: read through L2 (ld.global.cg).
+__global__ void __launch_bounds__(NTG) gather_stream_kernel(PoolView pv, int begin, int num,
+                                                            const uint8_t *host, int64_t host_stride,
+                                                            const int32_t *miss_ids, const int32_t *miss_row,
+                                                            const int32_t *counts, int stride,
+                                                            const int32_t *ready, int32_t *claim,
+                                                            int32_t *landed) {
+  const int lane = threadIdx.x & 31;
+  const int64_t rb = pv.row_bytes;
+  int b = 0, nmiss = -1;
+  while (b < num) {
+    if (nmiss < 0) {
+      ess_warp_wait_geq(ready + b, 1);
+      nmiss = __ldcg(counts + (int64_t)b * 4 + 1);
+    }
+    int j0 = 0;
+    if (lane == 0) j0 = atomicAdd(claim + b, GROWS);
+    j0 = __shfl_sync(0xffffffffu, j0, 0);
+    if (j0 >= nmiss) {
+      b++;
+      nmiss = -1;
+      continue;
+    }
+    const int nr = min(GROWS, nmiss - j0);
+    const uint8_t *src[GROWS];
+    uint8_t *dst[GROWS];
+#pragma unroll
+    for (int r = 0; r < GROWS; r++) {
+      src[r] = nullptr;
+      if (r < nr) {
+        const int id = __ldcg(miss_ids + (int64_t)b * stride + j0 + r);
+        const int row = __ldcg(miss_row + (int64_t)b * stride + j0 + r);
+        src[r] = host + ((int64_t)b * host_stride + id) * ESS_HOST_ROW_PITCH;
+        dst[r] = pv.rows + ((int64_t)(begin + b) * pv.rows_per_pool + row) * rb;
+      }
+    }
+    uint4 v[GROWS][2];
+#pragma unroll
+    for (int r = 0; r < GROWS; r++) {
+      v[r][1] = make_uint4(0, 0, 0, 0);
+      if (src[r]) {
+        v[r][0] = ld_host_v4(src[r] + lane * 16);
+        if (lane + 32 < ROW_CHUNKS) v[r][1] = ld_host_v4(src[r] + (lane + 32) * 16);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < GROWS; r++)
+      if (src[r] && store_slot_row(v[r][0], v[r][1], lane, dst[r], (int)rb)) ess_set_status(pv.status, ESS_ERR_RANGE);
+    if (landed) {
+      __threadfence();  // every lane's slot stores before the release add
+      __syncwarp();
+      if (lane == 0) ess_red_release_add(landed + b, nr);
+    }
+    if (lane == 0) SPROF_MAX(b, 2);
+  }
+}
+
 // K4, bulk-copy form (ESS_GATHER_BULK): each warp streams its contiguous run of the
 // flattened miss list through a ring of GB_RING 656-B shared-memory row buffers filled
 // by one-instruction `cp.async.bulk` copies straight from the mapped host store (one
@@ -1616,6 +1678,25 @@ int ess_gather_signal(ess_pool *p, int32_t begin, int32_t num, const void *d_hos
   return ESS_OK;
 }
 
+int ess_gather_stream(ess_pool *p, int32_t begin, int32_t num, const void *d_host_rows,
+                      int64_t host_pool_stride_rows, const int32_t *d_miss_ids,
+                      const int32_t *d_miss_row, const int32_t *d_counts, int32_t stride,
+                      const int32_t *d_ready, int32_t *d_claim, int32_t *d_landed, int32_t max_ctas,
+                      int32_t flags, void *stream) {
+  if (!range_ok(p, begin, num) || !p->rows || !d_host_rows || !d_miss_ids || !d_miss_row ||
+      !d_counts || stride < 1 || max_ctas < 1 || !d_ready || !d_claim || (flags & ESS_GATHER_BULK))
+    return ESS_ERR_ARG;
+  if (num == 0) return ESS_OK;
+  size_t smem = 0;
+  if (flags & ESS_GATHER_EXCLUSIVE_SM) smem = ESS_GATHER_EXCLUSIVE_SMEM;
+  if (int rc = ess_smem_optin((const void *)gather_stream_kernel, smem)) return rc;
+  gather_stream_kernel<<<max_ctas, NTG, smem, (cudaStream_t)stream>>>(
+      view(p), begin, num, (const uint8_t *)d_host_rows, host_pool_stride_rows, d_miss_ids, d_miss_row,
+      d_counts, stride, d_ready, d_claim, d_landed);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
+}
+
 int ess_pool_admit(ess_pool *p, int32_t begin, int32_t num, int32_t *d_hist, const int32_t *d_m,
                    double rho, const void *d_src_rows, int32_t src_stride, void *d_host_rows,
                    int64_t host_pool_stride_rows, int32_t *d_slot_out, void *stream) {
@@ -1645,3 +1726,7 @@ int ess_write_generated(ess_pool *p, int32_t begin, int32_t num, const int32_t *
 }
 
 }  // extern "C"
+
+#ifdef ESS_STREAM_PROF
+ESS_STREAM_PROF_READER(ess_debug_stream_prof_gather)
+#endif

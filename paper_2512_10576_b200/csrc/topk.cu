@@ -218,11 +218,14 @@ __device__ __forceinline__ void split_tail(int b, const int32_t *o, int n, const
   }
 }
 
-template <int CLN>
-__global__ void __launch_bounds__(NT, 1)
-    topk_kernel(const float *__restrict__ logits, int64_t ld, const int32_t *__restrict__ lens,
-                int k, int32_t *__restrict__ out, int out_ld, int32_t *__restrict__ counts,
-                SplitArgs sp) {
+// One row (b) of the top-k on this CTA (cluster).  STREAM: the row's logits are being
+// written by a concurrent indexer launch (ess_indexer_logits_stream) and were published
+// with a release; they are read through L2 (ld.global.cg), not the non-coherent path.
+template <int CLN, bool STREAM>
+__device__ __forceinline__ void topk_row(const int b, const float *__restrict__ logits, int64_t ld,
+                                         const int32_t *__restrict__ lens, int k,
+                                         int32_t *__restrict__ out, int out_ld,
+                                         int32_t *__restrict__ counts, const SplitArgs &sp) {
   extern __shared__ uint32_t skey[];  // slice_cap keys, then LCAP u16 list entries + NT trash
   uint16_t *list = reinterpret_cast<uint16_t *>(skey + slice_cap<CLN>(ld));
   __shared__ int hist[D1_BINS];
@@ -234,7 +237,6 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ int pre[2];   // cluster rows: (greater, equal) totals of the lower ranks (pushed)
   int rank = 0;
   if constexpr (CLN > 1) rank = (int)cg::this_cluster().block_rank();
-  const int b = blockIdx.x / CLN;
   const int len = (int)min((int64_t)lens[b / sp.len_div], ld);  // a len past the row stride reads no further
   const float *row = logits + (int64_t)b * ld;
   int32_t *o = out + (int64_t)b * out_ld;
@@ -276,7 +278,10 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
       for (int u = 0; u < U; u++) {
         const int i = i0 + u * NT * VEC;
-        if (i < n4) v[u] = __ldg(reinterpret_cast<const float4 *>(src + i));
+        if (i < n4) {
+          if constexpr (STREAM) v[u] = __ldcg(reinterpret_cast<const float4 *>(src + i));
+          else v[u] = __ldg(reinterpret_cast<const float4 *>(src + i));
+        }
       }
 #pragma unroll
       for (int u = 0; u < U; u++) {
@@ -293,7 +298,7 @@ __global__ void __launch_bounds__(NT, 1)
       }
     }
     for (int i = n4 + threadIdx.x; i < n; i += NT) {
-      const uint32_t key = score_key(src[i]);
+      const uint32_t key = score_key(STREAM ? __ldcg(src + i) : src[i]);
       skey[i] = key;
       atomicAdd(&hist[key >> D1_SHIFT], 1);
     }
@@ -545,6 +550,42 @@ __global__ void __launch_bounds__(NT, 1)
       split_tail(b, o, k, sp, wbuf);
     }
   }
+  KPROF(10);
+}
+
+template <int CLN>
+__global__ void __launch_bounds__(NT, 1)
+    topk_kernel(const float *__restrict__ logits, int64_t ld, const int32_t *__restrict__ lens,
+                int k, int32_t *__restrict__ out, int out_ld, int32_t *__restrict__ counts,
+                SplitArgs sp) {
+  topk_row<CLN, false>(blockIdx.x / CLN, logits, ld, lens, k, out, out_ld, counts, sp);
+}
+
+// Streamed step (K2 + K3a): a persistent grid walks the requests in order (CTA c takes
+// c, c + grid, ...); row b starts once the concurrent indexer has published all its
+// logits (done[b] == min(len, ld)); after the top-k and the hit/miss split the CTA
+// publishes ready[b] = 1 (release) for the streamed gather.  CLN-CTA clusters per row
+// (CLN = 2 halves a row's latency: the first rows gate the host link).
+template <int CLN>
+__global__ void __launch_bounds__(NT, 1)
+    topk_stream_kernel(const float *__restrict__ logits, int64_t ld, const int32_t *__restrict__ lens,
+                       int B, int k, int32_t *__restrict__ out, int out_ld,
+                       int32_t *__restrict__ counts, SplitArgs sp, const int32_t *done, int32_t *ready) {
+  const int nclu = gridDim.x / CLN;
+  for (int b = blockIdx.x / CLN; b < B; b += nclu) {
+    __syncthreads();  // the previous row's shared-memory readers are done
+    if (threadIdx.x < 32) ess_warp_wait_geq(done + b, (int)min((int64_t)lens[b], ld));
+    __syncthreads();
+    if (threadIdx.x == 0) SPROF(b, 0);
+    topk_row<CLN, true>(b, logits, ld, lens, k, out, out_ld, counts, sp);
+    __threadfence();  // this thread's selection / split outputs, before the flag
+    if constexpr (CLN > 1) cg::this_cluster().sync();  // every rank's part (rank 0 split)
+    else __syncthreads();
+    if (threadIdx.x == 0 && (CLN == 1 || cg::this_cluster().block_rank() == 0)) {
+      ess_st_release(ready + b, 1);
+      SPROF(b, 1);
+    }
+  }
 }
 
 template <int CLN>
@@ -668,3 +709,62 @@ extern "C" int ess_topk_split(const float *d_logits, int64_t ld, const int32_t *
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }
+
+// Streamed K2 + K3a (see topk_stream_kernel): rows <= 40K tokens (one CTA per row),
+// `ctas` persistent CTAs; d_done from ess_indexer_logits_stream, d_ready [batch] zero
+// at launch, set to 1 per request once its selection, split rows and counts are stored.
+extern "C" int ess_topk_split_stream(const float *d_logits, int64_t ld, const int32_t *d_len,
+                                     int32_t batch, int32_t k, int32_t *d_idx, int32_t idx_ld,
+                                     int32_t *d_count, ess_pool *pool, int32_t pool_begin,
+                                     int32_t *d_hit_row, int32_t *d_miss_ids, int32_t *d_miss_row,
+                                     int32_t *d_counts, int32_t out_stride, const int32_t *d_done,
+                                     int32_t *d_ready, int32_t ctas, void *stream) {
+  if (!pool || pool_begin < 0 || (int64_t)pool_begin + batch > pool->P || !d_hit_row ||
+      !d_miss_ids || !d_miss_row || !d_counts || out_stride < 1 || k > 2 * NT ||
+      pool->staging < k || !d_done || !d_ready || ctas == 0)
+    return ESS_ERR_ARG;
+  if (!d_logits || !d_len || !d_idx || !d_count || batch < 0 || k < 1 || idx_ld < k || ld < 1 ||
+      ld > SLICE_MAX)
+    return ESS_ERR_ARG;
+  if (batch == 0) return ESS_OK;
+  SplitArgs sp{};
+  sp.slot_of = pool->slot_of + (int64_t)pool_begin * pool->max_ids;
+  sp.max_ids = pool->max_ids;
+  sp.cap_max = pool->cap_max;
+  sp.hit_row = d_hit_row;
+  sp.miss_ids = d_miss_ids;
+  sp.miss_row = d_miss_row;
+  sp.counts = d_counts;
+  sp.out_stride = out_stride;
+  // ctas < 0: -ctas two-CTA clusters (each row on a CTA pair)
+  const int cln = ctas < 0 ? 2 : 1;
+  int nclu = ctas < 0 ? -ctas : ctas;
+  if (nclu > batch) nclu = batch;
+  const size_t smem = (size_t)(cln == 2 ? slice_cap<2>(ld) : slice_cap<1>(ld)) * sizeof(uint32_t) +
+                      (LCAP + NT) * sizeof(uint16_t);
+  const void *kern = cln == 2 ? (const void *)topk_stream_kernel<2> : (const void *)topk_stream_kernel<1>;
+  if (int rc = ess_smem_optin(kern, SLICE_MAX * sizeof(uint32_t) + (LCAP + NT) * sizeof(uint16_t))) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nclu * cln));
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cln;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (cln == 2)
+    ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, topk_stream_kernel<2>, d_logits, ld, d_len, (int)batch, (int)k, d_idx,
+                                    (int)idx_ld, d_count, sp, d_done, d_ready));
+  else
+    ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, topk_stream_kernel<1>, d_logits, ld, d_len, (int)batch, (int)k, d_idx,
+                                    (int)idx_ld, d_count, sp, d_done, d_ready));
+  return ESS_OK;
+}
+
+#ifdef ESS_STREAM_PROF
+ESS_STREAM_PROF_READER(ess_debug_stream_prof_topk)
+#endif

@@ -32,8 +32,8 @@ import torch
 from . import _lib
 from .attention import DEFAULT_SM_SCALE, SplitWorkspace, sparse_mla, sparse_mla_da
 from .cache import AccessBatch, PoolSet, pool_capacity
-from .indexer import indexer_logits, topk, topk_split
-from .transfer import HostLatentStore, gather, write_generated
+from .indexer import indexer_logits, indexer_logits_stream, topk, topk_split, topk_split_stream
+from .transfer import HostLatentStore, gather, gather_stream, write_generated
 
 ROW = 656
 
@@ -89,6 +89,12 @@ class DSADecodeLayer:
         self.min_gather_sms = 20
         self.early_gather_sms = int(os.environ.get("ESS_EARLY_GATHER_SMS", "20"))
         self.late_k1_ctas = int(os.environ.get("ESS_LATE_K1_CTAS", "0"))
+        # streamed schedule (overlap="stream"): request group of the indexer, persistent
+        # top-k and gather grid sizes
+        self.stream_group = int(os.environ.get("ESS_STREAM_GROUP", "8"))
+        self.stream_first = int(os.environ.get("ESS_STREAM_FIRST", "0"))  # first group (0: = group)
+        self.stream_topk_ctas = int(os.environ.get("ESS_STREAM_TOPK_CTAS", "16"))
+        self.stream_gather_ctas = int(os.environ.get("ESS_STREAM_GATHER_CTAS", "20"))
         self.Lmax = ((context_len + max_new_tokens + 127) // 128) * 128
         self.gen = torch.Generator(device=self.device).manual_seed(seed)
         d, g, B = self.device, self.gen, batch
@@ -252,6 +258,8 @@ class DSADecodeLayer:
             self._settle = z()
             self._counts_b = torch.empty((B, 4), dtype=torch.int32, device=self.device)
         acc = self.acc
+        if overlap == "stream":
+            return self._attend_stream(q_idx, q, new_rows, gather_ctas)
         if overlap == "none":
             self._select(q_idx, 0, B)
             gather(self.pool, self.store, acc, max_ctas=gather_ctas)
@@ -367,6 +375,87 @@ class DSADecodeLayer:
             main.wait_event(admitted)
         return self.out, self.lse
 
+    def stream_ok(self) -> bool:
+        """The streamed schedule's preconditions: early gather (every pool holds a whole
+        selection, staging rows), rows that fit one top-k CTA, and the fused DA launch."""
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        return (self.early_gather and self.Lmax <= 40 * 1024 and self.fuse_da and 2 * self.B <= sms - 8)
+
+    def _attend_stream(self, q_idx, q, new_rows, gather_ctas):
+        """The streamed step: K1, K2+K3a and K4 run CONCURRENTLY as three persistent grids
+        handing each request on through per-request counters instead of micro-batch
+        boundaries (PAPER.md:363-367's overlap taken to request granularity): the indexer
+        finishes the requests group by group (``stream_group`` requests with the whole
+        grid) and counts each request's stored logits rows; the top-k grid starts a row
+        as soon as its logits are complete and publishes its hit/miss split; the gather
+        grid fetches a request's misses as soon as that split is published.  The host
+        link thus starts ~one top-k after the first group instead of after a micro-
+        batch's indexer + top-k.  K3b, the settle, the admission and the fused DA
+        attention follow as in the DBA schedule.  The three grids are sized to be
+        co-resident (each CTA takes an SM): K1 gets the SMs the top-k and the gather
+        grids leave."""
+        if not self.stream_ok():
+            raise ValueError("the streamed schedule needs early gather, rows <= 40K tokens and the fused DA")
+        B, K, d, acc = self.B, self.K, self.device, self.acc
+        main = torch.cuda.current_stream(d)
+        if getattr(self, "_sync", None) is None:
+            self._sync = torch.zeros(3 * B, dtype=torch.int32, device=d)  # done | ready | claim
+        for name, prio in (("_side", -1), ("_sel", 0), ("_lru", 0), ("_adm", 0)):
+            if getattr(self, name, None) is None:
+                setattr(self, name, torch.cuda.Stream(d, priority=prio))
+        if getattr(self, "_landed", None) is None:
+            self._landed = torch.zeros(B, dtype=torch.int32, device=d)
+            self._ws = SplitWorkspace(B, d)
+        side, sel, lru = self._side, self._sel, self._lru
+        done, ready, claim = self._sync[:B], self._sync[B:2 * B], self._sync[2 * B:]
+        sms = torch.cuda.get_device_properties(d).multi_processor_count
+        nk2 = self.stream_topk_ctas
+        nk2 = min(B, nk2) if nk2 > 0 else -min(B, -nk2)
+        g = self.stream_gather_ctas
+        split = max(1, min(self.max_split, (sms - 8 - g) // (2 * B)))
+        if split > 1 and getattr(self, "_ws_split", None) is None:
+            self._ws_split = SplitWorkspace(B, d, splits=split)
+        self._sync.zero_()
+        start = torch.cuda.Event()
+        start.record(main)
+        k2_sms = nk2 if nk2 > 0 else -2 * nk2   # < 0: CTA-pair clusters per row
+        indexer_logits_stream(q_idx, self.w, self.k_cache, self.k_scale, self.lens, self.logits, done,
+                              self.stream_group | (self.stream_first << 16), sms - k2_sms - g)
+        sel.wait_event(start)
+        with torch.cuda.stream(sel):
+            topk_split_stream(self.logits, self.lens, K, self.idx, self.cnt, self.pool, acc, done, ready, nk2)
+            selected = torch.cuda.Event()
+            selected.record(sel)
+        side.wait_event(start)
+        with torch.cuda.stream(side):
+            gather_stream(self.pool, self.store, acc, ready, claim, self._landed, max_ctas=g)
+            fetched = torch.cuda.Event()
+            fetched.record(side)
+        lru.wait_event(selected)
+        with torch.cuda.stream(lru):  # K3b (LRU update, final slots), then the settle
+            self.pool.access(self.idx, self.cnt, out=AccessBatch(
+                counts=self._counts_b, sel_row=None, miss_ids=None, miss_row=self._settle, hit_row=None))
+            lru_ready = torch.cuda.Event()
+            lru_ready.record(lru)
+            lru.wait_event(fetched)
+            self.pool.settle(self._settle, acc.counts)
+            settled = torch.cuda.Event()
+            settled.record(lru)
+        if new_rows is not None:
+            self._adm.wait_event(lru_ready)
+            with torch.cuda.stream(self._adm):
+                self._append_device(new_rows)
+                admitted = torch.cuda.Event()
+                admitted.record(self._adm)
+        main.wait_event(selected)
+        sparse_mla_da(self.pool, q, acc, self._landed, self.sm_scale, out=self.out, lse=self.lse,
+                      split=split, workspace=self._ws_split if split > 1 else None)
+        main.wait_event(fetched)
+        main.wait_event(settled)
+        if new_rows is not None:
+            main.wait_event(admitted)
+        return self.out, self.lse
+
     # -- whole-step CUDA graph ------------------------------------------------------------
     def _append_device(self, new_rows: torch.Tensor) -> None:
         """append_token with every per-step scalar derived on the device: the new id is
@@ -382,7 +471,7 @@ class DSADecodeLayer:
         # a smaller pool keeps part of the selection in rows the admission may evict
         # (capacity only grows with history, so this holds for every later replay)
         hist_min = min(self.ctx_lens) + self.history - self.ctx
-        early = overlap in ("da", "dba") and math.floor(self.rho * hist_min) > self.K
+        early = overlap in ("da", "dba", "stream") and math.floor(self.rho * hist_min) > self.K
         self.attend(self.q_idx_in, self.q_in, gather_ctas=gather_ctas, overlap=overlap,
                     new_rows=self.rows_in if early else None, micro=self.micro)
         if not early:
@@ -394,6 +483,10 @@ class DSADecodeLayer:
         then K5 (+ the KV-split combine) and the admission."""
         if overlap == "none":
             return 6  # K1, K2, K3, K4, K5, admission
+        sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+        if overlap == "stream":  # K1, K2+K3a, K4, K3b, settle, K5 (+ combine), admission
+            split = max(1, min(self.max_split, (sms - 8 - self.stream_gather_ctas) // (2 * self.B)))
+            return 7 + (split > 1)
         micro = self.micro if overlap == "dba" else 1
         # early gather: K2 + K3a fused, + K3b, settle
         per_mb = 5 if self.early_gather else 4

@@ -164,3 +164,42 @@ def _check_topk_out(out, count, B, k, device):
     if out.stride(1) != 1 or out.shape[1] < k:
         raise ValueError("out must be int32 [B, >= k] with unit column stride")
     _lib.check_tensor(count, "count", torch.int32, (B,), device=device)
+
+
+def indexer_logits_stream(q_fp8, w, k_cache, k_scale, lens, out, done, group: int, max_ctas: int):
+    """K1 of the streamed step (ess_indexer_logits_stream): requests in groups of ``group``
+    with the whole grid, per-request completion counters ``done`` (int32 [B], zero at
+    launch) for the concurrent streamed top-k.  Shapes as ``indexer_logits``."""
+    _lib.require_cuda(k_cache)
+    B, Lmax, _ = k_cache.shape
+    _lib.check_tensor(q_fp8, "q_fp8", (torch.uint8, torch.float8_e4m3fn), (B, HEADS, DIM), device=k_cache.device)
+    _lib.check_tensor(w, "w", torch.float32, (B, HEADS), device=k_cache.device)
+    _lib.check_tensor(k_scale, "k_scale", torch.float32, (B, Lmax), device=k_cache.device)
+    _lib.check_tensor(lens, "lens", torch.int32, (B,), device=k_cache.device)
+    _lib.check_tensor(out, "out", torch.float32, (B, Lmax), device=k_cache.device)
+    _lib.check_tensor(done, "done", torch.int32, (B,), device=k_cache.device)
+    _lib.check(_lib.load().ess_indexer_logits_stream(
+        q_fp8.data_ptr(), w.data_ptr(), k_cache.data_ptr(), k_scale.data_ptr(), lens.data_ptr(), B, Lmax,
+        out.data_ptr(), max_ctas, group, done.data_ptr(), _lib.stream_handle()), "ess_indexer_logits_stream")
+    return out
+
+
+def topk_split_stream(logits, lens, k: int, out, count, pool, acc, done, ready, ctas: int, begin: int = 0):
+    """K2 + K3a of the streamed step (ess_topk_split_stream): ``ctas`` persistent CTAs take
+    the requests in order, each once ``done`` says its logits are complete; ``ready``
+    (int32 [B], zero at launch) is set per request when its split is stored."""
+    _lib.require_cuda(logits)
+    B, ld = _check_topk_args(logits, lens, k)
+    _check_topk_out(out, count, B, k, logits.device)
+    for name in ("hit_row", "miss_ids", "miss_row"):
+        t = getattr(acc, name)
+        if t.stride(1) != 1 or t.stride(0) != acc.miss_ids.stride(0) or t.shape[1] < k:
+            raise ValueError(f"acc.{name} rows must be unit-stride, share one row stride and hold k ids")
+    _lib.check_tensor(done, "done", torch.int32, (B,), device=logits.device)
+    _lib.check_tensor(ready, "ready", torch.int32, (B,), device=logits.device)
+    _lib.check(_lib.load().ess_topk_split_stream(
+        logits.data_ptr(), logits.stride(0), lens.data_ptr(), B, k, out.data_ptr(), out.stride(0),
+        count.data_ptr(), pool.handle, begin, acc.hit_row.data_ptr(), acc.miss_ids.data_ptr(),
+        acc.miss_row.data_ptr(), acc.counts.data_ptr(), acc.miss_ids.stride(0), done.data_ptr(),
+        ready.data_ptr(), ctas, _lib.stream_handle()), "ess_topk_split_stream")
+    return out, count

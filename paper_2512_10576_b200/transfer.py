@@ -173,6 +173,24 @@ def gather(pool: PoolSet, store: HostLatentStore, acc: AccessBatch, begin: int =
         "ess_gather")
 
 
+def gather_stream(pool: PoolSet, store: HostLatentStore, acc: AccessBatch, ready: torch.Tensor,
+                  claim: torch.Tensor, landed: torch.Tensor | None, begin: int = 0, max_ctas: int = 20,
+                  exclusive: bool = True, stream=None) -> None:
+    """K4 of the streamed step (ess_gather_stream): launched with the step, it fetches each
+    request's misses once ``ready`` (ess_topk_split_stream) publishes its split; ``claim``
+    (int32 [num], zero at launch) hands out chunks of each miss list to the warps."""
+    num = acc.counts.shape[0]
+    for t, name in ((ready, "ready"), (claim, "claim")):
+        if t.dtype != torch.int32 or t.numel() < num:
+            raise ValueError(f"{name} must be int32 with one entry per request")
+    flags = _lib.ESS_GATHER_EXCLUSIVE_SM if exclusive else 0
+    _lib.check(_lib.load().ess_gather_stream(
+        pool.handle, begin, num, store.pool_ptr(begin), store.rows_per_pool,
+        acc.miss_ids.data_ptr(), acc.miss_row.data_ptr(), acc.counts.data_ptr(), acc.miss_ids.stride(0),
+        ready.data_ptr(), claim.data_ptr(), _lib.ptr(landed), max_ctas, flags, _lib.stream_handle(stream)),
+        "ess_gather_stream")
+
+
 def write_generated(pool: PoolSet, store: HostLatentStore, ids: torch.Tensor, m: torch.Tensor,
                     slots: torch.Tensor, rows: torch.Tensor, begin: int = 0,
                     store_begin: int | None = None, stream=None) -> None:

@@ -51,6 +51,9 @@ wrap(decode, "topk_split", "K2+K3a topk+split")
 wrap(decode, "gather", "K4 gather (side)")
 wrap(decode, "sparse_mla_da", "K5 fused DA")
 wrap(decode, "sparse_mla", "K5 pass")
+wrap(decode, "indexer_logits_stream", "K1 stream")
+wrap(decode, "topk_split_stream", "K2+K3a stream")
+wrap(decode, "gather_stream", "K4 stream (side)")
 acc_f = decode.PoolSet.access
 
 
