@@ -135,12 +135,18 @@ int ess_pool_access(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d
  * d_req + r*req_stride, n = d_n[r]) as qtok consecutive access_steps in one launch.
  * d_sel_row is laid out like d_req (row r: the slot row of each id of set r); the
  * hit / miss / evicted id and row lists of a pool's sets are appended in set order in
- * its [out_stride >= qtok * req_stride] row; d_counts [num][4] are the sums. */
+ * its [out_stride >= qtok * req_stride] row; d_counts [num][4] are the sums.
+ * Optional attention split per set (all three or none), laid out like d_req: the rows
+ * of the set resident before the step (d_tok_hit_row) and those fetched this step by
+ * this set or an earlier one (d_tok_fresh_row), each in requested order, with
+ * d_tok_counts [num * qtok][2] = (resident, fetched). */
 int ess_pool_access_mtp(ess_pool *pool, int32_t begin, int32_t num, int32_t qtok,
                         const int32_t *d_req, const int32_t *d_n, int32_t req_stride,
                         int32_t *d_hit_ids, int32_t *d_miss_ids, int32_t *d_evicted_ids,
                         int32_t *d_sel_row, int32_t *d_hit_row, int32_t *d_miss_row,
-                        int32_t *d_counts, int32_t out_stride, int32_t flags, void *stream);
+                        int32_t *d_counts, int32_t out_stride, int32_t *d_tok_hit_row,
+                        int32_t *d_tok_fresh_row, int32_t *d_tok_counts, int32_t flags,
+                        void *stream);
 /* Early-gather split of ess_pool_access (needs staging_rows >= 2048 and n <= capacity):
  * ess_pool_split is the read-only hit/miss split — hit rows, miss ids and STAGING rows
  * (cap_max + j) for the misses, counts (hits, misses) — so the host-link gather can

@@ -33,7 +33,8 @@ SIGNATURES = {
     "ess_pool_grow": ([V, I32, I32, V, V], ctypes.c_int),
     "ess_pool_warmup": ([V, I32, I32, V, V, I32, V, V], ctypes.c_int),
     "ess_pool_access": ([V, I32, I32, V, V, I32, V, V, V, V, V, V, V, I32, I32, V], ctypes.c_int),
-    "ess_pool_access_mtp": ([V, I32, I32, I32, V, V, I32, V, V, V, V, V, V, V, I32, I32, V], ctypes.c_int),
+    "ess_pool_access_mtp": ([V, I32, I32, I32, V, V, I32, V, V, V, V, V, V, V, I32, V, V, V, I32, V],
+                            ctypes.c_int),
     "ess_pool_append": ([V, I32, I32, V, V, I32, V, V], ctypes.c_int),
     "ess_pool_split": ([V, I32, I32, V, V, I32, V, V, V, V, I32, V], ctypes.c_int),
     "ess_pool_settle": ([V, I32, I32, V, V, I32, V], ctypes.c_int),

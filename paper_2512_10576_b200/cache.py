@@ -159,12 +159,15 @@ class PoolSet:
 
     def access_mtp(self, req: torch.Tensor, n: torch.Tensor, begin: int = 0, lists: bool = False,
                    sort_evicted: bool = True, out: AccessBatch | None = None,
-                   sel_row: torch.Tensor | None = None) -> AccessBatch:
+                   sel_row: torch.Tensor | None = None, tok_split=None) -> AccessBatch:
         """MTP: ``qtok`` selection sets per pool, req [num, qtok, K] / n [num, qtok] (the
         layout of ``indexer.topk_mtp``), taken as qtok consecutive access_steps per pool in
         one launch — recency is updated by every selected set.  ``sel_row``
         [num, qtok, K] gets each set's slot rows; the hit/miss/evicted lists of a pool's
-        sets are appended in set order in its [num, qtok*K] rows; counts are the sums."""
+        sets are appended in set order in its [num, qtok*K] rows; counts are the sums.
+        ``tok_split`` = (hit_row, fresh_row [num, qtok, K], counts [num, qtok, 2]): per set,
+        the rows resident before the step and those fetched this step (attention pass 1
+        beside the gather, pass 2 after it)."""
         num, qtok, K = req.shape
         self._range(begin, num)
         if not 1 <= qtok <= _lib.MAX_QTOK:
@@ -185,12 +188,19 @@ class PoolSet:
         stride = lists_[0].stride(0) if lists_ else qtok * K
         if any(t.stride(0) != stride or t.stride(1) != 1 for t in lists_) or stride < qtok * K:
             raise ValueError("list outputs must share a row stride >= qtok * K")
+        if tok_split is not None:
+            th, tf, tc = tok_split
+            if (th.shape != (num, qtok, K) or tf.shape != (num, qtok, K) or tc.shape != (num, qtok, 2)
+                    or not (th.is_contiguous() and tf.is_contiguous() and tc.is_contiguous())):
+                raise ValueError("tok_split must be contiguous [num, qtok, K] x2 and [num, qtok, 2]")
         flags = _lib.ESS_ACCESS_SORT_EVICTED if sort_evicted else 0
         _lib.check(self._L.ess_pool_access_mtp(
             self._h, begin, num, qtok, req.data_ptr(), n.data_ptr(), K,
             _lib.ptr(out.hit_ids), _lib.ptr(out.miss_ids), _lib.ptr(out.evicted_ids),
             sel_row.data_ptr(), _lib.ptr(out.hit_row), _lib.ptr(out.miss_row),
-            out.counts.data_ptr(), stride, flags, _lib.stream_handle()), "ess_pool_access_mtp")
+            out.counts.data_ptr(), stride,
+            *((_lib.ptr(t) for t in tok_split) if tok_split is not None else (None, None, None)),
+            flags, _lib.stream_handle()), "ess_pool_access_mtp")
         out.sel_row = sel_row
         return out
 

@@ -52,6 +52,17 @@ constexpr size_t STAGE_SMEM_MAX = 180 * 1024;
 
 enum { MODE_ACCESS = 0, MODE_WARMUP = 1 };
 
+// MTP attention split (ess_pool_access_mtp): per selection set (request b, token j), the
+// rows resident before the step ("hit", attention pass 1 beside the gather) and the rows
+// fetched this step by this set or an earlier set of the request ("fresh", pass 2 after
+// the gather), each in requested order; cnt [num][qtok][2].  Marks live in a per-launch
+// shared-memory bitmap over the pool's slots.
+struct TokSplit {
+  int32_t *hit_row = nullptr;
+  int32_t *fresh_row = nullptr;
+  int32_t *cnt = nullptr;
+};
+
 struct StepSmem {
   int id[MAXR];
   int slot[MAXR];      // old slot (-1 = not resident), later the final row
@@ -337,7 +348,7 @@ __global__ void __launch_bounds__(NT, 1)
                      int32_t *miss_out, int32_t *ev_out, int32_t *sel_row_out,
                      int32_t *hit_row_out, int32_t *miss_row_out, int32_t *counts_out,
                      int out_stride, int flags,
-                     int64_t *inserted_out, int qtok, int sel_stride) {
+                     int64_t *inserted_out, int qtok, int sel_stride, TokSplit ts) {
   __shared__ StepSmem sm;
   extern __shared__ uint32_t stage_smem[];  // [cap_max] keys (STAGED)
   const int t = threadIdx.x;
@@ -351,6 +362,11 @@ __global__ void __launch_bounds__(NT, 1)
   // each a full access_step (recency updated by every selected set); the
   // hit / miss / evicted lists of the sets are appended per pool, the counts summed.
   int acc_hit = 0, acc_miss = 0, acc_ev = 0, acc_tr = 0;
+  uint32_t *fresh_bits = stage_smem + ((flags & POOL_STAGED) ? pv.cap_max : 0);  // TokSplit marks
+  if (ts.hit_row) {
+    for (int w = t; w < (pv.cap_max + 31) / 32; w += NT) fresh_bits[w] = 0u;
+    __syncthreads();
+  }
   for (int jq = 0; jq < qtok; jq++) {
   const int n = req_n[(int64_t)b * qtok + jq];
   const int32_t *reqj = req + ((int64_t)b * qtok + jq) * req_stride;
@@ -559,6 +575,7 @@ __global__ void __launch_bounds__(NT, 1)
           const uint32_t st = (MODE == MODE_ACCESS) ? clk + nhit + j : clk + i;
           key[s] = st;
           if (staged) skey[s] = st;  // the staged copy stays exact for the next MTP set
+          if (ts.hit_row) atomicOr(&fresh_bits[s >> 5], 1u << (s & 31));
           sm.slot[i] = s;
           if (MODE == MODE_ACCESS && miss_row_out) miss_row_out[out_base + acc_miss + j] = s;
         }
@@ -630,6 +647,7 @@ __global__ void __launch_bounds__(NT, 1)
           s = sm.sel[km++];
           slot_of[sm.id[i]] = s;
           slot_id[s] = sm.id[i];
+          if (ts.hit_row) atomicOr(&fresh_bits[s >> 5], 1u << (s & 31));
         }
         const uint32_t st = (MODE == MODE_ACCESS) ? clk + (i - keep0) : clk + i;
         key[s] = st;
@@ -645,6 +663,37 @@ __global__ void __launch_bounds__(NT, 1)
 
   PPROF(6);
   // ---- outputs + counters -----------------------------------------------------
+  if (MODE == MODE_ACCESS && ts.hit_row) {  // MTP attention split of this set
+    int fr[EPT], nf = 0, nh = 0;
+#pragma unroll
+    for (int e = 0; e < EPT; e++) {
+      const int i = t * EPT + e;
+      fr[e] = 0;
+      if (i < n) {
+        const int sl = sm.slot[i];
+        // staging rows (oversize transients) were fetched this step too
+        fr[e] = sl >= pv.cap_max ? 1 : (int)((fresh_bits[sl >> 5] >> (sl & 31)) & 1u);
+        nf += fr[e];
+        nh += 1 - fr[e];
+      }
+    }
+    int tot;
+    const int ex = block_exclusive_scan<NT>(nh | (nf << 16), sm.warp, &tot);
+    int ph = ex & 0xFFFF, pf = ex >> 16;
+    const int64_t rb = ((int64_t)b * qtok + jq) * sel_stride;
+#pragma unroll
+    for (int e = 0; e < EPT; e++) {
+      const int i = t * EPT + e;
+      if (i < n) {
+        if (fr[e]) ts.fresh_row[rb + pf++] = sm.slot[i];
+        else ts.hit_row[rb + ph++] = sm.slot[i];
+      }
+    }
+    if (t == 0) {
+      ts.cnt[((int64_t)b * qtok + jq) * 2 + 0] = tot & 0xFFFF;
+      ts.cnt[((int64_t)b * qtok + jq) * 2 + 1] = tot >> 16;
+    }
+  }
   if (MODE == MODE_ACCESS) {
     if (sel_row_out) {
 #pragma unroll
@@ -1486,7 +1535,7 @@ int ess_pool_warmup(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_id
   if (num == 0) return ESS_OK;
   pool_step_kernel<MODE_WARMUP><<<num, NT, 0, (cudaStream_t)stream>>>(
       view(p), begin, d_ids, d_n, stride, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-      nullptr, 0, 0, d_inserted, 1, 0);
+      nullptr, 0, 0, d_inserted, 1, 0, TokSplit{});
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }
@@ -1520,7 +1569,7 @@ static int pool_access_launch(ess_pool *p, int32_t begin, int32_t num, int32_t q
                               int32_t *d_hit_ids, int32_t *d_miss_ids, int32_t *d_evicted_ids,
                               int32_t *d_sel_row, int32_t sel_stride, int32_t *d_hit_row,
                               int32_t *d_miss_row, int32_t *d_counts, int32_t out_stride,
-                              int32_t flags, void *stream) {
+                              int32_t flags, void *stream, TokSplit ts = TokSplit{}) {
   if (!range_ok(p, begin, num) || !d_req || !d_n || req_stride < 0) return ESS_ERR_ARG;
   if ((d_hit_ids || d_miss_ids || d_evicted_ids || d_sel_row || d_hit_row || d_miss_row) &&
       out_stride < 1)
@@ -1528,15 +1577,17 @@ static int pool_access_launch(ess_pool *p, int32_t begin, int32_t num, int32_t q
   if (num == 0) return ESS_OK;
   if (flags & POOL_STAGED) return ESS_ERR_ARG;
   const size_t stage = (size_t)p->cap_max * 4;
-  size_t smem = 0;
-  if (stage <= STAGE_SMEM_MAX) {
-    if (int rc = ess_smem_optin((const void *)pool_step_kernel<MODE_ACCESS>, stage)) return rc;
-    smem = stage;
+  const size_t bits = ts.hit_row ? (size_t)(p->cap_max + 31) / 32 * 4 : 0;
+  size_t smem = bits;
+  if (stage + bits <= STAGE_SMEM_MAX) {
+    smem = stage + bits;
     flags |= POOL_STAGED;
   }
+  if (smem)
+    if (int rc = ess_smem_optin((const void *)pool_step_kernel<MODE_ACCESS>, smem)) return rc;
   pool_step_kernel<MODE_ACCESS><<<num, NT, smem, (cudaStream_t)stream>>>(
       view(p), begin, d_req, d_n, req_stride, d_hit_ids, d_miss_ids, d_evicted_ids, d_sel_row,
-      d_hit_row, d_miss_row, d_counts, out_stride, flags, nullptr, qtok, sel_stride);
+      d_hit_row, d_miss_row, d_counts, out_stride, flags, nullptr, qtok, sel_stride, ts);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }
@@ -1555,14 +1606,21 @@ int ess_pool_access_mtp(ess_pool *p, int32_t begin, int32_t num, int32_t qtok, c
                         const int32_t *d_n, int32_t req_stride, int32_t *d_hit_ids,
                         int32_t *d_miss_ids, int32_t *d_evicted_ids, int32_t *d_sel_row,
                         int32_t *d_hit_row, int32_t *d_miss_row, int32_t *d_counts,
-                        int32_t out_stride, int32_t flags, void *stream) {
+                        int32_t out_stride, int32_t *d_tok_hit_row, int32_t *d_tok_fresh_row,
+                        int32_t *d_tok_counts, int32_t flags, void *stream) {
   if (qtok < 1 || qtok > ESS_INDEXER_MAX_QTOK) return ESS_ERR_ARG;
+  if ((d_tok_hit_row || d_tok_fresh_row || d_tok_counts) && !(d_tok_hit_row && d_tok_fresh_row && d_tok_counts))
+    return ESS_ERR_ARG;
+  TokSplit ts;
+  ts.hit_row = d_tok_hit_row;
+  ts.fresh_row = d_tok_fresh_row;
+  ts.cnt = d_tok_counts;
   if ((d_hit_ids || d_miss_ids || d_evicted_ids || d_hit_row || d_miss_row) &&
       (int64_t)out_stride < (int64_t)qtok * req_stride)
     return ESS_ERR_ARG;  // the appended lists of qtok sets must fit a pool's row
   return pool_access_launch(p, begin, num, qtok, d_req, d_n, req_stride, d_hit_ids, d_miss_ids,
                             d_evicted_ids, d_sel_row, req_stride, d_hit_row, d_miss_row, d_counts,
-                            out_stride, flags, stream);
+                            out_stride, flags, stream, ts);
 }
 
 #ifdef ESS_POOL_PROF

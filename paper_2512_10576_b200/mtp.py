@@ -37,7 +37,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .attention import sparse_mla
+from .attention import SplitWorkspace, sparse_mla
 from .cache import AccessBatch
 from .decode import ROW, DSADecodeLayer, _e4m3, random_latent_rows
 from .indexer import indexer_logits, indexer_logits_mtp, topk, topk_mtp
@@ -134,14 +134,20 @@ class MTPDecodeLayer(DSADecodeLayer):
                micro: int = 2):
         """K1..K5 for the qtok query tokens of every request.  ``overlap="dba"``: the
         requests in ``micro`` micro-batches; micro-batch i's gather (side stream) overlaps
-        micro-batch i+1's indexer, whose grid leaves the gather its SMs (PAPER.md:363-367);
-        attention over all B * qtok query rows once the rows have landed.  ``"none"``:
-        K1 -> K2 -> K3 -> K4 -> K5 in order."""
+        micro-batch i+1's indexer, whose grid leaves the gather its SMs.
+        Attention is the paper's DA split per (request, token) row:
+        pass 1 over the rows its selection found resident while the gathers run, pass 2
+        over the rows fetched this step (by its own set or an earlier token's) once they
+        have landed, merged through the workspace.  ``"da"``: one micro-batch.
+        ``"none"``: K1 -> K2 -> K3 -> K4 -> K5 in order, one attention pass."""
         B, Q, K = self.B, self.qtok, self.K
         if self.acc is None:
             z = lambda: torch.empty((B, Q * K), dtype=torch.int32, device=self.device)  # noqa: E731
             self.acc = AccessBatch(counts=torch.empty((B, 4), dtype=torch.int32, device=self.device),
                                    sel_row=None, miss_ids=z(), miss_row=z(), hit_row=z())
+            t = lambda: torch.empty((B, Q, K), dtype=torch.int32, device=self.device)  # noqa: E731
+            self.tok_split = (t(), t(), torch.empty((B, Q, 2), dtype=torch.int32, device=self.device))
+            self._ws = SplitWorkspace(B * Q, self.device)
         if overlap not in ("none", "da", "dba"):
             raise ValueError(f"unknown overlap schedule {overlap!r}")
         main = torch.cuda.current_stream(self.device)
@@ -164,7 +170,9 @@ class MTPDecodeLayer(DSADecodeLayer):
             with torch.cuda.stream(sel):
                 topk_mtp(self.logits[a:b], self.lens[a:b], K, out=self.idx[a:b], count=self.cnt[a:b])
                 self.pool.access_mtp(self.idx[a:b], self.cnt[a:b], begin=a, out=self._view(a, b),
-                                     sel_row=self.sel_row[a:b])
+                                     sel_row=self.sel_row[a:b],
+                                     tok_split=None if overlap == "none" else
+                                     tuple(x[a:b] for x in self.tok_split))
                 ready = torch.cuda.Event()
                 ready.record(sel)
             side.wait_event(ready)
@@ -174,9 +182,20 @@ class MTPDecodeLayer(DSADecodeLayer):
             prev = b - a   # one SM per request for its qtok top-k rows (in waves) and K3
         done = torch.cuda.Event()
         done.record(side)
+        qv, ov, lv = q.view(B * Q, 128, 576), self.out.view(B * Q, 128, 512), self.lse.view(B * Q, 128)
+        if overlap == "none":
+            main.wait_event(done)
+            sparse_mla(self.pool, qv, self.sel_row.view(B * Q, K), self.cnt.view(B * Q), self.sm_scale,
+                       out=ov, lse=lv, qtok=Q)
+            return self.out, self.lse
+        th, tf, tc = self.tok_split
+        tc = tc.view(B * Q, 2)
+        main.wait_event(ready)  # every micro-batch's split lists
+        sparse_mla(self.pool, qv, th.view(B * Q, K), tc[:, 0], self.sm_scale, workspace=self._ws,
+                   mode="partial", qtok=Q)
         main.wait_event(done)
-        sparse_mla(self.pool, q.view(B * Q, 128, 576), self.sel_row.view(B * Q, K), self.cnt.view(B * Q),
-                   self.sm_scale, out=self.out.view(B * Q, 128, 512), lse=self.lse.view(B * Q, 128), qtok=Q)
+        sparse_mla(self.pool, qv, tf.view(B * Q, K), tc[:, 1], self.sm_scale, out=ov, lse=lv,
+                   workspace=self._ws, mode="resume", qtok=Q)
         return self.out, self.lse
 
     def step_counts(self) -> torch.Tensor:
@@ -223,9 +242,9 @@ class MTPDecodeLayer(DSADecodeLayer):
         self._admit(self.rows_in, self.accept_in)
 
     def launches_per_step(self, overlap: str) -> int:
-        """K1, K2, K3, K4 per micro-batch, then K5 and the admission."""
+        """K1, K2, K3, K4 per micro-batch, then K5 (two passes unless "none") and the admission."""
         micro = len(self.micro_batches(self.micro if overlap == "dba" else 1))
-        return 4 * micro + 2
+        return 4 * micro + (1 if overlap == "none" else 2) + 1
 
     def capture(self, overlap: str = "dba", gather_ctas: int = 32, accepted=None):
         """One eager step with ``accepted`` (default: qtok for every request), then the

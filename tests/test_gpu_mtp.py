@@ -73,8 +73,12 @@ def test_access_mtp_is_sequential_access_steps():
             for j in range(Q):
                 req[p, j, :len(sets[p][j])] = torch.from_numpy(sets[p][j].astype(np.int32))
                 n[p, j] = len(sets[p][j])
-        acc = ps.access_mtp(req.cuda(), n.cuda(), lists=True)
+        th = torch.full((P, Q, K), -7, dtype=torch.int32, device="cuda")
+        tf = torch.full((P, Q, K), -7, dtype=torch.int32, device="cuda")
+        tc = torch.empty((P, Q, 2), dtype=torch.int32, device="cuda")
+        acc = ps.access_mtp(req.cuda(), n.cuda(), lists=True, tok_split=(th, tf, tc))
         torch.cuda.synchronize()
+        th, tf, tc = th.cpu().numpy(), tf.cpu().numpy(), tc.cpu().numpy()
         counts = acc.counts.cpu().numpy()
         miss = acc.miss_ids.cpu().numpy()
         hit = acc.hit_ids.cpu().numpy()
@@ -82,8 +86,17 @@ def test_access_mtp_is_sequential_access_steps():
         sel = acc.sel_row.cpu().numpy()
         for p in range(P):
             hs, ms, es = [], [], []
+            fetched = set()
             for j in range(Q):
                 r = orc[p].access_step(sets[p][j].tolist())
+                # attention split of set j: ids resident before the step vs fetched by
+                # this or an earlier set (in requested order); rows checked below
+                fetched |= set(r.miss_ids)
+                fr = [x in fetched for x in sets[p][j].tolist()]
+                assert tc[p, j].tolist() == [len(fr) - sum(fr), sum(fr)], (step, p, j)
+                rows = ps.lookup(p, torch.from_numpy(sets[p][j].astype(np.int32)).cuda()).cpu().numpy()
+                np.testing.assert_array_equal(th[p, j, :len(fr) - sum(fr)], rows[~np.array(fr)])
+                np.testing.assert_array_equal(tf[p, j, :sum(fr)], rows[np.array(fr)])
                 hs += list(r.hit_ids)
                 ms += list(r.miss_ids)
                 es += list(r.evicted_ids)
@@ -143,7 +156,7 @@ def _mtp_chain(layer, orc, hist, accepted, q=None, q_idx=None, counts=None, attn
         orc[b].append_generated(new)
 
 
-@pytest.mark.parametrize("mtp,overlap", [(2, "dba"), (2, "none"), (1, "dba"), (3, "dba")])
+@pytest.mark.parametrize("mtp,overlap", [(2, "dba"), (2, "none"), (2, "da"), (1, "dba"), (3, "dba")])
 def test_mtp_layer_matches_oracle_chain(mtp, overlap):
     from paper_2512_10576_b200.cache import pool_capacity
     from paper_2512_10576_b200.mtp import MTPDecodeLayer, draw_accepted
