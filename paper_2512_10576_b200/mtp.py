@@ -32,6 +32,7 @@ C1-style oversize regime (cap < K) is served by the single-token layer.
 from __future__ import annotations
 
 import math
+from types import SimpleNamespace
 
 import numpy as np
 import torch
@@ -154,7 +155,13 @@ class MTPDecodeLayer(DSADecodeLayer):
         if getattr(self, "_side", None) is None:
             self._side = torch.cuda.Stream(self.device, priority=-1)
             self._sel = torch.cuda.Stream(self.device)
-        side, sel = self._side, self._sel
+            self._attn = torch.cuda.Stream(self.device)
+        side, sel, attn = self._side, self._sel, self._attn
+        split = overlap != "none"
+        qv, ov, lv = q.view(B * Q, 128, 576), self.out.view(B * Q, 128, 512), self.lse.view(B * Q, 128)
+        if split:
+            th, tf, tc = self.tok_split
+            th, tf, tc = th.view(B * Q, K), tf.view(B * Q, K), tc.view(B * Q, 2)
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         ranges = self.micro_batches(micro if overlap == "dba" else 1)
         prev = 0
@@ -178,24 +185,37 @@ class MTPDecodeLayer(DSADecodeLayer):
             side.wait_event(ready)
             with torch.cuda.stream(side):
                 g = gather_ctas if i == len(ranges) - 1 else max(gather_ctas, self.early_gather_sms)
-                gather(self.pool, self.store, self._view(a, b), begin=a, max_ctas=g)
+                # exclusive SMs: the host-link loads must not share an SM's miss tracking
+                # with the indexer or attention CTAs
+                gather(self.pool, self.store, self._view(a, b), begin=a, max_ctas=g, exclusive=True)
+                fetched = torch.cuda.Event()
+                fetched.record(side)
+            if split:
+                # this micro-batch's attention on its own stream, while later micro-batches
+                # select and gather: pass 1 over its resident rows right after its cache
+                # manager, pass 2 over its fetched rows once its gather has landed them
+                r0, r1 = a * Q, b * Q
+                ws = SimpleNamespace(o=self._ws.o[r0:r1], ml=self._ws.ml[r0:r1], splits=1)
+                attn.wait_event(ready)
+                with torch.cuda.stream(attn):
+                    sparse_mla(self.pool, qv[r0:r1], th[r0:r1], tc[r0:r1, 0], self.sm_scale, pool_begin=a,
+                               workspace=ws, mode="partial", qtok=Q)
+                attn.wait_event(fetched)
+                with torch.cuda.stream(attn):
+                    sparse_mla(self.pool, qv[r0:r1], tf[r0:r1], tc[r0:r1, 1], self.sm_scale, pool_begin=a,
+                               out=ov[r0:r1], lse=lv[r0:r1], workspace=ws, mode="resume", qtok=Q)
             prev = b - a   # one SM per request for its qtok top-k rows (in waves) and K3
         done = torch.cuda.Event()
         done.record(side)
-        qv, ov, lv = q.view(B * Q, 128, 576), self.out.view(B * Q, 128, 512), self.lse.view(B * Q, 128)
-        if overlap == "none":
+        if not split:
             main.wait_event(done)
             sparse_mla(self.pool, qv, self.sel_row.view(B * Q, K), self.cnt.view(B * Q), self.sm_scale,
                        out=ov, lse=lv, qtok=Q)
             return self.out, self.lse
-        th, tf, tc = self.tok_split
-        tc = tc.view(B * Q, 2)
-        main.wait_event(ready)  # every micro-batch's split lists
-        sparse_mla(self.pool, qv, th.view(B * Q, K), tc[:, 0], self.sm_scale, workspace=self._ws,
-                   mode="partial", qtok=Q)
+        attended = torch.cuda.Event()
+        attended.record(attn)
+        main.wait_event(attended)
         main.wait_event(done)
-        sparse_mla(self.pool, qv, tf.view(B * Q, K), tc[:, 1], self.sm_scale, out=ov, lse=lv,
-                   workspace=self._ws, mode="resume", qtok=Q)
         return self.out, self.lse
 
     def step_counts(self) -> torch.Tensor:
@@ -242,9 +262,10 @@ class MTPDecodeLayer(DSADecodeLayer):
         self._admit(self.rows_in, self.accept_in)
 
     def launches_per_step(self, overlap: str) -> int:
-        """K1, K2, K3, K4 per micro-batch, then K5 (two passes unless "none") and the admission."""
+        """K1, K2, K3, K4 per micro-batch, K5 (two passes per micro-batch unless "none"), and
+        the admission."""
         micro = len(self.micro_batches(self.micro if overlap == "dba" else 1))
-        return 4 * micro + (1 if overlap == "none" else 2) + 1
+        return 4 * micro + (1 if overlap == "none" else 2 * micro) + 1
 
     def capture(self, overlap: str = "dba", gather_ctas: int = 32, accepted=None):
         """One eager step with ``accepted`` (default: qtok for every request), then the
