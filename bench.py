@@ -861,29 +861,38 @@ def run_ceiling(args, cfg, dev):
     lens = request_lengths(cfg, B, seed=int(os.environ.get("RANK", "0")))
     L = lens if not isinstance(cfg["context_len"], int) else cfg["context_len"]
     total = args.warmup + args.steps
-    layer = DSADecodeLayer(B, L, 1.0, TOPK, max_new_tokens=total + 8, device=dev, seed=99,
+    layer = DSADecodeLayer(B, L, 1.0, TOPK, max_new_tokens=2 * total + 8, device=dev, seed=99,
                            drift=args.drift)
     layer.gather_ctas = args.gather_ctas
     layer.preload_full_history()
     inputs = [layer.next_queries() for _ in range(total)]
     new_rows = [random_latent_rows(B, dev, layer.gen).view(B, 1, 656) for _ in range(total)]
-    layer.capture("none", args.gather_ctas)  # all-HBM: its fastest schedule, nothing to gather
-    for t in range(1, args.warmup):
-        layer.step(inputs[t][0], inputs[t][1], new_rows[t])
-    torch.cuda.synchronize()
-    hits0, misses0 = layer.access_totals()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for t in range(args.warmup, total):
-        layer.step(inputs[t][0], inputs[t][1], new_rows[t])
-    e1.record()
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / args.steps
-    c = [x - y for x, y in zip(layer.access_totals(), (hits0, misses0))]
+    # all-HBM: nothing to gather, so the sequential step is one candidate; the streamed
+    # step (K1 || K2 as concurrent grids) is the other when its preconditions hold — the
+    # ceiling is the faster of the two (strict)
+    schedules = ["none"] + (["stream"] if layer.stream_ok() else [])
+    best = None
+    for sched in schedules:
+        layer.capture(sched, args.gather_ctas)
+        for t in range(1, args.warmup):
+            layer.step(inputs[t][0], inputs[t][1], new_rows[t])
+        torch.cuda.synchronize()
+        hits0, misses0 = layer.access_totals()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for t in range(args.warmup, total):
+            layer.step(inputs[t][0], inputs[t][1], new_rows[t])
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        c = [x - y for x, y in zip(layer.access_totals(), (hits0, misses0))]
+        if best is None or ms < best["ms_per_step"]:
+            best = {"value": B / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms,
+                    "hit_rate": c[0] / max(1, c[0] + c[1]), "schedule": sched}
+        best.setdefault("schedules_us", {})[sched] = ms * 1e3
     layer.pool.check("ceiling")
     layer.close()
-    return {"value": B / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms,
-            "hit_rate": c[0] / max(1, c[0] + c[1])}
+    return best
 
 
 def main():

@@ -381,30 +381,40 @@ __global__ void __launch_bounds__(NTHREADS, 1)
           }
         } else {
           // one MMA tile per unit: token jq's 64 heads are columns [jq*64, jq*64+64);
-          // logits row (b, jq) of [B][QT][k_ld]
+          // logits row (b, jq) of [B][QT][k_ld].  The 2*QT 32-column chunks are loaded
+          // one ahead (two register buffers): chunk c+1's tcgen05.ld is in flight while
+          // chunk c is folded, so the TMEM load latency hides behind the FMAs.
           const float4 *wq = reinterpret_cast<const float4 *>(c.wq[g]);
           const int64_t tok = (int64_t)cur.t * UNIT_M + row;
-#pragma unroll 1
-          for (int jq = 0; jq < QT; jq++) {
-            uint32_t r[64];
-            tmem_ld_32x32b_x64(tmem + ((uint32_t)(quarter * 32) << 16) + a * ACC_COLS + jq * HEADS, r);
-            tmem_ld_wait();
-            if (jq == QT - 1) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&c.tempty[a]);
-            }
-            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+          const uint32_t tbase = tmem + ((uint32_t)(quarter * 32) << 16) + a * ACC_COLS;
+          constexpr int NCH = 2 * QT;
+          uint32_t rbuf[2][32];
+          tmem_ld_32x32b_x32(tbase, rbuf[0]);
+          tmem_ld_wait();
+          float acc4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-            for (int h = 0; h < HEADS; h += 4) {
-              const float4 wv = wq[jq * (HEADS / 4) + h / 4];
-              a0 = fmaf(wv.x, fmaxf(__uint_as_float(r[h + 0]), 0.f), a0);
-              a1 = fmaf(wv.y, fmaxf(__uint_as_float(r[h + 1]), 0.f), a1);
-              a2 = fmaf(wv.z, fmaxf(__uint_as_float(r[h + 2]), 0.f), a2);
-              a3 = fmaf(wv.w, fmaxf(__uint_as_float(r[h + 3]), 0.f), a3);
+          for (int ch = 0; ch < NCH; ch++) {
+            if (ch + 1 < NCH) tmem_ld_32x32b_x32(tbase + (ch + 1) * 32, rbuf[(ch + 1) & 1]);
+            const uint32_t(&r)[32] = rbuf[ch & 1];
+            const int jq = ch >> 1, h0 = (ch & 1) * 32;
+#pragma unroll
+            for (int h = 0; h < 32; h += 4) {
+              const float4 wv = wq[jq * (HEADS / 4) + (h0 + h) / 4];
+              acc4[0] = fmaf(wv.x, fmaxf(__uint_as_float(r[h + 0]), 0.f), acc4[0]);
+              acc4[1] = fmaf(wv.y, fmaxf(__uint_as_float(r[h + 1]), 0.f), acc4[1]);
+              acc4[2] = fmaf(wv.z, fmaxf(__uint_as_float(r[h + 2]), 0.f), acc4[2]);
+              acc4[3] = fmaf(wv.w, fmaxf(__uint_as_float(r[h + 3]), 0.f), acc4[3]);
             }
-            if (valid[0]) logits[((int64_t)b * QT + jq) * k_ld + tok] = ((a0 + a1) + (a2 + a3)) * ks[0];
+            if (ch & 1) {  // token jq complete
+              if (valid[0])
+                logits[((int64_t)b * QT + jq) * k_ld + tok] = ((acc4[0] + acc4[1]) + (acc4[2] + acc4[3])) * ks[0];
+              acc4[0] = acc4[1] = acc4[2] = acc4[3] = 0.f;
+            }
+            tmem_ld_wait();
           }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&c.tempty[a]);
         }
         if (done) {  // streamed step: count this warp's stored rows of request b
 #pragma unroll
