@@ -1065,6 +1065,7 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
         asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(landed + cur_pool), "r"(tally)
                      : "memory");
     }
+    if (lane == 0 && tally > 0) SPROF_MAX(begin + cur_pool, 2);
     tally = 0;
   };
   for (int g0 = gbeg; g0 < gend; g0 += GROWS) {

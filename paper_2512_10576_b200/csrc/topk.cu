@@ -177,6 +177,7 @@ struct SplitArgs {
   int32_t *hit_row, *miss_ids, *miss_row, *counts;
   int32_t out_stride;
   int32_t len_div = 1;  // MTP: rows b*len_div .. b*len_div+len_div-1 share len[b]
+  int32_t prof_base = 0;  // ESS_STREAM_PROF: pool index of row 0
 };
 
 __device__ __forceinline__ void split_tail(int b, const int32_t *o, int n, const SplitArgs &sp,
@@ -549,6 +550,7 @@ __device__ __forceinline__ void topk_row(const int b, const float *__restrict__ 
     } else {
       split_tail(b, o, k, sp, wbuf);
     }
+    if (threadIdx.x == 0 && rank == 0) SPROF(sp.prof_base + b, 1);
   }
   KPROF(10);
 }
@@ -696,6 +698,7 @@ extern "C" int ess_topk_split(const float *d_logits, int64_t ld, const int32_t *
   sp.miss_row = d_miss_row;
   sp.counts = d_counts;
   sp.out_stride = out_stride;
+  sp.prof_base = pool_begin;
   // cluster rows: rank 0 of each cluster runs the split after a cluster barrier
   cudaStream_t st = (cudaStream_t)stream;
   int rc;

@@ -23,7 +23,8 @@ for fn in (L.ess_debug_stream_prof_topk, L.ess_debug_stream_prof_gather, L.ess_d
 buf = (ctypes.c_ulonglong * (1024 * 4))()
 buf2 = (ctypes.c_ulonglong * (1024 * 4))()
 buf3 = (ctypes.c_ulonglong * (1024 * 4))()
-layer.capture("stream", 32)
+OV = os.environ.get("OVERLAP", "stream")
+layer.capture(OV, 32)
 for t in range(6):
     q_idx, q = layer.next_queries()
     rows = random_latent_rows(B, "cuda", layer.gen).view(B, 1, 656)
@@ -55,3 +56,9 @@ for t in range(6):
         for b in list(range(0, B, 8)) + [B - 1]:
             print(f"  req {b:2d}: logits {(int(k1[b, 3]) - t0) / 1e3:6.1f}  topk {rel[b, 0]:6.1f}  ready {rel[b, 1]:6.1f}  landed {rel[b, 2]:6.1f}  (misses {m[b]})")
         print(f"  last landed {rel[:, 2].max():.1f}; ready span {rel[:, 1].min():.1f}..{rel[:, 1].max():.1f}")
+        order = np.argsort(rel[:, 2])
+        land = rel[order, 2]
+        cum = np.cumsum(m[order]) * 704 / 1e3  # KB landed
+        for f in (0.1, 0.25, 0.5, 0.75, 0.9, 1.0):
+            i = min(len(land) - 1, int(f * len(land)) - (1 if f == 1.0 else 0))
+            print(f"    {f:4.2f} of requests landed by {land[i]:6.1f} us ({cum[i] / 1e3:.2f} MB)")
