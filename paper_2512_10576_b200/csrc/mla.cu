@@ -477,23 +477,26 @@ __global__ void __launch_bounds__(NTHREADS, 1)
         const bool pos = l > 0.f;
         const float inv = 1.f / l;
         const float c0 = pos ? a0 * inv : (l == l ? 0.f : l), c1 = pos ? a1 * inv : c0;
-        // the KV ring is idle once o_done fired: stage this head's workspace half
-        // (1 KB) there as [16-B unit][head], all 64 copies in flight at once
-        const uint4 *wst = reinterpret_cast<const uint4 *>(skv);
-        if (resume) {
-          const uint32_t st = smem_u32(skv);
-#pragma unroll 8
-          for (int k = 0; k < V_HALF / 4; k++) cp_async16(st + (k * HEADS + h) * 16, wso + 4 * k, 16u);
-          cp_async_commit();
-          cp_async_wait<0>();
-        }
+        // pass 1's unnormalised state of this head (1 KB) is staged through the q
+        // tile's shared memory (free once o_done fired: every S MMA has completed; never
+        // touched by the row loaders) in two 512-B halves, [16-B unit][head], each half's
+        // 32 copies in flight at once.  A thread stages and reads only its own head.
+        const uint4 *wst = reinterpret_cast<const uint4 *>(sq);
 #pragma unroll 1
         for (int cc = 0; cc < V_HALF / 32; cc++) {
+          if (resume && (cc & 3) == 0) {
+            const uint32_t st = smem_u32(sq);
+            const int u0 = (cc >> 2) * 32;
+#pragma unroll 8
+            for (int k = 0; k < 32; k++) cp_async16(st + (k * HEADS + h) * 16, wso + 4 * (u0 + k), 16u);
+            cp_async_commit();
+            cp_async_wait<0>();
+          }
           float4 w[8];
 #pragma unroll
           for (int j = 0; j < 8; j++) {
             if (resume) {
-              const uint4 u = wst[(cc * 8 + j) * HEADS + h];
+              const uint4 u = wst[((cc & 3) * 8 + j) * HEADS + h];
               w[j] = make_float4(__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z),
                                  __uint_as_float(u.w));
             } else {
