@@ -569,9 +569,17 @@ def measure(args, cfg, dev, rank, world, agg_dev, drift, full, peaks, peak_kind,
         torch.cuda.synchronize()
         e2e_ms = e0.elapsed_time(e1) / K
         e2e_tok, e2e_t = aggregate(B * K, e2e_ms * K / 1e3, device=agg_dev)
+        h2d = h_in[0][0].numel() + h_in[0][1].numel() * 2
         rec["e2e"] = {"value": e2e_tok / e2e_t, "unit": "tokens/s",
-                      "h2d_bytes_per_step": h_in[0][0].numel() + h_in[0][1].numel() * 2,
+                      "h2d_bytes_per_step": h2d,
                       "d2h_bytes_per_step": h_out[0].numel() * 2}
+        # the H2D link carries the queries (DMA) and the misses (SM reads, 704 B each):
+        # its achieved rate vs the measured pinned-DMA peak, and the e2e bound it sets
+        if link_peak:
+            link_bytes = h2d + rec["misses_per_request_step"] * B * LINK_ROW_BYTES
+            rec["e2e"]["h2d_link_gbs"] = link_bytes / (e2e_ms * 1e-3) / 1e9
+            rec["e2e"]["h2d_link_frac_of_peak"] = rec["e2e"]["h2d_link_gbs"] / link_peak
+            rec["e2e"]["link_bound_tokens_per_s"] = B / (link_bytes / (link_peak * 1e9))
     layer.close()
     return rec
 
