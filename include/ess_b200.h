@@ -163,7 +163,8 @@ int ess_pool_settle(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d
 int ess_pool_append(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d_ids,
                     const int32_t *d_m, int32_t stride, int32_t *d_slot_out, void *stream);
 /* the decode step's tail in one launch (cache.py:191-195, :137-138, :122-134): per pool,
- * with h = d_hist[i] (history length) and m = d_m ? d_m[i] : 1 generated tokens:
+ * with h = d_hist[i] (history length) and m = d_m ? d_m[i] : 1 generated tokens
+ * (m <= src_stride, else ESS_ERR_ARG is latched):
  * grow capacity to max(1, floor(rho * (h + m))), admit ids h..h+m-1 at top recency
  * (LRU evictions counted), write each 656-B source row (d_src_rows [num][src_stride])
  * to the host store (D2H) and, dequantised, to its slot; d_hist[i] += m.              */

@@ -1340,7 +1340,8 @@ __global__ void __launch_bounds__(NTA) pool_admit_kernel(PoolView pv, int begin,
   const int64_t want = (int64_t)floor(rho * (double)(h + M));
   const int newcap = (int)(want < 1 ? 1 : want);
   int code = 0;
-  if (M < 0 || M > 64 || (int64_t)h + M > pv.max_ids) code = ESS_ERR_ARG;
+  // M rows per pool are read from the source: never more than its row stride holds
+  if (M < 0 || M > 64 || M > src_stride || (int64_t)h + M > pv.max_ids) code = ESS_ERR_ARG;
   else if (newcap < meta->cap) code = ESS_ERR_SHRINK;
   else if (newcap > pv.cap_max) code = ESS_ERR_CAPACITY;
   else if ((int64_t)h <= meta->watermark) code = ESS_ERR_DUPLICATE;

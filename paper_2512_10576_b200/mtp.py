@@ -297,6 +297,13 @@ class MTPDecodeLayer(DSADecodeLayer):
         or pinned host): verified tokens per request, 1..qtok; ``max_accepted`` (its max,
         if the caller knows it without a sync) keeps the host's room check exact."""
         m = self.qtok if max_accepted is None else int(max_accepted)
+        if not 1 <= m <= self.qtok:
+            raise ValueError(f"max_accepted must be in [1, {self.qtok}]")
+        if isinstance(accepted, torch.Tensor) and not accepted.is_cuda:
+            if accepted.shape != (self.B,) or int(accepted.min()) < 1 or int(accepted.max()) > m:
+                raise ValueError(f"accepted must hold one count in [1, {m}] per request")
+        # device-resident counts are checked by the admission kernel (m > qtok latches
+        # ESS_ERR_ARG; read by pool.check())
         self._check_room(m)
         self.q_idx_in.copy_(q_idx, non_blocking=True)
         self.q_in.copy_(q, non_blocking=True)

@@ -213,3 +213,23 @@ def test_mtp_graph_step_matches_oracle_chain():
         assert out[b, :int(cnt[b])].tolist() == orc[b].lru_order()
     assert layer.lens.tolist() == hist
     layer.close()
+
+
+def test_mtp_step_rejects_accepted_counts_beyond_the_verified_tokens():
+    """A request cannot accept more tokens than the step verified (qtok): host counts are
+    refused before the launch, device counts latch ESS_ERR_ARG in the admission kernel
+    (it would otherwise read the next request's rows)."""
+    from paper_2512_10576_b200.decode import random_latent_rows
+    from paper_2512_10576_b200.mtp import MTPDecodeLayer
+    layer = MTPDecodeLayer(2, 16384, 0.5, 2048, mtp=2, max_new_tokens=6, seed=3, drift=0.97)
+    layer.prefill_warmup(windows=2)
+    layer.capture("dba", accepted=[1, 2])
+    layer.pool.check("capture")
+    q_idx, q = layer.next_queries()
+    rows = random_latent_rows(6, "cuda", layer.gen).view(2, 3, 656)
+    with pytest.raises(ValueError):
+        layer.step(q_idx, q, rows, torch.tensor([4, 1], dtype=torch.int32))
+    layer.step(q_idx, q, rows, torch.tensor([4, 1], dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError):
+        layer.pool.check("device accepted > qtok")
+    layer.close()
