@@ -509,7 +509,8 @@ int launch_indexer(const void *d_q, const float *d_w, const void *d_k, const flo
   if (int rc = ess_smem_optin((const void *)indexer_kernel<QT>, C::SMEM_BYTES)) return rc;
   const int ctas = max_ctas > 0 && max_ctas < ess_sm_count() ? max_ctas : ess_sm_count();
   indexer_kernel<QT><<<ctas, NTHREADS, C::SMEM_BYTES, (cudaStream_t)stream>>>(
-      tk, tq, d_w, d_kscale, d_len, batch, k_ld, d_logits, group > 0 ? group : batch, d_done);
+      tk, tq, d_w, d_kscale, d_len, batch, k_ld, d_logits,
+      (group & 0xFFFF) ? group : ((group & ~0xFFFF) | (batch & 0xFFFF)), d_done);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
 }
@@ -552,6 +553,7 @@ extern "C" int ess_indexer_logits_stream(const void *d_q, const float *d_w, cons
                                          const float *d_kscale, const int32_t *d_len, int32_t batch,
                                          int64_t k_ld, float *d_logits, int32_t max_ctas, int32_t group,
                                          int32_t *d_done, void *stream) {
+  // group: requests per group (low 16 bits; 0 = one group), first group (high 16 bits)
   if (max_ctas < 0 || group < 0 || !d_done) return ESS_ERR_ARG;
   if (!d_q || !d_w || !d_k || !d_kscale || !d_len || !d_logits || batch < 0 ||
       batch > MAX_BATCH || k_ld < TILE_M || (k_ld % TILE_M) != 0 ||
