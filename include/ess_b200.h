@@ -79,6 +79,11 @@ typedef struct ess_pool ess_pool;
 /* ---- library ---------------------------------------------------------------- */
 const char *ess_version(void);
 const char *ess_status_string(int status);
+/* load every kernel of the library on the current device now (first call per device;
+ * lazy module loading would load a kernel at its first launch, which waits for the
+ * device — a deadlock when a running kernel spins on work a not-yet-loaded kernel
+ * produces, as in the streamed hand-offs) */
+int ess_preload(void);
 /* ESS_HOST_ROW_PITCH as compiled into this library */
 int ess_host_row_pitch(void);
 /* cudaHostRegister(mapped) + device alias: the host latent store (UVA gather source) */
@@ -139,14 +144,16 @@ int ess_pool_access(ess_pool *pool, int32_t begin, int32_t num, const int32_t *d
  * Optional attention split per set (all three or none), laid out like d_req: the rows
  * of the set resident before the step (d_tok_hit_row) and those fetched this step by
  * this set or an earlier one (d_tok_fresh_row), each in requested order, with
- * d_tok_counts [num * qtok][2] = (resident, fetched). */
+ * d_tok_counts [num * qtok][2] = (resident, fetched).  d_ready [num] (optional): set to 1
+ * (release) per pool once its lists and counts are stored — a concurrently running
+ * ess_gather_stream takes the pool's misses from then on. */
 int ess_pool_access_mtp(ess_pool *pool, int32_t begin, int32_t num, int32_t qtok,
                         const int32_t *d_req, const int32_t *d_n, int32_t req_stride,
                         int32_t *d_hit_ids, int32_t *d_miss_ids, int32_t *d_evicted_ids,
                         int32_t *d_sel_row, int32_t *d_hit_row, int32_t *d_miss_row,
                         int32_t *d_counts, int32_t out_stride, int32_t *d_tok_hit_row,
-                        int32_t *d_tok_fresh_row, int32_t *d_tok_counts, int32_t flags,
-                        void *stream);
+                        int32_t *d_tok_fresh_row, int32_t *d_tok_counts, int32_t *d_ready,
+                        int32_t flags, void *stream);
 /* Early-gather split of ess_pool_access (needs staging_rows >= 2048 and n <= capacity):
  * ess_pool_split is the read-only hit/miss split — hit rows, miss ids and STAGING rows
  * (cap_max + j) for the misses, counts (hits, misses) — so the host-link gather can

@@ -21,6 +21,7 @@ PI32, PI64, PV = ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64),
 SIGNATURES = {
     "ess_version": ([], ctypes.c_char_p),
     "ess_status_string": ([ctypes.c_int], ctypes.c_char_p),
+    "ess_preload": ([], ctypes.c_int),
     "ess_host_row_pitch": ([], ctypes.c_int),
     "ess_host_register": ([V, SZ, PV], ctypes.c_int),
     "ess_host_unregister": ([V], ctypes.c_int),
@@ -33,7 +34,7 @@ SIGNATURES = {
     "ess_pool_grow": ([V, I32, I32, V, V], ctypes.c_int),
     "ess_pool_warmup": ([V, I32, I32, V, V, I32, V, V], ctypes.c_int),
     "ess_pool_access": ([V, I32, I32, V, V, I32, V, V, V, V, V, V, V, I32, I32, V], ctypes.c_int),
-    "ess_pool_access_mtp": ([V, I32, I32, I32, V, V, I32, V, V, V, V, V, V, V, I32, V, V, V, I32, V],
+    "ess_pool_access_mtp": ([V, I32, I32, I32, V, V, I32, V, V, V, V, V, V, V, I32, V, V, V, V, I32, V],
                             ctypes.c_int),
     "ess_pool_append": ([V, I32, I32, V, V, I32, V, V], ctypes.c_int),
     "ess_pool_split": ([V, I32, I32, V, V, I32, V, V, V, V, I32, V], ctypes.c_int),
@@ -137,12 +138,21 @@ def stream_handle(stream=None):
     return s.cuda_stream
 
 
+_PRELOADED = set()
+
+
 def require_cuda(t=None) -> None:
     import torch
     if not torch.cuda.is_available():
         raise RuntimeError("ess_b200 needs a CUDA device (sm_100a); no CPU fallback exists")
     if t is not None and not t.is_cuda:
         raise ValueError("tensor must be on the CUDA device")
+    dev = torch.cuda.current_device()
+    if dev not in _PRELOADED:
+        # every kernel loaded before the first launch: with lazy module loading a kernel's
+        # first launch waits for the device, which deadlocks the streamed hand-offs
+        check(load().ess_preload(), "ess_preload")
+        _PRELOADED.add(dev)
 
 
 def check_tensor(t, name: str, dtypes, shape=None, contiguous: bool = True, device=None) -> None:

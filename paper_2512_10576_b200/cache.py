@@ -159,7 +159,8 @@ class PoolSet:
 
     def access_mtp(self, req: torch.Tensor, n: torch.Tensor, begin: int = 0, lists: bool = False,
                    sort_evicted: bool = True, out: AccessBatch | None = None,
-                   sel_row: torch.Tensor | None = None, tok_split=None) -> AccessBatch:
+                   sel_row: torch.Tensor | None = None, tok_split=None,
+                   ready: torch.Tensor | None = None) -> AccessBatch:
         """MTP: ``qtok`` selection sets per pool, req [num, qtok, K] / n [num, qtok] (the
         layout of ``indexer.topk_mtp``), taken as qtok consecutive access_steps per pool in
         one launch — recency is updated by every selected set.  ``sel_row``
@@ -167,7 +168,8 @@ class PoolSet:
         sets are appended in set order in its [num, qtok*K] rows; counts are the sums.
         ``tok_split`` = (hit_row, fresh_row [num, qtok, K], counts [num, qtok, 2]): per set,
         the rows resident before the step and those fetched this step (attention pass 1
-        beside the gather, pass 2 after it)."""
+        beside the gather, pass 2 after it).  ``ready`` (int32 [num]): each pool's flag is
+        set once its lists are stored (for a concurrently running ``gather_stream``)."""
         num, qtok, K = req.shape
         self._range(begin, num)
         if not 1 <= qtok <= _lib.MAX_QTOK:
@@ -200,7 +202,7 @@ class PoolSet:
             sel_row.data_ptr(), _lib.ptr(out.hit_row), _lib.ptr(out.miss_row),
             out.counts.data_ptr(), stride,
             *((_lib.ptr(t) for t in tok_split) if tok_split is not None else (None, None, None)),
-            flags, _lib.stream_handle()), "ess_pool_access_mtp")
+            _lib.ptr(ready), flags, _lib.stream_handle()), "ess_pool_access_mtp")
         out.sel_row = sel_row
         return out
 

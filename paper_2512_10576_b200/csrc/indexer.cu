@@ -568,3 +568,15 @@ extern "C" int ess_indexer_logits_stream(const void *d_q, const float *d_w, cons
 #ifdef ESS_STREAM_PROF
 ESS_STREAM_PROF_READER(ess_debug_stream_prof_k1)
 #endif
+
+// Load every kernel of this file now (lazy module loading would otherwise load a kernel
+// at its first launch, which waits for the device: a deadlock when a running kernel
+// spins on work the not-yet-loaded one produces — the streamed hand-offs).
+int ess_preload_indexer() {
+  cudaFuncAttributes a;
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)indexer_kernel<1>));
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)indexer_kernel<2>));
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)indexer_kernel<3>));
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)indexer_kernel<4>));
+  return ESS_OK;
+}

@@ -859,3 +859,10 @@ extern "C" int ess_sparse_mla_da_split(ess_pool *pool, int32_t pool_begin, const
                     count_stride, batch, sm_scale, d_out, d_lse, d_ws_o, d_ws_ml, MLA_AWAIT,
                     nsplit, stream);
 }
+
+int ess_preload_mla() {  // see ess_preload_indexer
+  cudaFuncAttributes a;
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)sparse_mla_kernel));
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)mla_combine_kernel));
+  return ESS_OK;
+}

@@ -910,3 +910,10 @@ int ess_launch_mla_pair(ess_pool *pool, int32_t pool_begin, const void *d_q, con
                                     d_lse, d_ws_o, d_ws_ml, (int)flags, (int)nsplit, pool->status));
   return ESS_OK;
 }
+
+int ess_preload_mla2() {  // see ess_preload_indexer
+  cudaFuncAttributes a;
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)sparse_mla_pair_kernel<true>));
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)sparse_mla_pair_kernel<false>));
+  return ESS_OK;
+}

@@ -61,6 +61,7 @@ struct TokSplit {
   int32_t *hit_row = nullptr;
   int32_t *fresh_row = nullptr;
   int32_t *cnt = nullptr;
+  int32_t *ready = nullptr;  // per pool: set to 1 (release) once its lists and counts are out
 };
 
 struct StepSmem {
@@ -420,6 +421,11 @@ __global__ void __launch_bounds__(NT, 1)
                                           : ((uint64_t)clk + (uint64_t)n > 0xFFFFFF00ull)
                                               ? ESS_ERR_CLOCK
                                               : ESS_ERR_ARG);
+    if (ts.ready && t == 0) {  // a waiting gather must not spin: publish an empty list
+      if (counts_out) counts_out[b * 4 + 1] = 0;
+      __threadfence();
+      ess_st_release(ts.ready + b, 1);
+    }
     return;
   }
 
@@ -743,6 +749,11 @@ __global__ void __launch_bounds__(NT, 1)
   acc_tr += n > cap ? n - cap : 0;
   __syncthreads();  // the next set reads the pool state (meta, keys) this one wrote
   }  // jq
+  if (ts.ready) {  // a concurrent streamed gather takes this pool's misses from here on
+    __threadfence();
+    __syncthreads();
+    if (t == 0) ess_st_release(ts.ready + b, 1);
+  }
 }
 
 __global__ void pool_reset_kernel(PoolView pv, int begin, int num, const int32_t *cap) {
@@ -1609,7 +1620,7 @@ int ess_pool_access_mtp(ess_pool *p, int32_t begin, int32_t num, int32_t qtok, c
                         int32_t *d_miss_ids, int32_t *d_evicted_ids, int32_t *d_sel_row,
                         int32_t *d_hit_row, int32_t *d_miss_row, int32_t *d_counts,
                         int32_t out_stride, int32_t *d_tok_hit_row, int32_t *d_tok_fresh_row,
-                        int32_t *d_tok_counts, int32_t flags, void *stream) {
+                        int32_t *d_tok_counts, int32_t *d_ready, int32_t flags, void *stream) {
   if (qtok < 1 || qtok > ESS_INDEXER_MAX_QTOK) return ESS_ERR_ARG;
   if ((d_tok_hit_row || d_tok_fresh_row || d_tok_counts) && !(d_tok_hit_row && d_tok_fresh_row && d_tok_counts))
     return ESS_ERR_ARG;
@@ -1617,6 +1628,7 @@ int ess_pool_access_mtp(ess_pool *p, int32_t begin, int32_t num, int32_t qtok, c
   ts.hit_row = d_tok_hit_row;
   ts.fresh_row = d_tok_fresh_row;
   ts.cnt = d_tok_counts;
+  ts.ready = d_ready;
   if ((d_hit_ids || d_miss_ids || d_evicted_ids || d_hit_row || d_miss_row) &&
       (int64_t)out_stride < (int64_t)qtok * req_stride)
     return ESS_ERR_ARG;  // the appended lists of qtok sets must fit a pool's row
@@ -1790,3 +1802,17 @@ int ess_write_generated(ess_pool *p, int32_t begin, int32_t num, const int32_t *
 #ifdef ESS_STREAM_PROF
 ESS_STREAM_PROF_READER(ess_debug_stream_prof_gather)
 #endif
+
+int ess_preload_pool() {  // see ess_preload_indexer
+  cudaFuncAttributes a;
+  const void *k[] = {(const void *)pool_step_kernel<MODE_ACCESS>, (const void *)pool_step_kernel<MODE_WARMUP>,
+                     (const void *)pool_reset_kernel, (const void *)pool_grow_kernel,
+                     (const void *)pool_append_kernel, (const void *)pool_lru_order_kernel,
+                     (const void *)pool_split_kernel, (const void *)pool_settle_kernel,
+                     (const void *)pool_counters_kernel, (const void *)gather_kernel,
+                     (const void *)gather_bulk_kernel, (const void *)gather_stream_kernel,
+                     (const void *)write_generated_kernel, (const void *)pool_admit_kernel,
+                     (const void *)pool_lookup_kernel, (const void *)pool_copy_kernel};
+  for (const void *f : k) ESS_CUDA_TRY(cudaFuncGetAttributes(&a, f));
+  return ESS_OK;
+}

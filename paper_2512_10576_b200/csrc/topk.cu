@@ -771,3 +771,14 @@ extern "C" int ess_topk_split_stream(const float *d_logits, int64_t ld, const in
 #ifdef ESS_STREAM_PROF
 ESS_STREAM_PROF_READER(ess_debug_stream_prof_topk)
 #endif
+
+int ess_preload_topk() {  // see ess_preload_indexer
+  cudaFuncAttributes a;
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)topk_kernel<1>));
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)topk_kernel<2>));
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)topk_kernel<4>));
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)topk_kernel<8>));
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)topk_stream_kernel<1>));
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)topk_stream_kernel<2>));
+  return ESS_OK;
+}

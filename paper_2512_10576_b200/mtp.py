@@ -32,6 +32,7 @@ C1-style oversize regime (cap < K) is served by the single-token layer.
 from __future__ import annotations
 
 import math
+import os
 from types import SimpleNamespace
 
 import numpy as np
@@ -42,7 +43,7 @@ from .attention import SplitWorkspace, sparse_mla
 from .cache import AccessBatch
 from .decode import ROW, DSADecodeLayer, _e4m3, random_latent_rows
 from .indexer import indexer_logits, indexer_logits_mtp, topk, topk_mtp
-from .transfer import gather
+from .transfer import gather, gather_stream
 
 
 class MTPDecodeLayer(DSADecodeLayer):
@@ -62,6 +63,10 @@ class MTPDecodeLayer(DSADecodeLayer):
                              f"floor(rho * ctx) = {self.cap0} < {qtok} * {topk_k}")
         self.qtok, self.mtp = qtok, int(mtp)
         self.early_gather = False
+        # streamed gathers (launched after each micro-batch's indexer, taking requests as
+        # the cache manager publishes them): correct, but the spinning CTAs cost the later
+        # indexer / top-k SMs (523 vs 490 us at C2 MTP = 2), so off by default
+        self.stream_gather = os.environ.get("ESS_MTP_STREAM_GATHER", "0") == "1"
         B, d, g, Q = self.B, self.device, self.gen, qtok
         self._zi = torch.randn((B, Q, 64, 128), device=d, generator=g)
         self._za = torch.randn((B, Q, 128, 576), device=d, generator=g)
@@ -164,6 +169,20 @@ class MTPDecodeLayer(DSADecodeLayer):
             th, tf, tc = th.view(B * Q, K), tf.view(B * Q, K), tc.view(B * Q, 2)
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
         ranges = self.micro_batches(micro if overlap == "dba" else 1)
+        # streamed gathers: each micro-batch's gather is launched as soon as its indexer is
+        # done and takes each request's misses the moment the cache manager publishes them
+        # (ready flags), so its CTAs are resident before that micro-batch's attention floods
+        # the SMs (launched after the cache manager, a gather queued behind 2 x qtok
+        # attention CTAs per request and ran at ~25 GB/s)
+        streamed = split and self.stream_gather
+        if streamed:
+            if getattr(self, "_gsync", None) is None:
+                self._gsync = torch.zeros(2 * B, dtype=torch.int32, device=self.device)  # ready | claim
+                self._gsides = []
+            while len(self._gsides) < len(ranges):
+                self._gsides.append(torch.cuda.Stream(self.device, priority=-1))
+            self._gsync.zero_()
+            gready, gclaim = self._gsync[:B], self._gsync[B:]
         prev = 0
         for i, (a, b) in enumerate(ranges):
             # later micro-batches' indexer leaves SMs to the running gather and to the
@@ -173,23 +192,34 @@ class MTPDecodeLayer(DSADecodeLayer):
                                self.lens[a:b], out=self.logits[a:b], max_ctas=ctas)
             scored = torch.cuda.Event()
             scored.record(main)
+            g = gather_ctas if i == len(ranges) - 1 else max(gather_ctas, self.early_gather_sms)
+            if streamed:
+                gs = self._gsides[i]
+                gs.wait_event(scored)
+                with torch.cuda.stream(gs):
+                    gather_stream(self.pool, self.store, self._view(a, b), gready[a:b], gclaim[a:b], None,
+                                  begin=a, max_ctas=g)
+                    fetched = torch.cuda.Event()
+                    fetched.record(gs)
+                side.wait_event(fetched)
             sel.wait_event(scored)
             with torch.cuda.stream(sel):
                 topk_mtp(self.logits[a:b], self.lens[a:b], K, out=self.idx[a:b], count=self.cnt[a:b])
                 self.pool.access_mtp(self.idx[a:b], self.cnt[a:b], begin=a, out=self._view(a, b),
                                      sel_row=self.sel_row[a:b],
                                      tok_split=None if overlap == "none" else
-                                     tuple(x[a:b] for x in self.tok_split))
+                                     tuple(x[a:b] for x in self.tok_split),
+                                     ready=gready[a:b] if streamed else None)
                 ready = torch.cuda.Event()
                 ready.record(sel)
-            side.wait_event(ready)
-            with torch.cuda.stream(side):
-                g = gather_ctas if i == len(ranges) - 1 else max(gather_ctas, self.early_gather_sms)
-                # exclusive SMs: the host-link loads must not share an SM's miss tracking
-                # with the indexer or attention CTAs
-                gather(self.pool, self.store, self._view(a, b), begin=a, max_ctas=g, exclusive=True)
-                fetched = torch.cuda.Event()
-                fetched.record(side)
+            if not streamed:
+                side.wait_event(ready)
+                with torch.cuda.stream(side):
+                    # exclusive SMs: the host-link loads must not share an SM's miss
+                    # tracking with the indexer or attention CTAs
+                    gather(self.pool, self.store, self._view(a, b), begin=a, max_ctas=g, exclusive=True)
+                    fetched = torch.cuda.Event()
+                    fetched.record(side)
             if split:
                 # this micro-batch's attention on its own stream, while later micro-batches
                 # select and gather: pass 1 over its resident rows right after its cache

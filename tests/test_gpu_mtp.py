@@ -156,12 +156,15 @@ def _mtp_chain(layer, orc, hist, accepted, q=None, q_idx=None, counts=None, attn
         orc[b].append_generated(new)
 
 
-@pytest.mark.parametrize("mtp,overlap", [(2, "dba"), (2, "none"), (2, "da"), (1, "dba"), (3, "dba")])
+@pytest.mark.parametrize("mtp,overlap", [(2, "dba"), (2, "none"), (2, "da"), (1, "dba"), (3, "dba"),
+                                         (2, "dba+streamed-gather")])
 def test_mtp_layer_matches_oracle_chain(mtp, overlap):
     from paper_2512_10576_b200.cache import pool_capacity
     from paper_2512_10576_b200.mtp import MTPDecodeLayer, draw_accepted
     B, K, ctx, rho = 4, 2048, 32768, 0.25
     layer = MTPDecodeLayer(B, ctx, rho, K, mtp=mtp, max_new_tokens=6, seed=7, drift=0.97)
+    if overlap.endswith("+streamed-gather"):  # gathers taking requests as K3 publishes them
+        overlap, layer.stream_gather = "dba", True
     wins = layer.prefill_warmup(windows=6, record=True)
     orc = [olru.OraclePool(pool_capacity(rho, ctx)) for _ in range(B)]
     for w in wins:
