@@ -174,7 +174,7 @@ class DSADecodeLayer:
         """The all-HBM ceiling's state: every request's whole history made
         resident in its pool (needs sparse_ratio = 1) and its slot rows filled from the
         host store, so every selection hits and no step gathers anything."""
-        if self.cap0 < max(self.ctx_lens):
+        if any(pool_capacity(self.rho, n) < n for n in self.ctx_lens):  # each pool its own history
             raise ValueError("preload_full_history needs a pool that holds the whole history (rho = 1)")
         B, d = self.B, self.device
         full = torch.arange(self.ctx, dtype=torch.int32, device=d)

@@ -254,3 +254,18 @@ def test_mixed_length_batch_matches_oracle(overlap):
         assert out[b, :int(cnt[b])].tolist() == orc[b].lru_order()
     assert layer.lens.tolist() == hist
     layer.close()
+
+
+def test_preload_full_history_mixed_lengths():
+    """The all-HBM ceiling's state for a mixed-length batch (C5): every pool holds its own
+    request's whole history at rho = 1, so a step hits every selected row."""
+    from paper_2512_10576_b200.decode import DSADecodeLayer
+    layer = DSADecodeLayer(3, [5000, 9000, 12000], 1.0, 2048, max_new_tokens=4, seed=5, drift=0.97)
+    layer.preload_full_history()
+    q_idx, q = layer.next_queries()
+    layer.attend(q_idx, q, overlap="none")
+    torch.cuda.synchronize()
+    counts = layer.step_counts().cpu().numpy()
+    assert (counts[:, 1] == 0).all() and (counts[:, 0] == 2048).all(), counts
+    layer.pool.check()
+    layer.close()
