@@ -14,8 +14,12 @@ import torch  # noqa: E402
 from paper_2512_10576_b200 import _lib  # noqa: E402
 from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows  # noqa: E402
 
-B, ctx, rho = 64, 32768, 0.25
+B, ctx, rho = {"c2": (64, 32768, 0.25), "c4": (64, 131072, 0.1)}[os.environ.get("CONFIG", "c2")]
 layer = DSADecodeLayer(B, ctx, rho, 2048, max_new_tokens=64, seed=1234, drift=0.97)
+if os.environ.get("MICRO"):
+    layer.micro = int(os.environ["MICRO"])
+if os.environ.get("FIRST"):
+    layer.first_frac = float(os.environ["FIRST"])
 layer.prefill_warmup(windows=32)
 L = _lib.load()
 for fn in (L.ess_debug_stream_prof_topk, L.ess_debug_stream_prof_gather, L.ess_debug_stream_prof_k1):
