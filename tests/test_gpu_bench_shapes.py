@@ -20,14 +20,14 @@ pytestmark = pytest.mark.gpu
 STEPS = 3
 
 
-def _run(cfg_name, attn_sample, logit_sample, steps=STEPS):
+def _run(cfg_name, attn_sample, logit_sample, steps=STEPS, overlap="dba"):
     import bench
     from paper_2512_10576_b200.decode import random_latent_rows
     cfg = bench.CONFIGS[cfg_name]
     layer, lens, wins = bench.product_layer(cfg, "cuda", steps + 2, drift=0.97, record=True)
     try:
         chain = OracleChain(layer, lens, wins, attn_sample=attn_sample, logit_sample=logit_sample)
-        eager = layer.capture("dba", layer.gather_ctas)   # one eager step, then the graph
+        eager = layer.capture(overlap, layer.gather_ctas)   # one eager step, then the graph
         chain.mirror(counts=eager)
         B = layer.B
         for _ in range(steps):
@@ -45,6 +45,12 @@ def _run(cfg_name, attn_sample, logit_sample, steps=STEPS):
 def test_c2_benchmarked_step_matches_oracle_chain():
     ranges = _run("c2", attn_sample=(0, 15, 16, 40, 63), logit_sample=(0, 63))
     assert ranges == [(0, 16), (16, 64)]  # the DBA 16 | 48 split of the bench line
+
+
+def test_c2_streamed_step_matches_oracle_chain():
+    """The streamed schedule (bench.py --overlap stream) at the C2 shape: K1 / K2 / K4 as
+    concurrent grids handing the 64 requests on through counters."""
+    _run("c2", attn_sample=(0, 7, 8, 40, 63), logit_sample=(0,), overlap="stream")
 
 
 def test_c4_benchmarked_step_matches_oracle_chain():
