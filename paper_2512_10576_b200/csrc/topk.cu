@@ -727,7 +727,7 @@ extern "C" int ess_topk_split_stream(const float *d_logits, int64_t ld, const in
       pool->staging < k || !d_done || !d_ready || ctas == 0)
     return ESS_ERR_ARG;
   if (!d_logits || !d_len || !d_idx || !d_count || batch < 0 || k < 1 || idx_ld < k || ld < 1 ||
-      ld > SLICE_MAX)
+      (ld + 7) / 8 > SLICE_MAX)
     return ESS_ERR_ARG;
   if (batch == 0) return ESS_OK;
   SplitArgs sp{};
@@ -739,13 +739,19 @@ extern "C" int ess_topk_split_stream(const float *d_logits, int64_t ld, const in
   sp.miss_row = d_miss_row;
   sp.counts = d_counts;
   sp.out_stride = out_stride;
-  // ctas < 0: -ctas two-CTA clusters (each row on a CTA pair)
-  const int cln = ctas < 0 ? 2 : 1;
+  // cluster size per row: the smallest whose slice fits shared memory (rows > 40K tokens
+  // take 2-8 CTAs, as ess_topk); ctas < 0 forces at least CTA pairs.  `ctas` counts rows
+  // worked on at once (clusters).
+  int cln = 1;
+  while (cln < 8 && (ld + cln - 1) / cln > SLICE_MAX) cln *= 2;
+  if (ctas < 0 && cln < 2) cln = 2;
   int nclu = ctas < 0 ? -ctas : ctas;
   if (nclu > batch) nclu = batch;
-  const size_t smem = (size_t)(cln == 2 ? slice_cap<2>(ld) : slice_cap<1>(ld)) * sizeof(uint32_t) +
+  const size_t smem = (size_t)(cln == 1 ? slice_cap<1>(ld) : cln == 2 ? slice_cap<2>(ld)
+                               : cln == 4 ? slice_cap<4>(ld) : slice_cap<8>(ld)) * sizeof(uint32_t) +
                       (LCAP + NT) * sizeof(uint16_t);
-  const void *kern = cln == 2 ? (const void *)topk_stream_kernel<2> : (const void *)topk_stream_kernel<1>;
+  const void *kern = cln == 1 ? (const void *)topk_stream_kernel<1> : cln == 2 ? (const void *)topk_stream_kernel<2>
+                     : cln == 4 ? (const void *)topk_stream_kernel<4> : (const void *)topk_stream_kernel<8>;
   if (int rc = ess_smem_optin(kern, SLICE_MAX * sizeof(uint32_t) + (LCAP + NT) * sizeof(uint16_t))) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nclu * cln));
@@ -759,12 +765,24 @@ extern "C" int ess_topk_split_stream(const float *d_logits, int64_t ld, const in
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (cln == 2)
-    ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, topk_stream_kernel<2>, d_logits, ld, d_len, (int)batch, (int)k, d_idx,
-                                    (int)idx_ld, d_count, sp, d_done, d_ready));
-  else
-    ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, topk_stream_kernel<1>, d_logits, ld, d_len, (int)batch, (int)k, d_idx,
-                                    (int)idx_ld, d_count, sp, d_done, d_ready));
+  switch (cln) {
+    case 1:
+      ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, topk_stream_kernel<1>, d_logits, ld, d_len, (int)batch, (int)k, d_idx,
+                                      (int)idx_ld, d_count, sp, d_done, d_ready));
+      break;
+    case 2:
+      ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, topk_stream_kernel<2>, d_logits, ld, d_len, (int)batch, (int)k, d_idx,
+                                      (int)idx_ld, d_count, sp, d_done, d_ready));
+      break;
+    case 4:
+      ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, topk_stream_kernel<4>, d_logits, ld, d_len, (int)batch, (int)k, d_idx,
+                                      (int)idx_ld, d_count, sp, d_done, d_ready));
+      break;
+    default:
+      ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, topk_stream_kernel<8>, d_logits, ld, d_len, (int)batch, (int)k, d_idx,
+                                      (int)idx_ld, d_count, sp, d_done, d_ready));
+      break;
+  }
   return ESS_OK;
 }
 
@@ -780,5 +798,7 @@ int ess_preload_topk() {  // see ess_preload_indexer
   ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)topk_kernel<8>));
   ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)topk_stream_kernel<1>));
   ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)topk_stream_kernel<2>));
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)topk_stream_kernel<4>));
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)topk_stream_kernel<8>));
   return ESS_OK;
 }

@@ -377,9 +377,9 @@ class DSADecodeLayer:
 
     def stream_ok(self) -> bool:
         """The streamed schedule's preconditions: early gather (every pool holds a whole
-        selection, staging rows), rows that fit one top-k CTA, and the fused DA launch."""
+        selection, staging rows), rows of at most 8 top-k CTAs, and the fused DA launch."""
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count
-        return (self.early_gather and self.Lmax <= 40 * 1024 and self.fuse_da and 2 * self.B <= sms - 8)
+        return (self.early_gather and self.Lmax <= 8 * 40 * 1024 and self.fuse_da and 2 * self.B <= sms - 8)
 
     def _attend_stream(self, q_idx, q, new_rows, gather_ctas):
         """The streamed step: K1, K2+K3a and K4 run CONCURRENTLY as three persistent grids
@@ -418,7 +418,10 @@ class DSADecodeLayer:
         self._sync.zero_()
         start = torch.cuda.Event()
         start.record(main)
-        k2_sms = nk2 if nk2 > 0 else -2 * nk2   # < 0: CTA-pair clusters per row
+        cln = 1  # CTAs per top-k row: the smallest cluster whose slice fits (rows > 40K tokens)
+        while cln < 8 and -(-self.Lmax // cln) > 40 * 1024:
+            cln *= 2
+        k2_sms = nk2 * cln if nk2 > 0 else -nk2 * max(2, cln)   # < 0: at least CTA pairs
         indexer_logits_stream(q_idx, self.w, self.k_cache, self.k_scale, self.lens, self.logits, done,
                               self.stream_group | (self.stream_first << 16), sms - k2_sms - g)
         sel.wait_event(start)

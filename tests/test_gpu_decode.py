@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("ctx,rho,fuse,overlap", [(8192, 0.25, True, "dba"), (4096, 0.25, True, "dba"),
                                                   (8192, 0.25, False, "dba"), (8192, 0.25, True, "da"),
                                                   (8192, 0.25, True, "none"), (8192, 0.25, True, "stream"),
-                                                  (32768, 0.25, True, "stream")])
+                                                  (32768, 0.25, True, "stream"), (131072, 0.1, True, "stream")])
 def test_decode_layer_matches_oracle_chain(ctx, rho, fuse, overlap):
     """fuse: the DA schedule as one K5 launch waiting on the gather's arrival counters
     (sparse_mla_da) vs. two K5 passes merged through the workspace."""
