@@ -146,7 +146,8 @@ class ClockSampler:
 # -------------------------------------------------------------------------------------
 # CPU leg: the oracle port on host cores (cpu_baseline and --impl reference)
 # -------------------------------------------------------------------------------------
-CPU_WARM_WINDOWS = 4  # prefill windows per request in the CPU leg (the GPU layer uses 32)
+CPU_WARM_WINDOWS = 8  # prefill windows per request in the CPU leg (the GPU layer uses 32)
+CPU_WARM_STEPS = 2    # untimed decode steps before the timed one (the GPU bench warms up too)
 
 
 def _cpu_request(task):
@@ -171,11 +172,12 @@ def _cpu_request(task):
             .view(torch.uint8).numpy()
 
     rng = np.random.default_rng(seed)
-    k = e4(rng.standard_normal((L, 128)) * 8)           # the GPU layer's key / query scales
+    Lx = L + CPU_WARM_STEPS + 1                          # history grows by one token per step
+    k = e4(rng.standard_normal((Lx, 128)) * 8)          # the GPU layer's key / query scales
     w = rng.standard_normal(64).astype(np.float32) / 8
-    ks = (rng.random(L).astype(np.float32) * 0.5 + 0.75)
-    host = rng.integers(0, 120, size=(L + 1, 656), dtype=np.uint8)   # latent rows (+ the new one)
-    host[:, 512:528] = np.full((L + 1, 4), 0.03, np.float32).view(np.uint8)
+    ks = (rng.random(Lx).astype(np.float32) * 0.5 + 0.75)
+    host = rng.integers(0, 120, size=(Lx + 1, 656), dtype=np.uint8)  # latent rows (+ the new ones)
+    host[:, 512:528] = np.full((Lx + 1, 4), 0.03, np.float32).view(np.uint8)
     host[:, 528:] = 0
     slots = np.zeros_like(host)                                       # the slot store
     a, sd = drift, float(np.sqrt(max(0.0, 1.0 - drift * drift)))
@@ -188,19 +190,26 @@ def _cpu_request(task):
             pool.warmup([dsa.topk_indices(dsa.indexer_logits(e4(zi * 4), w, k, ks, L), L, TOPK).tolist()])
         res = pool.lru_order()
         slots[res] = host[res]
-        zi = a * zi + sd * rng.standard_normal(zi.shape)
-        q = e4(zi * 4)
-        t0 = time.perf_counter()
-        logits = dsa.indexer_logits(q, w, k, ks, L)
-        idx = dsa.topk_indices(logits, L, TOPK)
-        r = pool.access_step(idx.tolist())
-        miss = np.asarray(r.miss_ids, dtype=np.int64)
-        slots[miss] = host[miss]                                      # K4: the miss gather
-        dsa.sparse_mla(qa, slots[idx], 1.0 / 192 ** 0.5)              # K5 over the slot rows
-        pool.grow_capacity(olru.pool_capacity(rho, L + 1))           # admission (cache.py:191-195)
-        pool.append_generated([L])
-        slots[L] = host[L]
-        return time.perf_counter() - t0, len(r.hit_ids), len(r.miss_ids)
+
+        def step(h):  # one decode step over a history of h tokens; the new token is id h
+            nonlocal zi
+            zi = a * zi + sd * rng.standard_normal(zi.shape)
+            q = e4(zi * 4)
+            t0 = time.perf_counter()
+            logits = dsa.indexer_logits(q, w, k, ks, h)
+            idx = dsa.topk_indices(logits, h, TOPK)
+            r = pool.access_step(idx.tolist())
+            miss = np.asarray(r.miss_ids, dtype=np.int64)
+            slots[miss] = host[miss]                                  # K4: the miss gather
+            dsa.sparse_mla(qa, slots[idx], 1.0 / 192 ** 0.5)          # K5 over the slot rows
+            pool.grow_capacity(olru.pool_capacity(rho, h + 1))       # admission (cache.py:191-195)
+            pool.append_generated([h])
+            slots[h] = host[h]
+            return time.perf_counter() - t0, len(r.hit_ids), len(r.miss_ids)
+
+        for s_ in range(CPU_WARM_STEPS):  # untimed, like the GPU bench's warm-up steps
+            step(L + s_)
+        return step(L + CPU_WARM_STEPS)
 
 
 def _cpu_pool(workers):
@@ -244,7 +253,8 @@ def cpu_reference_rate(cfg, budget_s: float = 12.0, seed: int = 0, drift: float 
     hit_rate = hits / max(1, hits + misses)
     sample = (f"{n_req} request-steps of the {cfg['workload']} workload at query drift {drift}, {cores} at a "
               f"time (one per core, spawn processes, single-threaded BLAS), each after an untimed "
-              f"{CPU_WARM_WINDOWS}-window prefill warm-up: numpy indexer + top-k + C LRU step + miss gather "
+              f"{CPU_WARM_WINDOWS}-window prefill warm-up and {CPU_WARM_STEPS} decode steps: numpy indexer + "
+              f"top-k + C LRU step + miss gather "
               f"into the slot store + numpy sparse MLA + admission (oracle port); mean {mean_t * 1e3:.1f} ms "
               f"per request-step, hit rate {hit_rate:.3f}, {wall:.2f} s wall")
     return cores / mean_t, sample, cores, hit_rate
@@ -275,7 +285,7 @@ def run_reference(args, cfg):
                        "sparse_ratio": cfg["sparse_ratio"],
                        "topk": TOPK, "query_drift": args.drift,
                        "overlap": "none (one request per core, sequential K1..K5 + admission)",
-                       "prefill_windows": CPU_WARM_WINDOWS},
+                       "prefill_windows": CPU_WARM_WINDOWS, "untimed_decode_steps": CPU_WARM_STEPS},
             "hit_rate": hit_rate,
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
                              "sample": sample},
