@@ -100,6 +100,12 @@ int ess_host_free(void *host_ptr, size_t bytes);
 /* diagnostic: write the device global timer (ns) to *d_dst in stream order; works
  * inside captured CUDA graphs (step timelines) */
 int ess_timestamp(uint64_t *d_dst, void *stream);
+/* up to ESS_COPY_MAX device-to-device copies (pointers 16-B aligned, sizes multiples of
+ * 16 B) in one SM kernel: the decode step's input staging (copy-engine D2D copies ran at
+ * ~0.4 TB/s with microseconds of latency each, in front of every step) */
+#define ESS_COPY_MAX 64
+int ess_copy_many(int32_t n, void *const *d_dst, const void *const *d_src, const int64_t *bytes,
+                  void *stream);
 
 /* ---- K3 cache manager: replaces offsim.cache.SparsePool (cache.py:29-134) ------ */
 /* num_pools pools over ids [0, max_ids), each with up to cap_max slots.  When

@@ -26,6 +26,7 @@ SIGNATURES = {
     "ess_host_register": ([V, SZ, PV], ctypes.c_int),
     "ess_host_unregister": ([V], ctypes.c_int),
     "ess_timestamp": ([V, V], ctypes.c_int),
+    "ess_copy_many": ([I32, PV, PV, PI64, V], ctypes.c_int),
     "ess_host_alloc": ([SZ, I32, I32, PV, PV, PI32], ctypes.c_int),
     "ess_host_free": ([V, SZ], ctypes.c_int),
     "ess_pool_create": ([PV, I32, I64, I32, I32, I32], ctypes.c_int),
@@ -173,3 +174,29 @@ def check_tensor(t, name: str, dtypes, shape=None, contiguous: bool = True, devi
         raise ValueError(f"{name} must be contiguous")
     if not t.is_cuda or (device is not None and t.device != device):
         raise ValueError(f"{name} must be on the CUDA device {device or ''}".rstrip())
+
+
+COPY_MAX = 64  # ESS_COPY_MAX
+
+
+def copy_many(pairs, stream=None) -> None:
+    """Device-to-device copies [(dst, src), ...] of contiguous CUDA tensors with equal byte
+    sizes, in one SM kernel per 64 pairs (ess_copy_many) — the decode step's input
+    staging.  Pairs that are not 16-B aligned / sized take torch's copy."""
+    fast = []
+    for dst, src in pairs:
+        nb = dst.numel() * dst.element_size()
+        if (src.dtype != dst.dtype or src.numel() != dst.numel() or not (dst.is_contiguous() and src.is_contiguous())
+                or not (dst.is_cuda and src.is_cuda)):
+            raise ValueError("copy_many: contiguous CUDA tensors of one dtype and size")
+        if nb % 16 or dst.data_ptr() % 16 or src.data_ptr() % 16:
+            dst.copy_(src.view(dst.shape), non_blocking=True)
+        elif nb:
+            fast.append((dst.data_ptr(), src.data_ptr(), nb))
+    for i in range(0, len(fast), COPY_MAX):
+        chunk = fast[i:i + COPY_MAX]
+        n = len(chunk)
+        d = (ctypes.c_void_p * n)(*[c[0] for c in chunk])
+        sp = (ctypes.c_void_p * n)(*[c[1] for c in chunk])
+        b = (ctypes.c_int64 * n)(*[c[2] for c in chunk])
+        check(load().ess_copy_many(n, d, sp, b, stream_handle(stream)), "ess_copy_many")

@@ -119,10 +119,55 @@ int ess_host_register(void *host_ptr, size_t bytes, void **d_alias) {
 
 // Diagnostic: one thread writes the device's global nanosecond timer to *d_dst, in
 // stream order (usable inside captured CUDA graphs, where events cannot be timed).
+// Input staging: up to ESS_COPY_MAX device-to-device copies (16-B aligned, multiples of
+// 16 B) in one grid-stride SM kernel.  The decode step's per-step inputs (q, q_idx, the
+// generated rows) land in the captured graph's static buffers this way: as separate
+// cudaMemcpyAsync copies they ran on the copy engine at ~0.4 TB/s plus a few us of
+// latency each, serialised in front of every step (24 us of a 211-us C2 step).
+struct CopyArgs {
+  uint4 *dst[ESS_COPY_MAX];
+  const uint4 *src[ESS_COPY_MAX];
+  int64_t pref[ESS_COPY_MAX + 1];  // 16-B units before copy i
+  int n;
+};
+
+__global__ void __launch_bounds__(256) copy_many_kernel(const __grid_constant__ CopyArgs a) {
+  const int64_t total = a.pref[a.n];
+  int c = 0;
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    while (u >= a.pref[c + 1]) c++;  // units are visited in increasing order per thread
+    const int64_t o = u - a.pref[c];
+    a.dst[c][o] = __ldg(a.src[c] + o);
+  }
+}
+
 __global__ void timestamp_kernel(uint64_t *dst) {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   *dst = t;
+}
+
+int ess_copy_many(int32_t n, void *const *d_dst, const void *const *d_src, const int64_t *bytes,
+                  void *stream) {
+  if (n < 0 || n > ESS_COPY_MAX || (n && (!d_dst || !d_src || !bytes))) return ESS_ERR_ARG;
+  CopyArgs a;
+  a.n = n;
+  a.pref[0] = 0;
+  for (int i = 0; i < n; i++) {
+    if (!d_dst[i] || !d_src[i] || bytes[i] < 0 || (bytes[i] & 15) ||
+        (reinterpret_cast<uintptr_t>(d_dst[i]) & 15) || (reinterpret_cast<uintptr_t>(d_src[i]) & 15))
+      return ESS_ERR_ARG;
+    a.dst[i] = static_cast<uint4 *>(d_dst[i]);
+    a.src[i] = static_cast<const uint4 *>(d_src[i]);
+    a.pref[i + 1] = a.pref[i] + bytes[i] / 16;
+  }
+  if (n == 0 || a.pref[n] == 0) return ESS_OK;
+  const int64_t want = (a.pref[n] + 255) / 256;
+  const int grid = (int)(want < 4 * (int64_t)ess_sm_count() ? want : 4 * (int64_t)ess_sm_count());
+  copy_many_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a);
+  ESS_CUDA_TRY(cudaGetLastError());
+  return ESS_OK;
 }
 
 int ess_timestamp(uint64_t *d_dst, void *stream) {
@@ -199,6 +244,7 @@ int ess_preload(void) {
   if (dev >= 0 && dev < 64 && done[dev]) return ESS_OK;
   cudaFuncAttributes a;
   ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)timestamp_kernel));
+  ESS_CUDA_TRY(cudaFuncGetAttributes(&a, (const void *)copy_many_kernel));
   if (int rc = ess_preload_indexer()) return rc;
   if (int rc = ess_preload_topk()) return rc;
   if (int rc = ess_preload_pool()) return rc;

@@ -541,9 +541,7 @@ class DSADecodeLayer:
         """One decode step through the captured graph: inputs land in the graph's
         static buffers (two device copies), then a single graph launch."""
         self._check_room()
-        self.q_idx_in.copy_(q_idx, non_blocking=True)
-        self.q_in.copy_(q, non_blocking=True)
-        self.rows_in.copy_(new_rows, non_blocking=True)
+        _lib.copy_many([(self.q_idx_in, q_idx), (self.q_in, q), (self.rows_in, new_rows)])
         self.graph.replay()
         self.history += 1
         return self.out, self.lse
@@ -585,9 +583,7 @@ class DSADecodeLayer:
             st_q.copy_(h_q, non_blocking=True)
             ev["in_ready"].record(cs)
         main.wait_event(ev["in_ready"])
-        self.q_idx_in.copy_(st_qi)
-        self.q_in.copy_(st_q)
-        self.rows_in.copy_(new_rows)
+        _lib.copy_many([(self.q_idx_in, st_qi), (self.q_in, st_q), (self.rows_in, new_rows)])
         ev["in_free"].record(main)
         self.graph.replay()
         self.history += 1
@@ -711,11 +707,11 @@ class DSADecodeModel:
         """queries: per layer (q_idx, q); new_rows: per layer [B, 1, 656] (or one shared)."""
         for layer in self.layers:
             layer._check_room()
+        pairs = []
         for i, (layer, (q_idx, q)) in enumerate(zip(self.layers, queries)):
-            layer.q_idx_in.copy_(q_idx, non_blocking=True)
-            layer.q_in.copy_(q, non_blocking=True)
-            layer.rows_in.copy_(new_rows[i] if isinstance(new_rows, (list, tuple)) else new_rows,
-                                non_blocking=True)
+            pairs += [(layer.q_idx_in, q_idx), (layer.q_in, q),
+                      (layer.rows_in, new_rows[i] if isinstance(new_rows, (list, tuple)) else new_rows)]
+        _lib.copy_many(pairs)  # every layer's inputs: one SM copy kernel per 64 tensors
         self.graph.replay()
         for layer in self.layers:
             layer.history += 1

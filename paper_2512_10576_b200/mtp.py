@@ -335,10 +335,12 @@ class MTPDecodeLayer(DSADecodeLayer):
         # device-resident counts are checked by the admission kernel (m > qtok latches
         # ESS_ERR_ARG; read by pool.check())
         self._check_room(m)
-        self.q_idx_in.copy_(q_idx, non_blocking=True)
-        self.q_in.copy_(q, non_blocking=True)
-        self.rows_in.copy_(new_rows, non_blocking=True)
-        self.accept_in.copy_(accepted, non_blocking=True)
+        pairs = [(self.q_idx_in, q_idx), (self.q_in, q), (self.rows_in, new_rows)]
+        if isinstance(accepted, torch.Tensor) and accepted.is_cuda:
+            pairs.append((self.accept_in, accepted))
+        else:
+            self.accept_in.copy_(torch.as_tensor(accepted, dtype=torch.int32), non_blocking=True)
+        _lib.copy_many(pairs)
         self.graph.replay()
         self.history += m
         return self.out, self.lse
