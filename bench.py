@@ -639,9 +639,7 @@ def run_ours(args, cfg):
             # MTP = 2, accept 1.7 (the paper's Table 2 32K setting) on the same shapes,
             # beside its all-HBM ceiling (rho = 1, nothing to gather)
             m = measure_mtp(args, cfg, dev, mtp=2, mean_accept=1.7)
-            mc = measure_mtp(args, cfg, dev, mtp=2, mean_accept=1.7, rho=1.0)
-            m["all_hbm_ceiling"] = {"value": mc["value"], "ms_per_step": mc["ms_per_step"],
-                                    "hit_rate": mc["hit_rate"], "frac_of_ceiling": m["value"] / mc["value"]}
+            m["all_hbm_ceiling"] = mtp_ceiling(args, cfg, dev, m)
             subs["c2_mtp2"] = m
         lo = argparse.Namespace(**{**vars(args), "e2e": False})
         subs[f"{cfg['name']}_drift_0.9"] = measure(lo, cfg, dev, rank, world, agg_dev, 0.9, False, peaks,
@@ -786,6 +784,17 @@ def run_model(args, cfg):
         dist.destroy_process_group()
 
 
+def mtp_ceiling(args, cfg, dev, m):
+    """The MTP step's all-HBM ceiling: every schedule at rho = 1, the fastest (strict)."""
+    runs = {s: measure_mtp(args, cfg, dev, mtp=m["mtp"], mean_accept=1.7, rho=1.0, overlap=s)
+            for s in ("none", "da", "dba")}
+    best = min(runs, key=lambda s: runs[s]["ms_per_step"])
+    mc = runs[best]
+    return {"value": mc["value"], "ms_per_step": mc["ms_per_step"], "hit_rate": mc["hit_rate"],
+            "schedule": best, "schedules_us": {s: round(r["ms_per_step"] * 1e3, 1) for s, r in runs.items()},
+            "frac_of_ceiling": m["value"] / mc["value"]}
+
+
 def measure_mtp(args, cfg, dev, mtp=2, mean_accept=1.7, rho=None, overlap="dba", seed=4321):
     """The MTP decode step (MTPDecodeLayer: mtp + 1 query tokens per request; the paper's
     Table 2 setting MTP = 2, accept 1.7 at 32K): graph replays with
@@ -816,7 +825,7 @@ def measure_mtp(args, cfg, dev, mtp=2, mean_accept=1.7, rho=None, overlap="dba",
     inputs = [layer.next_queries(None if t == 0 else acc_h[t - 1]) for t in range(total)]
     rows = [random_latent_rows(B * Q, dev, layer.gen).view(B, Q, 656) for _ in range(total)]
     acc_d = [torch.from_numpy(a).to(dev) for a in acc_h]
-    layer.capture(overlap if rho < 1.0 else "none", args.gather_ctas, accepted=acc_h[0])
+    layer.capture(overlap, args.gather_ctas, accepted=acc_h[0])
     for t in range(1, W):
         layer.step(inputs[t][0], inputs[t][1], rows[t], acc_d[t], max_accepted=int(acc_h[t].max()))
     torch.cuda.synchronize()
@@ -837,7 +846,7 @@ def measure_mtp(args, cfg, dev, mtp=2, mean_accept=1.7, rho=None, overlap="dba",
            "verified_tokens_per_s": B * Q / (ms * 1e-3), "mtp": mtp, "mean_accept_drawn": accepted / (B * K),
            "batch_per_gpu": B, "context_len": ctx, "sparse_ratio": rho,
            "hit_rate": hits / max(1, hits + misses), "misses_per_request_step": misses / (B * K),
-           "gpu_launches": layer.launches_per_step(overlap if rho < 1.0 else "none") * K,
+           "gpu_launches": layer.launches_per_step(overlap) * K, "schedule": overlap,
            "clocks": clocks.summary()}
     # the idempotent kernels alone on the last step's buffers (K1: the MTP indexer reads
     # each request's keys once; K2: B * qtok rows; K5: B * qtok query rows)
@@ -870,26 +879,29 @@ def measure_mtp(args, cfg, dev, mtp=2, mean_accept=1.7, rho=None, overlap="dba",
 
 def run_ceiling(args, cfg, dev):
     """Same kernels with the whole latent cache in HBM (rho = 1, full history preloaded):
-    every selection hits and the gather moves nothing (SURVEY §8d ceiling).  It runs the
-    sequential schedule, the fastest one when there is nothing to overlap (the DBA
-    split only pays when a gather has to hide), so the ceiling is the strict one."""
+    every selection hits and the gather moves nothing (SURVEY §8d ceiling).  Every
+    schedule is timed and the fastest is the ceiling (the strict one); all timings are
+    reported in ``schedules_us``."""
     import torch
     from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows
     B = cfg["batch"]
     lens = request_lengths(cfg, B, seed=int(os.environ.get("RANK", "0")))
     L = lens if not isinstance(cfg["context_len"], int) else cfg["context_len"]
     total = args.warmup + args.steps
-    layer = DSADecodeLayer(B, L, 1.0, TOPK, max_new_tokens=2 * total + 8, device=dev, seed=99,
+    layer = DSADecodeLayer(B, L, 1.0, TOPK, max_new_tokens=4 * total + 8, device=dev, seed=99,
                            drift=args.drift)
     layer.gather_ctas = args.gather_ctas
     layer.preload_full_history()
     inputs = [layer.next_queries() for _ in range(total)]
     new_rows = [random_latent_rows(B, dev, layer.gen).view(B, 1, 656) for _ in range(total)]
-    # all-HBM: nothing to gather, so the sequential step is one candidate; the streamed
-    # step (K1 || K2 as concurrent grids) is the other when its preconditions hold — the
-    # ceiling is the faster of the two (strict)
-    schedules = ["none"] + (["stream"] if layer.stream_ok() else [])
-    best = None
+    # all-HBM: nothing to gather, but the overlapped schedules still overlap attention
+    # with the top-k / cache manager of other requests, so every schedule is a candidate
+    # and the ceiling is the fastest (strict): sequential, DA, DBA (the config's split)
+    # and, when its preconditions hold, the streamed step
+    schedules = ["none", "da", "dba"] + (["stream"] if layer.stream_ok() else [])
+    best, measured = None, {}
+    layer.micro = cfg["micro"]
+    layer.first_frac = cfg["first"]
     for sched in schedules:
         layer.capture(sched, args.gather_ctas)
         for t in range(1, args.warmup):
@@ -904,10 +916,11 @@ def run_ceiling(args, cfg, dev):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.steps
         c = [x - y for x, y in zip(layer.access_totals(), (hits0, misses0))]
+        measured[sched] = round(ms * 1e3, 1)
         if best is None or ms < best["ms_per_step"]:
             best = {"value": B / (ms * 1e-3), "unit": "tokens/s", "ms_per_step": ms,
                     "hit_rate": c[0] / max(1, c[0] + c[1]), "schedule": sched}
-        best.setdefault("schedules_us", {})[sched] = ms * 1e3
+    best["schedules_us"] = measured
     layer.pool.check("ceiling")
     layer.close()
     return best
@@ -957,9 +970,7 @@ def main():
         dev = torch.device("cuda", 0)
         torch.cuda.set_device(dev)
         m = measure_mtp(args, cfg, dev, mtp=2, mean_accept=1.7)
-        mc = measure_mtp(args, cfg, dev, mtp=2, mean_accept=1.7, rho=1.0)
-        m["all_hbm_ceiling"] = {"value": mc["value"], "ms_per_step": mc["ms_per_step"],
-                                "frac_of_ceiling": m["value"] / mc["value"]}
+        m["all_hbm_ceiling"] = mtp_ceiling(args, cfg, dev, m)
         print(json.dumps(m), flush=True)
     elif args.impl == "reference":
         run_reference(args, cfg)
