@@ -522,7 +522,7 @@ def measure(args, cfg, dev, rank, world, agg_dev, drift, full, peaks, peak_kind,
            "slot_store_gb": layer.pool.num_pools * layer.pool.rows_per_pool * layer.pool.row_bytes / 1e9,
            "misses_per_request_step": misses / (B * K), "clocks": clocks.summary(),
            "gpu_launches": layer.launches_per_step(args.overlap) * K,
-           "micro_batches": layer.micro_batches(layer.micro) if args.overlap == "dba" else [(0, B)],
+           "micro_batches": layer.micro_batches(layer.micro) if args.overlap in ("dba", "dbs") else [(0, B)],
            "context_len": cfg["context_len"] if isinstance(cfg["context_len"], int)
            else "mixed {}-{} log-uniform, mean {:.0f}".format(*cfg["context_len"], sum(lens) / B)}
     # Eq. (1) selection similarity r over 4 more (untimed) steps
@@ -897,8 +897,8 @@ def run_ceiling(args, cfg, dev):
     # all-HBM: nothing to gather, but the overlapped schedules still overlap attention
     # with the top-k / cache manager of other requests, so every schedule is a candidate
     # and the ceiling is the fastest (strict): sequential, DA, DBA (the config's split)
-    # and, when its preconditions hold, the streamed step
-    schedules = ["none", "da", "dba"] + (["stream"] if layer.stream_ok() else [])
+    # and, when their preconditions hold, the streamed ones (dbs, stream)
+    schedules = ["none", "da", "dba"] + (["dbs", "stream"] if layer.stream_ok() else [])
     best, measured = None, {}
     layer.micro = cfg["micro"]
     layer.first_frac = cfg["first"]
@@ -935,7 +935,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--drift", type=float, default=0.97)
     ap.add_argument("--gather-ctas", type=int, default=32)
-    ap.add_argument("--overlap", default="dba", choices=["dba", "da", "none", "stream"])
+    ap.add_argument("--overlap", default="dba", choices=["dba", "dbs", "da", "none", "stream"])
     ap.add_argument("--micro", type=int, default=None, help="DBA micro-batches per step (default: per config)")
     ap.add_argument("--first", type=float, default=None,
                     help="DBA: fraction of the batch in the first micro-batch (default: per config)")

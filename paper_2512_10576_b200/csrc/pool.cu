@@ -1202,7 +1202,7 @@ __global__ void __launch_bounds__(NTG) gather_stream_kernel(PoolView pv, int beg
       __syncwarp();
       if (lane == 0) ess_red_release_add(landed + b, nr);
     }
-    if (lane == 0) SPROF_MAX(b, 2);
+    if (lane == 0) SPROF_MAX(begin + b, 2);
   }
 }
 

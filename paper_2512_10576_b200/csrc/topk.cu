@@ -578,14 +578,14 @@ __global__ void __launch_bounds__(NT, 1)
     __syncthreads();  // the previous row's shared-memory readers are done
     if (threadIdx.x < 32) ess_warp_wait_geq(done + b, (int)min((int64_t)lens[b], ld));
     __syncthreads();
-    if (threadIdx.x == 0) SPROF(b, 0);
+    if (threadIdx.x == 0) SPROF(sp.prof_base + b, 0);
     topk_row<CLN, true>(b, logits, ld, lens, k, out, out_ld, counts, sp);
     __threadfence();  // this thread's selection / split outputs, before the flag
     if constexpr (CLN > 1) cg::this_cluster().sync();  // every rank's part (rank 0 split)
     else __syncthreads();
     if (threadIdx.x == 0 && (CLN == 1 || cg::this_cluster().block_rank() == 0)) {
       ess_st_release(ready + b, 1);
-      SPROF(b, 1);
+      SPROF(sp.prof_base + b, 1);
     }
   }
 }
@@ -739,6 +739,7 @@ extern "C" int ess_topk_split_stream(const float *d_logits, int64_t ld, const in
   sp.miss_row = d_miss_row;
   sp.counts = d_counts;
   sp.out_stride = out_stride;
+  sp.prof_base = pool_begin;
   // cluster size per row: the smallest whose slice fits shared memory (rows > 40K tokens
   // take 2-8 CTAs, as ess_topk); ctas < 0 forces at least CTA pairs.  `ctas` counts rows
   // worked on at once (clusters).

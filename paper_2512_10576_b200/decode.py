@@ -265,8 +265,14 @@ class DSADecodeLayer:
             gather(self.pool, self.store, acc, max_ctas=gather_ctas)
             sparse_mla(self.pool, q, acc.sel_row, self.cnt, self.sm_scale, out=self.out, lse=self.lse)
             return self.out, self.lse
-        if overlap not in ("da", "dba"):
+        if overlap not in ("da", "dba", "dbs"):
             raise ValueError(f"unknown overlap schedule {overlap!r}")
+        # dbs: DBA whose later micro-batches are handed on per request (streamed K1 ->
+        # K2+K3a -> K4 as in overlap="stream"), so their first misses reach the link
+        # while the micro-batch's indexer still runs
+        dbs = overlap == "dbs"
+        if dbs and not self.stream_ok():
+            raise ValueError("the dbs schedule needs early gather, rows <= 40K tokens per CTA and the fused DA")
         main = torch.cuda.current_stream(self.device)
         if getattr(self, "_side", None) is None:
             self._side = torch.cuda.Stream(self.device, priority=-1)
@@ -285,7 +291,16 @@ class DSADecodeLayer:
         gsms = max(8, sms - 2 * B * split)
         if split > 1 and getattr(self, "_ws_split", None) is None:
             self._ws_split = SplitWorkspace(B, self.device, splits=split)
-        ranges = self.micro_batches(micro if overlap == "dba" else 1)
+        ranges = self.micro_batches(micro if overlap in ("dba", "dbs") else 1)
+        if dbs:
+            if getattr(self, "_sync", None) is None:
+                self._sync = torch.zeros(3 * B, dtype=torch.int32, device=self.device)  # done | ready | claim
+            self._sync.zero_()
+            done_c, ready_c, claim_c = self._sync[:B], self._sync[B:2 * B], self._sync[2 * B:]
+            cln = 1  # CTAs per streamed top-k row (rows > 40K tokens take a cluster)
+            while cln < 8 and -(-self.Lmax // cln) > 40 * 1024:
+                cln *= 2
+            nk2 = min(B, self.stream_topk_ctas)
         if getattr(self, "_sel", None) is None:
             self._sel = torch.cuda.Stream(self.device)
             self._lru = torch.cuda.Stream(self.device)
@@ -303,6 +318,14 @@ class DSADecodeLayer:
             ctas = 0 if i == 0 else sms - g_prev - prev
             if i > 0 and self.late_k1_ctas:  # cap: less HBM pressure beside the gather
                 ctas = min(ctas, self.late_k1_ctas)
+            if dbs and i > 0:
+                self._attend_dbs_mb(q_idx, a, b, sms - g_prev - max(prev, nk2 * cln), nk2, cln, g_i,
+                                    done_c, ready_c, claim_c, fused)
+                ready, fetched = self._dbs_selected, self._dbs_fetched
+                self._lru_mb(a, b, ready, fetched)
+                lru_ready = self._lru_ready
+                prev = nk2 * cln
+                continue
             indexer_logits(q_idx[a:b], self.w[a:b], self.k_cache[a:b], self.k_scale[a:b],
                            self.lens[a:b], out=self.logits[a:b], max_ctas=ctas)
             scored = torch.cuda.Event()
@@ -326,18 +349,8 @@ class DSADecodeLayer:
                 fetched = torch.cuda.Event()
                 fetched.record(side)
             if self.early_gather:
-                # K3b (the LRU update proper, reporting each miss's final slot) and the
-                # settle (staging -> final slots, after the gather) on their own stream, so
-                # neither delays the next micro-batch's selection or gather
-                lru.wait_event(ready)
-                with torch.cuda.stream(lru):
-                    self.pool.access(self.idx[a:b], self.cnt[a:b], begin=a, out=AccessBatch(
-                        counts=self._counts_b[a:b], sel_row=None, miss_ids=None,
-                        miss_row=self._settle[a:b], hit_row=None))
-                    lru_ready = torch.cuda.Event()
-                    lru_ready.record(lru)
-                    lru.wait_event(fetched)
-                    self.pool.settle(self._settle[a:b], self.acc.counts[a:b], begin=a)
+                self._lru_mb(a, b, ready, fetched)
+                lru_ready = self._lru_ready
             else:
                 lru_ready = ready
             prev = b - a
@@ -374,6 +387,50 @@ class DSADecodeLayer:
         if new_rows is not None:
             main.wait_event(admitted)
         return self.out, self.lse
+
+    def _lru_mb(self, a, b, ready, fetched) -> None:
+        """K3b (the LRU update proper, reporting each miss's final slot) and the settle
+        (staging -> final slots, after the gather) of requests [a, b) on their own stream,
+        so neither delays the next micro-batch's selection or gather."""
+        lru = self._lru
+        lru.wait_event(ready)
+        with torch.cuda.stream(lru):
+            self.pool.access(self.idx[a:b], self.cnt[a:b], begin=a, out=AccessBatch(
+                counts=self._counts_b[a:b], sel_row=None, miss_ids=None,
+                miss_row=self._settle[a:b], hit_row=None))
+            self._lru_ready = torch.cuda.Event()
+            self._lru_ready.record(lru)
+            lru.wait_event(fetched)
+            self.pool.settle(self._settle[a:b], self.acc.counts[a:b], begin=a)
+
+    def _attend_dbs_mb(self, q_idx, a, b, k1_ctas, nk2, cln, g, done, ready, claim, fused) -> None:
+        """One later micro-batch of the dbs schedule: its indexer (main stream) counts each
+        request's stored logits rows, a persistent top-k + split grid (selection stream,
+        after the previous micro-batch's top-k) starts each row once complete and
+        publishes it, and a persistent gather (side stream, after the previous gather)
+        fetches each published miss list.  Progress: the indexer waits on nothing, so
+        its CTAs always finish and free SMs for any not yet resident; the waiting grids
+        take nk2 * cln + g SMs."""
+        main, sel, side = torch.cuda.current_stream(self.device), self._sel, self._side
+        acc = self._acc_view(a, b)
+        # the top-k grid runs BESIDE this indexer: it waits only for what precedes it on
+        # the main stream (the zeroed counters, the previous indexer), not for it
+        before = torch.cuda.Event()
+        before.record(main)
+        indexer_logits_stream(q_idx[a:b], self.w[a:b], self.k_cache[a:b], self.k_scale[a:b], self.lens[a:b],
+                              self.logits[a:b], done[a:b], self.stream_group | (self.stream_first << 16),
+                              max(8, k1_ctas))
+        sel.wait_event(before)
+        with torch.cuda.stream(sel):
+            topk_split_stream(self.logits[a:b], self.lens[a:b], self.K, self.idx[a:b], self.cnt[a:b],
+                              self.pool, acc, done[a:b], ready[a:b], nk2, begin=a)
+            self._dbs_selected = torch.cuda.Event()
+            self._dbs_selected.record(sel)
+        with torch.cuda.stream(side):
+            gather_stream(self.pool, self.store, acc, ready[a:b], claim[a:b],
+                          self._landed[a:b] if fused else None, begin=a, max_ctas=g)
+            self._dbs_fetched = torch.cuda.Event()
+            self._dbs_fetched.record(side)
 
     def stream_ok(self) -> bool:
         """The streamed schedule's preconditions: early gather (every pool holds a whole
@@ -474,7 +531,7 @@ class DSADecodeLayer:
         # a smaller pool keeps part of the selection in rows the admission may evict
         # (capacity only grows with history, so this holds for every later replay)
         hist_min = min(self.ctx_lens) + self.history - self.ctx
-        early = overlap in ("da", "dba", "stream") and math.floor(self.rho * hist_min) > self.K
+        early = overlap in ("da", "dba", "dbs", "stream") and math.floor(self.rho * hist_min) > self.K
         self.attend(self.q_idx_in, self.q_in, gather_ctas=gather_ctas, overlap=overlap,
                     new_rows=self.rows_in if early else None, micro=self.micro)
         if not early:
@@ -490,7 +547,7 @@ class DSADecodeLayer:
         if overlap == "stream":  # K1, K2+K3a, K4, K3b, settle, K5 (+ combine), admission
             split = max(1, min(self.max_split, (sms - 8 - self.stream_gather_ctas) // (2 * self.B)))
             return 7 + (split > 1)
-        micro = self.micro if overlap == "dba" else 1
+        micro = self.micro if overlap in ("dba", "dbs") else 1
         # early gather: K2 + K3a fused, + K3b, settle
         per_mb = 5 if self.early_gather else 4
         sms = torch.cuda.get_device_properties(self.device).multi_processor_count

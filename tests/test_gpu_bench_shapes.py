@@ -53,6 +53,15 @@ def test_c2_streamed_step_matches_oracle_chain():
     _run("c2", attn_sample=(0, 7, 8, 40, 63), logit_sample=(0,), overlap="stream")
 
 
+def test_c2_dbs_step_matches_oracle_chain():
+    """DBA with the second micro-batch handed on per request (bench.py --overlap dbs)."""
+    _run("c2", attn_sample=(0, 15, 16, 17, 63), logit_sample=(0,), overlap="dbs")
+
+
+def test_c4_dbs_step_matches_oracle_chain():
+    _run("c4", attn_sample=(0, 12, 37, 38, 63), logit_sample=(), steps=2, overlap="dbs")
+
+
 def test_c4_benchmarked_step_matches_oracle_chain():
     ranges = _run("c4", attn_sample=(0, 11, 12, 37, 38, 63), logit_sample=(5,), steps=2)
     assert ranges == [(0, 12), (12, 38), (38, 64)]
@@ -62,9 +71,11 @@ def test_c5_benchmarked_step_matches_oracle_chain():
     _run("c5", attn_sample=(0, 23, 24, 63), logit_sample=(), steps=2)
 
 
-def test_all_hbm_ceiling_step_matches_oracle_chain():
-    """The ceiling the bench divides by (rho = 1, whole history resident, sequential
-    schedule): every selection hits, nothing is gathered, and the results are the same
+@pytest.mark.parametrize("sched", ["none", "da"])
+def test_all_hbm_ceiling_step_matches_oracle_chain(sched):
+    """The ceiling the bench divides by (rho = 1, whole history resident; bench.py takes
+    the fastest schedule — DA at C2 — so both the sequential and the DA step are
+    checked): every selection hits, nothing is gathered, and the results are the same
     as the offloaded step's oracle chain."""
     import bench
     from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows
@@ -77,7 +88,7 @@ def test_all_hbm_ceiling_step_matches_oracle_chain():
         for o in chain.orc:  # the oracle pools hold the whole history too
             for c0 in range(0, L, 2048):
                 o.warmup([list(range(c0, min(L, c0 + 2048)))])
-        eager = layer.capture("none", 32)
+        eager = layer.capture(sched, 32)
         chain.mirror(counts=eager)
         for _ in range(2):
             q_idx, q = layer.next_queries()

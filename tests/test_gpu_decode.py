@@ -15,7 +15,8 @@ pytestmark = pytest.mark.gpu
 @pytest.mark.parametrize("ctx,rho,fuse,overlap", [(8192, 0.25, True, "dba"), (4096, 0.25, True, "dba"),
                                                   (8192, 0.25, False, "dba"), (8192, 0.25, True, "da"),
                                                   (8192, 0.25, True, "none"), (8192, 0.25, True, "stream"),
-                                                  (32768, 0.25, True, "stream"), (131072, 0.1, True, "stream")])
+                                                  (32768, 0.25, True, "stream"), (131072, 0.1, True, "stream"),
+                                                  (8192, 0.25, True, "dbs"), (131072, 0.1, True, "dbs")])
 def test_decode_layer_matches_oracle_chain(ctx, rho, fuse, overlap):
     """fuse: the DA schedule as one K5 launch waiting on the gather's arrival counters
     (sparse_mla_da) vs. two K5 passes merged through the workspace."""
@@ -63,7 +64,7 @@ def test_decode_layer_matches_oracle_chain(ctx, rho, fuse, overlap):
 
 
 @pytest.mark.parametrize("overlap,micro,B", [("dba", 2, 4), ("dba", 3, 4), ("da", 1, 4), ("dba", 2, 40),
-                                             ("stream", 1, 4), ("stream", 1, 40)])
+                                             ("stream", 1, 4), ("stream", 1, 40), ("dbs", 2, 4), ("dbs", 3, 40)])
 def test_graph_step_with_overlap_matches_oracle_chain(overlap, micro, B):
     """The product step — two micro-batches, gathers on a side stream, whole step
     captured as a CUDA graph, history/capacity computed on device — stays bit-exact
