@@ -70,6 +70,13 @@ extern "C" {
                                   outside the f16 range (|x| >= 65520): latched, the
                                   output of that launch is not valid                  */
 
+/* Launch flag (OR-ed into ess_indexer_logits_ex's max_ctas, ess_gather(_signal)'s flags,
+ * ess_topk_split_ex's flags): programmatic dependent launch — the kernel may start while
+ * the previous kernel on the same stream is finishing (its prologue and launch latency
+ * hide under that kernel's tail) and waits on the device for it to complete before
+ * reading its outputs (griddepcontrol).  For back-to-back dependent launches on one
+ * stream, e.g. the first micro-batch's K1 -> K2 + K3a -> K4 chain. */
+#define ESS_LAUNCH_PDL (1 << 30)
 #define ESS_CLOCK_BASE (1u << 24)   /* recency stamps start here; free slots key = slot index */
 
 #define ESS_ACCESS_SORT_EVICTED 1 /* emit evicted ids sorted ascending (cache.py:120) */
@@ -211,6 +218,7 @@ int ess_pool_info(ess_pool *pool, int32_t *num_pools, int64_t *max_ids, int32_t 
 #define ESS_GATHER_EXCLUSIVE_SM 1        /* run only on SMs no attention CTA occupies */
 #define ESS_GATHER_EXCLUSIVE_SMEM (64 * 1024)
 #define ESS_GATHER_BULK 2                /* rows via cp.async.bulk into a smem ring, not 16-B loads */
+/* flags may also carry ESS_LAUNCH_PDL (ess_gather / ess_gather_signal) */
 int ess_gather(ess_pool *pool, int32_t begin, int32_t num, const void *d_host_rows,
                int64_t host_pool_stride_rows, const int32_t *d_miss_ids,
                const int32_t *d_miss_row, const int32_t *d_counts, int32_t stride,
@@ -246,7 +254,8 @@ int ess_indexer_logits(const void *d_q, const float *d_w, const void *d_k,
                        const float *d_kscale, const int32_t *d_len, int32_t batch,
                        int64_t k_ld, float *d_logits, void *stream);
 /* same, on at most max_ctas SMs (0 = all): leaves SMs free for a concurrent
- * host-link gather (the DBA micro-batch schedule) */
+ * host-link gather (the DBA micro-batch schedule); max_ctas may carry
+ * ESS_LAUNCH_PDL (K1 reads only its inputs, so it never waits for the previous kernel) */
 int ess_indexer_logits_ex(const void *d_q, const float *d_w, const void *d_k,
                           const float *d_kscale, const int32_t *d_len, int32_t batch,
                           int64_t k_ld, float *d_logits, int32_t max_ctas, void *stream);
@@ -295,6 +304,12 @@ int ess_topk_split(const float *d_logits, int64_t ld, const int32_t *d_len, int3
                    int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count, ess_pool *pool,
                    int32_t pool_begin, int32_t *d_hit_row, int32_t *d_miss_ids,
                    int32_t *d_miss_row, int32_t *d_counts, int32_t out_stride, void *stream);
+/* same with launch flags (ESS_LAUNCH_PDL) */
+int ess_topk_split_ex(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch,
+                      int32_t k, int32_t *d_idx, int32_t idx_ld, int32_t *d_count, ess_pool *pool,
+                      int32_t pool_begin, int32_t *d_hit_row, int32_t *d_miss_ids,
+                      int32_t *d_miss_row, int32_t *d_counts, int32_t out_stride, int32_t flags,
+                      void *stream);
 
 /* Streamed K2 + K3a: `ctas` persistent CTAs (ctas < 0: -ctas two-CTA clusters, one row
  * per pair) take the requests in order; row b starts

@@ -60,6 +60,7 @@ SIGNATURES = {
     "ess_topk": ([V, I64, V, I32, I32, V, I32, V, V], ctypes.c_int),
     "ess_topk_mtp": ([V, I64, V, I32, I32, I32, V, I32, V, V], ctypes.c_int),
     "ess_topk_split": ([V, I64, V, I32, I32, V, I32, V, V, I32, V, V, V, V, I32, V], ctypes.c_int),
+    "ess_topk_split_ex": ([V, I64, V, I32, I32, V, I32, V, V, I32, V, V, V, V, I32, I32, V], ctypes.c_int),
     "ess_sparse_mla": ([V, I32, V, V, I32, V, I32, I32, F32, V, V, V, V, I32, V], ctypes.c_int),
     "ess_sparse_mla_da": ([V, I32, V, V, V, I32, V, I32, V, I32, F32, V, V, V], ctypes.c_int),
     "ess_sparse_mla_da_split": ([V, I32, V, V, V, I32, V, I32, V, I32, F32, V, V, V, V, I32, V],
@@ -77,6 +78,7 @@ ESS_MLA_QTOK_SHIFT = 12
 MAX_QTOK = 4  # ESS_INDEXER_MAX_QTOK: query tokens per request and step (MTP width + 1)
 ESS_GATHER_EXCLUSIVE_SM = 1
 ESS_GATHER_BULK = 2
+ESS_LAUNCH_PDL = 1 << 30
 ESS_HOST_HUGEPAGES, ESS_HOST_NUMA_BOUND = 1, 2
 MAX_REQUEST = 2048
 LATENT_ROW_BYTES = 656   # host store / transfer format (e4m3 NoPE + scales + bf16 RoPE)

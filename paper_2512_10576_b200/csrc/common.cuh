@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/ess_b200.h"
 
 #define ESS_CUDA_TRY(expr)                                  \
@@ -151,6 +153,44 @@ __device__ __forceinline__ void ess_red_release_add(int32_t *p, int v) {
 }
 __device__ __forceinline__ void ess_st_release(int32_t *p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Programmatic dependent launch (ESS_LAUNCH_PDL): a kernel launched with programmatic
+// stream serialization may start before the previous kernel on its stream completes —
+// its CTAs become resident as the previous kernel's CTAs leave the SMs — and waits
+// with ess_pdl_wait() until that kernel has completed and its stores are visible.
+// ess_pdl_trigger() lets the NEXT kernel launch early.  Both are no-ops in a kernel
+// launched without the attribute.
+__device__ __forceinline__ void ess_pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void ess_pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+// Launch with optional thread-block cluster (cluster > 1) and programmatic stream
+// serialization (pdl).
+template <typename... KArgs, typename... Args>
+inline cudaError_t ess_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t stream, int cluster, bool pdl, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (cluster > 1) {
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = (unsigned)cluster;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    n++;
+  }
+  if (pdl) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    n++;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 // Bounded mbarrier / flag spin: trap instead of hanging the GPU on a protocol bug.

@@ -189,6 +189,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
   typename C::Ctrl &c = *reinterpret_cast<typename C::Ctrl *>(qbuf + 2 * QT_BYTES);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) K1PROF(0);
+  ess_pdl_trigger();  // a PDL-launched consumer (K2 + K3a) may take the SMs K1 leaves
 
   // unit prefix over requests (every CTA computes it): warp 0, 32 requests per round
   // (a serial loop of dependent-latency loads cost ~27 ns per request)
@@ -507,11 +508,12 @@ int launch_indexer(const void *d_q, const float *d_w, const void *d_k, const flo
   if (!make_map(&tk, d_k, (uint64_t)batch * (uint64_t)k_ld, TILE_M, kc)) return ESS_ERR_CUDA;
   if (!make_map(&tq, d_q, (uint64_t)batch * C::N, C::N, qc)) return ESS_ERR_CUDA;
   if (int rc = ess_smem_optin((const void *)indexer_kernel<QT>, C::SMEM_BYTES)) return rc;
+  const bool pdl = (max_ctas & ESS_LAUNCH_PDL) != 0;
+  max_ctas &= ~ESS_LAUNCH_PDL;
   const int ctas = max_ctas > 0 && max_ctas < ess_sm_count() ? max_ctas : ess_sm_count();
-  indexer_kernel<QT><<<ctas, NTHREADS, C::SMEM_BYTES, (cudaStream_t)stream>>>(
-      tk, tq, d_w, d_kscale, d_len, batch, k_ld, d_logits,
-      (group & 0xFFFF) ? group : ((group & ~0xFFFF) | (batch & 0xFFFF)), d_done);
-  ESS_CUDA_TRY(cudaGetLastError());
+  ESS_CUDA_TRY(ess_launch(indexer_kernel<QT>, dim3(ctas), dim3(NTHREADS), C::SMEM_BYTES, (cudaStream_t)stream,
+                          1, pdl, tk, tq, d_w, d_kscale, d_len, (int)batch, k_ld, d_logits,
+                          (int)((group & 0xFFFF) ? group : ((group & ~0xFFFF) | (batch & 0xFFFF))), d_done));
   return ESS_OK;
 }
 

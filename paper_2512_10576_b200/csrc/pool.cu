@@ -1046,6 +1046,8 @@ __global__ void __launch_bounds__(NTG) gather_kernel(PoolView pv, int begin, int
                                                      int stride, int32_t *landed) {
   extern __shared__ int pref[];  // [num + 1]
   __shared__ int wbuf[NTG / 32];
+  ess_pdl_trigger();
+  ess_pdl_wait();  // PDL-launched: the split's miss lists complete and visible
   int run = 0;
   for (int c0 = 0; c0 < num; c0 += NTG) {
     int i = c0 + threadIdx.x;
@@ -1741,12 +1743,13 @@ int ess_gather_signal(ess_pool *p, int32_t begin, int32_t num, const void *d_hos
   // attention leaves idle.
   if ((flags & ESS_GATHER_EXCLUSIVE_SM) && smem < ESS_GATHER_EXCLUSIVE_SMEM)
     smem = ESS_GATHER_EXCLUSIVE_SMEM;
+  if (bulk && (flags & ESS_LAUNCH_PDL)) return ESS_ERR_ARG;  // the bulk form has no PDL wait
   auto kern = bulk ? gather_bulk_kernel : gather_kernel;
   if (int rc = ess_smem_optin((const void *)kern, smem)) return rc;
-  kern<<<max_ctas, NTG, smem, (cudaStream_t)stream>>>(
-      view(p), begin, num, (const uint8_t *)d_host_rows, host_pool_stride_rows, d_miss_ids,
-      d_miss_row, d_counts, stride, d_landed);
-  ESS_CUDA_TRY(cudaGetLastError());
+  ESS_CUDA_TRY(ess_launch(kern, dim3(max_ctas), dim3(NTG), smem, (cudaStream_t)stream, 1,
+                          (flags & ESS_LAUNCH_PDL) != 0, view(p), (int)begin, (int)num,
+                          (const uint8_t *)d_host_rows, host_pool_stride_rows, d_miss_ids, d_miss_row,
+                          d_counts, (int)stride, d_landed));
   return ESS_OK;
 }
 

@@ -560,6 +560,8 @@ __global__ void __launch_bounds__(NT, 1)
     topk_kernel(const float *__restrict__ logits, int64_t ld, const int32_t *__restrict__ lens,
                 int k, int32_t *__restrict__ out, int out_ld, int32_t *__restrict__ counts,
                 SplitArgs sp) {
+  ess_pdl_trigger();  // a PDL-launched consumer (the gather) may become resident now
+  ess_pdl_wait();     // PDL-launched: the indexer's logits complete and visible
   topk_row<CLN, false>(blockIdx.x / CLN, logits, ld, lens, k, out, out_ld, counts, sp);
 }
 
@@ -593,26 +595,14 @@ __global__ void __launch_bounds__(NT, 1)
 template <int CLN>
 int launch_topk(const float *d_logits, int64_t ld, const int32_t *d_len, int32_t batch, int32_t k,
                 int32_t *d_idx, int32_t idx_ld, int32_t *d_count, cudaStream_t stream,
-                SplitArgs sp = SplitArgs{}) {
+                SplitArgs sp = SplitArgs{}, bool pdl = false) {
   const size_t smem = (size_t)slice_cap<CLN>(ld) * sizeof(uint32_t) + (LCAP + NT) * sizeof(uint16_t);
   // per (instantiation, device): opt in to the largest slice
   if (int rc = ess_smem_optin((const void *)topk_kernel<CLN>,
                               SLICE_MAX * sizeof(uint32_t) + (LCAP + NT) * sizeof(uint16_t)))
     return rc;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)batch * CLN);
-  cfg.blockDim = dim3(NT);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = CLN;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  ESS_CUDA_TRY(cudaLaunchKernelEx(&cfg, topk_kernel<CLN>, d_logits, ld, d_len, (int)k, d_idx,
-                                  (int)idx_ld, d_count, sp));
+  ESS_CUDA_TRY(ess_launch(topk_kernel<CLN>, dim3((unsigned)batch * CLN), dim3(NT), smem, stream, CLN, pdl,
+                          d_logits, ld, d_len, (int)k, d_idx, (int)idx_ld, d_count, sp));
   return ESS_OK;
 }
 
@@ -679,6 +669,17 @@ extern "C" int ess_topk_split(const float *d_logits, int64_t ld, const int32_t *
                               int32_t *d_count, ess_pool *pool, int32_t pool_begin,
                               int32_t *d_hit_row, int32_t *d_miss_ids, int32_t *d_miss_row,
                               int32_t *d_counts, int32_t out_stride, void *stream) {
+  return ess_topk_split_ex(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, pool, pool_begin,
+                           d_hit_row, d_miss_ids, d_miss_row, d_counts, out_stride, 0, stream);
+}
+
+extern "C" int ess_topk_split_ex(const float *d_logits, int64_t ld, const int32_t *d_len,
+                                 int32_t batch, int32_t k, int32_t *d_idx, int32_t idx_ld,
+                                 int32_t *d_count, ess_pool *pool, int32_t pool_begin,
+                                 int32_t *d_hit_row, int32_t *d_miss_ids, int32_t *d_miss_row,
+                                 int32_t *d_counts, int32_t out_stride, int32_t flags, void *stream) {
+  if (flags & ~ESS_LAUNCH_PDL) return ESS_ERR_ARG;
+  const bool pdl = (flags & ESS_LAUNCH_PDL) != 0;
   if (!pool || pool_begin < 0 || (int64_t)pool_begin + batch > pool->P || !d_hit_row ||
       !d_miss_ids || !d_miss_row || !d_counts || out_stride < 1 || k > 2 * NT ||
       pool->staging < k)
@@ -703,10 +704,10 @@ extern "C" int ess_topk_split(const float *d_logits, int64_t ld, const int32_t *
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
   switch (cln) {
-    case 1: rc = launch_topk<1>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, st, sp); break;
-    case 2: rc = launch_topk<2>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, st, sp); break;
-    case 4: rc = launch_topk<4>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, st, sp); break;
-    default: rc = launch_topk<8>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, st, sp); break;
+    case 1: rc = launch_topk<1>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, st, sp, pdl); break;
+    case 2: rc = launch_topk<2>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, st, sp, pdl); break;
+    case 4: rc = launch_topk<4>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, st, sp, pdl); break;
+    default: rc = launch_topk<8>(d_logits, ld, d_len, batch, k, d_idx, idx_ld, d_count, st, sp, pdl); break;
   }
   if (rc != ESS_OK) return rc;
   ESS_CUDA_TRY(cudaGetLastError());

@@ -89,6 +89,10 @@ class DSADecodeLayer:
         self.min_gather_sms = 20
         self.early_gather_sms = int(os.environ.get("ESS_EARLY_GATHER_SMS", "20"))
         self.late_k1_ctas = int(os.environ.get("ESS_LATE_K1_CTAS", "0"))
+        # DA / DBA: the first micro-batch's K1 -> K2 + K3a (-> K4) as programmatic
+        # dependent launches on one stream
+        self.pdl = os.environ.get("ESS_PDL", "0") == "1"
+        self.pdl_gather = int(os.environ.get("ESS_PDL_K1", "0"))  # 1: the next K1 without PDL
         # streamed schedule (overlap="stream"): request group of the indexer, persistent
         # top-k and gather grid sizes
         self.stream_group = int(os.environ.get("ESS_STREAM_GROUP", "8"))
@@ -306,6 +310,7 @@ class DSADecodeLayer:
             self._lru = torch.cuda.Stream(self.device)
         sel, lru = self._sel, self._lru
         ready = None
+        pdl_next = False  # launch the next indexer programmatically (behind a main-stream gather)
         prev = 0  # requests of the previous micro-batch (its K2/K3 run beside this K1)
         for i, (a, b) in enumerate(ranges):
             # K1 of micro-batch i on the main stream; its top-k and cache manager on the
@@ -327,7 +332,33 @@ class DSADecodeLayer:
                 prev = nk2 * cln
                 continue
             indexer_logits(q_idx[a:b], self.w[a:b], self.k_cache[a:b], self.k_scale[a:b],
-                           self.lens[a:b], out=self.logits[a:b], max_ctas=ctas)
+                           self.lens[a:b], out=self.logits[a:b], max_ctas=ctas, pdl=pdl_next)
+            pdl_next = False
+            if self.pdl and self.early_gather and i == 0:
+                # the first micro-batch's K1 -> K2 + K3a -> K4 chain back to back on the main
+                # stream with programmatic dependent launches: each kernel becomes resident
+                # on the SMs its producer's tail frees and waits on the device, so the first
+                # misses reach the host link without two launch latencies.  With one
+                # micro-batch (DA) the gather stays on the side stream (attention, next on
+                # the main stream, overlaps it).
+                topk_split(self.logits[a:b], self.lens[a:b], self.K, self.idx[a:b], self.cnt[a:b],
+                           self.pool, self._acc_view(a, b), begin=a, pdl=True)
+                ready = torch.cuda.Event()
+                ready.record(main)
+                # the next indexer reads nothing the split writes: it launches beside it.
+                # The gather stays on the side stream — an event recorded after a gather on
+                # the main stream would hold the next micro-batch's top-k until the gather ends.
+                pdl_next = self.pdl_gather == 0
+                side.wait_event(ready)
+                with torch.cuda.stream(side):
+                    gather(self.pool, self.store, self._acc_view(a, b), begin=a, max_ctas=g_i,
+                           exclusive=True, landed=self._landed[a:b] if fused else None)
+                    fetched = torch.cuda.Event()
+                    fetched.record(side)
+                self._lru_mb(a, b, ready, fetched)
+                lru_ready = self._lru_ready
+                prev = b - a
+                continue
             scored = torch.cuda.Event()
             scored.record(main)
             sel.wait_event(scored)
@@ -421,6 +452,7 @@ class DSADecodeLayer:
                               self.logits[a:b], done[a:b], self.stream_group | (self.stream_first << 16),
                               max(8, k1_ctas))
         sel.wait_event(before)
+        side.wait_event(before)  # the zeroed counters (the previous gather may be elsewhere)
         with torch.cuda.stream(sel):
             topk_split_stream(self.logits[a:b], self.lens[a:b], self.K, self.idx[a:b], self.cnt[a:b],
                               self.pool, acc, done[a:b], ready[a:b], nk2, begin=a)

@@ -19,14 +19,16 @@ TOPK = 2048
 
 def indexer_logits(q_fp8: torch.Tensor, w: torch.Tensor, k_cache: torch.Tensor,
                    k_scale: torch.Tensor, lens: torch.Tensor,
-                   out: torch.Tensor | None = None, max_ctas: int = 0) -> torch.Tensor:
+                   out: torch.Tensor | None = None, max_ctas: int = 0, pdl: bool = False) -> torch.Tensor:
     """logits[b, s] = k_scale[b, s] * sum_h w[b, h] * relu(q[b, h] . k[b, s]) for s < lens[b].
 
     q_fp8 [B, 64, 128] and k_cache [B, Lmax, 128] hold e4m3 bytes (uint8 or
     float8_e4m3fn), w [B, 64] f32, k_scale [B, Lmax] f32, lens [B] int32.
     Lmax must be a multiple of 128 and k_cache 16-byte aligned (TMA).
     Entries at s >= lens[b] are left untouched.  ``max_ctas`` > 0 caps the
-    persistent grid (SMs left free for a concurrent gather); 0 = every SM.
+    persistent grid (SMs left free for a concurrent gather); 0 = every SM.  ``pdl``:
+    programmatic dependent launch (ESS_LAUNCH_PDL) behind the previous kernel of the
+    stream, whose results K1 does not read.
     """
     _lib.require_cuda(k_cache)
     if k_cache.dim() != 3:
@@ -46,7 +48,8 @@ def indexer_logits(q_fp8: torch.Tensor, w: torch.Tensor, k_cache: torch.Tensor,
     _lib.check_tensor(out, "out", torch.float32, (B, Lmax), device=dev)
     _lib.check(_lib.load().ess_indexer_logits_ex(
         q_fp8.data_ptr(), w.data_ptr(), k_cache.data_ptr(), k_scale.data_ptr(), lens.data_ptr(),
-        B, Lmax, out.data_ptr(), max_ctas, _lib.stream_handle()), "ess_indexer_logits")
+        B, Lmax, out.data_ptr(), max_ctas | (_lib.ESS_LAUNCH_PDL if pdl else 0), _lib.stream_handle()),
+        "ess_indexer_logits")
     return out
 
 
@@ -128,10 +131,11 @@ def topk(logits: torch.Tensor, lens: torch.Tensor, k: int = TOPK,
 
 
 def topk_split(logits: torch.Tensor, lens: torch.Tensor, k: int, out: torch.Tensor, count: torch.Tensor,
-               pool, acc, begin: int = 0):
+               pool, acc, begin: int = 0, pdl: bool = False):
     """K2 fused with the early-gather hit/miss split of pools [begin, begin + B)
-    (ess_topk_split): selection ids into ``out``/``count``; hit rows, miss ids, staging
-    rows and counts into ``acc`` (an AccessBatch of row slices)."""
+    (ess_topk_split_ex): selection ids into ``out``/``count``; hit rows, miss ids, staging
+    rows and counts into ``acc`` (an AccessBatch of row slices).  ``pdl``: launched
+    programmatically behind the indexer on the same stream (waits for it on the device)."""
     _lib.require_cuda(logits)
     B, ld = _check_topk_args(logits, lens, k)
     _check_topk_out(out, count, B, k, logits.device)
@@ -141,11 +145,11 @@ def topk_split(logits: torch.Tensor, lens: torch.Tensor, k: int, out: torch.Tens
         if t.stride(1) != 1 or t.stride(0) != acc.miss_ids.stride(0) or t.shape[1] < k:
             raise ValueError(f"acc.{name} rows must be unit-stride, share one row stride and hold k ids")
     _lib.check_tensor(acc.counts, "acc.counts", torch.int32, (B, 4), device=logits.device)
-    _lib.check(_lib.load().ess_topk_split(
+    _lib.check(_lib.load().ess_topk_split_ex(
         logits.data_ptr(), logits.stride(0), lens.data_ptr(), B, k, out.data_ptr(), out.stride(0),
         count.data_ptr(), pool.handle, begin, acc.hit_row.data_ptr(), acc.miss_ids.data_ptr(),
         acc.miss_row.data_ptr(), acc.counts.data_ptr(), acc.miss_ids.stride(0),
-        _lib.stream_handle()), "ess_topk_split")
+        _lib.ESS_LAUNCH_PDL if pdl else 0, _lib.stream_handle()), "ess_topk_split")
     return out, count
 
 

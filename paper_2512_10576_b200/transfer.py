@@ -154,16 +154,20 @@ class HostLatentStore:
 
 def gather(pool: PoolSet, store: HostLatentStore, acc: AccessBatch, begin: int = 0,
            store_begin: int | None = None, max_ctas: int = 32, exclusive: bool = False,
-           stream=None, landed: torch.Tensor | None = None, bulk: bool | None = None) -> None:
+           stream=None, landed: torch.Tensor | None = None, bulk: bool | None = None,
+           pdl: bool = False) -> None:
     """Copy every miss row host[pool][miss_id] -> slot store[pool][miss_row] (K4),
     dequantising to the slot format on the way.  ``exclusive`` keeps the gather off
     SMs that run attention CTAs (overlapped schedule).  ``landed`` (int32 [num],
-    zero before the step; sparse_mla_da re-zeroes it) counts each request's landed rows."""
+    zero before the step; sparse_mla_da re-zeroes it) counts each request's landed rows.
+    ``pdl``: launched programmatically behind the split on the same stream (ESS_LAUNCH_PDL)."""
     num = acc.counts.shape[0]
     sb = begin if store_begin is None else store_begin
     flags = _lib.ESS_GATHER_EXCLUSIVE_SM if exclusive else 0
     if GATHER_BULK if bulk is None else bulk:
         flags |= _lib.ESS_GATHER_BULK
+    if pdl:
+        flags |= _lib.ESS_LAUNCH_PDL
     if landed is not None and (landed.dtype != torch.int32 or landed.numel() < num):
         raise ValueError("landed must be int32 with one counter per request")
     _lib.check(_lib.load().ess_gather_signal(

@@ -64,7 +64,8 @@ def test_decode_layer_matches_oracle_chain(ctx, rho, fuse, overlap):
 
 
 @pytest.mark.parametrize("overlap,micro,B", [("dba", 2, 4), ("dba", 3, 4), ("da", 1, 4), ("dba", 2, 40),
-                                             ("stream", 1, 4), ("stream", 1, 40), ("dbs", 2, 4), ("dbs", 3, 40)])
+                                             ("stream", 1, 4), ("stream", 1, 40), ("dbs", 2, 4), ("dbs", 3, 40),
+                                             ("dba+pdl", 2, 40), ("da+pdl", 1, 4)])
 def test_graph_step_with_overlap_matches_oracle_chain(overlap, micro, B):
     """The product step — two micro-batches, gathers on a side stream, whole step
     captured as a CUDA graph, history/capacity computed on device — stays bit-exact
@@ -103,6 +104,8 @@ def test_graph_step_with_overlap_matches_oracle_chain(overlap, micro, B):
             o.append_generated([hist - 1])
 
     layer.micro = micro
+    if overlap.endswith("+pdl"):  # the first micro-batch's K1 -> K2 + K3a (-> next K1) as PDL launches
+        layer.pdl, overlap = True, overlap[:-4]
     eager = layer.capture(overlap=overlap)    # runs one eager step first
     mirror(False, counts=eager)
     for _ in range(3):
