@@ -567,6 +567,11 @@ def measure(args, cfg, dev, rank, world, agg_dev, drift, full, peaks, peak_kind,
     # from pinned memory and its attention output D2H (layer.step_host: copy stream,
     # double-buffered staging, so transfers of step t overlap compute of t-1 / t+1)
     if args.e2e:
+        # link-serial pipeline (per-slot graphs: the query upload and the miss gather
+        # take turns on the host link) for the DA / DBA schedules
+        serial = args.overlap in ("da", "dba") and os.environ.get("ESS_E2E_SERIAL", "1") == "1"
+        if serial:
+            layer.capture_host(args.overlap, args.gather_ctas)
         h_in = [(qi.cpu().pin_memory(), q.cpu().pin_memory()) for qi, q in inputs[W:W + K]]
         h_out = [torch.empty(layer.out.shape, dtype=layer.out.dtype).pin_memory() for _ in range(K)]
         torch.cuda.synchronize()
@@ -582,7 +587,8 @@ def measure(args, cfg, dev, rank, world, agg_dev, drift, full, peaks, peak_kind,
         h2d = h_in[0][0].numel() + h_in[0][1].numel() * 2
         rec["e2e"] = {"value": e2e_tok / e2e_t, "unit": "tokens/s",
                       "h2d_bytes_per_step": h2d,
-                      "d2h_bytes_per_step": h_out[0].numel() * 2}
+                      "d2h_bytes_per_step": h_out[0].numel() * 2,
+                      "pipeline": "link-serial" if serial else "overlapped"}
         # the H2D link carries the queries (DMA) and the misses (SM reads, 704 B each):
         # its achieved rate vs the measured pinned-DMA peak, and the e2e bound it sets
         if link_peak:

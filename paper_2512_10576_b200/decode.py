@@ -310,6 +310,12 @@ class DSADecodeLayer:
             self._lru = torch.cuda.Stream(self.device)
         sel, lru = self._sel, self._lru
         ready = None
+        # step_host's link-serial graphs (capture_host): the first gather waits for the
+        # external "queries uploaded" event, the last one records "gathered"
+        ext = getattr(self, "_ext", None)
+        if ext is not None and dbs:
+            raise ValueError("capture_host supports the da / dba schedules")
+        ext_wait = ext is not None
         pdl_next = False  # launch the next indexer programmatically (behind a main-stream gather)
         prev = 0  # requests of the previous micro-batch (its K2/K3 run beside this K1)
         for i, (a, b) in enumerate(ranges):
@@ -350,6 +356,9 @@ class DSADecodeLayer:
                 # the main stream would hold the next micro-batch's top-k until the gather ends.
                 pdl_next = self.pdl_gather == 0
                 side.wait_event(ready)
+                if ext_wait:
+                    ext[0].wait(side)
+                    ext_wait = False
                 with torch.cuda.stream(side):
                     gather(self.pool, self.store, self._acc_view(a, b), begin=a, max_ctas=g_i,
                            exclusive=True, landed=self._landed[a:b] if fused else None)
@@ -374,6 +383,9 @@ class DSADecodeLayer:
                 ready = torch.cuda.Event()
                 ready.record(sel)
             side.wait_event(ready)
+            if ext_wait:
+                ext[0].wait(side)
+                ext_wait = False
             with torch.cuda.stream(side):
                 gather(self.pool, self.store, self._acc_view(a, b), begin=a, max_ctas=g_i,
                        exclusive=True, landed=self._landed[a:b] if fused else None)
@@ -389,6 +401,9 @@ class DSADecodeLayer:
             settled = torch.cuda.Event()
             settled.record(lru)
         main.wait_event(ready)  # attention reads every micro-batch's selections
+        if ext is not None:
+            ext[1].record(side)  # every gather of the step issued on the side stream
+            ext[0].wait(main)    # attention reads the uploaded queries
         if new_rows is not None:
             if getattr(self, "_adm", None) is None:
                 self._adm = torch.cuda.Stream(self.device)
@@ -644,15 +659,56 @@ class DSADecodeLayer:
             raise ValueError(f"decode step {self.history - self.ctx + 1} exceeds max_new_tokens: "
                              f"history {self.history} + 1 > Lmax {self.Lmax}")
 
+    def capture_host(self, overlap: str = "dba", gather_ctas: int = 32) -> None:
+        """Graphs for ``step_host``'s link-serial pipeline (after ``capture``): one per
+        host-staging slot, reading that slot's queries in place and writing its own
+        output buffer.  The queries' H2D copy (copy engine) and the miss gather (SM
+        reads) share the host link, and run together they both slow down (the copy
+        engines' traffic throttles SM-initiated host reads), so the
+        pipeline keeps them apart: step t+1's query upload starts when step t's last
+        gather has issued (an external event recorded inside graph t) and graph t+1's
+        first gather and its attention wait for that upload (an external event wait
+        node), while its indexer / top-k run under the upload."""
+        if overlap not in ("da", "dba"):
+            raise ValueError("capture_host supports the da / dba schedules")
+        if getattr(self, "graph", None) is None:
+            self.capture(overlap, gather_ctas)
+        base = (self.q_idx_in, self.q_in, self.out)
+        self._hslots = []
+        for _ in range(2):
+            slot = {"qi": torch.empty_like(base[0]), "q": torch.empty_like(base[1]),
+                    "out": torch.empty_like(base[2]), "uploaded": torch.cuda.Event(external=True),
+                    "gathered": torch.cuda.Event(external=True)}
+            for e in ("qi_ready", "in_free", "done", "out_free"):
+                slot[e] = torch.cuda.Event()
+            for e in ("uploaded", "gathered"):  # create the CUDA events before capture
+                slot[e].record()
+            slot["qi"].copy_(base[0])
+            slot["q"].copy_(base[1])
+            self.q_idx_in, self.q_in, self.out = slot["qi"], slot["q"], slot["out"]
+            self._ext = (slot["uploaded"], slot["gathered"])
+            try:
+                slot["graph"] = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(slot["graph"]):
+                    self._device_step(overlap, gather_ctas)
+            finally:
+                self._ext = None
+                self.q_idx_in, self.q_in, self.out = base
+            self._hslots.append(slot)
+        torch.cuda.synchronize(self.device)
+
     def step_host(self, h_q_idx: torch.Tensor, h_q: torch.Tensor, new_rows: torch.Tensor,
                   h_out: torch.Tensor) -> None:
         """One step with the queries in pinned host memory and the attention output
-        returned to pinned host memory.  H2D and D2H run on a copy stream into
+        returned to pinned host memory.  H2D and D2H run on copy streams into
         double-buffered device staging, so step t's transfers overlap steps t-1 / t+1
-        while every step still moves its own inputs and result over the host link.
-        Asynchronous: synchronise before reading ``h_out``."""
+        while every step still moves its own inputs and result over the host link;
+        after ``capture_host`` the query upload is kept off the link while the gathers
+        run (link-serial pipeline).  Asynchronous: synchronise before reading ``h_out``."""
         d = self.device
         self._check_room()
+        if getattr(self, "_hslots", None):
+            return self._step_host_serial(h_q_idx, h_q, new_rows, h_out)
         if getattr(self, "_cs", None) is None:
             self._cs = torch.cuda.Stream(d)    # H2D copies
             self._ds = torch.cuda.Stream(d)    # D2H copies (other PCIe direction)
@@ -683,6 +739,35 @@ class DSADecodeLayer:
         with torch.cuda.stream(ds):
             h_out.copy_(st_out, non_blocking=True)
             ev["out_free"].record(ds)
+
+    def _step_host_serial(self, h_q_idx, h_q, new_rows, h_out) -> None:
+        d = self.device
+        if getattr(self, "_cs", None) is None:
+            self._cs = torch.cuda.Stream(d)    # H2D copies
+            self._ds = torch.cuda.Stream(d)    # D2H copies (other PCIe direction)
+            self._slot = 0
+        main, cs, ds = torch.cuda.current_stream(d), self._cs, self._ds
+        k = self._slot
+        self._slot ^= 1
+        S, P = self._hslots[k], self._hslots[k ^ 1]
+        cs.wait_event(S["in_free"])       # the graph that last read slot k has finished
+        P["gathered"].wait(cs)            # the previous step's gathers are off the link
+        with torch.cuda.stream(cs):
+            S["qi"].copy_(h_q_idx, non_blocking=True)
+            S["qi_ready"].record(cs)
+            S["q"].copy_(h_q, non_blocking=True)
+            S["uploaded"].record(cs)      # graph k's gathers and attention wait on this
+        main.wait_event(S["qi_ready"])    # the indexer needs only the indexer queries
+        main.wait_event(S["out_free"])    # the D2H of slot k's previous output is done
+        _lib.copy_many([(self.rows_in, new_rows)])
+        S["graph"].replay()
+        self.history += 1
+        S["in_free"].record(main)
+        S["done"].record(main)
+        ds.wait_event(S["done"])
+        with torch.cuda.stream(ds):
+            h_out.copy_(S["out"], non_blocking=True)
+            S["out_free"].record(ds)
 
     def host_sync(self) -> None:
         """Wait for every outstanding step_host transfer."""

@@ -273,3 +273,43 @@ def test_preload_full_history_mixed_lengths():
     assert (counts[:, 1] == 0).all() and (counts[:, 0] == 2048).all(), counts
     layer.pool.check()
     layer.close()
+
+
+@pytest.mark.parametrize("serial", [False, True])
+def test_step_host_matches_device_step(serial):
+    """The public host-buffer step (queries from pinned memory, output back to pinned
+    memory) equals the device-input step on the same inputs: selections and cache
+    accounting bit for bit, attention to 1e-3.  serial: capture_host's link-serial
+    pipeline (per-slot graphs, external upload / gathered events)."""
+    from paper_2512_10576_b200.decode import DSADecodeLayer, random_latent_rows
+    B, ctx, rho, K = 8, 8192, 0.25, 2048
+    layers = [DSADecodeLayer(B, ctx, rho, K, max_new_tokens=12, seed=5, drift=0.97) for _ in range(2)]
+    for lay in layers:
+        lay.prefill_warmup(windows=6)
+        lay.capture("dba")
+    dev, host = layers
+    if serial:
+        host.capture_host("dba")
+    outs = []
+    for t in range(4):
+        q_idx, q = dev.next_queries()
+        host.next_queries()  # keep the two layers' query streams in step
+        rows = random_latent_rows(B, "cuda", dev.gen).view(B, 1, 656)
+        host.gen.set_state(dev.gen.get_state())
+        h_out = torch.empty(dev.out.shape, dtype=dev.out.dtype).pin_memory()
+        out, _ = dev.step(q_idx, q, rows)
+        host.step_host(q_idx.cpu().pin_memory(), q.cpu().pin_memory(), rows.clone(), h_out)
+        host.host_sync()
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(host.idx.cpu().numpy(), dev.idx.cpu().numpy())
+        np.testing.assert_array_equal(host.step_counts().cpu().numpy(), dev.step_counts().cpu().numpy())
+        o_dev, o_host = out.float().cpu(), h_out.float()
+        assert float((o_host - o_dev).norm() / o_dev.norm()) <= 1e-3, t
+        outs.append(float(o_host.norm()))
+    for lay in layers:
+        lay.pool.check()
+    a, ca = dev.pool.lru_order()
+    b, cb = host.pool.lru_order()
+    assert torch.equal(ca, cb) and all(a[i, :int(ca[i])].tolist() == b[i, :int(cb[i])].tolist() for i in range(B))
+    for lay in layers:
+        lay.close()
