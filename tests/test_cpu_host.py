@@ -50,6 +50,15 @@ def test_header_constants_match_python_mirror():
     assert int(defs["ESS_MLA_RESUME"]) == _lib.ESS_MLA_RESUME
     assert int(defs["ESS_GATHER_EXCLUSIVE_SM"]) == _lib.ESS_GATHER_EXCLUSIVE_SM
     assert int(defs["ESS_GATHER_BULK"]) == _lib.ESS_GATHER_BULK
+    assert re.search(r"#define ESS_LAUNCH_PDL \(1 << 30\)", src) and _lib.ESS_LAUNCH_PDL == 1 << 30
+
+
+def test_launch_flags_are_validated_without_gpu():
+    """ess_topk_split_ex rejects unknown launch flags before touching the device."""
+    L = _lib.load()
+    rc = L.ess_topk_split_ex(None, 128, None, 1, 1, None, 1, None, None, 0, None, None, None, None, 1,
+                             1 << 3, None)
+    assert rc == _lib.ESS_ERR_ARG
 
 
 def test_status_mapping():
