@@ -1,5 +1,6 @@
-"""gpurun_out/prof_*.ncu-rep -> profiles/r01_ncu_<kernel>.txt (SOL excerpt + key raw
-metrics) and profiles/traffic_<config>.json (K1 DRAM bytes per launch, read by bench.py)."""
+"""gpurun_out/prof_*.ncu-rep -> profiles/<ROUND>_ncu_<kernel>.txt (SOL excerpt + key raw
+metrics; ROUND env, default r01) and profiles/traffic_<config>.json (K1 DRAM bytes per
+launch, read by bench.py)."""
 import json
 import os
 import subprocess
@@ -15,12 +16,13 @@ SOL = ("Memory Throughput", "DRAM Throughput", "Duration", "L2 Cache Throughput"
 ALGO = {  # algorithmic bytes per launch at the prof_step shapes (B=64, len = ctx + steps)
     "indexer_kernel": lambda L: 64 * L * 136 + 64 * (64 * 128 + 256),
 }
+RND = os.environ.get("ROUND", "r01")
 for name in sys.argv[1:]:
     rep = os.path.join(OUT, f"prof_{name}.ncu-rep")
     det = subprocess.run(["ncu", "-i", rep, "--page", "details"], capture_output=True, text=True).stdout
     lines = [ln for ln in det.splitlines() if ln.strip().startswith(SOL) or "Section: GPU Speed Of Light" in ln]
     raw = summary(rep)[0]
-    with open(os.path.join(PROF, f"r01_ncu_{name}.txt"), "w") as f:
+    with open(os.path.join(PROF, f"{RND}_ncu_{name}.txt"), "w") as f:
         f.write(f"# ncu --set full --clock-control none, {name} (scripts/gpu_prof_round.sh; one steady-state launch)\n")
         f.write("\n".join(lines[:14]) + "\n# raw metrics\n")
         for k, (v, u) in ((k, v) for k, v in raw.items() if k != "name"):
@@ -35,7 +37,7 @@ for name in sys.argv[1:]:
         dur = float(raw["gpu__time_duration.sum"][0]) * (1e-3 if raw["gpu__time_duration.sum"][1] == "ns" else 1)
         with open(os.path.join(PROF, f"traffic_{cfg}.json"), "w") as f:
             json.dump({"kernel": "indexer_kernel", "config": f"{cfg.upper()}: B=64 (+step headroom)",
-                       "source": f"ncu --set full, gpurun_out/prof_{name}.ncu-rep (round 1, 256-token units)",
+                       "source": f"ncu --set full, gpurun_out/prof_{name}.ncu-rep ({RND})",
                        "indexer_dram_bytes_per_launch": int(rd + wr), "dram_read_bytes": int(rd),
                        "dram_write_bytes": int(wr), "algorithmic_bytes_per_launch": ALGO["indexer_kernel"](L),
                        "duration_us_ncu": dur}, f, indent=1)
