@@ -293,8 +293,22 @@ __device__ void sort_ids(StepSmem &sm, int n) {
 }
 
 __device__ __forceinline__ void copy_row(const uint8_t *src, uint8_t *dst, int lane, int bytes) {
-  for (int c = lane; c < bytes / 16; c += 32)
-    reinterpret_cast<uint4 *>(dst)[c] = reinterpret_cast<const uint4 *>(src)[c];
+  // every load of the row first, then the stores: one memory round trip per row, not
+  // one per 512-B chunk (rows up to 1536 B; longer rows loop)
+  const int n16 = bytes / 16;
+  for (int c0 = 0; c0 < n16; c0 += 96) {
+    uint4 v[3];
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      const int c = c0 + lane + 32 * k;
+      if (c < n16) v[k] = __ldcg(reinterpret_cast<const uint4 *>(src) + c);
+    }
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+      const int c = c0 + lane + 32 * k;
+      if (c < n16) reinterpret_cast<uint4 *>(dst)[c] = v[k];
+    }
+  }
 }
 
 // One 656-B latent row held by a warp (lane l: chunk l in v0; lanes 0..8: chunk
@@ -994,6 +1008,9 @@ __global__ void __launch_bounds__(NT) pool_split_kernel(PoolView pv, int begin,
 
 // settle: staging row cap_max + j -> final slot slot[j] (< 0: not admitted), one warp
 // per row, for the counts[b*4+1] misses of each pool
+#ifndef ESS_SETTLE_CTAS
+#define ESS_SETTLE_CTAS 8  // CTAs per pool (8 warps each, one row per warp at a time)
+#endif
 __global__ void pool_settle_kernel(PoolView pv, int begin, const int32_t *__restrict__ slot,
                                    const int32_t *__restrict__ counts, int stride) {
   const int b = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1573,7 +1590,7 @@ int ess_pool_settle(ess_pool *p, int32_t begin, int32_t num, const int32_t *d_sl
                     const int32_t *d_counts, int32_t stride, void *stream) {
   if (!range_ok(p, begin, num) || !p->rows || !d_slot || !d_counts || stride < 1) return ESS_ERR_ARG;
   if (num == 0) return ESS_OK;
-  pool_settle_kernel<<<dim3(num, 4), 256, 0, (cudaStream_t)stream>>>(view(p), begin, d_slot, d_counts,
+  pool_settle_kernel<<<dim3(num, ESS_SETTLE_CTAS), 256, 0, (cudaStream_t)stream>>>(view(p), begin, d_slot, d_counts,
                                                                      stride);
   ESS_CUDA_TRY(cudaGetLastError());
   return ESS_OK;
