@@ -98,9 +98,13 @@ int ess_host_register(void *host_ptr, size_t bytes, void **d_alias);
 int ess_host_unregister(void *host_ptr);
 /* allocate + register the host latent store: 2-MB aligned, transparent huge pages
  * (ESS_HOST_HUGEPAGES), bound to numa_node when >= 0; *placed reports which of the
- * two took effect.  Free with ess_host_free(host_ptr, bytes). */
+ * flags took effect.  ESS_HOST_VMM: one host-located VMM allocation (cuMemCreate,
+ * CU_MEM_LOCATION_TYPE_HOST_NUMA) mapped at one VA for device and CPU (*host_ptr ==
+ * *d_alias), falling back to the registered store when the driver has no host VMM.
+ * Free with ess_host_free(host_ptr, bytes). */
 #define ESS_HOST_HUGEPAGES 1
 #define ESS_HOST_NUMA_BOUND 2
+#define ESS_HOST_VMM 4
 int ess_host_alloc(size_t bytes, int32_t flags, int32_t numa_node, void **host_ptr, void **d_alias,
                    int32_t *placed);
 int ess_host_free(void *host_ptr, size_t bytes);

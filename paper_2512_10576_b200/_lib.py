@@ -79,7 +79,7 @@ MAX_QTOK = 4  # ESS_INDEXER_MAX_QTOK: query tokens per request and step (MTP wid
 ESS_GATHER_EXCLUSIVE_SM = 1
 ESS_GATHER_BULK = 2
 ESS_LAUNCH_PDL = 1 << 30
-ESS_HOST_HUGEPAGES, ESS_HOST_NUMA_BOUND = 1, 2
+ESS_HOST_HUGEPAGES, ESS_HOST_NUMA_BOUND, ESS_HOST_VMM = 1, 2, 4
 MAX_REQUEST = 2048
 LATENT_ROW_BYTES = 656   # host store / transfer format (e4m3 NoPE + scales + bf16 RoPE)
 # host store row pitch (64-B aligned rows; ESS_HOST_ROW_PITCH); the env override pairs with

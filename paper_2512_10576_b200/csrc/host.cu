@@ -7,6 +7,8 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <type_traits>
+#include <algorithm>
 #include <utility>
 
 #include "common.cuh"
@@ -187,9 +189,130 @@ constexpr size_t kHugePage = 2u << 20;
 size_t host_span(size_t bytes) { return (bytes + kHugePage - 1) / kHugePage * kHugePage; }
 }  // namespace
 
+// ESS_HOST_VMM: the store as ONE host-located VMM allocation (cuMemCreate with a
+// CU_MEM_LOCATION_TYPE_HOST_NUMA location, mapped at one VA for the device and the CPU).
+// A cudaHostRegister'd store is mapped into the GPU's page tables in small pages, THP or
+// not: random row reads across a multi-GB store then miss the SMs' translation caches,
+// and the gather needs >= 48 SMs at 5.5 GiB (C4) to reach the rate 20 SMs reach at
+// 1.4 GiB (scripts/gather_tlb.py).  The VMM allocation is mapped at its allocation
+// granularity.
+namespace {
+struct VmmFns {
+  decltype(&cuMemGetAllocationGranularity) gran = nullptr;
+  decltype(&cuMemCreate) create = nullptr;
+  decltype(&cuMemRelease) release = nullptr;
+  decltype(&cuMemAddressReserve) reserve = nullptr;
+  decltype(&cuMemAddressFree) vfree = nullptr;
+  decltype(&cuMemMap) map = nullptr;
+  decltype(&cuMemUnmap) unmap = nullptr;
+  decltype(&cuMemSetAccess) access = nullptr;
+  bool ok = false;
+};
+const VmmFns &vmm_fns() {
+  static VmmFns f;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto get = [](const char *name, auto &out) {
+      void *p = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        out = reinterpret_cast<std::remove_reference_t<decltype(out)>>(p);
+      return out != nullptr;
+    };
+    f.ok = get("cuMemGetAllocationGranularity", f.gran) & get("cuMemCreate", f.create) &
+           get("cuMemRelease", f.release) & get("cuMemAddressReserve", f.reserve) &
+           get("cuMemAddressFree", f.vfree) & get("cuMemMap", f.map) & get("cuMemUnmap", f.unmap) &
+           get("cuMemSetAccess", f.access);
+  });
+  return f;
+}
+struct VmmAlloc {
+  CUmemGenericAllocationHandle h;
+  size_t size;
+};
+std::mutex g_vmm_mu;
+std::map<uintptr_t, VmmAlloc> g_vmm;  // VA -> allocation (ess_host_free tells the two kinds apart)
+
+int vmm_alloc(size_t bytes, int32_t numa_node, void **ptr, size_t *mapped) {
+  const VmmFns &f = vmm_fns();
+  if (!f.ok) return ESS_ERR_CUDA;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return ESS_ERR_CUDA;
+  cudaFree(nullptr);  // the runtime's primary context is current for the driver calls
+  CUmemAllocationProp prop = {};
+  prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  prop.location.type = CU_MEM_LOCATION_TYPE_HOST_NUMA;
+  prop.location.id = numa_node >= 0 ? numa_node : 0;
+  size_t g = 0;
+  if (f.gran(&g, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS || !g) return ESS_ERR_CUDA;
+  const size_t size = (bytes + g - 1) / g * g;
+  CUmemGenericAllocationHandle h;
+  if (f.create(&h, size, &prop, 0) != CUDA_SUCCESS) return ESS_ERR_NOMEM;
+  CUdeviceptr va = 0;
+  if (f.reserve(&va, size, std::max<size_t>(g, kHugePage), 0, 0) != CUDA_SUCCESS) {
+    f.release(h);
+    return ESS_ERR_CUDA;
+  }
+  CUmemAccessDesc acc[2] = {};
+  acc[0].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc[0].location.id = dev;
+  acc[0].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  acc[1].location.type = CU_MEM_LOCATION_TYPE_HOST_NUMA;  // the CPU fills / writes back rows
+  acc[1].location.id = prop.location.id;
+  acc[1].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if (f.map(va, size, 0, h, 0) != CUDA_SUCCESS) {
+    f.vfree(va, size);
+    f.release(h);
+    return ESS_ERR_CUDA;
+  }
+  if (f.access(va, size, acc, 2) != CUDA_SUCCESS) {
+    f.unmap(va, size);
+    f.vfree(va, size);
+    f.release(h);
+    return ESS_ERR_CUDA;
+  }
+  {
+    std::lock_guard<std::mutex> l(g_vmm_mu);
+    g_vmm[(uintptr_t)va] = {h, size};
+  }
+  *ptr = reinterpret_cast<void *>(va);
+  *mapped = size;
+  return ESS_OK;
+}
+
+bool vmm_free(void *p) {
+  VmmAlloc a;
+  {
+    std::lock_guard<std::mutex> l(g_vmm_mu);
+    auto it = g_vmm.find((uintptr_t)p);
+    if (it == g_vmm.end()) return false;
+    a = it->second;
+    g_vmm.erase(it);
+  }
+  const VmmFns &f = vmm_fns();
+  f.unmap((CUdeviceptr)p, a.size);
+  f.vfree((CUdeviceptr)p, a.size);
+  f.release(a.h);
+  return true;
+}
+}  // namespace
+
 int ess_host_alloc(size_t bytes, int32_t flags, int32_t numa_node, void **host_ptr, void **d_alias,
                    int32_t *placed) {
   if (!bytes || !host_ptr || !d_alias) return ESS_ERR_ARG;
+  if (flags & ESS_HOST_VMM) {
+    void *p = nullptr;
+    size_t mapped = 0;
+    if (vmm_alloc(bytes, numa_node, &p, &mapped) == ESS_OK) {
+      memset(p, 0, bytes);  // CPU access check + first touch (as the register path)
+      *host_ptr = p;
+      *d_alias = p;
+      if (placed) *placed = ESS_HOST_VMM | (numa_node >= 0 ? ESS_HOST_NUMA_BOUND : 0);
+      return ESS_OK;
+    }
+    // no host VMM on this driver / platform: the registered store below
+  }
   const size_t span = host_span(bytes);
   void *raw = mmap(nullptr, span + kHugePage, PROT_READ | PROT_WRITE,
                    MAP_PRIVATE | MAP_ANONYMOUS | MAP_NORESERVE, -1, 0);
@@ -224,6 +347,7 @@ int ess_host_alloc(size_t bytes, int32_t flags, int32_t numa_node, void **host_p
 
 int ess_host_free(void *host_ptr, size_t bytes) {
   if (!host_ptr || !bytes) return ESS_ERR_ARG;
+  if (vmm_free(host_ptr)) return ESS_OK;
   const cudaError_t e = cudaHostUnregister(host_ptr);
   munmap(host_ptr, host_span(bytes));
   return e == cudaSuccess ? ESS_OK : ESS_ERR_CUDA;

@@ -89,6 +89,11 @@ class DSADecodeLayer:
         self.min_gather_sms = 20
         self.early_gather_sms = int(os.environ.get("ESS_EARLY_GATHER_SMS", "20"))
         self.late_k1_ctas = int(os.environ.get("ESS_LATE_K1_CTAS", "0"))
+        # DBA gathers on SMs shared with the indexer / attention CTAs (no exclusive-SM
+        # shared-memory reservation) and their CTA counts (0 = the exclusive defaults)
+        self.gather_shared = os.environ.get("ESS_GATHER_SHARED", "1") == "1"
+        self.shared_early_gather_ctas = int(os.environ.get("ESS_SHARED_EARLY_GATHER_CTAS", "48"))
+        self.shared_late_gather_ctas = int(os.environ.get("ESS_SHARED_LATE_GATHER_CTAS", "0"))
         # DA / DBA: the first micro-batch's K1 -> K2 + K3a (-> K4) as programmatic
         # dependent launches on one stream
         self.pdl = os.environ.get("ESS_PDL", "0") == "1"
@@ -326,6 +331,12 @@ class DSADecodeLayer:
             # attention, and may take more SMs (early_gather_sms) than the last one
             g_i = gsms if i == len(ranges) - 1 else max(gsms, self.early_gather_sms)
             g_prev = 0 if i == 0 else (gsms if i - 1 == len(ranges) - 1 else max(gsms, self.early_gather_sms))
+            if self.gather_shared:
+                # the gather's CTAs sit beside the indexer's / attention's on the same SMs
+                late = i == len(ranges) - 1
+                want = self.shared_late_gather_ctas if late else self.shared_early_gather_ctas
+                g_i = want or g_i
+                g_prev = 0
             ctas = 0 if i == 0 else sms - g_prev - prev
             if i > 0 and self.late_k1_ctas:  # cap: less HBM pressure beside the gather
                 ctas = min(ctas, self.late_k1_ctas)
@@ -361,7 +372,7 @@ class DSADecodeLayer:
                     ext_wait = False
                 with torch.cuda.stream(side):
                     gather(self.pool, self.store, self._acc_view(a, b), begin=a, max_ctas=g_i,
-                           exclusive=True, landed=self._landed[a:b] if fused else None)
+                           exclusive=not self.gather_shared, landed=self._landed[a:b] if fused else None)
                     fetched = torch.cuda.Event()
                     fetched.record(side)
                 self._lru_mb(a, b, ready, fetched)
@@ -388,7 +399,7 @@ class DSADecodeLayer:
                 ext_wait = False
             with torch.cuda.stream(side):
                 gather(self.pool, self.store, self._acc_view(a, b), begin=a, max_ctas=g_i,
-                       exclusive=True, landed=self._landed[a:b] if fused else None)
+                       exclusive=not self.gather_shared, landed=self._landed[a:b] if fused else None)
                 fetched = torch.cuda.Event()
                 fetched.record(side)
             if self.early_gather:

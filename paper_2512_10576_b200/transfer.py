@@ -24,6 +24,8 @@ from .cache import AccessBatch, PoolSet
 LATENT_BLOCK_BYTES = 656
 # K4 form: 16-B zero-copy loads (False) or cp.async.bulk row copies into a smem ring (True)
 GATHER_BULK = os.environ.get("ESS_GATHER_BULK", "0") == "1"
+# the host store as one host-located VMM allocation (ess_host_alloc ESS_HOST_VMM)
+HOST_VMM = os.environ.get("ESS_HOST_VMM", "0") == "1"
 PER_CALL_EFFECTIVE_H2D_GBS = 0.79
 PER_CALL_EFFECTIVE_D2H_GBS = 0.23
 
@@ -111,19 +113,23 @@ class HostLatentStore:
     64-B host-link request boundary.  ``host`` is the [pools, rows, 656] view."""
 
     def __init__(self, num_pools: int, rows_per_pool: int, hugepages: bool = True,
-                 numa_node: int | None = None, device=None):
+                 numa_node: int | None = None, device=None, vmm: bool | None = None):
         _lib.require_cuda()
+        if vmm is None:
+            vmm = HOST_VMM
         self.num_pools, self.rows_per_pool = num_pools, rows_per_pool
         self.row_bytes, self.pitch = LATENT_BLOCK_BYTES, _lib.HOST_ROW_PITCH
         n = num_pools * rows_per_pool * self.pitch
         node = gpu_numa_node(device) if numa_node is None else numa_node
         hp, alias, placed = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_int32(0)
-        _lib.check(_lib.load().ess_host_alloc(n, _lib.ESS_HOST_HUGEPAGES if hugepages else 0,
+        flags = (_lib.ESS_HOST_HUGEPAGES if hugepages else 0) | (_lib.ESS_HOST_VMM if vmm else 0)
+        _lib.check(_lib.load().ess_host_alloc(n, flags,
                                               -1 if node is None else node, ctypes.byref(hp),
                                               ctypes.byref(alias), ctypes.byref(placed)),
                    "ess_host_alloc")
         self._host_ptr, self._nbytes = hp.value, n
         self.hugepages = bool(placed.value & _lib.ESS_HOST_HUGEPAGES)
+        self.vmm = bool(placed.value & _lib.ESS_HOST_VMM)
         self.numa_node = node if placed.value & _lib.ESS_HOST_NUMA_BOUND else None
         raw = (ctypes.c_uint8 * n).from_address(hp.value)
         self._buf = torch.frombuffer(raw, dtype=torch.uint8).view(num_pools, rows_per_pool, self.pitch)

@@ -173,15 +173,18 @@ def _check_k5(o, lse, ref_o, ref_l, what):
 
 
 @pytest.mark.parametrize("fmt", [656, 1152], ids=["fp8slots", "f16slots"])
-@pytest.mark.parametrize("bulk", [False, True], ids=["ld16", "bulk"])
-def test_gather_and_write_back_are_exact(bulk, fmt):
+@pytest.mark.parametrize("bulk,vmm", [(False, False), (True, False), (False, True)],
+                         ids=["ld16", "bulk", "ld16-vmmstore"])
+def test_gather_and_write_back_are_exact(bulk, vmm, fmt):
     """K4 reads 656-B rows over the host link and admits them dequantised; the slot
-    row must equal the oracle's f16(f32(e4m3) * scale) ++ f16(bf16) bit for bit."""
+    row must equal the oracle's f16(f32(e4m3) * scale) ++ f16(bf16) bit for bit.
+    vmm: the host store as one host-located VMM allocation (ESS_HOST_VMM)."""
     from paper_2512_10576_b200.cache import PoolSet
     from paper_2512_10576_b200.decode import random_latent_rows
     from paper_2512_10576_b200.transfer import HostLatentStore, gather, write_generated
     P, ids, cap = 3, 5000, 1200
-    store = HostLatentStore(P, ids)
+    store = HostLatentStore(P, ids, vmm=vmm)
+    assert store.vmm == vmm
     for p in range(P):
         store.host[p].copy_(random_latent_rows(ids, "cuda"))
     pools = PoolSet(P, ids, cap, cap, row_bytes=fmt, staging_rows=0)
