@@ -48,6 +48,11 @@ CONFIGS = {
 }
 TOPK = 2048
 LINK_ROW_BYTES = 64 * ((656 + 63) // 64)  # a 64-B aligned 656-B row in 64-B read completions
+# K4 alone in the breakdown: 64 CTAs.  Random row reads across a multi-GB host store are
+# limited per SM (address translation), not per request in flight: at C4's 5.5-GiB store
+# 20 / 32 CTAs reach 30 / 36 GB/s, >= 48 CTAs the 41-42 GB/s that 20 reach at C2's 1.4 GiB
+# (profiles/r02_gather_store_size.txt)
+BREAKDOWN_GATHER_CTAS = 64
 METRIC = "decode tokens/s/GPU at 32K/128K ctx, latent cache offloaded; H2D gather GB/s"
 
 
@@ -368,8 +373,8 @@ def kernel_breakdown(layer, inputs, new_rows):
                                                 layer.lens, out=layer.logits))
         timed("topk", lambda: topk(layer.logits, layer.lens, layer.K, out=layer.idx, count=layer.cnt))
         acc = timed("cache", lambda: layer.pool.access(layer.idx, layer.cnt, out=acc))
-        g = lambda: gather(layer.pool, layer.store, acc, max_ctas=layer.gather_ctas)  # noqa: E731
-        w = (lambda: gather(layer.pool, layer.store, wake, max_ctas=layer.gather_ctas)) if wake else None
+        g = lambda: gather(layer.pool, layer.store, acc, max_ctas=BREAKDOWN_GATHER_CTAS)  # noqa: E731
+        w = (lambda: gather(layer.pool, layer.store, wake, max_ctas=BREAKDOWN_GATHER_CTAS)) if wake else None
         timed("gather", g, warm=w)
         timed("sparse_mla", lambda: sparse_mla(layer.pool, q, acc.sel_row, layer.cnt, layer.sm_scale,
                                                out=layer.out, lse=layer.lse))
@@ -562,6 +567,7 @@ def measure(args, cfg, dev, rank, world, agg_dev, drift, full, peaks, peak_kind,
                      "link_frac_of_link_peak": (gather_gbs * LINK_ROW_BYTES / 656 / link_peak
                                                 if gather_gbs and link_peak else None),
                      "miss_list": "cold: the breakdown step's own misses, after a gather of other rows",
+                     "ctas": BREAKDOWN_GATHER_CTAS,
                      "paper_flashtrans_gbs": 37.0}
     # e2e: through the public API with host buffers: every step copies its queries H2D
     # from pinned memory and its attention output D2H (layer.step_host: copy stream,
