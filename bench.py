@@ -491,7 +491,9 @@ def measure(args, cfg, dev, rank, world, agg_dev, drift, full, peaks, peak_kind,
 
     W, K, NB = args.warmup, args.steps, args.breakdown_steps
     total = W + K + NB + 4
-    layer, lens, _ = product_layer(cfg, dev, total + K, drift=drift, rank=rank, micro=args.micro,
+    # token budget per request: the graph warm-ups, timed steps, breakdown, similarity
+    # probe and the e2e pipeline (its capture and K steps) each append one token per step
+    layer, lens, _ = product_layer(cfg, dev, 2 * total + 2 * K + 32, drift=drift, rank=rank, micro=args.micro,
                                    first=args.first, gather_ctas=args.gather_ctas, world=world)
     B = layer.B
     inputs = [layer.next_queries() for _ in range(total)]
@@ -561,6 +563,9 @@ def measure(args, cfg, dev, rank, world, agg_dev, drift, full, peaks, peak_kind,
     # moves as 11 64-B read completions = 704 B.  Timed on the step's own (cold) miss list.
     rec["gather"] = {"bytes_per_step": gather_bytes, "gbs": gather_gbs,
                      "host_link_peak_gbs": link_peak,
+                     "host_link_peak_kind": "pinned cudaMemcpy H2D, 256 MB, best of 5, this box "
+                                            "(45-55 GB/s on most boxes; on a slow-DMA box the SM "
+                                            "gather can exceed it)",
                      "frac_of_link_peak": gather_gbs / link_peak if gather_gbs and link_peak else None,
                      "link_bytes_per_row": LINK_ROW_BYTES,
                      "link_gbs": gather_gbs * LINK_ROW_BYTES / 656 if gather_gbs else None,
