@@ -905,7 +905,8 @@ def run_ceiling(args, cfg, dev):
     lens = request_lengths(cfg, B, seed=int(os.environ.get("RANK", "0")))
     L = lens if not isinstance(cfg["context_len"], int) else cfg["context_len"]
     total = args.warmup + args.steps
-    layer = DSADecodeLayer(B, L, 1.0, TOPK, max_new_tokens=4 * total + 8, device=dev, seed=99,
+    # up to five schedules, each a capture step + (warmup - 1) + steps appended tokens
+    layer = DSADecodeLayer(B, L, 1.0, TOPK, max_new_tokens=6 * total + 16, device=dev, seed=99,
                            drift=args.drift)
     layer.gather_ctas = args.gather_ctas
     layer.preload_full_history()
