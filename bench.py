@@ -68,6 +68,18 @@ def request_lengths(cfg, n, seed=0):
     return [int(x) for x in np.exp(rng.uniform(np.log(lo), np.log(hi), size=n)).round()]
 
 
+def workload_config(cfg, args):
+    """The workload both arms run, identical in our line and the reference arm's (the
+    implementation's schedule and the host go in sibling keys): BASELINE's config name,
+    shapes, pool ratio, query drift, and the L2 statement of the timing rules."""
+    L = cfg["context_len"]
+    return {"workload": cfg["workload"], "layers": 1, "batch_per_gpu": cfg["batch"],
+            "context_len": L if isinstance(L, int) else "mixed {}-{} log-uniform".format(*L),
+            "sparse_ratio": cfg["sparse_ratio"],
+            "topk": TOPK, "query_drift": args.drift,
+            "l2": "inputs larger than L2 (indexer keys + slot pool > 600 MB/GPU)"}
+
+
 def init_ranks(local: int, world: int):
     """One process per GPU (NCCL for the barrier and the max-over-ranks timing).  With
     more ranks than GPUs (a harness check on a 1-GPU box) ranks share devices round-robin
@@ -284,13 +296,9 @@ def run_reference(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": cfg["workload"], "layers": 1, "batch_per_gpu": cfg["batch"],
-                       "context_len": cfg["context_len"] if isinstance(cfg["context_len"], int)
-                       else "mixed {}-{} log-uniform".format(*cfg["context_len"]),
-                       "sparse_ratio": cfg["sparse_ratio"],
-                       "topk": TOPK, "query_drift": args.drift,
-                       "overlap": "none (one request per core, sequential K1..K5 + admission)",
-                       "prefill_windows": CPU_WARM_WINDOWS, "untimed_decode_steps": CPU_WARM_STEPS},
+            "config": workload_config(cfg, args),
+            "schedule": {"overlap": "none (one request per core, sequential K1..K5 + admission)",
+                         "prefill_windows": CPU_WARM_WINDOWS, "untimed_decode_steps": CPU_WARM_STEPS},
             "hit_rate": hit_rate,
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "port",
                              "sample": sample},
@@ -675,14 +683,12 @@ def run_ours(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": main["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "e4m3/f16/f32",
             "data": "synthetic (random-weight DeepSeek-V3.2-Exp DSA shapes, drifting queries)",
-            "config": {"workload": cfg["workload"], "layers": 1, "batch_per_gpu": main["batch_per_gpu"],
-                       "context_len": main["context_len"], "sparse_ratio": cfg["sparse_ratio"],
-                       "topk": TOPK, "query_drift": args.drift, "overlap": args.overlap,
-                       "micro_batches": main["micro_batches"],
-                       "slot_row_bytes": main["slot_row_bytes"], "slot_store_gb": main["slot_store_gb"],
-                       "parallelism": f"dp{world} (requests sharded by dp.shard_requests, no collective)",
-                       "l2": "inputs larger than L2 (indexer keys + slot pool > 600 MB/GPU)",
-                       "host": host_info(bound_node)},
+            "config": workload_config(cfg, args),
+            "schedule": {"overlap": args.overlap, "micro_batches": main["micro_batches"],
+                         "context_len": main["context_len"],
+                         "slot_row_bytes": main["slot_row_bytes"], "slot_store_gb": main["slot_store_gb"],
+                         "parallelism": f"dp{world} (requests sharded by dp.shard_requests, no collective)"},
+            "host": host_info(bound_node),
             "e2e": main.get("e2e"),
             "roofline": main["roofline"],
             "cpu_baseline": {"value": cpu_v, "unit": "tokens/s", "cores": cpu_threads, "kind": "port",
