@@ -27,7 +27,7 @@ namespace {
 #define ESS_K1_SUB 2
 #endif
 #ifndef ESS_K1_STAGES
-#define ESS_K1_STAGES (ESS_K1_SUB == 1 ? 10 : ESS_K1_SUB == 2 ? 5 : 3)
+#define ESS_K1_STAGES (ESS_K1_SUB == 1 ? 10 : 3)
 #endif
 constexpr int TILE_M = 128;                 // tokens per MMA tile (M)
 constexpr int HEADS = ESS_INDEXER_HEADS;    // 64 heads per query token
