@@ -26,6 +26,9 @@ namespace {
 #ifndef ESS_K1_SUB
 #define ESS_K1_SUB 2
 #endif
+#ifndef ESS_K1_MTP_STAGES  // MTP instantiations (QT > 1); 0 = per-QT default
+#define ESS_K1_MTP_STAGES 0
+#endif
 #ifndef ESS_K1_STAGES
 #define ESS_K1_STAGES (ESS_K1_SUB == 1 ? 10 : 3)
 #endif
@@ -47,7 +50,7 @@ template <int QT>
 struct K1Cfg {
   static constexpr int SUB = QT == 1 ? ESS_K1_SUB : 1;         // MMA tiles per unit
   static constexpr int UNIT_M = SUB * TILE_M;                  // tokens per unit
-  static constexpr int STAGES = QT == 1 ? ESS_K1_STAGES : (QT == 2 ? 10 : 8);
+  static constexpr int STAGES = QT == 1 ? ESS_K1_STAGES : ESS_K1_MTP_STAGES > 0 ? ESS_K1_MTP_STAGES : (QT == 2 ? 10 : 8);
   static constexpr int N = HEADS * QT;                         // MMA N (all tokens' heads)
   static constexpr int UT_BYTES = SUB * KT_BYTES;
   static constexpr int QT_BYTES = N * DIM;                     // one request's q (x2 slots)
